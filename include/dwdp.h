@@ -1,0 +1,340 @@
+/*
+ * dwdp.h — C-ABI of the B200-native DWDP MoE hot path.
+ *
+ * Plain C types only (no torch, no CUDA headers): device pointers are
+ * `void*`, CUDA streams are passed as `void*` (a cudaStream_t / CUstream).
+ * Every entry point that can fail returns a status code; the message of the
+ * last failure on the calling thread is available from dwdp_last_error().
+ *
+ * Each declaration names the reference interface it replaces
+ * (/root/reference/proj/<file>:<line>). The planners are pure and
+ * reentrant; a dwdp_ctx is owned by one host thread driving one GPU.
+ */
+#ifndef DWDP_H
+#define DWDP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------
+ * Replaces the exception convention of include/dwdpsim/errors.hpp:11-28
+ * (ConfigError -> CLI exit 2, InvariantViolation -> exit 3, mapped in
+ * tools/dwdpsim_main.cpp:328-337). */
+#define DWDP_OK 0
+#define DWDP_ERR_CONFIG 2    /* ConfigError: invalid user input           */
+#define DWDP_ERR_INVARIANT 3 /* InvariantViolation: internal bug          */
+#define DWDP_ERR_CUDA 4      /* CUDA / driver failure, or no sm_100 device */
+
+const char* dwdp_last_error(void);
+/* Library build string (arch, CUDA version). */
+const char* dwdp_version(void);
+
+/* ======================================================================
+ * Expert placement table — include/dwdpsim/placement.hpp:13-43.
+ * ==================================================================== */
+typedef struct dwdp_placement dwdp_placement;
+
+/* build_placement(num_experts, group_size, extra_redundancy)
+ * (placement.hpp:30-34, src/placement.cpp:75-111). */
+int dwdp_placement_build(int num_experts, int group_size, int extra_redundancy,
+                         dwdp_placement** out);
+void dwdp_placement_free(dwdp_placement* p);
+/* PlacementPlan fields (placement.hpp:13-25). */
+int dwdp_placement_info(const dwdp_placement* p, int* group_size,
+                        int* num_experts, int* local_count, int* redundancy);
+/* local_sets[rank] (sorted), `experts` holds local_count entries. */
+int dwdp_placement_local_set(const dwdp_placement* p, int rank, int* experts);
+/* fetch_lists[rank] = (expert, source rank), E - local_count entries. */
+int dwdp_placement_fetch_list(const dwdp_placement* p, int rank, int* experts,
+                              int* sources);
+/* PlacementPlan::holds (src/placement.cpp:10-13). */
+int dwdp_placement_holds(const dwdp_placement* p, int rank, int expert,
+                         int* holds);
+/* PlacementPlan::validate (src/placement.cpp:15-45): 0 or 3. */
+int dwdp_placement_validate(const dwdp_placement* p);
+/* prefetch_bytes = (E - c) * expert_shard_bytes (src/placement.cpp:113-116). */
+int dwdp_prefetch_bytes(const dwdp_placement* p, double expert_shard_bytes,
+                        double* bytes);
+/* describe_placement (src/placement.cpp:118-150). *len in: capacity, out:
+ * bytes needed including the terminator. */
+int dwdp_placement_describe(const dwdp_placement* p, char* buf, size_t* len);
+/* assign_fetch_sources(num_experts, local_sets) (src/placement.cpp:47-73).
+ * local_sets is ragged: rank r owns local_flat[local_offsets[r] ..
+ * local_offsets[r+1]). Output per rank r: fetch_counts[r] entries starting
+ * at r * num_experts in fetch_experts / fetch_sources. */
+int dwdp_assign_fetch_sources(int num_experts, int group_size,
+                              const int* local_offsets, const int* local_flat,
+                              int* fetch_counts, int* fetch_experts,
+                              int* fetch_sources);
+
+/* ======================================================================
+ * TDM copy plan — include/dwdpsim/copyplan.hpp:15-51.
+ * ==================================================================== */
+typedef struct { /* ShardRef (copyplan.hpp:17-22) */
+  int32_t peer;
+  int32_t reserved;
+  uint64_t param_id;
+  uint64_t size;
+  uint64_t src_offset;
+} dwdp_shard_ref;
+
+typedef struct { /* Slice (copyplan.hpp:24-30) */
+  uint64_t param_id;
+  int32_t src_rank;
+  int32_t reserved;
+  uint64_t src_offset;
+  uint64_t dst_offset; /* relative to the per-(peer, param) buffer */
+  uint64_t length;
+} dwdp_slice;
+
+/* build_copy_plan(shards, slice_size, dst_rank) (src/copyplan.cpp:25-80).
+ * Size query when out == NULL: *n_inout receives the slice count. */
+int dwdp_copy_plan_build(const dwdp_shard_ref* shards, size_t n_shards,
+                         uint64_t slice_size, int dst_rank, dwdp_slice* out,
+                         size_t* n_inout);
+/* source_queues(plans, source) (src/copyplan.cpp:82-92): for each plan (in
+ * ascending dst order, one queue per distinct dst even if empty) the slices
+ * served by `source`, plan order preserved. out_dsts/out_counts receive
+ * *n_queues entries (capacity n_plans); `out` the concatenated slices. */
+int dwdp_source_queues(size_t n_plans, const int* dst_ranks,
+                       const dwdp_slice* const* plans, const size_t* plan_lens,
+                       int source, int* out_dsts, size_t* out_counts,
+                       size_t* n_queues, dwdp_slice* out, size_t* n_inout);
+
+/* ======================================================================
+ * Workload generator — include/dwdpsim/workload.hpp:14-79, rng.hpp.
+ * ==================================================================== */
+#define DWDP_ISL_FIXED 0
+#define DWDP_ISL_UNIFORM_RATIO 1
+#define DWDP_ISL_NORMAL 2
+
+typedef struct { /* WorkloadSpec + IslDist (workload.hpp:14-43) */
+  int32_t isl_kind;
+  int32_t batch_per_rank;
+  double length; /* Fixed: length; UniformRatio: max; Normal: mean */
+  double ratio;
+  double stddev;
+  int64_t max_num_tokens;
+  double routing_skew;
+  uint64_t seed;
+} dwdp_workload_spec;
+
+/* Rng::mix (rng.hpp:60-69). */
+uint64_t dwdp_rng_mix(uint64_t a, uint64_t b);
+/* route_tokens (src/workload.cpp:85-111): counts[num_experts]. */
+int dwdp_route_tokens(int64_t tokens, int num_experts, int top_k,
+                      double routing_skew, uint64_t seed, int64_t* counts);
+/* sample_batches (src/workload.cpp:137-173): tokens/requests
+ * [iterations][num_ranks]; routed (nullable) [iterations][num_ranks][E]. */
+int dwdp_sample_batches(const dwdp_workload_spec* spec, int num_experts,
+                        int top_k, int num_ranks, int iterations,
+                        int64_t* tokens, int64_t* requests, int64_t* routed);
+/* imbalance_cv (src/workload.cpp:175-189). */
+int dwdp_imbalance_cv(const int64_t* tokens, int n, double* cv);
+/* IslDist::cv (src/workload.cpp:24-36). */
+int dwdp_isl_cv(const dwdp_workload_spec* spec, double* cv);
+
+/* ======================================================================
+ * Cost model — include/dwdpsim/modelspec.hpp:22-75, hwmodel.hpp:29-52.
+ * ==================================================================== */
+typedef struct { /* MoeModelSpec, MoE-only subset */
+  int32_t num_layers;
+  int32_t num_experts;
+  int64_t hidden_dim;
+  int32_t top_k;
+  int32_t reserved;
+  int64_t expert_ffn_dim;
+  int64_t shared_ffn_dim;
+  double weight_bytes_per_param;
+  double act_bytes_per_element;
+} dwdp_model_spec;
+
+typedef struct { /* GpuSpec (hwmodel.hpp:29-38) */
+  double peak_flops;
+  double mem_bw;
+  double link_bw;
+} dwdp_gpu_spec;
+
+#define DWDP_CAT_GROUPED_GEMM 1 /* Category (hwmodel.hpp:14-23) */
+#define DWDP_CAT_DENSE_GEMM 2
+#define DWDP_CAT_OTHERS 3
+#define DWDP_CAT_COMMUNICATION 4
+#define DWDP_CAT_D2D_COPY 5
+#define DWDP_CAT_P2P_COPY 6
+#define DWDP_CAT_SYNC_WAIT 7
+
+typedef struct { /* OpCost (modelspec.hpp:37-41) + measured time */
+  int32_t category;
+  int32_t layer;
+  double flops;
+  double bytes;
+  double ns;
+} dwdp_op_cost;
+
+/* expert_shard_bytes (src/modelspec.cpp:32-36). */
+int dwdp_expert_shard_bytes(const dwdp_model_spec* m, double* bytes);
+/* moe_entries (src/modelspec.cpp:57-86): GroupedGemm (+ DenseGemm). */
+int dwdp_moe_entries(const dwdp_model_spec* m, double tokens,
+                     double routed_pairs, int experts_touched,
+                     dwdp_op_cost* out, int* n_out);
+/* roofline_time (src/hwmodel.cpp:68-73). */
+int dwdp_roofline_time(double flops, double bytes, const dwdp_gpu_spec* g,
+                       double* seconds);
+
+typedef struct { /* AnalyticResult (simcore.hpp:218-225) */
+  double t_compute_s;
+  double t_prefetch_s;
+  double t_all2all_s;
+  double compute_prefetch_ratio;
+  double dep_dwdp_speedup;
+  int32_t prefetch_saturated;
+  int32_t reserved;
+} dwdp_analytic_result;
+
+/* analytic_compare for the MoE-only layer (src/simcore.cpp:882-905). */
+int dwdp_analytic_compare(const dwdp_model_spec* m, const dwdp_gpu_spec* g,
+                          const dwdp_placement* p, int64_t tokens,
+                          dwdp_analytic_result* out);
+
+/* ======================================================================
+ * Per-GPU runtime: split-weight manager, prefetch engine, MoE forward.
+ * Replaces the simulated execution of simulate_dwdp / simulate_dep
+ * (include/dwdpsim/simcore.hpp:159-172, src/simcore.cpp:519-761) and the
+ * cost-only moe_entries with real sm_100a kernels.
+ * ==================================================================== */
+#define DWDP_SCORING_SOFTMAX 0
+#define DWDP_SCORING_SIGMOID 1
+#define DWDP_ENGINE_COPY 0 /* copy-engine peer copies on a side stream  */
+#define DWDP_ENGINE_PULL 1 /* one-launch SM pull kernel over NVLink      */
+
+typedef struct {
+  /* model */
+  int32_t num_layers;     /* L: layers of the MoE stack                   */
+  int32_t num_experts;    /* E                                            */
+  int64_t hidden;         /* h (multiple of 64)                           */
+  int64_t ffn;            /* f (multiple of 128)                          */
+  int64_t shared_ffn;     /* fs: 0 or == f                                */
+  int32_t top_k;
+  int32_t scoring;        /* DWDP_SCORING_*                               */
+  int32_t n_group;
+  int32_t topk_group;
+  int32_t norm_topk;
+  float routed_scale;
+  /* DWDP group */
+  int32_t rank;
+  int32_t group_size;     /* 1 = all experts local (no prefetch)          */
+  int32_t extra_redundancy;
+  int32_t device;         /* CUDA ordinal                                 */
+  /* DwdpOptions (simcore.hpp:64-71) */
+  int32_t merge_elim;     /* 1: GEMM reads split receive buffers in place  */
+  int32_t tdm;            /* 1: sliced round-robin plan, 0: monolithic     */
+  uint64_t slice_size;
+  int32_t engine;         /* DWDP_ENGINE_*                                 */
+  int32_t pull_ctas;      /* CTAs of the pull kernel                       */
+  /* synthetic weights */
+  uint64_t weight_seed;
+  int32_t weight_layers;  /* distinct weight sets; layer l uses l % this   */
+  int32_t reserved;
+  int64_t max_tokens;     /* workspace sizing (tokens per forward)         */
+} dwdp_ctx_config;
+
+typedef struct dwdp_ctx dwdp_ctx;
+typedef int64_t dwdp_prefetch; /* plan handle (CopyEngineSim plan id)     */
+
+int dwdp_ctx_create(const dwdp_ctx_config* cfg, dwdp_ctx** out);
+int dwdp_ctx_destroy(dwdp_ctx* ctx);
+/* Device bytes the context holds (weights + receive buffers + workspace). */
+int dwdp_ctx_memory(const dwdp_ctx* ctx, uint64_t* weight_bytes,
+                    uint64_t* recv_bytes, uint64_t* workspace_bytes);
+
+/* Multi-process peer wiring (one process per GPU): export this rank's
+ * weight-arena IPC handles, then hand every rank's blob to every rank. */
+#define DWDP_IPC_BLOB_BYTES 512
+int dwdp_ctx_export_ipc(dwdp_ctx* ctx, void* blob /*DWDP_IPC_BLOB_BYTES*/);
+int dwdp_ctx_open_peers(dwdp_ctx* ctx, const void* blobs /*N x BLOB*/);
+/* Single-process alternative: share arenas of contexts on other devices. */
+int dwdp_ctx_link_local(dwdp_ctx* const* ctxs, int n);
+
+/* Deterministic counter-hash init of the owned experts, shared expert,
+ * router (and e_score_correction_bias = bias_scale * U(-1,1)); then stages
+ * layer 0 (simcore.cpp:640-645, "layer 0 preloaded"). Synchronous. */
+int dwdp_ctx_init_weights(dwdp_ctx* ctx, float bias_scale);
+/* Overwrite the per-expert selection bias of every layer (e.g. a Zipf
+ * popularity tilt); host array [E] fp32. */
+int dwdp_ctx_set_bias(dwdp_ctx* ctx, const float* bias);
+/* Copy expert `e` tensor t (0 gate, 1 up, 2 down; e == E: shared) of
+ * layer `layer` as currently resident for that layer into host memory. */
+int dwdp_ctx_read_expert(dwdp_ctx* ctx, int layer, int expert, int t,
+                         void* host_bf16);
+
+/* ---- prefetch handles: CopyEngineSim (simcore.hpp:87-151) -------------
+ * issue_plan(dst, transfers, now) -> handle: enqueue the copy plan that
+ * pulls every non-local expert of global layer g into receive buffer
+ * g % 2, after the MoE of global layer g-1 released it (event-only
+ * ordering, never blocks the host, no collective). */
+int dwdp_prefetch_issue(dwdp_ctx* ctx, int64_t global_layer, dwdp_prefetch* h);
+/* plan_done */
+int dwdp_prefetch_query(dwdp_ctx* ctx, dwdp_prefetch h, int* done);
+/* MoeGate: make `stream` wait for the plan (cudaStreamWaitEvent). */
+int dwdp_prefetch_wait(dwdp_ctx* ctx, dwdp_prefetch h, void* stream);
+/* plan_start_time / plan_complete_time / plan_bytes, ns relative to the
+ * context's epoch event; -1 while pending. */
+int dwdp_prefetch_times(dwdp_ctx* ctx, dwdp_prefetch h, int64_t* start_ns,
+                        int64_t* end_ns, double* bytes);
+/* Copy plan of this rank (dst offsets relative to per-(peer,param) buffers). */
+int dwdp_ctx_copy_plan(dwdp_ctx* ctx, dwdp_slice* out, size_t* n_inout);
+
+/* ---- MoE forward -------------------------------------------------------
+ * moe_entries (src/modelspec.cpp:57-86) made real: router + top-k, permute,
+ * grouped GEMM1 + SwiGLU, grouped GEMM2, weighted combine (+ shared expert).
+ * x, y: device bf16 [T][h]. Weights of `layer` must be resident. */
+int dwdp_moe_forward(dwdp_ctx* ctx, int layer, const void* x, int64_t T,
+                     void* y, void* stream);
+/* One DWDP layer (simcore.cpp:676-710): MoeGate(g) = wait plan(g) and time
+ * the weight wait, issue plan(g+1), then the MoE of layer g % L. If
+ * `residual`, y = x + MoE(x). */
+int dwdp_layer_forward(dwdp_ctx* ctx, int64_t global_layer, const void* x,
+                       int64_t T, void* y, int residual, void* stream);
+/* L consecutive layers from the context's global layer cursor (one
+ * iteration of the stack); x and y may alias. */
+int dwdp_stack_forward(dwdp_ctx* ctx, const void* x, int64_t T, void* y,
+                       void* stream);
+/* Router + permutation only, for parity: idx/wts [T][k] (device),
+ * counts [E] and row_of [T][k] (device int32); *rows = padded rows. */
+int dwdp_route(dwdp_ctx* ctx, int layer, const void* x, int64_t T, void* idx,
+               void* wts, void* counts, void* row_of, int64_t* rows,
+               void* stream);
+
+/* ---- accounting: SimEvent / RunReport (simcore.hpp:29-61) --------------
+ * Per global layer measured after the fact from CUDA events. */
+typedef struct {
+  int64_t global_layer;
+  int64_t tokens;
+  double gate_wait_ns;   /* SyncWait "weight_wait": exposed prefetch  */
+  double moe_ns;         /* GroupedGemm+DenseGemm+Others of the layer */
+  double prefetch_ns;    /* P2PCopy of this layer's plan              */
+  double prefetch_bytes;
+  double merge_ns;       /* D2DCopy (merge_elim == 0 only)            */
+} dwdp_layer_record;
+/* Drain completed layer records (synchronises the context's streams). */
+int dwdp_ctx_records(dwdp_ctx* ctx, dwdp_layer_record* out, size_t* n_inout);
+/* Kernels launched by this context so far (for the bench's launch count). */
+int dwdp_ctx_launch_count(const dwdp_ctx* ctx, int64_t* n);
+
+/* ---- kernel-level entry points (tests / microbenchmarks) --------------- */
+/* D[M][N] = A[M][K] . B[N][K]^T, bf16 in, fp32 accumulate, bf16 out, on the
+ * tcgen05 grouped-GEMM kernel with one group. */
+int dwdp_gemm_bf16(const void* A, const void* B, void* D, int64_t M, int64_t N,
+                   int64_t K, void* stream);
+/* Fill a device bf16 buffer with the counter hash (oracle_fill_bf16). */
+int dwdp_fill_bf16(void* dst, int64_t n, uint64_t seed, float scale,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DWDP_H */

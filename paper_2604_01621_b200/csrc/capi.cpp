@@ -1,0 +1,569 @@
+// extern "C" boundary: include/dwdp.h. No exception crosses it; every entry
+// maps ConfigError -> 2, InvariantViolation -> 3, CUDA failures -> 4
+// (reference error contract: include/dwdpsim/errors.hpp:11-28).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/dwdp.h"
+#include "plan.hpp"
+#include "runtime.hpp"
+
+struct dwdp_placement {
+  dwdp::Placement p;
+};
+struct dwdp_ctx {
+  dwdp::Ctx* impl;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return DWDP_OK;
+  } catch (const dwdp::ConfigError& e) {
+    g_err = e.what();
+    return DWDP_ERR_CONFIG;
+  } catch (const dwdp::InvariantViolation& e) {
+    g_err = e.what();
+    return DWDP_ERR_INVARIANT;
+  } catch (const dwdp::CudaError& e) {
+    g_err = e.what();
+    return DWDP_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return DWDP_ERR_CUDA;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw dwdp::ConfigError(std::string(what) + " is NULL");
+}
+
+dwdp::ModelSpec to_model(const dwdp_model_spec* m) {
+  need(m, "model");
+  dwdp::require(m->hidden_dim > 0, "model.hidden_dim must be > 0");
+  dwdp::require(m->num_experts >= 1, "model.num_experts must be >= 1");
+  dwdp::require(m->top_k >= 1 && m->top_k <= m->num_experts,
+                "model.top_k must be in [1, num_experts]");
+  dwdp::require(m->expert_ffn_dim > 0, "model.expert_ffn_dim must be > 0");
+  dwdp::require(m->shared_ffn_dim >= 0, "model.shared_ffn_dim must be >= 0");
+  dwdp::require(m->weight_bytes_per_param > 0, "model.weight_bytes_per_param must be > 0");
+  dwdp::require(m->act_bytes_per_element > 0, "model.act_bytes_per_element must be > 0");
+  dwdp::ModelSpec s;
+  s.num_layers = m->num_layers;
+  s.num_experts = m->num_experts;
+  s.top_k = m->top_k;
+  s.hidden = m->hidden_dim;
+  s.ffn = m->expert_ffn_dim;
+  s.shared_ffn = m->shared_ffn_dim;
+  s.wbytes = m->weight_bytes_per_param;
+  s.abytes = m->act_bytes_per_element;
+  return s;
+}
+
+dwdp::WorkloadSpec to_spec(const dwdp_workload_spec* w) {
+  need(w, "spec");
+  dwdp::WorkloadSpec s;
+  s.isl_kind = w->isl_kind;
+  s.length = w->length;
+  s.ratio = w->ratio;
+  s.stddev = w->stddev;
+  s.max_num_tokens = w->max_num_tokens;
+  s.batch_per_rank = w->batch_per_rank;
+  s.routing_skew = w->routing_skew;
+  s.seed = w->seed;
+  return s;
+}
+
+dwdp::Ctx& C(dwdp_ctx* c) {
+  need(c, "ctx");
+  return *c->impl;
+}
+}  // namespace
+
+extern "C" {
+
+const char* dwdp_last_error(void) { return g_err.c_str(); }
+
+const char* dwdp_version(void) {
+  static const std::string v = "dwdp-b200 sm_100a cuda " + std::to_string(CUDART_VERSION);
+  return v.c_str();
+}
+
+// ---------------------------------------------------------------- placement
+int dwdp_placement_build(int E, int N, int extra, dwdp_placement** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = new dwdp_placement{dwdp::build_placement(E, N, extra)};
+  });
+}
+
+void dwdp_placement_free(dwdp_placement* p) { delete p; }
+
+int dwdp_placement_info(const dwdp_placement* p, int* n, int* e, int* c, int* r) {
+  return guard([&] {
+    need(p, "placement");
+    if (n) *n = p->p.group_size;
+    if (e) *e = p->p.num_experts;
+    if (c) *c = p->p.local_count;
+    if (r) *r = p->p.redundancy;
+  });
+}
+
+int dwdp_placement_local_set(const dwdp_placement* p, int rank, int* experts) {
+  return guard([&] {
+    need(p, "placement");
+    need(experts, "experts");
+    dwdp::require(rank >= 0 && rank < p->p.group_size, "placement: rank out of range");
+    const auto& s = p->p.local_sets[size_t(rank)];
+    std::copy(s.begin(), s.end(), experts);
+  });
+}
+
+int dwdp_placement_fetch_list(const dwdp_placement* p, int rank, int* experts, int* sources) {
+  return guard([&] {
+    need(p, "placement");
+    dwdp::require(rank >= 0 && rank < p->p.group_size, "placement: rank out of range");
+    const auto& f = p->p.fetch_lists[size_t(rank)];
+    for (size_t i = 0; i < f.size(); ++i) {
+      if (experts) experts[i] = f[i].first;
+      if (sources) sources[i] = f[i].second;
+    }
+  });
+}
+
+int dwdp_placement_holds(const dwdp_placement* p, int rank, int expert, int* holds) {
+  return guard([&] {
+    need(p, "placement");
+    need(holds, "holds");
+    dwdp::require(rank >= 0 && rank < p->p.group_size, "placement: rank out of range");
+    *holds = p->p.holds(rank, expert) ? 1 : 0;
+  });
+}
+
+int dwdp_placement_validate(const dwdp_placement* p) {
+  return guard([&] {
+    need(p, "placement");
+    p->p.validate();
+  });
+}
+
+int dwdp_prefetch_bytes(const dwdp_placement* p, double shard, double* bytes) {
+  return guard([&] {
+    need(p, "placement");
+    need(bytes, "bytes");
+    *bytes = double(p->p.num_experts - p->p.local_count) * shard;
+  });
+}
+
+int dwdp_placement_describe(const dwdp_placement* p, char* buf, size_t* len) {
+  return guard([&] {
+    need(p, "placement");
+    need(len, "len");
+    const std::string s = p->p.describe();
+    const size_t cap = *len;
+    *len = s.size() + 1;
+    if (buf && cap >= s.size() + 1) std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+int dwdp_assign_fetch_sources(int E, int N, const int* offs, const int* flat, int* counts,
+                              int* fe, int* fs) {
+  return guard([&] {
+    need(offs, "local_offsets");
+    need(flat, "local_flat");
+    dwdp::require(N >= 1 && E >= 1, "assign_fetch_sources: bad sizes");
+    std::vector<std::vector<int>> sets(static_cast<size_t>(N));
+    for (int r = 0; r < N; ++r)
+      for (int i = offs[r]; i < offs[r + 1]; ++i) {
+        dwdp::require(flat[i] >= 0 && flat[i] < E, "assign_fetch_sources: expert out of range");
+        sets[size_t(r)].push_back(flat[i]);
+      }
+    const auto fl = dwdp::assign_fetch_sources(E, sets);
+    for (int r = 0; r < N; ++r) {
+      if (counts) counts[r] = int(fl[size_t(r)].size());
+      for (size_t i = 0; i < fl[size_t(r)].size(); ++i) {
+        if (fe) fe[size_t(r) * size_t(E) + i] = fl[size_t(r)][i].first;
+        if (fs) fs[size_t(r) * size_t(E) + i] = fl[size_t(r)][i].second;
+      }
+    }
+  });
+}
+
+// ---------------------------------------------------------------- copy plan
+int dwdp_copy_plan_build(const dwdp_shard_ref* shards, size_t n, uint64_t slice, int dst,
+                         dwdp_slice* out, size_t* n_inout) {
+  return guard([&] {
+    need(n_inout, "n_inout");
+    if (n) need(shards, "shards");
+    std::vector<dwdp::ShardRef> v(n);
+    for (size_t i = 0; i < n; ++i)
+      v[i] = {shards[i].peer, shards[i].param_id, shards[i].size, shards[i].src_offset};
+    const auto plan = dwdp::build_copy_plan(v, slice, dst);
+    const size_t cap = *n_inout;
+    *n_inout = plan.size();
+    if (!out) return;
+    dwdp::require(cap >= plan.size(), "copy plan: output capacity too small");
+    for (size_t i = 0; i < plan.size(); ++i)
+      out[i] = {plan[i].param_id, plan[i].src_rank, 0, plan[i].src_offset, plan[i].dst_offset,
+                plan[i].length};
+  });
+}
+
+int dwdp_source_queues(size_t n_plans, const int* dsts, const dwdp_slice* const* plans,
+                       const size_t* lens, int source, int* out_dsts, size_t* out_counts,
+                       size_t* n_queues, dwdp_slice* out, size_t* n_inout) {
+  return guard([&] {
+    need(n_queues, "n_queues");
+    need(n_inout, "n_inout");
+    std::map<int, std::vector<dwdp_slice>> q;
+    for (size_t i = 0; i < n_plans; ++i) {
+      auto& v = q[dsts[i]];  // present even if empty
+      for (size_t j = 0; j < lens[i]; ++j)
+        if (plans[i][j].src_rank == source) v.push_back(plans[i][j]);
+    }
+    size_t total = 0;
+    for (auto& kv : q) total += kv.second.size();
+    const size_t cap = *n_inout;
+    *n_inout = total;
+    *n_queues = q.size();
+    if (!out) return;
+    dwdp::require(cap >= total, "source_queues: output capacity too small");
+    size_t i = 0, k = 0;
+    for (auto& kv : q) {
+      if (out_dsts) out_dsts[k] = kv.first;
+      if (out_counts) out_counts[k] = kv.second.size();
+      ++k;
+      for (auto& s : kv.second) out[i++] = s;
+    }
+  });
+}
+
+// ---------------------------------------------------------------- workload
+uint64_t dwdp_rng_mix(uint64_t a, uint64_t b) { return dwdp::Rng::mix(a, b); }
+
+int dwdp_route_tokens(int64_t tokens, int E, int k, double skew, uint64_t seed, int64_t* counts) {
+  return guard([&] {
+    need(counts, "counts");
+    const auto c = dwdp::route_tokens(tokens, E, k, skew, seed);
+    std::copy(c.begin(), c.end(), counts);
+  });
+}
+
+int dwdp_sample_batches(const dwdp_workload_spec* w, int E, int k, int N, int iters,
+                        int64_t* tokens, int64_t* requests, int64_t* routed) {
+  return guard([&] {
+    need(tokens, "tokens");
+    dwdp::require(k >= 1 && k <= E, "model.top_k must be in [1, num_experts]");
+    const auto b = dwdp::sample_batches(to_spec(w), E, k, N, iters, routed != nullptr);
+    for (int it = 0; it < iters; ++it)
+      for (int r = 0; r < N; ++r) {
+        const size_t i = size_t(it) * size_t(N) + size_t(r);
+        tokens[i] = b.tokens[size_t(it)][size_t(r)];
+        if (requests) requests[i] = b.requests[size_t(it)][size_t(r)];
+        if (routed)
+          std::copy(b.routed[size_t(it)][size_t(r)].begin(), b.routed[size_t(it)][size_t(r)].end(),
+                    routed + i * size_t(E));
+      }
+  });
+}
+
+int dwdp_imbalance_cv(const int64_t* tokens, int n, double* cv) {
+  return guard([&] {
+    need(cv, "cv");
+    dwdp::require(n >= 2, "imbalance_cv: need at least 2 ranks");
+    need(tokens, "tokens");
+    *cv = dwdp::imbalance_cv(std::vector<int64_t>(tokens, tokens + n));
+  });
+}
+
+int dwdp_isl_cv(const dwdp_workload_spec* w, double* cv) {
+  return guard([&] {
+    need(cv, "cv");
+    *cv = to_spec(w).cv();
+  });
+}
+
+// ---------------------------------------------------------------- costs
+int dwdp_expert_shard_bytes(const dwdp_model_spec* m, double* bytes) {
+  return guard([&] {
+    need(bytes, "bytes");
+    *bytes = dwdp::expert_shard_bytes(to_model(m));
+  });
+}
+
+int dwdp_moe_entries(const dwdp_model_spec* m, double tokens, double pairs, int touched,
+                     dwdp_op_cost* out, int* n_out) {
+  return guard([&] {
+    need(out, "out");
+    need(n_out, "n_out");
+    const auto e = dwdp::moe_entries(to_model(m), tokens, pairs, touched);
+    for (size_t i = 0; i < e.size(); ++i) out[i] = {e[i].category, 0, e[i].flops, e[i].bytes, 0.0};
+    *n_out = int(e.size());
+  });
+}
+
+int dwdp_roofline_time(double flops, double bytes, const dwdp_gpu_spec* g, double* s) {
+  return guard([&] {
+    need(g, "gpu");
+    need(s, "seconds");
+    dwdp::require(flops >= 0, "roofline_time: negative flops");
+    dwdp::require(bytes >= 0, "roofline_time: negative bytes");
+    dwdp::require(flops > 0 || bytes > 0, "roofline_time: operator has no work");
+    *s = std::max(flops / g->peak_flops, bytes / g->mem_bw);
+  });
+}
+
+int dwdp_analytic_compare(const dwdp_model_spec* m, const dwdp_gpu_spec* g,
+                          const dwdp_placement* p, int64_t tokens, dwdp_analytic_result* out) {
+  return guard([&] {
+    need(g, "gpu");
+    need(p, "placement");
+    need(out, "out");
+    const auto spec = to_model(m);
+    dwdp::require(p->p.num_experts == spec.num_experts,
+                  "analytic_compare: placement does not match the model");
+    dwdp::require(tokens >= 1, "layer_costs: tokens must be >= 1");
+    const double t = double(tokens);
+    double tc = 0;
+    for (const auto& op : dwdp::moe_entries(spec, t, t * spec.top_k, spec.num_experts))
+      tc += std::max(op.flops / g->peak_flops, op.bytes / g->mem_bw);
+    const double pf = double(p->p.num_experts - p->p.local_count) * dwdp::expert_shard_bytes(spec);
+    *out = {};
+    out->t_compute_s = tc;
+    out->t_prefetch_s = pf / g->link_bw;
+    out->t_all2all_s = 2.0 * t * spec.top_k * double(spec.hidden) * spec.abytes / g->link_bw;
+    const double t_dep = tc + out->t_all2all_s;
+    if (out->t_prefetch_s <= 0) {
+      out->prefetch_saturated = 1;
+      out->compute_prefetch_ratio = 1.0 / 0.0;
+      out->dep_dwdp_speedup = t_dep / tc;
+    } else {
+      out->compute_prefetch_ratio = tc / out->t_prefetch_s;
+      out->dep_dwdp_speedup = t_dep / std::max(tc, out->t_prefetch_s);
+    }
+  });
+}
+
+// ---------------------------------------------------------------- runtime
+int dwdp_ctx_create(const dwdp_ctx_config* cfg, dwdp_ctx** out) {
+  return guard([&] {
+    need(cfg, "cfg");
+    need(out, "out");
+    *out = new dwdp_ctx{new dwdp::Ctx(*cfg)};
+  });
+}
+
+int dwdp_ctx_destroy(dwdp_ctx* c) {
+  return guard([&] {
+    if (!c) return;
+    delete c->impl;
+    delete c;
+  });
+}
+
+int dwdp_ctx_memory(const dwdp_ctx* c, uint64_t* w, uint64_t* r, uint64_t* ws) {
+  return guard([&] {
+    need(c, "ctx");
+    if (w) *w = c->impl->weight_bytes;
+    if (r) *r = c->impl->recv_bytes;
+    if (ws) *ws = c->impl->workspace_bytes;
+  });
+}
+
+int dwdp_ctx_export_ipc(dwdp_ctx* c, void* blob) {
+  return guard([&] {
+    need(blob, "blob");
+    C(c).export_ipc(blob);
+  });
+}
+
+int dwdp_ctx_open_peers(dwdp_ctx* c, const void* blobs) {
+  return guard([&] {
+    need(blobs, "blobs");
+    C(c).open_peers(blobs);
+  });
+}
+
+int dwdp_ctx_link_local(dwdp_ctx* const* ctxs, int n) {
+  return guard([&] {
+    need(ctxs, "ctxs");
+    std::vector<dwdp::Ctx*> all;
+    for (int i = 0; i < n; ++i) all.push_back(&C(ctxs[i]));
+    for (auto* c : all) c->link_local(all);
+  });
+}
+
+int dwdp_ctx_init_weights(dwdp_ctx* c, float bias_scale) {
+  return guard([&] { C(c).init_weights(bias_scale); });
+}
+
+int dwdp_ctx_set_bias(dwdp_ctx* c, const float* bias) {
+  return guard([&] {
+    need(bias, "bias");
+    C(c).set_bias(bias);
+  });
+}
+
+int dwdp_ctx_read_expert(dwdp_ctx* c, int layer, int expert, int t, void* host) {
+  return guard([&] {
+    need(host, "host");
+    C(c).read_expert(layer, expert, t, host);
+  });
+}
+
+int dwdp_prefetch_issue(dwdp_ctx* c, int64_t g, dwdp_prefetch* h) {
+  return guard([&] {
+    need(h, "handle");
+    *h = C(c).prefetch_issue(g);
+  });
+}
+
+int dwdp_prefetch_query(dwdp_ctx* c, dwdp_prefetch h, int* done) {
+  return guard([&] {
+    need(done, "done");
+    *done = C(c).prefetch_done(h) ? 1 : 0;
+  });
+}
+
+int dwdp_prefetch_wait(dwdp_ctx* c, dwdp_prefetch h, void* stream) {
+  return guard([&] { C(c).prefetch_wait(h, static_cast<cudaStream_t>(stream)); });
+}
+
+int dwdp_prefetch_times(dwdp_ctx* c, dwdp_prefetch h, int64_t* s, int64_t* e, double* b) {
+  return guard([&] {
+    int64_t s0, e0;
+    double b0;
+    C(c).prefetch_times(h, &s0, &e0, &b0);
+    if (s) *s = s0;
+    if (e) *e = e0;
+    if (b) *b = b0;
+  });
+}
+
+int dwdp_ctx_copy_plan(dwdp_ctx* c, dwdp_slice* out, size_t* n_inout) {
+  return guard([&] {
+    need(n_inout, "n_inout");
+    const auto plan = C(c).copy_plan();
+    const size_t cap = *n_inout;
+    *n_inout = plan.size();
+    if (!out) return;
+    dwdp::require(cap >= plan.size(), "copy plan: output capacity too small");
+    for (size_t i = 0; i < plan.size(); ++i)
+      out[i] = {plan[i].param_id, plan[i].src_rank, 0, plan[i].src_offset, plan[i].dst_offset,
+                plan[i].length};
+  });
+}
+
+int dwdp_moe_forward(dwdp_ctx* c, int layer, const void* x, int64_t T, void* y, void* stream) {
+  return guard([&] {
+    if (T > 0) {
+      need(x, "x");
+      need(y, "y");
+    }
+    auto& ctx = C(c);
+    dwdp::require(layer >= 0 && layer < ctx.cfg.num_layers, "moe_forward: layer out of range");
+    ctx.moe_forward(layer, ctx.resident_parity(layer), static_cast<const uint16_t*>(x), T, static_cast<uint16_t*>(y),
+                    nullptr, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int dwdp_layer_forward(dwdp_ctx* c, int64_t g, const void* x, int64_t T, void* y, int residual,
+                       void* stream) {
+  return guard([&] {
+    if (T > 0) {
+      need(x, "x");
+      need(y, "y");
+    }
+    C(c).layer_forward(g, static_cast<const uint16_t*>(x), T, static_cast<uint16_t*>(y),
+                       residual != 0, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int dwdp_stack_forward(dwdp_ctx* c, const void* x, int64_t T, void* y, void* stream) {
+  return guard([&] {
+    if (T > 0) {
+      need(x, "x");
+      need(y, "y");
+    }
+    C(c).stack_forward(static_cast<const uint16_t*>(x), T, static_cast<uint16_t*>(y),
+                       static_cast<cudaStream_t>(stream));
+  });
+}
+
+int dwdp_route(dwdp_ctx* c, int layer, const void* x, int64_t T, void* idx, void* wts,
+               void* counts, void* row_of, int64_t* rows, void* stream) {
+  return guard([&] {
+    need(x, "x");
+    C(c).route(layer, static_cast<const uint16_t*>(x), T, static_cast<int32_t*>(idx),
+               static_cast<float*>(wts), static_cast<int32_t*>(counts),
+               static_cast<int32_t*>(row_of), rows, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int dwdp_ctx_records(dwdp_ctx* c, dwdp_layer_record* out, size_t* n_inout) {
+  return guard([&] {
+    need(n_inout, "n_inout");
+    *n_inout = C(c).drain_records(out, out ? *n_inout : 0);
+  });
+}
+
+int dwdp_ctx_launch_count(const dwdp_ctx* c, int64_t* n) {
+  return guard([&] {
+    need(c, "ctx");
+    need(n, "n");
+    *n = c->impl->launches;
+  });
+}
+
+int dwdp_gemm_bf16(const void* A, const void* B, void* D, int64_t M, int64_t N, int64_t K,
+                   void* stream) {
+  return guard([&] {
+    need(A, "A");
+    need(B, "B");
+    need(D, "D");
+    // A throwaway context-free path: the kernel only needs TMA maps and tables.
+    static dwdp::Ctx* tiny = nullptr;
+    if (!tiny) {
+      dwdp_ctx_config cfg{};
+      cfg.num_layers = 1;
+      cfg.num_experts = 1;
+      cfg.hidden = 256;
+      cfg.ffn = 128;
+      cfg.top_k = 1;
+      cfg.scoring = 0;
+      cfg.n_group = 1;
+      cfg.topk_group = 1;
+      cfg.routed_scale = 1.0f;
+      cfg.group_size = 1;
+      cfg.merge_elim = 1;
+      cfg.max_tokens = 1;
+      cfg.weight_layers = 1;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cfg.device = dev;
+      tiny = new dwdp::Ctx(cfg);
+    }
+    tiny->gemm_bf16(static_cast<const uint16_t*>(A), static_cast<const uint16_t*>(B),
+                    static_cast<uint16_t*>(D), M, N, K, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int dwdp_fill_bf16(void* dst, int64_t n, uint64_t seed, float scale, void* stream) {
+  return guard([&] {
+    need(dst, "dst");
+    dwdp::launch_fill(static_cast<uint16_t*>(dst), n, seed, scale,
+                      static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw dwdp::CudaError(cudaGetErrorString(e));
+  });
+}
+
+}  // extern "C"

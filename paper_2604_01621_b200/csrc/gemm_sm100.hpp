@@ -1,0 +1,35 @@
+// Grouped tcgen05 GEMM launch interface (see gemm_sm100.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace dwdp {
+
+struct GemmArgs {
+  int K;                        // reduction length (multiple of 64)
+  int n_out;                    // output columns (SwiGLU: multiple of 128, else of 256)
+  int rows_per_slot;            // B rows per arena slot
+  int E;                        // expert id of the shared-expert group
+  const int32_t* mblock_expert; // [m-blocks] expert of each 128-row block
+  const int32_t* slot_of;       // [E + 1] expert -> arena slot
+  const int32_t* meta;          // {total m-blocks, routed m-blocks, routed rows, T}
+  uint16_t* D;                  // bf16 output, row-major
+  int64_t ldd;                  // elements per output row
+  int64_t m_limit;              // rows >= m_limit are not stored
+  int shared_a2;                // shared-expert blocks read A from `a2` (GEMM1)
+};
+
+// 2-D bf16 TMA map over a row-major [rows][cols] matrix, box = 64 x box_rows,
+// SWIZZLE_128B (the UMMA K-major operand layout).
+CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int box_rows);
+
+// a: routed A rows (permuted tokens or H); a2: shared-expert A rows (x);
+// b0: gate (SwiGLU) or down arena; b1: up arena (SwiGLU only).
+void launch_grouped_gemm(bool swiglu, const CUtensorMap& a, const CUtensorMap& a2,
+                         const CUtensorMap& b0, const CUtensorMap& b1, const GemmArgs& args,
+                         int max_tiles, cudaStream_t st);
+
+}  // namespace dwdp

@@ -1,0 +1,596 @@
+// DWDP sm_100a kernels except the grouped GEMM (gemm_sm100.cu):
+// counter-hash init, router logits + scoring/top-k, stable permute/gather,
+// weighted combine and the NVLink pull kernel.
+//
+// Numerical contract with the oracle (oracle/dwdp_oracle.c): the router
+// logits are sequential fused multiply-adds over i = 0..h-1, the scoring
+// exponent is a fixed IEEE sequence (det_expf), and the permutation is the
+// stable expert-major order of (t, j) pairs — so expert indices, routing
+// weights and row positions are bit-identical to the CPU restatement.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.hpp"
+
+namespace dwdp {
+namespace {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t a, uint64_t b) {
+  uint64_t z = a + 0x9e3779b97f4a7c15ULL * (b + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ float hash_val(uint64_t seed, int64_t i, float scale) {
+  const uint32_t u = static_cast<uint32_t>(mix64(seed, static_cast<uint64_t>(i)) >> 40);
+  const float v = __fsub_rn(__fmul_rn(static_cast<float>(u), 0x1.0p-23f), 1.0f);
+  return __fmul_rn(v, scale);
+}
+
+__device__ __forceinline__ uint16_t bf16_bits(float f) {
+  return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+__device__ __forceinline__ float bf16_f(uint16_t b) {
+  return __uint_as_float(static_cast<uint32_t>(b) << 16);
+}
+
+// ---------------------------------------------------------------- init
+__global__ void fill_slots_kernel(uint16_t* __restrict__ dst, const uint64_t* __restrict__ seeds,
+                                  int nslots, int64_t slot_elems, float scale) {
+  const int64_t groups_per_slot = slot_elems / 8;
+  const int64_t total = groups_per_slot * nslots;
+  for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < total;
+       g += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t s = g / groups_per_slot;
+    const int64_t e0 = (g - s * groups_per_slot) * 8;
+    const uint64_t seed = seeds[s];
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      w[q] = uint32_t(bf16_bits(hash_val(seed, e0 + 2 * q, scale))) |
+             (uint32_t(bf16_bits(hash_val(seed, e0 + 2 * q + 1, scale))) << 16);
+    *reinterpret_cast<uint4*>(dst + s * slot_elems + e0) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+__global__ void fill_kernel(uint16_t* __restrict__ dst, int64_t n, uint64_t seed, float scale) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = bf16_bits(hash_val(seed, i, scale));
+}
+
+__global__ void fill_f32_kernel(float* __restrict__ dst, int64_t n, uint64_t seed, float scale) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = hash_val(seed, i, scale);
+}
+
+// ---------------------------------------------------------------- router
+// SIMT fp32 GEMM, 128 tokens x 128 experts per CTA, 8x8 outputs per thread.
+// Every output accumulates fma(x[t][i], w[e][i], acc) for i ascending.
+constexpr int RB_M = 128, RB_N = 128, RB_K = 16;
+
+__global__ void __launch_bounds__(256) router_logits_kernel(const uint16_t* __restrict__ x,
+                                                            const uint16_t* __restrict__ w,
+                                                            float* __restrict__ logits, int64_t T,
+                                                            int E, int64_t K) {
+  __shared__ __align__(16) float As[2][RB_K][RB_M];
+  __shared__ __align__(16) float Bs[2][RB_K][RB_N];
+  const int tid = threadIdx.x;
+  const int64_t m0 = int64_t(blockIdx.x) * RB_M;
+  const int n0 = blockIdx.y * RB_N;
+  // loader: thread -> (row = tid / 2, 8 consecutive k at (tid % 2) * 8)
+  const int lr = tid >> 1, lk = (tid & 1) * 8;
+  const bool a_ok = m0 + lr < T, b_ok = n0 + lr < E;
+  const uint16_t* ap = x + (m0 + lr) * K + lk;
+  const uint16_t* bp = w + int64_t(n0 + lr) * K + lk;
+  uint4 ra = make_uint4(0, 0, 0, 0), rb = make_uint4(0, 0, 0, 0);
+  auto gload = [&](int64_t k0) {
+    ra = a_ok ? *reinterpret_cast<const uint4*>(ap + k0) : make_uint4(0, 0, 0, 0);
+    rb = b_ok ? *reinterpret_cast<const uint4*>(bp + k0) : make_uint4(0, 0, 0, 0);
+  };
+  auto sstore = [&](int buf) {
+    const uint32_t av[4] = {ra.x, ra.y, ra.z, ra.w}, bv[4] = {rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      As[buf][lk + 2 * q][lr] = __uint_as_float(av[q] << 16);
+      As[buf][lk + 2 * q + 1][lr] = __uint_as_float(av[q] & 0xffff0000u);
+      Bs[buf][lk + 2 * q][lr] = __uint_as_float(bv[q] << 16);
+      Bs[buf][lk + 2 * q + 1][lr] = __uint_as_float(bv[q] & 0xffff0000u);
+    }
+  };
+  // compute mapping: rows {ty*4 + i, 64 + ty*4 + i}, cols {tx*4 + j, 64 + tx*4 + j}
+  const int tx = tid & 15, ty = tid >> 4;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+
+  const int64_t nk = K / RB_K;
+  gload(0);
+  sstore(0);
+  __syncthreads();
+  for (int64_t kt = 0; kt < nk; ++kt) {
+    const int buf = int(kt & 1);
+    if (kt + 1 < nk) gload((kt + 1) * RB_K);
+#pragma unroll
+    for (int kk = 0; kk < RB_K; ++kk) {
+      float a[8], b[8];
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tx * 4]);
+      a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+      a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+      b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
+    }
+    if (kt + 1 < nk) sstore(buf ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t t = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+    if (t >= T) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      if (e < E) logits[t * E + e] = acc[i][j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- top-k
+__device__ __forceinline__ float det_expf(float x) {
+  if (x < -87.0f) return 0.0f;
+  if (x > 88.0f) return __int_as_float(0x7f800000);
+  const float n = rintf(__fmul_rn(x, 1.44269504088896341f));
+  float r = __fmaf_rn(n, -0.693145751953125f, x);
+  r = __fmaf_rn(n, -1.428606765330187e-06f, r);
+  float p = 1.38888889e-3f;
+  p = __fmaf_rn(p, r, 8.33333333e-3f);
+  p = __fmaf_rn(p, r, 4.16666667e-2f);
+  p = __fmaf_rn(p, r, 1.66666667e-1f);
+  p = __fmaf_rn(p, r, 0.5f);
+  p = __fmaf_rn(p, r, 1.0f);
+  p = __fmaf_rn(p, r, 1.0f);
+  return ldexpf(p, int(n));
+}
+
+__device__ __forceinline__ bool better(float a, int ia, float b, int ib) {
+  return a > b || (a == b && ia < ib);
+}
+
+// Warp argmax over (value, index) pairs; lanes holding no candidate pass
+// (-inf, INT_MAX). Returns the winner on all lanes.
+__device__ __forceinline__ void warp_best(float& v, int& i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+    if (better(ov, oi, v, i)) {
+      v = ov;
+      i = oi;
+    }
+  }
+}
+
+constexpr int TOPK_MAXV = 16;  // E <= 512
+constexpr int TOPK_MAXK = 16;
+
+__global__ void __launch_bounds__(256) topk_kernel(const float* __restrict__ logits,
+                                                   const float* __restrict__ bias,
+                                                   int32_t* __restrict__ idx_out,
+                                                   float* __restrict__ wts_out, int64_t T,
+                                                   RouterCfg c) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int E = c.E;
+  const int V = (E + 31) >> 5;
+  const float NEG = __int_as_float(0xff800000);
+  float lg[TOPK_MAXV], sc[TOPK_MAXV], ch[TOPK_MAXV];
+  const float* row = logits + t * E;
+#pragma unroll
+  for (int v = 0; v < TOPK_MAXV; ++v) {
+    const int e = lane + 32 * v;
+    if (v < V && e < E) {
+      lg[v] = row[e];
+      if (c.scoring == 1) {
+        sc[v] = __fdiv_rn(1.0f, __fadd_rn(1.0f, det_expf(-lg[v])));
+        ch[v] = __fadd_rn(sc[v], bias ? bias[e] : 0.0f);
+      } else {
+        sc[v] = lg[v];
+        ch[v] = lg[v];
+      }
+    } else {
+      lg[v] = sc[v] = ch[v] = NEG;
+    }
+  }
+  const int G = c.n_group > 0 ? c.n_group : 1;
+  if (G > 1 && c.topk_group < G) {
+    const int gs = E / G;
+    uint32_t gsel = 0;  // bit g: group kept (G <= 32)
+    float gscore_mine = NEG;  // lane g holds group g's score
+    for (int g = 0; g < G; ++g) {
+      float b1v = NEG, b2v = NEG;
+      int b1i = 0x7fffffff, b2i = 0x7fffffff;
+      // top-1
+      float v1 = NEG;
+      int i1 = 0x7fffffff;
+#pragma unroll
+      for (int v = 0; v < TOPK_MAXV; ++v) {
+        const int e = lane + 32 * v;
+        if (v < V && e < E && e / gs == g && better(ch[v], e, v1, i1)) {
+          v1 = ch[v];
+          i1 = e;
+        }
+      }
+      warp_best(v1, i1);
+      b1v = v1;
+      b1i = i1;
+      float v2 = NEG;
+      int i2 = 0x7fffffff;
+#pragma unroll
+      for (int v = 0; v < TOPK_MAXV; ++v) {
+        const int e = lane + 32 * v;
+        if (v < V && e < E && e / gs == g && e != b1i && better(ch[v], e, v2, i2)) {
+          v2 = ch[v];
+          i2 = e;
+        }
+      }
+      warp_best(v2, i2);
+      b2v = v2;
+      b2i = i2;
+      (void)b2i;
+      const float gsc = gs >= 2 ? __fadd_rn(b1v, b2v) : b1v;
+      if (lane == g) gscore_mine = gsc;
+    }
+    for (int s = 0; s < c.topk_group; ++s) {
+      float v = (lane < G && !((gsel >> lane) & 1u)) ? gscore_mine : NEG;
+      int i = (lane < G && !((gsel >> lane) & 1u)) ? lane : 0x7fffffff;
+      warp_best(v, i);
+      gsel |= 1u << i;
+    }
+#pragma unroll
+    for (int v = 0; v < TOPK_MAXV; ++v) {
+      const int e = lane + 32 * v;
+      if (v < V && e < E && !((gsel >> (e / gs)) & 1u)) ch[v] = 0.0f;  // HF masked_fill 0.0
+    }
+  }
+  // top-k over ch, ties to the lower index
+  int sel[TOPK_MAXK];
+  uint32_t taken[TOPK_MAXV / 32 + 1] = {0};
+  (void)taken;
+  uint32_t taken_mask = 0;  // bit v of this lane's slots
+  for (int j = 0; j < c.k; ++j) {
+    float bv = NEG;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int v = 0; v < TOPK_MAXV; ++v) {
+      const int e = lane + 32 * v;
+      if (v < V && e < E && !((taken_mask >> v) & 1u) && better(ch[v], e, bv, bi)) {
+        bv = ch[v];
+        bi = e;
+      }
+    }
+    warp_best(bv, bi);
+    sel[j] = bi;
+    if ((bi & 31) == lane) taken_mask |= 1u << (bi >> 5);
+  }
+  // weights: fetch the winners' score / logit from their owning lanes
+  float wv[TOPK_MAXK];
+  for (int j = 0; j < c.k; ++j) {
+    const int e = sel[j];
+    float mine = 0.0f;
+#pragma unroll
+    for (int v = 0; v < TOPK_MAXV; ++v)
+      if (v == (e >> 5)) mine = (c.scoring == 1) ? sc[v] : lg[v];
+    wv[j] = __shfl_sync(0xffffffffu, mine, e & 31);
+  }
+  if (lane != 0) return;
+  if (c.scoring == 1) {
+    if (c.norm_topk) {
+      float s = 0.0f;
+      for (int j = 0; j < c.k; ++j) s = __fadd_rn(s, wv[j]);
+      s = __fadd_rn(s, 1e-20f);
+      for (int j = 0; j < c.k; ++j) wv[j] = __fdiv_rn(wv[j], s);
+    }
+  } else {
+    const float m = wv[0];
+    float s = 0.0f;
+    for (int j = 0; j < c.k; ++j) {
+      wv[j] = det_expf(__fsub_rn(wv[j], m));
+      if (c.norm_topk) s = __fadd_rn(s, wv[j]);
+    }
+    if (!c.norm_topk)
+      for (int e = 0; e < E; ++e) s = __fadd_rn(s, det_expf(__fsub_rn(row[e], m)));
+    for (int j = 0; j < c.k; ++j) wv[j] = __fdiv_rn(wv[j], s);
+  }
+  for (int j = 0; j < c.k; ++j) {
+    idx_out[t * c.k + j] = sel[j];
+    wts_out[t * c.k + j] = __fmul_rn(wv[j], c.routed_scale);
+  }
+}
+
+// ---------------------------------------------------------------- permute
+constexpr int PCH = 128;  // tokens per chunk
+constexpr int ROW_ALIGN = 128;
+
+__global__ void __launch_bounds__(256) permute_count_kernel(const int32_t* __restrict__ idx,
+                                                            int64_t T, int E, int k,
+                                                            int32_t* __restrict__ chunk_counts) {
+  extern __shared__ int32_t hist[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
+  __syncthreads();
+  const int64_t p0 = int64_t(blockIdx.x) * PCH * k;
+  const int64_t p1 = (p0 + int64_t(PCH) * k < T * k) ? p0 + int64_t(PCH) * k : T * k;
+  for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) atomicAdd(&hist[idx[p]], 1);
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    chunk_counts[int64_t(blockIdx.x) * E + e] = hist[e];
+}
+
+// One CTA: per-expert exclusive prefix over chunks, padded expert offsets,
+// m-block -> expert table.
+__global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict__ chunk_counts,
+                                                            int nchunks, int E, int64_t T,
+                                                            int shared, int32_t* __restrict__ counts,
+                                                            int32_t* __restrict__ expert_off,
+                                                            int32_t* __restrict__ mblock_expert,
+                                                            int32_t* __restrict__ meta) {
+  extern __shared__ int32_t sh[];  // [E] padded sizes, then [E] offsets
+  int32_t* pad = sh;
+  int32_t* off = sh + E;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int32_t run = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int32_t n = chunk_counts[int64_t(c) * E + e];
+      chunk_counts[int64_t(c) * E + e] = run;
+      run += n;
+    }
+    counts[e] = run;
+    pad[e] = (run + ROW_ALIGN - 1) / ROW_ALIGN * ROW_ALIGN;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t acc = 0;
+    for (int e = 0; e < E; ++e) {
+      off[e] = acc;
+      acc += pad[e];
+    }
+    const int32_t routed_mb = acc / ROW_ALIGN;
+    const int32_t shared_mb = shared ? int32_t((T + ROW_ALIGN - 1) / ROW_ALIGN) : 0;
+    meta[0] = routed_mb + shared_mb;
+    meta[1] = routed_mb;
+    meta[2] = acc;
+    meta[3] = int32_t(T);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    expert_off[e] = off[e];
+    for (int32_t b = off[e] / ROW_ALIGN; b < (off[e] + pad[e]) / ROW_ALIGN; ++b)
+      mblock_expert[b] = e;
+  }
+  if (shared) {
+    const int32_t rmb = meta[1];
+    for (int32_t b = threadIdx.x; b < meta[0] - rmb; b += blockDim.x) mblock_expert[rmb + b] = E;
+  }
+}
+
+__global__ void __launch_bounds__(256) permute_scatter_kernel(
+    const int32_t* __restrict__ idx, const uint16_t* __restrict__ x, int64_t T, int E, int k,
+    int64_t h, const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ expert_off,
+    int32_t* __restrict__ row_of, uint16_t* __restrict__ xperm) {
+  extern __shared__ int32_t sm[];  // cursor[E], rows[PCH * k]
+  int32_t* cursor = sm;
+  int32_t* rows = sm + E;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) cursor[e] = 0;
+  __syncthreads();
+  const int64_t t0 = int64_t(blockIdx.x) * PCH;
+  const int ntok = int(T - t0 < PCH ? T - t0 : PCH);
+  const int npairs = ntok * k;
+  if (threadIdx.x < 32) {  // warp 0 ranks pairs in (t, j) order
+    const int lane = threadIdx.x;
+    for (int s = 0; s < npairs; s += 32) {
+      const int pl = s + lane;
+      const bool act = pl < npairs;
+      const unsigned am = __ballot_sync(0xffffffffu, act);
+      if (act) {
+        const int e = idx[t0 * k + pl];
+        const unsigned peers = __match_any_sync(am, e);
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        const int before = cursor[e];
+        const int pos = expert_off[e] + chunk_base[int64_t(blockIdx.x) * E + e] + before + rank;
+        rows[pl] = pos;
+        row_of[t0 * k + pl] = pos;
+        __syncwarp(am);
+        if (lane == 31 - __clz(peers)) cursor[e] = before + __popc(peers);
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // gather: each warp copies whole token rows to their k destinations
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t segs = h / 8;
+  for (int tl = warp; tl < ntok; tl += blockDim.x >> 5) {
+    const uint4* src = reinterpret_cast<const uint4*>(x + (t0 + tl) * h);
+    for (int64_t s = lane; s < segs; s += 32) {
+      const uint4 v = __ldg(src + s);
+      for (int j = 0; j < k; ++j)
+        reinterpret_cast<uint4*>(xperm + int64_t(rows[tl * k + j]) * h)[s] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- combine
+__global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict__ O,
+                                                      const int32_t* __restrict__ row_of,
+                                                      const float* __restrict__ wts,
+                                                      const int32_t* __restrict__ meta,
+                                                      const uint16_t* __restrict__ resid,
+                                                      uint16_t* __restrict__ y, int64_t T, int k,
+                                                      int64_t h, int shared) {
+  const int64_t t = blockIdx.x;
+  if (t >= T) return;
+  __shared__ int32_t srow[TOPK_MAXK + 1];
+  __shared__ float sw[TOPK_MAXK];
+  if (threadIdx.x < k) {
+    srow[threadIdx.x] = row_of[t * k + threadIdx.x];
+    sw[threadIdx.x] = wts[t * k + threadIdx.x];
+  }
+  if (threadIdx.x == 0) srow[TOPK_MAXK] = shared ? meta[2] + int32_t(t) : 0;
+  __syncthreads();
+  const int64_t segs = h / 8;
+  for (int64_t s = threadIdx.x; s < segs; s += blockDim.x) {
+    float acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+    for (int j = 0; j < k; ++j) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(O + int64_t(srow[j]) * h) + s);
+      const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+      const float wj = sw[j];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[2 * q] = __fmaf_rn(wj, __uint_as_float(u[q] << 16), acc[2 * q]);
+        acc[2 * q + 1] = __fmaf_rn(wj, __uint_as_float(u[q] & 0xffff0000u), acc[2 * q + 1]);
+      }
+    }
+    if (shared) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(O + int64_t(srow[TOPK_MAXK]) * h) + s);
+      const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[2 * q] += __uint_as_float(u[q] << 16);
+        acc[2 * q + 1] += __uint_as_float(u[q] & 0xffff0000u);
+      }
+    }
+    if (resid) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(resid + t * h) + s);
+      const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[2 * q] += __uint_as_float(u[q] << 16);
+        acc[2 * q + 1] += __uint_as_float(u[q] & 0xffff0000u);
+      }
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      o[q] = uint32_t(bf16_bits(acc[2 * q])) | (uint32_t(bf16_bits(acc[2 * q + 1])) << 16);
+    reinterpret_cast<uint4*>(y + t * h)[s] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// ---------------------------------------------------------------- pull
+__device__ __forceinline__ uint4 ld_nc_na(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Items are claimed in plan order (item i by CTA i mod grid), so the
+// concurrently active slices follow the TDM peer rotation.
+__global__ void __launch_bounds__(1024) pull_kernel(const PullItem* __restrict__ items, int n) {
+  constexpr int U = 4;
+  for (int it = blockIdx.x; it < n; it += gridDim.x) {
+    const PullItem w = items[it];
+    const uint4* src = reinterpret_cast<const uint4*>(w.src);
+    uint4* dst = reinterpret_cast<uint4*>(w.dst);
+    const int64_t nv = int64_t(w.len / 16);
+    const int64_t step = int64_t(blockDim.x) * U;
+    int64_t i = threadIdx.x;
+    for (; i + (U - 1) * blockDim.x < nv; i += step) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_nc_na(src + i + u * blockDim.x);
+#pragma unroll
+      for (int u = 0; u < U; ++u) __stcs(dst + i + u * blockDim.x, v[u]);
+    }
+    for (; i < nv; i += blockDim.x) __stcs(dst + i, ld_nc_na(src + i));
+    const int64_t tail0 = nv * 16;
+    for (int64_t b = tail0 + threadIdx.x; b < int64_t(w.len); b += blockDim.x)
+      static_cast<uint8_t*>(w.dst)[b] = static_cast<const uint8_t*>(w.src)[b];
+  }
+}
+
+int grid_for(int64_t work, int block) {
+  int64_t g = (work + block - 1) / block;
+  if (g > 148 * 16) g = 148 * 16;
+  return int(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+void launch_fill_slots(uint16_t* dst, const uint64_t* seeds, int nslots, int64_t slot_elems,
+                       float scale, cudaStream_t st) {
+  if (nslots <= 0) return;
+  fill_slots_kernel<<<grid_for(nslots * (slot_elems / 8), 256), 256, 0, st>>>(dst, seeds, nslots,
+                                                                             slot_elems, scale);
+}
+
+void launch_fill(uint16_t* dst, int64_t n, uint64_t seed, float scale, cudaStream_t st) {
+  if (n > 0) fill_kernel<<<grid_for(n, 256), 256, 0, st>>>(dst, n, seed, scale);
+}
+
+void launch_fill_f32(float* dst, int64_t n, uint64_t seed, float scale, cudaStream_t st) {
+  if (n > 0) fill_f32_kernel<<<grid_for(n, 256), 256, 0, st>>>(dst, n, seed, scale);
+}
+
+void launch_router_logits(const uint16_t* x, const uint16_t* w, float* logits, int64_t T, int E,
+                          int64_t K, cudaStream_t st) {
+  if (T <= 0) return;
+  dim3 grid(unsigned((T + RB_M - 1) / RB_M), unsigned((E + RB_N - 1) / RB_N));
+  router_logits_kernel<<<grid, 256, 0, st>>>(x, w, logits, T, E, K);
+}
+
+void launch_topk(const float* logits, const float* bias, int32_t* idx, float* wts, int64_t T,
+                 const RouterCfg& c, cudaStream_t st) {
+  if (T <= 0) return;
+  topk_kernel<<<unsigned((T + 7) / 8), 256, 0, st>>>(logits, bias, idx, wts, T, c);
+}
+
+int64_t permute_scratch_ints(int64_t T, int E) {
+  const int64_t nch = (T + PCH - 1) / PCH;
+  return nch * E + E;
+}
+
+void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int k, int64_t h,
+                    int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
+                    int32_t* meta, uint16_t* xperm, int32_t* scratch, cudaStream_t st) {
+  const int nch = int((T + PCH - 1) / PCH);
+  int32_t* chunk_counts = scratch;
+  int32_t* expert_off = scratch + int64_t(nch) * E;
+  if (nch > 0)
+    permute_count_kernel<<<nch, 256, E * sizeof(int32_t), st>>>(idx, T, E, k, chunk_counts);
+  permute_scan_kernel<<<1, 1024, 2 * E * sizeof(int32_t), st>>>(
+      chunk_counts, nch, E, T, shared, counts, expert_off, mblock_expert, meta);
+  if (nch > 0)
+    permute_scatter_kernel<<<nch, 256, (E + PCH * k) * sizeof(int32_t), st>>>(
+        idx, x, T, E, k, h, chunk_counts, expert_off, row_of, xperm);
+}
+
+void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
+                    const int32_t* meta, const uint16_t* resid, uint16_t* y, int64_t T, int k,
+                    int64_t h, int shared, cudaStream_t st) {
+  if (T > 0)
+    combine_kernel<<<unsigned(T), 128, 0, st>>>(O, row_of, wts, meta, resid, y, T, k, h, shared);
+}
+
+void launch_pull(const PullItem* items, int n, int ctas, cudaStream_t st) {
+  if (n > 0) pull_kernel<<<ctas, 1024, 0, st>>>(items, n);
+}
+
+}  // namespace dwdp

@@ -1,0 +1,57 @@
+// Launch wrappers of the DWDP sm_100a kernels (host-callable, plain types).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace dwdp {
+
+struct RouterCfg {
+  int E, k, scoring, n_group, topk_group, norm_topk;
+  float routed_scale;
+};
+
+// Counter-hash bf16 fill (bit-identical to oracle_fill_bf16): slot s of
+// `nslots` consecutive slots of `slot_elems` elements uses seeds[s].
+void launch_fill_slots(uint16_t* dst, const uint64_t* seeds_dev, int nslots,
+                       int64_t slot_elems, float scale, cudaStream_t st);
+void launch_fill(uint16_t* dst, int64_t n, uint64_t seed, float scale, cudaStream_t st);
+void launch_fill_f32(float* dst, int64_t n, uint64_t seed, float scale, cudaStream_t st);
+
+// logits[T][E] = sum_i x[t][i] * w[e][i], fp32 fused multiply-adds in
+// ascending i (bit-exact contract with the oracle).
+void launch_router_logits(const uint16_t* x, const uint16_t* w, float* logits, int64_t T,
+                          int E, int64_t K, cudaStream_t st);
+// Scoring + group-limited top-k + weights; idx/wts [T][k].
+void launch_topk(const float* logits, const float* bias, int32_t* idx, float* wts, int64_t T,
+                 const RouterCfg& c, cudaStream_t st);
+
+// Stable expert-major permutation + gather of x rows.
+//  counts[E]            tokens per expert
+//  row_of[T*k]          destination row of pair (t, j)
+//  mblock_expert[...]   expert of each 128-row block (routed then shared = E)
+//  meta[4]              {total m-blocks, routed m-blocks, routed rows, T}
+// scratch: >= permute_scratch_ints(T, E) int32.
+int64_t permute_scratch_ints(int64_t T, int E);
+void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int k, int64_t h,
+                    int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
+                    int32_t* meta, uint16_t* xperm, int32_t* scratch, cudaStream_t st);
+
+// y[t] = sum_j w[t,j] * O[row_of[t,j]] (+ O[shared_row0 + t]) (+ x[t]).
+void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
+                    const int32_t* meta, const uint16_t* resid, uint16_t* y, int64_t T, int k,
+                    int64_t h, int shared, cudaStream_t st);
+
+// One-launch P2P pull of a slice list over NVLink: work[i] = {src, dst, len}.
+struct PullItem {
+  const void* src;
+  void* dst;
+  uint64_t len;
+};
+void launch_pull(const PullItem* items_dev, int n_items, int ctas, cudaStream_t st);
+
+// Grouped GEMM on tcgen05 (gemm_sm100.cu). See GemmArgs there.
+struct GroupedGemm;
+
+}  // namespace dwdp

@@ -1,0 +1,597 @@
+// Per-GPU DWDP runtime. Reference semantics (paths under /root/reference/proj):
+//   split-weight placement  — north-star item 1; experts of placement.cpp:75-111
+//   prefetch engine/handles — CopyEngineSim, simcore.cpp:72-283 / simcore.hpp:87-151
+//   per-rank layer loop     — simulate_dwdp MoeGate/MoeOps, simcore.cpp:640-733
+//   static transfer list    — prefetch_transfers, simcore.cpp:486-515
+#include "runtime.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+
+#include "gemm_sm100.hpp"
+
+namespace dwdp {
+
+namespace {
+constexpr uint32_t kIpcMagic = 0x44574450;  // "DWDP"
+struct IpcBlob {
+  uint32_t magic;
+  int32_t rank, nslots, c;
+  int64_t slot_elems;
+  cudaIpcMemHandle_t h[3];
+};
+static_assert(sizeof(IpcBlob) <= DWDP_IPC_BLOB_BYTES, "ipc blob too large");
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) DWDP_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+uint64_t tensor_seed(uint64_t base, int layer, int expert, int t) {
+  return Rng::mix(Rng::mix(base, 0x1000ULL + uint64_t(layer)), uint64_t(expert) * 8ULL + uint64_t(t));
+}
+}  // namespace
+
+// ===================================================================== //
+// construction
+
+Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
+  E_ = c.num_experts;
+  k_ = c.top_k;
+  L_ = c.num_layers;
+  WL_ = c.weight_layers > 0 ? std::min(c.weight_layers, c.num_layers) : c.num_layers;
+  N_ = c.group_size;
+  rank_ = c.rank;
+  h_ = c.hidden;
+  f_ = c.ffn;
+  shared_ = c.shared_ffn > 0;
+  require(L_ >= 1, "ctx: num_layers must be >= 1");
+  require(E_ >= 1 && E_ <= 512, "ctx: num_experts must be in [1, 512]");
+  require(k_ >= 1 && k_ <= 16 && k_ <= E_, "ctx: top_k must be in [1, min(16, E)]");
+  require(h_ > 0 && h_ % 256 == 0, "ctx: hidden must be a positive multiple of 256");
+  require(f_ > 0 && f_ % 128 == 0, "ctx: ffn must be a positive multiple of 128");
+  require(c.shared_ffn == 0 || c.shared_ffn == c.ffn, "ctx: shared_ffn must be 0 or == ffn");
+  require(c.scoring == 0 || c.scoring == 1, "ctx: unknown scoring");
+  const int G = c.n_group > 0 ? c.n_group : 1;
+  require(G <= 32 && E_ % G == 0, "ctx: n_group must divide E and be <= 32");
+  require(c.topk_group >= 1 && c.topk_group <= G, "ctx: topk_group must be in [1, n_group]");
+  require(N_ >= 1, "ctx: group_size must be >= 1");
+  require(rank_ >= 0 && rank_ < N_, "ctx: rank out of range");
+  require(c.max_tokens >= 1, "ctx: max_tokens must be >= 1");
+  require(c.engine == DWDP_ENGINE_COPY || c.engine == DWDP_ENGINE_PULL, "ctx: unknown engine");
+  require(!c.tdm || c.slice_size > 0, "dwdp.slice_size must be > 0 with tdm");
+  DeviceGuard dg(c.device);
+  int cc = 0;
+  cudaDeviceProp prop;
+  DWDP_CUDA(cudaGetDeviceProperties(&prop, c.device));
+  cc = prop.major * 10 + prop.minor;
+  if (cc < 100 || cc >= 110)
+    throw CudaError("dwdp: device " + std::to_string(c.device) + " is sm_" + std::to_string(cc) +
+                    "; this build targets sm_100a only");
+  num_sms_ = prop.multiProcessorCount;
+  if (N_ >= 2) pl_ = build_placement(E_, N_, c.extra_redundancy);
+  build_layout();
+
+  // ---- arenas (one allocation per tensor kind so each is an IPC object)
+  slot_elems_ = f_ * h_;
+  const uint64_t slot_bytes = uint64_t(slot_elems_) * 2;
+  for (int t = 0; t < 3; ++t) {
+    arena_[t] = static_cast<uint16_t*>(dalloc(slot_bytes * uint64_t(nslots_), nullptr));
+  }
+  weight_bytes = 3 * slot_bytes * uint64_t(recv_base_);
+  recv_bytes = 3 * slot_bytes * uint64_t(nslots_ - recv_base_);
+  router_w_ = static_cast<uint16_t*>(dalloc(size_t(WL_) * E_ * h_ * 2, &weight_bytes));
+  bias_ = static_cast<float*>(dalloc(size_t(WL_) * E_ * 4, &weight_bytes));
+  DWDP_CUDA(cudaMemset(bias_, 0, size_t(WL_) * E_ * 4));
+
+  // ---- slot tables [L][2][E+1]
+  std::vector<int32_t> tab(size_t(L_) * 2 * (E_ + 1));
+  for (int l = 0; l < L_; ++l)
+    for (int p = 0; p < 2; ++p)
+      for (int e = 0; e <= E_; ++e) tab[(size_t(l) * 2 + p) * (E_ + 1) + e] = slot_of(l, p, e);
+  slot_tab_ = static_cast<int32_t*>(dalloc(tab.size() * 4, &workspace_bytes));
+  DWDP_CUDA(cudaMemcpy(slot_tab_, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+
+  // ---- workspace sized for max_tokens
+  max_tokens_ = c.max_tokens;
+  max_mb_ = (max_tokens_ * k_ + int64_t(E_) * 127) / 128 + 1 + (shared_ ? (max_tokens_ + 127) / 128 : 0);
+  max_rows_ = max_mb_ * 128;
+  logits_ = static_cast<float*>(dalloc(size_t(max_tokens_) * E_ * 4, &workspace_bytes));
+  idx_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * k_ * 4, &workspace_bytes));
+  wts_ = static_cast<float*>(dalloc(size_t(max_tokens_) * k_ * 4, &workspace_bytes));
+  row_of_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * k_ * 4, &workspace_bytes));
+  counts_ = static_cast<int32_t*>(dalloc(size_t(E_) * 4, &workspace_bytes));
+  mblock_ = static_cast<int32_t*>(dalloc(size_t(max_mb_) * 4, &workspace_bytes));
+  meta_ = static_cast<int32_t*>(dalloc(16 * 4, &workspace_bytes));
+  scratch_ = static_cast<int32_t*>(
+      dalloc(size_t(permute_scratch_ints(max_tokens_, E_)) * 4, &workspace_bytes));
+  xperm_ = static_cast<uint16_t*>(dalloc(size_t(max_rows_) * h_ * 2, &workspace_bytes));
+  hbuf_ = static_cast<uint16_t*>(dalloc(size_t(max_rows_) * f_ * 2, &workspace_bytes));
+
+  tm_gate_ = make_tmap_bf16(arena_[0], int64_t(nslots_) * f_, h_, 128);
+  tm_up_ = make_tmap_bf16(arena_[1], int64_t(nslots_) * f_, h_, 128);
+  tm_down_ = make_tmap_bf16(arena_[2], int64_t(nslots_) * h_, f_, 256);
+  tm_xperm_ = make_tmap_bf16(xperm_, max_rows_, h_, 128);
+  tm_h_ = make_tmap_bf16(hbuf_, max_rows_, f_, 128);
+
+  DWDP_CUDA(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
+  DWDP_CUDA(cudaEventCreate(&epoch_));
+  DWDP_CUDA(cudaEventRecord(epoch_, copy_st_));
+  for (auto& ev : moe_done_) DWDP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  for (int t = 0; t < 3; ++t) peer_arena_[t].assign(size_t(N_), nullptr);
+  resident_parity_.assign(size_t(L_), 0);
+  build_copy_plan();
+  DWDP_CUDA(cudaDeviceSynchronize());
+}
+
+Ctx::~Ctx() {
+  DeviceGuard dg(cfg.device);
+  cudaDeviceSynchronize();
+  for (auto& r : recs_)
+    for (cudaEvent_t e : {r.gate0, r.gate1, r.moe_end, r.merge_end})
+      if (e) cudaEventDestroy(e);
+  for (auto& p : plans_) {
+    if (p.start) cudaEventDestroy(p.start);
+    if (p.done) cudaEventDestroy(p.done);
+  }
+  for (cudaEvent_t e : free_events_) cudaEventDestroy(e);
+  for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
+  void* bufs[] = {arena_[0], arena_[1], arena_[2], router_w_, bias_, slot_tab_, logits_, idx_,
+                  wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  for (auto& ev : moe_done_)
+    if (ev) cudaEventDestroy(ev);
+  if (epoch_) cudaEventDestroy(epoch_);
+  if (copy_st_) cudaStreamDestroy(copy_st_);
+}
+
+void* Ctx::dalloc(size_t bytes, uint64_t* account) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  DWDP_CUDA(cudaMalloc(&p, bytes));
+  if (account) *account += bytes;
+  return p;
+}
+
+// Arena slot layout (per tensor kind, all three identical):
+//   [0, WL*c)                  owned experts, weight layer wl at wl*c
+//   [WL*c, WL*c + WL)          shared expert of each weight layer
+//   [recv, recv + 2*(E-c))     DWDP receive buffers, parity g % 2
+//   [merge, merge + (E-c))     merged copy (merge_elim == 0 baseline only)
+void Ctx::build_layout() {
+  local_index_.assign(size_t(E_), -1);
+  recv_index_.assign(size_t(E_), -1);
+  if (N_ >= 2) {
+    c_ = pl_.local_count;
+    const auto& mine = pl_.local_sets[size_t(rank_)];
+    for (int i = 0; i < c_; ++i) local_index_[size_t(mine[size_t(i)])] = i;
+    int j = 0;
+    for (const auto& f : pl_.fetch_lists[size_t(rank_)]) recv_index_[size_t(f.first)] = j++;
+    nrecv_ = E_ - c_;
+  } else {
+    c_ = E_;
+    for (int e = 0; e < E_; ++e) local_index_[size_t(e)] = e;
+    nrecv_ = 0;
+  }
+  shared_base_ = WL_ * c_;
+  recv_base_ = shared_base_ + (shared_ ? WL_ : 0);
+  merge_base_ = recv_base_ + 2 * nrecv_;
+  nslots_ = merge_base_ + (cfg.merge_elim ? 0 : nrecv_);
+}
+
+int Ctx::slot_of(int layer, int parity, int e) const {
+  const int wl = layer % WL_;
+  if (e == E_) return shared_ ? shared_base_ + wl : 0;
+  if (local_index_[size_t(e)] >= 0) return wl * c_ + local_index_[size_t(e)];
+  if (!cfg.merge_elim) return merge_base_ + recv_index_[size_t(e)];
+  return recv_base_ + parity * nrecv_ + recv_index_[size_t(e)];
+}
+
+// Static per-rank transfer list (prefetch_transfers, simcore.cpp:486-515):
+// for each tensor, one ShardRef per (peer, contiguous run of slots); the
+// reference emits one per (peer, tensor) with src_offset 0, which is the
+// single-run case (every divisible placement).
+void Ctx::build_copy_plan() {
+  runs_.clear();
+  plan_slices_.clear();
+  plan_bytes_ = 0;
+  if (nrecv_ == 0) return;
+  std::vector<ShardRun> base;  // tensor-independent runs
+  std::map<int, int> runs_per_peer;
+  for (const auto& [e, src] : pl_.fetch_lists[size_t(rank_)]) {
+    const auto& ls = pl_.local_sets[size_t(src)];
+    const int sslot = int(std::lower_bound(ls.begin(), ls.end(), e) - ls.begin());
+    const int dslot = recv_index_[size_t(e)];
+    if (!base.empty() && base.back().peer == src &&
+        base.back().src_slot0 + base.back().count == sslot &&
+        base.back().dst_slot0 + base.back().count == dslot) {
+      ++base.back().count;
+    } else {
+      base.push_back({src, 0, 1, sslot, dslot, uint64_t(runs_per_peer[src]++)});
+    }
+  }
+  std::stable_sort(base.begin(), base.end(),
+                   [](const ShardRun& a, const ShardRun& b) { return a.peer < b.peer; });
+  const uint64_t slot_bytes = uint64_t(slot_elems_) * 2;
+  std::vector<ShardRef> shards;
+  uint64_t max_size = 0;
+  for (int t = 0; t < 3; ++t)
+    for (const auto& b : base) {
+      ShardRun r = b;
+      r.tensor = t;
+      r.param_id = uint64_t(t) + 3 * b.param_id;  // b.param_id = run index within peer
+      runs_.push_back(r);
+      shards.push_back({r.peer, r.param_id, uint64_t(r.count) * slot_bytes,
+                        uint64_t(r.src_slot0) * slot_bytes});
+      max_size = std::max(max_size, uint64_t(r.count) * slot_bytes);
+    }
+  const uint64_t slice = cfg.tdm ? cfg.slice_size : max_size;
+  plan_slices_ = dwdp::build_copy_plan(shards, slice, rank_);
+  for (const auto& s : plan_slices_) plan_bytes_ += double(s.length);
+}
+
+void* Ctx::peer_src(int peer, int t, int wl, uint64_t src_offset) const {
+  const uint64_t slot_bytes = uint64_t(slot_elems_) * 2;
+  return static_cast<uint8_t*>(peer_arena_[t][size_t(peer)]) + uint64_t(wl) * c_ * slot_bytes +
+         src_offset;
+}
+
+uint8_t* Ctx::dst_addr(int t, int parity, const ShardRun& r, uint64_t dst_offset) const {
+  const uint64_t slot_bytes = uint64_t(slot_elems_) * 2;
+  return reinterpret_cast<uint8_t*>(arena_[t]) +
+         uint64_t(recv_base_ + parity * nrecv_ + r.dst_slot0) * slot_bytes + dst_offset;
+}
+
+// ===================================================================== //
+// peers
+
+void Ctx::export_ipc(void* out) {
+  DeviceGuard dg(cfg.device);
+  IpcBlob b{};
+  b.magic = kIpcMagic;
+  b.rank = rank_;
+  b.nslots = nslots_;
+  b.c = c_;
+  b.slot_elems = slot_elems_;
+  for (int t = 0; t < 3; ++t) DWDP_CUDA(cudaIpcGetMemHandle(&b.h[t], arena_[t]));
+  std::memset(out, 0, DWDP_IPC_BLOB_BYTES);
+  std::memcpy(out, &b, sizeof b);
+}
+
+void Ctx::open_peers(const void* blobs) {
+  DeviceGuard dg(cfg.device);
+  for (int p = 0; p < N_; ++p) {
+    if (p == rank_) continue;
+    IpcBlob b;
+    std::memcpy(&b, static_cast<const uint8_t*>(blobs) + size_t(p) * DWDP_IPC_BLOB_BYTES, sizeof b);
+    require(b.magic == kIpcMagic && b.rank == p, "open_peers: malformed blob");
+    require(b.c == c_ && b.slot_elems == slot_elems_, "open_peers: peer arena geometry differs");
+    for (int t = 0; t < 3; ++t) {
+      void* ptr = nullptr;
+      DWDP_CUDA(cudaIpcOpenMemHandle(&ptr, b.h[t], cudaIpcMemLazyEnablePeerAccess));
+      peer_arena_[t][size_t(p)] = ptr;
+      ipc_opened_.push_back(ptr);
+    }
+  }
+  link_local({});
+}
+
+void Ctx::link_local(const std::vector<Ctx*>& all) {
+  DeviceGuard dg(cfg.device);
+  for (Ctx* o : all) {
+    if (o == this) continue;
+    if (o->cfg.device != cfg.device) {
+      const cudaError_t e = cudaDeviceEnablePeerAccess(o->cfg.device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) DWDP_CUDA(e);
+      cudaGetLastError();
+    }
+    for (int t = 0; t < 3; ++t) peer_arena_[t][size_t(o->rank_)] = o->arena_[t];
+  }
+  // Pull-kernel work lists for every (weight layer, parity).
+  if (nrecv_ == 0) return;
+  const size_t n = plan_slices_.size();
+  std::vector<PullItem> items(size_t(WL_) * 2 * n);
+  std::map<std::pair<int, uint64_t>, const ShardRun*> by_shard;
+  for (const auto& r : runs_) by_shard[{r.peer, r.param_id}] = &r;
+  for (int wl = 0; wl < WL_; ++wl)
+    for (int par = 0; par < 2; ++par)
+      for (size_t i = 0; i < n; ++i) {
+        const Slice& s = plan_slices_[i];
+        const ShardRun* r = by_shard.at({s.src_rank, s.param_id});
+        if (!peer_arena_[r->tensor][size_t(r->peer)]) return;  // peers not wired yet
+        items[(size_t(wl) * 2 + size_t(par)) * n + i] = {
+            peer_src(r->peer, r->tensor, wl, s.src_offset), dst_addr(r->tensor, par, *r, s.dst_offset),
+            s.length};
+      }
+  if (!pull_items_) pull_items_ = static_cast<PullItem*>(dalloc(items.size() * sizeof(PullItem), &workspace_bytes));
+  DWDP_CUDA(cudaMemcpy(pull_items_, items.data(), items.size() * sizeof(PullItem), cudaMemcpyHostToDevice));
+}
+
+// ===================================================================== //
+// weights
+
+void Ctx::init_weights(float bias_scale) {
+  DeviceGuard dg(cfg.device);
+  const uint64_t base = cfg.weight_seed;
+  const int owned = recv_base_;  // local + shared slots
+  std::vector<uint64_t> seeds(static_cast<size_t>(owned));
+  uint64_t* dseeds = static_cast<uint64_t*>(dalloc(size_t(owned) * 8 + 8, nullptr));
+  const float sh = 1.0f / std::sqrt(float(h_)), sf = 1.0f / std::sqrt(float(f_));
+  const std::vector<int> ident = [&] {
+    std::vector<int> v(static_cast<size_t>(E_));
+    for (int e = 0; e < E_; ++e) v[size_t(e)] = e;
+    return v;
+  }();
+  const std::vector<int>& mine = N_ >= 2 ? pl_.local_sets[size_t(rank_)] : ident;
+  for (int t = 0; t < 3; ++t) {
+    for (int wl = 0; wl < WL_; ++wl) {
+      for (int i = 0; i < c_; ++i) seeds[size_t(wl * c_ + i)] = tensor_seed(base, wl, mine[size_t(i)], t);
+      if (shared_) seeds[size_t(shared_base_ + wl)] = tensor_seed(base, wl, E_, t);
+    }
+    DWDP_CUDA(cudaMemcpy(dseeds, seeds.data(), size_t(owned) * 8, cudaMemcpyHostToDevice));
+    launch_fill_slots(arena_[t], dseeds, owned, slot_elems_, t == 2 ? sf : sh, nullptr);
+    ++launches;
+    DWDP_CUDA(cudaGetLastError());
+  }
+  for (int wl = 0; wl < WL_; ++wl) {
+    launch_fill(router_w_ + size_t(wl) * E_ * h_, int64_t(E_) * h_, tensor_seed(base, wl, E_ + 1, 0),
+                sh, nullptr);
+    if (bias_scale != 0.0f)
+      launch_fill_f32(bias_ + size_t(wl) * E_, E_, tensor_seed(base, wl, E_ + 1, 1), bias_scale, nullptr);
+    launches += 2;
+  }
+  DWDP_CUDA(cudaGetLastError());
+  DWDP_CUDA(cudaDeviceSynchronize());
+  cudaFree(dseeds);
+}
+
+void Ctx::set_bias(const float* host) {
+  DeviceGuard dg(cfg.device);
+  for (int wl = 0; wl < WL_; ++wl)
+    DWDP_CUDA(cudaMemcpy(bias_ + size_t(wl) * E_, host, size_t(E_) * 4, cudaMemcpyHostToDevice));
+}
+
+void Ctx::read_expert(int layer, int expert, int t, void* host) {
+  DeviceGuard dg(cfg.device);
+  require(layer >= 0 && layer < L_ && expert >= 0 && expert <= E_ && t >= 0 && t < 3,
+          "read_expert: index out of range");
+  require(expert < E_ || shared_, "read_expert: no shared expert");
+  const int slot = slot_of(layer, resident_parity_[size_t(layer)], expert);
+  DWDP_CUDA(cudaMemcpy(host, arena_[t] + int64_t(slot) * slot_elems_, size_t(slot_elems_) * 2,
+                       cudaMemcpyDeviceToHost));
+}
+
+// ===================================================================== //
+// prefetch engine: issue_plan / plan_done / plan_*_time
+
+cudaEvent_t Ctx::take_event() {
+  if (!free_events_.empty()) {
+    cudaEvent_t e = free_events_.back();
+    free_events_.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  DWDP_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+int64_t Ctx::prefetch_issue(int64_t g) {
+  DeviceGuard dg(cfg.device);
+  if (nrecv_ == 0) return -1;  // full replication: nothing to fetch (simcore.cpp:625-628)
+  require(g >= 0, "prefetch_issue: negative layer");
+  if (plan_of_g_.size() <= size_t(g)) plan_of_g_.resize(size_t(g) + 1, -2);
+  invariant(plan_of_g_[size_t(g)] == -2, "dwdp: plan double issue");
+  for (int p = 0; p < N_; ++p)
+    require(p == rank_ || peer_arena_[0][size_t(p)] != nullptr, "prefetch_issue: peers not wired");
+  const int par = int(g & 1), l = int(g % L_), wl = l % WL_;
+  // WAR: buffer g%2 was last read by the MoE of layer g-2.
+  if (moe_done_recorded_[par]) DWDP_CUDA(cudaStreamWaitEvent(copy_st_, moe_done_[par], 0));
+  Plan pl;
+  pl.g = g;
+  pl.start = take_event();
+  pl.done = take_event();
+  pl.bytes = plan_bytes_;
+  DWDP_CUDA(cudaEventRecord(pl.start, copy_st_));
+  if (cfg.engine == DWDP_ENGINE_PULL) {
+    require(pull_items_ != nullptr, "prefetch_issue: pull lists not built (peers not wired)");
+    const size_t n = plan_slices_.size();
+    launch_pull(pull_items_ + (size_t(wl) * 2 + size_t(par)) * n, int(n),
+                cfg.pull_ctas > 0 ? cfg.pull_ctas : 16, copy_st_);
+    ++launches;
+    DWDP_CUDA(cudaGetLastError());
+  } else {
+    std::map<std::pair<int, uint64_t>, const ShardRun*> by_shard;
+    for (const auto& r : runs_) by_shard[{r.peer, r.param_id}] = &r;
+    for (const Slice& s : plan_slices_) {
+      const ShardRun* r = by_shard.at({s.src_rank, s.param_id});
+      DWDP_CUDA(cudaMemcpyAsync(dst_addr(r->tensor, par, *r, s.dst_offset),
+                                peer_src(r->peer, r->tensor, wl, s.src_offset), s.length,
+                                cudaMemcpyDeviceToDevice, copy_st_));
+    }
+  }
+  DWDP_CUDA(cudaEventRecord(pl.done, copy_st_));
+  plans_.push_back(pl);
+  plan_of_g_[size_t(g)] = int64_t(plans_.size()) - 1;
+  resident_parity_[size_t(l)] = par;
+  return int64_t(plans_.size()) - 1;
+}
+
+bool Ctx::prefetch_done(int64_t h) {
+  if (h < 0) return true;
+  require(size_t(h) < plans_.size(), "prefetch: unknown handle");
+  const cudaError_t e = cudaEventQuery(plans_[size_t(h)].done);
+  if (e == cudaErrorNotReady) return false;
+  DWDP_CUDA(e);
+  return true;
+}
+
+void Ctx::prefetch_wait(int64_t h, cudaStream_t st) {
+  if (h < 0) return;
+  require(size_t(h) < plans_.size(), "prefetch: unknown handle");
+  DWDP_CUDA(cudaStreamWaitEvent(st, plans_[size_t(h)].done, 0));
+}
+
+void Ctx::prefetch_times(int64_t h, int64_t* s, int64_t* e, double* bytes) {
+  *s = *e = -1;
+  *bytes = 0;
+  if (h < 0) return;
+  require(size_t(h) < plans_.size(), "prefetch: unknown handle");
+  const Plan& p = plans_[size_t(h)];
+  *bytes = p.bytes;
+  if (!prefetch_done(h)) return;
+  float ms0 = 0, ms1 = 0;
+  DWDP_CUDA(cudaEventElapsedTime(&ms0, epoch_, p.start));
+  DWDP_CUDA(cudaEventElapsedTime(&ms1, epoch_, p.done));
+  *s = int64_t(std::llround(double(ms0) * 1e6));
+  *e = int64_t(std::llround(double(ms1) * 1e6));
+}
+
+// ===================================================================== //
+// MoE forward
+
+void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint16_t* y,
+                      const uint16_t* resid, cudaStream_t st) {
+  require(layer >= 0 && layer < L_, "moe_forward: layer out of range");
+  require(T >= 0 && T <= max_tokens_, "moe_forward: T exceeds max_tokens");
+  if (T == 0) return;
+  const int wl = layer % WL_;
+  RouterCfg rc{E_, k_, cfg.scoring, cfg.n_group, cfg.topk_group, cfg.norm_topk, cfg.routed_scale};
+  launch_router_logits(x, router_w_ + size_t(wl) * E_ * h_, logits_, T, E_, h_, st);
+  launch_topk(logits_, bias_ + size_t(wl) * E_, idx_, wts_, T, rc, st);
+  launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, meta_, xperm_,
+                 scratch_, st);
+  const int64_t mb_ub = (T * k_ + int64_t(E_) * 127) / 128 + 1 + (shared_ ? (T + 127) / 128 : 0);
+  const CUtensorMap tm_x = shared_ ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
+  const int32_t* stab = slot_tab_ + (size_t(layer) * 2 + size_t(parity)) * (E_ + 1);
+  GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1};
+  launch_grouped_gemm(true, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
+  GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0};
+  launch_grouped_gemm(false, tm_h_, tm_h_, tm_down_, tm_down_, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
+  launch_combine(xperm_, row_of_, wts_, meta_, resid, y, T, k_, h_, shared_ ? 1 : 0, st);
+  launches += 8;
+  DWDP_CUDA(cudaGetLastError());
+}
+
+// One DWDP layer: MoeGate(g) then MoeOps(g) (simcore.cpp:676-710).
+void Ctx::layer_forward(int64_t g, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
+                        cudaStream_t st) {
+  DeviceGuard dg(cfg.device);
+  const int l = int(g % L_), par = int(g & 1);
+  LayerRec rec{g, T, take_event(), take_event(), take_event(), nullptr, -1};
+  DWDP_CUDA(cudaEventRecord(rec.gate0, st));
+  if (nrecv_ > 0) {
+    if (plan_of_g_.size() <= size_t(g) || plan_of_g_[size_t(g)] == -2) prefetch_issue(g);
+    rec.plan = plan_of_g_[size_t(g)];
+    prefetch_wait(rec.plan, st);  // weight_wait (simcore.cpp:684-690)
+  }
+  DWDP_CUDA(cudaEventRecord(rec.gate1, st));
+  // Double buffering: the next layer's buffer is free once this layer's
+  // weights are in use (simcore.cpp:694-696).
+  if (nrecv_ > 0 && (plan_of_g_.size() <= size_t(g + 1) || plan_of_g_[size_t(g + 1)] == -2))
+    prefetch_issue(g + 1);
+  if (nrecv_ > 0 && !cfg.merge_elim) {  // D2D merge baseline (simcore.cpp:700-703)
+    const uint64_t bytes = uint64_t(nrecv_) * uint64_t(slot_elems_) * 2;
+    for (int t = 0; t < 3; ++t)
+      DWDP_CUDA(cudaMemcpyAsync(arena_[t] + int64_t(merge_base_) * slot_elems_,
+                                arena_[t] + int64_t(recv_base_ + par * nrecv_) * slot_elems_, bytes,
+                                cudaMemcpyDeviceToDevice, st));
+    rec.merge_end = take_event();
+    DWDP_CUDA(cudaEventRecord(rec.merge_end, st));
+  }
+  moe_forward(l, par, x, T, y, residual ? x : nullptr, st);
+  DWDP_CUDA(cudaEventRecord(moe_done_[par], st));
+  moe_done_recorded_[par] = true;
+  DWDP_CUDA(cudaEventRecord(rec.moe_end, st));
+  recs_.push_back(rec);
+}
+
+void Ctx::stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t st) {
+  for (int l = 0; l < L_; ++l) {
+    const int64_t g = cursor_++;
+    layer_forward(g, l == 0 ? x : y, T, y, true, st);
+  }
+}
+
+void Ctx::route(int layer, const uint16_t* x, int64_t T, int32_t* idx, float* wts,
+                int32_t* counts, int32_t* row_of, int64_t* rows, cudaStream_t st) {
+  DeviceGuard dg(cfg.device);
+  require(T >= 1 && T <= max_tokens_, "route: T out of range");
+  const int wl = layer % WL_;
+  RouterCfg rc{E_, k_, cfg.scoring, cfg.n_group, cfg.topk_group, cfg.norm_topk, cfg.routed_scale};
+  launch_router_logits(x, router_w_ + size_t(wl) * E_ * h_, logits_, T, E_, h_, st);
+  launch_topk(logits_, bias_ + size_t(wl) * E_, idx_, wts_, T, rc, st);
+  launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, meta_, xperm_,
+                 scratch_, st);
+  launches += 5;
+  const size_t tk = size_t(T) * size_t(k_);
+  if (idx) DWDP_CUDA(cudaMemcpyAsync(idx, idx_, tk * 4, cudaMemcpyDeviceToDevice, st));
+  if (wts) DWDP_CUDA(cudaMemcpyAsync(wts, wts_, tk * 4, cudaMemcpyDeviceToDevice, st));
+  if (counts) DWDP_CUDA(cudaMemcpyAsync(counts, counts_, size_t(E_) * 4, cudaMemcpyDeviceToDevice, st));
+  if (row_of) DWDP_CUDA(cudaMemcpyAsync(row_of, row_of_, tk * 4, cudaMemcpyDeviceToDevice, st));
+  int32_t meta[4];
+  DWDP_CUDA(cudaMemcpyAsync(meta, meta_, 16, cudaMemcpyDeviceToHost, st));
+  DWDP_CUDA(cudaStreamSynchronize(st));
+  if (rows) *rows = meta[2];
+}
+
+size_t Ctx::drain_records(dwdp_layer_record* out, size_t cap) {
+  DeviceGuard dg(cfg.device);
+  size_t n = 0;
+  while (!recs_.empty() && n < cap) {
+    LayerRec r = recs_.front();
+    recs_.pop_front();
+    DWDP_CUDA(cudaEventSynchronize(r.moe_end));
+    float wait = 0, moe = 0, merge = 0, pf = 0;
+    DWDP_CUDA(cudaEventElapsedTime(&wait, r.gate0, r.gate1));
+    DWDP_CUDA(cudaEventElapsedTime(&moe, r.merge_end ? r.merge_end : r.gate1, r.moe_end));
+    if (r.merge_end) DWDP_CUDA(cudaEventElapsedTime(&merge, r.gate1, r.merge_end));
+    double pbytes = 0;
+    if (r.plan >= 0) {
+      const Plan& p = plans_[size_t(r.plan)];
+      DWDP_CUDA(cudaEventSynchronize(p.done));
+      DWDP_CUDA(cudaEventElapsedTime(&pf, p.start, p.done));
+      pbytes = p.bytes;
+    }
+    if (out) out[n] = {r.g, r.tokens, double(wait) * 1e6, double(moe) * 1e6, double(pf) * 1e6, pbytes,
+                       double(merge) * 1e6};
+    ++n;
+    for (cudaEvent_t e : {r.gate0, r.gate1, r.moe_end, r.merge_end})
+      if (e) free_events_.push_back(e);
+  }
+  return n;
+}
+
+// ===================================================================== //
+// single-group GEMM for kernel tests
+
+void Ctx::gemm_bf16(const uint16_t* A, const uint16_t* B, uint16_t* D, int64_t M, int64_t N,
+                    int64_t K, cudaStream_t st) {
+  DeviceGuard dg(cfg.device);
+  require(M >= 1 && N % 256 == 0 && K % 64 == 0 && N > 0 && K > 0, "gemm: need N%256==0, K%64==0");
+  const int64_t mb = (M + 127) / 128;
+  int32_t* tabs = static_cast<int32_t*>(dalloc(size_t(mb + 8) * 4, nullptr));
+  DWDP_CUDA(cudaMemsetAsync(tabs, 0, size_t(mb + 8) * 4, st));
+  const int32_t meta[4] = {int32_t(mb), int32_t(mb), int32_t(mb * 128), 0};
+  DWDP_CUDA(cudaMemcpyAsync(tabs + mb + 4, meta, 16, cudaMemcpyHostToDevice, st));
+  const CUtensorMap ta = make_tmap_bf16(A, M, K, 128);
+  const CUtensorMap tb = make_tmap_bf16(B, N, K, 256);
+  GemmArgs a{int(K), int(N), int(N), 1, tabs, tabs + mb, tabs + mb + 4, D, N, M, 0};
+  launch_grouped_gemm(false, ta, ta, tb, tb, a, int(mb * (N / 256)), st);
+  ++launches;
+  DWDP_CUDA(cudaGetLastError());
+  DWDP_CUDA(cudaStreamSynchronize(st));
+  cudaFree(tabs);
+}
+
+}  // namespace dwdp

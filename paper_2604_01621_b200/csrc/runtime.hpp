@@ -1,0 +1,137 @@
+// Per-GPU DWDP runtime: split-weight arenas, prefetch engine, layer loop.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <deque>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/dwdp.h"
+#include "kernels.hpp"
+#include "plan.hpp"
+
+namespace dwdp {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define DWDP_CUDA(x)                                                                         \
+  do {                                                                                       \
+    const cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                                   \
+      throw ::dwdp::CudaError(std::string(#x) + ": " + cudaGetErrorString(e_) + " at " +     \
+                              __FILE__ + ":" + std::to_string(__LINE__));                     \
+  } while (0)
+
+// One fetched shard: a run of `count` consecutive expert slots of tensor
+// `tensor` held by `peer` (ShardRef of the reference, simcore.cpp:500-507).
+struct ShardRun {
+  int peer, tensor, count;
+  int src_slot0;  // first slot inside the peer's local region of a weight layer
+  int dst_slot0;  // first slot inside this rank's receive region
+  uint64_t param_id;
+};
+
+struct Plan {  // one issued prefetch (CopyEngineSim::Plan)
+  int64_t g = -1;
+  cudaEvent_t start = nullptr, done = nullptr;
+  double bytes = 0;
+};
+
+struct LayerRec {
+  int64_t g, tokens;
+  cudaEvent_t gate0, gate1, moe_end, merge_end;
+  int64_t plan;  // index into plans_ or -1
+};
+
+class Ctx {
+ public:
+  explicit Ctx(const dwdp_ctx_config& cfg);
+  ~Ctx();
+
+  void export_ipc(void* blob);
+  void open_peers(const void* blobs);
+  void link_local(const std::vector<Ctx*>& all);
+  void init_weights(float bias_scale);
+  void set_bias(const float* host);
+  void read_expert(int layer, int expert, int t, void* host);
+
+  int64_t prefetch_issue(int64_t g);
+  bool prefetch_done(int64_t h);
+  void prefetch_wait(int64_t h, cudaStream_t st);
+  void prefetch_times(int64_t h, int64_t* s, int64_t* e, double* bytes);
+
+  void moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint16_t* y,
+                   const uint16_t* resid, cudaStream_t st);
+  void layer_forward(int64_t g, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
+                     cudaStream_t st);
+  void stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t st);
+  void route(int layer, const uint16_t* x, int64_t T, int32_t* idx, float* wts,
+             int32_t* counts, int32_t* row_of, int64_t* rows, cudaStream_t st);
+  size_t drain_records(dwdp_layer_record* out, size_t cap);
+  std::vector<Slice> copy_plan() const { return plan_slices_; }
+  int resident_parity(int l) const { return resident_parity_.at(size_t(l)); }
+
+  void gemm_bf16(const uint16_t* A, const uint16_t* B, uint16_t* D, int64_t M, int64_t N,
+                 int64_t K, cudaStream_t st);
+
+  dwdp_ctx_config cfg;
+  uint64_t weight_bytes = 0, recv_bytes = 0, workspace_bytes = 0;
+  int64_t launches = 0;
+
+ private:
+  void* dalloc(size_t bytes, uint64_t* account);
+  void build_layout();
+  void build_copy_plan();
+  int slot_of(int layer, int parity, int expert) const;
+  void* peer_src(int peer, int t, int wl, uint64_t src_offset) const;
+  uint8_t* dst_addr(int t, int parity, const ShardRun& r, uint64_t dst_offset) const;
+
+  int E_, k_, L_, WL_, N_, rank_, c_ = 0, nrecv_ = 0;
+  int64_t h_, f_;
+  bool shared_;
+  Placement pl_;
+  std::vector<int> local_index_;  // expert -> index in local set, -1 if remote
+  std::vector<int> recv_index_;   // expert -> slot in receive region, -1 if local
+  // arenas: 0 gate [slots][f][h], 1 up [slots][f][h], 2 down [slots][h][f]
+  uint16_t* arena_[3] = {nullptr, nullptr, nullptr};
+  int64_t slot_elems_ = 0;
+  int nslots_ = 0, shared_base_ = 0, recv_base_ = 0, merge_base_ = 0;
+  std::vector<void*> peer_arena_[3];   // per peer rank (nullptr for self)
+  std::vector<void*> ipc_opened_;
+  uint16_t* router_w_ = nullptr;       // [WL][E][h]
+  float* bias_ = nullptr;              // [WL][E]
+  int32_t* slot_tab_ = nullptr;        // [L][2][E+1]
+  // workspace
+  int64_t max_tokens_ = 0, max_rows_ = 0, max_mb_ = 0;
+  float* logits_ = nullptr;
+  int32_t *idx_ = nullptr, *counts_ = nullptr, *row_of_ = nullptr, *mblock_ = nullptr,
+          *meta_ = nullptr, *scratch_ = nullptr;
+  float* wts_ = nullptr;
+  uint16_t *xperm_ = nullptr, *hbuf_ = nullptr;
+  CUtensorMap tm_gate_, tm_up_, tm_down_, tm_xperm_, tm_h_;
+  // prefetch engine
+  std::vector<ShardRun> runs_;
+  std::vector<Slice> plan_slices_;
+  double plan_bytes_ = 0;
+  cudaStream_t copy_st_ = nullptr;
+  cudaEvent_t epoch_ = nullptr;
+  cudaEvent_t moe_done_[2] = {nullptr, nullptr};
+  bool moe_done_recorded_[2] = {false, false};
+  std::vector<Plan> plans_;
+  std::vector<int64_t> plan_of_g_;  // global layer -> plan index (-1 preloaded)
+  PullItem* pull_items_ = nullptr;  // device [WL][2][n_slices]
+  int64_t cursor_ = 0;              // next global layer of stack_forward
+  std::vector<int> resident_parity_;
+  std::deque<LayerRec> recs_;
+  std::vector<cudaEvent_t> free_events_;
+  cudaEvent_t take_event();
+  int num_sms_ = 148;
+};
+
+}  // namespace dwdp

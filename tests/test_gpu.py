@@ -1,0 +1,226 @@
+"""GPU parity tests: the sm_100a path through the C-ABI against the oracle.
+
+Bar: routing indices, weights, expert counts and permutation rows bit-exact;
+layer outputs within normwise relative error 1e-2 of the oracle's fp32
+(bf16 storage of H, O and y), GEMM within 1e-2 of a torch fp32 reference.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2604_01621_b200 as D
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2  # normwise relative error vs the oracle's fp32 (stated in BASELINE.md §3)
+
+
+def _bf16_np(t):
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _scale(n):
+    return float(np.float32(1.0) / np.sqrt(np.float32(n)))
+
+
+@pytest.fixture(scope="module")
+def dev():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    assert torch.cuda.get_device_capability(0) == (10, 0), "sm_100 required"
+    return torch.device("cuda:0")
+
+
+def make_x(T, h, seed, dev):
+    x = torch.empty((T, h), dtype=torch.bfloat16, device=dev)
+    if T:
+        D.fill_bf16(x, seed, 1.0)
+    torch.cuda.synchronize()
+    return x
+
+
+def oracle_cfg(c: D.DwdpConfig):
+    return O.MoeConfig(c.hidden, c.num_experts, c.top_k, c.ffn, c.shared_ffn, c.scoring,
+                       c.n_group, c.topk_group, c.norm_topk, c.routed_scale)
+
+
+CONFIGS = {
+    "tiny": D.DwdpConfig.tiny(),  # BASELINE config 1 layer (softmax top-2, E16, h512)
+    "tiny_shared": D.DwdpConfig.tiny(shared_ffn=1024),
+    "mid_sigmoid": D.DwdpConfig(num_layers=1, num_experts=64, hidden=1024, ffn=256, shared_ffn=256,
+                                top_k=6, n_group=8, topk_group=4, max_tokens=2048),
+    "r1": D.DwdpConfig(num_layers=1, max_tokens=512),  # BASELINE config 2 shapes
+}
+
+
+@pytest.fixture(scope="module")
+def ctxs(dev):
+    out = {}
+    for name, cfg in CONFIGS.items():
+        c = D.DwdpContext(cfg)
+        c.init_weights()
+        if cfg.scoring == 1:
+            c.set_bias((np.arange(cfg.num_experts) % 7 - 3).astype(np.float32) * 0.01)
+        out[name] = c
+    yield out
+    for c in out.values():
+        c.close()
+
+
+def _bias(cfg):
+    if cfg.scoring != 1:
+        return None
+    return (np.arange(cfg.num_experts) % 7 - 3).astype(np.float32) * 0.01
+
+
+# ---------------------------------------------------------------- kernels
+
+def test_fill_matches_oracle(dev, orc):
+    t = torch.empty(100_003, dtype=torch.bfloat16, device=dev)
+    D.fill_bf16(t, 12345, 0.37)
+    torch.cuda.synchronize()
+    assert (_bf16_np(t) == orc.fill_bf16(12345, t.numel(), 0.37)).all()
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 512, 1024), (1, 256, 7168),
+                                   (2048, 7168, 2048), (1000, 4096, 7168)])
+def test_gemm_vs_torch(dev, M, N, K):
+    g = torch.Generator(device=dev).manual_seed(M + N + K)
+    A = torch.randn((M, K), device=dev, generator=g).to(torch.bfloat16)
+    B = (torch.randn((N, K), device=dev, generator=g) / K ** 0.5).to(torch.bfloat16)
+    Dm = D.gemm_bf16(A, B)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().T
+    assert _rel(Dm.float().cpu().numpy(), ref.cpu().numpy()) < TOL
+
+
+# ---------------------------------------------------------------- routing
+
+@pytest.mark.parametrize("name,T", [("tiny", 1), ("tiny", 7), ("tiny", 64), ("tiny", 1000),
+                                    ("mid_sigmoid", 1), ("mid_sigmoid", 333),
+                                    ("r1", 1), ("r1", 37), ("r1", 256)])
+def test_route_bit_exact(dev, ctxs, orc, name, T):
+    cfg = CONFIGS[name]
+    ctx = ctxs[name]
+    x = make_x(T, cfg.hidden, 99 + T, dev)
+    idx, wts, counts, row_of, rows = ctx.route(0, x)
+    torch.cuda.synchronize()
+    wr = orc.fill_bf16(orc.tensor_seed(cfg.weight_seed, 0, cfg.num_experts + 1, 0),
+                       cfg.num_experts * cfg.hidden, _scale(cfg.hidden))
+    _, oidx, owts = orc.route(oracle_cfg(cfg), _bf16_np(x).reshape(-1), T, wr, _bias(cfg))
+    assert (idx.cpu().numpy() == oidx).all()
+    assert (wts.cpu().numpy().view(np.uint32) == owts.view(np.uint32)).all()  # bitwise
+    total, ocounts, orow = orc.permute(oidx, cfg.num_experts, 128)
+    assert (counts.cpu().numpy() == ocounts).all()
+    assert (row_of.cpu().numpy() == orow).all()
+    assert rows == total
+
+
+# ---------------------------------------------------------------- layer forward
+
+@pytest.mark.parametrize("name,T", [("tiny", 1), ("tiny", 64), ("tiny", 1000), ("tiny_shared", 129),
+                                    ("mid_sigmoid", 200), ("r1", 16)])
+def test_moe_forward_vs_oracle(dev, ctxs, orc, name, T):
+    cfg = CONFIGS[name]
+    ctx = ctxs[name]
+    x = make_x(T, cfg.hidden, 7 + T, dev)
+    y = ctx.moe_forward(0, x)
+    torch.cuda.synchronize()
+    yo, _, _ = orc.moe_forward_seeded(oracle_cfg(cfg), cfg.weight_seed, 0,
+                                      _bf16_np(x).reshape(-1), T, _bias(cfg))
+    err = _rel(y.float().cpu().numpy(), yo)
+    assert err < TOL, err
+
+
+def test_empty_batch_is_a_noop(dev, ctxs):
+    x = torch.empty((0, 512), dtype=torch.bfloat16, device=dev)
+    ctxs["tiny"].moe_forward(0, x)
+    torch.cuda.synchronize()
+
+
+def test_stack_forward_residual(dev, orc):
+    cfg = D.DwdpConfig.tiny(num_layers=2, max_tokens=256)
+    ctx = D.DwdpContext(cfg)
+    ctx.init_weights()
+    x = make_x(50, cfg.hidden, 3, dev)
+    y = ctx.stack_forward(x)
+    torch.cuda.synchronize()
+    xf = _bf16_np(x).reshape(-1)
+    h = O.bf16_to_f32(xf).reshape(50, -1)
+    for layer in range(2):
+        yo, _, _ = orc.moe_forward_seeded(oracle_cfg(cfg), cfg.weight_seed, layer,
+                                          O.bf16_round(h).reshape(-1), 50, None)
+        h = h + yo
+    assert _rel(y.float().cpu().numpy(), h) < TOL
+    recs = ctx.records()
+    assert [r["global_layer"] for r in recs] == [0, 1]
+    assert ctx.launch_count() > 0
+    ctx.close()
+
+
+# ---------------------------------------------------------------- DWDP on one GPU
+
+MID = dict(num_layers=3, num_experts=64, hidden=1024, ffn=256, shared_ffn=256, top_k=6,
+           n_group=8, topk_group=4, max_tokens=512, weight_layers=3)
+
+
+@pytest.mark.parametrize("engine,tdm,slice_size,merge", [(D.ENGINE_COPY, 1, 1 << 20, 1),
+                                                          (D.ENGINE_PULL, 1, 1 << 20, 1),
+                                                          (D.ENGINE_COPY, 0, 1 << 20, 1),
+                                                          (D.ENGINE_COPY, 1, 300_000, 0)])
+def test_dwdp_group_of_two_matches_all_local(dev, engine, tdm, slice_size, merge):
+    """Two DWDP ranks (one process, one GPU) pulling from each other give the
+    same layer outputs, bit for bit, as the all-local model (same seed)."""
+    full = D.DwdpContext(D.DwdpConfig(**MID))
+    full.init_weights()
+    ranks = [D.DwdpContext(D.DwdpConfig(**MID, rank=r, group_size=2, engine=engine, tdm=tdm,
+                                        slice_size=slice_size, merge_elim=merge))
+             for r in range(2)]
+    for c in ranks:
+        c.init_weights()
+    D.DwdpContext.link_local(ranks)
+    xs = [make_x(100 + 37 * r, MID["hidden"], 50 + r, dev) for r in range(2)]
+    for g in range(5):  # crosses an iteration boundary (L = 3)
+        for r in range(2):
+            y = ranks[r].layer_forward(g, xs[r], residual=False)
+            yf = full.moe_forward(g % 3, xs[r])
+            torch.cuda.synchronize()
+            assert torch.equal(y, yf), (g, r)
+    # received experts are byte-identical to the owner's copy
+    plan = D.build_placement(64, 2)
+    for r in range(2):
+        for e, src in plan.fetch_lists[r][:4]:
+            for t in range(3):
+                layer = 4 % 3
+                assert (ranks[r].read_expert(layer, e, t) == ranks[src].read_expert(layer, e, t)).all()
+    recs = ranks[0].records()
+    assert len(recs) == 5
+    pf = recs[1]["prefetch_bytes"]
+    assert pf == 32 * 3 * MID["hidden"] * MID["ffn"] * 2  # (E - c) * expert_shard_bytes
+    assert all(r["gate_wait_ns"] >= 0 for r in recs)
+    for c in ranks + [full]:
+        c.close()
+
+
+def test_prefetch_handles(dev):
+    ranks = [D.DwdpContext(D.DwdpConfig(**MID, rank=r, group_size=2)) for r in range(2)]
+    for c in ranks:
+        c.init_weights()
+    D.DwdpContext.link_local(ranks)
+    h = ranks[0].prefetch_issue(0)
+    assert h >= 0
+    ranks[0].prefetch_wait(h)
+    torch.cuda.synchronize()
+    assert ranks[0].prefetch_query(h)
+    s, e, b = ranks[0].prefetch_times(h)
+    assert 0 <= s <= e and b == 32 * 3 * MID["hidden"] * MID["ffn"] * 2
+    with pytest.raises(D.InvariantViolation):
+        ranks[0].prefetch_issue(0)  # double issue (simcore.cpp:624)
+    plan = ranks[0].copy_plan()
+    assert sum(s.length for s in plan) == b
+    for c in ranks:
+        c.close()
