@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""DWDP MoE-stack throughput on B200 (BASELINE.json metric: output tokens/s/GPU
+at 1/2/4/8 B200 vs DEP; exposed prefetch ms/layer).
+
+A step = one forward pass of the 8-layer DeepSeek-R1-shaped MoE stack
+(h 7168, E 256 top-8, f 2048, 1 shared expert, bf16) over one rank's batch.
+Batches come from the reference workload generator (sample_batches,
+src/workload.cpp:137-173): ISL 8K with seq-len CV 0.2, MNT 32768 tokens/rank.
+N = 1: config 2 (all 256 experts local; the 8 layers alias one 22.5 GB
+weight set because 8 x 22.5 GB does not fit in 180 GB). N > 1: config 3
+(DWDP: 256/N owned experts per layer per GPU, the rest pulled from peers one
+layer ahead over NVLink, no collective, no barrier on the layer path).
+
+    python bench.py [--gpus N --steps K --warmup W]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+    python bench.py --impl reference      # CPU reference arm (oracle port)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "output tokens/sec/GPU at 1/2/4/8 B200 vs DEP; exposed prefetch ms/layer"
+R1 = dict(h=7168, E=256, k=8, f=2048, fs=2048)
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+         "source": "fallback (B200_PROFILING.md)"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update({k: m[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in m})
+        p["source"] = "measured (MEASURED_PEAKS.json)"
+    except (OSError, ValueError):
+        pass
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 9
+                          for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_baseline(tokens: int, layers: int):
+    """Oracle port on this host's cores (bounded sample), rank 0 / N = 1 only."""
+    from oracle import cpu_moe
+    tps, cores, secs = cpu_moe.time_layer(tokens, layers, steps=1, warmup=1)
+    return {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "sample": f"{tokens} tokens through the {layers}-layer R1 MoE stack "
+                      f"(fp32 math, bf16 resident weights, {secs:.1f} s/step)"}
+
+
+def reference_arm(args):
+    """--impl reference: the CPU path of the hot path (oracle/ C restatement of the
+    MoE layer; the reference itself has no numerical MoE) on all host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import cpu_moe, oracle as O
+    tokens = args.ref_tokens
+    layer = cpu_moe.CpuMoeLayer(cpu_moe.r1_config(), 2604_01621)
+    x = O.oracle().fill_bf16(0xC0FFEE, tokens * R1["h"], 1.0)
+    layer.prepare(x, tokens)
+    for _ in range(args.warmup):
+        layer.forward(x, tokens)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        h = x
+        for _ in range(args.layers):
+            y, _, _ = layer.forward(h, tokens)
+            h = O.bf16_round(O.bf16_to_f32(h).reshape(tokens, -1) + y).reshape(-1)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = tokens / dt
+    sim = None
+    r = O.ref()
+    if r is not None:  # the reference's own CPU code on this path: its simulator
+        t1 = time.perf_counter()
+        r.simulate(True, args.layers, 7168, 256, 8, 2048, 2048, 2.0, 1382.3e12, 6552.6e9, 900e9,
+                   max(args.gpus, 2), 6, 2, 2, 8192.0, 1.0, 0.2 * 8192, args.tokens,
+                   args.tokens // 8192, 7)
+        sim = {"simulate_dwdp_wall_s": time.perf_counter() - t1}
+    cores = os.cpu_count()
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "R1 MoE stack (CPU oracle port, bounded sample)",
+                       "layers": args.layers, "tokens_per_step": tokens},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "sample": f"{tokens} tokens/step x {args.layers} layers"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "reference_simulator": sim}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dwdp", choices=["dwdp", "reference"])
+    ap.add_argument("--tokens", type=int, default=32768, help="MNT tokens per rank per step")
+    ap.add_argument("--cv", type=float, default=0.2, help="sequence-length CV")
+    ap.add_argument("--layers", type=int, default=8)
+    ap.add_argument("--engine", default="copy", choices=["copy", "pull"])
+    ap.add_argument("--slice-size", type=int, default=64 << 20)
+    ap.add_argument("--no-tdm", action="store_true")
+    ap.add_argument("--merged", action="store_true", help="merge_elim off (D2D merge baseline)")
+    ap.add_argument("--pull-ctas", type=int, default=16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=16)
+    ap.add_argument("--ref-tokens", type=int, default=16)
+    ap.add_argument("--profile", action="store_true", help="1 layer, for ncu captures")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_01621_b200 as D
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def allmax(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    layers = 1 if args.profile else args.layers
+    model = D.r1_model(layers)
+    iters = args.warmup + args.steps
+    spec = D.WorkloadSpec(D.IslDist.from_cv(8192, args.cv), args.tokens,
+                          max(1, args.tokens // 8192), 0.0, 7)
+    batches = D.sample_batches(spec, model, world, iters, with_routing=False)
+    toks = [[b.tokens[r] for r in range(world)] for b in batches]
+
+    cfg = D.DwdpConfig(num_layers=layers, rank=rank, group_size=world, device=local,
+                       engine=D.ENGINE_PULL if args.engine == "pull" else D.ENGINE_COPY,
+                       tdm=0 if args.no_tdm else 1, slice_size=args.slice_size,
+                       merge_elim=0 if args.merged else 1, pull_ctas=args.pull_ctas,
+                       weight_layers=layers if world > 1 else 1, kernel_timing=1,
+                       max_tokens=args.tokens)
+    ctx = D.DwdpContext(cfg)
+    ctx.init_weights()
+    if world > 1:
+        blobs = [None] * world
+        dist.all_gather_object(blobs, ctx.export_ipc())
+        ctx.open_peers(b"".join(blobs))
+    torch.cuda.synchronize()
+    barrier()
+
+    T_max = max(max(t) for t in toks)
+    x = torch.empty((T_max, R1["h"]), dtype=torch.bfloat16, device=dev)
+    D.fill_bf16(x, 0xC0FFEE + rank, 1.0)
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+
+    for it in range(args.warmup):
+        T = toks[it][rank]
+        ctx.stack_forward(x[:T], y[:T])
+    torch.cuda.synchronize()
+    ctx.records()
+    n0 = ctx.launch_count()
+
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for it in range(args.warmup, iters):
+            T = toks[it][rank]
+            ctx.stack_forward(x[:T], y[:T])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = ctx.launch_count() - n0
+    ms_local = ev0.elapsed_time(ev1)
+    ms = allmax(ms_local)
+    recs = ctx.records()
+    total_tokens = sum(sum(toks[it]) for it in range(args.warmup, iters))
+    value = total_tokens / (ms / 1e3)
+
+    # ---- per-kernel split and roofline of the dominant kernel (grouped GEMM1)
+    k, h, f = R1["k"], R1["h"], R1["f"]
+    g1_ns = sum(r["gemm1_ns"] for r in recs)
+    g1_flops = sum(2.0 * (r["tokens"] * k + r["tokens"]) * 2 * f * h for r in recs)
+    g2_ns = sum(r["gemm2_ns"] for r in recs)
+    g2_flops = sum(2.0 * (r["tokens"] * k + r["tokens"]) * f * h for r in recs)
+    pk = peaks()
+    achieved = g1_flops / (g1_ns * 1e-9) / 1e12 if g1_ns else 0.0
+    split = {key: sum(r[key] for r in recs) / 1e6 / max(len(recs), 1)
+             for key in ("router_ns", "permute_ns", "gemm1_ns", "gemm2_ns", "combine_ns",
+                         "moe_ns", "gate_wait_ns", "prefetch_ns")}
+    exposed_ms = split["gate_wait_ns"]
+    pf_bytes = sum(r["prefetch_bytes"] for r in recs)
+    pf_ns = sum(r["prefetch_ns"] for r in recs)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "gemm1_dram.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.empty((T_max, h), dtype=torch.bfloat16, pin_memory=True)
+        hy = torch.empty((T_max, h), dtype=torch.bfloat16, pin_memory=True)
+        hx.copy_(x.cpu())
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h2d = d2h = 0
+        e0.record(stream)
+        for it in range(args.warmup, iters):
+            T = toks[it][rank]
+            x[:T].copy_(hx[:T], non_blocking=True)
+            ctx.stack_forward(x[:T], y[:T])
+            hy[:T].copy_(y[:T], non_blocking=True)
+            h2d += T * h * 2
+            d2h += T * h * 2
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = allmax(e0.elapsed_time(e1))
+        e2e = {"value": total_tokens / (ems / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+               "api": "dwdp_stack_forward (C-ABI) with pinned host input/output"}
+        ctx.records()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args.cpu_tokens, layers)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "error": str(e)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (counter-hash random-init weights and activations)",
+            "config": {"workload": ("R1 MoE stack, config 2 (all experts local)" if world == 1
+                                    else "R1 MoE stack, config 3 (DWDP)"),
+                       "layers": layers, "hidden": h, "experts": 256, "top_k": k, "ffn": f,
+                       "shared_experts": 1, "mnt_tokens_per_rank": args.tokens,
+                       "isl": 8192, "seq_len_cv": args.cv,
+                       "tokens_per_step_rank0": [toks[it][0] for it in range(args.warmup, iters)],
+                       "weights": ("one 22.5 GB set aliased by all layers (N=1)" if world == 1
+                                   else f"{256 // world} owned experts/layer/GPU, {layers} layers"),
+                       "prefetch_engine": args.engine if world > 1 else None,
+                       "slice_size": args.slice_size if world > 1 else None,
+                       "l2": "inputs larger than L2: 22.5 GB of expert weights per layer",
+                       "parallelism": f"dwdp{world}"},
+            "tokens_per_s_per_gpu": value / world,
+            "exposed_prefetch_ms_per_layer": exposed_ms,
+            "prefetch": ({"bytes_per_layer": pf_bytes / max(len(recs), 1),
+                          "gbs": pf_bytes / pf_ns if pf_ns else None,
+                          "ms_per_layer": split["prefetch_ns"]} if world > 1 else None),
+            "kernel_ms_per_layer": {k2.replace("_ns", ""): v for k2, v in split.items()},
+            "roofline": {"bound": "tensor", "kernel": "grouped GEMM1 (gate/up + SwiGLU, tcgen05)",
+                         "achieved": achieved, "peak": pk["bf16_tflops_sustained"],
+                         "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops_sustained"],
+                         "peak_source": pk["source"] + ", sustained bf16",
+                         "flops_per_launch": g1_flops / max(len(recs), 1),
+                         "gemm2_tflops": g2_flops / (g2_ns * 1e-9) / 1e12 if g2_ns else None,
+                         "traffic": traffic},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    barrier()
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

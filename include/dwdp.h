@@ -238,7 +238,7 @@ typedef struct {
   /* synthetic weights */
   uint64_t weight_seed;
   int32_t weight_layers;  /* distinct weight sets; layer l uses l % this   */
-  int32_t reserved;
+  int32_t kernel_timing;  /* 1: CUDA events between the layer's kernels    */
   int64_t max_tokens;     /* workspace sizing (tokens per forward)         */
 } dwdp_ctx_config;
 
@@ -319,6 +319,13 @@ typedef struct {
   double prefetch_ns;    /* P2PCopy of this layer's plan              */
   double prefetch_bytes;
   double merge_ns;       /* D2DCopy (merge_elim == 0 only)            */
+  /* per-kernel split of moe_ns (kernel_timing == 1, else 0):         */
+  double router_ns;      /* router logits + scoring/top-k             */
+  double permute_ns;     /* count/scan/scatter+gather                 */
+  double gemm1_ns;       /* grouped GEMM gate/up + SwiGLU             */
+  double gemm2_ns;       /* grouped GEMM down                         */
+  double combine_ns;     /* weighted combine (+ shared, residual)     */
+  int64_t routed_rows;   /* padded expert-major rows of the layer     */
 } dwdp_layer_record;
 /* Drain completed layer records (synchronises the context's streams). */
 int dwdp_ctx_records(dwdp_ctx* ctx, dwdp_layer_record* out, size_t* n_inout);

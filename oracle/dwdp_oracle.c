@@ -388,8 +388,24 @@ static inline float hash_val(uint64_t seed, int64_t i, float scale) {
   return v * scale;
 }
 
+typedef struct {
+  uint64_t seed;
+  int64_t n;
+  float scale;
+  uint16_t* out;
+} fill_arg;
+
+static void fill_chunk(void* p, int64_t c) {
+  const fill_arg* a = (const fill_arg*)p;
+  const int64_t lo = c << 20, hi = lo + (1 << 20) < a->n ? lo + (1 << 20) : a->n;
+  for (int64_t i = lo; i < hi; ++i) a->out[i] = f32_to_bf16(hash_val(a->seed, i, a->scale));
+}
+
+static void parallel_for(int64_t n, int nthreads, void (*fn)(void*, int64_t), void* arg);
+
 void oracle_fill_bf16(uint64_t seed, int64_t n, float scale, uint16_t* out) {
-  for (int64_t i = 0; i < n; ++i) out[i] = f32_to_bf16(hash_val(seed, i, scale));
+  fill_arg a = {seed, n, scale, out};
+  parallel_for((n + (1 << 20) - 1) >> 20, 0, fill_chunk, &a);
 }
 
 /* ---- tiny parallel-for ------------------------------------------------ */
@@ -577,6 +593,30 @@ static inline float dotf(const float* a, const float* b, int64_t n) {
 
 static inline float siluf(float g) { return g / (1.0f + expf(-g)); }
 
+static inline float dot_bf16(const float* a, const uint16_t* w, int64_t n) {
+  float acc[16] = {0};
+  int64_t i = 0;
+  for (; i + 16 <= n; i += 16)
+    for (int j = 0; j < 16; ++j) acc[j] += a[i + j] * bf16_to_f32(w[i + j]);
+  float s = 0.0f;
+  for (int j = 0; j < 16; ++j) s += acc[j];
+  for (; i < n; ++i) s += a[i] * bf16_to_f32(w[i]);
+  return s;
+}
+
+static void ffn_rows_bf16(const uint16_t* gate, const uint16_t* up, const uint16_t* down,
+                          int64_t h, int64_t f, const float* const* xr, const float* scale,
+                          float* const* yr, int n, float* hbuf) {
+  /* weight rows outer, token rows inner: each weight row is streamed once */
+  for (int64_t j = 0; j < f; ++j)
+    for (int r = 0; r < n; ++r)
+      hbuf[(int64_t)r * f + j] =
+          siluf(dot_bf16(xr[r], gate + j * h, h)) * dot_bf16(xr[r], up + j * h, h);
+  for (int64_t i = 0; i < h; ++i)
+    for (int r = 0; r < n; ++r)
+      yr[r][i] += scale[r] * dot_bf16(hbuf + (int64_t)r * f, down + i * f, f);
+}
+
 /* y_rows[r] += scale[r] * FFN(x_rows[r]) for n rows of one expert. */
 static void ffn_rows(const float* gate, const float* up, const float* down,
                      int64_t h, int64_t f, const float* const* xr,
@@ -601,6 +641,7 @@ typedef struct {
   const float* wts;
   /* explicit weights (NULL for seeded) */
   const float *wg, *wu, *wd, *sg, *su, *sd;
+  const uint16_t *const *bg, *const *bu, *const *bd; /* resident bf16 weights */
   float* part; /* [E+1][T][h] partial outputs when needed */
   int64_t* pairs_of; /* per expert: list of (t, j) pair ids; CSR */
   int64_t* pair_start;
@@ -641,15 +682,16 @@ static void expert_job(void* p, int64_t e64) {
   const int64_t f = e < E ? a->cfg->ffn : a->cfg->shared_ffn;
   const int64_t n = e < E ? a->pair_start[e + 1] - a->pair_start[e] : a->T;
   if (n == 0) return;
-  float* g = malloc(sizeof(float) * (size_t)(f * h));
-  float* u = malloc(sizeof(float) * (size_t)(f * h));
-  float* d = malloc(sizeof(float) * (size_t)(h * f));
-  float* hb = malloc(sizeof(float) * (size_t)f);
+  const int resident = a->bg != NULL;
+  float* g = resident ? NULL : malloc(sizeof(float) * (size_t)(f * h));
+  float* u = resident ? NULL : malloc(sizeof(float) * (size_t)(f * h));
+  float* d = resident ? NULL : malloc(sizeof(float) * (size_t)(h * f));
+  float* hb = malloc(sizeof(float) * (size_t)(f * n));
   float* out = calloc((size_t)(n * h), sizeof(float));
   const float** xr = malloc(sizeof(float*) * (size_t)n);
   float** yr = malloc(sizeof(float*) * (size_t)n);
   float* sc = malloc(sizeof(float) * (size_t)n);
-  load_expert(a, e, f, g, u, d);
+  if (!resident) load_expert(a, e, f, g, u, d);
   for (int64_t r = 0; r < n; ++r) {
     const int64_t pid = e < E ? a->pairs_of[a->pair_start[e] + r] : r * a->cfg->top_k;
     const int64_t t = pid / a->cfg->top_k;
@@ -657,7 +699,10 @@ static void expert_job(void* p, int64_t e64) {
     yr[r] = out + r * h;
     sc[r] = e < E ? a->wts[pid] : 1.0f;
   }
-  ffn_rows(g, u, d, h, f, xr, sc, yr, (int)n, hb);
+  if (resident)
+    ffn_rows_bf16(a->bg[e], a->bu[e], a->bd[e], h, f, xr, sc, yr, (int)n, hb);
+  else
+    ffn_rows(g, u, d, h, f, xr, sc, yr, (int)n, hb);
   /* scatter into the per-pair partial buffer (deterministic reduction later) */
   for (int64_t r = 0; r < n; ++r) {
     const int64_t pid = e < E ? a->pairs_of[a->pair_start[e] + r] : -1 - (r);
@@ -680,8 +725,9 @@ static void moe_forward_common(const oracle_moe_config* cfg, uint64_t base,
                                const int32_t* idx, const float* wts,
                                const float* wg, const float* wu,
                                const float* wd, const float* sg,
-                               const float* su, const float* sd, float* y,
-                               int nthreads) {
+                               const float* su, const float* sd,
+                               const uint16_t* const* bg, const uint16_t* const* bu,
+                               const uint16_t* const* bd, float* y, int nthreads) {
   const int E = cfg->num_experts, k = cfg->top_k;
   const int64_t h = cfg->hidden;
   ffn_arg a;
@@ -699,6 +745,9 @@ static void moe_forward_common(const oracle_moe_config* cfg, uint64_t base,
   a.sg = sg;
   a.su = su;
   a.sd = sd;
+  a.bg = bg;
+  a.bu = bu;
+  a.bd = bd;
   const int64_t npart = T * k + (cfg->shared_ffn > 0 ? T : 0);
   a.part = calloc((size_t)(npart * h), sizeof(float));
   a.pair_start = calloc((size_t)E + 1, sizeof(int64_t));
@@ -737,7 +786,7 @@ void oracle_moe_forward_seeded(const oracle_moe_config* cfg, uint64_t base,
   float* xf = malloc(sizeof(float) * (size_t)(T * h + 1));
   for (int64_t i = 0; i < T * h; ++i) xf[i] = bf16_to_f32(x[i]);
   moe_forward_common(cfg, base, layer, xf, T, idx, wts, NULL, NULL, NULL, NULL,
-                     NULL, NULL, y, nthreads);
+                     NULL, NULL, NULL, NULL, NULL, y, nthreads);
   free(xf);
   free(logits);
   free(wr);
@@ -755,6 +804,25 @@ void oracle_moe_forward_explicit(const oracle_moe_config* cfg, const float* x,
   route_arg ra = {cfg, NULL, x, NULL, w_router, bias, logits, idx, wts};
   parallel_for(T, 0, route_one, &ra);
   moe_forward_common(cfg, 0, 0, x, T, idx, wts, w_gate, w_up, w_down, s_gate,
-                     s_up, s_down, y, 0);
+                     s_up, s_down, NULL, NULL, NULL, y, 0);
+  free(logits);
+}
+
+void oracle_moe_forward_bf16w(const oracle_moe_config* cfg, const uint16_t* x,
+                              int64_t T, const uint16_t* w_router,
+                              const float* bias, const uint16_t* const* gate,
+                              const uint16_t* const* up,
+                              const uint16_t* const* down, float* y,
+                              int32_t* idx, float* wts, int nthreads) {
+  const int64_t h = cfg->hidden;
+  const int E = cfg->num_experts;
+  float* logits = malloc(sizeof(float) * (size_t)(T * E + 1));
+  route_arg ra = {cfg, x, NULL, w_router, NULL, bias, logits, idx, wts};
+  parallel_for(T, nthreads, route_one, &ra);
+  float* xf = malloc(sizeof(float) * (size_t)(T * h + 1));
+  for (int64_t i = 0; i < T * h; ++i) xf[i] = bf16_to_f32(x[i]);
+  moe_forward_common(cfg, 0, 0, xf, T, idx, wts, NULL, NULL, NULL, NULL, NULL, NULL, gate, up,
+                     down, y, nthreads);
+  free(xf);
   free(logits);
 }

@@ -143,6 +143,22 @@ class _Oracle(_Api):
         L.oracle_permute.argtypes = [P, i64, i32, i32, i32, P, P]
         L.oracle_moe_forward_seeded.argtypes = [P, u64, i32, P, i64, P, P, P, P, i32]
         L.oracle_moe_forward_explicit.argtypes = [P, P, i64, P, P, P, P, P, P, P, P, P, P, P]
+        L.oracle_moe_forward_bf16w.argtypes = [P, P, i64, P, P, P, P, P, P, P, P, i32]
+
+    def moe_forward_bf16w(self, cfg: MoeConfig, x_bf16: np.ndarray, T: int,
+                          w_router_bf16: np.ndarray, bias, gate: list, up: list, down: list,
+                          nthreads: int = 0):
+        """gate/up/down: per expert (E+1 entries, shared last) uint16 arrays or None."""
+        n = cfg.num_experts + 1
+        arr = lambda L: (C.c_void_p * n)(*[None if a is None else a.ctypes.data for a in L])  # noqa: E731
+        y = np.zeros(T * cfg.hidden, np.float32)
+        idx = np.zeros(T * cfg.top_k, np.int32)
+        wts = np.zeros(T * cfg.top_k, np.float32)
+        self.lib.oracle_moe_forward_bf16w(C.byref(cfg), _ptr(x_bf16), T, _ptr(w_router_bf16),
+                                          _ptr(bias), arr(gate), arr(up), arr(down), _ptr(y),
+                                          _ptr(idx), _ptr(wts), nthreads)
+        return (y.reshape(T, cfg.hidden), idx.reshape(T, cfg.top_k),
+                wts.reshape(T, cfg.top_k))
 
     def moe_entries(self, h, f, fs, wb, ab, tokens, pairs, touched):
         out = np.zeros(4, np.float64)

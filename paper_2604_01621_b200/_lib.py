@@ -70,12 +70,14 @@ class CtxConfigC(C.Structure):
                 ("group_size", i32), ("extra_redundancy", i32), ("device", i32),
                 ("merge_elim", i32), ("tdm", i32), ("slice_size", u64), ("engine", i32),
                 ("pull_ctas", i32), ("weight_seed", u64), ("weight_layers", i32),
-                ("reserved", i32), ("max_tokens", i64)]
+                ("kernel_timing", i32), ("max_tokens", i64)]
 
 
 class LayerRecordC(C.Structure):
     _fields_ = [("global_layer", i64), ("tokens", i64), ("gate_wait_ns", f64), ("moe_ns", f64),
-                ("prefetch_ns", f64), ("prefetch_bytes", f64), ("merge_ns", f64)]
+                ("prefetch_ns", f64), ("prefetch_bytes", f64), ("merge_ns", f64),
+                ("router_ns", f64), ("permute_ns", f64), ("gemm1_ns", f64), ("gemm2_ns", f64),
+                ("combine_ns", f64), ("routed_rows", i64)]
 
 
 # name -> (restype, argtypes); every int-returning entry is a status code.

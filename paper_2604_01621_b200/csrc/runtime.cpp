@@ -138,13 +138,14 @@ Ctx::~Ctx() {
   DeviceGuard dg(cfg.device);
   cudaDeviceSynchronize();
   for (auto& r : recs_)
-    for (cudaEvent_t e : {r.gate0, r.gate1, r.moe_end, r.merge_end})
+    for (cudaEvent_t e : {r.gate0, r.gate1, r.moe_end, r.merge_end, r.k[0], r.k[1], r.k[2], r.k[3]})
       if (e) cudaEventDestroy(e);
   for (auto& p : plans_) {
     if (p.start) cudaEventDestroy(p.start);
     if (p.done) cudaEventDestroy(p.done);
   }
   for (cudaEvent_t e : free_events_) cudaEventDestroy(e);
+  if (meta_ring_) cudaFreeHost(meta_ring_);
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   void* bufs[] = {arena_[0], arena_[1], arena_[2], router_w_, bias_, slot_tab_, logits_, idx_,
                   wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_};
@@ -461,25 +462,41 @@ void Ctx::prefetch_times(int64_t h, int64_t* s, int64_t* e, double* bytes) {
 // MoE forward
 
 void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint16_t* y,
-                      const uint16_t* resid, cudaStream_t st) {
+                      const uint16_t* resid, cudaStream_t st, LayerRec* rec) {
   require(layer >= 0 && layer < L_, "moe_forward: layer out of range");
   require(T >= 0 && T <= max_tokens_, "moe_forward: T exceeds max_tokens");
   if (T == 0) return;
+  const bool timed = rec != nullptr && cfg.kernel_timing != 0;
+  auto mark = [&](int i) {
+    if (!timed) return;
+    rec->k[i] = take_event();
+    DWDP_CUDA(cudaEventRecord(rec->k[i], st));
+  };
   const int wl = layer % WL_;
   RouterCfg rc{E_, k_, cfg.scoring, cfg.n_group, cfg.topk_group, cfg.norm_topk, cfg.routed_scale};
   launch_router_logits(x, router_w_ + size_t(wl) * E_ * h_, logits_, T, E_, h_, st);
   launch_topk(logits_, bias_ + size_t(wl) * E_, idx_, wts_, T, rc, st);
+  mark(0);
   launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, meta_, xperm_,
                  scratch_, st);
+  mark(1);
   const int64_t mb_ub = (T * k_ + int64_t(E_) * 127) / 128 + 1 + (shared_ ? (T + 127) / 128 : 0);
   const CUtensorMap tm_x = shared_ ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
   const int32_t* stab = slot_tab_ + (size_t(layer) * 2 + size_t(parity)) * (E_ + 1);
   GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1};
   launch_grouped_gemm(true, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
+  mark(2);
   GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0};
   launch_grouped_gemm(false, tm_h_, tm_h_, tm_down_, tm_down_, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
+  mark(3);
   launch_combine(xperm_, row_of_, wts_, meta_, resid, y, T, k_, h_, shared_ ? 1 : 0, st);
   launches += 8;
+  if (timed) {
+    if (!meta_ring_) DWDP_CUDA(cudaHostAlloc(&meta_ring_, kMetaRing * 4 * sizeof(int32_t), 0));
+    rec->meta_slot = meta_ring_pos_;
+    meta_ring_pos_ = (meta_ring_pos_ + 1) % kMetaRing;
+    DWDP_CUDA(cudaMemcpyAsync(meta_ring_ + rec->meta_slot * 4, meta_, 16, cudaMemcpyDeviceToHost, st));
+  }
   DWDP_CUDA(cudaGetLastError());
 }
 
@@ -509,7 +526,7 @@ void Ctx::layer_forward(int64_t g, const uint16_t* x, int64_t T, uint16_t* y, bo
     rec.merge_end = take_event();
     DWDP_CUDA(cudaEventRecord(rec.merge_end, st));
   }
-  moe_forward(l, par, x, T, y, residual ? x : nullptr, st);
+  moe_forward(l, par, x, T, y, residual ? x : nullptr, st, &rec);
   DWDP_CUDA(cudaEventRecord(moe_done_[par], st));
   moe_done_recorded_[par] = true;
   DWDP_CUDA(cudaEventRecord(rec.moe_end, st));
@@ -563,10 +580,22 @@ size_t Ctx::drain_records(dwdp_layer_record* out, size_t cap) {
       DWDP_CUDA(cudaEventElapsedTime(&pf, p.start, p.done));
       pbytes = p.bytes;
     }
-    if (out) out[n] = {r.g, r.tokens, double(wait) * 1e6, double(moe) * 1e6, double(pf) * 1e6, pbytes,
-                       double(merge) * 1e6};
+    double kns[5] = {0, 0, 0, 0, 0};
+    if (r.k[0] && r.k[3]) {
+      cudaEvent_t seq[6] = {r.merge_end ? r.merge_end : r.gate1, r.k[0], r.k[1], r.k[2], r.k[3],
+                            r.moe_end};
+      for (int i = 0; i < 5; ++i) {
+        float ms = 0;
+        DWDP_CUDA(cudaEventElapsedTime(&ms, seq[i], seq[i + 1]));
+        kns[i] = double(ms) * 1e6;
+      }
+    }
+    const int64_t rows = r.meta_slot >= 0 ? meta_ring_[r.meta_slot * 4 + 2] : -1;
+    if (out)
+      out[n] = {r.g,    r.tokens, double(wait) * 1e6, double(moe) * 1e6, double(pf) * 1e6, pbytes,
+                double(merge) * 1e6, kns[0], kns[1], kns[2], kns[3], kns[4], rows};
     ++n;
-    for (cudaEvent_t e : {r.gate0, r.gate1, r.moe_end, r.merge_end})
+    for (cudaEvent_t e : {r.gate0, r.gate1, r.moe_end, r.merge_end, r.k[0], r.k[1], r.k[2], r.k[3]})
       if (e) free_events_.push_back(e);
   }
   return n;

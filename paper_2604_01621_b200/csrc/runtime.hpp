@@ -47,6 +47,8 @@ struct LayerRec {
   int64_t g, tokens;
   cudaEvent_t gate0, gate1, moe_end, merge_end;
   int64_t plan;  // index into plans_ or -1
+  cudaEvent_t k[4] = {nullptr, nullptr, nullptr, nullptr};  // after router/permute/gemm1/gemm2
+  int meta_slot = -1;                                       // pinned copy of meta[2]
 };
 
 class Ctx {
@@ -67,7 +69,7 @@ class Ctx {
   void prefetch_times(int64_t h, int64_t* s, int64_t* e, double* bytes);
 
   void moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint16_t* y,
-                   const uint16_t* resid, cudaStream_t st);
+                   const uint16_t* resid, cudaStream_t st, LayerRec* rec = nullptr);
   void layer_forward(int64_t g, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
                      cudaStream_t st);
   void stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t st);
@@ -131,6 +133,9 @@ class Ctx {
   std::deque<LayerRec> recs_;
   std::vector<cudaEvent_t> free_events_;
   cudaEvent_t take_event();
+  int32_t* meta_ring_ = nullptr;  // pinned host ring for per-layer routed rows
+  int meta_ring_pos_ = 0;
+  static constexpr int kMetaRing = 4096;
   int num_sms_ = 148;
 };
 

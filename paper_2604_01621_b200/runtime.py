@@ -41,6 +41,7 @@ class DwdpConfig:
     pull_ctas: int = 16
     weight_seed: int = 2604_01621
     weight_layers: int = 0    # 0 = num_layers
+    kernel_timing: int = 0    # CUDA events between the layer's kernels
     max_tokens: int = 32768
 
     @staticmethod
@@ -54,7 +55,7 @@ class DwdpConfig:
 
     def c(self) -> CtxConfigC:
         d = asdict(self)
-        return CtxConfigC(**{k: d[k] for k, _ in CtxConfigC._fields_ if k != "reserved"})
+        return CtxConfigC(**{k: d[k] for k, _ in CtxConfigC._fields_})
 
 
 def _ptr(t) -> int | None:
