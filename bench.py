@@ -108,9 +108,12 @@ def reference_arm(args):
     tokens = args.ref_tokens
     layer = cpu_moe.CpuMoeLayer(cpu_moe.r1_config(), 2604_01621)
     x = O.oracle().fill_bf16(0xC0FFEE, tokens * R1["h"], 1.0)
-    layer.prepare(x, tokens)
-    for _ in range(args.warmup):
-        layer.forward(x, tokens)
+    for _ in range(max(args.warmup, 1)):  # materialise every expert the stack touches
+        h = x
+        for _ in range(args.layers):
+            layer.prepare(h, tokens)
+            y, _, _ = layer.forward(h, tokens)
+            h = O.bf16_round(O.bf16_to_f32(h).reshape(tokens, -1) + y).reshape(-1)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         h = x

@@ -51,6 +51,10 @@ class CpuMoeLayer:
         self._materialise(sorted(need))
 
     def forward(self, x_bf16: np.ndarray, T: int, nthreads: int = 0):
+        _, idx, _ = self.o.route(self.cfg, x_bf16, T, self.w_router, self.bias)
+        missing = [e for e in np.unique(idx).tolist() if self.gate[e] is None]
+        if missing:
+            raise RuntimeError(f"experts {missing[:4]}... not materialised; call prepare()")
         return self.o.moe_forward_bf16w(self.cfg, x_bf16, T, self.w_router, self.bias, self.gate,
                                         self.up, self.down, nthreads)
 
@@ -68,8 +72,12 @@ def time_layer(tokens: int, layers: int, steps: int, warmup: int, seed: int = 26
     x = o.fill_bf16(0xC0FFEE, tokens * cfg.hidden, 1.0)
     layer.prepare(x, tokens)
     cores = os.cpu_count() or 1
-    for _ in range(warmup):
-        layer.forward(x, tokens)
+    for _ in range(max(warmup, 1)):  # materialises every expert the stack touches
+        h = x
+        for _ in range(layers):
+            layer.prepare(h, tokens)
+            y, _, _ = layer.forward(h, tokens)
+            h = O.bf16_round(O.bf16_to_f32(h).reshape(tokens, -1) + y).reshape(-1)
     t0 = time.perf_counter()
     for _ in range(steps):
         h = x
