@@ -160,6 +160,7 @@ def main():
     ap.add_argument("--merged", action="store_true", help="merge_elim off (D2D merge baseline)")
     ap.add_argument("--pull-ctas", type=int, default=16)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dep", action="store_true", help="skip the same-box DEP baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=16)
     ap.add_argument("--ref-tokens", type=int, default=16)
@@ -213,6 +214,10 @@ def main():
         blobs = [None] * world
         dist.all_gather_object(blobs, ctx.export_ipc())
         ctx.open_peers(b"".join(blobs))
+        if not args.no_dep:
+            ids = [D.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(ids, src=0)
+            ctx.dep_init(ids[0])
     torch.cuda.synchronize()
     barrier()
 
@@ -294,6 +299,36 @@ def main():
                "api": "dwdp_stack_forward (C-ABI) with pinned host input/output"}
         ctx.records()
 
+    # ---- DEP baseline on the same box: same kernels + NCCL all-to-alls
+    dep = None
+    if world > 1 and not args.no_dep:
+        for it in range(args.warmup):
+            T = toks[it][rank]
+            ctx.dep_stack_forward(x[:T], y[:T])
+        torch.cuda.synchronize()
+        ctx.records()
+        barrier()
+        torch.cuda.synchronize()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        for it in range(args.warmup, iters):
+            T = toks[it][rank]
+            ctx.dep_stack_forward(x[:T], y[:T])
+        d1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        dms = allmax(d0.elapsed_time(d1))
+        drecs = ctx.records()
+        dval = total_tokens / (dms / 1e3)
+        dep = {"value": dval, "unit": "tokens/s", "tokens_per_s_per_gpu": dval / world,
+               "ms_per_step": dms / args.steps,
+               "comm_ms_per_layer": sum(r["comm_ns"] for r in drecs) / 1e6 / max(len(drecs), 1),
+               "kernel_ms_per_layer": {key.replace("_ns", ""): sum(r[key] for r in drecs) / 1e6
+                                       / max(len(drecs), 1)
+                                       for key in ("router_ns", "permute_ns", "gemm1_ns",
+                                                   "gemm2_ns", "combine_ns")},
+               "dwdp_over_dep": value / dval}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -332,6 +367,7 @@ def main():
                          "flops_per_launch": g1_flops / max(len(recs), 1),
                          "gemm2_tflops": g2_flops / (g2_ns * 1e-9) / 1e12 if g2_ns else None,
                          "traffic": traffic},
+            "dep_baseline": dep,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
         }

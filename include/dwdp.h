@@ -326,11 +326,25 @@ typedef struct {
   double gemm2_ns;       /* grouped GEMM down                         */
   double combine_ns;     /* weighted combine (+ shared, residual)     */
   int64_t routed_rows;   /* padded expert-major rows of the layer     */
+  double comm_ns;        /* DEP: dispatch + combine all-to-alls (incl.
+                            the waits for the slowest rank)            */
 } dwdp_layer_record;
 /* Drain completed layer records (synchronises the context's streams). */
 int dwdp_ctx_records(dwdp_ctx* ctx, dwdp_layer_record* out, size_t* n_inout);
 /* Kernels launched by this context so far (for the bench's launch count). */
 int dwdp_ctx_launch_count(const dwdp_ctx* ctx, int64_t* n);
+
+/* ---- DEP baseline: simulate_dep (simcore.hpp:152-157, simcore.cpp:346-478)
+ * made real: the same kernels with the dispatch and combine all-to-alls
+ * (NCCL grouped send/recv after a counts all-gather). Requires
+ * group_size | num_experts (contiguous EP blocks == the DWDP placement). */
+#define DWDP_NCCL_ID_BYTES 128
+int dwdp_nccl_unique_id(void* id /*DWDP_NCCL_ID_BYTES*/);
+int dwdp_dep_init(dwdp_ctx* ctx, const void* nccl_id);
+int dwdp_dep_layer_forward(dwdp_ctx* ctx, int layer, const void* x, int64_t T,
+                           void* y, int residual, void* stream);
+int dwdp_dep_stack_forward(dwdp_ctx* ctx, const void* x, int64_t T, void* y,
+                           void* stream);
 
 /* ---- kernel-level entry points (tests / microbenchmarks) --------------- */
 /* D[M][N] = A[M][K] . B[N][K]^T, bf16 in, fp32 accumulate, bf16 out, on the

@@ -11,4 +11,4 @@ from .planning import (CopyPlan, GpuSpec, IslDist, MoeModelSpec, OpCost, Placeme
                        describe_placement, expert_shard_bytes, imbalance_cv, moe_entries,
                        prefetch_bytes, r1_model, roofline_time, route_tokens, sample_batches,
                        source_queues)
-from .runtime import DwdpConfig, DwdpContext, fill_bf16, gemm_bf16  # noqa: F401
+from .runtime import DwdpConfig, DwdpContext, fill_bf16, gemm_bf16, nccl_unique_id  # noqa: F401

@@ -77,7 +77,7 @@ class LayerRecordC(C.Structure):
     _fields_ = [("global_layer", i64), ("tokens", i64), ("gate_wait_ns", f64), ("moe_ns", f64),
                 ("prefetch_ns", f64), ("prefetch_bytes", f64), ("merge_ns", f64),
                 ("router_ns", f64), ("permute_ns", f64), ("gemm1_ns", f64), ("gemm2_ns", f64),
-                ("combine_ns", f64), ("routed_rows", i64)]
+                ("combine_ns", f64), ("routed_rows", i64), ("comm_ns", f64)]
 
 
 # name -> (restype, argtypes); every int-returning entry is a status code.
@@ -127,6 +127,10 @@ SIGNATURES = {
     "dwdp_route": (i32, [P, i32, P, i64, P, P, P, P, C.POINTER(i64), P]),
     "dwdp_ctx_records": (i32, [P, P, C.POINTER(sz)]),
     "dwdp_ctx_launch_count": (i32, [P, C.POINTER(i64)]),
+    "dwdp_nccl_unique_id": (i32, [P]),
+    "dwdp_dep_init": (i32, [P, P]),
+    "dwdp_dep_layer_forward": (i32, [P, i32, P, i64, P, i32, P]),
+    "dwdp_dep_stack_forward": (i32, [P, P, i64, P, P]),
     "dwdp_gemm_bf16": (i32, [P, P, P, i64, i64, i64, P]),
     "dwdp_fill_bf16": (i32, [P, i64, u64, f32, P]),
 }

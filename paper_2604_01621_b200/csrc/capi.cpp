@@ -523,6 +523,43 @@ int dwdp_ctx_launch_count(const dwdp_ctx* c, int64_t* n) {
   });
 }
 
+int dwdp_nccl_unique_id(void* id) {
+  return guard([&] {
+    need(id, "id");
+    dwdp::nccl_unique_id(id);
+  });
+}
+
+int dwdp_dep_init(dwdp_ctx* c, const void* id) {
+  return guard([&] {
+    need(id, "nccl_id");
+    C(c).dep_init(id);
+  });
+}
+
+int dwdp_dep_layer_forward(dwdp_ctx* c, int layer, const void* x, int64_t T, void* y,
+                           int residual, void* stream) {
+  return guard([&] {
+    if (T > 0) {
+      need(x, "x");
+      need(y, "y");
+    }
+    C(c).dep_layer_forward(layer, static_cast<const uint16_t*>(x), T, static_cast<uint16_t*>(y),
+                           residual != 0, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int dwdp_dep_stack_forward(dwdp_ctx* c, const void* x, int64_t T, void* y, void* stream) {
+  return guard([&] {
+    if (T > 0) {
+      need(x, "x");
+      need(y, "y");
+    }
+    C(c).dep_stack_forward(static_cast<const uint16_t*>(x), T, static_cast<uint16_t*>(y),
+                           static_cast<cudaStream_t>(stream));
+  });
+}
+
 int dwdp_gemm_bf16(const void* A, const void* B, void* D, int64_t M, int64_t N, int64_t K,
                    void* stream) {
   return guard([&] {

@@ -1,0 +1,273 @@
+// DEP baseline: "the same kernels with the two all-to-alls".
+//
+// Reference semantics: simulate_dep (/root/reference/proj/src/simcore.cpp:346-478):
+// EP partition into contiguous expert blocks (:359-370), per layer barrier +
+// dispatch all-to-all, expert-parallel MoE over the tokens routed to the
+// rank's block (:401-451), barrier + combine all-to-all (:452-465).
+//
+// B200 realisation: router/top-k/permute on the rank's own tokens (shared
+// kernels), an NCCL all-gather of the per-expert counts (the host needs the
+// message sizes: DEP's inherent synchronisation point), grouped ncclSend /
+// ncclRecv of the expert-sorted rows, the grouped GEMMs over the received
+// rows (each (source, expert) segment padded to 128 rows so the m-block ->
+// expert table needs no regroup copy), the reverse all-to-all back into the
+// send layout, and the weighted combine. NCCL is resolved at run time from
+// the copy the process already loaded (torch), so libdwdp.so has no link
+// dependency on it.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "gemm_sm100.hpp"
+#include "runtime.hpp"
+
+namespace dwdp {
+namespace {
+
+struct NcclId {
+  char internal[DWDP_NCCL_ID_BYTES];
+};
+constexpr int kBf16 = 9, kInt32 = 2;
+
+struct Nccl {
+  int (*GetUniqueId)(NcclId*) = nullptr;
+  int (*CommInitRank)(void**, int, NcclId, int) = nullptr;
+  int (*CommDestroy)(void*) = nullptr;
+  int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+
+const Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    auto sym = [&](const char* s) { return dlsym(h, s); };
+    n.GetUniqueId = reinterpret_cast<decltype(n.GetUniqueId)>(sym("ncclGetUniqueId"));
+    n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(sym("ncclCommInitRank"));
+    n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(sym("ncclCommDestroy"));
+    n.Send = reinterpret_cast<decltype(n.Send)>(sym("ncclSend"));
+    n.Recv = reinterpret_cast<decltype(n.Recv)>(sym("ncclRecv"));
+    n.AllGather = reinterpret_cast<decltype(n.AllGather)>(sym("ncclAllGather"));
+    n.GroupStart = reinterpret_cast<decltype(n.GroupStart)>(sym("ncclGroupStart"));
+    n.GroupEnd = reinterpret_cast<decltype(n.GroupEnd)>(sym("ncclGroupEnd"));
+    n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(sym("ncclGetErrorString"));
+  });
+  if (!n.CommInitRank || !n.Send || !n.Recv || !n.AllGather)
+    throw CudaError("NCCL not available (libnccl.so.2 not loadable)");
+  return n;
+}
+
+void nccl_check(int r, const char* what) {
+  if (r != 0)
+    throw CudaError(std::string(what) + ": " +
+                    (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error"));
+}
+
+inline int64_t pad128(int64_t n) { return (n + 127) / 128 * 128; }
+
+}  // namespace
+
+void nccl_destroy(void* comm) {
+  if (comm && nccl().CommDestroy) nccl().CommDestroy(comm);
+}
+
+void nccl_unique_id(void* out) {
+  NcclId id;
+  nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+  std::memcpy(out, &id, sizeof id);
+}
+
+void Ctx::dep_init(const void* unique_id) {
+  struct DG {
+    int prev = -1;
+    explicit DG(int d) {
+      cudaGetDevice(&prev);
+      cudaSetDevice(d);
+    }
+    ~DG() { cudaSetDevice(prev); }
+  } dg(cfg.device);
+  require(N_ >= 2, "dep: group_size must be >= 2");
+  require(E_ % N_ == 0, "dep: group_size must divide num_experts");
+  require(nccl_ == nullptr, "dep: already initialised");
+  NcclId id;
+  std::memcpy(&id, unique_id, sizeof id);
+  nccl_check(nccl().CommInitRank(&nccl_, N_, id, rank_), "ncclCommInitRank");
+  dep_counts_all_ = static_cast<int32_t*>(dalloc(size_t(N_) * E_ * 4, &workspace_bytes));
+  DWDP_CUDA(cudaHostAlloc(&dep_counts_host_, size_t(N_) * E_ * 4, 0));
+  dep_tab_cap_ = max_mb_ * 2 + 16;
+  dep_tab_ = static_cast<int32_t*>(dalloc(size_t(dep_tab_cap_) * 4, &workspace_bytes));
+  DWDP_CUDA(cudaHostAlloc(&dep_tab_host_, size_t(dep_tab_cap_) * 4, 0));
+  dep_reserve(max_rows_);
+}
+
+void Ctx::dep_reserve(int64_t rows) {
+  if (rows <= dep_cap_rows_) return;
+  rows = rows + rows / 4;  // headroom for routing imbalance across ranks
+  DWDP_CUDA(cudaDeviceSynchronize());
+  if (dep_recv_) cudaFree(dep_recv_);
+  if (dep_h_) cudaFree(dep_h_);
+  dep_recv_ = static_cast<uint16_t*>(dalloc(size_t(rows) * h_ * 2, nullptr));
+  dep_h_ = static_cast<uint16_t*>(dalloc(size_t(rows) * f_ * 2, nullptr));
+  dep_cap_rows_ = rows;
+  tm_dep_recv_ = make_tmap_bf16(dep_recv_, rows, h_, 128);
+  tm_dep_h_ = make_tmap_bf16(dep_h_, rows, f_, 128);
+  const int64_t need_tab = rows / 128 + 16;
+  if (need_tab > dep_tab_cap_) {
+    cudaFree(dep_tab_);
+    cudaFreeHost(dep_tab_host_);
+    dep_tab_cap_ = need_tab;
+    dep_tab_ = static_cast<int32_t*>(dalloc(size_t(dep_tab_cap_) * 4, nullptr));
+    DWDP_CUDA(cudaHostAlloc(&dep_tab_host_, size_t(dep_tab_cap_) * 4, 0));
+  }
+}
+
+void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
+                            cudaStream_t st) {
+  struct DG {
+    int prev = -1;
+    explicit DG(int d) {
+      cudaGetDevice(&prev);
+      cudaSetDevice(d);
+    }
+    ~DG() { cudaSetDevice(prev); }
+  } dg(cfg.device);
+  require(nccl_ != nullptr, "dep: call dep_init first");
+  require(layer >= 0 && layer < L_, "dep: layer out of range");
+  require(T >= 0 && T <= max_tokens_, "dep: T exceeds max_tokens");
+  const Nccl& n = nccl();
+  const int wl = layer % WL_;
+  const int per = E_ / N_;
+  LayerRec rec{int64_t(layer), T, take_event(), take_event(), take_event(), nullptr, -1};
+  DWDP_CUDA(cudaEventRecord(rec.gate0, st));
+  DWDP_CUDA(cudaEventRecord(rec.gate1, st));
+  auto mark = [&](cudaEvent_t* slot) {
+    *slot = take_event();
+    DWDP_CUDA(cudaEventRecord(*slot, st));
+  };
+  // 1. router + top-k + permute of the rank's own tokens (send layout)
+  RouterCfg rc{E_, k_, cfg.scoring, cfg.n_group, cfg.topk_group, cfg.norm_topk, cfg.routed_scale};
+  if (T > 0) {
+    launch_router_logits(x, router_w_ + size_t(wl) * E_ * h_, logits_, T, E_, h_, st);
+    launch_topk(logits_, bias_ + size_t(wl) * E_, idx_, wts_, T, rc, st);
+  }
+  mark(&rec.k[0]);
+  if (T > 0)
+    launch_permute(idx_, x, T, E_, k_, h_, 0, counts_, row_of_, mblock_, meta_, xperm_, scratch_, st);
+  else
+    DWDP_CUDA(cudaMemsetAsync(counts_, 0, size_t(E_) * 4, st));
+  mark(&rec.k[1]);
+  // 2. counts exchange (host needs every message size)
+  nccl_check(n.AllGather(counts_, dep_counts_all_, size_t(E_), kInt32, nccl_, st), "ncclAllGather");
+  DWDP_CUDA(cudaMemcpyAsync(dep_counts_host_, dep_counts_all_, size_t(N_) * E_ * 4,
+                            cudaMemcpyDeviceToHost, st));
+  DWDP_CUDA(cudaStreamSynchronize(st));
+  const int32_t* ca = dep_counts_host_;
+  const size_t nr = static_cast<size_t>(N_);
+  std::vector<int64_t> send_off(nr), send_rows(nr), recv_off(nr), recv_rows(nr);
+  int64_t acc = 0;
+  for (int d = 0; d < N_; ++d) {
+    send_off[size_t(d)] = acc;
+    int64_t r = 0;
+    for (int e = d * per; e < (d + 1) * per; ++e) r += pad128(ca[size_t(rank_) * E_ + e]);
+    send_rows[size_t(d)] = r;
+    acc += r;
+  }
+  acc = 0;
+  int64_t nblocks = 0;
+  for (int s = 0; s < N_; ++s) {
+    recv_off[size_t(s)] = acc;
+    int64_t r = 0;
+    for (int e = rank_ * per; e < (rank_ + 1) * per; ++e) r += pad128(ca[size_t(s) * E_ + e]);
+    recv_rows[size_t(s)] = r;
+    acc += r;
+  }
+  const int64_t routed_rows = acc;
+  const int64_t shared_blocks = shared_ ? (T + 127) / 128 : 0;
+  dep_reserve(routed_rows + shared_blocks * 128);
+  // m-block -> expert over the receive layout, then the shared expert blocks
+  for (int s = 0; s < N_; ++s)
+    for (int e = rank_ * per; e < (rank_ + 1) * per; ++e)
+      for (int64_t b = 0; b < pad128(ca[size_t(s) * E_ + e]) / 128; ++b) dep_tab_host_[4 + nblocks++] = e;
+  const int64_t routed_mb = nblocks;
+  for (int64_t b = 0; b < shared_blocks; ++b) dep_tab_host_[4 + nblocks++] = E_;
+  dep_tab_host_[0] = int32_t(nblocks);
+  dep_tab_host_[1] = int32_t(routed_mb);
+  dep_tab_host_[2] = int32_t(routed_rows);
+  dep_tab_host_[3] = int32_t(T);
+  DWDP_CUDA(cudaMemcpyAsync(dep_tab_, dep_tab_host_, size_t(4 + nblocks) * 4,
+                            cudaMemcpyHostToDevice, st));
+  // 3. dispatch all-to-all
+  const size_t rowel = size_t(h_);
+  nccl_check(n.GroupStart(), "ncclGroupStart");
+  for (int p = 0; p < N_; ++p) {
+    if (p == rank_) continue;
+    if (send_rows[size_t(p)])
+      nccl_check(n.Send(xperm_ + send_off[size_t(p)] * h_, size_t(send_rows[size_t(p)]) * rowel,
+                        kBf16, p, nccl_, st), "ncclSend");
+    if (recv_rows[size_t(p)])
+      nccl_check(n.Recv(dep_recv_ + recv_off[size_t(p)] * h_, size_t(recv_rows[size_t(p)]) * rowel,
+                        kBf16, p, nccl_, st), "ncclRecv");
+  }
+  nccl_check(n.GroupEnd(), "ncclGroupEnd");
+  if (send_rows[size_t(rank_)])
+    DWDP_CUDA(cudaMemcpyAsync(dep_recv_ + recv_off[size_t(rank_)] * h_,
+                              xperm_ + send_off[size_t(rank_)] * h_,
+                              size_t(send_rows[size_t(rank_)]) * rowel * 2, cudaMemcpyDeviceToDevice, st));
+  mark(&rec.comm[1]);
+  // 4. expert-parallel grouped GEMMs (+ shared expert on own tokens)
+  const int32_t* stab = slot_tab_ + size_t(layer) * 2 * (E_ + 1);
+  const int32_t* dmeta = dep_tab_;
+  const int32_t* dmb = dep_tab_ + 4;
+  if (nblocks > 0) {
+    const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_dep_recv_;
+    GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1};
+    launch_grouped_gemm(true, tm_dep_recv_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
+  }
+  mark(&rec.k[2]);
+  if (nblocks > 0) {
+    GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0};
+    launch_grouped_gemm(false, tm_dep_h_, tm_dep_h_, tm_down_, tm_down_, g2, int(nblocks * (h_ / 256)), st);
+  }
+  mark(&rec.k[3]);
+  // 5. combine all-to-all: results back into the send layout (xperm)
+  nccl_check(n.GroupStart(), "ncclGroupStart");
+  for (int p = 0; p < N_; ++p) {
+    if (p == rank_) continue;
+    if (recv_rows[size_t(p)])
+      nccl_check(n.Send(dep_recv_ + recv_off[size_t(p)] * h_, size_t(recv_rows[size_t(p)]) * rowel,
+                        kBf16, p, nccl_, st), "ncclSend");
+    if (send_rows[size_t(p)])
+      nccl_check(n.Recv(xperm_ + send_off[size_t(p)] * h_, size_t(send_rows[size_t(p)]) * rowel,
+                        kBf16, p, nccl_, st), "ncclRecv");
+  }
+  nccl_check(n.GroupEnd(), "ncclGroupEnd");
+  if (send_rows[size_t(rank_)])
+    DWDP_CUDA(cudaMemcpyAsync(xperm_ + send_off[size_t(rank_)] * h_,
+                              dep_recv_ + recv_off[size_t(rank_)] * h_,
+                              size_t(send_rows[size_t(rank_)]) * rowel * 2, cudaMemcpyDeviceToDevice, st));
+  mark(&rec.comm[3]);
+  // 6. weighted combine (shared rows follow the routed rows of the receive buffer)
+  launch_combine(xperm_, row_of_, wts_, shared_ ? dep_recv_ + routed_rows * h_ : nullptr, nullptr,
+                 residual ? x : nullptr, y, T, k_, h_, st);
+  launches += 8;
+  DWDP_CUDA(cudaGetLastError());
+  DWDP_CUDA(cudaEventRecord(rec.moe_end, st));
+  rec.rows = routed_rows;
+  recs_.push_back(rec);
+}
+
+void Ctx::dep_stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t st) {
+  for (int l = 0; l < L_; ++l) dep_layer_forward(l, l == 0 ? x : y, T, y, true, st);
+}
+
+}  // namespace dwdp

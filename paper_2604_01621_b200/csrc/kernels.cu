@@ -437,10 +437,11 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
 __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict__ O,
                                                       const int32_t* __restrict__ row_of,
                                                       const float* __restrict__ wts,
-                                                      const int32_t* __restrict__ meta,
+                                                      const uint16_t* __restrict__ S,
+                                                      const int32_t* __restrict__ s_meta,
                                                       const uint16_t* __restrict__ resid,
                                                       uint16_t* __restrict__ y, int64_t T, int k,
-                                                      int64_t h, int shared) {
+                                                      int64_t h) {
   const int64_t t = blockIdx.x;
   if (t >= T) return;
   __shared__ int32_t srow[TOPK_MAXK + 1];
@@ -449,8 +450,9 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
     srow[threadIdx.x] = row_of[t * k + threadIdx.x];
     sw[threadIdx.x] = wts[t * k + threadIdx.x];
   }
-  if (threadIdx.x == 0) srow[TOPK_MAXK] = shared ? meta[2] + int32_t(t) : 0;
+  if (threadIdx.x == 0) srow[TOPK_MAXK] = (s_meta ? s_meta[2] : 0) + int32_t(t);
   __syncthreads();
+  const bool shared = S != nullptr;
   const int64_t segs = h / 8;
   for (int64_t s = threadIdx.x; s < segs; s += blockDim.x) {
     float acc[8];
@@ -467,7 +469,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
       }
     }
     if (shared) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(O + int64_t(srow[TOPK_MAXK]) * h) + s);
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(S + int64_t(srow[TOPK_MAXK]) * h) + s);
       const uint32_t u[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -583,10 +585,10 @@ void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int
 }
 
 void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
-                    const int32_t* meta, const uint16_t* resid, uint16_t* y, int64_t T, int k,
-                    int64_t h, int shared, cudaStream_t st) {
+                    const uint16_t* S, const int32_t* s_meta, const uint16_t* resid, uint16_t* y,
+                    int64_t T, int k, int64_t h, cudaStream_t st) {
   if (T > 0)
-    combine_kernel<<<unsigned(T), 128, 0, st>>>(O, row_of, wts, meta, resid, y, T, k, h, shared);
+    combine_kernel<<<unsigned(T), 128, 0, st>>>(O, row_of, wts, S, s_meta, resid, y, T, k, h);
 }
 
 void launch_pull(const PullItem* items, int n, int ctas, cudaStream_t st) {

@@ -38,10 +38,12 @@ void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
                     int32_t* meta, uint16_t* xperm, int32_t* scratch, cudaStream_t st);
 
-// y[t] = sum_j w[t,j] * O[row_of[t,j]] (+ O[shared_row0 + t]) (+ x[t]).
+// y[t] = sum_j w[t,j] * O[row_of[t,j]] (+ S[s_off + t]) (+ x[t]); the shared
+// expert rows start at S + s_off*h with s_off = s_meta ? s_meta[2] : 0
+// (S == nullptr: no shared expert).
 void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
-                    const int32_t* meta, const uint16_t* resid, uint16_t* y, int64_t T, int k,
-                    int64_t h, int shared, cudaStream_t st);
+                    const uint16_t* S, const int32_t* s_meta, const uint16_t* resid, uint16_t* y,
+                    int64_t T, int k, int64_t h, cudaStream_t st);
 
 // One-launch P2P pull of a slice list over NVLink: work[i] = {src, dst, len}.
 struct PullItem {

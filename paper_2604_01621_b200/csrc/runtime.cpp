@@ -138,8 +138,15 @@ Ctx::~Ctx() {
   DeviceGuard dg(cfg.device);
   cudaDeviceSynchronize();
   for (auto& r : recs_)
-    for (cudaEvent_t e : {r.gate0, r.gate1, r.moe_end, r.merge_end, r.k[0], r.k[1], r.k[2], r.k[3]})
+    for (cudaEvent_t e : {r.gate0, r.gate1, r.moe_end, r.merge_end, r.k[0], r.k[1], r.k[2], r.k[3],
+                          r.comm[0], r.comm[1], r.comm[2], r.comm[3]})
       if (e) cudaEventDestroy(e);
+  nccl_destroy(nccl_);
+  for (void* b : {static_cast<void*>(dep_recv_), static_cast<void*>(dep_h_),
+                  static_cast<void*>(dep_counts_all_), static_cast<void*>(dep_tab_)})
+    if (b) cudaFree(b);
+  if (dep_counts_host_) cudaFreeHost(dep_counts_host_);
+  if (dep_tab_host_) cudaFreeHost(dep_tab_host_);
   for (auto& p : plans_) {
     if (p.start) cudaEventDestroy(p.start);
     if (p.done) cudaEventDestroy(p.done);
@@ -489,7 +496,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0};
   launch_grouped_gemm(false, tm_h_, tm_h_, tm_down_, tm_down_, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
   mark(3);
-  launch_combine(xperm_, row_of_, wts_, meta_, resid, y, T, k_, h_, shared_ ? 1 : 0, st);
+  launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
   launches += 8;
   if (timed) {
     if (!meta_ring_) DWDP_CUDA(cudaHostAlloc(&meta_ring_, kMetaRing * 4 * sizeof(int32_t), 0));
@@ -580,22 +587,31 @@ size_t Ctx::drain_records(dwdp_layer_record* out, size_t cap) {
       DWDP_CUDA(cudaEventElapsedTime(&pf, p.start, p.done));
       pbytes = p.bytes;
     }
-    double kns[5] = {0, 0, 0, 0, 0};
-    if (r.k[0] && r.k[3]) {
-      cudaEvent_t seq[6] = {r.merge_end ? r.merge_end : r.gate1, r.k[0], r.k[1], r.k[2], r.k[3],
-                            r.moe_end};
-      for (int i = 0; i < 5; ++i) {
-        float ms = 0;
-        DWDP_CUDA(cudaEventElapsedTime(&ms, seq[i], seq[i + 1]));
-        kns[i] = double(ms) * 1e6;
-      }
+    auto el = [](cudaEvent_t a, cudaEvent_t b) {
+      float ms = 0;
+      DWDP_CUDA(cudaEventElapsedTime(&ms, a, b));
+      return double(ms) * 1e6;
+    };
+    double kns[5] = {0, 0, 0, 0, 0}, comm = 0;
+    const cudaEvent_t begin = r.merge_end ? r.merge_end : r.gate1;
+    if (r.k[0] && r.k[3] && r.comm[1] && r.comm[3]) {  // DEP layer
+      kns[0] = el(begin, r.k[0]);
+      kns[1] = el(r.k[0], r.k[1]);
+      kns[2] = el(r.comm[1], r.k[2]);
+      kns[3] = el(r.k[2], r.k[3]);
+      kns[4] = el(r.comm[3], r.moe_end);
+      comm = el(r.k[1], r.comm[1]) + el(r.k[3], r.comm[3]);
+    } else if (r.k[0] && r.k[3]) {
+      const cudaEvent_t seq[6] = {begin, r.k[0], r.k[1], r.k[2], r.k[3], r.moe_end};
+      for (int i = 0; i < 5; ++i) kns[i] = el(seq[i], seq[i + 1]);
     }
-    const int64_t rows = r.meta_slot >= 0 ? meta_ring_[r.meta_slot * 4 + 2] : -1;
+    const int64_t rows = r.rows >= 0 ? r.rows : r.meta_slot >= 0 ? meta_ring_[r.meta_slot * 4 + 2] : -1;
     if (out)
       out[n] = {r.g,    r.tokens, double(wait) * 1e6, double(moe) * 1e6, double(pf) * 1e6, pbytes,
-                double(merge) * 1e6, kns[0], kns[1], kns[2], kns[3], kns[4], rows};
+                double(merge) * 1e6, kns[0], kns[1], kns[2], kns[3], kns[4], rows, comm};
     ++n;
-    for (cudaEvent_t e : {r.gate0, r.gate1, r.moe_end, r.merge_end, r.k[0], r.k[1], r.k[2], r.k[3]})
+    for (cudaEvent_t e : {r.gate0, r.gate1, r.moe_end, r.merge_end, r.k[0], r.k[1], r.k[2], r.k[3],
+                          r.comm[0], r.comm[1], r.comm[2], r.comm[3]})
       if (e) free_events_.push_back(e);
   }
   return n;

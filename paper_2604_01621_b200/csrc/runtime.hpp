@@ -20,6 +20,9 @@ struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+void nccl_unique_id(void* out);  // dep.cpp
+void nccl_destroy(void* comm);
+
 #define DWDP_CUDA(x)                                                                         \
   do {                                                                                       \
     const cudaError_t e_ = (x);                                                              \
@@ -49,6 +52,9 @@ struct LayerRec {
   int64_t plan;  // index into plans_ or -1
   cudaEvent_t k[4] = {nullptr, nullptr, nullptr, nullptr};  // after router/permute/gemm1/gemm2
   int meta_slot = -1;                                       // pinned copy of meta[2]
+  // DEP: [0] dispatch start, [1] dispatch end, [2] return start, [3] return end
+  cudaEvent_t comm[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t rows = -1;                                        // host-known routed rows (DEP)
 };
 
 class Ctx {
@@ -81,6 +87,13 @@ class Ctx {
 
   void gemm_bf16(const uint16_t* A, const uint16_t* B, uint16_t* D, int64_t M, int64_t N,
                  int64_t K, cudaStream_t st);
+
+  // DEP baseline (dep.cpp): expert parallelism over the same contiguous
+  // blocks, dispatch + combine all-to-alls over NCCL (simcore.cpp:346-478).
+  void dep_init(const void* nccl_unique_id);
+  void dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
+                         cudaStream_t st);
+  void dep_stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t st);
 
   dwdp_ctx_config cfg;
   uint64_t weight_bytes = 0, recv_bytes = 0, workspace_bytes = 0;
@@ -136,6 +149,18 @@ class Ctx {
   int32_t* meta_ring_ = nullptr;  // pinned host ring for per-layer routed rows
   int meta_ring_pos_ = 0;
   static constexpr int kMetaRing = 4096;
+  // DEP state
+  void* nccl_ = nullptr;                 // ncclComm_t
+  uint16_t* dep_recv_ = nullptr;         // received X, then O, + shared rows
+  uint16_t* dep_h_ = nullptr;            // H of the received rows
+  int64_t dep_cap_rows_ = 0;
+  int32_t* dep_counts_all_ = nullptr;    // device [N][E]
+  int32_t* dep_counts_host_ = nullptr;   // pinned [N][E]
+  int32_t* dep_tab_ = nullptr;           // device m-block table + meta
+  int32_t* dep_tab_host_ = nullptr;      // pinned staging
+  int64_t dep_tab_cap_ = 0;
+  CUtensorMap tm_dep_recv_, tm_dep_h_;
+  void dep_reserve(int64_t rows);
   int num_sms_ = 148;
 };
 

@@ -183,6 +183,22 @@ class DwdpContext:
                                _ptr(row_of), C.byref(rows), _stream(stream)))
         return idx, wts, counts, row_of, rows.value
 
+    # -- DEP baseline (same kernels + NCCL all-to-alls) ----------------------
+    def dep_init(self, nccl_id: bytes) -> None:
+        assert len(nccl_id) == 128
+        check(lib().dwdp_dep_init(self.h, C.create_string_buffer(nccl_id, 128)))
+
+    def dep_layer_forward(self, layer: int, x, y=None, residual: bool = True, stream=None):
+        y = self._out(x, y)
+        check(lib().dwdp_dep_layer_forward(self.h, layer, _ptr(x), x.shape[0], _ptr(y),
+                                           int(residual), _stream(stream)))
+        return y
+
+    def dep_stack_forward(self, x, y=None, stream=None):
+        y = self._out(x, y)
+        check(lib().dwdp_dep_stack_forward(self.h, _ptr(x), x.shape[0], _ptr(y), _stream(stream)))
+        return y
+
     # -- accounting ----------------------------------------------------------
     def records(self) -> list[dict]:
         out = []
@@ -198,6 +214,12 @@ class DwdpContext:
         n = C.c_int64()
         check(lib().dwdp_ctx_launch_count(self.h, C.byref(n)))
         return n.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().dwdp_nccl_unique_id(buf))
+    return buf.raw
 
 
 def gemm_bf16(A, B, D=None, stream=None):

@@ -1,0 +1,80 @@
+"""torchrun worker for tests/test_multigpu.py (one process per GPU).
+
+Every rank runs three variants of the same 3-layer MoE stack on its own
+tokens: DWDP (owned experts + one-sided NVLink pulls through CUDA IPC), DEP
+(same kernels + NCCL all-to-alls) and the all-local model on the same seed.
+Rows are independent in every kernel, so all three must agree bit for bit."""
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_01621_b200 as D  # noqa: E402
+
+MID = dict(num_layers=3, num_experts=64, hidden=1024, ffn=256, shared_ffn=256, top_k=6,
+           n_group=8, topk_group=4, max_tokens=1024, weight_layers=3)
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    engine = int(os.environ.get("DWDP_ENGINE", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    ctx = D.DwdpContext(D.DwdpConfig(**MID, rank=rank, group_size=world, device=local,
+                                     engine=engine, slice_size=1 << 19))
+    ctx.init_weights()
+    blobs = [None] * world
+    dist.all_gather_object(blobs, ctx.export_ipc())
+    ctx.open_peers(b"".join(blobs))
+    ids = [D.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(ids, src=0)
+    ctx.dep_init(ids[0])
+    full = D.DwdpContext(D.DwdpConfig(**MID, device=local))
+    full.init_weights()
+    torch.cuda.synchronize()
+    dist.barrier()
+
+    T = 100 + 61 * rank
+    x = torch.empty((T, MID["hidden"]), dtype=torch.bfloat16, device=dev)
+    D.fill_bf16(x, 1000 + rank, 1.0)
+    bad = 0
+    for g in range(5):  # crosses the stack boundary (L = 3): prefetch of layer 0 again
+        l = g % 3
+        y_dwdp = ctx.layer_forward(g, x, residual=False)
+        y_dep = ctx.dep_layer_forward(l, x, residual=False)
+        y_ref = full.moe_forward(l, x)
+        torch.cuda.synchronize()
+        if not torch.equal(y_dwdp, y_ref):
+            print(f"rank {rank} layer {g}: DWDP != all-local", flush=True)
+            bad += 1
+        if not torch.equal(y_dep, y_ref):
+            diff = (y_dep.float() - y_ref.float()).abs().max().item()
+            print(f"rank {rank} layer {g}: DEP != all-local (max abs diff {diff})", flush=True)
+            bad += 1
+    # stack variants through the public API
+    y1 = ctx.stack_forward(x)
+    y2 = ctx.dep_stack_forward(x)
+    torch.cuda.synchronize()
+    if not torch.equal(y1, y2):
+        print(f"rank {rank}: stack DWDP != stack DEP", flush=True)
+        bad += 1
+    recs = ctx.records()
+    waits = [r["gate_wait_ns"] for r in recs if r["prefetch_bytes"] > 0]
+    t = torch.tensor([bad], device=dev)
+    dist.all_reduce(t)
+    if rank == 0:
+        print(f"MPCHECK world={world} engine={engine} failures={int(t.item())} "
+              f"records={len(recs)} max_wait_ms={max(waits) / 1e6 if waits else 0:.3f}", flush=True)
+    ctx.close()
+    full.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(1 if int(t.item()) else 0)
+
+
+if __name__ == "__main__":
+    main()
