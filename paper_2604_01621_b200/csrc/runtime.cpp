@@ -512,6 +512,7 @@ void Ctx::layer_forward(int64_t g, const uint16_t* x, int64_t T, uint16_t* y, bo
                         cudaStream_t st) {
   DeviceGuard dg(cfg.device);
   const int l = int(g % L_), par = int(g & 1);
+  cursor_ = std::max(cursor_, g + 1);
   LayerRec rec{g, T, take_event(), take_event(), take_event(), nullptr, -1};
   DWDP_CUDA(cudaEventRecord(rec.gate0, st));
   if (nrecv_ > 0) {
@@ -540,11 +541,11 @@ void Ctx::layer_forward(int64_t g, const uint16_t* x, int64_t T, uint16_t* y, bo
   recs_.push_back(rec);
 }
 
+// One iteration of the stack starts at the next global layer that is layer 0
+// (global layer g = iteration * L + l, simcore.cpp:711-728).
 void Ctx::stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t st) {
-  for (int l = 0; l < L_; ++l) {
-    const int64_t g = cursor_++;
-    layer_forward(g, l == 0 ? x : y, T, y, true, st);
-  }
+  const int64_t g0 = (cursor_ + L_ - 1) / L_ * L_;
+  for (int l = 0; l < L_; ++l) layer_forward(g0 + l, l == 0 ? x : y, T, y, true, st);
 }
 
 void Ctx::route(int layer, const uint16_t* x, int64_t T, int32_t* idx, float* wts,
