@@ -526,12 +526,48 @@ static void select_token(const oracle_moe_config* cfg, const float* logit,
   for (int j = 0; j < k; ++j) wts[j] = wts[j] * cfg->routed_scale;
 }
 
+/* Router logits (north-star semantics of x . Wr^T in fp32, made exactly
+ * reproducible): every bf16 row is put on a 22-bit fixed-point grid relative
+ * to its largest exponent field emax (value = Q * 2^(emax - 148); elements
+ * more than 14 binades below the row maximum are truncated to the grid), the
+ * dot product of two rows is the exact int64 sum of Q_x * Q_w, rounded ONCE to
+ * fp32 and scaled by 2^(emax_x + emax_w - 296). Order-free, so the device
+ * computes it bit-identically with int8 tensor cores (three digit planes). */
+static inline uint16_t f32_bits_bf16(float f) { /* exact for bf16 values */
+  union {
+    float f;
+    uint32_t u;
+  } c;
+  c.f = f;
+  return (uint16_t)(c.u >> 16);
+}
+
+static void quant_row(const uint16_t* b, const float* f, int64_t K, int32_t* q, int* emax) {
+  int m = 0;
+  for (int64_t i = 0; i < K; ++i) {
+    const uint16_t v = b ? b[i] : f32_bits_bf16(f[i]);
+    const int E = (v >> 7) & 0xFF, M = v & 0x7F;
+    const int mant = E ? (M | 0x80) : M, eb = E ? E : 1;
+    if (mant && eb > m) m = eb;
+  }
+  if (m == 0) m = 1;
+  for (int64_t i = 0; i < K; ++i) {
+    const uint16_t v = b ? b[i] : f32_bits_bf16(f[i]);
+    const int E = (v >> 7) & 0xFF, M = v & 0x7F;
+    const int mant = E ? (M | 0x80) : M, eb = E ? E : 1;
+    const int sh = eb - m + 14;
+    const int qq = sh >= 0 ? (mant << sh) : (sh > -8 ? (mant >> -sh) : 0);
+    q[i] = (v & 0x8000) ? -qq : qq;
+  }
+  *emax = m;
+}
+
 typedef struct {
   const oracle_moe_config* cfg;
   const uint16_t* x16;
   const float* x32;
-  const uint16_t* w16;
-  const float* w32;
+  const int32_t* wq; /* [E][h] quantised router rows */
+  const int* we;     /* [E] their exponents */
   const float* bias;
   float* logits;
   int32_t* idx;
@@ -543,23 +579,40 @@ static void route_one(void* p, int64_t t) {
   const int64_t h = a->cfg->hidden;
   const int E = a->cfg->num_experts;
   float* lg = a->logits + t * E;
+  int32_t* xq = malloc(sizeof(int32_t) * (size_t)h);
+  int ex;
+  quant_row(a->x16 ? a->x16 + t * h : NULL, a->x32 ? a->x32 + t * h : NULL, h, xq, &ex);
   for (int e = 0; e < E; ++e) {
-    float acc = 0.0f; /* sequential fused multiply-add, i = 0..h-1 */
-    for (int64_t i = 0; i < h; ++i) {
-      const float xv = a->x16 ? bf16_to_f32(a->x16[t * h + i]) : a->x32[t * h + i];
-      const float wv = a->w16 ? bf16_to_f32(a->w16[(int64_t)e * h + i]) : a->w32[(int64_t)e * h + i];
-      acc = fmaf(xv, wv, acc);
-    }
-    lg[e] = acc;
+    const int32_t* wr = a->wq + (int64_t)e * h;
+    int64_t z = 0;
+    for (int64_t i = 0; i < h; ++i) z += (int64_t)xq[i] * (int64_t)wr[i];
+    lg[e] = ldexpf((float)z, ex + a->we[e] - 296);
   }
+  free(xq);
   select_token(a->cfg, lg, a->bias, a->idx + t * a->cfg->top_k, a->wts + t * a->cfg->top_k);
+}
+
+/* Quantise the router rows once, route every token, release. */
+static void route_all(const oracle_moe_config* cfg, const uint16_t* x16, const float* x32,
+                      int64_t T, const uint16_t* w16, const float* w32, const float* bias,
+                      float* logits, int32_t* idx, float* wts, int nthreads) {
+  const int64_t h = cfg->hidden;
+  const int E = cfg->num_experts;
+  int32_t* wq = malloc(sizeof(int32_t) * (size_t)(E * h));
+  int* we = malloc(sizeof(int) * (size_t)E);
+  for (int e = 0; e < E; ++e)
+    quant_row(w16 ? w16 + (int64_t)e * h : NULL, w32 ? w32 + (int64_t)e * h : NULL, h,
+              wq + (int64_t)e * h, &we[e]);
+  route_arg a = {cfg, x16, x32, wq, we, bias, logits, idx, wts};
+  parallel_for(T, nthreads, route_one, &a);
+  free(wq);
+  free(we);
 }
 
 void oracle_route(const oracle_moe_config* cfg, const uint16_t* x, int64_t T,
                   const uint16_t* w_router, const float* bias, float* logits,
                   int32_t* idx, float* wts) {
-  route_arg a = {cfg, x, NULL, w_router, NULL, bias, logits, idx, wts};
-  parallel_for(T, 0, route_one, &a);
+  route_all(cfg, x, NULL, T, w_router, NULL, bias, logits, idx, wts, 0);
 }
 
 int64_t oracle_permute(const int32_t* idx, int64_t T, int E, int k, int align,
@@ -781,8 +834,7 @@ void oracle_moe_forward_seeded(const oracle_moe_config* cfg, uint64_t base,
   uint16_t* wr = malloc(sizeof(uint16_t) * (size_t)(E * h));
   oracle_fill_bf16(oracle_tensor_seed(base, layer, E + 1, 0), E * h, 1.0f / sqrtf((float)h), wr);
   float* logits = malloc(sizeof(float) * (size_t)(T * E + 1));
-  route_arg ra = {cfg, x, NULL, wr, NULL, bias, logits, idx, wts};
-  parallel_for(T, nthreads, route_one, &ra);
+  route_all(cfg, x, NULL, T, wr, NULL, bias, logits, idx, wts, nthreads);
   float* xf = malloc(sizeof(float) * (size_t)(T * h + 1));
   for (int64_t i = 0; i < T * h; ++i) xf[i] = bf16_to_f32(x[i]);
   moe_forward_common(cfg, base, layer, xf, T, idx, wts, NULL, NULL, NULL, NULL,
@@ -801,8 +853,7 @@ void oracle_moe_forward_explicit(const oracle_moe_config* cfg, const float* x,
                                  float* wts) {
   const int E = cfg->num_experts;
   float* logits = malloc(sizeof(float) * (size_t)(T * E + 1));
-  route_arg ra = {cfg, NULL, x, NULL, w_router, bias, logits, idx, wts};
-  parallel_for(T, 0, route_one, &ra);
+  route_all(cfg, NULL, x, T, NULL, w_router, bias, logits, idx, wts, 0);
   moe_forward_common(cfg, 0, 0, x, T, idx, wts, w_gate, w_up, w_down, s_gate,
                      s_up, s_down, NULL, NULL, NULL, y, 0);
   free(logits);
@@ -817,8 +868,7 @@ void oracle_moe_forward_bf16w(const oracle_moe_config* cfg, const uint16_t* x,
   const int64_t h = cfg->hidden;
   const int E = cfg->num_experts;
   float* logits = malloc(sizeof(float) * (size_t)(T * E + 1));
-  route_arg ra = {cfg, x, NULL, w_router, NULL, bias, logits, idx, wts};
-  parallel_for(T, nthreads, route_one, &ra);
+  route_all(cfg, x, NULL, T, w_router, NULL, bias, logits, idx, wts, nthreads);
   float* xf = malloc(sizeof(float) * (size_t)(T * h + 1));
   for (int64_t i = 0; i < T * h; ++i) xf[i] = bf16_to_f32(x[i]);
   moe_forward_common(cfg, 0, 0, xf, T, idx, wts, NULL, NULL, NULL, NULL, NULL, NULL, gate, up,

@@ -155,11 +155,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
     DWDP_CUDA(cudaEventRecord(*slot, st));
   };
   // 1. router + top-k + permute of the rank's own tokens (send layout)
-  RouterCfg rc{E_, k_, cfg.scoring, cfg.n_group, cfg.topk_group, cfg.norm_topk, cfg.routed_scale};
-  if (T > 0) {
-    launch_router_logits(x, router_w_ + size_t(wl) * E_ * h_, logits_, T, E_, h_, st);
-    launch_topk(logits_, bias_ + size_t(wl) * E_, idx_, wts_, T, rc, st);
-  }
+  if (T > 0) route_logits(wl, x, T, st);
   mark(&rec.k[0]);
   if (T > 0)
     launch_permute(idx_, x, T, E_, k_, h_, 0, counts_, row_of_, mblock_, meta_, xperm_, scratch_, st);
@@ -231,12 +227,12 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   if (nblocks > 0) {
     const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_dep_recv_;
     GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1};
-    launch_grouped_gemm(true, tm_dep_recv_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
+    launch_grouped_gemm(GEMM_SWIGLU, tm_dep_recv_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
   }
   mark(&rec.k[2]);
   if (nblocks > 0) {
     GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0};
-    launch_grouped_gemm(false, tm_dep_h_, tm_dep_h_, tm_down_, tm_down_, g2, int(nblocks * (h_ / 256)), st);
+    launch_grouped_gemm(GEMM_PLAIN, tm_dep_h_, tm_dep_h_, tm_down_, tm_down_, g2, int(nblocks * (h_ / 256)), st);
   }
   mark(&rec.k[3]);
   // 5. combine all-to-all: results back into the send layout (xperm)

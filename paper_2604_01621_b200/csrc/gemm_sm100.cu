@@ -120,16 +120,32 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
          (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
-// Instruction descriptor: bf16 x bf16 -> fp32, both K-major, M=128, N=256.
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
-                           (uint32_t(BM >> 4) << 24);
+// Kernel modes: SwiGLU-fused bf16 (GEMM1), plain bf16 (GEMM2), and the exact
+// int8 x int8 -> int32 mode of the router (kind::i8, order-free accumulation).
+constexpr int kSwiGLU = 0, kPlain = 1, kInt8 = 2;
+// Instruction descriptor, both operands K-major, M=128, N=256:
+//   f16 kind: bf16 x bf16 -> fp32 (c_format 1, a/b_format 1 = BF16)
+//   i8 kind:  s8 x s8 -> s32      (c_format 2, a/b_format 1 = signed)
+template <int MODE>
+__host__ __device__ constexpr uint32_t idesc() {
+  return (MODE == kInt8 ? (2u << 4) : (1u << 4)) | (1u << 7) | (1u << 10) |
+         (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+}
+__device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc_v, uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc_v), "r"(accum));
+}
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(a))) |
          (uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(b))) << 16);
 }
 
-template <bool SWIGLU>
+template <int MODE>
 __global__ void __launch_bounds__(256, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmA2,
@@ -176,9 +192,11 @@ __global__ void __launch_bounds__(256, 1)
 
   const int total_mb = p.meta[0];
   const int routed_mb = p.meta[1];
-  const int nb_count = SWIGLU ? p.n_out / 128 : p.n_out / BN;
+  constexpr bool SWIGLU = MODE == kSwiGLU;
+  constexpr int BKE = MODE == kInt8 ? 128 : 64;  // K elements per 128-byte smem row
+  const int nb_count = SWIGLU ? p.n_out / 128 : (p.n_out + BN - 1) / BN;
   const int num_tiles = total_mb * nb_count;
-  const int kb_count = p.K / BK;
+  const int kb_count = p.K / BKE;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -194,12 +212,12 @@ __global__ void __launch_bounds__(256, 1)
         for (int kb = 0; kb < kb_count; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], A_STAGE + B_STAGE);
-          tma_load_2d(sA + s * A_STAGE, am, &full[s], kb * BK, arow);
+          tma_load_2d(sA + s * A_STAGE, am, &full[s], kb * BKE, arow);
           if (SWIGLU) {
-            tma_load_2d(sB + s * B_STAGE, &tmB0, &full[s], kb * BK, brow);
-            tma_load_2d(sB + s * B_STAGE + B_STAGE / 2, &tmB1, &full[s], kb * BK, brow);
+            tma_load_2d(sB + s * B_STAGE, &tmB0, &full[s], kb * BKE, brow);
+            tma_load_2d(sB + s * B_STAGE + B_STAGE / 2, &tmB1, &full[s], kb * BKE, brow);
           } else {
-            tma_load_2d(sB + s * B_STAGE, &tmB0, &full[s], kb * BK, brow);
+            tma_load_2d(sB + s * B_STAGE, &tmB0, &full[s], kb * BKE, brow);
           }
           if (++s == STAGES) {
             s = 0;
@@ -225,8 +243,12 @@ __global__ void __launch_bounds__(256, 1)
           const uint64_t ad = sw128_desc(smem_u32(sA + s * A_STAGE));
           const uint64_t bd = sw128_desc(smem_u32(sB + s * B_STAGE));
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)  // +32 B along K per UMMA_K = 16
-            tc_mma(d, ad + 2 * k, bd + 2 * k, IDESC, (kb | k) != 0);
+          for (int k = 0; k < 4; ++k) {  // +32 B along K per MMA (16 bf16 or 32 int8)
+            if (MODE == kInt8)
+              tc_mma_i8(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0);
+            else
+              tc_mma(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0);
+          }
           tc_commit(&empty[s]);
           if (++s == STAGES) {
             s = 0;
@@ -248,7 +270,26 @@ __global__ void __launch_bounds__(256, 1)
       const int64_t row = int64_t(mb) * BM + q * 32 + lane;
       const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(a * BN);
       const bool store = row < p.m_limit;
-      if (SWIGLU) {
+      if (MODE == kInt8) {
+        int32_t* out = reinterpret_cast<int32_t*>(p.D) + row * p.ldd + nb * BN;
+        const int cols = p.n_out - nb * BN < BN ? p.n_out - nb * BN : BN;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(tbase + c, v);
+          if (store && c < cols) {
+            if (c + 32 <= cols) {
+              int4* o4 = reinterpret_cast<int4*>(out + c);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                o4[i] = make_int4(__float_as_int(v[4 * i]), __float_as_int(v[4 * i + 1]),
+                                  __float_as_int(v[4 * i + 2]), __float_as_int(v[4 * i + 3]));
+            } else {
+              for (int i = 0; i < cols - c; ++i) out[c + i] = __float_as_int(v[i]);
+            }
+          }
+        }
+      } else if (SWIGLU) {
         uint16_t* out = p.D + row * p.ldd + nb * 128;
 #pragma unroll 1
         for (int c = 0; c < 128; c += 32) {
@@ -322,44 +363,62 @@ EncodeTiled encoder() {
   return fn;
 }
 
-int g_num_sms = 0;
 
 }  // namespace
 
-CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int box_rows) {
+CUtensorMap make_tmap_2d(const void* base, int64_t rows, int64_t cols, int box_rows, bool int8) {
   CUtensorMap m;
+  const int esz = int8 ? 1 : 2;
   const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
-  const cuuint64_t strides[1] = {cuuint64_t(cols) * 2};
-  const cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(box_rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(cols) * esz};
+  const cuuint32_t box[2] = {cuuint32_t(128 / esz), cuuint32_t(box_rows)};  // 128-byte rows
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
-                               dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUresult r = encoder()(&m, int8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                               2, const_cast<void*>(base), dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
   return m;
 }
 
-void launch_grouped_gemm(bool swiglu, const CUtensorMap& a, const CUtensorMap& a2,
+CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int box_rows) {
+  return make_tmap_2d(base, rows, cols, box_rows, false);
+}
+
+CUtensorMap make_tmap_i8(const void* base, int64_t rows, int64_t cols, int box_rows) {
+  return make_tmap_2d(base, rows, cols, box_rows, true);
+}
+
+void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
                          const CUtensorMap& b0, const CUtensorMap& b1, const GemmArgs& args,
                          int max_tiles, cudaStream_t st) {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(grouped_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_BYTES);
-    cudaFuncSetAttribute(grouped_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_BYTES);
-  });
+  static std::mutex mu;
+  static uint64_t configured = 0;  // bit per device: smem attribute set
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!((configured >> dev) & 1)) {
+      cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+      cudaFuncSetAttribute(grouped_gemm_kernel<kSwiGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           SMEM_BYTES);
+      cudaFuncSetAttribute(grouped_gemm_kernel<kPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           SMEM_BYTES);
+      cudaFuncSetAttribute(grouped_gemm_kernel<kInt8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           SMEM_BYTES);
+      configured |= uint64_t(1) << dev;
+    }
+  }
   if (max_tiles <= 0) return;
-  const int grid = max_tiles < g_num_sms ? max_tiles : g_num_sms;
-  if (swiglu)
-    grouped_gemm_kernel<true><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+  const int grid = max_tiles < sms[dev] ? max_tiles : sms[dev];
+  if (mode == kSwiGLU)
+    grouped_gemm_kernel<kSwiGLU><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+  else if (mode == kPlain)
+    grouped_gemm_kernel<kPlain><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
   else
-    grouped_gemm_kernel<false><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+    grouped_gemm_kernel<kInt8><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
 }
 
 }  // namespace dwdp

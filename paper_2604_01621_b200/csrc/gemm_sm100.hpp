@@ -16,7 +16,7 @@ struct GemmArgs {
   const int32_t* mblock_expert; // [m-blocks] expert of each 128-row block
   const int32_t* slot_of;       // [E + 1] expert -> arena slot
   const int32_t* meta;          // {total m-blocks, routed m-blocks, routed rows, T}
-  uint16_t* D;                  // bf16 output, row-major
+  uint16_t* D;                  // bf16 output (int32 in GEMM_INT8 mode), row-major
   int64_t ldd;                  // elements per output row
   int64_t m_limit;              // rows >= m_limit are not stored
   int shared_a2;                // shared-expert blocks read A from `a2` (GEMM1)
@@ -25,10 +25,14 @@ struct GemmArgs {
 // 2-D bf16 TMA map over a row-major [rows][cols] matrix, box = 64 x box_rows,
 // SWIZZLE_128B (the UMMA K-major operand layout).
 CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int box_rows);
+// Same for an int8 matrix (box = 128 x box_rows).
+CUtensorMap make_tmap_i8(const void* base, int64_t rows, int64_t cols, int box_rows);
+
+constexpr int GEMM_SWIGLU = 0, GEMM_PLAIN = 1, GEMM_INT8 = 2;
 
 // a: routed A rows (permuted tokens or H); a2: shared-expert A rows (x);
 // b0: gate (SwiGLU) or down arena; b1: up arena (SwiGLU only).
-void launch_grouped_gemm(bool swiglu, const CUtensorMap& a, const CUtensorMap& a2,
+void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
                          const CUtensorMap& b0, const CUtensorMap& b1, const GemmArgs& args,
                          int max_tiles, cudaStream_t st);
 

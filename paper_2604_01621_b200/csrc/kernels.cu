@@ -187,8 +187,24 @@ __device__ __forceinline__ void warp_best(float& v, int& i) {
 constexpr int TOPK_MAXV = 16;  // E <= 512
 constexpr int TOPK_MAXK = 16;
 
-__global__ void __launch_bounds__(256) topk_kernel(const float* __restrict__ logits,
+// Exact logit from the 9 digit-plane products: Z = sum_{a,b} 2^{8(a+b)} C_ab
+// (int64, exact), rounded once to fp32, scaled by the row exponents.
+__device__ __forceinline__ float exact_logit(const int32_t* __restrict__ C, int64_t T, int E,
+                                             int64_t t, int e, int sx) {
+  long long z = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      z += static_cast<long long>(C[(a * T + t) * (3 * E) + b * E + e]) * (1LL << (8 * (a + b)));
+  return ldexpf(__ll2float_rn(z), sx);
+}
+
+__global__ void __launch_bounds__(256) topk_kernel(const int32_t* __restrict__ C,
+                                                   const int32_t* __restrict__ ex,
+                                                   const int32_t* __restrict__ ew,
                                                    const float* __restrict__ bias,
+                                                   float* __restrict__ logits,
                                                    int32_t* __restrict__ idx_out,
                                                    float* __restrict__ wts_out, int64_t T,
                                                    RouterCfg c) {
@@ -199,12 +215,14 @@ __global__ void __launch_bounds__(256) topk_kernel(const float* __restrict__ log
   const int V = (E + 31) >> 5;
   const float NEG = __int_as_float(0xff800000);
   float lg[TOPK_MAXV], sc[TOPK_MAXV], ch[TOPK_MAXV];
-  const float* row = logits + t * E;
+  float* row = logits + t * E;
+  const int xe = ex[t];
 #pragma unroll
   for (int v = 0; v < TOPK_MAXV; ++v) {
     const int e = lane + 32 * v;
     if (v < V && e < E) {
-      lg[v] = row[e];
+      lg[v] = exact_logit(C, T, E, t, e, xe + ew[e] - 296);
+      row[e] = lg[v];
       if (c.scoring == 1) {
         sc[v] = __fdiv_rn(1.0f, __fadd_rn(1.0f, det_expf(-lg[v])));
         ch[v] = __fadd_rn(sc[v], bias ? bias[e] : 0.0f);
@@ -297,6 +315,7 @@ __global__ void __launch_bounds__(256) topk_kernel(const float* __restrict__ log
       if (v == (e >> 5)) mine = (c.scoring == 1) ? sc[v] : lg[v];
     wv[j] = __shfl_sync(0xffffffffu, mine, e & 31);
   }
+  __syncwarp();  // logits row written by all lanes is read by lane 0 below
   if (lane != 0) return;
   if (c.scoring == 1) {
     if (c.norm_topk) {
@@ -320,6 +339,77 @@ __global__ void __launch_bounds__(256) topk_kernel(const float* __restrict__ log
     idx_out[t * c.k + j] = sel[j];
     wts_out[t * c.k + j] = __fmul_rn(wv[j], c.routed_scale);
   }
+}
+
+// ---------------------------------------------------------------- router quant
+// bf16 bits -> (mantissa incl. implicit bit, exponent field clamped to >= 1)
+__device__ __forceinline__ void bf16_fields(uint32_t b, int& mant, int& eb) {
+  const int E = int((b >> 7) & 0xFFu), M = int(b & 0x7Fu);
+  mant = E ? (M | 0x80) : M;
+  eb = E ? E : 1;
+}
+
+__device__ __forceinline__ int fixed22(uint32_t b, int emax) {
+  int mant, eb;
+  bf16_fields(b, mant, eb);
+  const int sh = eb - emax + 14;
+  int q = sh >= 0 ? (mant << sh) : (sh > -8 ? (mant >> -sh) : 0);
+  return (b & 0x8000u) ? -q : q;
+}
+
+// One warp per row: pass 1 finds the row exponent, pass 2 writes the three
+// balanced int8 digit planes (Q = d0 + 256 d1 + 65536 d2, |Q| < 2^22).
+__global__ void __launch_bounds__(256) router_quant_kernel(const uint16_t* __restrict__ src,
+                                                           int64_t R, int64_t K,
+                                                           int8_t* __restrict__ dst,
+                                                           int32_t* __restrict__ emax,
+                                                           int32_t* __restrict__ meta) {
+  if (meta && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int mb = int((3 * R + 127) / 128);
+    meta[0] = mb;
+    meta[1] = mb;
+    meta[2] = 0;
+    meta[3] = 0;
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t r = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= R) return;
+  const uint4* row = reinterpret_cast<const uint4*>(src + r * K);
+  const int64_t nch = K / 8;
+  int m = 0;
+  for (int64_t c = lane; c < nch; c += 32) {
+    const uint4 v = __ldg(row + c);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      int mant, eb;
+      bf16_fields((w[q >> 1] >> (16 * (q & 1))) & 0xFFFFu, mant, eb);
+      if (mant && eb > m) m = eb;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (m == 0) m = 1;
+  for (int64_t c = lane; c < nch; c += 32) {
+    const uint4 v = __ldg(row + c);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t p0[2] = {0, 0}, p1[2] = {0, 0}, p2[2] = {0, 0};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int Q = fixed22((w[q >> 1] >> (16 * (q & 1))) & 0xFFFFu, m);
+      const int d0 = int(int8_t(uint8_t(Q & 0xFF)));
+      const int Q1 = (Q - d0) >> 8;
+      const int d1 = int(int8_t(uint8_t(Q1 & 0xFF)));
+      const int d2 = (Q1 - d1) >> 8;
+      p0[q >> 2] |= uint32_t(uint8_t(d0)) << (8 * (q & 3));
+      p1[q >> 2] |= uint32_t(uint8_t(d1)) << (8 * (q & 3));
+      p2[q >> 2] |= uint32_t(uint8_t(d2)) << (8 * (q & 3));
+    }
+    *reinterpret_cast<uint2*>(dst + (0 * R + r) * K + c * 8) = make_uint2(p0[0], p0[1]);
+    *reinterpret_cast<uint2*>(dst + (1 * R + r) * K + c * 8) = make_uint2(p1[0], p1[1]);
+    *reinterpret_cast<uint2*>(dst + (2 * R + r) * K + c * 8) = make_uint2(p2[0], p2[1]);
+  }
+  if (lane == 0) emax[r] = m;
 }
 
 // ---------------------------------------------------------------- permute
@@ -558,10 +648,17 @@ void launch_router_logits(const uint16_t* x, const uint16_t* w, float* logits, i
   router_logits_kernel<<<grid, 256, 0, st>>>(x, w, logits, T, E, K);
 }
 
-void launch_topk(const float* logits, const float* bias, int32_t* idx, float* wts, int64_t T,
-                 const RouterCfg& c, cudaStream_t st) {
+void launch_topk(const int32_t* C, const int32_t* ex, const int32_t* ew, const float* bias,
+                 float* logits, int32_t* idx, float* wts, int64_t T, const RouterCfg& c,
+                 cudaStream_t st) {
   if (T <= 0) return;
-  topk_kernel<<<unsigned((T + 7) / 8), 256, 0, st>>>(logits, bias, idx, wts, T, c);
+  topk_kernel<<<unsigned((T + 7) / 8), 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
+}
+
+void launch_router_quant(const uint16_t* src, int64_t R, int64_t K, int8_t* dst, int32_t* emax,
+                         int32_t* meta, cudaStream_t st) {
+  if (R <= 0) return;
+  router_quant_kernel<<<unsigned((R + 7) / 8), 256, 0, st>>>(src, R, K, dst, emax, meta);
 }
 
 int64_t permute_scratch_ints(int64_t T, int E) {

@@ -20,12 +20,25 @@ void launch_fill(uint16_t* dst, int64_t n, uint64_t seed, float scale, cudaStrea
 void launch_fill_f32(float* dst, int64_t n, uint64_t seed, float scale, cudaStream_t st);
 
 // logits[T][E] = sum_i x[t][i] * w[e][i], fp32 fused multiply-adds in
-// ascending i (bit-exact contract with the oracle).
+// ascending i (SIMT reference kernel, kept for microbenchmarks).
 void launch_router_logits(const uint16_t* x, const uint16_t* w, float* logits, int64_t T,
                           int E, int64_t K, cudaStream_t st);
-// Scoring + group-limited top-k + weights; idx/wts [T][k].
-void launch_topk(const float* logits, const float* bias, int32_t* idx, float* wts, int64_t T,
-                 const RouterCfg& c, cudaStream_t st);
+
+// Exact router (the production path). Each bf16 row is mapped to 22-bit
+// fixed point relative to its largest exponent (Q_i = mant_i << (e_i - emax +
+// 14), truncated below the grid) and split into three balanced int8 digit
+// planes dst[p][r][k] (Q = d0 + 2^8 d1 + 2^16 d2); emax[r] is the row
+// exponent. The logits are then the int8 tensor-core products of the planes,
+// recombined exactly in int64 and rounded once: bit-identical to the oracle.
+// If meta != nullptr, writes the single-group GEMM table {mb, mb, 0, 0} for
+// 3R rows.
+void launch_router_quant(const uint16_t* src, int64_t R, int64_t K, int8_t* dst, int32_t* emax,
+                         int32_t* meta, cudaStream_t st);
+// Scoring + group-limited top-k + weights; idx/wts [T][k]. Logits come from
+// the 9 int32 digit-plane products C[3T][3E] and the row exponents.
+void launch_topk(const int32_t* C, const int32_t* ex, const int32_t* ew, const float* bias,
+                 float* logits, int32_t* idx, float* wts, int64_t T, const RouterCfg& c,
+                 cudaStream_t st);
 
 // Stable expert-major permutation + gather of x rows.
 //  counts[E]            tokens per expert

@@ -117,6 +117,17 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
       dalloc(size_t(permute_scratch_ints(max_tokens_, E_)) * 4, &workspace_bytes));
   xperm_ = static_cast<uint16_t*>(dalloc(size_t(max_rows_) * h_ * 2, &workspace_bytes));
   hbuf_ = static_cast<uint16_t*>(dalloc(size_t(max_rows_) * f_ * 2, &workspace_bytes));
+  router_wq_ = static_cast<int8_t*>(dalloc(size_t(WL_) * 3 * E_ * h_, &weight_bytes));
+  router_we_ = static_cast<int32_t*>(dalloc(size_t(WL_) * E_ * 4, &weight_bytes));
+  for (int wl = 0; wl < WL_; ++wl)
+    tm_rw_.push_back(make_tmap_i8(router_wq_ + size_t(wl) * 3 * E_ * h_, 3 * int64_t(E_), h_, 256));
+  xq_ = static_cast<int8_t*>(dalloc(size_t(max_tokens_) * 3 * h_, &workspace_bytes));
+  xe_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * 4, &workspace_bytes));
+  rC_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * 9 * E_ * 4, &workspace_bytes));
+  rmeta_ = static_cast<int32_t*>(dalloc(16, &workspace_bytes));
+  const size_t nz = size_t((3 * max_tokens_ + 127) / 128 + 8);
+  zeros_ = static_cast<int32_t*>(dalloc(nz * 4, &workspace_bytes));
+  DWDP_CUDA(cudaMemset(zeros_, 0, nz * 4));
 
   tm_gate_ = make_tmap_bf16(arena_[0], int64_t(nslots_) * f_, h_, 128);
   tm_up_ = make_tmap_bf16(arena_[1], int64_t(nslots_) * f_, h_, 128);
@@ -155,7 +166,8 @@ Ctx::~Ctx() {
   if (meta_ring_) cudaFreeHost(meta_ring_);
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   void* bufs[] = {arena_[0], arena_[1], arena_[2], router_w_, bias_, slot_tab_, logits_, idx_,
-                  wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_};
+                  wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_,
+                  router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (auto& ev : moe_done_)
@@ -357,7 +369,9 @@ void Ctx::init_weights(float bias_scale) {
                 sh, nullptr);
     if (bias_scale != 0.0f)
       launch_fill_f32(bias_ + size_t(wl) * E_, E_, tensor_seed(base, wl, E_ + 1, 1), bias_scale, nullptr);
-    launches += 2;
+    launch_router_quant(router_w_ + size_t(wl) * E_ * h_, E_, h_, router_wq_ + size_t(wl) * 3 * E_ * h_,
+                        router_we_ + size_t(wl) * E_, nullptr, nullptr);
+    launches += 3;
   }
   DWDP_CUDA(cudaGetLastError());
   DWDP_CUDA(cudaDeviceSynchronize());
@@ -468,6 +482,21 @@ void Ctx::prefetch_times(int64_t h, int64_t* s, int64_t* e, double* bytes) {
 // ===================================================================== //
 // MoE forward
 
+// Exact router: digit planes of x (quant kernel), int8 tensor-core products
+// against the weight planes, exact recombination + scoring + top-k.
+void Ctx::route_logits(int wl, const uint16_t* x, int64_t T, cudaStream_t st) {
+  launch_router_quant(x, T, h_, xq_, xe_, rmeta_, st);
+  const CUtensorMap tx = make_tmap_i8(xq_, 3 * T, h_, 128);
+  GemmArgs ga{int(h_), 3 * E_, 0, -1, zeros_, zeros_, rmeta_,
+              reinterpret_cast<uint16_t*>(rC_), 3 * int64_t(E_), 3 * T, 0};
+  const int64_t tiles = (3 * T + 127) / 128 * ((3 * E_ + 255) / 256);
+  launch_grouped_gemm(GEMM_INT8, tx, tx, tm_rw_[size_t(wl)], tm_rw_[size_t(wl)], ga,
+                      int(std::min<int64_t>(tiles, 1 << 30)), st);
+  RouterCfg rc{E_, k_, cfg.scoring, cfg.n_group, cfg.topk_group, cfg.norm_topk, cfg.routed_scale};
+  launch_topk(rC_, xe_, router_we_ + size_t(wl) * E_, bias_ + size_t(wl) * E_, logits_, idx_, wts_,
+              T, rc, st);
+}
+
 void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint16_t* y,
                       const uint16_t* resid, cudaStream_t st, LayerRec* rec) {
   require(layer >= 0 && layer < L_, "moe_forward: layer out of range");
@@ -480,9 +509,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     DWDP_CUDA(cudaEventRecord(rec->k[i], st));
   };
   const int wl = layer % WL_;
-  RouterCfg rc{E_, k_, cfg.scoring, cfg.n_group, cfg.topk_group, cfg.norm_topk, cfg.routed_scale};
-  launch_router_logits(x, router_w_ + size_t(wl) * E_ * h_, logits_, T, E_, h_, st);
-  launch_topk(logits_, bias_ + size_t(wl) * E_, idx_, wts_, T, rc, st);
+  route_logits(wl, x, T, st);
   mark(0);
   launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, meta_, xperm_,
                  scratch_, st);
@@ -491,10 +518,10 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   const CUtensorMap tm_x = shared_ ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
   const int32_t* stab = slot_tab_ + (size_t(layer) * 2 + size_t(parity)) * (E_ + 1);
   GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1};
-  launch_grouped_gemm(true, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
+  launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(2);
   GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0};
-  launch_grouped_gemm(false, tm_h_, tm_h_, tm_down_, tm_down_, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
+  launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tm_down_, tm_down_, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
   mark(3);
   launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
   launches += 8;
@@ -553,9 +580,7 @@ void Ctx::route(int layer, const uint16_t* x, int64_t T, int32_t* idx, float* wt
   DeviceGuard dg(cfg.device);
   require(T >= 1 && T <= max_tokens_, "route: T out of range");
   const int wl = layer % WL_;
-  RouterCfg rc{E_, k_, cfg.scoring, cfg.n_group, cfg.topk_group, cfg.norm_topk, cfg.routed_scale};
-  launch_router_logits(x, router_w_ + size_t(wl) * E_ * h_, logits_, T, E_, h_, st);
-  launch_topk(logits_, bias_ + size_t(wl) * E_, idx_, wts_, T, rc, st);
+  route_logits(wl, x, T, st);
   launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, meta_, xperm_,
                  scratch_, st);
   launches += 5;
@@ -633,7 +658,7 @@ void Ctx::gemm_bf16(const uint16_t* A, const uint16_t* B, uint16_t* D, int64_t M
   const CUtensorMap ta = make_tmap_bf16(A, M, K, 128);
   const CUtensorMap tb = make_tmap_bf16(B, N, K, 256);
   GemmArgs a{int(K), int(N), int(N), 1, tabs, tabs + mb, tabs + mb + 4, D, N, M, 0};
-  launch_grouped_gemm(false, ta, ta, tb, tb, a, int(mb * (N / 256)), st);
+  launch_grouped_gemm(GEMM_PLAIN, ta, ta, tb, tb, a, int(mb * (N / 256)), st);
   ++launches;
   DWDP_CUDA(cudaGetLastError());
   DWDP_CUDA(cudaStreamSynchronize(st));

@@ -121,6 +121,16 @@ class Ctx {
   std::vector<void*> ipc_opened_;
   uint16_t* router_w_ = nullptr;       // [WL][E][h]
   float* bias_ = nullptr;              // [WL][E]
+  // exact int8 router: weight digit planes [WL][3][E][h] + row exponents
+  int8_t* router_wq_ = nullptr;
+  int32_t* router_we_ = nullptr;
+  std::vector<CUtensorMap> tm_rw_;
+  int8_t* xq_ = nullptr;               // activation digit planes [3][T][h]
+  int32_t* xe_ = nullptr;              // activation row exponents [T]
+  int32_t* rC_ = nullptr;              // int32 plane products [3T][3E]
+  int32_t* rmeta_ = nullptr;           // single-group GEMM table
+  int32_t* zeros_ = nullptr;
+  void route_logits(int wl, const uint16_t* x, int64_t T, cudaStream_t st);
   int32_t* slot_tab_ = nullptr;        // [L][2][E+1]
   // workspace
   int64_t max_tokens_ = 0, max_rows_ = 0, max_mb_ = 0;
