@@ -159,6 +159,7 @@ def main():
     ap.add_argument("--no-tdm", action="store_true")
     ap.add_argument("--merged", action="store_true", help="merge_elim off (D2D merge baseline)")
     ap.add_argument("--pull-ctas", type=int, default=16)
+    ap.add_argument("--ce-inflight", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dep", action="store_true", help="skip the same-box DEP baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -206,6 +207,7 @@ def main():
                        engine=D.ENGINE_PULL if args.engine == "pull" else D.ENGINE_COPY,
                        tdm=0 if args.no_tdm else 1, slice_size=args.slice_size,
                        merge_elim=0 if args.merged else 1, pull_ctas=args.pull_ctas,
+                       ce_inflight=args.ce_inflight,
                        weight_layers=layers if world > 1 else 1, kernel_timing=1,
                        max_tokens=args.tokens)
     ctx = D.DwdpContext(cfg)

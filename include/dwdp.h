@@ -235,6 +235,9 @@ typedef struct {
   uint64_t slice_size;
   int32_t engine;         /* DWDP_ENGINE_*                                 */
   int32_t pull_ctas;      /* CTAs of the pull kernel                       */
+  int32_t ce_inflight;    /* copy-engine transfers in flight per plan
+                             (GpuSpec::ce_inflight, hwmodel.hpp:33)       */
+  int32_t reserved0;
   /* synthetic weights */
   uint64_t weight_seed;
   int32_t weight_layers;  /* distinct weight sets; layer l uses l % this   */

@@ -69,7 +69,8 @@ class CtxConfigC(C.Structure):
                 ("topk_group", i32), ("norm_topk", i32), ("routed_scale", f32), ("rank", i32),
                 ("group_size", i32), ("extra_redundancy", i32), ("device", i32),
                 ("merge_elim", i32), ("tdm", i32), ("slice_size", u64), ("engine", i32),
-                ("pull_ctas", i32), ("weight_seed", u64), ("weight_layers", i32),
+                ("pull_ctas", i32), ("ce_inflight", i32), ("reserved0", i32),
+                ("weight_seed", u64), ("weight_layers", i32),
                 ("kernel_timing", i32), ("max_tokens", i64)]
 
 

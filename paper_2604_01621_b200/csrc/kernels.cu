@@ -163,7 +163,9 @@ __device__ __forceinline__ float det_expf(float x) {
   p = __fmaf_rn(p, r, 0.5f);
   p = __fmaf_rn(p, r, 1.0f);
   p = __fmaf_rn(p, r, 1.0f);
-  return ldexpf(p, int(n));
+  // n in [-126, 127] and p in (0.7, 1.42): one correctly rounded multiply by
+  // the exact power of two equals ldexpf(p, n) (the oracle's formulation).
+  return __fmul_rn(p, __int_as_float((int(n) + 127) << 23));
 }
 
 __device__ __forceinline__ bool better(float a, int ia, float b, int ib) {
@@ -197,7 +199,9 @@ __device__ __forceinline__ float exact_logit(const int32_t* __restrict__ C, int6
 #pragma unroll
     for (int b = 0; b < 3; ++b)
       z += static_cast<long long>(C[(a * T + t) * (3 * E) + b * E + e]) * (1LL << (8 * (a + b)));
-  return ldexpf(__ll2float_rn(z), sx);
+  const float f = __ll2float_rn(z);
+  // exact power-of-two scaling == ldexpf whenever 2^sx is a normal float
+  return (sx >= -126 && sx <= 127) ? __fmul_rn(f, __int_as_float((sx + 127) << 23)) : ldexpf(f, sx);
 }
 
 __global__ void __launch_bounds__(256) topk_kernel(const int32_t* __restrict__ C,

@@ -136,6 +136,16 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   tm_h_ = make_tmap_bf16(hbuf_, max_rows_, f_, 128);
 
   DWDP_CUDA(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
+  for (int i = 1; i < std::max(1, c.ce_inflight); ++i) {
+    cudaStream_t s;
+    cudaEvent_t a, b;
+    DWDP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    DWDP_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    DWDP_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    ce_st_.push_back(s);
+    ce_fork_.push_back(a);
+    ce_join_.push_back(b);
+  }
   DWDP_CUDA(cudaEventCreate(&epoch_));
   DWDP_CUDA(cudaEventRecord(epoch_, copy_st_));
   for (auto& ev : moe_done_) DWDP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -174,6 +184,11 @@ Ctx::~Ctx() {
     if (ev) cudaEventDestroy(ev);
   if (epoch_) cudaEventDestroy(epoch_);
   if (copy_st_) cudaStreamDestroy(copy_st_);
+  for (size_t i = 0; i < ce_st_.size(); ++i) {
+    cudaStreamDestroy(ce_st_[i]);
+    cudaEventDestroy(ce_fork_[i]);
+    cudaEventDestroy(ce_join_[i]);
+  }
 }
 
 void* Ctx::dalloc(size_t bytes, uint64_t* account) {
@@ -433,13 +448,27 @@ int64_t Ctx::prefetch_issue(int64_t g) {
     ++launches;
     DWDP_CUDA(cudaGetLastError());
   } else {
+    // ce_inflight copy streams: slice i of the TDM plan goes to stream
+    // i mod ce_inflight, so consecutive slices (different peers in the plan's
+    // rotation) are in flight together (CopyEngineSim admit, simcore.cpp:134-161).
+    const size_t ns = ce_st_.size() + 1;
+    for (size_t i = 0; i + 1 < ns; ++i) {
+      DWDP_CUDA(cudaEventRecord(ce_fork_[i], copy_st_));
+      DWDP_CUDA(cudaStreamWaitEvent(ce_st_[i], ce_fork_[i], 0));
+    }
     std::map<std::pair<int, uint64_t>, const ShardRun*> by_shard;
     for (const auto& r : runs_) by_shard[{r.peer, r.param_id}] = &r;
-    for (const Slice& s : plan_slices_) {
+    for (size_t i = 0; i < plan_slices_.size(); ++i) {
+      const Slice& s = plan_slices_[i];
       const ShardRun* r = by_shard.at({s.src_rank, s.param_id});
+      const cudaStream_t cs = (i % ns) == 0 ? copy_st_ : ce_st_[i % ns - 1];
       DWDP_CUDA(cudaMemcpyAsync(dst_addr(r->tensor, par, *r, s.dst_offset),
                                 peer_src(r->peer, r->tensor, wl, s.src_offset), s.length,
-                                cudaMemcpyDeviceToDevice, copy_st_));
+                                cudaMemcpyDeviceToDevice, cs));
+    }
+    for (size_t i = 0; i + 1 < ns; ++i) {
+      DWDP_CUDA(cudaEventRecord(ce_join_[i], ce_st_[i]));
+      DWDP_CUDA(cudaStreamWaitEvent(copy_st_, ce_join_[i], 0));
     }
   }
   DWDP_CUDA(cudaEventRecord(pl.done, copy_st_));

@@ -145,6 +145,8 @@ class Ctx {
   std::vector<Slice> plan_slices_;
   double plan_bytes_ = 0;
   cudaStream_t copy_st_ = nullptr;
+  std::vector<cudaStream_t> ce_st_;    // extra copy streams: ce_inflight - 1
+  std::vector<cudaEvent_t> ce_fork_, ce_join_;
   cudaEvent_t epoch_ = nullptr;
   cudaEvent_t moe_done_[2] = {nullptr, nullptr};
   bool moe_done_recorded_[2] = {false, false};

@@ -39,6 +39,8 @@ class DwdpConfig:
     slice_size: int = 1 << 20
     engine: int = ENGINE_COPY
     pull_ctas: int = 16
+    ce_inflight: int = 2      # copy-engine transfers in flight (reference GpuSpec default 2)
+    reserved0: int = 0
     weight_seed: int = 2604_01621
     weight_layers: int = 0    # 0 = num_layers
     kernel_timing: int = 0    # CUDA events between the layer's kernels
