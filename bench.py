@@ -158,7 +158,7 @@ def main():
     ap.add_argument("--slice-size", type=int, default=64 << 20)
     ap.add_argument("--no-tdm", action="store_true")
     ap.add_argument("--merged", action="store_true", help="merge_elim off (D2D merge baseline)")
-    ap.add_argument("--pull-ctas", type=int, default=16)
+    ap.add_argument("--pull-ctas", type=int, default=148)
     ap.add_argument("--ce-inflight", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dep", action="store_true", help="skip the same-box DEP baseline")

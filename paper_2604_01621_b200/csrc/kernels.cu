@@ -589,37 +589,86 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
 }
 
 // ---------------------------------------------------------------- pull
-__device__ __forceinline__ uint4 ld_nc_na(const uint4* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
+// TMA bulk pull: one elected thread per CTA streams its slices (slice i by
+// CTA i mod grid, so the slices in flight follow the TDM peer rotation) from
+// peer HBM over NVLink into a 2 x 16 KB shared-memory ring
+// (cp.async.bulk global->shared, mbarrier completion) and out to the local
+// receive buffer (cp.async.bulk shared->global, bulk-group completion). The
+// 33 KB footprint lets a pull CTA sit next to a grouped-GEMM CTA on every SM.
+constexpr int PULL_CHUNK = 8192, PULL_BUFS = 4;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// Items are claimed in plan order (item i by CTA i mod grid), so the
-// concurrently active slices follow the TDM peer rotation.
-__global__ void __launch_bounds__(1024) pull_kernel(const PullItem* __restrict__ items, int n) {
-  constexpr int U = 4;
-  for (int it = blockIdx.x; it < n; it += gridDim.x) {
-    const PullItem w = items[it];
-    const uint4* src = reinterpret_cast<const uint4*>(w.src);
-    uint4* dst = reinterpret_cast<uint4*>(w.dst);
-    const int64_t nv = int64_t(w.len / 16);
-    const int64_t step = int64_t(blockDim.x) * U;
-    int64_t i = threadIdx.x;
-    for (; i + (U - 1) * blockDim.x < nv; i += step) {
-      uint4 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = ld_nc_na(src + i + u * blockDim.x);
-#pragma unroll
-      for (int u = 0; u < U; ++u) __stcs(dst + i + u * blockDim.x, v[u]);
+struct PullCursor {  // walks this CTA's chunks: items blockIdx.x + j*gridDim.x
+  int it;
+  uint64_t off;
+  __device__ void advance(const PullItem* items) {
+    off += PULL_CHUNK;
+    if (off >= items[it].len) {
+      it += gridDim.x;
+      off = 0;
     }
-    for (; i < nv; i += blockDim.x) __stcs(dst + i, ld_nc_na(src + i));
-    const int64_t tail0 = nv * 16;
-    for (int64_t b = tail0 + threadIdx.x; b < int64_t(w.len); b += blockDim.x)
-      static_cast<uint8_t*>(w.dst)[b] = static_cast<const uint8_t*>(w.src)[b];
   }
+};
+
+__global__ void __launch_bounds__(32) tma_pull_kernel(const PullItem* __restrict__ items, int n) {
+  __shared__ __align__(128) uint8_t buf[PULL_BUFS][PULL_CHUNK];
+  __shared__ __align__(8) uint64_t bar[PULL_BUFS];
+  if (threadIdx.x != 0) return;
+  for (int b = 0; b < PULL_BUFS; ++b)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[b])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  uint32_t phase = 0;  // bit b: parity of buffer b's next completion
+  auto load = [&](int b, const PullCursor& c) {
+    const PullItem& w = items[c.it];
+    const uint32_t len = uint32_t(w.len - c.off < PULL_CHUNK ? w.len - c.off : PULL_CHUNK);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar[b])),
+                 "r"(len)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(buf[b])),
+        "l"(static_cast<const uint8_t*>(w.src) + c.off), "r"(len), "r"(smem_addr(&bar[b]))
+        : "memory");
+  };
+  PullCursor prod{int(blockIdx.x), 0}, cons = prod;
+  int issued = 0, done = 0;
+  while (issued < PULL_BUFS && prod.it < n) {  // prologue: fill the ring
+    load(issued, prod);
+    prod.advance(items);
+    ++issued;
+  }
+  while (done < issued) {
+    const int b = done % PULL_BUFS;
+    uint32_t ok = 0;
+    do {
+      asm volatile(
+          "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+          "selp.u32 %0, 1, 0, p;\n}"
+          : "=r"(ok)
+          : "r"(smem_addr(&bar[b])), "r"((phase >> b) & 1u)
+          : "memory");
+    } while (!ok);
+    phase ^= 1u << b;
+    const PullItem& w = items[cons.it];
+    const uint32_t len = uint32_t(w.len - cons.off < PULL_CHUNK ? w.len - cons.off : PULL_CHUNK);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                     static_cast<uint8_t*>(w.dst) + cons.off),
+                 "r"(smem_addr(buf[b])), "r"(len)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    cons.advance(items);
+    ++done;
+    if (prod.it < n) {  // refill buffer b once its store has read shared memory
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      load(b, prod);
+      prod.advance(items);
+      ++issued;
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 int grid_for(int64_t work, int block) {
@@ -693,7 +742,7 @@ void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
 }
 
 void launch_pull(const PullItem* items, int n, int ctas, cudaStream_t st) {
-  if (n > 0) pull_kernel<<<ctas, 1024, 0, st>>>(items, n);
+  if (n > 0) tma_pull_kernel<<<ctas, 32, 0, st>>>(items, n);
 }
 
 }  // namespace dwdp

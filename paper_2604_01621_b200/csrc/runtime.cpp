@@ -70,6 +70,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   require(c.max_tokens >= 1, "ctx: max_tokens must be >= 1");
   require(c.engine == DWDP_ENGINE_COPY || c.engine == DWDP_ENGINE_PULL, "ctx: unknown engine");
   require(!c.tdm || c.slice_size > 0, "dwdp.slice_size must be > 0 with tdm");
+  require(!c.tdm || c.slice_size % 16 == 0, "dwdp.slice_size must be a multiple of 16 bytes");
   DeviceGuard dg(c.device);
   int cc = 0;
   cudaDeviceProp prop;
@@ -444,7 +445,7 @@ int64_t Ctx::prefetch_issue(int64_t g) {
     require(pull_items_ != nullptr, "prefetch_issue: pull lists not built (peers not wired)");
     const size_t n = plan_slices_.size();
     launch_pull(pull_items_ + (size_t(wl) * 2 + size_t(par)) * n, int(n),
-                cfg.pull_ctas > 0 ? cfg.pull_ctas : 16, copy_st_);
+                cfg.pull_ctas > 0 ? cfg.pull_ctas : num_sms_, copy_st_);
     ++launches;
     DWDP_CUDA(cudaGetLastError());
   } else {

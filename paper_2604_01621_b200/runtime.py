@@ -38,7 +38,7 @@ class DwdpConfig:
     tdm: int = 1
     slice_size: int = 1 << 20
     engine: int = ENGINE_COPY
-    pull_ctas: int = 16
+    pull_ctas: int = 148      # pull-kernel CTAs (one per SM, co-resident with the GEMM)
     ce_inflight: int = 2      # copy-engine transfers in flight (reference GpuSpec default 2)
     reserved0: int = 0
     weight_seed: int = 2604_01621
