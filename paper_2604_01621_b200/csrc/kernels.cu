@@ -654,10 +654,14 @@ __global__ void __launch_bounds__(32) tma_pull_kernel(const PullItem* __restrict
     phase ^= 1u << b;
     const PullItem& w = items[cons.it];
     const uint32_t len = uint32_t(w.len - cons.off < PULL_CHUNK ? w.len - cons.off : PULL_CHUNK);
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-                     static_cast<uint8_t*>(w.dst) + cons.off),
-                 "r"(smem_addr(buf[b])), "r"(len)
-                 : "memory");
+    // streamed into the receive buffer: evict-first so the 17-20 GB per layer
+    // does not push the running GEMM's expert weights out of L2
+    asm volatile(
+        "{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+        "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, pol;\n}" ::"l"(
+            static_cast<uint8_t*>(w.dst) + cons.off),
+        "r"(smem_addr(buf[b])), "r"(len)
+        : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     cons.advance(items);
     ++done;
