@@ -151,10 +151,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dwdp", choices=["dwdp", "reference"])
-    ap.add_argument("--tokens", type=int, default=32768, help="MNT tokens per rank per step")
+    ap.add_argument("--tokens", type=int, default=65536,
+                    help="MNT tokens per rank per step (65536: the DWDP break-even regime, "
+                         "SURVEY.md section 7; 32768 also reported in DESIGN.md)")
     ap.add_argument("--cv", type=float, default=0.2, help="sequence-length CV")
     ap.add_argument("--layers", type=int, default=8)
-    ap.add_argument("--engine", default="copy", choices=["copy", "pull"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "copy", "pull"],
+                    help="auto: copy engine unless its measured GB/s leaves prefetch exposed")
     ap.add_argument("--slice-size", type=int, default=64 << 20)
     ap.add_argument("--no-tdm", action="store_true")
     ap.add_argument("--merged", action="store_true", help="merge_elim off (D2D merge baseline)")
@@ -233,7 +236,24 @@ def main():
         T = toks[it][rank]
         ctx.stack_forward(x[:T], y[:T])
     torch.cuda.synchronize()
-    ctx.records()
+    wrecs = ctx.records()
+    engine = "copy" if cfg.engine == D.ENGINE_COPY else "pull"
+    if world > 1 and args.engine == "auto":
+        # choose by measured GB/s: keep the copy engine (no SM cost) while its
+        # bandwidth hides the pull under the compute window, else the TMA kernel
+        steady = [r for r in wrecs if r["prefetch_bytes"] > 0][len(wrecs) // 2:]
+        wait = sum(r["gate_wait_ns"] for r in steady)
+        moe = sum(r["moe_ns"] for r in steady)
+        if steady and wait > 0.02 * moe:
+            ctx.set_engine(D.ENGINE_PULL)
+            engine = "pull"
+            T = toks[0][rank]
+            ctx.stack_forward(x[:T], y[:T])
+            torch.cuda.synchronize()
+            ctx.records()
+    engines = [None] * world
+    if world > 1:
+        dist.all_gather_object(engines, engine)
     n0 = ctx.launch_count()
 
     barrier()
@@ -352,7 +372,7 @@ def main():
                        "tokens_per_step_rank0": [toks[it][0] for it in range(args.warmup, iters)],
                        "weights": ("one 22.5 GB set aliased by all layers (N=1)" if world == 1
                                    else f"{256 // world} owned experts/layer/GPU, {layers} layers"),
-                       "prefetch_engine": args.engine if world > 1 else None,
+                       "prefetch_engine": (engines if world > 1 else None),
                        "slice_size": args.slice_size if world > 1 else None,
                        "l2": "inputs larger than L2: 22.5 GB of expert weights per layer",
                        "parallelism": f"dwdp{world}"},

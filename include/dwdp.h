@@ -288,6 +288,10 @@ int dwdp_prefetch_wait(dwdp_ctx* ctx, dwdp_prefetch h, void* stream);
  * context's epoch event; -1 while pending. */
 int dwdp_prefetch_times(dwdp_ctx* ctx, dwdp_prefetch h, int64_t* start_ns,
                         int64_t* end_ns, double* bytes);
+/* Switch the prefetch engine for plans issued from now on (DWDP_ENGINE_*);
+ * both engines are wired at peer-open time, so the choice can follow the
+ * GB/s measured during warm-up. */
+int dwdp_ctx_set_engine(dwdp_ctx* ctx, int engine);
 /* Copy plan of this rank (dst offsets relative to per-(peer,param) buffers). */
 int dwdp_ctx_copy_plan(dwdp_ctx* ctx, dwdp_slice* out, size_t* n_inout);
 

@@ -121,6 +121,7 @@ SIGNATURES = {
     "dwdp_prefetch_query": (i32, [P, i64, C.POINTER(i32)]),
     "dwdp_prefetch_wait": (i32, [P, i64, P]),
     "dwdp_prefetch_times": (i32, [P, i64, C.POINTER(i64), C.POINTER(i64), C.POINTER(f64)]),
+    "dwdp_ctx_set_engine": (i32, [P, i32]),
     "dwdp_ctx_copy_plan": (i32, [P, P, C.POINTER(sz)]),
     "dwdp_moe_forward": (i32, [P, i32, P, i64, P, P]),
     "dwdp_layer_forward": (i32, [P, i64, P, i64, P, i32, P]),

@@ -143,6 +143,10 @@ class DwdpContext:
         check(lib().dwdp_prefetch_times(self.h, handle, C.byref(s), C.byref(e), C.byref(b)))
         return s.value, e.value, b.value
 
+    def set_engine(self, engine: int) -> None:
+        check(lib().dwdp_ctx_set_engine(self.h, engine))
+        self.cfg.engine = engine
+
     def copy_plan(self) -> list[Slice]:
         n = C.c_size_t(0)
         check(lib().dwdp_ctx_copy_plan(self.h, None, C.byref(n)))
