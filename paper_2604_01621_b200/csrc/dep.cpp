@@ -107,6 +107,8 @@ void Ctx::dep_init(const void* unique_id) {
   dep_tab_cap_ = max_mb_ * 2 + 16;
   dep_tab_ = static_cast<int32_t*>(dalloc(size_t(dep_tab_cap_) * 4, &workspace_bytes));
   DWDP_CUDA(cudaHostAlloc(&dep_tab_host_, size_t(dep_tab_cap_) * 4, 0));
+  dep_seg_ = static_cast<int2*>(dalloc(size_t(dep_tab_cap_) * sizeof(int2), &workspace_bytes));
+  DWDP_CUDA(cudaHostAlloc(&dep_seg_host_, size_t(dep_tab_cap_) * sizeof(int2), 0));
   dep_reserve(max_rows_);
 }
 
@@ -125,9 +127,13 @@ void Ctx::dep_reserve(int64_t rows) {
   if (need_tab > dep_tab_cap_) {
     cudaFree(dep_tab_);
     cudaFreeHost(dep_tab_host_);
+    cudaFree(dep_seg_);
+    cudaFreeHost(dep_seg_host_);
     dep_tab_cap_ = need_tab;
     dep_tab_ = static_cast<int32_t*>(dalloc(size_t(dep_tab_cap_) * 4, nullptr));
     DWDP_CUDA(cudaHostAlloc(&dep_tab_host_, size_t(dep_tab_cap_) * 4, 0));
+    dep_seg_ = static_cast<int2*>(dalloc(size_t(dep_tab_cap_) * sizeof(int2), nullptr));
+    DWDP_CUDA(cudaHostAlloc(&dep_seg_host_, size_t(dep_tab_cap_) * sizeof(int2), 0));
   }
 }
 
@@ -158,7 +164,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   if (T > 0) route_logits(wl, x, T, st);
   mark(&rec.k[0]);
   if (T > 0)
-    launch_permute(idx_, x, T, E_, k_, h_, 0, counts_, row_of_, mblock_, meta_, xperm_, scratch_, st);
+    launch_permute(idx_, x, T, E_, k_, h_, 0, counts_, row_of_, mblock_, mbseg_, meta_, xperm_, scratch_, st);
   else
     DWDP_CUDA(cudaMemsetAsync(counts_, 0, size_t(E_) * 4, st));
   mark(&rec.k[1]);
@@ -191,16 +197,28 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   const int64_t shared_blocks = shared_ ? (T + 127) / 128 : 0;
   dep_reserve(routed_rows + shared_blocks * 128);
   // m-block -> expert over the receive layout, then the shared expert blocks
+  // (each (source, expert) run of m-blocks is one raster segment)
   for (int s = 0; s < N_; ++s)
-    for (int e = rank_ * per; e < (rank_ + 1) * per; ++e)
-      for (int64_t b = 0; b < pad128(ca[size_t(s) * E_ + e]) / 128; ++b) dep_tab_host_[4 + nblocks++] = e;
+    for (int e = rank_ * per; e < (rank_ + 1) * per; ++e) {
+      const int2 seg = make_int2(int(nblocks), int(pad128(ca[size_t(s) * E_ + e]) / 128));
+      for (int b = 0; b < seg.y; ++b) {
+        dep_seg_host_[nblocks] = seg;
+        dep_tab_host_[4 + nblocks++] = e;
+      }
+    }
   const int64_t routed_mb = nblocks;
-  for (int64_t b = 0; b < shared_blocks; ++b) dep_tab_host_[4 + nblocks++] = E_;
+  const int2 sseg = make_int2(int(routed_mb), int(shared_blocks));
+  for (int64_t b = 0; b < shared_blocks; ++b) {
+    dep_seg_host_[nblocks] = sseg;
+    dep_tab_host_[4 + nblocks++] = E_;
+  }
   dep_tab_host_[0] = int32_t(nblocks);
   dep_tab_host_[1] = int32_t(routed_mb);
   dep_tab_host_[2] = int32_t(routed_rows);
   dep_tab_host_[3] = int32_t(T);
   DWDP_CUDA(cudaMemcpyAsync(dep_tab_, dep_tab_host_, size_t(4 + nblocks) * 4,
+                            cudaMemcpyHostToDevice, st));
+  DWDP_CUDA(cudaMemcpyAsync(dep_seg_, dep_seg_host_, size_t(nblocks + 1) * sizeof(int2),
                             cudaMemcpyHostToDevice, st));
   // 3. dispatch all-to-all
   const size_t rowel = size_t(h_);
@@ -226,12 +244,12 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   const int32_t* dmb = dep_tab_ + 4;
   if (nblocks > 0) {
     const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_dep_recv_;
-    GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1};
+    GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1, dep_seg_};
     launch_grouped_gemm(GEMM_SWIGLU, tm_dep_recv_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
   }
   mark(&rec.k[2]);
   if (nblocks > 0) {
-    GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0};
+    GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_};
     launch_grouped_gemm(GEMM_PLAIN, tm_dep_h_, tm_dep_h_, tm_down_, tm_down_, g2, int(nblocks * (h_ / 256)), st);
   }
   mark(&rec.k[3]);

@@ -145,6 +145,22 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
          (uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(b))) << 16);
 }
 
+// Linear tile id -> (m-block, n-block). Tiles of a segment (consecutive
+// m-blocks of one expert) occupy the id range [start*NB, (start+len)*NB), so
+// the segment is found from the m-block tile/NB falls in; inside it the raster
+// is n-block-major.
+__device__ __forceinline__ void tile_coords(int tile, int nb_count, const int2* __restrict__ seg,
+                                            int& mb, int& nb) {
+  mb = tile / nb_count;
+  nb = tile - mb * nb_count;
+  if (seg) {
+    const int2 s = seg[mb];
+    const int local = tile - s.x * nb_count;
+    nb = local / s.y;
+    mb = s.x + (local - nb * s.y);
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -203,7 +219,8 @@ __global__ void __launch_bounds__(256, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int mb = tile / nb_count, nb = tile - mb * nb_count;
+        int mb, nb;
+        tile_coords(tile, nb_count, p.mb_seg, mb, nb);
         const int e = p.mblock_expert[mb];
         const bool sh = p.shared_a2 && e == p.E;
         const CUtensorMap* am = sh ? &tmA2 : &tmA;
@@ -262,7 +279,8 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-      const int mb = tile / nb_count, nb = tile - mb * nb_count;
+      int mb, nb;
+        tile_coords(tile, nb_count, p.mb_seg, mb, nb);
       const int a = local & 1;
       const uint32_t aph = (local >> 1) & 1;
       mbar_wait(&tfull[a], aph);

@@ -20,6 +20,11 @@ struct GemmArgs {
   int64_t ldd;                  // elements per output row
   int64_t m_limit;              // rows >= m_limit are not stored
   int shared_a2;                // shared-expert blocks read A from `a2` (GEMM1)
+  // Optional [m-blocks] {first m-block, m-block count} of the expert segment
+  // each m-block belongs to: tiles are then rastered n-block-major inside a
+  // segment so the concurrently running CTAs share B tiles (the expert's
+  // weights) and only the segment's A rows stay live in L2.
+  const int2* mb_seg;
 };
 
 // 2-D bf16 TMA map over a row-major [rows][cols] matrix, box = 64 x box_rows,

@@ -441,6 +441,7 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
                                                             int shared, int32_t* __restrict__ counts,
                                                             int32_t* __restrict__ expert_off,
                                                             int32_t* __restrict__ mblock_expert,
+                                                            int2* __restrict__ mb_seg,
                                                             int32_t* __restrict__ meta) {
   extern __shared__ int32_t sh[];  // [E] padded sizes, then [E] offsets
   int32_t* pad = sh;
@@ -472,12 +473,19 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
   __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     expert_off[e] = off[e];
-    for (int32_t b = off[e] / ROW_ALIGN; b < (off[e] + pad[e]) / ROW_ALIGN; ++b)
+    const int2 seg = make_int2(off[e] / ROW_ALIGN, pad[e] / ROW_ALIGN);
+    for (int32_t b = seg.x; b < seg.x + seg.y; ++b) {
       mblock_expert[b] = e;
+      mb_seg[b] = seg;
+    }
   }
   if (shared) {
     const int32_t rmb = meta[1];
-    for (int32_t b = threadIdx.x; b < meta[0] - rmb; b += blockDim.x) mblock_expert[rmb + b] = E;
+    const int2 seg = make_int2(rmb, meta[0] - rmb);
+    for (int32_t b = threadIdx.x; b < seg.y; b += blockDim.x) {
+      mblock_expert[rmb + b] = E;
+      mb_seg[rmb + b] = seg;
+    }
   }
 }
 
@@ -725,14 +733,15 @@ int64_t permute_scratch_ints(int64_t T, int E) {
 
 void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int k, int64_t h,
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
-                    int32_t* meta, uint16_t* xperm, int32_t* scratch, cudaStream_t st) {
+                    int2* mb_seg, int32_t* meta, uint16_t* xperm, int32_t* scratch,
+                    cudaStream_t st) {
   const int nch = int((T + PCH - 1) / PCH);
   int32_t* chunk_counts = scratch;
   int32_t* expert_off = scratch + int64_t(nch) * E;
   if (nch > 0)
     permute_count_kernel<<<nch, 256, E * sizeof(int32_t), st>>>(idx, T, E, k, chunk_counts);
   permute_scan_kernel<<<1, 1024, 2 * E * sizeof(int32_t), st>>>(
-      chunk_counts, nch, E, T, shared, counts, expert_off, mblock_expert, meta);
+      chunk_counts, nch, E, T, shared, counts, expert_off, mblock_expert, mb_seg, meta);
   if (nch > 0)
     permute_scatter_kernel<<<nch, 256, (E + PCH * k) * sizeof(int32_t), st>>>(
         idx, x, T, E, k, h, chunk_counts, expert_off, row_of, xperm);

@@ -113,6 +113,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   row_of_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * k_ * 4, &workspace_bytes));
   counts_ = static_cast<int32_t*>(dalloc(size_t(E_) * 4, &workspace_bytes));
   mblock_ = static_cast<int32_t*>(dalloc(size_t(max_mb_) * 4, &workspace_bytes));
+  mbseg_ = static_cast<int2*>(dalloc(size_t(max_mb_) * sizeof(int2), &workspace_bytes));
   meta_ = static_cast<int32_t*>(dalloc(16 * 4, &workspace_bytes));
   scratch_ = static_cast<int32_t*>(
       dalloc(size_t(permute_scratch_ints(max_tokens_, E_)) * 4, &workspace_bytes));
@@ -178,7 +179,8 @@ Ctx::~Ctx() {
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   void* bufs[] = {arena_[0], arena_[1], arena_[2], router_w_, bias_, slot_tab_, logits_, idx_,
                   wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_,
-                  router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_};
+                  router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_, mbseg_, dep_seg_};
+  if (dep_seg_host_) cudaFreeHost(dep_seg_host_);
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (auto& ev : moe_done_)
@@ -518,7 +520,7 @@ void Ctx::route_logits(int wl, const uint16_t* x, int64_t T, cudaStream_t st) {
   launch_router_quant(x, T, h_, xq_, xe_, rmeta_, st);
   const CUtensorMap tx = make_tmap_i8(xq_, 3 * T, h_, 128);
   GemmArgs ga{int(h_), 3 * E_, 0, -1, zeros_, zeros_, rmeta_,
-              reinterpret_cast<uint16_t*>(rC_), 3 * int64_t(E_), 3 * T, 0};
+              reinterpret_cast<uint16_t*>(rC_), 3 * int64_t(E_), 3 * T, 0, nullptr};
   const int64_t tiles = (3 * T + 127) / 128 * ((3 * E_ + 255) / 256);
   launch_grouped_gemm(GEMM_INT8, tx, tx, tm_rw_[size_t(wl)], tm_rw_[size_t(wl)], ga,
                       int(std::min<int64_t>(tiles, 1 << 30)), st);
@@ -541,16 +543,16 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   const int wl = layer % WL_;
   route_logits(wl, x, T, st);
   mark(0);
-  launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, meta_, xperm_,
+  launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, meta_, xperm_,
                  scratch_, st);
   mark(1);
   const int64_t mb_ub = (T * k_ + int64_t(E_) * 127) / 128 + 1 + (shared_ ? (T + 127) / 128 : 0);
   const CUtensorMap tm_x = shared_ ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
   const int32_t* stab = slot_tab_ + (size_t(layer) * 2 + size_t(parity)) * (E_ + 1);
-  GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1};
+  GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_};
   launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(2);
-  GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0};
+  GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_};
   launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tm_down_, tm_down_, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
   mark(3);
   launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
@@ -611,7 +613,7 @@ void Ctx::route(int layer, const uint16_t* x, int64_t T, int32_t* idx, float* wt
   require(T >= 1 && T <= max_tokens_, "route: T out of range");
   const int wl = layer % WL_;
   route_logits(wl, x, T, st);
-  launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, meta_, xperm_,
+  launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, meta_, xperm_,
                  scratch_, st);
   launches += 5;
   const size_t tk = size_t(T) * size_t(k_);
@@ -687,7 +689,7 @@ void Ctx::gemm_bf16(const uint16_t* A, const uint16_t* B, uint16_t* D, int64_t M
   DWDP_CUDA(cudaMemcpyAsync(tabs + mb + 4, meta, 16, cudaMemcpyHostToDevice, st));
   const CUtensorMap ta = make_tmap_bf16(A, M, K, 128);
   const CUtensorMap tb = make_tmap_bf16(B, N, K, 256);
-  GemmArgs a{int(K), int(N), int(N), 1, tabs, tabs + mb, tabs + mb + 4, D, N, M, 0};
+  GemmArgs a{int(K), int(N), int(N), 1, tabs, tabs + mb, tabs + mb + 4, D, N, M, 0, nullptr};
   launch_grouped_gemm(GEMM_PLAIN, ta, ta, tb, tb, a, int(mb * (N / 256)), st);
   ++launches;
   DWDP_CUDA(cudaGetLastError());

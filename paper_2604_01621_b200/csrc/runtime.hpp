@@ -138,6 +138,7 @@ class Ctx {
   int32_t *idx_ = nullptr, *counts_ = nullptr, *row_of_ = nullptr, *mblock_ = nullptr,
           *meta_ = nullptr, *scratch_ = nullptr;
   float* wts_ = nullptr;
+  int2* mbseg_ = nullptr;               // [max_mb] expert segment of each m-block
   uint16_t *xperm_ = nullptr, *hbuf_ = nullptr;
   CUtensorMap tm_gate_, tm_up_, tm_down_, tm_xperm_, tm_h_;
   // prefetch engine
@@ -170,6 +171,8 @@ class Ctx {
   int32_t* dep_counts_host_ = nullptr;   // pinned [N][E]
   int32_t* dep_tab_ = nullptr;           // device m-block table + meta
   int32_t* dep_tab_host_ = nullptr;      // pinned staging
+  int2* dep_seg_ = nullptr;              // device (source, expert) segment table
+  int2* dep_seg_host_ = nullptr;
   int64_t dep_tab_cap_ = 0;
   CUtensorMap tm_dep_recv_, tm_dep_h_;
   void dep_reserve(int64_t rows);
