@@ -164,7 +164,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   if (T > 0) route_logits(wl, x, T, st);
   mark(&rec.k[0]);
   if (T > 0)
-    launch_permute(idx_, x, T, E_, k_, h_, 0, counts_, row_of_, mblock_, mbseg_, meta_, xperm_, scratch_, st);
+    launch_permute(idx_, x, T, E_, k_, h_, 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_, xperm_, scratch_, st);
   else
     DWDP_CUDA(cudaMemsetAsync(counts_, 0, size_t(E_) * 4, st));
   mark(&rec.k[1]);

@@ -78,6 +78,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// 4 gathered rows x 64 bf16 (4 x 128 B) into consecutive smem rows.
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int col, int4 rows) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(col), "r"(rows.x), "r"(rows.y),
+      "r"(rows.z), "r"(rows.w)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -214,32 +224,40 @@ __global__ void __launch_bounds__(256, 1)
   const int num_tiles = total_mb * nb_count;
   const int kb_count = p.K / BKE;
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
-      int s = 0;
-      uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        int mb, nb;
-        tile_coords(tile, nb_count, p.mb_seg, mb, nb);
-        const int e = p.mblock_expert[mb];
-        const bool sh = p.shared_a2 && e == p.E;
-        const CUtensorMap* am = sh ? &tmA2 : &tmA;
-        const int arow = (sh ? mb - routed_mb : mb) * BM;
-        const int brow = p.slot_of[e] * p.rows_per_slot + nb * (SWIGLU ? 128 : BN);
-        for (int kb = 0; kb < kb_count; ++kb) {
+  if (warp == 0) {  // ------------------ TMA producer (lane 0; all lanes when gathering)
+    int s = 0;
+    uint32_t ph = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      int mb, nb;
+      tile_coords(tile, nb_count, p.mb_seg, mb, nb);
+      const int e = p.mblock_expert[mb];
+      const bool sh = p.shared_a2 && e == p.E;
+      const bool gather = p.a_rows != nullptr && !sh;
+      const CUtensorMap* am = sh ? &tmA2 : &tmA;
+      const int arow = (sh ? mb - routed_mb : mb) * BM;
+      const int brow = p.slot_of[e] * p.rows_per_slot + nb * (SWIGLU ? 128 : BN);
+      // gather mode: lane l owns source rows 4l..4l+3 of this m-block
+      const int4 rows4 = gather ? *reinterpret_cast<const int4*>(p.a_rows + int64_t(mb) * BM + 4 * lane)
+                                : make_int4(0, 0, 0, 0);
+      for (int kb = 0; kb < kb_count; ++kb) {
+        if (lane == 0) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], A_STAGE + B_STAGE);
-          tma_load_2d(sA + s * A_STAGE, am, &full[s], kb * BKE, arow);
+          if (!gather) tma_load_2d(sA + s * A_STAGE, am, &full[s], kb * BKE, arow);
           if (SWIGLU) {
             tma_load_2d(sB + s * B_STAGE, &tmB0, &full[s], kb * BKE, brow);
             tma_load_2d(sB + s * B_STAGE + B_STAGE / 2, &tmB1, &full[s], kb * BKE, brow);
           } else {
             tma_load_2d(sB + s * B_STAGE, &tmB0, &full[s], kb * BKE, brow);
           }
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
-          }
+        }
+        if (gather) {
+          __syncwarp();  // slot s is free (lane 0 waited on it)
+          tma_gather4(sA + s * A_STAGE + lane * 4 * 128, am, &full[s], kb * BKE, rows4);
+        }
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
         }
       }
     }

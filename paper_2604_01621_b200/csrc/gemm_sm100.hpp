@@ -25,6 +25,10 @@ struct GemmArgs {
   // segment so the concurrently running CTAs share B tiles (the expert's
   // weights) and only the segment's A rows stay live in L2.
   const int2* mb_seg;
+  // Optional [routed rows] source row of every padded expert-major row: A is
+  // then gathered straight from the token matrix (`a` must be a gather map,
+  // box 64 x 1) with TMA tile::gather4, so no permuted copy is materialised.
+  const int32_t* a_rows;
 };
 
 // 2-D bf16 TMA map over a row-major [rows][cols] matrix, box = 64 x box_rows,

@@ -241,40 +241,41 @@ __global__ void __launch_bounds__(256) topk_kernel(const int32_t* __restrict__ C
   const int G = c.n_group > 0 ? c.n_group : 1;
   if (G > 1 && c.topk_group < G) {
     const int gs = E / G;
-    uint32_t gsel = 0;  // bit g: group kept (G <= 32)
+    int grp[TOPK_MAXV];  // group of each of this lane's slots (one division per slot)
+#pragma unroll
+    for (int v = 0; v < TOPK_MAXV; ++v) {
+      const int e = lane + 32 * v;
+      grp[v] = (v < V && e < E) ? e / gs : -1;
+    }
+    uint32_t gsel = 0;        // bit g: group kept (G <= 32)
     float gscore_mine = NEG;  // lane g holds group g's score
     for (int g = 0; g < G; ++g) {
-      float b1v = NEG, b2v = NEG;
-      int b1i = 0x7fffffff, b2i = 0x7fffffff;
-      // top-1
-      float v1 = NEG;
-      int i1 = 0x7fffffff;
+      // top-2 of the group: one lane-local pass keeping the best two, then
+      // two warp reductions (the second excludes the first winner)
+      float v1 = NEG, v2 = NEG;
+      int i1 = 0x7fffffff, i2 = 0x7fffffff;
 #pragma unroll
       for (int v = 0; v < TOPK_MAXV; ++v) {
+        if (grp[v] != g) continue;
         const int e = lane + 32 * v;
-        if (v < V && e < E && e / gs == g && better(ch[v], e, v1, i1)) {
+        if (better(ch[v], e, v1, i1)) {
+          v2 = v1;
+          i2 = i1;
           v1 = ch[v];
           i1 = e;
-        }
-      }
-      warp_best(v1, i1);
-      b1v = v1;
-      b1i = i1;
-      float v2 = NEG;
-      int i2 = 0x7fffffff;
-#pragma unroll
-      for (int v = 0; v < TOPK_MAXV; ++v) {
-        const int e = lane + 32 * v;
-        if (v < V && e < E && e / gs == g && e != b1i && better(ch[v], e, v2, i2)) {
+        } else if (better(ch[v], e, v2, i2)) {
           v2 = ch[v];
           i2 = e;
         }
       }
-      warp_best(v2, i2);
-      b2v = v2;
-      b2i = i2;
-      (void)b2i;
-      const float gsc = gs >= 2 ? __fadd_rn(b1v, b2v) : b1v;
+      float w1 = v1;
+      int j1 = i1;
+      warp_best(w1, j1);
+      // runner-up: this lane's best candidate other than the winner
+      float w2 = (i1 == j1) ? v2 : v1;
+      int j2 = (i1 == j1) ? i2 : i1;
+      warp_best(w2, j2);
+      const float gsc = gs >= 2 ? __fadd_rn(w1, w2) : w1;
       if (lane == g) gscore_mine = gsc;
     }
     for (int s = 0; s < c.topk_group; ++s) {
@@ -284,10 +285,8 @@ __global__ void __launch_bounds__(256) topk_kernel(const int32_t* __restrict__ C
       gsel |= 1u << i;
     }
 #pragma unroll
-    for (int v = 0; v < TOPK_MAXV; ++v) {
-      const int e = lane + 32 * v;
-      if (v < V && e < E && !((gsel >> (e / gs)) & 1u)) ch[v] = 0.0f;  // HF masked_fill 0.0
-    }
+    for (int v = 0; v < TOPK_MAXV; ++v)
+      if (grp[v] >= 0 && !((gsel >> grp[v]) & 1u)) ch[v] = 0.0f;  // HF masked_fill 0.0
   }
   // top-k over ch, ties to the lower index
   int sel[TOPK_MAXK];
@@ -442,6 +441,7 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
                                                             int32_t* __restrict__ expert_off,
                                                             int32_t* __restrict__ mblock_expert,
                                                             int2* __restrict__ mb_seg,
+                                                            int32_t* __restrict__ src_row,
                                                             int32_t* __restrict__ meta) {
   extern __shared__ int32_t sh[];  // [E] padded sizes, then [E] offsets
   int32_t* pad = sh;
@@ -478,6 +478,8 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
       mblock_expert[b] = e;
       mb_seg[b] = seg;
     }
+    if (src_row)  // padding rows gather token 0 (computed, never read)
+      for (int32_t r = off[e] + counts[e]; r < off[e] + pad[e]; ++r) src_row[r] = 0;
   }
   if (shared) {
     const int32_t rmb = meta[1];
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
 __global__ void __launch_bounds__(256) permute_scatter_kernel(
     const int32_t* __restrict__ idx, const uint16_t* __restrict__ x, int64_t T, int E, int k,
     int64_t h, const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ expert_off,
-    int32_t* __restrict__ row_of, uint16_t* __restrict__ xperm) {
+    int32_t* __restrict__ row_of, int32_t* __restrict__ src_row, uint16_t* __restrict__ xperm) {
   extern __shared__ int32_t sm[];  // cursor[E], rows[PCH * k]
   int32_t* cursor = sm;
   int32_t* rows = sm + E;
@@ -515,6 +517,7 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
         const int pos = expert_off[e] + chunk_base[int64_t(blockIdx.x) * E + e] + before + rank;
         rows[pl] = pos;
         row_of[t0 * k + pl] = pos;
+        if (src_row) src_row[pos] = int32_t(t0 + pl / k);
         __syncwarp(am);
         if (lane == 31 - __clz(peers)) cursor[e] = before + __popc(peers);
       }
@@ -522,6 +525,7 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
     }
   }
   __syncthreads();
+  if (!xperm) return;  // GEMM1 gathers the rows itself (TMA tile::gather4)
   // gather: each warp copies whole token rows to their k destinations
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t segs = h / 8;
@@ -733,18 +737,18 @@ int64_t permute_scratch_ints(int64_t T, int E) {
 
 void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int k, int64_t h,
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
-                    int2* mb_seg, int32_t* meta, uint16_t* xperm, int32_t* scratch,
-                    cudaStream_t st) {
+                    int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
+                    int32_t* scratch, cudaStream_t st) {
   const int nch = int((T + PCH - 1) / PCH);
   int32_t* chunk_counts = scratch;
   int32_t* expert_off = scratch + int64_t(nch) * E;
   if (nch > 0)
     permute_count_kernel<<<nch, 256, E * sizeof(int32_t), st>>>(idx, T, E, k, chunk_counts);
   permute_scan_kernel<<<1, 1024, 2 * E * sizeof(int32_t), st>>>(
-      chunk_counts, nch, E, T, shared, counts, expert_off, mblock_expert, mb_seg, meta);
+      chunk_counts, nch, E, T, shared, counts, expert_off, mblock_expert, mb_seg, src_row, meta);
   if (nch > 0)
     permute_scatter_kernel<<<nch, 256, (E + PCH * k) * sizeof(int32_t), st>>>(
-        idx, x, T, E, k, h, chunk_counts, expert_off, row_of, xperm);
+        idx, x, T, E, k, h, chunk_counts, expert_off, row_of, src_row, xperm);
 }
 
 void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,

@@ -48,10 +48,12 @@ void launch_topk(const int32_t* C, const int32_t* ex, const int32_t* ew, const f
 // scratch: >= permute_scratch_ints(T, E) int32.
 int64_t permute_scratch_ints(int64_t T, int E);
 //  mb_seg[...]          {first m-block, m-blocks} of each m-block's expert
+//  src_row[routed rows] source token of every expert-major row (nullable)
+//  xperm                expert-major copy of the rows (nullable: GEMM1 gathers)
 void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int k, int64_t h,
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
-                    int2* mb_seg, int32_t* meta, uint16_t* xperm, int32_t* scratch,
-                    cudaStream_t st);
+                    int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
+                    int32_t* scratch, cudaStream_t st);
 
 // y[t] = sum_j w[t,j] * O[row_of[t,j]] (+ S[s_off + t]) (+ x[t]); the shared
 // expert rows start at S + s_off*h with s_off = s_meta ? s_meta[2] : 0

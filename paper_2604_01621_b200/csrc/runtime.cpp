@@ -114,6 +114,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   counts_ = static_cast<int32_t*>(dalloc(size_t(E_) * 4, &workspace_bytes));
   mblock_ = static_cast<int32_t*>(dalloc(size_t(max_mb_) * 4, &workspace_bytes));
   mbseg_ = static_cast<int2*>(dalloc(size_t(max_mb_) * sizeof(int2), &workspace_bytes));
+  srcrow_ = static_cast<int32_t*>(dalloc(size_t(max_rows_) * 4, &workspace_bytes));
   meta_ = static_cast<int32_t*>(dalloc(16 * 4, &workspace_bytes));
   scratch_ = static_cast<int32_t*>(
       dalloc(size_t(permute_scratch_ints(max_tokens_, E_)) * 4, &workspace_bytes));
@@ -179,7 +180,7 @@ Ctx::~Ctx() {
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   void* bufs[] = {arena_[0], arena_[1], arena_[2], router_w_, bias_, slot_tab_, logits_, idx_,
                   wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_,
-                  router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_, mbseg_, dep_seg_};
+                  router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_, mbseg_, dep_seg_, srcrow_};
   if (dep_seg_host_) cudaFreeHost(dep_seg_host_);
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -543,14 +544,16 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   const int wl = layer % WL_;
   route_logits(wl, x, T, st);
   mark(0);
-  launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, meta_, xperm_,
+  launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, srcrow_, meta_, nullptr,
                  scratch_, st);
   mark(1);
   const int64_t mb_ub = (T * k_ + int64_t(E_) * 127) / 128 + 1 + (shared_ ? (T + 127) / 128 : 0);
   const CUtensorMap tm_x = shared_ ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
   const int32_t* stab = slot_tab_ + (size_t(layer) * 2 + size_t(parity)) * (E_ + 1);
-  GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_};
-  launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
+  // routed A rows are gathered straight from x (TMA tile::gather4 by src_row)
+  const CUtensorMap tm_xg = make_tmap_bf16(x, T, h_, 1);
+  GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_, srcrow_};
+  launch_grouped_gemm(GEMM_SWIGLU, tm_xg, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(2);
   GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_};
   launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tm_down_, tm_down_, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
@@ -613,7 +616,7 @@ void Ctx::route(int layer, const uint16_t* x, int64_t T, int32_t* idx, float* wt
   require(T >= 1 && T <= max_tokens_, "route: T out of range");
   const int wl = layer % WL_;
   route_logits(wl, x, T, st);
-  launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, meta_, xperm_,
+  launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, srcrow_, meta_, nullptr,
                  scratch_, st);
   launches += 5;
   const size_t tk = size_t(T) * size_t(k_);

@@ -139,6 +139,7 @@ class Ctx {
           *meta_ = nullptr, *scratch_ = nullptr;
   float* wts_ = nullptr;
   int2* mbseg_ = nullptr;               // [max_mb] expert segment of each m-block
+  int32_t* srcrow_ = nullptr;           // [max_rows] source token of each routed row
   uint16_t *xperm_ = nullptr, *hbuf_ = nullptr;
   CUtensorMap tm_gate_, tm_up_, tm_down_, tm_xperm_, tm_h_;
   // prefetch engine
