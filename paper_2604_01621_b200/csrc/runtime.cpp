@@ -544,16 +544,18 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   const int wl = layer % WL_;
   route_logits(wl, x, T, st);
   mark(0);
-  launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, srcrow_, meta_, nullptr,
+  launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_, xperm_,
                  scratch_, st);
   mark(1);
   const int64_t mb_ub = (T * k_ + int64_t(E_) * 127) / 128 + 1 + (shared_ ? (T + 127) / 128 : 0);
   const CUtensorMap tm_x = shared_ ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
   const int32_t* stab = slot_tab_ + (size_t(layer) * 2 + size_t(parity)) * (E_ + 1);
-  // routed A rows are gathered straight from x (TMA tile::gather4 by src_row)
-  const CUtensorMap tm_xg = make_tmap_bf16(x, T, h_, 1);
-  GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_, srcrow_};
-  launch_grouped_gemm(GEMM_SWIGLU, tm_xg, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
+  // Routed A rows come from the materialised expert-major copy. (GEMM1 can
+  // also gather them from x with TMA tile::gather4 via GemmArgs::a_rows; on
+  // B200 that measured 2.5x slower: 32 scattered 128-byte row fetches per
+  // k-block defeat L2 reuse across the expert's 16 n-block tiles.)
+  GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_};
+  launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(2);
   GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_};
   launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tm_down_, tm_down_, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
