@@ -208,6 +208,8 @@ int dwdp_analytic_compare(const dwdp_model_spec* m, const dwdp_gpu_spec* g,
  * ==================================================================== */
 #define DWDP_SCORING_SOFTMAX 0
 #define DWDP_SCORING_SIGMOID 1
+#define DWDP_WEIGHT_BF16 0
+#define DWDP_WEIGHT_FP8 1
 #define DWDP_ENGINE_COPY 0 /* copy-engine peer copies on a side stream  */
 #define DWDP_ENGINE_PULL 1 /* one-launch SM pull kernel over NVLink      */
 
@@ -237,7 +239,9 @@ typedef struct {
   int32_t pull_ctas;      /* CTAs of the pull kernel                       */
   int32_t ce_inflight;    /* copy-engine transfers in flight per plan
                              (GpuSpec::ce_inflight, hwmodel.hpp:33)       */
-  int32_t reserved0;
+  int32_t weight_dtype;   /* DWDP_WEIGHT_BF16 / DWDP_WEIGHT_FP8 (e4m3 with
+                             per-output-channel fp32 scales; activations
+                             quantised per row, W8A8 on tcgen05 f8f6f4)   */
   /* synthetic weights */
   uint64_t weight_seed;
   int32_t weight_layers;  /* distinct weight sets; layer l uses l % this   */
@@ -270,7 +274,9 @@ int dwdp_ctx_init_weights(dwdp_ctx* ctx, float bias_scale);
  * popularity tilt); host array [E] fp32. */
 int dwdp_ctx_set_bias(dwdp_ctx* ctx, const float* bias);
 /* Copy expert `e` tensor t (0 gate, 1 up, 2 down; e == E: shared) of
- * layer `layer` as currently resident for that layer into host memory. */
+ * layer `layer` as currently resident for that layer into host memory
+ * (raw storage: bf16, or e4m3 bytes for fp8). For fp8, t = 3, 4, 5 read the
+ * fp32 per-row scales of gate, up, down. */
 int dwdp_ctx_read_expert(dwdp_ctx* ctx, int layer, int expert, int t,
                          void* host_bf16);
 

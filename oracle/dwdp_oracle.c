@@ -657,6 +657,102 @@ static inline float dot_bf16(const float* a, const uint16_t* w, int64_t n) {
   return s;
 }
 
+/* ---- W8A8 emulation ---------------------------------------------------
+ * Follows the device W8A8 path (paper_2604_01621_b200/csrc/kernels.cu
+ * fp8 helpers + gemm_sm100.cu FP8 epilogues): weights and activations are
+ * e4m3 with per-row fp32 scales; GEMM products are exact, sums fp32; GEMM1
+ * output = acc * (sx * sw), H = bf16(silu(g) * u) re-quantised per row;
+ * GEMM2 output = acc * (sh * sd). */
+uint8_t oracle_f32_to_e4m3(float x) {
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  const uint32_t s = (u >> 24) & 0x80u;
+  const uint32_t a = u & 0x7fffffffu;
+  if (a > 0x7f800000u) return (uint8_t)(s | 0x7f);
+  if (a >= 0x43e00000u) return (uint8_t)(s | 0x7e);
+  const int e = (int)(a >> 23) - 127;
+  if (e < -6) {
+    float av;
+    memcpy(&av, &a, 4);
+    const float q = rintf(av * 512.0f);
+    return (uint8_t)(s | (uint32_t)q);
+  }
+  const uint32_t m = a & 0x7fffffu;
+  uint32_t m3 = m >> 20;
+  const uint32_t rem = m & 0xfffffu;
+  if (rem > 0x80000u || (rem == 0x80000u && (m3 & 1u))) ++m3;
+  uint32_t code = ((uint32_t)(e + 7) << 3) + m3;
+  if (code > 0x7e) code = 0x7e;
+  return (uint8_t)(s | code);
+}
+
+float oracle_e4m3_to_f32(uint8_t b) {
+  const uint32_t e = (b >> 3) & 0xf, m = b & 7;
+  float v;
+  if (e) {
+    const uint32_t bits = ((e + 120) << 23) | (m << 20);
+    memcpy(&v, &bits, 4);
+  } else {
+    v = (float)m * 0.001953125f;
+  }
+  return (b & 0x80) ? -v : v;
+}
+
+void oracle_e4m3_encode(const float* x, int64_t n, uint8_t* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = oracle_f32_to_e4m3(x[i]);
+}
+
+void oracle_quant_row_e4m3(const float* v, int64_t K, uint8_t* q, float* s) {
+  float amax = 0.0f;
+  for (int64_t i = 0; i < K; ++i) amax = fmaxf(amax, fabsf(v[i]));
+  const float sc = amax > 0.0f ? amax / 448.0f : 1.0f;
+  for (int64_t i = 0; i < K; ++i) q[i] = oracle_f32_to_e4m3(v[i] / sc);
+  *s = sc;
+}
+
+/* Quantise n rows of length K into dequantised-grid floats (q values, not
+ * multiplied by the scale) + scales. */
+static void quant_rows_grid(const float* src, int64_t n, int64_t K, float* grid, float* scales,
+                            uint8_t* tmp) {
+  for (int64_t r = 0; r < n; ++r) {
+    oracle_quant_row_e4m3(src + r * K, K, tmp, scales + r);
+    for (int64_t i = 0; i < K; ++i) grid[r * K + i] = oracle_e4m3_to_f32(tmp[i]);
+  }
+}
+
+static void ffn_rows_w8a8(const float* gate, const float* up, const float* down, int64_t h,
+                          int64_t f, const float* const* xr, const float* scale,
+                          float* const* yr, int n) {
+  const int64_t mx = h > f ? h : f;
+  uint8_t* tmp = malloc((size_t)mx);
+  float* gq = malloc(sizeof(float) * (size_t)(f * h));
+  float* uq = malloc(sizeof(float) * (size_t)(f * h));
+  float* dq = malloc(sizeof(float) * (size_t)(h * f));
+  float* gs = malloc(sizeof(float) * (size_t)f);
+  float* us = malloc(sizeof(float) * (size_t)f);
+  float* ds = malloc(sizeof(float) * (size_t)h);
+  quant_rows_grid(gate, f, h, gq, gs, tmp);
+  quant_rows_grid(up, f, h, uq, us, tmp);
+  quant_rows_grid(down, h, f, dq, ds, tmp);
+  float* xq = malloc(sizeof(float) * (size_t)h);
+  float* hb = malloc(sizeof(float) * (size_t)f);
+  float* hq = malloc(sizeof(float) * (size_t)f);
+  for (int r = 0; r < n; ++r) {
+    float sx, sh;
+    quant_rows_grid(xr[r], 1, h, xq, &sx, tmp);
+    for (int64_t j = 0; j < f; ++j) {
+      const float g = dotf(xq, gq + j * h, h) * (sx * gs[j]);
+      const float u = dotf(xq, uq + j * h, h) * (sx * us[j]);
+      hb[j] = bf16_to_f32(f32_to_bf16(siluf(g) * u));
+    }
+    quant_rows_grid(hb, 1, f, hq, &sh, tmp);
+    for (int64_t i = 0; i < h; ++i)
+      yr[r][i] += scale[r] * bf16_to_f32(f32_to_bf16(dotf(hq, dq + i * f, f) * (sh * ds[i])));
+  }
+  free(tmp); free(gq); free(uq); free(dq); free(gs); free(us); free(ds);
+  free(xq); free(hb); free(hq);
+}
+
 static void ffn_rows_bf16(const uint16_t* gate, const uint16_t* up, const uint16_t* down,
                           int64_t h, int64_t f, const float* const* xr, const float* scale,
                           float* const* yr, int n, float* hbuf) {
@@ -752,7 +848,19 @@ static void expert_job(void* p, int64_t e64) {
     yr[r] = out + r * h;
     sc[r] = e < E ? a->wts[pid] : 1.0f;
   }
-  if (resident)
+  if (a->cfg->w8a8) {
+    if (resident) {
+      g = malloc(sizeof(float) * (size_t)(f * h));
+      u = malloc(sizeof(float) * (size_t)(f * h));
+      d = malloc(sizeof(float) * (size_t)(h * f));
+      for (int64_t i = 0; i < f * h; ++i) {
+        g[i] = bf16_to_f32(a->bg[e][i]);
+        u[i] = bf16_to_f32(a->bu[e][i]);
+        d[i] = bf16_to_f32(a->bd[e][i]);
+      }
+    }
+    ffn_rows_w8a8(g, u, d, h, f, xr, sc, yr, (int)n);
+  } else if (resident)
     ffn_rows_bf16(a->bg[e], a->bu[e], a->bd[e], h, f, xr, sc, yr, (int)n, hb);
   else
     ffn_rows(g, u, d, h, f, xr, sc, yr, (int)n, hb);

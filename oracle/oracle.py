@@ -37,7 +37,8 @@ class MoeConfig(C.Structure):
     _fields_ = [("hidden", i64), ("num_experts", C.c_int32), ("top_k", C.c_int32),
                 ("ffn", i64), ("shared_ffn", i64), ("scoring", C.c_int32),
                 ("n_group", C.c_int32), ("topk_group", C.c_int32),
-                ("norm_topk", C.c_int32), ("routed_scale", f32)]
+                ("norm_topk", C.c_int32), ("routed_scale", f32),
+                ("w8a8", C.c_int32)]
 
 
 class _Api:
@@ -142,6 +143,8 @@ class _Oracle(_Api):
         L.oracle_permute.restype = i64
         L.oracle_permute.argtypes = [P, i64, i32, i32, i32, P, P]
         L.oracle_moe_forward_seeded.argtypes = [P, u64, i32, P, i64, P, P, P, P, i32]
+        L.oracle_e4m3_encode.argtypes = [P, i64, P]
+        L.oracle_quant_row_e4m3.argtypes = [P, i64, P, P]
         L.oracle_moe_forward_explicit.argtypes = [P, P, i64, P, P, P, P, P, P, P, P, P, P, P]
         L.oracle_moe_forward_bf16w.argtypes = [P, P, i64, P, P, P, P, P, P, P, P, i32]
 
@@ -196,6 +199,19 @@ class _Oracle(_Api):
         row_of = np.zeros(T * k, np.int64)
         total = self.lib.oracle_permute(_ptr(idx), T, E, k, align, _ptr(counts), _ptr(row_of))
         return int(total), counts, row_of.reshape(T, k)
+
+    def e4m3_encode(self, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float32).reshape(-1)
+        out = np.zeros(x.size, np.uint8)
+        self.lib.oracle_e4m3_encode(_ptr(x), x.size, _ptr(out))
+        return out
+
+    def quant_row_e4m3(self, v):
+        v = np.ascontiguousarray(v, np.float32).reshape(-1)
+        q = np.zeros(v.size, np.uint8)
+        s = C.c_float()
+        self.lib.oracle_quant_row_e4m3(_ptr(v), v.size, _ptr(q), C.byref(s))
+        return q, s.value
 
     def moe_forward_seeded(self, cfg: MoeConfig, base: int, layer: int, x_bf16: np.ndarray,
                            T: int, bias: np.ndarray | None, nthreads: int = 0):

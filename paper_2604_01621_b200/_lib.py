@@ -14,6 +14,7 @@ P = C.c_void_p
 DWDP_OK, DWDP_ERR_CONFIG, DWDP_ERR_INVARIANT, DWDP_ERR_CUDA = 0, 2, 3, 4
 IPC_BLOB_BYTES = 512
 ENGINE_COPY, ENGINE_PULL = 0, 1
+WEIGHT_BF16, WEIGHT_FP8 = 0, 1
 
 
 class ConfigError(ValueError):
@@ -69,7 +70,7 @@ class CtxConfigC(C.Structure):
                 ("topk_group", i32), ("norm_topk", i32), ("routed_scale", f32), ("rank", i32),
                 ("group_size", i32), ("extra_redundancy", i32), ("device", i32),
                 ("merge_elim", i32), ("tdm", i32), ("slice_size", u64), ("engine", i32),
-                ("pull_ctas", i32), ("ce_inflight", i32), ("reserved0", i32),
+                ("pull_ctas", i32), ("ce_inflight", i32), ("weight_dtype", i32),
                 ("weight_seed", u64), ("weight_layers", i32),
                 ("kernel_timing", i32), ("max_tokens", i64)]
 

@@ -99,6 +99,7 @@ void Ctx::dep_init(const void* unique_id) {
   require(N_ >= 2, "dep: group_size must be >= 2");
   require(E_ % N_ == 0, "dep: group_size must divide num_experts");
   require(nccl_ == nullptr, "dep: already initialised");
+  require(!fp8_, "dep: the DEP baseline runs bf16 weights only");
   NcclId id;
   std::memcpy(&id, unique_id, sizeof id);
   nccl_check(nccl().CommInitRank(&nccl_, N_, id, rank_), "ncclCommInitRank");

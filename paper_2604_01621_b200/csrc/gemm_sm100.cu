@@ -130,15 +130,18 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
          (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
-// Kernel modes: SwiGLU-fused bf16 (GEMM1), plain bf16 (GEMM2), and the exact
-// int8 x int8 -> int32 mode of the router (kind::i8, order-free accumulation).
-constexpr int kSwiGLU = 0, kPlain = 1, kInt8 = 2;
+// Kernel modes: SwiGLU-fused bf16 (GEMM1), plain bf16 (GEMM2), the exact
+// int8 x int8 -> int32 mode of the router (kind::i8, order-free accumulation),
+// and the W8A8 e4m3 modes (kind::f8f6f4, scales applied in the epilogue).
+constexpr int kSwiGLU = 0, kPlain = 1, kInt8 = 2, kSwiGLU8 = 3, kPlain8 = 4;
 // Instruction descriptor, both operands K-major, M=128, N=256:
-//   f16 kind: bf16 x bf16 -> fp32 (c_format 1, a/b_format 1 = BF16)
-//   i8 kind:  s8 x s8 -> s32      (c_format 2, a/b_format 1 = signed)
+//   f16 kind:    bf16 x bf16 -> fp32 (c_format 1, a/b_format 1 = BF16)
+//   i8 kind:     s8 x s8 -> s32      (c_format 2, a/b_format 1 = signed)
+//   f8f6f4 kind: e4m3 x e4m3 -> fp32 (c_format 1, a/b_format 0 = E4M3)
 template <int MODE>
 __host__ __device__ constexpr uint32_t idesc() {
-  return (MODE == kInt8 ? (2u << 4) : (1u << 4)) | (1u << 7) | (1u << 10) |
+  return (MODE == kInt8 ? (2u << 4) : (1u << 4)) |
+         (MODE == kSwiGLU8 || MODE == kPlain8 ? 0u : (1u << 7) | (1u << 10)) |
          (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
 }
 __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
@@ -147,6 +150,14 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint6
       "{\n.reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc_v), "r"(accum));
+}
+__device__ __forceinline__ void tc_mma_f8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc_v, uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc_v), "r"(accum));
 }
 
@@ -218,8 +229,9 @@ __global__ void __launch_bounds__(256, 1)
 
   const int total_mb = p.meta[0];
   const int routed_mb = p.meta[1];
-  constexpr bool SWIGLU = MODE == kSwiGLU;
-  constexpr int BKE = MODE == kInt8 ? 128 : 64;  // K elements per 128-byte smem row
+  constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8;
+  constexpr bool FP8 = MODE == kSwiGLU8 || MODE == kPlain8;
+  constexpr int BKE = (MODE == kInt8 || FP8) ? 128 : 64;  // K elements per 128-byte smem row
   const int nb_count = SWIGLU ? p.n_out / 128 : (p.n_out + BN - 1) / BN;
   const int num_tiles = total_mb * nb_count;
   const int kb_count = p.K / BKE;
@@ -281,6 +293,8 @@ __global__ void __launch_bounds__(256, 1)
           for (int k = 0; k < 4; ++k) {  // +32 B along K per MMA (16 bf16 or 32 int8)
             if (MODE == kInt8)
               tc_mma_i8(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0);
+            else if (FP8)
+              tc_mma_f8(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0);
             else
               tc_mma(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0);
           }
@@ -306,6 +320,17 @@ __global__ void __launch_bounds__(256, 1)
       const int64_t row = int64_t(mb) * BM + q * 32 + lane;
       const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(a * BN);
       const bool store = row < p.m_limit;
+      // fp8: per-row activation scale x per-output-channel weight scale
+      float sa = 1.0f;
+      const float* sb0 = nullptr;
+      const float* sb1 = nullptr;
+      if (FP8) {
+        sa = p.a_scale[row];
+        const int64_t b0 = int64_t(p.slot_of[p.mblock_expert[mb]]) * p.rows_per_slot +
+                           int64_t(nb) * (SWIGLU ? 128 : BN);
+        sb0 = p.b_scale0 + b0;
+        sb1 = SWIGLU ? p.b_scale1 + b0 : nullptr;
+      }
       if (MODE == kInt8) {
         int32_t* out = reinterpret_cast<int32_t*>(p.D) + row * p.ldd + nb * BN;
         const int cols = p.n_out - nb * BN < BN ? p.n_out - nb * BN : BN;
@@ -332,6 +357,13 @@ __global__ void __launch_bounds__(256, 1)
           float g[32], u[32];
           tmem_ld32(tbase + c, g);
           tmem_ld32(tbase + 128 + c, u);
+          if (FP8) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              g[i] *= sa * __ldg(sb0 + c + i);
+              u[i] *= sa * __ldg(sb1 + c + i);
+            }
+          }
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -353,6 +385,10 @@ __global__ void __launch_bounds__(256, 1)
         for (int c = 0; c < BN; c += 32) {
           float v[32];
           tmem_ld32(tbase + c, v);
+          if (FP8) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] *= sa * __ldg(sb0 + c + i);
+          }
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
@@ -444,6 +480,10 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
                            SMEM_BYTES);
       cudaFuncSetAttribute(grouped_gemm_kernel<kInt8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            SMEM_BYTES);
+      cudaFuncSetAttribute(grouped_gemm_kernel<kSwiGLU8>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+      cudaFuncSetAttribute(grouped_gemm_kernel<kPlain8>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
       configured |= uint64_t(1) << dev;
     }
   }
@@ -453,8 +493,12 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
     grouped_gemm_kernel<kSwiGLU><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
   else if (mode == kPlain)
     grouped_gemm_kernel<kPlain><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
-  else
+  else if (mode == kInt8)
     grouped_gemm_kernel<kInt8><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+  else if (mode == kSwiGLU8)
+    grouped_gemm_kernel<kSwiGLU8><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+  else
+    grouped_gemm_kernel<kPlain8><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
 }
 
 }  // namespace dwdp

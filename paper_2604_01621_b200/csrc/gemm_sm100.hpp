@@ -29,6 +29,11 @@ struct GemmArgs {
   // then gathered straight from the token matrix (`a` must be a gather map,
   // box 64 x 1) with TMA tile::gather4, so no permuted copy is materialised.
   const int32_t* a_rows;
+  // fp8 modes: D = (A_q . B_q^T) * a_scale[row] * b_scale[B row]; SwiGLU uses
+  // b_scale0 for the gate rows and b_scale1 for the up rows.
+  const float* a_scale;
+  const float* b_scale0;
+  const float* b_scale1;
 };
 
 // 2-D bf16 TMA map over a row-major [rows][cols] matrix, box = 64 x box_rows,
@@ -37,7 +42,8 @@ CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int box
 // Same for an int8 matrix (box = 128 x box_rows).
 CUtensorMap make_tmap_i8(const void* base, int64_t rows, int64_t cols, int box_rows);
 
-constexpr int GEMM_SWIGLU = 0, GEMM_PLAIN = 1, GEMM_INT8 = 2;
+constexpr int GEMM_SWIGLU = 0, GEMM_PLAIN = 1, GEMM_INT8 = 2, GEMM_SWIGLU_FP8 = 3,
+              GEMM_PLAIN_FP8 = 4;
 
 // a: routed A rows (permuted tokens or H); a2: shared-expert A rows (x);
 // b0: gate (SwiGLU) or down arena; b1: up arena (SwiGLU only).

@@ -69,6 +69,111 @@ __global__ void fill_f32_kernel(float* __restrict__ dst, int64_t n, uint64_t see
     dst[i] = hash_val(seed, i, scale);
 }
 
+// ---------------------------------------------------------------- fp8 (e4m3)
+// fp32 -> e4m3 (OCP E4M3, no inf): round to nearest even on the integer
+// mantissa, saturate to +-448. Same integer recipe as oracle_f32_to_e4m3.
+__device__ __forceinline__ uint8_t f32_to_e4m3(float x) {
+  const uint32_t u = __float_as_uint(x);
+  const uint32_t s = (u >> 24) & 0x80u;
+  const uint32_t a = u & 0x7fffffffu;
+  if (a > 0x7f800000u) return uint8_t(s | 0x7f);  // NaN
+  if (a >= 0x43e00000u) return uint8_t(s | 0x7e);  // >= 448: saturate
+  const int e = int(a >> 23) - 127;
+  if (e < -6) {  // subnormal: multiple of 2^-9, RNE
+    const float q = rintf(__fmul_rn(__uint_as_float(a), 512.0f));
+    return uint8_t(s | uint32_t(q));  // q == 8 encodes the min normal 0x08
+  }
+  const uint32_t m = a & 0x7fffffu;
+  uint32_t m3 = m >> 20;
+  const uint32_t rem = m & 0xfffffu;
+  if (rem > 0x80000u || (rem == 0x80000u && (m3 & 1u))) ++m3;
+  uint32_t code = (uint32_t(e + 7) << 3) + m3;  // mantissa carry bumps the exponent
+  if (code > 0x7e) code = 0x7e;
+  return uint8_t(s | code);
+}
+
+__device__ __forceinline__ float e4m3_to_f32(uint32_t b) {
+  const uint32_t e = (b >> 3) & 0xf, m = b & 7;
+  const float v = e ? __uint_as_float(((e + 120) << 23) | (m << 20)) : float(m) * 0.001953125f;
+  return (b & 0x80) ? -v : v;
+}
+
+// Quantised synthetic expert weights: one warp per (slot, row); the row's
+// bf16 values come from the same counter hash as the bf16 init; scale =
+// absmax / 448 (1 if the row is zero), q = e4m3(v / scale).
+__global__ void __launch_bounds__(256) fp8_fill_rows_kernel(uint8_t* __restrict__ dst,
+                                                            float* __restrict__ scales,
+                                                            const uint64_t* __restrict__ seeds,
+                                                            int nslots, int rows, int64_t K,
+                                                            float scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wid >= int64_t(nslots) * rows) return;
+  const int64_t slot = wid / rows, r = wid - slot * rows;
+  const uint64_t seed = seeds[slot];
+  auto val = [&](int64_t k) { return bf16_f(bf16_bits(hash_val(seed, r * K + k, scale))); };
+  float amax = 0.0f;
+  for (int64_t k = lane; k < K; k += 32) amax = fmaxf(amax, fabsf(val(k)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const float s = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+  uint8_t* out = dst + (slot * rows + r) * K;
+  for (int64_t k = lane * 4; k < K; k += 128) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w |= uint32_t(f32_to_e4m3(__fdiv_rn(val(k + q), s))) << (8 * q);
+    *reinterpret_cast<uint32_t*>(out + k) = w;
+  }
+  if (lane == 0) scales[slot * rows + r] = s;
+}
+
+// One warp per bf16 row: per-row e4m3 quantisation (scale = absmax / 448).
+__device__ __forceinline__ float row_absmax_bf16(const uint4* row, int64_t nch, int lane) {
+  float amax = 0.0f;
+  for (int64_t c = lane; c < nch; c += 32) {
+    const uint4 v = __ldg(row + c);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      amax = fmaxf(amax, fmaxf(fabsf(__uint_as_float(w[q] << 16)),
+                               fabsf(__uint_as_float(w[q] & 0xffff0000u))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  return amax;
+}
+
+__device__ __forceinline__ uint2 quant8(uint4 v, float s) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t o[2] = {0, 0};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    o[q >> 1] |= uint32_t(f32_to_e4m3(__fdiv_rn(__uint_as_float(w[q] << 16), s))) << (16 * (q & 1));
+    o[q >> 1] |= uint32_t(f32_to_e4m3(__fdiv_rn(__uint_as_float(w[q] & 0xffff0000u), s)))
+                 << (16 * (q & 1) + 8);
+  }
+  return make_uint2(o[0], o[1]);
+}
+
+// H (bf16, rows < meta[0]*128) -> e4m3 + per-row scale (GEMM2's A operand).
+__global__ void __launch_bounds__(256) quant_rows_fp8_kernel(const uint16_t* __restrict__ src,
+                                                             int64_t max_rows, int64_t K,
+                                                             const int32_t* __restrict__ meta,
+                                                             uint8_t* __restrict__ dst,
+                                                             float* __restrict__ scales) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t rows = meta ? int64_t(meta[0]) * 128 : max_rows;
+  if (r >= rows) return;
+  const uint4* row = reinterpret_cast<const uint4*>(src + r * K);
+  const int64_t nch = K / 8;
+  const float amax = row_absmax_bf16(row, nch, lane);
+  const float s = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+  uint2* out = reinterpret_cast<uint2*>(dst + r * K);
+  for (int64_t c = lane; c < nch; c += 32) out[c] = quant8(__ldg(row + c), s);
+  if (lane == 0) scales[r] = s;
+}
+
 // ---------------------------------------------------------------- router
 // SIMT fp32 GEMM, 128 tokens x 128 experts per CTA, 8x8 outputs per thread.
 // Every output accumulates fma(x[t][i], w[e][i], acc) for i ascending.
@@ -494,7 +599,9 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
 __global__ void __launch_bounds__(256) permute_scatter_kernel(
     const int32_t* __restrict__ idx, const uint16_t* __restrict__ x, int64_t T, int E, int k,
     int64_t h, const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ expert_off,
-    int32_t* __restrict__ row_of, int32_t* __restrict__ src_row, uint16_t* __restrict__ xperm) {
+    int32_t* __restrict__ row_of, int32_t* __restrict__ src_row, uint16_t* __restrict__ xperm,
+    uint8_t* __restrict__ xperm8, float* __restrict__ xscale, const int32_t* __restrict__ meta,
+    int shared) {
   extern __shared__ int32_t sm[];  // cursor[E], rows[PCH * k]
   int32_t* cursor = sm;
   int32_t* rows = sm + E;
@@ -525,9 +632,27 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
     }
   }
   __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (xperm8) {  // W8A8: quantise each token row once (per-row scale), write k + shared copies
+    const int64_t nch = h / 8;
+    const int32_t shared_row0 = shared ? meta[2] : 0;
+    for (int tl = warp; tl < ntok; tl += blockDim.x >> 5) {
+      const uint4* src = reinterpret_cast<const uint4*>(x + (t0 + tl) * h);
+      const float amax = row_absmax_bf16(src, nch, lane);
+      const float s = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+      for (int64_t c = lane; c < nch; c += 32) {
+        const uint2 q = quant8(__ldg(src + c), s);
+        for (int j = 0; j < k; ++j)
+          reinterpret_cast<uint2*>(xperm8 + int64_t(rows[tl * k + j]) * h)[c] = q;
+        if (shared) reinterpret_cast<uint2*>(xperm8 + int64_t(shared_row0 + t0 + tl) * h)[c] = q;
+      }
+      if (lane < k) xscale[rows[tl * k + lane]] = s;
+      if (shared && lane == 0) xscale[shared_row0 + t0 + tl] = s;
+    }
+    return;
+  }
   if (!xperm) return;  // GEMM1 gathers the rows itself (TMA tile::gather4)
   // gather: each warp copies whole token rows to their k destinations
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t segs = h / 8;
   for (int tl = warp; tl < ntok; tl += blockDim.x >> 5) {
     const uint4* src = reinterpret_cast<const uint4*>(x + (t0 + tl) * h);
@@ -738,7 +863,7 @@ int64_t permute_scratch_ints(int64_t T, int E) {
 void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int k, int64_t h,
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
                     int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
-                    int32_t* scratch, cudaStream_t st) {
+                    int32_t* scratch, cudaStream_t st, uint8_t* xperm8, float* xscale) {
   const int nch = int((T + PCH - 1) / PCH);
   int32_t* chunk_counts = scratch;
   int32_t* expert_off = scratch + int64_t(nch) * E;
@@ -748,7 +873,23 @@ void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int
       chunk_counts, nch, E, T, shared, counts, expert_off, mblock_expert, mb_seg, src_row, meta);
   if (nch > 0)
     permute_scatter_kernel<<<nch, 256, (E + PCH * k) * sizeof(int32_t), st>>>(
-        idx, x, T, E, k, h, chunk_counts, expert_off, row_of, src_row, xperm);
+        idx, x, T, E, k, h, chunk_counts, expert_off, row_of, src_row, xperm, xperm8, xscale,
+        meta, shared);
+}
+
+void launch_fp8_fill_rows(uint8_t* dst, float* scales, const uint64_t* seeds, int nslots, int rows,
+                          int64_t K, float scale, cudaStream_t st) {
+  const int64_t warps = int64_t(nslots) * rows;
+  if (warps > 0)
+    fp8_fill_rows_kernel<<<unsigned((warps + 7) / 8), 256, 0, st>>>(dst, scales, seeds, nslots, rows,
+                                                                   K, scale);
+}
+
+void launch_quant_rows_fp8(const uint16_t* src, int64_t max_rows, int64_t K, const int32_t* meta,
+                           uint8_t* dst, float* scales, cudaStream_t st) {
+  if (max_rows > 0)
+    quant_rows_fp8_kernel<<<unsigned((max_rows + 7) / 8), 256, 0, st>>>(src, max_rows, K, meta, dst,
+                                                                        scales);
 }
 
 void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,

@@ -53,7 +53,18 @@ int64_t permute_scratch_ints(int64_t T, int E);
 void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int k, int64_t h,
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
                     int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
-                    int32_t* scratch, cudaStream_t st);
+                    int32_t* scratch, cudaStream_t st, uint8_t* xperm8 = nullptr,
+                    float* xscale = nullptr);
+// W8A8 (weight_dtype fp8): xperm8 [rows][h] e4m3 copies of the token rows
+// (routed rows + shared rows from meta[2]) with per-row scales xscale.
+
+// fp8 expert weights: per (slot, row) scale = absmax/448, q = e4m3(v/scale)
+// over the bf16 counter-hash values (bit-identical to the oracle).
+void launch_fp8_fill_rows(uint8_t* dst, float* scales, const uint64_t* seeds, int nslots, int rows,
+                          int64_t K, float scale, cudaStream_t st);
+// bf16 rows (rows < meta[0]*128) -> e4m3 + per-row scale.
+void launch_quant_rows_fp8(const uint16_t* src, int64_t max_rows, int64_t K, const int32_t* meta,
+                           uint8_t* dst, float* scales, cudaStream_t st);
 
 // y[t] = sum_j w[t,j] * O[row_of[t,j]] (+ S[s_off + t]) (+ x[t]); the shared
 // expert rows start at S + s_off*h with s_off = s_meta ? s_meta[2] : 0

@@ -20,7 +20,8 @@ struct IpcBlob {
   uint32_t magic;
   int32_t rank, nslots, c;
   int64_t slot_elems;
-  cudaIpcMemHandle_t h[3];
+  int32_t ntens, reserved;
+  cudaIpcMemHandle_t h[6];
 };
 static_assert(sizeof(IpcBlob) <= DWDP_IPC_BLOB_BYTES, "ipc blob too large");
 
@@ -55,6 +56,11 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   h_ = c.hidden;
   f_ = c.ffn;
   shared_ = c.shared_ffn > 0;
+  require(c.weight_dtype == DWDP_WEIGHT_BF16 || c.weight_dtype == DWDP_WEIGHT_FP8,
+          "ctx: unknown weight_dtype");
+  fp8_ = c.weight_dtype == DWDP_WEIGHT_FP8;
+  esz_ = fp8_ ? 1 : 2;
+  ntens_ = fp8_ ? 6 : 3;
   require(L_ >= 1, "ctx: num_layers must be >= 1");
   require(E_ >= 1 && E_ <= 512, "ctx: num_experts must be in [1, 512]");
   require(k_ >= 1 && k_ <= 16 && k_ <= E_, "ctx: top_k must be in [1, min(16, E)]");
@@ -85,12 +91,15 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
 
   // ---- arenas (one allocation per tensor kind so each is an IPC object)
   slot_elems_ = f_ * h_;
-  const uint64_t slot_bytes = uint64_t(slot_elems_) * 2;
-  for (int t = 0; t < 3; ++t) {
-    arena_[t] = static_cast<uint16_t*>(dalloc(slot_bytes * uint64_t(nslots_), nullptr));
+  for (int t = 0; t < 3; ++t)
+    arena_[t] = static_cast<uint16_t*>(dalloc(tsb(t) * uint64_t(nslots_), nullptr));
+  if (fp8_)
+    for (int t = 0; t < 3; ++t)
+      sarena_[t] = static_cast<float*>(dalloc(tsb(3 + t) * uint64_t(nslots_), nullptr));
+  for (int t = 0; t < ntens_; ++t) {
+    weight_bytes += tsb(t) * uint64_t(recv_base_);
+    recv_bytes += tsb(t) * uint64_t(nslots_ - recv_base_);
   }
-  weight_bytes = 3 * slot_bytes * uint64_t(recv_base_);
-  recv_bytes = 3 * slot_bytes * uint64_t(nslots_ - recv_base_);
   router_w_ = static_cast<uint16_t*>(dalloc(size_t(WL_) * E_ * h_ * 2, &weight_bytes));
   bias_ = static_cast<float*>(dalloc(size_t(WL_) * E_ * 4, &weight_bytes));
   DWDP_CUDA(cudaMemset(bias_, 0, size_t(WL_) * E_ * 4));
@@ -132,11 +141,19 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   zeros_ = static_cast<int32_t*>(dalloc(nz * 4, &workspace_bytes));
   DWDP_CUDA(cudaMemset(zeros_, 0, nz * 4));
 
-  tm_gate_ = make_tmap_bf16(arena_[0], int64_t(nslots_) * f_, h_, 128);
-  tm_up_ = make_tmap_bf16(arena_[1], int64_t(nslots_) * f_, h_, 128);
-  tm_down_ = make_tmap_bf16(arena_[2], int64_t(nslots_) * h_, f_, 256);
+  auto tmap = fp8_ ? make_tmap_i8 : make_tmap_bf16;  // e4m3 tiles use the byte map
+  tm_gate_ = tmap(arena_[0], int64_t(nslots_) * f_, h_, 128);
+  tm_up_ = tmap(arena_[1], int64_t(nslots_) * f_, h_, 128);
+  tm_down_ = tmap(arena_[2], int64_t(nslots_) * h_, f_, 256);
   tm_xperm_ = make_tmap_bf16(xperm_, max_rows_, h_, 128);
   tm_h_ = make_tmap_bf16(hbuf_, max_rows_, f_, 128);
+  if (fp8_) {
+    h8_ = static_cast<uint8_t*>(dalloc(size_t(max_rows_) * f_, &workspace_bytes));
+    xs_ = static_cast<float*>(dalloc(size_t(max_rows_) * 4, &workspace_bytes));
+    hs_ = static_cast<float*>(dalloc(size_t(max_rows_) * 4, &workspace_bytes));
+    tm_x8_ = make_tmap_i8(xperm_, max_rows_, h_, 128);  // X_perm8 reuses the xperm_ bytes
+    tm_h8_ = make_tmap_i8(h8_, max_rows_, f_, 128);
+  }
 
   DWDP_CUDA(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
   for (int i = 1; i < std::max(1, c.ce_inflight); ++i) {
@@ -152,7 +169,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   DWDP_CUDA(cudaEventCreate(&epoch_));
   DWDP_CUDA(cudaEventRecord(epoch_, copy_st_));
   for (auto& ev : moe_done_) DWDP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  for (int t = 0; t < 3; ++t) peer_arena_[t].assign(size_t(N_), nullptr);
+  for (int t = 0; t < 6; ++t) peer_arena_[t].assign(size_t(N_), nullptr);
   resident_parity_.assign(size_t(L_), 0);
   build_copy_plan();
   DWDP_CUDA(cudaDeviceSynchronize());
@@ -180,7 +197,8 @@ Ctx::~Ctx() {
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   void* bufs[] = {arena_[0], arena_[1], arena_[2], router_w_, bias_, slot_tab_, logits_, idx_,
                   wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_,
-                  router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_, mbseg_, dep_seg_, srcrow_};
+                  router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_, mbseg_, dep_seg_, srcrow_,
+                  sarena_[0], sarena_[1], sarena_[2], h8_, xs_, hs_};
   if (dep_seg_host_) cudaFreeHost(dep_seg_host_);
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -262,18 +280,17 @@ void Ctx::build_copy_plan() {
   }
   std::stable_sort(base.begin(), base.end(),
                    [](const ShardRun& a, const ShardRun& b) { return a.peer < b.peer; });
-  const uint64_t slot_bytes = uint64_t(slot_elems_) * 2;
   std::vector<ShardRef> shards;
   uint64_t max_size = 0;
-  for (int t = 0; t < 3; ++t)
+  for (int t = 0; t < ntens_; ++t)  // 3 weight tensors (+ 3 fp8 scale tensors)
     for (const auto& b : base) {
       ShardRun r = b;
       r.tensor = t;
-      r.param_id = uint64_t(t) + 3 * b.param_id;  // b.param_id = run index within peer
+      r.param_id = uint64_t(t) + uint64_t(ntens_) * b.param_id;  // b.param_id = run index within peer
       runs_.push_back(r);
-      shards.push_back({r.peer, r.param_id, uint64_t(r.count) * slot_bytes,
-                        uint64_t(r.src_slot0) * slot_bytes});
-      max_size = std::max(max_size, uint64_t(r.count) * slot_bytes);
+      shards.push_back({r.peer, r.param_id, uint64_t(r.count) * tsb(t),
+                        uint64_t(r.src_slot0) * tsb(t)});
+      max_size = std::max(max_size, uint64_t(r.count) * tsb(t));
     }
   const uint64_t slice = cfg.tdm ? cfg.slice_size : max_size;
   plan_slices_ = dwdp::build_copy_plan(shards, slice, rank_);
@@ -281,15 +298,12 @@ void Ctx::build_copy_plan() {
 }
 
 void* Ctx::peer_src(int peer, int t, int wl, uint64_t src_offset) const {
-  const uint64_t slot_bytes = uint64_t(slot_elems_) * 2;
-  return static_cast<uint8_t*>(peer_arena_[t][size_t(peer)]) + uint64_t(wl) * c_ * slot_bytes +
+  return static_cast<uint8_t*>(peer_arena_[t][size_t(peer)]) + uint64_t(wl) * c_ * tsb(t) +
          src_offset;
 }
 
 uint8_t* Ctx::dst_addr(int t, int parity, const ShardRun& r, uint64_t dst_offset) const {
-  const uint64_t slot_bytes = uint64_t(slot_elems_) * 2;
-  return reinterpret_cast<uint8_t*>(arena_[t]) +
-         uint64_t(recv_base_ + parity * nrecv_ + r.dst_slot0) * slot_bytes + dst_offset;
+  return tbase(t) + uint64_t(recv_base_ + parity * nrecv_ + r.dst_slot0) * tsb(t) + dst_offset;
 }
 
 // ===================================================================== //
@@ -303,7 +317,8 @@ void Ctx::export_ipc(void* out) {
   b.nslots = nslots_;
   b.c = c_;
   b.slot_elems = slot_elems_;
-  for (int t = 0; t < 3; ++t) DWDP_CUDA(cudaIpcGetMemHandle(&b.h[t], arena_[t]));
+  b.ntens = ntens_;
+  for (int t = 0; t < ntens_; ++t) DWDP_CUDA(cudaIpcGetMemHandle(&b.h[t], tbase(t)));
   std::memset(out, 0, DWDP_IPC_BLOB_BYTES);
   std::memcpy(out, &b, sizeof b);
 }
@@ -315,8 +330,9 @@ void Ctx::open_peers(const void* blobs) {
     IpcBlob b;
     std::memcpy(&b, static_cast<const uint8_t*>(blobs) + size_t(p) * DWDP_IPC_BLOB_BYTES, sizeof b);
     require(b.magic == kIpcMagic && b.rank == p, "open_peers: malformed blob");
-    require(b.c == c_ && b.slot_elems == slot_elems_, "open_peers: peer arena geometry differs");
-    for (int t = 0; t < 3; ++t) {
+    require(b.c == c_ && b.slot_elems == slot_elems_ && b.ntens == ntens_,
+            "open_peers: peer arena geometry differs");
+    for (int t = 0; t < ntens_; ++t) {
       void* ptr = nullptr;
       DWDP_CUDA(cudaIpcOpenMemHandle(&ptr, b.h[t], cudaIpcMemLazyEnablePeerAccess));
       peer_arena_[t][size_t(p)] = ptr;
@@ -335,7 +351,7 @@ void Ctx::link_local(const std::vector<Ctx*>& all) {
       if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) DWDP_CUDA(e);
       cudaGetLastError();
     }
-    for (int t = 0; t < 3; ++t) peer_arena_[t][size_t(o->rank_)] = o->arena_[t];
+    for (int t = 0; t < ntens_; ++t) peer_arena_[t][size_t(o->rank_)] = o->tbase(t);
   }
   // Pull-kernel work lists for every (weight layer, parity).
   if (nrecv_ == 0) return;
@@ -379,7 +395,11 @@ void Ctx::init_weights(float bias_scale) {
       if (shared_) seeds[size_t(shared_base_ + wl)] = tensor_seed(base, wl, E_, t);
     }
     DWDP_CUDA(cudaMemcpy(dseeds, seeds.data(), size_t(owned) * 8, cudaMemcpyHostToDevice));
-    launch_fill_slots(arena_[t], dseeds, owned, slot_elems_, t == 2 ? sf : sh, nullptr);
+    if (fp8_)  // e4m3 rows + per-row scales over the same bf16 values
+      launch_fp8_fill_rows(tbase(t), sarena_[t], dseeds, owned, int(trows(t)), t == 2 ? f_ : h_,
+                           t == 2 ? sf : sh, nullptr);
+    else
+      launch_fill_slots(arena_[t], dseeds, owned, slot_elems_, t == 2 ? sf : sh, nullptr);
     ++launches;
     DWDP_CUDA(cudaGetLastError());
   }
@@ -405,12 +425,11 @@ void Ctx::set_bias(const float* host) {
 
 void Ctx::read_expert(int layer, int expert, int t, void* host) {
   DeviceGuard dg(cfg.device);
-  require(layer >= 0 && layer < L_ && expert >= 0 && expert <= E_ && t >= 0 && t < 3,
+  require(layer >= 0 && layer < L_ && expert >= 0 && expert <= E_ && t >= 0 && t < ntens_,
           "read_expert: index out of range");
   require(expert < E_ || shared_, "read_expert: no shared expert");
   const int slot = slot_of(layer, resident_parity_[size_t(layer)], expert);
-  DWDP_CUDA(cudaMemcpy(host, arena_[t] + int64_t(slot) * slot_elems_, size_t(slot_elems_) * 2,
-                       cudaMemcpyDeviceToHost));
+  DWDP_CUDA(cudaMemcpy(host, tbase(t) + uint64_t(slot) * tsb(t), tsb(t), cudaMemcpyDeviceToHost));
 }
 
 // ===================================================================== //
@@ -544,12 +563,34 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   const int wl = layer % WL_;
   route_logits(wl, x, T, st);
   mark(0);
+  const int64_t mb_ub = (T * k_ + int64_t(E_) * 127) / 128 + 1 + (shared_ ? (T + 127) / 128 : 0);
+  const int32_t* stab = slot_tab_ + (size_t(layer) * 2 + size_t(parity)) * (E_ + 1);
+  if (fp8_) {
+    // W8A8: the permute writes e4m3 copies of every routed row and of the
+    // shared-expert rows (after meta[2]) with per-row scales; GEMM1 emits
+    // bf16 H, which is re-quantised per row for GEMM2.
+    uint8_t* x8 = reinterpret_cast<uint8_t*>(xperm_);
+    launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_,
+                   nullptr, scratch_, st, x8, xs_);
+    mark(1);
+    GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 0, mbseg_,
+                nullptr, xs_, sarena_[0], sarena_[1]};
+    launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_x8_, tm_x8_, tm_gate_, tm_up_, g1,
+                        int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
+    launch_quant_rows_fp8(hbuf_, max_rows_, f_, meta_, h8_, hs_, st);
+    mark(2);
+    GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
+                nullptr, hs_, sarena_[2], nullptr};
+    launch_grouped_gemm(GEMM_PLAIN_FP8, tm_h8_, tm_h8_, tm_down_, tm_down_, g2,
+                        int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
+    mark(3);
+    launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
+    launches += 9;
+  } else {
   launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_, xperm_,
                  scratch_, st);
   mark(1);
-  const int64_t mb_ub = (T * k_ + int64_t(E_) * 127) / 128 + 1 + (shared_ ? (T + 127) / 128 : 0);
   const CUtensorMap tm_x = shared_ ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
-  const int32_t* stab = slot_tab_ + (size_t(layer) * 2 + size_t(parity)) * (E_ + 1);
   // Routed A rows come from the materialised expert-major copy. (GEMM1 can
   // also gather them from x with TMA tile::gather4 via GemmArgs::a_rows; on
   // B200 that measured 2.5x slower: 32 scattered 128-byte row fetches per
@@ -562,6 +603,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   mark(3);
   launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
   launches += 8;
+  }
   if (timed) {
     if (!meta_ring_) DWDP_CUDA(cudaHostAlloc(&meta_ring_, kMetaRing * 4 * sizeof(int32_t), 0));
     rec->meta_slot = meta_ring_pos_;
@@ -590,11 +632,10 @@ void Ctx::layer_forward(int64_t g, const uint16_t* x, int64_t T, uint16_t* y, bo
   if (nrecv_ > 0 && (plan_of_g_.size() <= size_t(g + 1) || plan_of_g_[size_t(g + 1)] == -2))
     prefetch_issue(g + 1);
   if (nrecv_ > 0 && !cfg.merge_elim) {  // D2D merge baseline (simcore.cpp:700-703)
-    const uint64_t bytes = uint64_t(nrecv_) * uint64_t(slot_elems_) * 2;
-    for (int t = 0; t < 3; ++t)
-      DWDP_CUDA(cudaMemcpyAsync(arena_[t] + int64_t(merge_base_) * slot_elems_,
-                                arena_[t] + int64_t(recv_base_ + par * nrecv_) * slot_elems_, bytes,
-                                cudaMemcpyDeviceToDevice, st));
+    for (int t = 0; t < ntens_; ++t)
+      DWDP_CUDA(cudaMemcpyAsync(tbase(t) + uint64_t(merge_base_) * tsb(t),
+                                tbase(t) + uint64_t(recv_base_ + par * nrecv_) * tsb(t),
+                                uint64_t(nrecv_) * tsb(t), cudaMemcpyDeviceToDevice, st));
     rec.merge_end = take_event();
     DWDP_CUDA(cudaEventRecord(rec.merge_end, st));
   }

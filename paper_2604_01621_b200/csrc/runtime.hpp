@@ -114,10 +114,27 @@ class Ctx {
   std::vector<int> local_index_;  // expert -> index in local set, -1 if remote
   std::vector<int> recv_index_;   // expert -> slot in receive region, -1 if local
   // arenas: 0 gate [slots][f][h], 1 up [slots][f][h], 2 down [slots][h][f]
+  // (bf16, or e4m3 bytes when fp8); fp8 adds per-row fp32 scale arenas
+  // 3 gate [slots][f], 4 up [slots][f], 5 down [slots][h]. Every tensor
+  // arena is one IPC object and one prefetched "param" of the copy plan.
   uint16_t* arena_[3] = {nullptr, nullptr, nullptr};
+  float* sarena_[3] = {nullptr, nullptr, nullptr};
+  bool fp8_ = false;
+  int esz_ = 2, ntens_ = 3;
   int64_t slot_elems_ = 0;
   int nslots_ = 0, shared_base_ = 0, recv_base_ = 0, merge_base_ = 0;
-  std::vector<void*> peer_arena_[3];   // per peer rank (nullptr for self)
+  std::vector<void*> peer_arena_[6];   // per tensor arena, per peer rank (nullptr for self)
+  uint8_t* tbase(int t) const {
+    return t < 3 ? reinterpret_cast<uint8_t*>(arena_[t]) : reinterpret_cast<uint8_t*>(sarena_[t - 3]);
+  }
+  int64_t trows(int t) const { return (t % 3) == 2 ? h_ : f_; }  // rows per slot
+  uint64_t tsb(int t) const {  // bytes per slot of tensor arena t
+    return t < 3 ? uint64_t(slot_elems_) * uint64_t(esz_) : uint64_t(trows(t)) * 4;
+  }
+  // W8A8 activations
+  uint8_t* h8_ = nullptr;               // e4m3 H [max_rows][f]
+  float *xs_ = nullptr, *hs_ = nullptr;  // per-row scales of X_perm8 / H8
+  CUtensorMap tm_x8_, tm_h8_;
   std::vector<void*> ipc_opened_;
   uint16_t* router_w_ = nullptr;       // [WL][E][h]
   float* bias_ = nullptr;              // [WL][E]

@@ -10,7 +10,7 @@ from dataclasses import asdict, dataclass
 
 import numpy as np
 
-from ._lib import (ENGINE_COPY, IPC_BLOB_BYTES, CtxConfigC, LayerRecordC, SliceC, check, lib)
+from ._lib import (ENGINE_COPY, IPC_BLOB_BYTES, WEIGHT_FP8, CtxConfigC, LayerRecordC, SliceC, check, lib)
 from .planning import Slice
 
 
@@ -40,7 +40,7 @@ class DwdpConfig:
     engine: int = ENGINE_COPY
     pull_ctas: int = 148      # pull-kernel CTAs (one per SM, co-resident with the GEMM)
     ce_inflight: int = 2      # copy-engine transfers in flight (reference GpuSpec default 2)
-    reserved0: int = 0
+    weight_dtype: int = 0     # 0 bf16, 1 fp8 e4m3 (W8A8, per-channel weight scales)
     weight_seed: int = 2604_01621
     weight_layers: int = 0    # 0 = num_layers
     kernel_timing: int = 0    # CUDA events between the layer's kernels
@@ -119,10 +119,15 @@ class DwdpContext:
         check(lib().dwdp_ctx_set_bias(self.h, b.ctypes.data))
 
     def read_expert(self, layer: int, expert: int, t: int) -> np.ndarray:
-        rows, cols = (self.cfg.ffn, self.cfg.hidden) if t < 2 else (self.cfg.hidden, self.cfg.ffn)
-        out = np.zeros(rows * cols, np.uint16)
+        """Resident copy of tensor t (0 gate, 1 up, 2 down: bf16 bits, or e4m3
+        bytes for fp8 weights; fp8 only: 3/4/5 = their per-row fp32 scales)."""
+        rows, cols = (self.cfg.ffn, self.cfg.hidden) if t % 3 < 2 else (self.cfg.hidden, self.cfg.ffn)
+        if t >= 3:
+            out = np.zeros(rows, np.float32)
+        else:
+            out = np.zeros(rows * cols, np.uint8 if self.cfg.weight_dtype == WEIGHT_FP8 else np.uint16)
         check(lib().dwdp_ctx_read_expert(self.h, layer, expert, t, out.ctypes.data))
-        return out.reshape(rows, cols)
+        return out if t >= 3 else out.reshape(rows, cols)
 
     # -- prefetch handles (CopyEngineSim API) -------------------------------
     def prefetch_issue(self, global_layer: int) -> int:

@@ -136,6 +136,98 @@ def test_moe_forward_vs_oracle(dev, ctxs, orc, name, T):
     assert err < TOL, err
 
 
+# ---------------------------------------------------------------- fp8 W8A8
+
+TOL_FP8 = 1e-2   # vs the oracle's W8A8 emulation (fp32 sum order, rare bf16-H ulp flips)
+TOL_FP8_Q = 8e-2  # quantisation error vs the bf16 oracle (e4m3 weights + activations)
+
+FP8_CONFIGS = {
+    "tiny_fp8": D.DwdpConfig.tiny(weight_dtype=D.WEIGHT_FP8),
+    "mid_fp8": D.DwdpConfig(num_layers=1, num_experts=64, hidden=1024, ffn=256, shared_ffn=256,
+                            top_k=6, n_group=8, topk_group=4, max_tokens=2048,
+                            weight_dtype=D.WEIGHT_FP8),
+    "r1_fp8": D.DwdpConfig(num_layers=1, max_tokens=512, weight_dtype=D.WEIGHT_FP8),
+}
+
+
+@pytest.fixture(scope="module")
+def ctxs8(dev):
+    out = {}
+    for name, cfg in FP8_CONFIGS.items():
+        c = D.DwdpContext(cfg)
+        c.init_weights()
+        if cfg.scoring == 1:
+            c.set_bias(_bias(cfg))
+        out[name] = c
+    yield out
+    for c in out.values():
+        c.close()
+
+
+@pytest.mark.parametrize("name", ["tiny_fp8", "mid_fp8"])
+def test_fp8_weights_bit_exact(dev, ctxs8, orc, name):
+    """Resident e4m3 expert rows + per-row scales == oracle quantisation of
+    the same counter-hash bf16 rows."""
+    cfg = FP8_CONFIGS[name]
+    h, f = cfg.hidden, cfg.ffn
+    for e in (0, cfg.num_experts - 1) + ((cfg.num_experts,) if cfg.shared_ffn else ()):
+        for t in range(3):
+            rows, K = (f, h) if t < 2 else (h, f)
+            sc = _scale(h) if t < 2 else _scale(f)
+            w = O.bf16_to_f32(orc.fill_bf16(orc.tensor_seed(cfg.weight_seed, 0, e, t), rows * K, sc))
+            q = ctxs8[name].read_expert(0, e, t)
+            s = ctxs8[name].read_expert(0, e, 3 + t)
+            for r in (0, 1, rows // 2, rows - 1):
+                oq, os_ = orc.quant_row_e4m3(w[r * K:(r + 1) * K])
+                assert (q[r] == oq).all(), (e, t, r)
+                assert np.float32(s[r]) == np.float32(os_), (e, t, r)
+
+
+@pytest.mark.parametrize("name,T", [("tiny_fp8", 1), ("tiny_fp8", 300), ("mid_fp8", 200),
+                                    ("mid_fp8", 1), ("r1_fp8", 16)])
+def test_moe_forward_fp8_vs_oracle(dev, ctxs8, orc, name, T):
+    cfg = FP8_CONFIGS[name]
+    x = make_x(T, cfg.hidden, 11 + T, dev)
+    y = ctxs8[name].moe_forward(0, x)
+    torch.cuda.synchronize()
+    oc = oracle_cfg(cfg)
+    oc.w8a8 = 1
+    yo8, _, _ = orc.moe_forward_seeded(oc, cfg.weight_seed, 0, _bf16_np(x).reshape(-1), T, _bias(cfg))
+    yo, _, _ = orc.moe_forward_seeded(oracle_cfg(cfg), cfg.weight_seed, 0, _bf16_np(x).reshape(-1), T,
+                                      _bias(cfg))
+    yd = y.float().cpu().numpy()
+    assert _rel(yd, yo8) < TOL_FP8, _rel(yd, yo8)
+    assert _rel(yd, yo) < TOL_FP8_Q, _rel(yd, yo)
+
+
+def test_dwdp_fp8_group_of_two_matches_all_local(dev):
+    """fp8 arenas (weights + scale tensors) prefetched over the pull kernel
+    give bit-identical outputs to the all-local fp8 model."""
+    kw = dict(MID, weight_dtype=D.WEIGHT_FP8)
+    full = D.DwdpContext(D.DwdpConfig(**kw))
+    full.init_weights()
+    for engine in (D.ENGINE_COPY, D.ENGINE_PULL):
+        ranks = [D.DwdpContext(D.DwdpConfig(**kw, rank=r, group_size=2, engine=engine,
+                                            slice_size=1 << 20)) for r in range(2)]
+        for c in ranks:
+            c.init_weights()
+        D.DwdpContext.link_local(ranks)
+        xs = [make_x(90 + 41 * r, MID["hidden"], 70 + r, dev) for r in range(2)]
+        for g in range(4):
+            for r in range(2):
+                y = ranks[r].layer_forward(g, xs[r], residual=False)
+                yf = full.moe_forward(g % 3, xs[r])
+                torch.cuda.synchronize()
+                assert torch.equal(y, yf), (engine, g, r)
+        recs = ranks[0].records()
+        # (E - c) experts x (3 e4m3 tensors + 3 fp32 scale vectors)
+        h, f = MID["hidden"], MID["ffn"]
+        assert recs[1]["prefetch_bytes"] == 32 * (3 * h * f + 4 * (2 * f + h))
+        for c in ranks:
+            c.close()
+    full.close()
+
+
 def test_empty_batch_is_a_noop(dev, ctxs):
     x = torch.empty((0, 512), dtype=torch.bfloat16, device=dev)
     ctxs["tiny"].moe_forward(0, x)

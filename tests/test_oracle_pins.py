@@ -141,3 +141,18 @@ def test_oracle_permute_is_stable_expert_major(orc):
 def test_det_expf_accuracy(orc):
     for v in np.linspace(-20, 20, 101, dtype=np.float32):
         assert abs(orc.expf(float(v)) - np.exp(np.float64(v))) <= 4e-7 * np.exp(np.float64(v))
+
+
+def test_e4m3_encode_matches_torch(orc):
+    """The oracle's integer e4m3 encoder (shared bit for bit with the device
+    quantisers) equals torch's float8_e4m3fn cast inside +-448."""
+    import torch
+    rng = np.random.default_rng(0)
+    x = np.concatenate([rng.standard_normal(20000).astype(np.float32) * s
+                        for s in (1e-3, 0.1, 1.0, 10.0, 100.0)])
+    x = np.concatenate([x, np.float32([0.0, -0.0, 448.0, -448.0, 2 ** -9, 2 ** -10,
+                                       3 * 2 ** -10, 1.5 * 2 ** -9, 2 ** -6, 0.9 * 2 ** -6])])
+    x = x[np.abs(x) <= 448]
+    ref = torch.from_numpy(x).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+    assert (orc.e4m3_encode(x) == ref).all()
+    assert orc.e4m3_encode(np.float32([1e6, -1e6]))[0] == 0x7E  # saturates (no inf in e4m3fn)
