@@ -31,6 +31,11 @@ sys.path.insert(0, ROOT)
 
 METRIC = "output tokens/sec/GPU at 1/2/4/8 B200 vs DEP; exposed prefetch ms/layer"
 R1 = dict(h=7168, E=256, k=8, f=2048, fs=2048)
+# Zipf skew on the device router: bias_e = -beta*s*ln(e+1) added to the
+# sigmoid scores (selection only). beta = 0.05 gives a routed-count CV of 2.05
+# at s = 0.8 on the R1 router, matching the reference's Zipf(0.8) counts
+# (route_tokens, src/workload.cpp:85-111: CV 1.97); calibration in DESIGN.md.
+ZIPF_BETA = 0.05
 
 
 def peaks():
@@ -169,6 +174,12 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=16)
     ap.add_argument("--ref-tokens", type=int, default=16)
     ap.add_argument("--profile", action="store_true", help="1 layer, for ncu captures")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp8"],
+                    help="expert weights: bf16, or e4m3 W8A8 with per-row scales (config 5)")
+    ap.add_argument("--decode", type=int, default=0,
+                    help="decode phase (config 5): B tokens/rank every step instead of prefill batches")
+    ap.add_argument("--zipf", type=float, default=0.0,
+                    help="expert-routing skew s: router bias -ZIPF_BETA*s*ln(e+1)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -201,10 +212,14 @@ def main():
     layers = 1 if args.profile else args.layers
     model = D.r1_model(layers)
     iters = args.warmup + args.steps
-    spec = D.WorkloadSpec(D.IslDist.from_cv(8192, args.cv), args.tokens,
-                          max(1, args.tokens // 8192), 0.0, 7)
-    batches = D.sample_batches(spec, model, world, iters, with_routing=False)
-    toks = [[b.tokens[r] for r in range(world)] for b in batches]
+    if args.decode:  # one output token per request, B requests per rank
+        toks = [[args.decode] * world for _ in range(iters)]
+    else:
+        spec = D.WorkloadSpec(D.IslDist.from_cv(8192, args.cv), args.tokens,
+                              max(1, args.tokens // 8192), 0.0, 7)
+        batches = D.sample_batches(spec, model, world, iters, with_routing=False)
+        toks = [[b.tokens[r] for r in range(world)] for b in batches]
+    fp8 = args.dtype == "fp8"
 
     cfg = D.DwdpConfig(num_layers=layers, rank=rank, group_size=world, device=local,
                        engine=D.ENGINE_PULL if args.engine == "pull" else D.ENGINE_COPY,
@@ -212,9 +227,13 @@ def main():
                        merge_elim=0 if args.merged else 1, pull_ctas=args.pull_ctas,
                        ce_inflight=args.ce_inflight,
                        weight_layers=layers if world > 1 else 1, kernel_timing=1,
-                       max_tokens=args.tokens)
+                       max_tokens=args.decode or args.tokens,
+                       weight_dtype=D.WEIGHT_FP8 if fp8 else D.WEIGHT_BF16)
     ctx = D.DwdpContext(cfg)
     ctx.init_weights()
+    if args.zipf > 0:
+        import numpy as np
+        ctx.set_bias((-ZIPF_BETA * args.zipf * np.log(np.arange(R1["E"]) + 1.0)).astype(np.float32))
     if world > 1:
         blobs = [None] * world
         dist.all_gather_object(blobs, ctx.export_ipc())
@@ -231,6 +250,12 @@ def main():
     D.fill_bf16(x, 0xC0FFEE + rank, 1.0)
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream()
+    # routed-count statistics of rank 0's first batch (skew and touched experts)
+    _, _, cnt, _, _ = ctx.route(0, x[:toks[0][rank]])
+    cnt = cnt.double().cpu()
+    routing = {"count_cv": float(cnt.std(unbiased=False) / cnt.mean()),
+               "touched_experts": int((cnt > 0).sum()), "zipf_s": args.zipf,
+               "bias": f"-{ZIPF_BETA}*s*ln(e+1)" if args.zipf > 0 else "0"}
 
     for it in range(args.warmup):
         T = toks[it][rank]
@@ -282,9 +307,28 @@ def main():
     g2_flops = sum(2.0 * (r["tokens"] * k + r["tokens"]) * f * h for r in recs)
     pk = peaks()
     achieved = g1_flops / (g1_ns * 1e-9) / 1e12 if g1_ns else 0.0
+    esz = 1 if fp8 else 2
+    if args.decode:
+        # decode: GEMM1 streams the gate/up rows of every touched expert once
+        # (+ the shared expert); token rows are noise next to 2*f*h*esz bytes
+        g1_bytes = (routing["touched_experts"] + 1) * 2 * f * h * esz
+        gbs = g1_bytes * len(recs) / (g1_ns * 1e-9) / 1e9 if g1_ns else 0.0
+        roof = {"bound": "hbm", "kernel": "grouped GEMM1 (gate/up + SwiGLU, tcgen05), weight streaming",
+                "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+                "peak_source": pk["source"] + ", HBM copy",
+                "bytes_per_launch": g1_bytes, "tflops": achieved, "traffic": None}
+    else:
+        tpk = pk["bf16_tflops_sustained"] * (2 if fp8 else 1)
+        roof = {"bound": "tensor", "kernel": "grouped GEMM1 (gate/up + SwiGLU, tcgen05)",
+                "achieved": achieved, "peak": tpk, "unit": "TFLOP/s", "frac": achieved / tpk,
+                "peak_source": pk["source"] + (", sustained bf16 x 2 (fp8 dense rate; no measured fp8 figure)"
+                                               if fp8 else ", sustained bf16"),
+                "flops_per_launch": g1_flops / max(len(recs), 1),
+                "gemm2_tflops": g2_flops / (g2_ns * 1e-9) / 1e12 if g2_ns else None,
+                "traffic": traffic if not fp8 else None}
     split = {key: sum(r[key] for r in recs) / 1e6 / max(len(recs), 1)
              for key in ("router_ns", "permute_ns", "gemm1_ns", "gemm2_ns", "combine_ns",
-                         "moe_ns", "gate_wait_ns", "prefetch_ns")}
+                         "moe_ns", "gate_wait_ns", "prefetch_ns", "merge_ns")}
     exposed_ms = split["gate_wait_ns"]
     pf_bytes = sum(r["prefetch_bytes"] for r in recs)
     pf_ns = sum(r["prefetch_ns"] for r in recs)
@@ -362,9 +406,13 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "e4m3 (W8A8, fp32 accumulate)" if fp8 else "bf16",
             "data": "synthetic (counter-hash random-init weights and activations)",
-            "config": {"workload": ("R1 MoE stack, config 2 (all experts local)" if world == 1
+            "config": {"workload": (f"R1 MoE stack, config 5 (decode B={args.decode}, "
+                                    f"{'fp8' if fp8 else 'bf16'}, zipf {args.zipf}, "
+                                    f"{'merged' if args.merged else 'split'} fetch)" if args.decode
+                                    else "R1 MoE stack, config 2 (all experts local)" if world == 1
                                     else "R1 MoE stack, config 3 (DWDP)"),
                        "layers": layers, "hidden": h, "experts": 256, "top_k": k, "ffn": f,
                        "shared_experts": 1, "mnt_tokens_per_rank": args.tokens,
@@ -374,21 +422,17 @@ def main():
                                    else f"{256 // world} owned experts/layer/GPU, {layers} layers"),
                        "prefetch_engine": (engines if world > 1 else None),
                        "slice_size": args.slice_size if world > 1 else None,
-                       "l2": "inputs larger than L2: 22.5 GB of expert weights per layer",
+                       "l2": "inputs larger than L2: {} GB of expert weights per layer".format(
+                           "11.3 (e4m3)" if fp8 else "22.5 (bf16)"),
                        "parallelism": f"dwdp{world}"},
             "tokens_per_s_per_gpu": value / world,
             "exposed_prefetch_ms_per_layer": exposed_ms,
+            "merge_ms_per_layer": split["merge_ns"] if args.merged else None,
             "prefetch": ({"bytes_per_layer": pf_bytes / max(len(recs), 1),
                           "gbs": pf_bytes / pf_ns if pf_ns else None,
                           "ms_per_layer": split["prefetch_ns"]} if world > 1 else None),
             "kernel_ms_per_layer": {k2.replace("_ns", ""): v for k2, v in split.items()},
-            "roofline": {"bound": "tensor", "kernel": "grouped GEMM1 (gate/up + SwiGLU, tcgen05)",
-                         "achieved": achieved, "peak": pk["bf16_tflops_sustained"],
-                         "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops_sustained"],
-                         "peak_source": pk["source"] + ", sustained bf16",
-                         "flops_per_launch": g1_flops / max(len(recs), 1),
-                         "gemm2_tflops": g2_flops / (g2_ns * 1e-9) / 1e12 if g2_ns else None,
-                         "traffic": traffic},
+            "roofline": roof, "routing": routing,
             "dep_baseline": dep,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -29,7 +29,7 @@ namespace {
 struct NcclId {
   char internal[DWDP_NCCL_ID_BYTES];
 };
-constexpr int kBf16 = 9, kInt32 = 2;
+constexpr int kUint8 = 1, kInt32 = 2, kFloat32 = 7, kBf16 = 9;
 
 struct Nccl {
   int (*GetUniqueId)(NcclId*) = nullptr;
@@ -99,7 +99,6 @@ void Ctx::dep_init(const void* unique_id) {
   require(N_ >= 2, "dep: group_size must be >= 2");
   require(E_ % N_ == 0, "dep: group_size must divide num_experts");
   require(nccl_ == nullptr, "dep: already initialised");
-  require(!fp8_, "dep: the DEP baseline runs bf16 weights only");
   NcclId id;
   std::memcpy(&id, unique_id, sizeof id);
   nccl_check(nccl().CommInitRank(&nccl_, N_, id, rank_), "ncclCommInitRank");
@@ -124,6 +123,15 @@ void Ctx::dep_reserve(int64_t rows) {
   dep_cap_rows_ = rows;
   tm_dep_recv_ = make_tmap_bf16(dep_recv_, rows, h_, 128);
   tm_dep_h_ = make_tmap_bf16(dep_h_, rows, f_, 128);
+  if (fp8_) {
+    for (void* b : {static_cast<void*>(dep_h8_), static_cast<void*>(dep_xs_), static_cast<void*>(dep_hs_)})
+      if (b) cudaFree(b);
+    dep_h8_ = static_cast<uint8_t*>(dalloc(size_t(rows) * f_, nullptr));
+    dep_xs_ = static_cast<float*>(dalloc(size_t(rows) * 4, nullptr));
+    dep_hs_ = static_cast<float*>(dalloc(size_t(rows) * 4, nullptr));
+    tm_dep_x8_ = make_tmap_i8(dep_recv_, rows, h_, 128);
+    tm_dep_h8_ = make_tmap_i8(dep_h8_, rows, f_, 128);
+  }
   const int64_t need_tab = rows / 128 + 16;
   if (need_tab > dep_tab_cap_) {
     cudaFree(dep_tab_);
@@ -164,7 +172,12 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   // 1. router + top-k + permute of the rank's own tokens (send layout)
   if (T > 0) route_logits(wl, x, T, st);
   mark(&rec.k[0]);
-  if (T > 0)
+  // fp8: e4m3 send rows + scales, the shared-expert rows after the routed ones
+  uint8_t* x8 = reinterpret_cast<uint8_t*>(xperm_);
+  if (T > 0 && fp8_)
+    launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_,
+                   nullptr, scratch_, st, x8, xs_);
+  else if (T > 0)
     launch_permute(idx_, x, T, E_, k_, h_, 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_, xperm_, scratch_, st);
   else
     DWDP_CUDA(cudaMemsetAsync(counts_, 0, size_t(E_) * 4, st));
@@ -195,6 +208,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
     acc += r;
   }
   const int64_t routed_rows = acc;
+  const int64_t send_total = send_off[nr - 1] + send_rows[nr - 1];
   const int64_t shared_blocks = shared_ ? (T + 127) / 128 : 0;
   dep_reserve(routed_rows + shared_blocks * 128);
   // m-block -> expert over the receive layout, then the shared expert blocks
@@ -221,35 +235,65 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
                             cudaMemcpyHostToDevice, st));
   DWDP_CUDA(cudaMemcpyAsync(dep_seg_, dep_seg_host_, size_t(nblocks + 1) * sizeof(int2),
                             cudaMemcpyHostToDevice, st));
-  // 3. dispatch all-to-all
+  // 3. dispatch all-to-all (bf16 rows, or e4m3 rows + their fp32 scales)
   const size_t rowel = size_t(h_);
+  uint8_t* r8 = reinterpret_cast<uint8_t*>(dep_recv_);
   nccl_check(n.GroupStart(), "ncclGroupStart");
   for (int p = 0; p < N_; ++p) {
     if (p == rank_) continue;
-    if (send_rows[size_t(p)])
-      nccl_check(n.Send(xperm_ + send_off[size_t(p)] * h_, size_t(send_rows[size_t(p)]) * rowel,
-                        kBf16, p, nccl_, st), "ncclSend");
-    if (recv_rows[size_t(p)])
-      nccl_check(n.Recv(dep_recv_ + recv_off[size_t(p)] * h_, size_t(recv_rows[size_t(p)]) * rowel,
-                        kBf16, p, nccl_, st), "ncclRecv");
+    const size_t so = size_t(send_off[size_t(p)]), sr = size_t(send_rows[size_t(p)]);
+    const size_t ro = size_t(recv_off[size_t(p)]), rr = size_t(recv_rows[size_t(p)]);
+    if (fp8_) {
+      if (sr) {
+        nccl_check(n.Send(x8 + so * rowel, sr * rowel, kUint8, p, nccl_, st), "ncclSend");
+        nccl_check(n.Send(xs_ + so, sr, kFloat32, p, nccl_, st), "ncclSend");
+      }
+      if (rr) {
+        nccl_check(n.Recv(r8 + ro * rowel, rr * rowel, kUint8, p, nccl_, st), "ncclRecv");
+        nccl_check(n.Recv(dep_xs_ + ro, rr, kFloat32, p, nccl_, st), "ncclRecv");
+      }
+    } else {
+      if (sr) nccl_check(n.Send(xperm_ + so * rowel, sr * rowel, kBf16, p, nccl_, st), "ncclSend");
+      if (rr) nccl_check(n.Recv(dep_recv_ + ro * rowel, rr * rowel, kBf16, p, nccl_, st), "ncclRecv");
+    }
   }
   nccl_check(n.GroupEnd(), "ncclGroupEnd");
-  if (send_rows[size_t(rank_)])
-    DWDP_CUDA(cudaMemcpyAsync(dep_recv_ + recv_off[size_t(rank_)] * h_,
-                              xperm_ + send_off[size_t(rank_)] * h_,
-                              size_t(send_rows[size_t(rank_)]) * rowel * 2, cudaMemcpyDeviceToDevice, st));
+  if (send_rows[size_t(rank_)]) {
+    const size_t so = size_t(send_off[size_t(rank_)]), ro = size_t(recv_off[size_t(rank_)]);
+    const size_t sr = size_t(send_rows[size_t(rank_)]);
+    if (fp8_) {
+      DWDP_CUDA(cudaMemcpyAsync(r8 + ro * rowel, x8 + so * rowel, sr * rowel, cudaMemcpyDeviceToDevice, st));
+      DWDP_CUDA(cudaMemcpyAsync(dep_xs_ + ro, xs_ + so, sr * 4, cudaMemcpyDeviceToDevice, st));
+    } else {
+      DWDP_CUDA(cudaMemcpyAsync(dep_recv_ + ro * rowel, xperm_ + so * rowel, sr * rowel * 2,
+                                cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  if (fp8_ && shared_ && T > 0)  // shared-row scales follow the received rows
+    DWDP_CUDA(cudaMemcpyAsync(dep_xs_ + routed_rows, xs_ + send_total, size_t(T) * 4,
+                              cudaMemcpyDeviceToDevice, st));
   mark(&rec.comm[1]);
   // 4. expert-parallel grouped GEMMs (+ shared expert on own tokens)
   const int32_t* stab = slot_tab_ + size_t(layer) * 2 * (E_ + 1);
   const int32_t* dmeta = dep_tab_;
   const int32_t* dmb = dep_tab_ + 4;
-  if (nblocks > 0) {
+  if (nblocks > 0 && fp8_) {
+    const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_i8(x8 + send_total * h_, T, h_, 128) : tm_dep_x8_;
+    GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1, dep_seg_,
+                nullptr, dep_xs_, sarena_[0], sarena_[1]};
+    launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_dep_x8_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
+    launch_quant_rows_fp8(dep_h_, dep_cap_rows_, f_, dmeta, dep_h8_, dep_hs_, st);
+  } else if (nblocks > 0) {
     const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_dep_recv_;
     GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1, dep_seg_};
     launch_grouped_gemm(GEMM_SWIGLU, tm_dep_recv_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
   }
   mark(&rec.k[2]);
-  if (nblocks > 0) {
+  if (nblocks > 0 && fp8_) {
+    GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
+                nullptr, dep_hs_, sarena_[2], nullptr};
+    launch_grouped_gemm(GEMM_PLAIN_FP8, tm_dep_h8_, tm_dep_h8_, tm_down_, tm_down_, g2, int(nblocks * (h_ / 256)), st);
+  } else if (nblocks > 0) {
     GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_};
     launch_grouped_gemm(GEMM_PLAIN, tm_dep_h_, tm_dep_h_, tm_down_, tm_down_, g2, int(nblocks * (h_ / 256)), st);
   }
@@ -274,7 +318,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   // 6. weighted combine (shared rows follow the routed rows of the receive buffer)
   launch_combine(xperm_, row_of_, wts_, shared_ ? dep_recv_ + routed_rows * h_ : nullptr, nullptr,
                  residual ? x : nullptr, y, T, k_, h_, st);
-  launches += 8;
+  launches += fp8_ ? 9 : 8;
   DWDP_CUDA(cudaGetLastError());
   DWDP_CUDA(cudaEventRecord(rec.moe_end, st));
   rec.rows = routed_rows;

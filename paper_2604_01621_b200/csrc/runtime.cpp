@@ -184,9 +184,12 @@ Ctx::~Ctx() {
       if (e) cudaEventDestroy(e);
   nccl_destroy(nccl_);
   for (void* b : {static_cast<void*>(dep_recv_), static_cast<void*>(dep_h_),
-                  static_cast<void*>(dep_counts_all_), static_cast<void*>(dep_tab_)})
+                  static_cast<void*>(dep_counts_all_), static_cast<void*>(dep_tab_),
+                  static_cast<void*>(dep_seg_), static_cast<void*>(dep_h8_),
+                  static_cast<void*>(dep_xs_), static_cast<void*>(dep_hs_)})
     if (b) cudaFree(b);
   if (dep_counts_host_) cudaFreeHost(dep_counts_host_);
+  if (dep_seg_host_) cudaFreeHost(dep_seg_host_);
   if (dep_tab_host_) cudaFreeHost(dep_tab_host_);
   for (auto& p : plans_) {
     if (p.start) cudaEventDestroy(p.start);

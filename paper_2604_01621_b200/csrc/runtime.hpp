@@ -193,6 +193,11 @@ class Ctx {
   int2* dep_seg_host_ = nullptr;
   int64_t dep_tab_cap_ = 0;
   CUtensorMap tm_dep_recv_, tm_dep_h_;
+  // fp8 DEP: received e4m3 rows live in dep_recv_ (bytes), their scales in
+  // dep_xs_; H is re-quantised into dep_h8_ / dep_hs_
+  uint8_t* dep_h8_ = nullptr;
+  float *dep_xs_ = nullptr, *dep_hs_ = nullptr;
+  CUtensorMap tm_dep_x8_, tm_dep_h8_;
   void dep_reserve(int64_t rows);
   int num_sms_ = 148;
 };

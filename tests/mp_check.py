@@ -21,11 +21,12 @@ def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     engine = int(os.environ.get("DWDP_ENGINE", "0"))
+    wdt = int(os.environ.get("DWDP_WEIGHT", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     ctx = D.DwdpContext(D.DwdpConfig(**MID, rank=rank, group_size=world, device=local,
-                                     engine=engine, slice_size=1 << 19))
+                                     engine=engine, slice_size=1 << 19, weight_dtype=wdt))
     ctx.init_weights()
     blobs = [None] * world
     dist.all_gather_object(blobs, ctx.export_ipc())
@@ -33,7 +34,7 @@ def main():
     ids = [D.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(ids, src=0)
     ctx.dep_init(ids[0])
-    full = D.DwdpContext(D.DwdpConfig(**MID, device=local))
+    full = D.DwdpContext(D.DwdpConfig(**MID, device=local, weight_dtype=wdt))
     full.init_weights()
     torch.cuda.synchronize()
     dist.barrier()
@@ -67,7 +68,7 @@ def main():
     t = torch.tensor([bad], device=dev)
     dist.all_reduce(t)
     if rank == 0:
-        print(f"MPCHECK world={world} engine={engine} failures={int(t.item())} "
+        print(f"MPCHECK world={world} engine={engine} weight_dtype={wdt} failures={int(t.item())} "
               f"records={len(recs)} max_wait_ms={max(waits) / 1e6 if waits else 0:.3f}", flush=True)
     ctx.close()
     full.close()
