@@ -299,6 +299,16 @@ def main():
     total_tokens = sum(sum(toks[it]) for it in range(args.warmup, iters))
     value = total_tokens / (ms / 1e3)
 
+    def gather(obj):
+        if world == 1:
+            return [obj]
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    from paper_2604_01621_b200 import report as RP
+    all_recs = gather(recs)
+
     # ---- per-kernel split and roofline of the dominant kernel (grouped GEMM1)
     k, h, f = R1["k"], R1["h"], R1["f"]
     g1_ns = sum(r["gemm1_ns"] for r in recs)
@@ -385,6 +395,7 @@ def main():
         barrier()
         dms = allmax(d0.elapsed_time(d1))
         drecs = ctx.records()
+        all_drecs = gather(drecs)
         dval = total_tokens / (dms / 1e3)
         dep = {"value": dval, "unit": "tokens/s", "tokens_per_s_per_gpu": dval / world,
                "ms_per_step": dms / args.steps,
@@ -394,6 +405,26 @@ def main():
                                        for key in ("router_ns", "permute_ns", "gemm1_ns",
                                                    "gemm2_ns", "combine_ns")},
                "dwdp_over_dep": value / dval}
+
+    # ---- RunReport accounting (simcore.hpp:29-61, 177-213) over the measured
+    # events of every rank, and the analytic model beside it (a15, a16)
+    acct = None
+    if rank == 0:
+        tab = RP.report_from_records(all_recs, layers, 0)
+        acct = {"dwdp": tab.as_dict(), "breakdown_csv": tab.to_csv()}
+        if dep is not None:
+            dtab = RP.report_from_records(all_drecs, layers, 0)
+            cmp_ = RP.compare_reports(dtab, tab)  # a = DEP baseline, b = DWDP
+            acct.update(dep=dtab.as_dict(), comparison_dep_vs_dwdp=cmp_.as_dict(),
+                        comparison_csv=cmp_.to_csv())
+        if world > 1:
+            mean_t = total_tokens / (args.steps * world)
+            acct["analytic_compare"] = D.analytic_compare(
+                D.r1_model(layers, 1.0 if fp8 else 2.0),
+                D.GpuSpec(pk["bf16_tflops_sustained"] * 1e12 * (2 if fp8 else 1), pk["hbm_gbs"] * 1e9,
+                          900e9),
+                D.build_placement(R1["E"], world), int(mean_t))
+            acct["analytic_compare"]["tokens_per_rank"] = mean_t
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -433,7 +464,7 @@ def main():
                           "ms_per_layer": split["prefetch_ns"]} if world > 1 else None),
             "kernel_ms_per_layer": {k2.replace("_ns", ""): v for k2, v in split.items()},
             "roofline": roof, "routing": routing,
-            "dep_baseline": dep,
+            "dep_baseline": dep, "report": acct,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
         }

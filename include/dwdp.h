@@ -341,9 +341,79 @@ typedef struct {
   int64_t routed_rows;   /* padded expert-major rows of the layer     */
   double comm_ns;        /* DEP: dispatch + combine all-to-alls (incl.
                             the waits for the slowest rank)            */
+  double dispatch_ns;    /* DEP: the dispatch part of comm_ns          */
+  /* absolute times on the context's clock (ns since its creation): */
+  double start_ns;       /* MoeGate entry (before the weight wait)     */
+  double end_ns;         /* end of the layer's last kernel             */
+  double prefetch_start_ns, prefetch_end_ns; /* this layer's plan, -1 if none */
 } dwdp_layer_record;
 /* Drain completed layer records (synchronises the context's streams). */
 int dwdp_ctx_records(dwdp_ctx* ctx, dwdp_layer_record* out, size_t* n_inout);
+
+/* ---- RunReport / breakdown / compare_reports (simcore.hpp:29-61, 177-213;
+ * simcore.cpp:18-63, 766-876) over measured events. Categories keep the
+ * reference's Category order (hwmodel.hpp:14-23). */
+#define DWDP_CAT_ATTENTION 0
+#define DWDP_CAT_GROUPED_GEMM 1
+#define DWDP_CAT_DENSE_GEMM 2
+#define DWDP_CAT_OTHERS 3
+#define DWDP_CAT_COMMUNICATION 4
+#define DWDP_CAT_D2D_COPY 5
+#define DWDP_CAT_P2P_COPY 6
+#define DWDP_CAT_SYNC_WAIT 7
+#define DWDP_NUM_CATEGORIES 8
+/* SimEvent::detail strings as codes */
+#define DWDP_DETAIL_NONE 0
+#define DWDP_DETAIL_WEIGHT_WAIT 1
+#define DWDP_DETAIL_DISPATCH 2
+#define DWDP_DETAIL_COMBINE 3
+#define DWDP_DETAIL_BARRIER 4
+typedef struct {
+  int32_t rank;
+  int32_t stream;   /* 0 compute, 1 copy engine (Stream) */
+  int32_t category; /* DWDP_CAT_* */
+  int32_t layer;
+  int32_t iteration;
+  int32_t detail;   /* DWDP_DETAIL_* */
+  int64_t start_ns, end_ns;
+  double bytes;
+} dwdp_sim_event;
+typedef struct {
+  double compute_us[DWDP_NUM_CATEGORIES]; /* mean us per rank and steady iteration */
+  double copy_us[DWDP_NUM_CATEGORIES];
+  int32_t compute_present[DWDP_NUM_CATEGORIES]; /* category has an entry (map key) */
+  int32_t copy_present[DWDP_NUM_CATEGORIES];
+  double iteration_latency_us;
+  int32_t p2p_fully_overlapped;
+  int32_t reserved;
+  double tokens_per_s; /* RunReport::throughput_tokens_per_s */
+} dwdp_breakdown;
+typedef struct {
+  double a_us[DWDP_NUM_CATEGORIES], b_us[DWDP_NUM_CATEGORIES];
+  double delta_frac[DWDP_NUM_CATEGORIES]; /* (a - b) / a_latency */
+  int32_t has_delta[DWDP_NUM_CATEGORIES]; /* 0 for P2PCopy (off the critical path) */
+  double a_latency_us, b_latency_us, overall_frac, gross_sync_comm_pct;
+} dwdp_comparison;
+/* breakdown(RunReport) over an explicit event list; iter_* are
+ * [num_ranks][iterations] row-major. Validates per-(rank, stream) overlap. */
+int dwdp_report_breakdown(const dwdp_sim_event* events, size_t n, int num_ranks,
+                          int iterations, int warmup_iterations,
+                          const int64_t* iter_start, const int64_t* iter_end,
+                          const int64_t* iter_tokens, dwdp_breakdown* out);
+/* Measured run: per-rank layer records (whole iterations of num_layers
+ * layers, as drained by dwdp_ctx_records) -> events -> breakdown. recs is
+ * the concatenation of the ranks' records, counts[r] records each. If
+ * events != NULL, up to *n_events events are written (total in *n_events). */
+int dwdp_report_from_records(const dwdp_layer_record* recs, const size_t* counts,
+                             int num_ranks, int num_layers, int warmup_iterations,
+                             dwdp_breakdown* out, dwdp_sim_event* events,
+                             size_t* n_events);
+int dwdp_compare_reports(const dwdp_breakdown* a, const dwdp_breakdown* b,
+                         dwdp_comparison* out);
+/* BreakdownTable::to_csv / ComparisonTable::to_csv; *len_inout = capacity in,
+ * bytes needed (incl. NUL) out. */
+int dwdp_breakdown_csv(const dwdp_breakdown* b, char* buf, size_t* len_inout);
+int dwdp_comparison_csv(const dwdp_comparison* c, char* buf, size_t* len_inout);
 /* Kernels launched by this context so far (for the bench's launch count). */
 int dwdp_ctx_launch_count(const dwdp_ctx* ctx, int64_t* n);
 

@@ -248,6 +248,12 @@ class _Ref(_Api):
         L.ref_simulate.argtypes = [i32, i32, i64, i32, i32, i64, i64, f64, f64, f64, f64, i32,
                                    i32, i32, i32, f64, f64, f64, i64, i32, u64, i32, u64, i32, P]
         L.ref_analytic.argtypes = [i64, i32, i32, i64, i64, f64, f64, f64, f64, i32, i64, P]
+        L.ref_simulate_store.argtypes = [i32, i32, i32, i64, i32, i32, i64, i64, f64, f64, f64, f64,
+                                         i32, i32, i32, i32, f64, f64, f64, i64, i32, u64, i32, u64,
+                                         i32, P]
+        L.ref_report_events.argtypes = [i32, P, P, P, P, P, P, P]
+        L.ref_report_breakdown.argtypes = [i32, P, C.c_char_p, i32]
+        L.ref_compare.argtypes = [P, P, P, C.c_char_p, i32]
 
     def moe_entries(self, h, f, fs, wb, ab, tokens, pairs, touched, E=256, k=8):
         out = np.zeros(4, np.float64)
@@ -264,6 +270,44 @@ class _Ref(_Api):
                                    int(tdm), slice_size, int(merge_elim), _ptr(out))
         assert st == 0, self.lib.ref_last_error()
         return {"tokens_per_s": out[0], "latency_us": out[1], "exposed_us_per_layer": out[2]}
+
+    def simulate_report(self, slot: int, dwdp: bool, layers, h, E, k, f, fs, wb, peak, mem_bw,
+                        link_bw, N, iters, warmup, kind, length, ratio, sd, mnt, bpr, seed,
+                        tdm=True, slice_size=1 << 20, merge_elim=True):
+        """Run the reference simulator into report slot `slot`; return its
+        events, iteration spans, breakdown (35 packed doubles) and CSV."""
+        n = C.c_int()
+        st = self.lib.ref_simulate_store(slot, int(dwdp), layers, h, E, k, f, fs, wb, peak, mem_bw,
+                                         link_bw, N, iters, warmup, kind, length, ratio, sd, mnt,
+                                         bpr, seed, int(tdm), slice_size, int(merge_elim),
+                                         C.byref(n))
+        assert st == 0, self.lib.ref_last_error()
+        ne = n.value
+        i32a = np.zeros((max(ne, 1), 6), np.int32)
+        i64a = np.zeros((max(ne, 1), 2), np.int64)
+        by = np.zeros(max(ne, 1), np.float64)
+        isa = np.zeros(N * iters, np.int64)
+        iea = np.zeros(N * iters, np.int64)
+        tka = np.zeros(N * iters, np.int64)
+        dims = np.zeros(3, np.int32)
+        st = self.lib.ref_report_events(slot, _ptr(i32a), _ptr(i64a), _ptr(by), _ptr(isa),
+                                        _ptr(iea), _ptr(tka), _ptr(dims))
+        assert st == 0, self.lib.ref_last_error()
+        bd = np.zeros(35, np.float64)
+        csv = C.create_string_buffer(8192)
+        st = self.lib.ref_report_breakdown(slot, _ptr(bd), csv, 8192)
+        assert st == 0, self.lib.ref_last_error()
+        return {"events": (i32a[:ne], i64a[:ne], by[:ne]), "iter_start": isa, "iter_end": iea,
+                "iter_tokens": tka, "dims": dims.tolist(), "breakdown": bd,
+                "csv": csv.value.decode()}
+
+    def compare(self, a35: np.ndarray, b35: np.ndarray):
+        out = np.zeros(36, np.float64)
+        csv = C.create_string_buffer(8192)
+        st = self.lib.ref_compare(_ptr(np.ascontiguousarray(a35, np.float64)),
+                                  _ptr(np.ascontiguousarray(b35, np.float64)), _ptr(out), csv, 8192)
+        assert st == 0, self.lib.ref_last_error()
+        return out, csv.value.decode()
 
     def analytic(self, h, E, k, f, fs, wb, peak, mem_bw, link_bw, N, tokens):
         out = np.zeros(4, np.float64)

@@ -10,6 +10,7 @@
 // Error convention mirrors include/dwdp.h: 0 ok, 2 ConfigError, 3
 // InvariantViolation (reference: include/dwdpsim/errors.hpp:11-28).
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -186,17 +187,16 @@ int ref_moe_entries(int64_t hidden, int E, int top_k, int64_t ffn,
   });
 }
 
-// Runs the reference simulator (DWDP when dwdp!=0, else DEP) over batches
-// drawn from the workload spec; returns tokens/s, mean latency (us) and
-// exposed weight-wait us per layer per rank.
-int ref_simulate(int dwdp, int layers, int64_t hidden, int E, int top_k,
-                 int64_t ffn, int64_t shared_ffn, double wbytes,
-                 double peak_flops, double mem_bw, double link_bw, int N,
-                 int iters, int warmup, int isl_kind, double length,
-                 double ratio, double sd, int64_t mnt, int batch_per_rank,
-                 uint64_t seed, int tdm, uint64_t slice, int merge_elim,
-                 double* out3) {
-  return guarded([&] {
+}  // extern "C"
+
+namespace {
+RunReport g_reports[4];  // slots for the report-accounting pins
+
+RunReport run_sim(int dwdp, int layers, int64_t hidden, int E, int top_k, int64_t ffn,
+                  int64_t shared_ffn, double wbytes, double peak_flops, double mem_bw,
+                  double link_bw, int N, int iters, int warmup, int isl_kind, double length,
+                  double ratio, double sd, int64_t mnt, int batch_per_rank, uint64_t seed,
+                  int tdm, uint64_t slice, int merge_elim) {
     MoeModelSpec m =
         make_model(layers, hidden, E, top_k, ffn, shared_ffn, wbytes, 2.0);
     GpuSpec g;
@@ -215,17 +215,153 @@ int ref_simulate(int dwdp, int layers, int64_t hidden, int E, int top_k,
     w.batch_per_rank = batch_per_rank;
     w.seed = seed;
     const auto batches = sample_batches(w, m, N, iters);
-    RunReport rep;
     if (dwdp) {
       DwdpOptions o;
       o.tdm = tdm != 0;
       o.slice_size = slice;
       o.merge_elim = merge_elim != 0;
-      rep = simulate_dwdp(m, g, ip, batches, build_placement(E, N, 0), o,
-                          warmup);
-    } else {
-      rep = simulate_dep(m, g, ip, batches, N, warmup);
+      return simulate_dwdp(m, g, ip, batches, build_placement(E, N, 0), o, warmup);
     }
+    return simulate_dep(m, g, ip, batches, N, warmup);
+}
+
+int detail_code(const std::string& d) {
+  if (d == "weight_wait") return 1;
+  if (d == "dispatch") return 2;
+  if (d == "combine") return 3;
+  if (d == "barrier") return 4;
+  return 0;
+}
+
+// BreakdownTable <-> 35 doubles: compute[8], copy[8], compute_present[8],
+// copy_present[8], latency, overlapped, tokens/s
+void pack_breakdown(const BreakdownTable& t, double tps, double* o) {
+  for (int i = 0; i < 35; ++i) o[i] = 0;
+  for (const auto& [c, us] : t.compute_us) {
+    o[static_cast<int>(c)] = us;
+    o[16 + static_cast<int>(c)] = 1;
+  }
+  for (const auto& [c, us] : t.copy_us) {
+    o[8 + static_cast<int>(c)] = us;
+    o[24 + static_cast<int>(c)] = 1;
+  }
+  o[32] = t.iteration_latency_us;
+  o[33] = t.p2p_fully_overlapped ? 1 : 0;
+  o[34] = tps;
+}
+
+BreakdownTable unpack_breakdown(const double* o) {
+  BreakdownTable t;
+  for (int i = 0; i < 8; ++i) {
+    if (o[16 + i] != 0) t.compute_us[static_cast<Category>(i)] = o[i];
+    if (o[24 + i] != 0) t.copy_us[static_cast<Category>(i)] = o[8 + i];
+  }
+  t.iteration_latency_us = o[32];
+  t.p2p_fully_overlapped = o[33] != 0;
+  return t;
+}
+
+void put_str(const std::string& s, char* buf, int cap) {
+  if (cap <= 0) return;
+  const size_t n = std::min(s.size(), size_t(cap - 1));
+  std::memcpy(buf, s.data(), n);
+  buf[n] = 0;
+}
+}  // namespace
+
+extern "C" {
+
+// Simulate into report slot `slot` (0..3) for the accounting pins.
+int ref_simulate_store(int slot, int dwdp, int layers, int64_t hidden, int E, int top_k,
+                       int64_t ffn, int64_t shared_ffn, double wbytes, double peak_flops,
+                       double mem_bw, double link_bw, int N, int iters, int warmup,
+                       int isl_kind, double length, double ratio, double sd, int64_t mnt,
+                       int batch_per_rank, uint64_t seed, int tdm, uint64_t slice,
+                       int merge_elim, int* n_events) {
+  return guarded([&] {
+    require(slot >= 0 && slot < 4, "slot out of range");
+    g_reports[slot] = run_sim(dwdp, layers, hidden, E, top_k, ffn, shared_ffn, wbytes,
+                              peak_flops, mem_bw, link_bw, N, iters, warmup, isl_kind, length,
+                              ratio, sd, mnt, batch_per_rank, seed, tdm, slice, merge_elim);
+    *n_events = static_cast<int>(g_reports[slot].events.size());
+  });
+}
+
+// Events of a stored report: i32[n][6] {rank, stream, category, layer,
+// iteration, detail}, i64[n][2] {start, end}, bytes[n]; iteration spans
+// [ranks][iters]; dims = {ranks, iterations, warmup}.
+int ref_report_events(int slot, int32_t* i32, int64_t* i64, double* bytes, int64_t* is,
+                      int64_t* ie, int64_t* tk, int* dims) {
+  return guarded([&] {
+    const RunReport& r = g_reports[slot];
+    for (size_t i = 0; i < r.events.size(); ++i) {
+      const SimEvent& e = r.events[i];
+      int32_t* p = i32 + 6 * i;
+      p[0] = e.rank;
+      p[1] = static_cast<int32_t>(e.stream);
+      p[2] = static_cast<int32_t>(e.category);
+      p[3] = e.layer;
+      p[4] = e.iteration;
+      p[5] = detail_code(e.detail);
+      i64[2 * i] = e.start;
+      i64[2 * i + 1] = e.end;
+      bytes[i] = e.bytes;
+    }
+    for (int k = 0; k < r.num_ranks; ++k)
+      for (int it = 0; it < r.iterations; ++it) {
+        is[k * r.iterations + it] = r.iter_start[k][it];
+        ie[k * r.iterations + it] = r.iter_end[k][it];
+        tk[k * r.iterations + it] = r.iter_tokens[k][it];
+      }
+    dims[0] = r.num_ranks;
+    dims[1] = r.iterations;
+    dims[2] = r.warmup_iterations;
+  });
+}
+
+int ref_report_breakdown(int slot, double* out35, char* csv, int cap) {
+  return guarded([&] {
+    const BreakdownTable t = breakdown(g_reports[slot]);
+    pack_breakdown(t, g_reports[slot].throughput_tokens_per_s(), out35);
+    put_str(t.to_csv(), csv, cap);
+  });
+}
+
+// compare_reports over two packed breakdowns: out[8 a, 8 b, 8 delta,
+// 8 has_delta, a_lat, b_lat, overall, gross].
+int ref_compare(const double* a35, const double* b35, double* out36, char* csv, int cap) {
+  return guarded([&] {
+    const ComparisonTable t = compare_reports(unpack_breakdown(a35), unpack_breakdown(b35));
+    for (int i = 0; i < 36; ++i) out36[i] = 0;
+    for (const auto& row : t.rows) {
+      const int c = static_cast<int>(row.category);
+      out36[c] = row.a_us;
+      out36[8 + c] = row.b_us;
+      out36[16 + c] = row.delta_frac ? *row.delta_frac : 0.0;
+      out36[24 + c] = row.delta_frac ? 1 : 0;
+    }
+    out36[32] = t.a_latency_us;
+    out36[33] = t.b_latency_us;
+    out36[34] = t.overall_frac;
+    out36[35] = t.gross_sync_comm_pct;
+    put_str(t.to_csv(), csv, cap);
+  });
+}
+
+// Runs the reference simulator (DWDP when dwdp!=0, else DEP) over batches
+// drawn from the workload spec; returns tokens/s, mean latency (us) and
+// exposed weight-wait us per layer per rank.
+int ref_simulate(int dwdp, int layers, int64_t hidden, int E, int top_k,
+                 int64_t ffn, int64_t shared_ffn, double wbytes,
+                 double peak_flops, double mem_bw, double link_bw, int N,
+                 int iters, int warmup, int isl_kind, double length,
+                 double ratio, double sd, int64_t mnt, int batch_per_rank,
+                 uint64_t seed, int tdm, uint64_t slice, int merge_elim,
+                 double* out3) {
+  return guarded([&] {
+    RunReport rep = run_sim(dwdp, layers, hidden, E, top_k, ffn, shared_ffn, wbytes, peak_flops,
+                            mem_bw, link_bw, N, iters, warmup, isl_kind, length, ratio, sd, mnt,
+                            batch_per_rank, seed, tdm, slice, merge_elim);
     double wait_ns = 0;
     for (const auto& e : rep.events)
       if (e.category == Category::SyncWait && e.detail == "weight_wait" &&

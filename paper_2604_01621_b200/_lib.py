@@ -79,7 +79,30 @@ class LayerRecordC(C.Structure):
     _fields_ = [("global_layer", i64), ("tokens", i64), ("gate_wait_ns", f64), ("moe_ns", f64),
                 ("prefetch_ns", f64), ("prefetch_bytes", f64), ("merge_ns", f64),
                 ("router_ns", f64), ("permute_ns", f64), ("gemm1_ns", f64), ("gemm2_ns", f64),
-                ("combine_ns", f64), ("routed_rows", i64), ("comm_ns", f64)]
+                ("combine_ns", f64), ("routed_rows", i64), ("comm_ns", f64),
+                ("dispatch_ns", f64), ("start_ns", f64), ("end_ns", f64),
+                ("prefetch_start_ns", f64), ("prefetch_end_ns", f64)]
+
+
+NC = 8  # DWDP_NUM_CATEGORIES
+
+
+class SimEventC(C.Structure):
+    _fields_ = [("rank", i32), ("stream", i32), ("category", i32), ("layer", i32),
+                ("iteration", i32), ("detail", i32), ("start_ns", i64), ("end_ns", i64),
+                ("bytes", f64)]
+
+
+class BreakdownC(C.Structure):
+    _fields_ = [("compute_us", f64 * NC), ("copy_us", f64 * NC), ("compute_present", i32 * NC),
+                ("copy_present", i32 * NC), ("iteration_latency_us", f64),
+                ("p2p_fully_overlapped", i32), ("reserved", i32), ("tokens_per_s", f64)]
+
+
+class ComparisonC(C.Structure):
+    _fields_ = [("a_us", f64 * NC), ("b_us", f64 * NC), ("delta_frac", f64 * NC),
+                ("has_delta", i32 * NC), ("a_latency_us", f64), ("b_latency_us", f64),
+                ("overall_frac", f64), ("gross_sync_comm_pct", f64)]
 
 
 # name -> (restype, argtypes); every int-returning entry is a status code.
@@ -136,6 +159,16 @@ SIGNATURES = {
     "dwdp_dep_stack_forward": (i32, [P, P, i64, P, P]),
     "dwdp_gemm_bf16": (i32, [P, P, P, i64, i64, i64, P]),
     "dwdp_fill_bf16": (i32, [P, i64, u64, f32, P]),
+
+    "dwdp_report_breakdown": (i32, [P, sz, i32, i32, i32, P, P,
+                                    P, C.POINTER(BreakdownC)]),
+    "dwdp_report_from_records": (i32, [P, P, i32, i32, i32,
+                                       C.POINTER(BreakdownC), P,
+                                       C.POINTER(sz)]),
+    "dwdp_compare_reports": (i32, [C.POINTER(BreakdownC), C.POINTER(BreakdownC),
+                                   C.POINTER(ComparisonC)]),
+    "dwdp_breakdown_csv": (i32, [C.POINTER(BreakdownC), C.c_char_p, C.POINTER(sz)]),
+    "dwdp_comparison_csv": (i32, [C.POINTER(ComparisonC), C.c_char_p, C.POINTER(sz)]),
 }
 
 _lib = None

@@ -20,7 +20,7 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
 CU = ["kernels.cu", "gemm_sm100.cu"]
-CPP = ["plan.cpp", "runtime.cpp", "dep.cpp", "capi.cpp"]
+CPP = ["plan.cpp", "report.cpp", "runtime.cpp", "dep.cpp", "capi.cpp"]
 HEADERS = ["kernels.hpp", "gemm_sm100.hpp", "plan.hpp", "runtime.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

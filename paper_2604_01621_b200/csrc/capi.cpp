@@ -10,6 +10,7 @@
 
 #include "../../include/dwdp.h"
 #include "plan.hpp"
+#include "report.hpp"
 #include "runtime.hpp"
 
 struct dwdp_placement {
@@ -607,6 +608,139 @@ int dwdp_fill_bf16(void* dst, int64_t n, uint64_t seed, float scale, void* strea
                       static_cast<cudaStream_t>(stream));
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw dwdp::CudaError(cudaGetErrorString(e));
+  });
+}
+
+// ---- accounting ------------------------------------------------------------
+
+namespace {
+
+void copy_str(const std::string& s, char* buf, size_t* len) {
+  const size_t cap = *len;
+  *len = s.size() + 1;
+  if (buf && cap >= s.size() + 1) std::memcpy(buf, s.c_str(), s.size() + 1);
+}
+
+void finish_report(const dwdp::RunReport& rep, dwdp_breakdown* out) {
+  rep.validate_streams();
+  dwdp::breakdown_to_c(dwdp::breakdown(rep), rep.throughput_tokens_per_s(), out);
+}
+
+}  // namespace
+
+int dwdp_report_breakdown(const dwdp_sim_event* ev, size_t n, int num_ranks, int iterations,
+                          int warmup, const int64_t* is, const int64_t* ie, const int64_t* tk,
+                          dwdp_breakdown* out) {
+  return guard([&] {
+    need(out, "out");
+    need(is, "iter_start");
+    need(ie, "iter_end");
+    need(tk, "iter_tokens");
+    dwdp::require(ev != nullptr || n == 0, "events: null");
+    dwdp::require(num_ranks >= 1 && iterations >= 1 && warmup >= 0 && warmup < iterations,
+                  "report: bad rank / iteration counts");
+    dwdp::RunReport rep;
+    rep.num_ranks = num_ranks;
+    rep.iterations = iterations;
+    rep.warmup_iterations = warmup;
+    for (size_t i = 0; i < n; ++i) {
+      const dwdp_sim_event& e = ev[i];
+      dwdp::require(e.category >= 0 && e.category < DWDP_NUM_CATEGORIES, "report: bad category");
+      dwdp::require(e.rank >= 0 && e.rank < num_ranks, "report: event rank out of range");
+      rep.events.push_back({e.rank, static_cast<dwdp::Stream>(e.stream != 0),
+                            static_cast<dwdp::Category>(e.category), e.start_ns, e.end_ns, e.layer,
+                            e.iteration, e.bytes, e.detail});
+    }
+    const size_t nr = static_cast<size_t>(num_ranks), ni = static_cast<size_t>(iterations);
+    rep.iter_start.assign(nr, std::vector<int64_t>(ni));
+    rep.iter_end.assign(nr, std::vector<int64_t>(ni));
+    rep.iter_tokens.assign(nr, std::vector<int64_t>(ni));
+    for (size_t r = 0; r < nr; ++r)
+      for (size_t i = 0; i < ni; ++i) {
+        rep.iter_start[r][i] = is[r * ni + i];
+        rep.iter_end[r][i] = ie[r * ni + i];
+        rep.iter_tokens[r][i] = tk[r * ni + i];
+      }
+    finish_report(rep, out);
+  });
+}
+
+int dwdp_report_from_records(const dwdp_layer_record* recs, const size_t* counts, int num_ranks,
+                             int num_layers, int warmup, dwdp_breakdown* out,
+                             dwdp_sim_event* events, size_t* n_events) {
+  return guard([&] {
+    need(recs, "records");
+    need(counts, "counts");
+    need(out, "out");
+    dwdp::require(num_ranks >= 1 && num_layers >= 1 && warmup >= 0, "report: bad sizes");
+    dwdp::RunReport rep;
+    rep.num_ranks = num_ranks;
+    rep.num_layers = num_layers;
+    rep.warmup_iterations = warmup;
+    size_t off = 0;
+    for (int r = 0; r < num_ranks; ++r) {
+      dwdp::append_rank_events(rep, r, recs + off, counts[r]);
+      off += counts[r];
+    }
+    dwdp::require(warmup < rep.iterations, "report: warmup must leave a steady iteration");
+    finish_report(rep, out);
+    if (n_events) {
+      const size_t cap = events ? *n_events : 0;
+      for (size_t i = 0; i < rep.events.size() && i < cap; ++i) {
+        const dwdp::SimEvent& e = rep.events[i];
+        events[i] = {e.rank, static_cast<int32_t>(e.stream), static_cast<int32_t>(e.category), e.layer,
+                     e.iteration, e.detail, e.start, e.end, e.bytes};
+      }
+      *n_events = rep.events.size();
+    }
+  });
+}
+
+int dwdp_compare_reports(const dwdp_breakdown* a, const dwdp_breakdown* b, dwdp_comparison* out) {
+  return guard([&] {
+    need(a, "a");
+    need(b, "b");
+    need(out, "out");
+    const dwdp::ComparisonTable t =
+        dwdp::compare_reports(dwdp::breakdown_from_c(*a), dwdp::breakdown_from_c(*b));
+    *out = dwdp_comparison{};
+    for (const auto& row : t.rows) {
+      const int i = static_cast<int>(row.category);
+      out->a_us[i] = row.a_us;
+      out->b_us[i] = row.b_us;
+      out->has_delta[i] = row.delta_frac ? 1 : 0;
+      out->delta_frac[i] = row.delta_frac ? *row.delta_frac : 0.0;
+    }
+    out->a_latency_us = t.a_latency_us;
+    out->b_latency_us = t.b_latency_us;
+    out->overall_frac = t.overall_frac;
+    out->gross_sync_comm_pct = t.gross_sync_comm_pct;
+  });
+}
+
+int dwdp_breakdown_csv(const dwdp_breakdown* b, char* buf, size_t* len) {
+  return guard([&] {
+    need(b, "breakdown");
+    need(len, "len");
+    copy_str(dwdp::breakdown_from_c(*b).to_csv(), buf, len);
+  });
+}
+
+int dwdp_comparison_csv(const dwdp_comparison* c, char* buf, size_t* len) {
+  return guard([&] {
+    need(c, "comparison");
+    need(len, "len");
+    dwdp::ComparisonTable t;
+    for (int i = 0; i < DWDP_NUM_CATEGORIES; ++i) {
+      dwdp::ComparisonRow row{static_cast<dwdp::Category>(i), c->a_us[i], c->b_us[i], std::nullopt};
+      if (c->has_delta[i]) row.delta_frac = c->delta_frac[i];
+      t.rows.push_back(row);
+    }
+    t.a_latency_us = c->a_latency_us;
+    t.b_latency_us = c->b_latency_us;
+    t.overall_frac = c->overall_frac;
+    t.gross_sync_comm_pct = c->gross_sync_comm_pct;
+    copy_str(t.to_csv(), buf, len);
   });
 }
 

@@ -10,6 +10,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.hpp"
@@ -521,17 +522,26 @@ __global__ void __launch_bounds__(256) router_quant_kernel(const uint16_t* __res
 }
 
 // ---------------------------------------------------------------- permute
-constexpr int PCH = 128;  // tokens per chunk
+// Tokens per chunk: 128, halved (down to 8) while that leaves fewer than two
+// chunks per SM, so small (decode) batches still spread the row copies over
+// the whole GPU. Pairs are ranked chunk by chunk, so the permutation is the
+// same stable expert-major order for every chunk size.
+constexpr int PCH_MAX = 128, PCH_MIN = 8;
 constexpr int ROW_ALIGN = 128;
+inline int permute_chunk(int64_t T) {
+  int pch = PCH_MAX;
+  while (pch > PCH_MIN && (T + pch - 1) / pch < 2 * 148) pch >>= 1;
+  return pch;
+}
 
 __global__ void __launch_bounds__(256) permute_count_kernel(const int32_t* __restrict__ idx,
-                                                            int64_t T, int E, int k,
+                                                            int64_t T, int E, int k, int pch,
                                                             int32_t* __restrict__ chunk_counts) {
   extern __shared__ int32_t hist[];
   for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
   __syncthreads();
-  const int64_t p0 = int64_t(blockIdx.x) * PCH * k;
-  const int64_t p1 = (p0 + int64_t(PCH) * k < T * k) ? p0 + int64_t(PCH) * k : T * k;
+  const int64_t p0 = int64_t(blockIdx.x) * pch * k;
+  const int64_t p1 = (p0 + int64_t(pch) * k < T * k) ? p0 + int64_t(pch) * k : T * k;
   for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) atomicAdd(&hist[idx[p]], 1);
   __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x)
@@ -601,14 +611,14 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
     int64_t h, const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ expert_off,
     int32_t* __restrict__ row_of, int32_t* __restrict__ src_row, uint16_t* __restrict__ xperm,
     uint8_t* __restrict__ xperm8, float* __restrict__ xscale, const int32_t* __restrict__ meta,
-    int shared) {
-  extern __shared__ int32_t sm[];  // cursor[E], rows[PCH * k]
+    int shared, int pch) {
+  extern __shared__ int32_t sm[];  // cursor[E], rows[pch * k]
   int32_t* cursor = sm;
   int32_t* rows = sm + E;
   for (int e = threadIdx.x; e < E; e += blockDim.x) cursor[e] = 0;
   __syncthreads();
-  const int64_t t0 = int64_t(blockIdx.x) * PCH;
-  const int ntok = int(T - t0 < PCH ? T - t0 : PCH);
+  const int64_t t0 = int64_t(blockIdx.x) * pch;
+  const int ntok = int(T - t0 < pch ? T - t0 : pch);
   const int npairs = ntok * k;
   if (threadIdx.x < 32) {  // warp 0 ranks pairs in (t, j) order
     const int lane = threadIdx.x;
@@ -856,7 +866,8 @@ void launch_router_quant(const uint16_t* src, int64_t R, int64_t K, int8_t* dst,
 }
 
 int64_t permute_scratch_ints(int64_t T, int E) {
-  const int64_t nch = (T + PCH - 1) / PCH;
+  // chunks <= max(T / 128, 2 * (2 * 148)) + 1 (permute_chunk halves only below 296)
+  const int64_t nch = std::max<int64_t>((T + PCH_MAX - 1) / PCH_MAX, 4 * 148 + 1);
   return nch * E + E;
 }
 
@@ -864,17 +875,18 @@ void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
                     int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
                     int32_t* scratch, cudaStream_t st, uint8_t* xperm8, float* xscale) {
-  const int nch = int((T + PCH - 1) / PCH);
+  const int pch = permute_chunk(T);
+  const int nch = int((T + pch - 1) / pch);
   int32_t* chunk_counts = scratch;
   int32_t* expert_off = scratch + int64_t(nch) * E;
   if (nch > 0)
-    permute_count_kernel<<<nch, 256, E * sizeof(int32_t), st>>>(idx, T, E, k, chunk_counts);
+    permute_count_kernel<<<nch, 256, E * sizeof(int32_t), st>>>(idx, T, E, k, pch, chunk_counts);
   permute_scan_kernel<<<1, 1024, 2 * E * sizeof(int32_t), st>>>(
       chunk_counts, nch, E, T, shared, counts, expert_off, mblock_expert, mb_seg, src_row, meta);
   if (nch > 0)
-    permute_scatter_kernel<<<nch, 256, (E + PCH * k) * sizeof(int32_t), st>>>(
+    permute_scatter_kernel<<<nch, 256, (E + pch * k) * sizeof(int32_t), st>>>(
         idx, x, T, E, k, h, chunk_counts, expert_off, row_of, src_row, xperm, xperm8, xscale,
-        meta, shared);
+        meta, shared, pch);
 }
 
 void launch_fp8_fill_rows(uint8_t* dst, float* scales, const uint64_t* seeds, int nslots, int rows,

@@ -713,9 +713,16 @@ size_t Ctx::drain_records(dwdp_layer_record* out, size_t cap) {
       for (int i = 0; i < 5; ++i) kns[i] = el(seq[i], seq[i + 1]);
     }
     const int64_t rows = r.rows >= 0 ? r.rows : r.meta_slot >= 0 ? meta_ring_[r.meta_slot * 4 + 2] : -1;
+    const double dispatch = (r.k[1] && r.comm[1]) ? el(r.k[1], r.comm[1]) : 0.0;
+    double pf0 = -1, pf1 = -1;
+    if (r.plan >= 0) {
+      pf0 = el(epoch_, plans_[size_t(r.plan)].start);
+      pf1 = el(epoch_, plans_[size_t(r.plan)].done);
+    }
     if (out)
       out[n] = {r.g,    r.tokens, double(wait) * 1e6, double(moe) * 1e6, double(pf) * 1e6, pbytes,
-                double(merge) * 1e6, kns[0], kns[1], kns[2], kns[3], kns[4], rows, comm};
+                double(merge) * 1e6, kns[0], kns[1], kns[2], kns[3], kns[4], rows, comm, dispatch,
+                el(epoch_, r.gate0), el(epoch_, r.moe_end), pf0, pf1};
     ++n;
     for (cudaEvent_t e : {r.gate0, r.gate1, r.moe_end, r.merge_end, r.k[0], r.k[1], r.k[2], r.k[3],
                           r.comm[0], r.comm[1], r.comm[2], r.comm[3]})
