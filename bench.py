@@ -317,6 +317,11 @@ def main():
     g2_flops = sum(2.0 * (r["tokens"] * k + r["tokens"]) * f * h for r in recs)
     pk = peaks()
     achieved = g1_flops / (g1_ns * 1e-9) / 1e12 if g1_ns else 0.0
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "gemm1_dram.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
     esz = 1 if fp8 else 2
     if args.decode:
         # decode: GEMM1 streams the gate/up rows of every touched expert once
@@ -342,11 +347,6 @@ def main():
     exposed_ms = split["gate_wait_ns"]
     pf_bytes = sum(r["prefetch_bytes"] for r in recs)
     pf_ns = sum(r["prefetch_ns"] for r in recs)
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "gemm1_dram.json")
-    if os.path.exists(prof):
-        with open(prof) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
 
     # ---- e2e through the public API with host buffers
     e2e = None

@@ -168,17 +168,24 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 
 // Linear tile id -> (m-block, n-block). Tiles of a segment (consecutive
 // m-blocks of one expert) occupy the id range [start*NB, (start+len)*NB), so
-// the segment is found from the m-block tile/NB falls in; inside it the raster
-// is n-block-major.
+// the segment is found from the m-block tile/NB falls in. Inside a segment the
+// raster keeps the smaller operand set live in L2 while the ~148 concurrent
+// tiles sweep the other: n-block-major (all of the segment's A rows live, B
+// n-blocks streamed once) while the segment's A rows (len*128 per K) are at
+// most its B rows (NB*256 per K) -- every routed expert -- and m-block-major
+// (B live, A streamed once) for long segments such as the shared expert's
+// T rows, which n-major would re-read from HBM once per n-block.
 __device__ __forceinline__ void tile_coords(int tile, int nb_count, const int2* __restrict__ seg,
                                             int& mb, int& nb) {
   mb = tile / nb_count;
   nb = tile - mb * nb_count;
   if (seg) {
     const int2 s = seg[mb];
-    const int local = tile - s.x * nb_count;
-    nb = local / s.y;
-    mb = s.x + (local - nb * s.y);
+    if (s.y <= 2 * nb_count) {
+      const int local = tile - s.x * nb_count;
+      nb = local / s.y;
+      mb = s.x + (local - nb * s.y);
+    }
   }
 }
 

@@ -563,7 +563,18 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
   int32_t* off = sh + E;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int32_t run = 0;
-    for (int c = 0; c < nchunks; ++c) {
+    int c = 0;
+    for (; c + 8 <= nchunks; c += 8) {  // 8 independent loads in flight
+      int32_t n[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) n[u] = chunk_counts[int64_t(c + u) * E + e];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        chunk_counts[int64_t(c + u) * E + e] = run;
+        run += n[u];
+      }
+    }
+    for (; c < nchunks; ++c) {
       const int32_t n = chunk_counts[int64_t(c) * E + e];
       chunk_counts[int64_t(c) * E + e] = run;
       run += n;
@@ -662,14 +673,26 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
     return;
   }
   if (!xperm) return;  // GEMM1 gathers the rows itself (TMA tile::gather4)
-  // gather: each warp copies whole token rows to their k destinations
+  // gather: each warp copies whole token rows to their k destinations, four
+  // 16-byte loads in flight per lane before the 4k stores (latency hiding)
   const int64_t segs = h / 8;
   for (int tl = warp; tl < ntok; tl += blockDim.x >> 5) {
     const uint4* src = reinterpret_cast<const uint4*>(x + (t0 + tl) * h);
-    for (int64_t s = lane; s < segs; s += 32) {
+    const int32_t* dst = rows + tl * k;
+    int64_t s = lane;
+    for (; s + 96 < segs; s += 128) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(src + s + 32 * u);
+      for (int j = 0; j < k; ++j) {
+        uint4* d = reinterpret_cast<uint4*>(xperm + int64_t(dst[j]) * h) + s;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) d[32 * u] = v[u];
+      }
+    }
+    for (; s < segs; s += 32) {
       const uint4 v = __ldg(src + s);
-      for (int j = 0; j < k; ++j)
-        reinterpret_cast<uint4*>(xperm + int64_t(rows[tl * k + j]) * h)[s] = v;
+      for (int j = 0; j < k; ++j) reinterpret_cast<uint4*>(xperm + int64_t(dst[j]) * h)[s] = v;
     }
   }
 }

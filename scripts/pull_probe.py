@@ -1,0 +1,56 @@
+#!/usr/bin/env python
+"""Prefetch-engine probe on two GPUs of one process: rank 0 pulls one R1
+layer's remote experts (128 experts x gate/up/down, 11.3 GB bf16) from rank 1
+over NVLink with the chosen engine; prints achieved GB/s per plan. Used for
+the ncu capture of the TMA pull kernel (one process, so ncu sees every
+launch) and for engine GB/s numbers in DESIGN.md.
+
+    python scripts/pull_probe.py --engine pull --plans 4
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2604_01621_b200 as D  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--engine", default="pull", choices=["pull", "copy"])
+    ap.add_argument("--plans", type=int, default=4)
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp8"])
+    ap.add_argument("--slice-size", type=int, default=64 << 20)
+    a = ap.parse_args()
+    assert torch.cuda.device_count() >= 2, "needs two GPUs"
+    eng = D.ENGINE_PULL if a.engine == "pull" else D.ENGINE_COPY
+    ctxs = [D.DwdpContext(D.DwdpConfig(num_layers=2, rank=r, group_size=2, device=r, engine=eng,
+                                       slice_size=a.slice_size, weight_layers=2, max_tokens=128,
+                                       weight_dtype=D.WEIGHT_FP8 if a.dtype == "fp8" else
+                                       D.WEIGHT_BF16))
+            for r in range(2)]
+    for c in ctxs:
+        c.init_weights()
+    D.DwdpContext.link_local(ctxs)
+    torch.cuda.synchronize(0)
+    res = []
+    for g in range(1, a.plans + 1):  # layer 0 is preloaded
+        h = ctxs[0].prefetch_issue(g)
+        ctxs[0].prefetch_wait(h)
+        torch.cuda.synchronize(0)
+        s, e, b = ctxs[0].prefetch_times(h)
+        res.append({"plan": g, "bytes": b, "ms": (e - s) / 1e6, "gbs": b / (e - s)})
+    print(json.dumps({"engine": a.engine, "dtype": a.dtype, "slice_size": a.slice_size,
+                      "plans": res}), flush=True)
+    for c in ctxs:
+        c.close()
+
+
+if __name__ == "__main__":
+    main()
