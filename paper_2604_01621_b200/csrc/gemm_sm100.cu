@@ -258,6 +258,10 @@ __global__ void __launch_bounds__(256, 1)
       // gather mode: lane l owns source rows 4l..4l+3 of this m-block
       const int4 rows4 = gather ? *reinterpret_cast<const int4*>(p.a_rows + int64_t(mb) * BM + 4 * lane)
                                 : make_int4(0, 0, 0, 0);
+      // (L2 priority hints on these loads were measured and rejected: evict-first
+      // on the streamed operand made GEMM1 read 210 GB from HBM instead of 37;
+      // evict-last on the reused one cut the isolated kernel's HBM reads to
+      // 26 GB but its lines outlive the kernel and slowed the full step 11%.)
       for (int kb = 0; kb < kb_count; ++kb) {
         if (lane == 0) {
           mbar_wait(&empty[s], ph ^ 1);
