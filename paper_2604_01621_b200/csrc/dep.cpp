@@ -9,7 +9,8 @@
 // kernels), an NCCL all-gather of the per-expert counts (the host needs the
 // message sizes: DEP's inherent synchronisation point), grouped ncclSend /
 // ncclRecv of the expert-sorted rows, the grouped GEMMs over the received
-// rows (each (source, expert) segment padded to 128 rows so the m-block ->
+// rows (each (source, expert) segment padded to the GEMM row alignment, 128
+// or 256 rows with CTA pairs, so the m-block ->
 // expert table needs no regroup copy), the reverse all-to-all back into the
 // send layout, and the weighted combine. NCCL is resolved at run time from
 // the copy the process already loaded (torch), so libdwdp.so has no link
@@ -73,7 +74,6 @@ void nccl_check(int r, const char* what) {
                     (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error"));
 }
 
-inline int64_t pad128(int64_t n) { return (n + 127) / 128 * 128; }
 
 }  // namespace
 
@@ -178,7 +178,8 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
     launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_,
                    nullptr, scratch_, st, x8, xs_);
   else if (T > 0)
-    launch_permute(idx_, x, T, E_, k_, h_, 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_, xperm_, scratch_, st);
+    launch_permute(idx_, x, T, E_, k_, h_, 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_, xperm_, scratch_, st,
+                   nullptr, nullptr, row_align_);
   else
     DWDP_CUDA(cudaMemsetAsync(counts_, 0, size_t(E_) * 4, st));
   mark(&rec.k[1]);
@@ -188,13 +189,15 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
                             cudaMemcpyDeviceToHost, st));
   DWDP_CUDA(cudaStreamSynchronize(st));
   const int32_t* ca = dep_counts_host_;
+  // segments padded like the permute's send layout (256 rows with CTA pairs)
+  auto padr = [&](int64_t n) { return (n + row_align_ - 1) / row_align_ * row_align_; };
   const size_t nr = static_cast<size_t>(N_);
   std::vector<int64_t> send_off(nr), send_rows(nr), recv_off(nr), recv_rows(nr);
   int64_t acc = 0;
   for (int d = 0; d < N_; ++d) {
     send_off[size_t(d)] = acc;
     int64_t r = 0;
-    for (int e = d * per; e < (d + 1) * per; ++e) r += pad128(ca[size_t(rank_) * E_ + e]);
+    for (int e = d * per; e < (d + 1) * per; ++e) r += padr(ca[size_t(rank_) * E_ + e]);
     send_rows[size_t(d)] = r;
     acc += r;
   }
@@ -203,19 +206,19 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   for (int s = 0; s < N_; ++s) {
     recv_off[size_t(s)] = acc;
     int64_t r = 0;
-    for (int e = rank_ * per; e < (rank_ + 1) * per; ++e) r += pad128(ca[size_t(s) * E_ + e]);
+    for (int e = rank_ * per; e < (rank_ + 1) * per; ++e) r += padr(ca[size_t(s) * E_ + e]);
     recv_rows[size_t(s)] = r;
     acc += r;
   }
   const int64_t routed_rows = acc;
   const int64_t send_total = send_off[nr - 1] + send_rows[nr - 1];
-  const int64_t shared_blocks = shared_ ? (T + 127) / 128 : 0;
+  const int64_t shared_blocks = shared_ ? padr(T) / 128 : 0;
   dep_reserve(routed_rows + shared_blocks * 128);
   // m-block -> expert over the receive layout, then the shared expert blocks
   // (each (source, expert) run of m-blocks is one raster segment)
   for (int s = 0; s < N_; ++s)
     for (int e = rank_ * per; e < (rank_ + 1) * per; ++e) {
-      const int2 seg = make_int2(int(nblocks), int(pad128(ca[size_t(s) * E_ + e]) / 128));
+      const int2 seg = make_int2(int(nblocks), int(padr(ca[size_t(s) * E_ + e]) / 128));
       for (int b = 0; b < seg.y; ++b) {
         dep_seg_host_[nblocks] = seg;
         dep_tab_host_[4 + nblocks++] = e;
@@ -285,7 +288,8 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
     launch_quant_rows_fp8(dep_h_, dep_cap_rows_, f_, dmeta, dep_h8_, dep_hs_, st);
   } else if (nblocks > 0) {
     const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_dep_recv_;
-    GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1, dep_seg_};
+    GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1, dep_seg_,
+                nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0};
     launch_grouped_gemm(GEMM_SWIGLU, tm_dep_recv_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
   }
   mark(&rec.k[2]);
@@ -294,8 +298,10 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
                 nullptr, dep_hs_, sarena_[2], nullptr};
     launch_grouped_gemm(GEMM_PLAIN_FP8, tm_dep_h8_, tm_dep_h8_, tm_down_, tm_down_, g2, int(nblocks * (h_ / 256)), st);
   } else if (nblocks > 0) {
-    GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_};
-    launch_grouped_gemm(GEMM_PLAIN, tm_dep_h_, tm_dep_h_, tm_down_, tm_down_, g2, int(nblocks * (h_ / 256)), st);
+    GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
+                nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0};
+    const CUtensorMap& tmd = gemm_pair_ ? tm_down_p_ : tm_down_;
+    launch_grouped_gemm(GEMM_PLAIN, tm_dep_h_, tm_dep_h_, tmd, tmd, g2, int(nblocks * (h_ / 256)), st);
   }
   mark(&rec.k[3]);
   // 5. combine all-to-all: results back into the send layout (xperm)

@@ -189,6 +189,98 @@ __device__ __forceinline__ void tile_coords(int tile, int nb_count, const int2* 
   }
 }
 
+// Epilogue of one 128 x BN accumulator tile: warp q of the epilogue group
+// owns TMEM lanes (rows) 32q..32q+31; tbase addresses this warp's lanes and
+// the tile's accumulator columns.
+template <int MODE>
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb, uint32_t tbase, int q,
+                                              int lane) {
+  constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8;
+  constexpr bool FP8 = MODE == kSwiGLU8 || MODE == kPlain8;
+  const int64_t row = int64_t(mb) * BM + q * 32 + lane;
+  const bool store = row < p.m_limit;
+  // fp8: per-row activation scale x per-output-channel weight scale
+  float sa = 1.0f;
+  const float* sb0 = nullptr;
+  const float* sb1 = nullptr;
+  if (FP8) {
+    sa = p.a_scale[row];
+    const int64_t b0 = int64_t(p.slot_of[p.mblock_expert[mb]]) * p.rows_per_slot +
+                       int64_t(nb) * (SWIGLU ? 128 : BN);
+    sb0 = p.b_scale0 + b0;
+    sb1 = SWIGLU ? p.b_scale1 + b0 : nullptr;
+  }
+  if (MODE == kInt8) {
+    int32_t* out = reinterpret_cast<int32_t*>(p.D) + row * p.ldd + nb * BN;
+    const int cols = p.n_out - nb * BN < BN ? p.n_out - nb * BN : BN;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      tmem_ld32(tbase + c, v);
+      if (store && c < cols) {
+        if (c + 32 <= cols) {
+          int4* o4 = reinterpret_cast<int4*>(out + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            o4[i] = make_int4(__float_as_int(v[4 * i]), __float_as_int(v[4 * i + 1]),
+                              __float_as_int(v[4 * i + 2]), __float_as_int(v[4 * i + 3]));
+        } else {
+          for (int i = 0; i < cols - c; ++i) out[c + i] = __float_as_int(v[i]);
+        }
+      }
+    }
+  } else if (SWIGLU) {
+    uint16_t* out = p.D + row * p.ldd + nb * 128;
+#pragma unroll 1
+    for (int c = 0; c < 128; c += 32) {
+      float g[32], u[32];
+      tmem_ld32(tbase + c, g);
+      tmem_ld32(tbase + 128 + c, u);
+      if (FP8) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          g[i] *= sa * __ldg(sb0 + c + i);
+          u[i] *= sa * __ldg(sb1 + c + i);
+        }
+      }
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float g0 = g[2 * i], g1 = g[2 * i + 1];
+        const float h0 = __fdividef(g0, 1.0f + __expf(-g0)) * u[2 * i];
+        const float h1 = __fdividef(g1, 1.0f + __expf(-g1)) * u[2 * i + 1];
+        pk[i] = pack_bf16(h0, h1);
+      }
+      if (store) {
+        uint4* o4 = reinterpret_cast<uint4*>(out + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          o4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      }
+    }
+  } else {
+    uint16_t* out = p.D + row * p.ldd + nb * BN;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      tmem_ld32(tbase + c, v);
+      if (FP8) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= sa * __ldg(sb0 + c + i);
+      }
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+      if (store) {
+        uint4* o4 = reinterpret_cast<uint4*>(out + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          o4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      }
+    }
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -328,89 +420,7 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t aph = (local >> 1) & 1;
       mbar_wait(&tfull[a], aph);
       tc_fence_after();
-      const int64_t row = int64_t(mb) * BM + q * 32 + lane;
-      const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(a * BN);
-      const bool store = row < p.m_limit;
-      // fp8: per-row activation scale x per-output-channel weight scale
-      float sa = 1.0f;
-      const float* sb0 = nullptr;
-      const float* sb1 = nullptr;
-      if (FP8) {
-        sa = p.a_scale[row];
-        const int64_t b0 = int64_t(p.slot_of[p.mblock_expert[mb]]) * p.rows_per_slot +
-                           int64_t(nb) * (SWIGLU ? 128 : BN);
-        sb0 = p.b_scale0 + b0;
-        sb1 = SWIGLU ? p.b_scale1 + b0 : nullptr;
-      }
-      if (MODE == kInt8) {
-        int32_t* out = reinterpret_cast<int32_t*>(p.D) + row * p.ldd + nb * BN;
-        const int cols = p.n_out - nb * BN < BN ? p.n_out - nb * BN : BN;
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          float v[32];
-          tmem_ld32(tbase + c, v);
-          if (store && c < cols) {
-            if (c + 32 <= cols) {
-              int4* o4 = reinterpret_cast<int4*>(out + c);
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                o4[i] = make_int4(__float_as_int(v[4 * i]), __float_as_int(v[4 * i + 1]),
-                                  __float_as_int(v[4 * i + 2]), __float_as_int(v[4 * i + 3]));
-            } else {
-              for (int i = 0; i < cols - c; ++i) out[c + i] = __float_as_int(v[i]);
-            }
-          }
-        }
-      } else if (SWIGLU) {
-        uint16_t* out = p.D + row * p.ldd + nb * 128;
-#pragma unroll 1
-        for (int c = 0; c < 128; c += 32) {
-          float g[32], u[32];
-          tmem_ld32(tbase + c, g);
-          tmem_ld32(tbase + 128 + c, u);
-          if (FP8) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              g[i] *= sa * __ldg(sb0 + c + i);
-              u[i] *= sa * __ldg(sb1 + c + i);
-            }
-          }
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float g0 = g[2 * i], g1 = g[2 * i + 1];
-            const float h0 = __fdividef(g0, 1.0f + __expf(-g0)) * u[2 * i];
-            const float h1 = __fdividef(g1, 1.0f + __expf(-g1)) * u[2 * i + 1];
-            pk[i] = pack_bf16(h0, h1);
-          }
-          if (store) {
-            uint4* o4 = reinterpret_cast<uint4*>(out + c);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              o4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-          }
-        }
-      } else {
-        uint16_t* out = p.D + row * p.ldd + nb * BN;
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          float v[32];
-          tmem_ld32(tbase + c, v);
-          if (FP8) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] *= sa * __ldg(sb0 + c + i);
-          }
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
-          if (store) {
-            uint4* o4 = reinterpret_cast<uint4*>(out + c);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              o4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-          }
-        }
-      }
+      epilogue_tile<MODE>(p, mb, nb, tmem_base + (uint32_t(q * 32) << 16) + uint32_t(a * BN), q, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[a]);
@@ -421,6 +431,226 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------- CTA pair
+// 2-SM variant (cta_group::2) for the bf16 expert GEMMs. A cluster of two
+// CTAs on one TPC computes a 256 x 256 tile: CTA r loads A rows of m-block
+// 2*pair + r and half of B (SwiGLU: r = 0 the 128 gate rows, r = 1 the 128 up
+// rows; plain: B rows [128r, 128r + 128) of the n-block), and the leader's
+// single thread issues M256 x N256 x K16 MMAs that read A and B from both
+// CTAs' shared memory and accumulate each CTA's 128 rows in its own TMEM. Per
+// CTA this halves the B bytes moved from L2 and read from shared memory per
+// MMA flop (32 KB per 64-deep k-block instead of 48 KB). Requires expert
+// segments padded to 256 rows (permute row_align 256), so both m-blocks of a
+// pair always belong to the same expert.
+constexpr int P_STAGE = 2 * BM * BK * 2;  // A (16 KB) + half of B (16 KB) per CTA
+constexpr int P_STAGES = 6;
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE + 1024 + 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(const void* p, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// TMA tile load into this CTA's smem whose completion is signalled on the
+// leader CTA's mbarrier (cluster address).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cl,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cl), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc_v, uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc_v), "r"(accum));
+}
+// Commit the leader's MMAs to the same-offset mbarrier in both CTAs.
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+// bf16 x bf16 -> fp32, M = 256 (pair), N = 256, both operands K-major.
+constexpr uint32_t kPairIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
+                                (uint32_t(256 >> 4) << 24);
+
+// Pair tile id -> (pair index, n-block); segments in m-blocks are even.
+__device__ __forceinline__ void pair_coords(int tile, int nb_count, const int2* __restrict__ seg,
+                                            int& mp, int& nb) {
+  mp = tile / nb_count;
+  nb = tile - mp * nb_count;
+  if (seg) {
+    const int2 s = seg[2 * mp];
+    const int px = s.x >> 1, py = s.y >> 1;
+    if (py <= nb_count) {  // A rows (256 per pair) <= B rows (256 per n-block): n-major
+      const int local = tile - px * nb_count;
+      nb = local / py;
+      mp = px + (local - nb * py);
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                             const __grid_constant__ CUtensorMap tmA2,
+                             const __grid_constant__ CUtensorMap tmB0,
+                             const __grid_constant__ CUtensorMap tmB1, GemmArgs p) {
+  static_assert(MODE == kSwiGLU || MODE == kPlain, "pair kernel: bf16 modes only");
+  constexpr bool SWIGLU = MODE == kSwiGLU;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE);
+  uint64_t* empty = full + P_STAGES;
+  uint64_t* tfull = empty + P_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  auto sA = [&](int st) { return smem + st * P_STAGE; };
+  auto sB = [&](int st) { return smem + st * P_STAGE + BM * BK * 2; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < P_STAGES; ++st) {
+      mbar_init(&full[st], 2);   // leader: its expect_tx arrive + the peer's arrive
+      mbar_init(&empty[st], 1);  // one multicast commit per stage use
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // leader: 4 local + 4 peer epilogue warps
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB0)) : "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int total_mb = p.meta[0];
+  const int routed_mb = p.meta[1];
+  const int nb_count = SWIGLU ? p.n_out / 128 : (p.n_out + BN - 1) / BN;
+  const int num_tiles = (total_mb >> 1) * nb_count;
+  const int kb_count = p.K / BK;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------ TMA producer (both CTAs)
+      const uint32_t full_cl0 = map_to_rank(&full[0], 0);  // leader's full[0]
+      int st = 0;
+      uint32_t ph = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        int mp, nb;
+        pair_coords(tile, nb_count, p.mb_seg, mp, nb);
+        const int mb = 2 * mp + int(rank);
+        const int e = p.mblock_expert[mb];
+        const bool sh = p.shared_a2 && e == p.E;
+        const CUtensorMap* am = sh ? &tmA2 : &tmA;
+        const int arow = (sh ? mb - routed_mb : mb) * BM;
+        const CUtensorMap* bm = (SWIGLU && rank == 1) ? &tmB1 : &tmB0;
+        const int brow = p.slot_of[e] * p.rows_per_slot +
+                         (SWIGLU ? nb * 128 : nb * BN + int(rank) * 128);
+        for (int kb = 0; kb < kb_count; ++kb) {
+          mbar_wait(&empty[st], ph ^ 1);
+          const uint32_t bar = full_cl0 + uint32_t(st) * 8u;
+          if (rank == 0)
+            mbar_expect_tx(&full[st], 2 * P_STAGE);
+          else
+            mbar_arrive_cluster(bar);
+          tma_load_2d_pair(sA(st), am, bar, kb * BK, arow);
+          tma_load_2d_pair(sB(st), bm, bar, kb * BK, brow);
+          if (++st == P_STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader only)
+      int st = 0;
+      uint32_t ph = 0;
+      int local = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
+        const int a = local & 1;
+        const uint32_t aph = (local >> 1) & 1;
+        mbar_wait(&tempty[a], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + uint32_t(a * BN);
+        for (int kb = 0; kb < kb_count; ++kb) {
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          const uint64_t ad = sw128_desc(smem_u32(sA(st)));
+          const uint64_t bd = sw128_desc(smem_u32(sB(st)));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) tc_mma_pair(d, ad + 2 * k, bd + 2 * k, kPairIdesc, (kb | k) != 0);
+          tc_commit_pair(&empty[st]);
+          if (++st == P_STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+        tc_commit_pair(&tfull[a]);
+      }
+    }
+  } else if (warp >= 4) {  // ------------- epilogue (both CTAs, own 128 rows)
+    const int q = warp & 3;
+    const uint32_t tempty_cl0 = map_to_rank(&tempty[0], 0);
+    int local = 0;
+    for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
+      int mp, nb;
+      pair_coords(tile, nb_count, p.mb_seg, mp, nb);
+      const int a = local & 1;
+      const uint32_t aph = (local >> 1) & 1;
+      mbar_wait(&tfull[a], aph);
+      tc_fence_after();
+      epilogue_tile<MODE>(p, 2 * mp + int(rank), nb,
+                          tmem_base + (uint32_t(q * 32) << 16) + uint32_t(a * BN), q, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_cl0 + uint32_t(a) * 8u);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(TMEM_COLS));
   }
 }
@@ -495,10 +725,23 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
       cudaFuncSetAttribute(grouped_gemm_kernel<kPlain8>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+      cudaFuncSetAttribute(grouped_gemm_pair_kernel<kSwiGLU>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
+      cudaFuncSetAttribute(grouped_gemm_pair_kernel<kPlain>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
       configured |= uint64_t(1) << dev;
     }
   }
   if (max_tiles <= 0) return;
+  if (args.pair && (mode == kSwiGLU || mode == kPlain)) {
+    int g = max_tiles < sms[dev] ? max_tiles : sms[dev];
+    g = g < 2 ? 2 : (g & ~1);  // whole clusters of two
+    if (mode == kSwiGLU)
+      grouped_gemm_pair_kernel<kSwiGLU><<<g, 256, P_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+    else
+      grouped_gemm_pair_kernel<kPlain><<<g, 256, P_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+    return;
+  }
   const int grid = max_tiles < sms[dev] ? max_tiles : sms[dev];
   if (mode == kSwiGLU)
     grouped_gemm_kernel<kSwiGLU><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);

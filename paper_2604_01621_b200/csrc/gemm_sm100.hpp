@@ -34,6 +34,10 @@ struct GemmArgs {
   const float* a_scale;
   const float* b_scale0;
   const float* b_scale1;
+  // bf16 modes: run the 2-SM CTA-pair kernel (cta_group::2, 256 x 256 tiles).
+  // Needs every expert segment (and the shared block) padded to 256 rows and,
+  // for GEMM_PLAIN, a B map with 128-row boxes.
+  int pair;
 };
 
 // 2-D bf16 TMA map over a row-major [rows][cols] matrix, box = 64 x box_rows,

@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(256) router_quant_kernel(const uint16_t* __res
 // the whole GPU. Pairs are ranked chunk by chunk, so the permutation is the
 // same stable expert-major order for every chunk size.
 constexpr int PCH_MAX = 128, PCH_MIN = 8;
-constexpr int ROW_ALIGN = 128;
+constexpr int MB_ROWS = 128;  // rows per GEMM m-block
 inline int permute_chunk(int64_t T) {
   int pch = PCH_MAX;
   while (pch > PCH_MIN && (T + pch - 1) / pch < 2 * 148) pch >>= 1;
@@ -552,7 +552,8 @@ __global__ void __launch_bounds__(256) permute_count_kernel(const int32_t* __res
 // m-block -> expert table.
 __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict__ chunk_counts,
                                                             int nchunks, int E, int64_t T,
-                                                            int shared, int32_t* __restrict__ counts,
+                                                            int shared, int align,
+                                                            int32_t* __restrict__ counts,
                                                             int32_t* __restrict__ expert_off,
                                                             int32_t* __restrict__ mblock_expert,
                                                             int2* __restrict__ mb_seg,
@@ -580,7 +581,7 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
       run += n;
     }
     counts[e] = run;
-    pad[e] = (run + ROW_ALIGN - 1) / ROW_ALIGN * ROW_ALIGN;
+    pad[e] = (run + align - 1) / align * align;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -589,8 +590,8 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
       off[e] = acc;
       acc += pad[e];
     }
-    const int32_t routed_mb = acc / ROW_ALIGN;
-    const int32_t shared_mb = shared ? int32_t((T + ROW_ALIGN - 1) / ROW_ALIGN) : 0;
+    const int32_t routed_mb = acc / MB_ROWS;
+    const int32_t shared_mb = shared ? int32_t((T + align - 1) / align * (align / MB_ROWS)) : 0;
     meta[0] = routed_mb + shared_mb;
     meta[1] = routed_mb;
     meta[2] = acc;
@@ -599,7 +600,7 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
   __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     expert_off[e] = off[e];
-    const int2 seg = make_int2(off[e] / ROW_ALIGN, pad[e] / ROW_ALIGN);
+    const int2 seg = make_int2(off[e] / MB_ROWS, pad[e] / MB_ROWS);
     for (int32_t b = seg.x; b < seg.x + seg.y; ++b) {
       mblock_expert[b] = e;
       mb_seg[b] = seg;
@@ -897,7 +898,8 @@ int64_t permute_scratch_ints(int64_t T, int E) {
 void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int k, int64_t h,
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
                     int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
-                    int32_t* scratch, cudaStream_t st, uint8_t* xperm8, float* xscale) {
+                    int32_t* scratch, cudaStream_t st, uint8_t* xperm8, float* xscale,
+                    int row_align) {
   const int pch = permute_chunk(T);
   const int nch = int((T + pch - 1) / pch);
   int32_t* chunk_counts = scratch;
@@ -905,7 +907,8 @@ void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int
   if (nch > 0)
     permute_count_kernel<<<nch, 256, E * sizeof(int32_t), st>>>(idx, T, E, k, pch, chunk_counts);
   permute_scan_kernel<<<1, 1024, 2 * E * sizeof(int32_t), st>>>(
-      chunk_counts, nch, E, T, shared, counts, expert_off, mblock_expert, mb_seg, src_row, meta);
+      chunk_counts, nch, E, T, shared, row_align, counts, expert_off, mblock_expert, mb_seg, src_row,
+      meta);
   if (nch > 0)
     permute_scatter_kernel<<<nch, 256, (E + pch * k) * sizeof(int32_t), st>>>(
         idx, x, T, E, k, h, chunk_counts, expert_off, row_of, src_row, xperm, xperm8, xscale,

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 
@@ -60,6 +61,13 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
           "ctx: unknown weight_dtype");
   fp8_ = c.weight_dtype == DWDP_WEIGHT_FP8;
   esz_ = fp8_ ? 1 : 2;
+  // bf16 expert GEMMs run on CTA pairs (cta_group::2, 256-row tiles), which
+  // needs 256-row expert segments; DWDP_GEMM_PAIR=0 selects the 1-SM kernel.
+  {
+    const char* env = std::getenv("DWDP_GEMM_PAIR");
+    gemm_pair_ = !fp8_ && !(env && env[0] == '0');
+    row_align_ = gemm_pair_ ? 256 : 128;
+  }
   ntens_ = fp8_ ? 6 : 3;
   require(L_ >= 1, "ctx: num_layers must be >= 1");
   require(E_ >= 1 && E_ <= 512, "ctx: num_experts must be in [1, 512]");
@@ -114,7 +122,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
 
   // ---- workspace sized for max_tokens
   max_tokens_ = c.max_tokens;
-  max_mb_ = (max_tokens_ * k_ + int64_t(E_) * 127) / 128 + 1 + (shared_ ? (max_tokens_ + 127) / 128 : 0);
+  max_mb_ = mb_bound(max_tokens_);
   max_rows_ = max_mb_ * 128;
   logits_ = static_cast<float*>(dalloc(size_t(max_tokens_) * E_ * 4, &workspace_bytes));
   idx_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * k_ * 4, &workspace_bytes));
@@ -145,6 +153,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   tm_gate_ = tmap(arena_[0], int64_t(nslots_) * f_, h_, 128);
   tm_up_ = tmap(arena_[1], int64_t(nslots_) * f_, h_, 128);
   tm_down_ = tmap(arena_[2], int64_t(nslots_) * h_, f_, 256);
+  if (gemm_pair_) tm_down_p_ = tmap(arena_[2], int64_t(nslots_) * h_, f_, 128);  // half n-block per CTA
   tm_xperm_ = make_tmap_bf16(xperm_, max_rows_, h_, 128);
   tm_h_ = make_tmap_bf16(hbuf_, max_rows_, f_, 128);
   if (fp8_) {
@@ -566,7 +575,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   const int wl = layer % WL_;
   route_logits(wl, x, T, st);
   mark(0);
-  const int64_t mb_ub = (T * k_ + int64_t(E_) * 127) / 128 + 1 + (shared_ ? (T + 127) / 128 : 0);
+  const int64_t mb_ub = mb_bound(T);
   const int32_t* stab = slot_tab_ + (size_t(layer) * 2 + size_t(parity)) * (E_ + 1);
   if (fp8_) {
     // W8A8: the permute writes e4m3 copies of every routed row and of the
@@ -591,18 +600,21 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     launches += 9;
   } else {
   launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_, xperm_,
-                 scratch_, st);
+                 scratch_, st, nullptr, nullptr, row_align_);
   mark(1);
   const CUtensorMap tm_x = shared_ ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
   // Routed A rows come from the materialised expert-major copy. (GEMM1 can
   // also gather them from x with TMA tile::gather4 via GemmArgs::a_rows; on
   // B200 that measured 2.5x slower: 32 scattered 128-byte row fetches per
   // k-block defeat L2 reuse across the expert's 16 n-block tiles.)
-  GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_};
+  GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_,
+              nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0};
   launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(2);
-  GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_};
-  launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tm_down_, tm_down_, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
+  GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
+              nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0};
+  const CUtensorMap& tmd = gemm_pair_ ? tm_down_p_ : tm_down_;
+  launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tmd, tmd, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
   mark(3);
   launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
   launches += 8;

@@ -159,6 +159,14 @@ class Ctx {
   int32_t* srcrow_ = nullptr;           // [max_rows] source token of each routed row
   uint16_t *xperm_ = nullptr, *hbuf_ = nullptr;
   CUtensorMap tm_gate_, tm_up_, tm_down_, tm_xperm_, tm_h_;
+  CUtensorMap tm_down_p_;          // down arena with 128-row boxes (CTA-pair GEMM2)
+  bool gemm_pair_ = false;         // bf16 expert GEMMs on CTA pairs
+  int row_align_ = 128;            // expert segment padding (256 with pairs)
+  // upper bound on the m-blocks of T tokens (routed segments + shared block)
+  int64_t mb_bound(int64_t T) const {
+    return (T * k_ + int64_t(E_) * (row_align_ - 1)) / 128 + 2 +
+           (shared_ ? (T + row_align_ - 1) / row_align_ * (row_align_ / 128) : 0);
+  }
   // prefetch engine
   std::vector<ShardRun> runs_;
   std::vector<Slice> plan_slices_;

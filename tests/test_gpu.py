@@ -316,3 +316,20 @@ def test_prefetch_handles(dev):
     assert sum(s.length for s in plan) == b
     for c in ranks:
         c.close()
+
+
+def test_gemm_pair_matches_single_cta(dev, monkeypatch):
+    """The CTA-pair GEMM path (cta_group::2, 256-row segments, the default for
+    bf16) and the 1-SM path give the same layer outputs."""
+    cfg = CONFIGS["mid_sigmoid"]
+    outs = []
+    for pair in ("1", "0"):
+        monkeypatch.setenv("DWDP_GEMM_PAIR", pair)
+        c = D.DwdpContext(cfg)
+        c.init_weights()
+        c.set_bias(_bias(cfg))
+        x = make_x(333, cfg.hidden, 5, dev)
+        outs.append(c.moe_forward(0, x).float().cpu().numpy())
+        torch.cuda.synchronize()
+        c.close()
+    assert _rel(outs[0], outs[1]) < 1e-3
