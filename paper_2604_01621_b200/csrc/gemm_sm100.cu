@@ -24,6 +24,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -447,7 +448,7 @@ __global__ void __launch_bounds__(256, 1)
 // segments padded to 256 rows (permute row_align 256), so both m-blocks of a
 // pair always belong to the same expert.
 constexpr int P_STAGE = 2 * BM * BK * 2;  // A (16 KB) + half of B (16 KB) per CTA
-constexpr int P_STAGES = 6;
+constexpr int P_STAGES = 7;
 constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE + 1024 + 256;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -537,7 +538,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const uint32_t rank = cluster_rank();
   if (threadIdx.x == 0) {
     for (int st = 0; st < P_STAGES; ++st) {
-      mbar_init(&full[st], 2);   // leader: its expect_tx arrive + the peer's arrive
+      mbar_init(&full[st], 1);   // leader: its expect_tx arrive (both CTAs' TMA bytes)
       mbar_init(&empty[st], 1);  // one multicast commit per stage use
     }
     for (int a = 0; a < 2; ++a) {
@@ -588,10 +589,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         for (int kb = 0; kb < kb_count; ++kb) {
           mbar_wait(&empty[st], ph ^ 1);
           const uint32_t bar = full_cl0 + uint32_t(st) * 8u;
-          if (rank == 0)
-            mbar_expect_tx(&full[st], 2 * P_STAGE);
-          else
-            mbar_arrive_cluster(bar);
+          // Only the leader arrives (expecting both CTAs' bytes). The peer's
+          // complete_tx may land first (the phase cannot complete while the
+          // leader's arrival is pending); a remote arrive from the peer would
+          // put a cluster-scope release fence in front of every load.
+          if (rank == 0) mbar_expect_tx(&full[st], 2 * P_STAGE);
           tma_load_2d_pair(sA(st), am, bar, kb * BK, arow);
           tma_load_2d_pair(sB(st), bm, bar, kb * BK, brow);
           if (++st == P_STAGES) {
@@ -709,6 +711,7 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
   static std::mutex mu;
   static uint64_t configured = 0;  // bit per device: smem attribute set
   static int sms[64] = {0};
+  static int pair_clusters[64] = {0};  // co-resident CTA pairs (some TPCs cannot host one)
   int dev = 0;
   cudaGetDevice(&dev);
   {
@@ -729,13 +732,35 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
       cudaFuncSetAttribute(grouped_gemm_pair_kernel<kPlain>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
+      {
+        cudaLaunchConfig_t lc = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.gridDim = dim3(unsigned(sms[dev] & ~1));
+        lc.blockDim = dim3(256);
+        lc.dynamicSmemBytes = P_SMEM_BYTES;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, grouped_gemm_pair_kernel<kSwiGLU>, &lc) != cudaSuccess)
+          n = 0;
+        cudaGetLastError();
+        pair_clusters[dev] = n > 0 ? n : sms[dev] / 2;
+        if (std::getenv("DWDP_VERBOSE"))
+          std::fprintf(stderr, "dwdp: device %d: %d SMs, %d co-resident CTA pairs\n", dev, sms[dev],
+                       pair_clusters[dev]);
+      }
       configured |= uint64_t(1) << dev;
     }
   }
   if (max_tiles <= 0) return;
   if (args.pair && (mode == kSwiGLU || mode == kPlain)) {
-    int g = max_tiles < sms[dev] ? max_tiles : sms[dev];
-    g = g < 2 ? 2 : (g & ~1);  // whole clusters of two
+    const int cap = 2 * pair_clusters[dev];
+    int g = max_tiles < cap ? max_tiles : cap;
+    g = g < 2 ? 2 : (g & ~1);  // whole clusters of two, all co-resident (persistent)
     if (mode == kSwiGLU)
       grouped_gemm_pair_kernel<kSwiGLU><<<g, 256, P_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
     else
