@@ -289,7 +289,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   } else if (nblocks > 0) {
     const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_dep_recv_;
     GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1, dep_seg_,
-                nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0};
+                nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_};
     launch_grouped_gemm(GEMM_SWIGLU, tm_dep_recv_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
   }
   mark(&rec.k[2]);
@@ -299,7 +299,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
     launch_grouped_gemm(GEMM_PLAIN_FP8, tm_dep_h8_, tm_dep_h8_, tm_down_, tm_down_, g2, int(nblocks * (h_ / 256)), st);
   } else if (nblocks > 0) {
     GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
-                nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0};
+                nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_};
     const CUtensorMap& tmd = gemm_pair_ ? tm_down_p_ : tm_down_;
     launch_grouped_gemm(GEMM_PLAIN, tm_dep_h_, tm_dep_h_, tmd, tmd, g2, int(nblocks * (h_ / 256)), st);
   }

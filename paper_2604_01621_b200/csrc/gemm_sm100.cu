@@ -501,13 +501,13 @@ constexpr uint32_t kPairIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(B
 
 // Pair tile id -> (pair index, n-block); segments in m-blocks are even.
 __device__ __forceinline__ void pair_coords(int tile, int nb_count, const int2* __restrict__ seg,
-                                            int& mp, int& nb) {
+                                            int raster, int& mp, int& nb) {
   mp = tile / nb_count;
   nb = tile - mp * nb_count;
-  if (seg) {
+  if (seg && raster != 1) {
     const int2 s = seg[2 * mp];
     const int px = s.x >> 1, py = s.y >> 1;
-    if (py <= nb_count) {  // A rows (256 per pair) <= B rows (256 per n-block): n-major
+    if (raster == 2 || py <= nb_count) {  // A rows (256 per pair) <= B rows (256 per n-block): n-major
       const int local = tile - px * nb_count;
       nb = local / py;
       mp = px + (local - nb * py);
@@ -577,7 +577,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       uint32_t ph = 0;
       for (int tile = cid; tile < num_tiles; tile += ncl) {
         int mp, nb;
-        pair_coords(tile, nb_count, p.mb_seg, mp, nb);
+        pair_coords(tile, nb_count, p.mb_seg, p.raster, mp, nb);
         const int mb = 2 * mp + int(rank);
         const int e = p.mblock_expert[mb];
         const bool sh = p.shared_a2 && e == p.E;
@@ -636,7 +636,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     int local = 0;
     for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
       int mp, nb;
-      pair_coords(tile, nb_count, p.mb_seg, mp, nb);
+      pair_coords(tile, nb_count, p.mb_seg, p.raster, mp, nb);
       const int a = local & 1;
       const uint32_t aph = (local >> 1) & 1;
       mbar_wait(&tfull[a], aph);

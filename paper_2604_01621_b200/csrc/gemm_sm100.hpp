@@ -38,6 +38,9 @@ struct GemmArgs {
   // Needs every expert segment (and the shared block) padded to 256 rows and,
   // for GEMM_PLAIN, a B map with 128-row boxes.
   int pair;
+  // segment raster: 0 auto (n-block-major while the segment's A rows <= its
+  // B rows), 1 always m-block-major, 2 always n-block-major (experiments)
+  int raster;
 };
 
 // 2-D bf16 TMA map over a row-major [rows][cols] matrix, box = 64 x box_rows,

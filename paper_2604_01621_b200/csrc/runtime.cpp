@@ -67,6 +67,8 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     const char* env = std::getenv("DWDP_GEMM_PAIR");
     gemm_pair_ = !fp8_ && !(env && env[0] == '0');
     row_align_ = gemm_pair_ ? 256 : 128;
+    const char* r = std::getenv("DWDP_RASTER");  // experiments: m / n (default auto)
+    raster_ = r ? (r[0] == 'm' ? 1 : r[0] == 'n' ? 2 : 0) : 0;
   }
   ntens_ = fp8_ ? 6 : 3;
   require(L_ >= 1, "ctx: num_layers must be >= 1");
@@ -608,11 +610,11 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   // B200 that measured 2.5x slower: 32 scattered 128-byte row fetches per
   // k-block defeat L2 reuse across the expert's 16 n-block tiles.)
   GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_,
-              nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0};
+              nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_};
   launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(2);
   GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
-              nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0};
+              nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_};
   const CUtensorMap& tmd = gemm_pair_ ? tm_down_p_ : tm_down_;
   launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tmd, tmd, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
   mark(3);

@@ -162,6 +162,7 @@ class Ctx {
   CUtensorMap tm_down_p_;          // down arena with 128-row boxes (CTA-pair GEMM2)
   bool gemm_pair_ = false;         // bf16 expert GEMMs on CTA pairs
   int row_align_ = 128;            // expert segment padding (256 with pairs)
+  int raster_ = 0;                 // GemmArgs::raster (DWDP_RASTER experiments)
   // upper bound on the m-blocks of T tokens (routed segments + shared block)
   int64_t mb_bound(int64_t T) const {
     return (T * k_ + int64_t(E_) * (row_align_ - 1)) / 128 + 2 +
