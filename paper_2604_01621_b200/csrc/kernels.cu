@@ -450,6 +450,152 @@ __global__ void __launch_bounds__(256) topk_kernel(const int32_t* __restrict__ C
   }
 }
 
+// Same contract as topk_kernel for E = 32*V with every lane's V experts in
+// one routing group (E % 32 == 0, (E / n_group) % V == 0): lane l owns the
+// contiguous experts [V*l, V*l + V), so the 9 plane products are read as int4
+// vectors, a group's top-2 is a lane-local top-2 merged over the group's
+// E/(n_group*V) lanes (two xor shuffles for R1) and the kept groups are
+// ranked from G broadcast scores. Results are bit-identical to topk_kernel.
+template <int V>
+__global__ void __launch_bounds__(256) topk_contig_kernel(const int32_t* __restrict__ C,
+                                                          const int32_t* __restrict__ ex,
+                                                          const int32_t* __restrict__ ew,
+                                                          const float* __restrict__ bias,
+                                                          float* __restrict__ logits,
+                                                          int32_t* __restrict__ idx_out,
+                                                          float* __restrict__ wts_out, int64_t T,
+                                                          RouterCfg c) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int E = c.E;
+  const int e0 = V * lane;
+  const float NEG = __int_as_float(0xff800000);
+  long long z[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) z[i] = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const int32_t* src = C + (a * T + t) * (3 * E) + b * E + e0;
+      int32_t w[V];
+      if (V % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < V; i += 4) {
+          const int4 q = __ldg(reinterpret_cast<const int4*>(src + i));
+          w[i] = q.x;
+          w[i + 1] = q.y;
+          w[i + 2] = q.z;
+          w[i + 3] = q.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) w[i] = __ldg(src + i);
+      }
+#pragma unroll
+      for (int i = 0; i < V; ++i) z[i] += static_cast<long long>(w[i]) * (1LL << (8 * (a + b)));
+    }
+  const int xe = ex[t];
+  float lg[V], sc[V], ch[V];
+  float* row = logits + t * E;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int sx = xe + ew[e0 + i] - 296;
+    const float f = __ll2float_rn(z[i]);
+    lg[i] = (sx >= -126 && sx <= 127) ? __fmul_rn(f, __int_as_float((sx + 127) << 23)) : ldexpf(f, sx);
+    row[e0 + i] = lg[i];
+    if (c.scoring == 1) {
+      sc[i] = __fdiv_rn(1.0f, __fadd_rn(1.0f, det_expf(-lg[i])));
+      ch[i] = __fadd_rn(sc[i], bias ? bias[e0 + i] : 0.0f);
+    } else {
+      sc[i] = lg[i];
+      ch[i] = lg[i];
+    }
+  }
+  const int G = c.n_group > 0 ? c.n_group : 1;
+  if (G > 1 && c.topk_group < G) {
+    const int gs = E / G, lpg = gs / V;  // experts and lanes per group
+    // lane-local top-2 values, then merge across the group's lanes
+    float v1 = NEG, v2 = NEG;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      if (ch[i] > v1) {
+        v2 = v1;
+        v1 = ch[i];
+      } else if (ch[i] > v2) {
+        v2 = ch[i];
+      }
+    }
+    for (int o = 1; o < lpg; o <<= 1) {
+      const float o1 = __shfl_xor_sync(0xffffffffu, v1, o);
+      const float o2 = __shfl_xor_sync(0xffffffffu, v2, o);
+      const float hi = fmaxf(v1, o1);
+      const float lo = fmaxf(fminf(v1, o1), fmaxf(v2, o2));
+      v1 = hi;
+      v2 = lo;
+    }
+    const float gsc = gs >= 2 ? __fadd_rn(v1, v2) : v1;
+    const int g = lane / lpg;
+    int rank = 0;
+    for (int h = 0; h < G; ++h) {
+      const float sh = __shfl_sync(0xffffffffu, gsc, h * lpg);
+      rank += (sh > gsc || (sh == gsc && h < g)) ? 1 : 0;
+    }
+    if (rank >= c.topk_group)
+#pragma unroll
+      for (int i = 0; i < V; ++i) ch[i] = 0.0f;  // HF masked_fill 0.0
+  }
+  int sel[TOPK_MAXK];
+  uint32_t taken = 0;
+  for (int j = 0; j < c.k; ++j) {
+    float bv = NEG;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < V; ++i)
+      if (!((taken >> i) & 1u) && better(ch[i], e0 + i, bv, bi)) {
+        bv = ch[i];
+        bi = e0 + i;
+      }
+    warp_best(bv, bi);
+    sel[j] = bi;
+    if (bi / V == lane) taken |= 1u << (bi - e0);
+  }
+  float wv[TOPK_MAXK];
+  for (int j = 0; j < c.k; ++j) {
+    const int e = sel[j];
+    float mine = 0.0f;
+#pragma unroll
+    for (int i = 0; i < V; ++i)
+      if (e0 + i == e) mine = (c.scoring == 1) ? sc[i] : lg[i];
+    wv[j] = __shfl_sync(0xffffffffu, mine, e / V);
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  if (c.scoring == 1) {
+    if (c.norm_topk) {
+      float s = 0.0f;
+      for (int j = 0; j < c.k; ++j) s = __fadd_rn(s, wv[j]);
+      s = __fadd_rn(s, 1e-20f);
+      for (int j = 0; j < c.k; ++j) wv[j] = __fdiv_rn(wv[j], s);
+    }
+  } else {
+    const float m = wv[0];
+    float s = 0.0f;
+    for (int j = 0; j < c.k; ++j) {
+      wv[j] = det_expf(__fsub_rn(wv[j], m));
+      if (c.norm_topk) s = __fadd_rn(s, wv[j]);
+    }
+    if (!c.norm_topk)
+      for (int e = 0; e < E; ++e) s = __fadd_rn(s, det_expf(__fsub_rn(row[e], m)));
+    for (int j = 0; j < c.k; ++j) wv[j] = __fdiv_rn(wv[j], s);
+  }
+  for (int j = 0; j < c.k; ++j) {
+    idx_out[t * c.k + j] = sel[j];
+    wts_out[t * c.k + j] = __fmul_rn(wv[j], c.routed_scale);
+  }
+}
+
 // ---------------------------------------------------------------- router quant
 // bf16 bits -> (mantissa incl. implicit bit, exponent field clamped to >= 1)
 __device__ __forceinline__ void bf16_fields(uint32_t b, int& mant, int& eb) {
@@ -468,11 +614,13 @@ __device__ __forceinline__ int fixed22(uint32_t b, int emax) {
 
 // One warp per row: pass 1 finds the row exponent, pass 2 writes the three
 // balanced int8 digit planes (Q = d0 + 256 d1 + 65536 d2, |Q| < 2^22).
+constexpr int RQ_WARPS = 2;  // rows (warps) per CTA when the rows are staged in smem
+
 __global__ void __launch_bounds__(256) router_quant_kernel(const uint16_t* __restrict__ src,
                                                            int64_t R, int64_t K,
                                                            int8_t* __restrict__ dst,
                                                            int32_t* __restrict__ emax,
-                                                           int32_t* __restrict__ meta) {
+                                                           int32_t* __restrict__ meta, int staged) {
   if (meta && blockIdx.x == 0 && threadIdx.x == 0) {
     const int mb = int((3 * R + 127) / 128);
     meta[0] = mb;
@@ -485,6 +633,55 @@ __global__ void __launch_bounds__(256) router_quant_kernel(const uint16_t* __res
   if (r >= R) return;
   const uint4* row = reinterpret_cast<const uint4*>(src + r * K);
   const int64_t nch = K / 8;
+  extern __shared__ uint4 rq_rows[];  // [warps per block][nch] when staged
+  if (staged) {  // one HBM read: pass 1 stages the row in smem, pass 2 quantises from it
+    uint4* srow = rq_rows + (threadIdx.x >> 5) * nch;
+    int m = 0;
+    for (int64_t c0 = lane; c0 < nch; c0 += 32 * 4) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t c = c0 + 32 * u;
+        v[u] = c < nch ? __ldg(row + c) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t c = c0 + 32 * u;
+        if (c < nch) srow[c] = v[u];
+        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          int mant, eb;
+          bf16_fields((w[q >> 1] >> (16 * (q & 1))) & 0xFFFFu, mant, eb);
+          if (mant && eb > m) m = eb;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (m == 0) m = 1;
+    for (int64_t c = lane; c < nch; c += 32) {
+      const uint4 v = srow[c];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      uint32_t p0[2] = {0, 0}, p1[2] = {0, 0}, p2[2] = {0, 0};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int Q = fixed22((w[q >> 1] >> (16 * (q & 1))) & 0xFFFFu, m);
+        const int d0 = int(int8_t(uint8_t(Q & 0xFF)));
+        const int Q1 = (Q - d0) >> 8;
+        const int d1 = int(int8_t(uint8_t(Q1 & 0xFF)));
+        const int d2 = (Q1 - d1) >> 8;
+        p0[q >> 2] |= uint32_t(uint8_t(d0)) << (8 * (q & 3));
+        p1[q >> 2] |= uint32_t(uint8_t(d1)) << (8 * (q & 3));
+        p2[q >> 2] |= uint32_t(uint8_t(d2)) << (8 * (q & 3));
+      }
+      *reinterpret_cast<uint2*>(dst + (0 * R + r) * K + c * 8) = make_uint2(p0[0], p0[1]);
+      *reinterpret_cast<uint2*>(dst + (1 * R + r) * K + c * 8) = make_uint2(p1[0], p1[1]);
+      *reinterpret_cast<uint2*>(dst + (2 * R + r) * K + c * 8) = make_uint2(p2[0], p2[1]);
+    }
+    if (lane == 0) emax[r] = m;
+    return;
+  }
   int m = 0;
   for (int64_t c = lane; c < nch; c += 32) {
     const uint4 v = __ldg(row + c);
@@ -880,13 +1077,33 @@ void launch_topk(const int32_t* C, const int32_t* ex, const int32_t* ew, const f
                  float* logits, int32_t* idx, float* wts, int64_t T, const RouterCfg& c,
                  cudaStream_t st) {
   if (T <= 0) return;
-  topk_kernel<<<unsigned((T + 7) / 8), 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
+  const unsigned grid = unsigned((T + 7) / 8);
+  const int G = c.n_group > 0 ? c.n_group : 1;
+  const int V = c.E / 32;
+  const bool contig = c.E % 32 == 0 && (V == 1 || V == 2 || V == 4 || V == 8) &&
+                      (G == 1 || ((c.E / G) % V == 0 && (c.E / G) / V <= 32 &&
+                                  (((c.E / G) / V) & ((c.E / G) / V - 1)) == 0));
+  if (contig && V == 8)
+    topk_contig_kernel<8><<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
+  else if (contig && V == 4)
+    topk_contig_kernel<4><<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
+  else if (contig && V == 2)
+    topk_contig_kernel<2><<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
+  else if (contig && V == 1)
+    topk_contig_kernel<1><<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
+  else
+    topk_kernel<<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
 }
 
 void launch_router_quant(const uint16_t* src, int64_t R, int64_t K, int8_t* dst, int32_t* emax,
                          int32_t* meta, cudaStream_t st) {
   if (R <= 0) return;
-  router_quant_kernel<<<unsigned((R + 7) / 8), 256, 0, st>>>(src, R, K, dst, emax, meta);
+  const size_t smem = size_t(RQ_WARPS) * size_t(K) * 2;
+  if (smem <= 48 * 1024)
+    router_quant_kernel<<<unsigned((R + RQ_WARPS - 1) / RQ_WARPS), 32 * RQ_WARPS, smem, st>>>(
+        src, R, K, dst, emax, meta, 1);
+  else
+    router_quant_kernel<<<unsigned((R + 7) / 8), 256, 0, st>>>(src, R, K, dst, emax, meta, 0);
 }
 
 int64_t permute_scratch_ints(int64_t T, int E) {

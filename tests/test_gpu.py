@@ -54,6 +54,13 @@ CONFIGS = {
     "mid_sigmoid": D.DwdpConfig(num_layers=1, num_experts=64, hidden=1024, ffn=256, shared_ffn=256,
                                 top_k=6, n_group=8, topk_group=4, max_tokens=2048),
     "r1": D.DwdpConfig(num_layers=1, max_tokens=512),  # BASELINE config 2 shapes
+    # top-k kernel variants: contiguous-lane layout with 8 lanes per group, and
+    # softmax over all E without renormalisation (norm_topk = 0)
+    "e128_g4": D.DwdpConfig(num_layers=1, num_experts=128, hidden=512, ffn=256, top_k=4, n_group=4,
+                            topk_group=2, max_tokens=512),
+    "e32_softmax": D.DwdpConfig(num_layers=1, num_experts=32, hidden=512, ffn=256, top_k=3,
+                                scoring=0, n_group=1, topk_group=1, norm_topk=0, routed_scale=1.0,
+                                max_tokens=512),
 }
 
 
@@ -102,7 +109,8 @@ def test_gemm_vs_torch(dev, M, N, K):
 
 @pytest.mark.parametrize("name,T", [("tiny", 1), ("tiny", 7), ("tiny", 64), ("tiny", 1000),
                                     ("mid_sigmoid", 1), ("mid_sigmoid", 333),
-                                    ("r1", 1), ("r1", 37), ("r1", 256)])
+                                    ("r1", 1), ("r1", 37), ("r1", 256), ("e128_g4", 77),
+                                    ("e32_softmax", 129)])
 def test_route_bit_exact(dev, ctxs, orc, name, T):
     cfg = CONFIGS[name]
     ctx = ctxs[name]
