@@ -174,11 +174,12 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   mark(&rec.k[0]);
   // fp8: e4m3 send rows + scales, the shared-expert rows after the routed ones
   uint8_t* x8 = reinterpret_cast<uint8_t*>(xperm_);
+  int np = 0;
   if (T > 0 && fp8_)
-    launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_,
+    np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_,
                    nullptr, scratch_, st, x8, xs_);
   else if (T > 0)
-    launch_permute(idx_, x, T, E_, k_, h_, 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_, xperm_, scratch_, st,
+    np = launch_permute(idx_, x, T, E_, k_, h_, 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_, xperm_, scratch_, st,
                    nullptr, nullptr, row_align_);
   else
     DWDP_CUDA(cudaMemsetAsync(counts_, 0, size_t(E_) * 4, st));
@@ -324,7 +325,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   // 6. weighted combine (shared rows follow the routed rows of the receive buffer)
   launch_combine(xperm_, row_of_, wts_, shared_ ? dep_recv_ + routed_rows * h_ : nullptr, nullptr,
                  residual ? x : nullptr, y, T, k_, h_, st);
-  launches += fp8_ ? 9 : 8;
+  launches += (T > 0 ? 3 : 0) + np + (nblocks > 0 ? (fp8_ ? 3 : 2) : 0) + 1;
   DWDP_CUDA(cudaGetLastError());
   DWDP_CUDA(cudaEventRecord(rec.moe_end, st));
   rec.rows = routed_rows;

@@ -614,7 +614,8 @@ __device__ __forceinline__ int fixed22(uint32_t b, int emax) {
 
 // One warp per row: pass 1 finds the row exponent, pass 2 writes the three
 // balanced int8 digit planes (Q = d0 + 256 d1 + 65536 d2, |Q| < 2^22).
-constexpr int RQ_WARPS = 2;  // rows (warps) per CTA when the rows are staged in smem
+constexpr int RQ_WARPS = 2;   // rows (warps) per CTA when the rows are staged in smem
+constexpr int RQ_UNROLL = 7;  // 16-byte loads in flight per lane (h = 7168: 4 x 7 x 32 chunks)
 
 __global__ void __launch_bounds__(256) router_quant_kernel(const uint16_t* __restrict__ src,
                                                            int64_t R, int64_t K,
@@ -637,15 +638,15 @@ __global__ void __launch_bounds__(256) router_quant_kernel(const uint16_t* __res
   if (staged) {  // one HBM read: pass 1 stages the row in smem, pass 2 quantises from it
     uint4* srow = rq_rows + (threadIdx.x >> 5) * nch;
     int m = 0;
-    for (int64_t c0 = lane; c0 < nch; c0 += 32 * 4) {
-      uint4 v[4];
+    for (int64_t c0 = lane; c0 < nch; c0 += 32 * RQ_UNROLL) {
+      uint4 v[RQ_UNROLL];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < RQ_UNROLL; ++u) {
         const int64_t c = c0 + 32 * u;
         v[u] = c < nch ? __ldg(row + c) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < RQ_UNROLL; ++u) {
         const int64_t c = c0 + 32 * u;
         if (c < nch) srow[c] = v[u];
         const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
@@ -895,6 +896,72 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
   }
 }
 
+// Row replication with the bulk-copy (TMA) engine: one thread per CTA loads
+// each token row (h*2 bytes) into shared memory with cp.async.bulk and writes
+// it to its k expert-major destinations with k bulk stores, so the 8x write
+// amplification of the permute costs no per-16-byte instructions (the warp
+// copy above is issue-bound at the power-capped SM clock). A ring of PB_BUFS
+// rows keeps the next loads in flight while the stores of a row drain.
+constexpr int PB_BUFS = 3;
+
+__device__ __forceinline__ uint32_t pb_smem(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(32) permute_copy_bulk_kernel(const uint16_t* __restrict__ x,
+                                                               int64_t T, int k, int64_t h,
+                                                               const int32_t* __restrict__ row_of,
+                                                               uint16_t* __restrict__ xperm,
+                                                               int tpc) {
+  extern __shared__ __align__(128) uint8_t pbuf[];
+  __shared__ __align__(8) uint64_t bar[PB_BUFS];
+  if (threadIdx.x != 0) return;
+  const uint32_t bytes = uint32_t(h * 2);
+  const int64_t t0 = int64_t(blockIdx.x) * tpc;
+  const int n = int(T - t0 < tpc ? T - t0 : tpc);
+  if (n <= 0) return;
+  for (int b = 0; b < PB_BUFS; ++b)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(pb_smem(&bar[b])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  auto load = [&](int i) {
+    const int b = i % PB_BUFS;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(pb_smem(&bar[b])),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            pb_smem(pbuf + size_t(b) * bytes)),
+        "l"(x + (t0 + i) * h), "r"(bytes), "r"(pb_smem(&bar[b]))
+        : "memory");
+  };
+  for (int i = 0; i < PB_BUFS && i < n; ++i) load(i);
+  for (int i = 0; i < n; ++i) {
+    const int b = i % PB_BUFS;
+    const uint32_t parity = uint32_t(i / PB_BUFS) & 1u;
+    uint32_t ok = 0;
+    do {
+      asm volatile(
+          "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+          "selp.u32 %0, 1, 0, p;\n}"
+          : "=r"(ok)
+          : "r"(pb_smem(&bar[b])), "r"(parity)
+          : "memory");
+    } while (!ok);
+    const int32_t* dst = row_of + (t0 + i) * k;
+    for (int j = 0; j < k; ++j)
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                       xperm + int64_t(dst[j]) * h),
+                   "r"(pb_smem(pbuf + size_t(b) * bytes)), "r"(bytes)
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (i + PB_BUFS < n) {  // buffer b is refilled once its stores have read it
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      load(i + PB_BUFS);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- combine
 __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict__ O,
                                                       const int32_t* __restrict__ row_of,
@@ -1112,7 +1179,7 @@ int64_t permute_scratch_ints(int64_t T, int E) {
   return nch * E + E;
 }
 
-void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int k, int64_t h,
+int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int k, int64_t h,
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
                     int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
                     int32_t* scratch, cudaStream_t st, uint8_t* xperm8, float* xscale,
@@ -1126,10 +1193,20 @@ void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int
   permute_scan_kernel<<<1, 1024, 2 * E * sizeof(int32_t), st>>>(
       chunk_counts, nch, E, T, shared, row_align, counts, expert_off, mblock_expert, mb_seg, src_row,
       meta);
+  // bf16 rows: rank in the scatter kernel, replicate with the bulk-copy kernel
+  const bool bulk = xperm != nullptr && xperm8 == nullptr && h % 8 == 0 &&
+                    size_t(PB_BUFS) * size_t(h) * 2 <= 48 * 1024;
   if (nch > 0)
     permute_scatter_kernel<<<nch, 256, (E + pch * k) * sizeof(int32_t), st>>>(
-        idx, x, T, E, k, h, chunk_counts, expert_off, row_of, src_row, xperm, xperm8, xscale,
-        meta, shared, pch);
+        idx, x, T, E, k, h, chunk_counts, expert_off, row_of, src_row, bulk ? nullptr : xperm,
+        xperm8, xscale, meta, shared, pch);
+  if (bulk && T > 0) {
+    const int per_sm = 5;  // 43 KB of row buffers per CTA
+    const int tpc = int(std::max<int64_t>(1, (T + 148 * per_sm - 1) / (148 * per_sm)));
+    permute_copy_bulk_kernel<<<unsigned((T + tpc - 1) / tpc), 32, size_t(PB_BUFS) * h * 2, st>>>(
+        x, T, k, h, row_of, xperm, tpc);
+  }
+  return (nch > 0 ? 2 : 0) + 1 + (bulk && T > 0 ? 1 : 0);
 }
 
 void launch_fp8_fill_rows(uint8_t* dst, float* scales, const uint64_t* seeds, int nslots, int rows,

@@ -50,7 +50,8 @@ int64_t permute_scratch_ints(int64_t T, int E);
 //  mb_seg[...]          {first m-block, m-blocks} of each m-block's expert
 //  src_row[routed rows] source token of every expert-major row (nullable)
 //  xperm                expert-major copy of the rows (nullable: GEMM1 gathers)
-void launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int k, int64_t h,
+// Returns the number of kernels launched.
+int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int k, int64_t h,
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
                     int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
                     int32_t* scratch, cudaStream_t st, uint8_t* xperm8 = nullptr,

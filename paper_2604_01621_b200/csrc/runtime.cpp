@@ -584,8 +584,8 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     // shared-expert rows (after meta[2]) with per-row scales; GEMM1 emits
     // bf16 H, which is re-quantised per row for GEMM2.
     uint8_t* x8 = reinterpret_cast<uint8_t*>(xperm_);
-    launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_,
-                   nullptr, scratch_, st, x8, xs_);
+    const int np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_,
+                                  nullptr, meta_, nullptr, scratch_, st, x8, xs_);
     mark(1);
     GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 0, mbseg_,
                 nullptr, xs_, sarena_[0], sarena_[1]};
@@ -599,10 +599,10 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
                         int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
     mark(3);
     launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
-    launches += 9;
+    launches += 3 + np + 3 + 1;  // router 3, permute, GEMM1 + quant + GEMM2, combine
   } else {
-  launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_, xperm_,
-                 scratch_, st, nullptr, nullptr, row_align_);
+  const int np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_,
+                                nullptr, meta_, xperm_, scratch_, st, nullptr, nullptr, row_align_);
   mark(1);
   const CUtensorMap tm_x = shared_ ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
   // Routed A rows come from the materialised expert-major copy. (GEMM1 can
@@ -619,7 +619,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tmd, tmd, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
   mark(3);
   launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
-  launches += 8;
+  launches += 3 + np + 2 + 1;  // router 3, permute, GEMM1, GEMM2, combine
   }
   if (timed) {
     if (!meta_ring_) DWDP_CUDA(cudaHostAlloc(&meta_ring_, kMetaRing * 4 * sizeof(int32_t), 0));

@@ -56,9 +56,9 @@ CONFIGS = {
     "r1": D.DwdpConfig(num_layers=1, max_tokens=512),  # BASELINE config 2 shapes
     # top-k kernel variants: contiguous-lane layout with 8 lanes per group, and
     # softmax over all E without renormalisation (norm_topk = 0)
-    "e128_g4": D.DwdpConfig(num_layers=1, num_experts=128, hidden=512, ffn=256, top_k=4, n_group=4,
-                            topk_group=2, max_tokens=512),
-    "e32_softmax": D.DwdpConfig(num_layers=1, num_experts=32, hidden=512, ffn=256, top_k=3,
+    "e128_g4": D.DwdpConfig(num_layers=1, num_experts=128, hidden=512, ffn=256, shared_ffn=256,
+                            top_k=4, n_group=4, topk_group=2, max_tokens=512),
+    "e32_softmax": D.DwdpConfig(num_layers=1, num_experts=32, hidden=512, ffn=256, shared_ffn=0, top_k=3,
                                 scoring=0, n_group=1, topk_group=1, norm_topk=0, routed_scale=1.0,
                                 max_tokens=512),
 }
