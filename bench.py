@@ -161,7 +161,7 @@ def main():
                          "SURVEY.md section 7; 32768 also reported in DESIGN.md)")
     ap.add_argument("--cv", type=float, default=0.2, help="sequence-length CV")
     ap.add_argument("--layers", type=int, default=8)
-    ap.add_argument("--engine", default="auto", choices=["auto", "copy", "pull"],
+    ap.add_argument("--engine", default="auto", choices=["auto", "copy", "pull", "hybrid"],
                     help="auto: copy engine unless its measured GB/s leaves prefetch exposed")
     ap.add_argument("--slice-size", type=int, default=64 << 20)
     ap.add_argument("--no-tdm", action="store_true")
@@ -222,7 +222,8 @@ def main():
     fp8 = args.dtype == "fp8"
 
     cfg = D.DwdpConfig(num_layers=layers, rank=rank, group_size=world, device=local,
-                       engine=D.ENGINE_PULL if args.engine == "pull" else D.ENGINE_COPY,
+                       engine={"pull": D.ENGINE_PULL, "hybrid": D.ENGINE_HYBRID}.get(args.engine,
+                                                                                      D.ENGINE_COPY),
                        tdm=0 if args.no_tdm else 1, slice_size=args.slice_size,
                        merge_elim=0 if args.merged else 1, pull_ctas=args.pull_ctas,
                        ce_inflight=args.ce_inflight,
@@ -262,7 +263,7 @@ def main():
         ctx.stack_forward(x[:T], y[:T])
     torch.cuda.synchronize()
     wrecs = ctx.records()
-    engine = "copy" if cfg.engine == D.ENGINE_COPY else "pull"
+    engine = {D.ENGINE_COPY: "copy", D.ENGINE_PULL: "pull", D.ENGINE_HYBRID: "hybrid"}[cfg.engine]
     if world > 1 and args.engine == "auto":
         # choose by measured GB/s: keep the copy engine (no SM cost) while its
         # bandwidth hides the pull under the compute window, else the TMA kernel

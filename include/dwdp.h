@@ -212,6 +212,8 @@ int dwdp_analytic_compare(const dwdp_model_spec* m, const dwdp_gpu_spec* g,
 #define DWDP_WEIGHT_FP8 1
 #define DWDP_ENGINE_COPY 0 /* copy-engine peer copies on a side stream  */
 #define DWDP_ENGINE_PULL 1 /* one-launch SM pull kernel over NVLink      */
+#define DWDP_ENGINE_HYBRID 2 /* odd TDM slices on the pull kernel, even ones
+                                on the copy engines, both at once          */
 
 typedef struct {
   /* model */

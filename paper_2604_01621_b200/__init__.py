@@ -3,7 +3,7 @@
 The drop-in boundary is the C-ABI in include/dwdp.h (libdwdp.so, sm_100a).
 This package mirrors the reference operator API (dwdpsim names) on top of it.
 """
-from ._lib import (ENGINE_COPY, ENGINE_PULL, WEIGHT_BF16, WEIGHT_FP8, ConfigError, CudaError, InvariantViolation,  # noqa: F401
+from ._lib import (ENGINE_COPY, ENGINE_HYBRID, ENGINE_PULL, WEIGHT_BF16, WEIGHT_FP8, ConfigError, CudaError, InvariantViolation,  # noqa: F401
                    lib)
 from .planning import (CopyPlan, GpuSpec, IslDist, MoeModelSpec, OpCost, PlacementPlan,  # noqa: F401
                        RankBatch, ShardRef, Slice, WorkloadSpec, analytic_compare,

@@ -13,7 +13,7 @@ P = C.c_void_p
 
 DWDP_OK, DWDP_ERR_CONFIG, DWDP_ERR_INVARIANT, DWDP_ERR_CUDA = 0, 2, 3, 4
 IPC_BLOB_BYTES = 512
-ENGINE_COPY, ENGINE_PULL = 0, 1
+ENGINE_COPY, ENGINE_PULL, ENGINE_HYBRID = 0, 1, 2
 WEIGHT_BF16, WEIGHT_FP8 = 0, 1
 
 

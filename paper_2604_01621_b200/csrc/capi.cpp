@@ -451,7 +451,8 @@ int dwdp_prefetch_times(dwdp_ctx* c, dwdp_prefetch h, int64_t* s, int64_t* e, do
 
 int dwdp_ctx_set_engine(dwdp_ctx* c, int engine) {
   return guard([&] {
-    dwdp::require(engine == DWDP_ENGINE_COPY || engine == DWDP_ENGINE_PULL, "ctx: unknown engine");
+    dwdp::require(engine == DWDP_ENGINE_COPY || engine == DWDP_ENGINE_PULL || engine == DWDP_ENGINE_HYBRID,
+                  "ctx: unknown engine");
     C(c).cfg.engine = engine;
   });
 }

@@ -84,7 +84,8 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   require(N_ >= 1, "ctx: group_size must be >= 1");
   require(rank_ >= 0 && rank_ < N_, "ctx: rank out of range");
   require(c.max_tokens >= 1, "ctx: max_tokens must be >= 1");
-  require(c.engine == DWDP_ENGINE_COPY || c.engine == DWDP_ENGINE_PULL, "ctx: unknown engine");
+  require(c.engine == DWDP_ENGINE_COPY || c.engine == DWDP_ENGINE_PULL || c.engine == DWDP_ENGINE_HYBRID,
+          "ctx: unknown engine");
   require(!c.tdm || c.slice_size > 0, "dwdp.slice_size must be > 0 with tdm");
   require(!c.tdm || c.slice_size % 16 == 0, "dwdp.slice_size must be a multiple of 16 bytes");
   DeviceGuard dg(c.device);
@@ -210,7 +211,7 @@ Ctx::~Ctx() {
   if (meta_ring_) cudaFreeHost(meta_ring_);
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   void* bufs[] = {arena_[0], arena_[1], arena_[2], router_w_, bias_, slot_tab_, logits_, idx_,
-                  wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_,
+                  wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_, pull_items_odd_,
                   router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_, mbseg_, dep_seg_, srcrow_,
                   sarena_[0], sarena_[1], sarena_[2], h8_, xs_, hs_};
   if (dep_seg_host_) cudaFreeHost(dep_seg_host_);
@@ -385,6 +386,14 @@ void Ctx::link_local(const std::vector<Ctx*>& all) {
       }
   if (!pull_items_) pull_items_ = static_cast<PullItem*>(dalloc(items.size() * sizeof(PullItem), &workspace_bytes));
   DWDP_CUDA(cudaMemcpy(pull_items_, items.data(), items.size() * sizeof(PullItem), cudaMemcpyHostToDevice));
+  // hybrid engine: the odd slices of every (weight layer, parity) list
+  n_odd_ = n / 2;
+  std::vector<PullItem> odd(size_t(WL_) * 2 * std::max<size_t>(n_odd_, 1));
+  for (size_t lp = 0; lp < size_t(WL_) * 2; ++lp)
+    for (size_t i = 0; i < n_odd_; ++i) odd[lp * n_odd_ + i] = items[lp * n + 2 * i + 1];
+  if (!pull_items_odd_)
+    pull_items_odd_ = static_cast<PullItem*>(dalloc(odd.size() * sizeof(PullItem), &workspace_bytes));
+  DWDP_CUDA(cudaMemcpy(pull_items_odd_, odd.data(), odd.size() * sizeof(PullItem), cudaMemcpyHostToDevice));
 }
 
 // ===================================================================== //
@@ -484,6 +493,35 @@ int64_t Ctx::prefetch_issue(int64_t g) {
                 cfg.pull_ctas > 0 ? cfg.pull_ctas : num_sms_, copy_st_);
     ++launches;
     DWDP_CUDA(cudaGetLastError());
+  } else if (cfg.engine == DWDP_ENGINE_HYBRID) {
+    // Both engines at once: odd slices through the pull kernel on the copy
+    // stream, even slices as copy-engine copies on the side streams.
+    require(pull_items_odd_ != nullptr, "prefetch_issue: pull lists not built (peers not wired)");
+    require(!ce_st_.empty(), "prefetch_issue: hybrid engine needs ce_inflight >= 2");
+    const size_t ns = ce_st_.size();
+    for (size_t i = 0; i < ns; ++i) {
+      DWDP_CUDA(cudaEventRecord(ce_fork_[i], copy_st_));
+      DWDP_CUDA(cudaStreamWaitEvent(ce_st_[i], ce_fork_[i], 0));
+    }
+    if (n_odd_ > 0) {
+      launch_pull(pull_items_odd_ + (size_t(wl) * 2 + size_t(par)) * n_odd_, int(n_odd_),
+                  cfg.pull_ctas > 0 ? cfg.pull_ctas : num_sms_, copy_st_);
+      ++launches;
+      DWDP_CUDA(cudaGetLastError());
+    }
+    std::map<std::pair<int, uint64_t>, const ShardRun*> by_shard;
+    for (const auto& r : runs_) by_shard[{r.peer, r.param_id}] = &r;
+    for (size_t i = 0; i < plan_slices_.size(); i += 2) {
+      const Slice& s = plan_slices_[i];
+      const ShardRun* r = by_shard.at({s.src_rank, s.param_id});
+      DWDP_CUDA(cudaMemcpyAsync(dst_addr(r->tensor, par, *r, s.dst_offset),
+                                peer_src(r->peer, r->tensor, wl, s.src_offset), s.length,
+                                cudaMemcpyDeviceToDevice, ce_st_[(i / 2) % ns]));
+    }
+    for (size_t i = 0; i < ns; ++i) {
+      DWDP_CUDA(cudaEventRecord(ce_join_[i], ce_st_[i]));
+      DWDP_CUDA(cudaStreamWaitEvent(copy_st_, ce_join_[i], 0));
+    }
   } else {
     // ce_inflight copy streams: slice i of the TDM plan goes to stream
     // i mod ce_inflight, so consecutive slices (different peers in the plan's

@@ -181,6 +181,8 @@ class Ctx {
   std::vector<Plan> plans_;
   std::vector<int64_t> plan_of_g_;  // global layer -> plan index (-1 preloaded)
   PullItem* pull_items_ = nullptr;  // device [WL][2][n_slices]
+  PullItem* pull_items_odd_ = nullptr;  // hybrid: device [WL][2][n_slices / 2] (odd slices)
+  size_t n_odd_ = 0;
   int64_t cursor_ = 0;              // next global layer of stack_forward
   std::vector<int> resident_parity_;
   std::deque<LayerRec> recs_;

@@ -23,13 +23,13 @@ import paper_2604_01621_b200 as D  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--engine", default="pull", choices=["pull", "copy"])
+    ap.add_argument("--engine", default="pull", choices=["pull", "copy", "hybrid"])
     ap.add_argument("--plans", type=int, default=4)
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp8"])
     ap.add_argument("--slice-size", type=int, default=64 << 20)
     a = ap.parse_args()
     assert torch.cuda.device_count() >= 2, "needs two GPUs"
-    eng = D.ENGINE_PULL if a.engine == "pull" else D.ENGINE_COPY
+    eng = {"pull": D.ENGINE_PULL, "copy": D.ENGINE_COPY, "hybrid": D.ENGINE_HYBRID}[a.engine]
     ctxs = [D.DwdpContext(D.DwdpConfig(num_layers=2, rank=r, group_size=2, device=r, engine=eng,
                                        slice_size=a.slice_size, weight_layers=2, max_tokens=128,
                                        weight_dtype=D.WEIGHT_FP8 if a.dtype == "fp8" else
