@@ -162,7 +162,8 @@ def main():
     ap.add_argument("--cv", type=float, default=0.2, help="sequence-length CV")
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--engine", default="auto", choices=["auto", "copy", "pull", "hybrid"],
-                    help="auto: copy engine unless its measured GB/s leaves prefetch exposed")
+                    help="auto: copy engine unless its measured GB/s leaves prefetch exposed, "
+                         "then the hybrid engine")
     ap.add_argument("--slice-size", type=int, default=64 << 20)
     ap.add_argument("--no-tdm", action="store_true")
     ap.add_argument("--merged", action="store_true", help="merge_elim off (D2D merge baseline)")
@@ -271,8 +272,10 @@ def main():
         wait = sum(r["gate_wait_ns"] for r in steady)
         moe = sum(r["moe_ns"] for r in steady)
         if steady and wait > 0.02 * moe:
-            ctx.set_engine(D.ENGINE_PULL)
-            engine = "pull"
+            # both engines at once (odd TDM slices on the pull kernel, even on
+            # the copy engines): 786 GB/s vs 687 (copy) / 647 (pull) alone
+            ctx.set_engine(D.ENGINE_HYBRID)
+            engine = "hybrid"
             T = toks[0][rank]
             ctx.stack_forward(x[:T], y[:T])
             torch.cuda.synchronize()

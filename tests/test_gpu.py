@@ -270,6 +270,7 @@ MID = dict(num_layers=3, num_experts=64, hidden=1024, ffn=256, shared_ffn=256, t
 
 @pytest.mark.parametrize("engine,tdm,slice_size,merge", [(D.ENGINE_COPY, 1, 1 << 20, 1),
                                                           (D.ENGINE_PULL, 1, 1 << 20, 1),
+                                                          (D.ENGINE_HYBRID, 1, 1 << 20, 1),
                                                           (D.ENGINE_COPY, 0, 1 << 20, 1),
                                                           (D.ENGINE_COPY, 1, 300_000, 0)])
 def test_dwdp_group_of_two_matches_all_local(dev, engine, tdm, slice_size, merge):

@@ -12,7 +12,7 @@ from conftest import ROOT
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
-@pytest.mark.parametrize("engine,weight", [(0, 0), (1, 0), (1, 1), (0, 1)])
+@pytest.mark.parametrize("engine,weight", [(0, 0), (1, 0), (2, 0), (1, 1), (0, 1)])
 def test_dwdp_and_dep_match_all_local(engine, weight):
     n = torch.cuda.device_count()
     if n < 2:
