@@ -163,7 +163,7 @@ def main():
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--engine", default="auto", choices=["auto", "copy", "pull", "hybrid"],
                     help="auto: copy engine unless its measured GB/s leaves prefetch exposed, "
-                         "then the hybrid engine")
+                         "then the SM engine (pull or hybrid) with the higher measured GB/s")
     ap.add_argument("--slice-size", type=int, default=64 << 20)
     ap.add_argument("--no-tdm", action="store_true")
     ap.add_argument("--merged", action="store_true", help="merge_elim off (D2D merge baseline)")
@@ -272,14 +272,20 @@ def main():
         wait = sum(r["gate_wait_ns"] for r in steady)
         moe = sum(r["moe_ns"] for r in steady)
         if steady and wait > 0.02 * moe:
-            # both engines at once (odd TDM slices on the pull kernel, even on
-            # the copy engines): 786 GB/s vs 687 (copy) / 647 (pull) alone
-            ctx.set_engine(D.ENGINE_HYBRID)
-            engine = "hybrid"
-            T = toks[0][rank]
-            ctx.stack_forward(x[:T], y[:T])
-            torch.cuda.synchronize()
-            ctx.records()
+            # the copy engine leaves prefetch exposed: run one step on each SM
+            # engine (TMA pull kernel; hybrid = pull kernel + copy engines on
+            # alternating slices) and keep the one with the higher in-step GB/s
+            best = (0.0, "pull", D.ENGINE_PULL)
+            for name, eid in (("pull", D.ENGINE_PULL), ("hybrid", D.ENGINE_HYBRID)):
+                ctx.set_engine(eid)
+                T = toks[0][rank]
+                ctx.stack_forward(x[:T], y[:T])
+                torch.cuda.synchronize()
+                rr = [r for r in ctx.records() if r["prefetch_bytes"] > 0]
+                gbs = sum(r["prefetch_bytes"] for r in rr) / max(sum(r["prefetch_ns"] for r in rr), 1.0)
+                best = max(best, (gbs, name, eid))
+            ctx.set_engine(best[2])
+            engine = best[1]
     engines = [None] * world
     if world > 1:
         dist.all_gather_object(engines, engine)
