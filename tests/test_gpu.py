@@ -342,3 +342,36 @@ def test_gemm_pair_matches_single_cta(dev, monkeypatch):
         torch.cuda.synchronize()
         c.close()
     assert _rel(outs[0], outs[1]) < 1e-3
+
+
+@pytest.mark.parametrize("group,extra,engine", [(3, 0, D.ENGINE_COPY), (3, 1, D.ENGINE_PULL),
+                                                (2, 5, D.ENGINE_COPY), (5, 0, D.ENGINE_HYBRID)])
+def test_dwdp_non_divisible_and_redundant_placements(dev, group, extra, engine):
+    """non-divisible (N = 3, 5) and redundant (extra > 0)
+    placements. Ranks own overlapping expert arcs, fetch sources come from
+    assign_fetch_sources and a peer's slots can form several contiguous runs
+    (multi-run shards); outputs stay bit-identical to the all-local model."""
+    full = D.DwdpContext(D.DwdpConfig(**MID))
+    full.init_weights()
+    ranks = [D.DwdpContext(D.DwdpConfig(**MID, rank=r, group_size=group, extra_redundancy=extra,
+                                        engine=engine, slice_size=1 << 20))
+             for r in range(group)]
+    for c in ranks:
+        c.init_weights()
+    D.DwdpContext.link_local(ranks)
+    plan = D.build_placement(MID["num_experts"], group, extra)
+    xs = [make_x(64 + 29 * r, MID["hidden"], 90 + r, dev) for r in range(group)]
+    for g in range(4):
+        for r in range(group):
+            y = ranks[r].layer_forward(g, xs[r], residual=False)
+            yf = full.moe_forward(g % 3, xs[r])
+            torch.cuda.synchronize()
+            assert torch.equal(y, yf), (group, extra, g, r)
+    for r in range(group):
+        recs = ranks[r].records()
+        fetched = len(plan.fetch_lists[r])
+        assert recs[1]["prefetch_bytes"] == fetched * 3 * MID["hidden"] * MID["ffn"] * 2
+        for e, src in plan.fetch_lists[r][:3]:
+            assert (ranks[r].read_expert(3 % 3, e, 0) == ranks[src].read_expert(3 % 3, e, 0)).all()
+    for c in ranks + [full]:
+        c.close()
