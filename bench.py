@@ -446,6 +446,26 @@ def main():
                                                    "gemm2_ns", "combine_ns")},
                "dwdp_over_dep": value / dval}
 
+    # ---- whole-step roofline (north star / SURVEY.md §8(d)): per layer the
+    # slower of the layer's flops at the tensor peak and the remote-expert
+    # bytes over NVLink (900 GB/s per direction), summed over the timed steps
+    # with each step's heaviest rank
+    f_tok = 2.0 * h * (3 * k * f + 3 * R1["fs"] + R1["E"])
+    p_peak = pk["bf16_tflops_sustained"] * 1e12 * (2 if fp8 else 1)
+    c_loc = -(-R1["E"] // world)
+    b_rem = (R1["E"] - c_loc) * 3.0 * h * f * (1 if fp8 else 2) if world > 1 else 0.0
+    t_tensor = sum(layers * max(toks[it]) * f_tok / p_peak for it in range(args.warmup, iters))
+    t_link = args.steps * layers * b_rem / 900e9
+    t_roof = sum(layers * max(max(toks[it]) * f_tok / p_peak, b_rem / 900e9)
+                 for it in range(args.warmup, iters))
+    step_roof = {"t_roof_ms_per_step": t_roof * 1e3 / args.steps,
+                 "t_measured_ms_per_step": ms / args.steps, "frac": t_roof / (ms * 1e-3),
+                 "bound": "tensor" if t_tensor >= t_link else "nvlink",
+                 "t_tensor_ms_per_step": t_tensor * 1e3 / args.steps,
+                 "t_nvlink_ms_per_step": t_link * 1e3 / args.steps,
+                 "flops_per_token_layer": f_tok, "remote_bytes_per_layer": b_rem,
+                 "peak_tflops": p_peak / 1e12, "link_gbs": 900.0}
+
     # ---- RunReport accounting (simcore.hpp:29-61, 177-213) over the measured
     # events of every rank, and the analytic model beside it (a15, a16)
     acct = None
@@ -503,7 +523,7 @@ def main():
                           "gbs": pf_bytes / pf_ns if pf_ns else None,
                           "ms_per_layer": split["prefetch_ns"]} if world > 1 else None),
             "kernel_ms_per_layer": {k2.replace("_ns", ""): v for k2, v in split.items()},
-            "roofline": roof, "routing": routing,
+            "roofline": roof, "step_roofline": step_roof, "routing": routing,
             "dep_baseline": dep, "report": acct,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),

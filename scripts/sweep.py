@@ -53,6 +53,7 @@ def main():
                            "dep_comm_ms_per_layer": dep.get("comm_ms_per_layer"),
                            "engine": d["config"].get("prefetch_engine"),
                            "prefetch_gbs": (d.get("prefetch") or {}).get("gbs"),
+                           "step_roofline_frac": (d.get("step_roofline") or {}).get("frac"),
                            "clocks": d.get("clocks")}
                 out.write(json.dumps(rec) + "\n")
                 out.flush()

@@ -64,7 +64,8 @@ def main():
                                "routing": d.get("routing"),
                                "engine": d["config"].get("prefetch_engine"),
                                "prefetch_gbs": (d.get("prefetch") or {}).get("gbs"),
-                               "clocks": d.get("clocks")}
+                               "step_roofline_frac": (d.get("step_roofline") or {}).get("frac"),
+                           "clocks": d.get("clocks")}
                     out.write(json.dumps(rec) + "\n")
                     out.flush()
                     print(json.dumps(rec), flush=True)
