@@ -179,6 +179,7 @@ def main():
                     help="expert weights: bf16, or e4m3 W8A8 with per-row scales (config 5)")
     ap.add_argument("--decode", type=int, default=0,
                     help="decode phase (config 5): B tokens/rank every step instead of prefill batches")
+    ap.add_argument("--trace", default="", help="write a chrome trace of the timed DWDP steps here")
     ap.add_argument("--zipf", type=float, default=0.0,
                     help="expert-routing skew s: router bias -ZIPF_BETA*s*ln(e+1)")
     args = ap.parse_args()
@@ -470,8 +471,12 @@ def main():
     # events of every rank, and the analytic model beside it (a15, a16)
     acct = None
     if rank == 0:
-        tab = RP.report_from_records(all_recs, layers, 0)
+        tab, evs = RP.report_from_records(all_recs, layers, 0, with_events=True)
         acct = {"dwdp": tab.as_dict(), "breakdown_csv": tab.to_csv()}
+        if args.trace:
+            with open(args.trace, "w") as fh:
+                json.dump(RP.chrome_trace(evs), fh)
+            acct["trace"] = args.trace
         if dep is not None:
             dtab = RP.report_from_records(all_drecs, layers, 0)
             cmp_ = RP.compare_reports(dtab, tab)  # a = DEP baseline, b = DWDP

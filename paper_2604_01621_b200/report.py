@@ -130,3 +130,22 @@ def compare_reports(a: BreakdownTable, b: BreakdownTable) -> ComparisonTable:
              "delta_frac": out.delta_frac[i] if out.has_delta[i] else None} for i in range(NC)]
     return ComparisonTable(rows, out.a_latency_us, out.b_latency_us, out.overall_frac,
                            out.gross_sync_comm_pct, out)
+
+
+DETAIL_NAMES = {v: k for k, v in DETAILS.items()}
+
+
+def chrome_trace(events: np.ndarray) -> list[dict]:
+    """Chrome trace of measured SimEvents, in the reference's layout
+    (report_to_chrome_trace, src/report_io.cpp:58-76): one complete ("X")
+    event per SimEvent, pid = rank, tid 0 compute / 1 copy stream, us."""
+    out = []
+    for e in events:
+        cat = CATEGORIES[int(e["category"])]
+        det = DETAIL_NAMES.get(int(e["detail"]), "")
+        name = cat + (":" + det if det else "") + " L" + str(int(e["layer"]))
+        out.append({"name": name, "cat": cat, "ph": "X", "ts": float(e["start_ns"]) / 1e3,
+                    "dur": float(e["end_ns"] - e["start_ns"]) / 1e3, "pid": int(e["rank"]),
+                    "tid": int(e["stream"]),
+                    "args": {"iteration": int(e["iteration"]), "bytes": float(e["bytes"])}})
+    return out

@@ -114,3 +114,18 @@ def test_report_from_records_dwdp_and_dep():
     assert "GrossSyncComm" in cmp_.to_csv()
     with pytest.raises(D.ConfigError):
         R.report_from_records([recs[:5]], L, 1)  # partial iteration
+
+
+def test_chrome_trace_layout():
+    recs, t = [], 0.0
+    for g in range(4):
+        recs.append(_rec(g, 100, t, 50.0 if g == 2 else 0.0, (10.0, 5.0, 40.0, 20.0, 5.0),
+                         pf=(t - 30, t + 1)))
+        t = recs[-1]["end_ns"] + 10
+    _, ev = R.report_from_records([recs], 2, 0, with_events=True)
+    tr = R.chrome_trace(ev)
+    assert len(tr) == len(ev)
+    w = [x for x in tr if x["name"].startswith("SyncWait:weight_wait")]
+    assert w and all(x["tid"] == 0 and x["ph"] == "X" for x in w)
+    p = [x for x in tr if x["cat"] == "P2PCopy"]
+    assert p and all(x["tid"] == 1 for x in p) and p[0]["args"]["bytes"] == 1e9
