@@ -1036,19 +1036,37 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-struct PullCursor {  // walks this CTA's chunks: items blockIdx.x + j*gridDim.x
-  int it;
+// Chunk c of slice i has global index c * n + i (slice-interleaved), and CTA
+// b takes indices b, b + grid, b + 2 grid, ...: every CTA gets the same number
+// of chunks whatever the slice count and sizes, and the chunks in flight at
+// any moment come from all slices -- i.e. from every peer of the TDM rotation
+// at once -- instead of one CTA streaming a whole 64 MB slice from one peer.
+// Indices past the end of a shorter slice are skipped.
+struct PullCursor {
+  uint64_t g;  // global chunk index
+  int it;      // slice of g (n = done)
   uint64_t off;
-  __device__ void advance(const PullItem* items) {
-    off += PULL_CHUNK;
-    if (off >= items[it].len) {
-      it += gridDim.x;
-      off = 0;
+  __device__ void seek(const PullItem* items, int n, uint64_t total) {
+    while (g < total) {
+      const int i = int(g % uint64_t(n));
+      const uint64_t o = (g / uint64_t(n)) * PULL_CHUNK;
+      if (o < items[i].len) {
+        it = i;
+        off = o;
+        return;
+      }
+      g += gridDim.x;
     }
+    it = n;
+  }
+  __device__ void advance(const PullItem* items, int n, uint64_t total) {
+    g += gridDim.x;
+    seek(items, n, total);
   }
 };
 
-__global__ void __launch_bounds__(32) tma_pull_kernel(const PullItem* __restrict__ items, int n) {
+__global__ void __launch_bounds__(32) tma_pull_kernel(const PullItem* __restrict__ items, int n,
+                                                      uint64_t total) {
   __shared__ __align__(128) uint8_t buf[PULL_BUFS][PULL_CHUNK];
   __shared__ __align__(8) uint64_t bar[PULL_BUFS];
   if (threadIdx.x != 0) return;
@@ -1068,11 +1086,13 @@ __global__ void __launch_bounds__(32) tma_pull_kernel(const PullItem* __restrict
         "l"(static_cast<const uint8_t*>(w.src) + c.off), "r"(len), "r"(smem_addr(&bar[b]))
         : "memory");
   };
-  PullCursor prod{int(blockIdx.x), 0}, cons = prod;
+  PullCursor prod{blockIdx.x, 0, 0};
+  prod.seek(items, n, total);
+  PullCursor cons = prod;
   int issued = 0, done = 0;
   while (issued < PULL_BUFS && prod.it < n) {  // prologue: fill the ring
     load(issued, prod);
-    prod.advance(items);
+    prod.advance(items, n, total);
     ++issued;
   }
   while (done < issued) {
@@ -1098,12 +1118,12 @@ __global__ void __launch_bounds__(32) tma_pull_kernel(const PullItem* __restrict
         "r"(smem_addr(buf[b])), "r"(len)
         : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    cons.advance(items);
+    cons.advance(items, n, total);
     ++done;
     if (prod.it < n) {  // refill buffer b once its store has read shared memory
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       load(b, prod);
-      prod.advance(items);
+      prod.advance(items, n, total);
       ++issued;
     }
   }
@@ -1231,8 +1251,9 @@ void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
     combine_kernel<<<unsigned(T), 128, 0, st>>>(O, row_of, wts, S, s_meta, resid, y, T, k, h);
 }
 
-void launch_pull(const PullItem* items, int n, int ctas, cudaStream_t st) {
-  if (n > 0) tma_pull_kernel<<<ctas, 32, 0, st>>>(items, n);
+void launch_pull(const PullItem* items, int n, uint64_t max_len, int ctas, cudaStream_t st) {
+  const uint64_t total = (max_len + PULL_CHUNK - 1) / PULL_CHUNK * uint64_t(n);
+  if (n > 0) tma_pull_kernel<<<ctas, 32, 0, st>>>(items, n, total);
 }
 
 }  // namespace dwdp

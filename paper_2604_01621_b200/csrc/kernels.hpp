@@ -82,7 +82,8 @@ struct PullItem {
   void* dst;
   uint64_t len;
 };
-void launch_pull(const PullItem* items_dev, int n_items, int ctas, cudaStream_t st);
+// max_len: the longest item (bytes); chunks are interleaved across items.
+void launch_pull(const PullItem* items_dev, int n_items, uint64_t max_len, int ctas, cudaStream_t st);
 
 // Grouped GEMM on tcgen05 (gemm_sm100.cu). See GemmArgs there.
 struct GroupedGemm;

@@ -386,6 +386,8 @@ void Ctx::link_local(const std::vector<Ctx*>& all) {
       }
   if (!pull_items_) pull_items_ = static_cast<PullItem*>(dalloc(items.size() * sizeof(PullItem), &workspace_bytes));
   DWDP_CUDA(cudaMemcpy(pull_items_, items.data(), items.size() * sizeof(PullItem), cudaMemcpyHostToDevice));
+  pull_max_len_ = 0;
+  for (const Slice& sl : plan_slices_) pull_max_len_ = std::max<uint64_t>(pull_max_len_, sl.length);
   // hybrid engine: the odd slices of every (weight layer, parity) list
   n_odd_ = n / 2;
   std::vector<PullItem> odd(size_t(WL_) * 2 * std::max<size_t>(n_odd_, 1));
@@ -489,7 +491,7 @@ int64_t Ctx::prefetch_issue(int64_t g) {
   if (cfg.engine == DWDP_ENGINE_PULL) {
     require(pull_items_ != nullptr, "prefetch_issue: pull lists not built (peers not wired)");
     const size_t n = plan_slices_.size();
-    launch_pull(pull_items_ + (size_t(wl) * 2 + size_t(par)) * n, int(n),
+    launch_pull(pull_items_ + (size_t(wl) * 2 + size_t(par)) * n, int(n), pull_max_len_,
                 cfg.pull_ctas > 0 ? cfg.pull_ctas : num_sms_, copy_st_);
     ++launches;
     DWDP_CUDA(cudaGetLastError());
@@ -504,7 +506,7 @@ int64_t Ctx::prefetch_issue(int64_t g) {
       DWDP_CUDA(cudaStreamWaitEvent(ce_st_[i], ce_fork_[i], 0));
     }
     if (n_odd_ > 0) {
-      launch_pull(pull_items_odd_ + (size_t(wl) * 2 + size_t(par)) * n_odd_, int(n_odd_),
+      launch_pull(pull_items_odd_ + (size_t(wl) * 2 + size_t(par)) * n_odd_, int(n_odd_), pull_max_len_,
                   cfg.pull_ctas > 0 ? cfg.pull_ctas : num_sms_, copy_st_);
       ++launches;
       DWDP_CUDA(cudaGetLastError());

@@ -183,6 +183,7 @@ class Ctx {
   PullItem* pull_items_ = nullptr;  // device [WL][2][n_slices]
   PullItem* pull_items_odd_ = nullptr;  // hybrid: device [WL][2][n_slices / 2] (odd slices)
   size_t n_odd_ = 0;
+  uint64_t pull_max_len_ = 0;          // longest slice (pull-kernel chunk grid)
   int64_t cursor_ = 0;              // next global layer of stack_forward
   std::vector<int> resident_parity_;
   std::deque<LayerRec> recs_;
