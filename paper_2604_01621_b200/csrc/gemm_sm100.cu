@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(256, 1)
 // segments padded to 256 rows (permute row_align 256), so both m-blocks of a
 // pair always belong to the same expert.
 constexpr int P_STAGE = 2 * BM * BK * 2;  // A (16 KB) + half of B (16 KB) per CTA
-// 6 stages (194 KB) leave room on every SM for one prefetch pull CTA (33 KB):
+// 6 stages (194 KB) leave room on every SM for one prefetch pull CTA (25 KB):
 // with 7 the pull kernel could not co-reside and DWDP at N=4 fell 10-20%.
 constexpr int P_STAGES = 6;
 constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE + 1024 + 256;

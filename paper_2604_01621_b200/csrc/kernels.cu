@@ -1024,13 +1024,15 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
 }
 
 // ---------------------------------------------------------------- pull
-// TMA bulk pull: one elected thread per CTA streams its slices (slice i by
-// CTA i mod grid, so the slices in flight follow the TDM peer rotation) from
-// peer HBM over NVLink into a 2 x 16 KB shared-memory ring
-// (cp.async.bulk global->shared, mbarrier completion) and out to the local
-// receive buffer (cp.async.bulk shared->global, bulk-group completion). The
-// 33 KB footprint lets a pull CTA sit next to a grouped-GEMM CTA on every SM.
-constexpr int PULL_CHUNK = 8192, PULL_BUFS = 4;
+// TMA bulk pull: one elected thread per CTA streams 8 KB chunks of the copy
+// plan's slices (interleaved over slices, see PullCursor) from peer HBM over
+// NVLink into a shared-memory ring (cp.async.bulk global->shared, mbarrier
+// completion) and out to the local receive buffer (cp.async.bulk
+// shared->global, bulk-group completion).
+// 3 x 8 KB ring (25 KB with the barriers): fits next to a 194 KB grouped-GEMM
+// CTA on every SM (228 KB per SM, 1 KB reserved per CTA), so the pull runs
+// concurrently with the expert GEMMs instead of queueing behind them.
+constexpr int PULL_CHUNK = 8192, PULL_BUFS = 3;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
