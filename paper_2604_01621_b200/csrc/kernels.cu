@@ -1029,10 +1029,11 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
 // NVLink into a shared-memory ring (cp.async.bulk global->shared, mbarrier
 // completion) and out to the local receive buffer (cp.async.bulk
 // shared->global, bulk-group completion).
-// 3 x 8 KB ring (25 KB with the barriers): fits next to a 194 KB grouped-GEMM
+// 3 x 16 KB ring (49 KB with the barriers): fits next to a 162 KB grouped-GEMM
 // CTA on every SM (228 KB per SM, 1 KB reserved per CTA), so the pull runs
-// concurrently with the expert GEMMs instead of queueing behind them.
-constexpr int PULL_CHUNK = 8192, PULL_BUFS = 3;
+// concurrently with the expert GEMMs instead of queueing behind them. 48 KB
+// in flight per SM: the all-to-all pull is latency x bytes-in-flight bound.
+constexpr int PULL_CHUNK = 16384, PULL_BUFS = 3;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -1069,8 +1070,9 @@ struct PullCursor {
 
 __global__ void __launch_bounds__(32) tma_pull_kernel(const PullItem* __restrict__ items, int n,
                                                       uint64_t total) {
-  __shared__ __align__(128) uint8_t buf[PULL_BUFS][PULL_CHUNK];
+  extern __shared__ __align__(128) uint8_t pull_smem[];  // PULL_BUFS chunks (dynamic: > 48 KB)
   __shared__ __align__(8) uint64_t bar[PULL_BUFS];
+  auto buf = [&](int b) { return pull_smem + size_t(b) * PULL_CHUNK; };
   if (threadIdx.x != 0) return;
   for (int b = 0; b < PULL_BUFS; ++b)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[b])));
@@ -1084,7 +1086,7 @@ __global__ void __launch_bounds__(32) tma_pull_kernel(const PullItem* __restrict
                  : "memory");
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_addr(buf[b])),
+            smem_addr(buf(b))),
         "l"(static_cast<const uint8_t*>(w.src) + c.off), "r"(len), "r"(smem_addr(&bar[b]))
         : "memory");
   };
@@ -1117,7 +1119,7 @@ __global__ void __launch_bounds__(32) tma_pull_kernel(const PullItem* __restrict
         "{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
         "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, pol;\n}" ::"l"(
             static_cast<uint8_t*>(w.dst) + cons.off),
-        "r"(smem_addr(buf[b])), "r"(len)
+        "r"(smem_addr(buf(b))), "r"(len)
         : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     cons.advance(items, n, total);
@@ -1255,7 +1257,15 @@ void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
 
 void launch_pull(const PullItem* items, int n, uint64_t max_len, int ctas, cudaStream_t st) {
   const uint64_t total = (max_len + PULL_CHUNK - 1) / PULL_CHUNK * uint64_t(n);
-  if (n > 0) tma_pull_kernel<<<ctas, 32, 0, st>>>(items, n, total);
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_set[dev]) {
+    cudaFuncSetAttribute(tma_pull_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         PULL_BUFS * PULL_CHUNK);
+    attr_set[dev] = true;
+  }
+  if (n > 0) tma_pull_kernel<<<ctas, 32, PULL_BUFS * PULL_CHUNK, st>>>(items, n, total);
 }
 
 }  // namespace dwdp
