@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 
 #include "kernels.hpp"
@@ -1033,7 +1034,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
 // CTA on every SM (228 KB per SM, 1 KB reserved per CTA), so the pull runs
 // concurrently with the expert GEMMs instead of queueing behind them. 48 KB
 // in flight per SM: the all-to-all pull is latency x bytes-in-flight bound.
-constexpr int PULL_CHUNK = 16384, PULL_BUFS = 3;
+constexpr int PULL_CHUNK_DEFAULT = 16384, PULL_BUFS_DEFAULT = 3, PULL_BUFS_MAX = 8;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -1046,13 +1047,14 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 // at once -- instead of one CTA streaming a whole 64 MB slice from one peer.
 // Indices past the end of a shorter slice are skipped.
 struct PullCursor {
+  uint32_t chunk;  // bytes per chunk
   uint64_t g;  // global chunk index
   int it;      // slice of g (n = done)
   uint64_t off;
   __device__ void seek(const PullItem* items, int n, uint64_t total) {
     while (g < total) {
       const int i = int(g % uint64_t(n));
-      const uint64_t o = (g / uint64_t(n)) * PULL_CHUNK;
+      const uint64_t o = (g / uint64_t(n)) * chunk;
       if (o < items[i].len) {
         it = i;
         off = o;
@@ -1069,18 +1071,18 @@ struct PullCursor {
 };
 
 __global__ void __launch_bounds__(32) tma_pull_kernel(const PullItem* __restrict__ items, int n,
-                                                      uint64_t total) {
-  extern __shared__ __align__(128) uint8_t pull_smem[];  // PULL_BUFS chunks (dynamic: > 48 KB)
-  __shared__ __align__(8) uint64_t bar[PULL_BUFS];
-  auto buf = [&](int b) { return pull_smem + size_t(b) * PULL_CHUNK; };
+                                                      uint64_t total, uint32_t chunk, int nbufs) {
+  extern __shared__ __align__(128) uint8_t pull_smem[];  // nbufs chunks (dynamic)
+  __shared__ __align__(8) uint64_t bar[PULL_BUFS_MAX];
+  auto buf = [&](int b) { return pull_smem + size_t(b) * chunk; };
   if (threadIdx.x != 0) return;
-  for (int b = 0; b < PULL_BUFS; ++b)
+  for (int b = 0; b < nbufs; ++b)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[b])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   uint32_t phase = 0;  // bit b: parity of buffer b's next completion
   auto load = [&](int b, const PullCursor& c) {
     const PullItem& w = items[c.it];
-    const uint32_t len = uint32_t(w.len - c.off < PULL_CHUNK ? w.len - c.off : PULL_CHUNK);
+    const uint32_t len = uint32_t(w.len - c.off < chunk ? w.len - c.off : chunk);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar[b])),
                  "r"(len)
                  : "memory");
@@ -1090,17 +1092,17 @@ __global__ void __launch_bounds__(32) tma_pull_kernel(const PullItem* __restrict
         "l"(static_cast<const uint8_t*>(w.src) + c.off), "r"(len), "r"(smem_addr(&bar[b]))
         : "memory");
   };
-  PullCursor prod{blockIdx.x, 0, 0};
+  PullCursor prod{chunk, blockIdx.x, 0, 0};
   prod.seek(items, n, total);
   PullCursor cons = prod;
   int issued = 0, done = 0;
-  while (issued < PULL_BUFS && prod.it < n) {  // prologue: fill the ring
+  while (issued < nbufs && prod.it < n) {  // prologue: fill the ring
     load(issued, prod);
     prod.advance(items, n, total);
     ++issued;
   }
   while (done < issued) {
-    const int b = done % PULL_BUFS;
+    const int b = done % nbufs;
     uint32_t ok = 0;
     do {
       asm volatile(
@@ -1112,7 +1114,7 @@ __global__ void __launch_bounds__(32) tma_pull_kernel(const PullItem* __restrict
     } while (!ok);
     phase ^= 1u << b;
     const PullItem& w = items[cons.it];
-    const uint32_t len = uint32_t(w.len - cons.off < PULL_CHUNK ? w.len - cons.off : PULL_CHUNK);
+    const uint32_t len = uint32_t(w.len - cons.off < chunk ? w.len - cons.off : chunk);
     // streamed into the receive buffer: evict-first so the 17-20 GB per layer
     // does not push the running GEMM's expert weights out of L2
     asm volatile(
@@ -1256,16 +1258,27 @@ void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
 }
 
 void launch_pull(const PullItem* items, int n, uint64_t max_len, int ctas, cudaStream_t st) {
-  const uint64_t total = (max_len + PULL_CHUNK - 1) / PULL_CHUNK * uint64_t(n);
+  // chunk size and ring depth: 16 KB x 3 by default; DWDP_PULL_CHUNK /
+  // DWDP_PULL_BUFS override them for experiments (the ring must stay small
+  // enough to co-reside with a grouped-GEMM CTA)
+  static int chunk = 0, bufs = 0;
   static bool attr_set[64] = {false};
+  if (chunk == 0) {
+    const char* c = std::getenv("DWDP_PULL_CHUNK");
+    const char* b = std::getenv("DWDP_PULL_BUFS");
+    chunk = c ? std::max(1024, std::min(65536, std::atoi(c))) / 16 * 16 : PULL_CHUNK_DEFAULT;
+    bufs = b ? std::max(1, std::min(PULL_BUFS_MAX, std::atoi(b))) : PULL_BUFS_DEFAULT;
+  }
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev]) {
     cudaFuncSetAttribute(tma_pull_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         PULL_BUFS * PULL_CHUNK);
+                         PULL_BUFS_MAX * 65536 > 200 * 1024 ? 200 * 1024 : PULL_BUFS_MAX * 65536);
     attr_set[dev] = true;
   }
-  if (n > 0) tma_pull_kernel<<<ctas, 32, PULL_BUFS * PULL_CHUNK, st>>>(items, n, total);
+  const uint64_t total = (max_len + chunk - 1) / chunk * uint64_t(n);
+  if (n > 0)
+    tma_pull_kernel<<<ctas, 32, size_t(bufs) * chunk, st>>>(items, n, total, uint32_t(chunk), bufs);
 }
 
 }  // namespace dwdp
