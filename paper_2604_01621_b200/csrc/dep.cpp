@@ -177,7 +177,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   int np = 0;
   if (T > 0 && fp8_)
     np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_,
-                   nullptr, scratch_, st, x8, xs_);
+                   nullptr, scratch_, st, x8, xs_, row_align_);
   else if (T > 0)
     np = launch_permute(idx_, x, T, E_, k_, h_, 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_, xperm_, scratch_, st,
                    nullptr, nullptr, row_align_);
@@ -284,7 +284,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   if (nblocks > 0 && fp8_) {
     const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_i8(x8 + send_total * h_, T, h_, 128) : tm_dep_x8_;
     GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1, dep_seg_,
-                nullptr, dep_xs_, sarena_[0], sarena_[1]};
+                nullptr, dep_xs_, sarena_[0], sarena_[1], gemm_pair_ ? 1 : 0, raster_};
     launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_dep_x8_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
     launch_quant_rows_fp8(dep_h_, dep_cap_rows_, f_, dmeta, dep_h8_, dep_hs_, st);
   } else if (nblocks > 0) {
@@ -296,8 +296,9 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   mark(&rec.k[2]);
   if (nblocks > 0 && fp8_) {
     GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
-                nullptr, dep_hs_, sarena_[2], nullptr};
-    launch_grouped_gemm(GEMM_PLAIN_FP8, tm_dep_h8_, tm_dep_h8_, tm_down_, tm_down_, g2, int(nblocks * (h_ / 256)), st);
+                nullptr, dep_hs_, sarena_[2], nullptr, gemm_pair_ ? 1 : 0, raster_};
+    const CUtensorMap& tmd8 = gemm_pair_ ? tm_down_p_ : tm_down_;
+    launch_grouped_gemm(GEMM_PLAIN_FP8, tm_dep_h8_, tm_dep_h8_, tmd8, tmd8, g2, int(nblocks * (h_ / 256)), st);
   } else if (nblocks > 0) {
     GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
                 nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_};

@@ -500,9 +500,21 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
       "h"(uint16_t(3))
       : "memory");
 }
-// bf16 x bf16 -> fp32, M = 256 (pair), N = 256, both operands K-major.
-constexpr uint32_t kPairIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
-                                (uint32_t(256 >> 4) << 24);
+// M = 256 (pair), N = 256, both operands K-major: bf16 x bf16 -> fp32 or
+// e4m3 x e4m3 -> fp32 (a/b_format 0).
+template <bool FP8>
+__host__ __device__ constexpr uint32_t pair_idesc() {
+  return (1u << 4) | (FP8 ? 0u : (1u << 7) | (1u << 10)) | (uint32_t(BN >> 3) << 17) |
+         (uint32_t(256 >> 4) << 24);
+}
+__device__ __forceinline__ void tc_mma_pair_f8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc_v, uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc_v), "r"(accum));
+}
 
 // Pair tile id -> (pair index, n-block); segments in m-blocks are even.
 __device__ __forceinline__ void pair_coords(int tile, int nb_count, const int2* __restrict__ seg,
@@ -526,8 +538,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                              const __grid_constant__ CUtensorMap tmA2,
                              const __grid_constant__ CUtensorMap tmB0,
                              const __grid_constant__ CUtensorMap tmB1, GemmArgs p) {
-  static_assert(MODE == kSwiGLU || MODE == kPlain, "pair kernel: bf16 modes only");
-  constexpr bool SWIGLU = MODE == kSwiGLU;
+  static_assert(MODE != kInt8, "pair kernel: expert GEMM modes only");
+  constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8;
+  constexpr bool FP8 = MODE == kSwiGLU8 || MODE == kPlain8;
+  constexpr int BKE = FP8 ? 128 : 64;  // K elements per 128-byte smem row
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -572,7 +586,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const int routed_mb = p.meta[1];
   const int nb_count = SWIGLU ? p.n_out / 128 : (p.n_out + BN - 1) / BN;
   const int num_tiles = (total_mb >> 1) * nb_count;
-  const int kb_count = p.K / BK;
+  const int kb_count = p.K / BKE;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
   if (warp == 0) {
@@ -599,8 +613,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           // leader's arrival is pending); a remote arrive from the peer would
           // put a cluster-scope release fence in front of every load.
           if (rank == 0) mbar_expect_tx(&full[st], 2 * P_STAGE);
-          tma_load_2d_pair(sA(st), am, bar, kb * BK, arow);
-          tma_load_2d_pair(sB(st), bm, bar, kb * BK, brow);
+          tma_load_2d_pair(sA(st), am, bar, kb * BKE, arow);
+          tma_load_2d_pair(sB(st), bm, bar, kb * BKE, brow);
           if (++st == P_STAGES) {
             st = 0;
             ph ^= 1;
@@ -625,7 +639,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           const uint64_t ad = sw128_desc(smem_u32(sA(st)));
           const uint64_t bd = sw128_desc(smem_u32(sB(st)));
 #pragma unroll
-          for (int k = 0; k < 4; ++k) tc_mma_pair(d, ad + 2 * k, bd + 2 * k, kPairIdesc, (kb | k) != 0);
+          for (int k = 0; k < 4; ++k) {  // +32 B along K per MMA (16 bf16 or 32 e4m3)
+            if (FP8)
+              tc_mma_pair_f8(d, ad + 2 * k, bd + 2 * k, pair_idesc<true>(), (kb | k) != 0);
+            else
+              tc_mma_pair(d, ad + 2 * k, bd + 2 * k, pair_idesc<false>(), (kb | k) != 0);
+          }
           tc_commit_pair(&empty[st]);
           if (++st == P_STAGES) {
             st = 0;
@@ -737,6 +756,10 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
       cudaFuncSetAttribute(grouped_gemm_pair_kernel<kPlain>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
+      cudaFuncSetAttribute(grouped_gemm_pair_kernel<kSwiGLU8>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
+      cudaFuncSetAttribute(grouped_gemm_pair_kernel<kPlain8>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
       {
         cudaLaunchConfig_t lc = {};
         cudaLaunchAttribute at[1];
@@ -762,14 +785,18 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
     }
   }
   if (max_tiles <= 0) return;
-  if (args.pair && (mode == kSwiGLU || mode == kPlain)) {
+  if (args.pair && mode != kInt8) {
     const int cap = 2 * pair_clusters[dev];
     int g = max_tiles < cap ? max_tiles : cap;
     g = g < 2 ? 2 : (g & ~1);  // whole clusters of two, all co-resident (persistent)
     if (mode == kSwiGLU)
       grouped_gemm_pair_kernel<kSwiGLU><<<g, 256, P_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
-    else
+    else if (mode == kPlain)
       grouped_gemm_pair_kernel<kPlain><<<g, 256, P_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+    else if (mode == kSwiGLU8)
+      grouped_gemm_pair_kernel<kSwiGLU8><<<g, 256, P_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+    else
+      grouped_gemm_pair_kernel<kPlain8><<<g, 256, P_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
     return;
   }
   const int grid = max_tiles < sms[dev] ? max_tiles : sms[dev];

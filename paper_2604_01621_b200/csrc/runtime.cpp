@@ -65,7 +65,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   // needs 256-row expert segments; DWDP_GEMM_PAIR=0 selects the 1-SM kernel.
   {
     const char* env = std::getenv("DWDP_GEMM_PAIR");
-    gemm_pair_ = !fp8_ && !(env && env[0] == '0');
+    gemm_pair_ = !(env && env[0] == '0');
     row_align_ = gemm_pair_ ? 256 : 128;
     const char* r = std::getenv("DWDP_RASTER");  // experiments: m / n (default auto)
     raster_ = r ? (r[0] == 'm' ? 1 : r[0] == 'n' ? 2 : 0) : 0;
@@ -625,17 +625,18 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     // bf16 H, which is re-quantised per row for GEMM2.
     uint8_t* x8 = reinterpret_cast<uint8_t*>(xperm_);
     const int np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_,
-                                  nullptr, meta_, nullptr, scratch_, st, x8, xs_);
+                                  nullptr, meta_, nullptr, scratch_, st, x8, xs_, row_align_);
     mark(1);
     GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 0, mbseg_,
-                nullptr, xs_, sarena_[0], sarena_[1]};
+                nullptr, xs_, sarena_[0], sarena_[1], gemm_pair_ ? 1 : 0, raster_};
     launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_x8_, tm_x8_, tm_gate_, tm_up_, g1,
                         int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
     launch_quant_rows_fp8(hbuf_, max_rows_, f_, meta_, h8_, hs_, st);
     mark(2);
     GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
-                nullptr, hs_, sarena_[2], nullptr};
-    launch_grouped_gemm(GEMM_PLAIN_FP8, tm_h8_, tm_h8_, tm_down_, tm_down_, g2,
+                nullptr, hs_, sarena_[2], nullptr, gemm_pair_ ? 1 : 0, raster_};
+    const CUtensorMap& tmd8 = gemm_pair_ ? tm_down_p_ : tm_down_;
+    launch_grouped_gemm(GEMM_PLAIN_FP8, tm_h8_, tm_h8_, tmd8, tmd8, g2,
                         int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
     mark(3);
     launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);

@@ -327,10 +327,11 @@ def test_prefetch_handles(dev):
         c.close()
 
 
-def test_gemm_pair_matches_single_cta(dev, monkeypatch):
-    """The CTA-pair GEMM path (cta_group::2, 256-row segments, the default for
-    bf16) and the 1-SM path give the same layer outputs."""
-    cfg = CONFIGS["mid_sigmoid"]
+@pytest.mark.parametrize("name", ["mid_sigmoid", "mid_fp8"])
+def test_gemm_pair_matches_single_cta(dev, monkeypatch, name):
+    """The CTA-pair GEMM path (cta_group::2, 256-row segments, the default)
+    and the 1-SM path give the same layer outputs (bf16 and e4m3 weights)."""
+    cfg = CONFIGS.get(name) or FP8_CONFIGS[name]
     outs = []
     for pair in ("1", "0"):
         monkeypatch.setenv("DWDP_GEMM_PAIR", pair)
