@@ -37,10 +37,10 @@ namespace {
 constexpr int BM = 128;
 constexpr int BN = 256;  // accumulator columns per tile
 constexpr int BK = 64;   // 128 B of bf16 = one SWIZZLE_128B atom row
-// 3 stages (145 KB): the 1-SM kernel (router int8 GEMM, fp8 expert GEMMs) must
-// also fit beside a 49 KB prefetch pull CTA, or it queues behind the whole pull
-// (measured: the router GEMM waited 24 ms per layer with 4 stages at N = 4).
-constexpr int STAGES = 3;
+// 4 stages (194 KB): the 1-SM kernel (router int8 GEMM) must also fit beside a
+// 26 KB prefetch pull CTA, or it queues behind the whole pull (measured: the
+// router GEMM waited 24 ms per layer next to a 49 KB pull CTA at N = 4).
+constexpr int STAGES = 4;
 constexpr int A_STAGE = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE = BN * BK * 2;  // 32 KB
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
@@ -451,9 +451,10 @@ __global__ void __launch_bounds__(256, 1)
 // segments padded to 256 rows (permute row_align 256), so both m-blocks of a
 // pair always belong to the same expert.
 constexpr int P_STAGE = 2 * BM * BK * 2;  // A (16 KB) + half of B (16 KB) per CTA
-// 5 stages (162 KB) leave room on every SM for one prefetch pull CTA (49 KB):
-// with 7 the pull kernel could not co-reside and DWDP at N=4 fell 10-20%.
-constexpr int P_STAGES = 5;
+// 6 stages (194 KB) leave room on every SM for one prefetch pull CTA (26 KB):
+// with 7 the pull kernel could not co-reside and DWDP at N=4 fell 10-20%;
+// with 5 GEMM2's tensor pipe dropped from 94% to 86% active.
+constexpr int P_STAGES = 6;
 constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE + 1024 + 256;
 
 __device__ __forceinline__ uint32_t cluster_rank() {

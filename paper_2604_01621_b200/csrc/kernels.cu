@@ -1030,11 +1030,11 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
 // NVLink into a shared-memory ring (cp.async.bulk global->shared, mbarrier
 // completion) and out to the local receive buffer (cp.async.bulk
 // shared->global, bulk-group completion).
-// 3 x 16 KB ring (49 KB with the barriers): fits next to a 162 KB grouped-GEMM
+// 3 x 8 KB ring (26 KB with the barriers): fits next to a 194 KB grouped-GEMM
 // CTA on every SM (228 KB per SM, 1 KB reserved per CTA), so the pull runs
-// concurrently with the expert GEMMs instead of queueing behind them. 48 KB
-// in flight per SM: the all-to-all pull is latency x bytes-in-flight bound.
-constexpr int PULL_CHUNK_DEFAULT = 16384, PULL_BUFS_DEFAULT = 3, PULL_BUFS_MAX = 8;
+// concurrently with the expert GEMMs instead of queueing behind them. The
+// achieved GB/s was flat over 4-32 KB chunks x 2-8 buffers (the fabric sets it).
+constexpr int PULL_CHUNK_DEFAULT = 8192, PULL_BUFS_DEFAULT = 3, PULL_BUFS_MAX = 8;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -1258,7 +1258,7 @@ void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
 }
 
 void launch_pull(const PullItem* items, int n, uint64_t max_len, int ctas, cudaStream_t st) {
-  // chunk size and ring depth: 16 KB x 3 by default; DWDP_PULL_CHUNK /
+  // chunk size and ring depth: 8 KB x 3 by default; DWDP_PULL_CHUNK /
   // DWDP_PULL_BUFS override them for experiments (the ring must stay small
   // enough to co-reside with a grouped-GEMM CTA)
   static int chunk = 0, bufs = 0;
