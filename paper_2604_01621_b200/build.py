@@ -21,7 +21,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 
 CU = ["kernels.cu", "gemm_sm100.cu"]
 CPP = ["plan.cpp", "report.cpp", "runtime.cpp", "dep.cpp", "capi.cpp"]
-HEADERS = ["kernels.hpp", "gemm_sm100.hpp", "plan.hpp", "runtime.hpp"]
+HEADERS = ["kernels.hpp", "gemm_sm100.hpp", "plan.hpp", "runtime.hpp", "report.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -94,12 +94,6 @@ __device__ __forceinline__ uint8_t f32_to_e4m3(float x) {
   return uint8_t(s | code);
 }
 
-__device__ __forceinline__ float e4m3_to_f32(uint32_t b) {
-  const uint32_t e = (b >> 3) & 0xf, m = b & 7;
-  const float v = e ? __uint_as_float(((e + 120) << 23) | (m << 20)) : float(m) * 0.001953125f;
-  return (b & 0x80) ? -v : v;
-}
-
 // Quantised synthetic expert weights: one warp per (slot, row); the row's
 // bf16 values come from the same counter hash as the bf16 init; scale =
 // absmax / 448 (1 if the row is zero), q = e4m3(v / scale).
@@ -397,8 +391,6 @@ __global__ void __launch_bounds__(256) topk_kernel(const int32_t* __restrict__ C
   }
   // top-k over ch, ties to the lower index
   int sel[TOPK_MAXK];
-  uint32_t taken[TOPK_MAXV / 32 + 1] = {0};
-  (void)taken;
   uint32_t taken_mask = 0;  // bit v of this lane's slots
   for (int j = 0; j < c.k; ++j) {
     float bv = NEG;
