@@ -490,6 +490,17 @@ def main():
                           900e9),
                 D.build_placement(R1["E"], world), int(mean_t))
             acct["analytic_compare"]["tokens_per_rank"] = mean_t
+            # the same model calibrated with this run's
+            # measured rates (grouped-GEMM TFLOP/s, in-step prefetch GB/s) beside
+            # the measured DWDP/DEP ratio
+            gemm_tf = (g1_flops + g2_flops) / ((g1_ns + g2_ns) * 1e-9) if (g1_ns + g2_ns) else p_peak
+            link = pf_bytes / pf_ns * 1e9 if pf_ns else 900e9
+            cal = D.analytic_compare(D.r1_model(layers, 1.0 if fp8 else 2.0),
+                                     D.GpuSpec(gemm_tf, pk["hbm_gbs"] * 1e9, link),
+                                     D.build_placement(R1["E"], world), int(mean_t))
+            cal.update(gemm_tflops_measured=gemm_tf / 1e12, prefetch_gbs_measured=link / 1e9,
+                       measured_dwdp_over_dep=(dep or {}).get("dwdp_over_dep"))
+            acct["analytic_compare_calibrated"] = cal
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
