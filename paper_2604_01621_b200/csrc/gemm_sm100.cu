@@ -503,10 +503,19 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
 }
 // M = 256 (pair), N = 256, both operands K-major: bf16 x bf16 -> fp32 or
 // e4m3 x e4m3 -> fp32 (a/b_format 0).
-template <bool FP8>
+template <int MODE>
 __host__ __device__ constexpr uint32_t pair_idesc() {
-  return (1u << 4) | (FP8 ? 0u : (1u << 7) | (1u << 10)) | (uint32_t(BN >> 3) << 17) |
-         (uint32_t(256 >> 4) << 24);
+  return (MODE == kInt8 ? (2u << 4) : (1u << 4)) |
+         (MODE == kSwiGLU8 || MODE == kPlain8 ? 0u : (1u << 7) | (1u << 10)) |
+         (uint32_t(BN >> 3) << 17) | (uint32_t(256 >> 4) << 24);
+}
+__device__ __forceinline__ void tc_mma_pair_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc_v, uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc_v), "r"(accum));
 }
 __device__ __forceinline__ void tc_mma_pair_f8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                                uint32_t idesc_v, uint32_t accum) {
@@ -539,10 +548,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                              const __grid_constant__ CUtensorMap tmA2,
                              const __grid_constant__ CUtensorMap tmB0,
                              const __grid_constant__ CUtensorMap tmB1, GemmArgs p) {
-  static_assert(MODE != kInt8, "pair kernel: expert GEMM modes only");
   constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8;
   constexpr bool FP8 = MODE == kSwiGLU8 || MODE == kPlain8;
-  constexpr int BKE = FP8 ? 128 : 64;  // K elements per 128-byte smem row
+  constexpr int BKE = (FP8 || MODE == kInt8) ? 128 : 64;  // K elements per 128-byte smem row
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -641,10 +649,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           const uint64_t bd = sw128_desc(smem_u32(sB(st)));
 #pragma unroll
           for (int k = 0; k < 4; ++k) {  // +32 B along K per MMA (16 bf16 or 32 e4m3)
-            if (FP8)
-              tc_mma_pair_f8(d, ad + 2 * k, bd + 2 * k, pair_idesc<true>(), (kb | k) != 0);
+            if (MODE == kInt8)
+              tc_mma_pair_i8(d, ad + 2 * k, bd + 2 * k, pair_idesc<MODE>(), (kb | k) != 0);
+            else if (FP8)
+              tc_mma_pair_f8(d, ad + 2 * k, bd + 2 * k, pair_idesc<MODE>(), (kb | k) != 0);
             else
-              tc_mma_pair(d, ad + 2 * k, bd + 2 * k, pair_idesc<false>(), (kb | k) != 0);
+              tc_mma_pair(d, ad + 2 * k, bd + 2 * k, pair_idesc<MODE>(), (kb | k) != 0);
           }
           tc_commit_pair(&empty[st]);
           if (++st == P_STAGES) {
@@ -761,6 +771,8 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
       cudaFuncSetAttribute(grouped_gemm_pair_kernel<kPlain8>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
+      cudaFuncSetAttribute(grouped_gemm_pair_kernel<kInt8>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
       {
         cudaLaunchConfig_t lc = {};
         cudaLaunchAttribute at[1];
@@ -786,7 +798,7 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
     }
   }
   if (max_tiles <= 0) return;
-  if (args.pair && mode != kInt8) {
+  if (args.pair) {
     const int cap = 2 * pair_clusters[dev];
     int g = max_tiles < cap ? max_tiles : cap;
     g = g < 2 ? 2 : (g & ~1);  // whole clusters of two, all co-resident (persistent)
@@ -796,8 +808,10 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
       grouped_gemm_pair_kernel<kPlain><<<g, 256, P_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
     else if (mode == kSwiGLU8)
       grouped_gemm_pair_kernel<kSwiGLU8><<<g, 256, P_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
-    else
+    else if (mode == kPlain8)
       grouped_gemm_pair_kernel<kPlain8><<<g, 256, P_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+    else
+      grouped_gemm_pair_kernel<kInt8><<<g, 256, P_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
     return;
   }
   const int grid = max_tiles < sms[dev] ? max_tiles : sms[dev];

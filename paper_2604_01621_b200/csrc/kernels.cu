@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(256) router_quant_kernel(const uint16_t* __res
                                                            int32_t* __restrict__ emax,
                                                            int32_t* __restrict__ meta, int staged) {
   if (meta && blockIdx.x == 0 && threadIdx.x == 0) {
-    const int mb = int((3 * R + 127) / 128);
+    const int mb = int((3 * R + 255) / 256) * 2;  // even: whole CTA-pair tiles (rows >= 3R not stored)
     meta[0] = mb;
     meta[1] = mb;
     meta[2] = 0;

@@ -142,8 +142,10 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   hbuf_ = static_cast<uint16_t*>(dalloc(size_t(max_rows_) * f_ * 2, &workspace_bytes));
   router_wq_ = static_cast<int8_t*>(dalloc(size_t(WL_) * 3 * E_ * h_, &weight_bytes));
   router_we_ = static_cast<int32_t*>(dalloc(size_t(WL_) * E_ * 4, &weight_bytes));
-  for (int wl = 0; wl < WL_; ++wl)
+  for (int wl = 0; wl < WL_; ++wl) {
     tm_rw_.push_back(make_tmap_i8(router_wq_ + size_t(wl) * 3 * E_ * h_, 3 * int64_t(E_), h_, 256));
+    tm_rw_p_.push_back(make_tmap_i8(router_wq_ + size_t(wl) * 3 * E_ * h_, 3 * int64_t(E_), h_, 128));
+  }
   xq_ = static_cast<int8_t*>(dalloc(size_t(max_tokens_) * 3 * h_, &workspace_bytes));
   xe_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * 4, &workspace_bytes));
   rC_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * 9 * E_ * 4, &workspace_bytes));
@@ -594,10 +596,11 @@ void Ctx::route_logits(int wl, const uint16_t* x, int64_t T, cudaStream_t st) {
   launch_router_quant(x, T, h_, xq_, xe_, rmeta_, st);
   const CUtensorMap tx = make_tmap_i8(xq_, 3 * T, h_, 128);
   GemmArgs ga{int(h_), 3 * E_, 0, -1, zeros_, zeros_, rmeta_,
-              reinterpret_cast<uint16_t*>(rC_), 3 * int64_t(E_), 3 * T, 0, nullptr};
+              reinterpret_cast<uint16_t*>(rC_), 3 * int64_t(E_), 3 * T, 0, nullptr,
+              nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, 0};
   const int64_t tiles = (3 * T + 127) / 128 * ((3 * E_ + 255) / 256);
-  launch_grouped_gemm(GEMM_INT8, tx, tx, tm_rw_[size_t(wl)], tm_rw_[size_t(wl)], ga,
-                      int(std::min<int64_t>(tiles, 1 << 30)), st);
+  const CUtensorMap& tb = gemm_pair_ ? tm_rw_p_[size_t(wl)] : tm_rw_[size_t(wl)];
+  launch_grouped_gemm(GEMM_INT8, tx, tx, tb, tb, ga, int(std::min<int64_t>(tiles, 1 << 30)), st);
   RouterCfg rc{E_, k_, cfg.scoring, cfg.n_group, cfg.topk_group, cfg.norm_topk, cfg.routed_scale};
   launch_topk(rC_, xe_, router_we_ + size_t(wl) * E_, bias_ + size_t(wl) * E_, logits_, idx_, wts_,
               T, rc, st);
