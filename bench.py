@@ -180,6 +180,9 @@ def main():
     ap.add_argument("--decode", type=int, default=0,
                     help="decode phase (config 5): B tokens/rank every step instead of prefill batches")
     ap.add_argument("--trace", default="", help="write a chrome trace of the timed DWDP steps here")
+    ap.add_argument("--oversubscribe", action="store_true",
+                    help="code-path test: WORLD_SIZE > GPUs (ranks share GPUs, gloo, no DEP); "
+                         "numbers from such a run are not bench values")
     ap.add_argument("--zipf", type=float, default=0.0,
                     help="expert-routing skew s: router bias -ZIPF_BETA*s*ln(e+1)")
     args = ap.parse_args()
@@ -195,21 +198,31 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    if args.oversubscribe:  # code-path test only: several ranks per GPU, gloo plumbing, no DEP
+        local = local % torch.cuda.device_count()
+        args.no_dep = True
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.oversubscribe:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def allmax(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        t = torch.tensor([v], device="cpu" if args.oversubscribe else dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if args.oversubscribe:
+                torch.cuda.synchronize()
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
 
     layers = 1 if args.profile else args.layers
     model = D.r1_model(layers)
