@@ -51,6 +51,7 @@ def oracle_cfg(c: D.DwdpConfig):
 CONFIGS = {
     "tiny": D.DwdpConfig.tiny(),  # BASELINE config 1 layer (softmax top-2, E16, h512)
     "tiny_shared": D.DwdpConfig.tiny(shared_ffn=1024),
+    # T = 2000: ~190 rows per expert, so expert segments span a full CTA pair
     "mid_sigmoid": D.DwdpConfig(num_layers=1, num_experts=64, hidden=1024, ffn=256, shared_ffn=256,
                                 top_k=6, n_group=8, topk_group=4, max_tokens=2048),
     "r1": D.DwdpConfig(num_layers=1, max_tokens=512),  # BASELINE config 2 shapes
@@ -131,7 +132,8 @@ def test_route_bit_exact(dev, ctxs, orc, name, T):
 # ---------------------------------------------------------------- layer forward
 
 @pytest.mark.parametrize("name,T", [("tiny", 1), ("tiny", 64), ("tiny", 1000), ("tiny_shared", 129),
-                                    ("mid_sigmoid", 200), ("r1", 16)])
+                                    ("mid_sigmoid", 200), ("mid_sigmoid", 2000),
+                                    ("r1", 16), ("r1", 300)])
 def test_moe_forward_vs_oracle(dev, ctxs, orc, name, T):
     cfg = CONFIGS[name]
     ctx = ctxs[name]
@@ -192,7 +194,7 @@ def test_fp8_weights_bit_exact(dev, ctxs8, orc, name):
 
 
 @pytest.mark.parametrize("name,T", [("tiny_fp8", 1), ("tiny_fp8", 300), ("mid_fp8", 200),
-                                    ("mid_fp8", 1), ("r1_fp8", 16)])
+                                    ("mid_fp8", 1), ("mid_fp8", 2000), ("r1_fp8", 16)])
 def test_moe_forward_fp8_vs_oracle(dev, ctxs8, orc, name, T):
     cfg = FP8_CONFIGS[name]
     x = make_x(T, cfg.hidden, 11 + T, dev)
@@ -374,5 +376,27 @@ def test_dwdp_non_divisible_and_redundant_placements(dev, group, extra, engine):
         assert recs[1]["prefetch_bytes"] == fetched * 3 * MID["hidden"] * MID["ffn"] * 2
         for e, src in plan.fetch_lists[r][:3]:
             assert (ranks[r].read_expert(3 % 3, e, 0) == ranks[src].read_expert(3 % 3, e, 0)).all()
+    for c in ranks + [full]:
+        c.close()
+
+
+@pytest.mark.parametrize("engine", [D.ENGINE_COPY, D.ENGINE_PULL])
+def test_dwdp_large_batch_bitwise(dev, engine):
+    """DWDP at ~180-350 rows per expert (segments spanning CTA pairs, several
+    permute chunks) stays bit-identical to the all-local model."""
+    kw = dict(MID, max_tokens=4096)
+    full = D.DwdpContext(D.DwdpConfig(**kw))
+    full.init_weights()
+    ranks = [D.DwdpContext(D.DwdpConfig(**kw, rank=r, group_size=2, engine=engine)) for r in range(2)]
+    for c in ranks:
+        c.init_weights()
+    D.DwdpContext.link_local(ranks)
+    xs = [make_x(1900 + 1800 * r, MID["hidden"], 300 + r, dev) for r in range(2)]
+    for g in range(3):
+        for r in range(2):
+            y = ranks[r].layer_forward(g, xs[r], residual=False)
+            yf = full.moe_forward(g % 3, xs[r])
+            torch.cuda.synchronize()
+            assert torch.equal(y, yf), (engine, g, r)
     for c in ranks + [full]:
         c.close()
