@@ -109,6 +109,8 @@ void Ctx::dep_init(const void* unique_id) {
   DWDP_CUDA(cudaHostAlloc(&dep_tab_host_, size_t(dep_tab_cap_) * 4, 0));
   dep_seg_ = static_cast<int2*>(dalloc(size_t(dep_tab_cap_) * sizeof(int2), &workspace_bytes));
   DWDP_CUDA(cudaHostAlloc(&dep_seg_host_, size_t(dep_tab_cap_) * sizeof(int2), 0));
+  dep_mbrows_ = static_cast<int32_t*>(dalloc(size_t(dep_tab_cap_) * 4, &workspace_bytes));
+  DWDP_CUDA(cudaHostAlloc(&dep_mbrows_host_, size_t(dep_tab_cap_) * 4, 0));
   dep_reserve(max_rows_);
 }
 
@@ -138,11 +140,15 @@ void Ctx::dep_reserve(int64_t rows) {
     cudaFreeHost(dep_tab_host_);
     cudaFree(dep_seg_);
     cudaFreeHost(dep_seg_host_);
+    cudaFree(dep_mbrows_);
+    cudaFreeHost(dep_mbrows_host_);
     dep_tab_cap_ = need_tab;
     dep_tab_ = static_cast<int32_t*>(dalloc(size_t(dep_tab_cap_) * 4, nullptr));
     DWDP_CUDA(cudaHostAlloc(&dep_tab_host_, size_t(dep_tab_cap_) * 4, 0));
     dep_seg_ = static_cast<int2*>(dalloc(size_t(dep_tab_cap_) * sizeof(int2), nullptr));
     DWDP_CUDA(cudaHostAlloc(&dep_seg_host_, size_t(dep_tab_cap_) * sizeof(int2), 0));
+    dep_mbrows_ = static_cast<int32_t*>(dalloc(size_t(dep_tab_cap_) * 4, nullptr));
+    DWDP_CUDA(cudaHostAlloc(&dep_mbrows_host_, size_t(dep_tab_cap_) * 4, 0));
   }
 }
 
@@ -177,7 +183,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   int np = 0;
   if (T > 0 && fp8_)
     np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_,
-                   nullptr, scratch_, st, x8, xs_, row_align_);
+                   nullptr, scratch_, st, x8, xs_, row_align_);  // send side: padding unused
   else if (T > 0)
     np = launch_permute(idx_, x, T, E_, k_, h_, 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_, xperm_, scratch_, st,
                    nullptr, nullptr, row_align_);
@@ -219,9 +225,11 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   // (each (source, expert) run of m-blocks is one raster segment)
   for (int s = 0; s < N_; ++s)
     for (int e = rank_ * per; e < (rank_ + 1) * per; ++e) {
-      const int2 seg = make_int2(int(nblocks), int(padr(ca[size_t(s) * E_ + e]) / 128));
+      const int32_t cnt = ca[size_t(s) * E_ + e];
+      const int2 seg = make_int2(int(nblocks), int(padr(cnt) / 128));
       for (int b = 0; b < seg.y; ++b) {
         dep_seg_host_[nblocks] = seg;
+        dep_mbrows_host_[nblocks] = std::max(0, std::min(128, cnt - 128 * b));
         dep_tab_host_[4 + nblocks++] = e;
       }
     }
@@ -229,6 +237,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   const int2 sseg = make_int2(int(routed_mb), int(shared_blocks));
   for (int64_t b = 0; b < shared_blocks; ++b) {
     dep_seg_host_[nblocks] = sseg;
+    dep_mbrows_host_[nblocks] = int32_t(std::max<int64_t>(0, std::min<int64_t>(128, T - 128 * b)));
     dep_tab_host_[4 + nblocks++] = E_;
   }
   dep_tab_host_[0] = int32_t(nblocks);
@@ -238,6 +247,8 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   DWDP_CUDA(cudaMemcpyAsync(dep_tab_, dep_tab_host_, size_t(4 + nblocks) * 4,
                             cudaMemcpyHostToDevice, st));
   DWDP_CUDA(cudaMemcpyAsync(dep_seg_, dep_seg_host_, size_t(nblocks + 1) * sizeof(int2),
+                            cudaMemcpyHostToDevice, st));
+  DWDP_CUDA(cudaMemcpyAsync(dep_mbrows_, dep_mbrows_host_, size_t(nblocks + 1) * 4,
                             cudaMemcpyHostToDevice, st));
   // 3. dispatch all-to-all (bf16 rows, or e4m3 rows + their fp32 scales)
   const size_t rowel = size_t(h_);
@@ -284,24 +295,24 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   if (nblocks > 0 && fp8_) {
     const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_i8(x8 + send_total * h_, T, h_, 128) : tm_dep_x8_;
     GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1, dep_seg_,
-                nullptr, dep_xs_, sarena_[0], sarena_[1], gemm_pair_ ? 1 : 0, raster_};
+                nullptr, dep_xs_, sarena_[0], sarena_[1], gemm_pair_ ? 1 : 0, raster_, dep_mbrows_};
     launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_dep_x8_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
     launch_quant_rows_fp8(dep_h_, dep_cap_rows_, f_, dmeta, dep_h8_, dep_hs_, st);
   } else if (nblocks > 0) {
     const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_dep_recv_;
     GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1, dep_seg_,
-                nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_};
+                nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_, dep_mbrows_};
     launch_grouped_gemm(GEMM_SWIGLU, tm_dep_recv_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
   }
   mark(&rec.k[2]);
   if (nblocks > 0 && fp8_) {
     GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
-                nullptr, dep_hs_, sarena_[2], nullptr, gemm_pair_ ? 1 : 0, raster_};
+                nullptr, dep_hs_, sarena_[2], nullptr, gemm_pair_ ? 1 : 0, raster_, dep_mbrows_};
     const CUtensorMap& tmd8 = gemm_pair_ ? tm_down_p_ : tm_down_;
     launch_grouped_gemm(GEMM_PLAIN_FP8, tm_dep_h8_, tm_dep_h8_, tmd8, tmd8, g2, int(nblocks * (h_ / 256)), st);
   } else if (nblocks > 0) {
     GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
-                nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_};
+                nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_, dep_mbrows_};
     const CUtensorMap& tmd = gemm_pair_ ? tm_down_p_ : tm_down_;
     launch_grouped_gemm(GEMM_PLAIN, tm_dep_h_, tm_dep_h_, tmd, tmd, g2, int(nblocks * (h_ / 256)), st);
   }

@@ -202,7 +202,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
   constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8;
   constexpr bool FP8 = MODE == kSwiGLU8 || MODE == kPlain8;
   const int64_t row = int64_t(mb) * BM + q * 32 + lane;
-  const bool store = row < p.m_limit;
+  const bool store = row < p.m_limit && (p.mb_rows == nullptr || q * 32 + lane < p.mb_rows[mb]);
   // fp8: per-row activation scale x per-output-channel weight scale
   float sa = 1.0f;
   const float* sb0 = nullptr;

@@ -41,6 +41,9 @@ struct GemmArgs {
   // segment raster: 0 auto (n-block-major while the segment's A rows <= its
   // B rows), 1 always m-block-major, 2 always n-block-major (experiments)
   int raster;
+  // Optional [m-blocks] real rows of each m-block: the epilogue does not
+  // store the padding rows (decode batches are mostly padding).
+  const int32_t* mb_rows;
 };
 
 // 2-D bf16 TMA map over a row-major [rows][cols] matrix, box = 64 x box_rows,

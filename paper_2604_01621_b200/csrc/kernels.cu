@@ -749,7 +749,8 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
                                                             int32_t* __restrict__ mblock_expert,
                                                             int2* __restrict__ mb_seg,
                                                             int32_t* __restrict__ src_row,
-                                                            int32_t* __restrict__ meta) {
+                                                            int32_t* __restrict__ meta,
+                                                            int32_t* __restrict__ mb_rows) {
   extern __shared__ int32_t sh[];  // [E] padded sizes, then [E] offsets
   int32_t* pad = sh;
   int32_t* off = sh + E;
@@ -795,6 +796,10 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
     for (int32_t b = seg.x; b < seg.x + seg.y; ++b) {
       mblock_expert[b] = e;
       mb_seg[b] = seg;
+      if (mb_rows) {  // real (non-padding) rows of the m-block
+        const int32_t v = counts[e] - (b - seg.x) * MB_ROWS;
+        mb_rows[b] = v < 0 ? 0 : (v > MB_ROWS ? MB_ROWS : v);
+      }
     }
     if (src_row)  // padding rows gather token 0 (computed, never read)
       for (int32_t r = off[e] + counts[e]; r < off[e] + pad[e]; ++r) src_row[r] = 0;
@@ -805,6 +810,10 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
     for (int32_t b = threadIdx.x; b < seg.y; b += blockDim.x) {
       mblock_expert[rmb + b] = E;
       mb_seg[rmb + b] = seg;
+      if (mb_rows) {
+        const int64_t v = T - int64_t(b) * MB_ROWS;
+        mb_rows[rmb + b] = v < 0 ? 0 : (v > MB_ROWS ? MB_ROWS : int32_t(v));
+      }
     }
   }
 }
@@ -1201,7 +1210,7 @@ int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int 
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
                     int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
                     int32_t* scratch, cudaStream_t st, uint8_t* xperm8, float* xscale,
-                    int row_align) {
+                    int row_align, int32_t* mb_rows) {
   const int pch = permute_chunk(T);
   const int nch = int((T + pch - 1) / pch);
   int32_t* chunk_counts = scratch;
@@ -1210,7 +1219,7 @@ int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int 
     permute_count_kernel<<<nch, 256, E * sizeof(int32_t), st>>>(idx, T, E, k, pch, chunk_counts);
   permute_scan_kernel<<<1, 1024, 2 * E * sizeof(int32_t), st>>>(
       chunk_counts, nch, E, T, shared, row_align, counts, expert_off, mblock_expert, mb_seg, src_row,
-      meta);
+      meta, mb_rows);
   // bf16 rows: rank in the scatter kernel, replicate with the bulk-copy kernel
   const bool bulk = xperm != nullptr && xperm8 == nullptr && h % 8 == 0 &&
                     size_t(PB_BUFS) * size_t(h) * 2 <= 48 * 1024;

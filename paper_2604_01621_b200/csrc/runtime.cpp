@@ -134,6 +134,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   counts_ = static_cast<int32_t*>(dalloc(size_t(E_) * 4, &workspace_bytes));
   mblock_ = static_cast<int32_t*>(dalloc(size_t(max_mb_) * 4, &workspace_bytes));
   mbseg_ = static_cast<int2*>(dalloc(size_t(max_mb_) * sizeof(int2), &workspace_bytes));
+  mbrows_ = static_cast<int32_t*>(dalloc(size_t(max_mb_) * 4, &workspace_bytes));
   srcrow_ = static_cast<int32_t*>(dalloc(size_t(max_rows_) * 4, &workspace_bytes));
   meta_ = static_cast<int32_t*>(dalloc(16 * 4, &workspace_bytes));
   scratch_ = static_cast<int32_t*>(
@@ -199,11 +200,11 @@ Ctx::~Ctx() {
   nccl_destroy(nccl_);
   for (void* b : {static_cast<void*>(dep_recv_), static_cast<void*>(dep_h_),
                   static_cast<void*>(dep_counts_all_), static_cast<void*>(dep_tab_),
-                  static_cast<void*>(dep_seg_), static_cast<void*>(dep_h8_),
+                  static_cast<void*>(dep_mbrows_), static_cast<void*>(dep_h8_),
                   static_cast<void*>(dep_xs_), static_cast<void*>(dep_hs_)})
     if (b) cudaFree(b);
   if (dep_counts_host_) cudaFreeHost(dep_counts_host_);
-  if (dep_seg_host_) cudaFreeHost(dep_seg_host_);
+  if (dep_mbrows_host_) cudaFreeHost(dep_mbrows_host_);
   if (dep_tab_host_) cudaFreeHost(dep_tab_host_);
   for (auto& p : plans_) {
     if (p.start) cudaEventDestroy(p.start);
@@ -214,7 +215,7 @@ Ctx::~Ctx() {
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   void* bufs[] = {arena_[0], arena_[1], arena_[2], router_w_, bias_, slot_tab_, logits_, idx_,
                   wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_, pull_items_odd_,
-                  router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_, mbseg_, dep_seg_, srcrow_,
+                  router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_, mbseg_, mbrows_, dep_seg_, srcrow_,
                   sarena_[0], sarena_[1], sarena_[2], h8_, xs_, hs_};
   if (dep_seg_host_) cudaFreeHost(dep_seg_host_);
   for (void* b : bufs)
@@ -628,16 +629,16 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     // bf16 H, which is re-quantised per row for GEMM2.
     uint8_t* x8 = reinterpret_cast<uint8_t*>(xperm_);
     const int np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_,
-                                  nullptr, meta_, nullptr, scratch_, st, x8, xs_, row_align_);
+                                  nullptr, meta_, nullptr, scratch_, st, x8, xs_, row_align_, mbrows_);
     mark(1);
     GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 0, mbseg_,
-                nullptr, xs_, sarena_[0], sarena_[1], gemm_pair_ ? 1 : 0, raster_};
+                nullptr, xs_, sarena_[0], sarena_[1], gemm_pair_ ? 1 : 0, raster_, mbrows_};
     launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_x8_, tm_x8_, tm_gate_, tm_up_, g1,
                         int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
     launch_quant_rows_fp8(hbuf_, max_rows_, f_, meta_, h8_, hs_, st);
     mark(2);
     GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
-                nullptr, hs_, sarena_[2], nullptr, gemm_pair_ ? 1 : 0, raster_};
+                nullptr, hs_, sarena_[2], nullptr, gemm_pair_ ? 1 : 0, raster_, mbrows_};
     const CUtensorMap& tmd8 = gemm_pair_ ? tm_down_p_ : tm_down_;
     launch_grouped_gemm(GEMM_PLAIN_FP8, tm_h8_, tm_h8_, tmd8, tmd8, g2,
                         int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
@@ -646,7 +647,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     launches += 3 + np + 3 + 1;  // router 3, permute, GEMM1 + quant + GEMM2, combine
   } else {
   const int np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_,
-                                nullptr, meta_, xperm_, scratch_, st, nullptr, nullptr, row_align_);
+                                nullptr, meta_, xperm_, scratch_, st, nullptr, nullptr, row_align_, mbrows_);
   mark(1);
   const CUtensorMap tm_x = shared_ ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
   // Routed A rows come from the materialised expert-major copy. (GEMM1 can
@@ -654,11 +655,11 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   // B200 that measured 2.5x slower: 32 scattered 128-byte row fetches per
   // k-block defeat L2 reuse across the expert's 16 n-block tiles.)
   GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_,
-              nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_};
+              nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_, mbrows_};
   launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(2);
   GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
-              nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_};
+              nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_, mbrows_};
   const CUtensorMap& tmd = gemm_pair_ ? tm_down_p_ : tm_down_;
   launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tmd, tmd, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
   mark(3);

@@ -156,6 +156,7 @@ class Ctx {
           *meta_ = nullptr, *scratch_ = nullptr;
   float* wts_ = nullptr;
   int2* mbseg_ = nullptr;               // [max_mb] expert segment of each m-block
+  int32_t* mbrows_ = nullptr;           // [max_mb] real rows of each m-block
   int32_t* srcrow_ = nullptr;           // [max_rows] source token of each routed row
   uint16_t *xperm_ = nullptr, *hbuf_ = nullptr;
   CUtensorMap tm_gate_, tm_up_, tm_down_, tm_xperm_, tm_h_;
@@ -203,6 +204,8 @@ class Ctx {
   int32_t* dep_tab_host_ = nullptr;      // pinned staging
   int2* dep_seg_ = nullptr;              // device (source, expert) segment table
   int2* dep_seg_host_ = nullptr;
+  int32_t* dep_mbrows_ = nullptr;        // device real rows per m-block
+  int32_t* dep_mbrows_host_ = nullptr;
   int64_t dep_tab_cap_ = 0;
   CUtensorMap tm_dep_recv_, tm_dep_h_;
   // fp8 DEP: received e4m3 rows live in dep_recv_ (bytes), their scales in
