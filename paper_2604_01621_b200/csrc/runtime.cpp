@@ -623,31 +623,37 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   mark(0);
   const int64_t mb_ub = mb_bound(T);
   const int32_t* stab = slot_tab_ + (size_t(layer) * 2 + size_t(parity)) * (E_ + 1);
+  // CTA pairs need 256-row expert segments. Below one 128-row m-block per
+  // expert on average (decode batches) the padding would double the MMA and
+  // A-tile work of every expert, so such calls use 128-row segments and the
+  // 1-SM kernel. (Rank-local choice: the DEP layout keeps row_align_.)
+  const bool pair = gemm_pair_ && T * k_ >= int64_t(E_) * 128;
+  const int align = pair ? row_align_ : 128;
+  const CUtensorMap& tmdown = pair ? tm_down_p_ : tm_down_;
   if (fp8_) {
     // W8A8: the permute writes e4m3 copies of every routed row and of the
     // shared-expert rows (after meta[2]) with per-row scales; GEMM1 emits
     // bf16 H, which is re-quantised per row for GEMM2.
     uint8_t* x8 = reinterpret_cast<uint8_t*>(xperm_);
     const int np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_,
-                                  nullptr, meta_, nullptr, scratch_, st, x8, xs_, row_align_, mbrows_);
+                                  nullptr, meta_, nullptr, scratch_, st, x8, xs_, align, mbrows_);
     mark(1);
     GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 0, mbseg_,
-                nullptr, xs_, sarena_[0], sarena_[1], gemm_pair_ ? 1 : 0, raster_, mbrows_};
+                nullptr, xs_, sarena_[0], sarena_[1], pair ? 1 : 0, raster_, mbrows_};
     launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_x8_, tm_x8_, tm_gate_, tm_up_, g1,
                         int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
     launch_quant_rows_fp8(hbuf_, max_rows_, f_, meta_, h8_, hs_, st);
     mark(2);
     GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
-                nullptr, hs_, sarena_[2], nullptr, gemm_pair_ ? 1 : 0, raster_, mbrows_};
-    const CUtensorMap& tmd8 = gemm_pair_ ? tm_down_p_ : tm_down_;
-    launch_grouped_gemm(GEMM_PLAIN_FP8, tm_h8_, tm_h8_, tmd8, tmd8, g2,
+                nullptr, hs_, sarena_[2], nullptr, pair ? 1 : 0, raster_, mbrows_};
+    launch_grouped_gemm(GEMM_PLAIN_FP8, tm_h8_, tm_h8_, tmdown, tmdown, g2,
                         int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
     mark(3);
     launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
     launches += 3 + np + 3 + 1;  // router 3, permute, GEMM1 + quant + GEMM2, combine
   } else {
   const int np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_,
-                                nullptr, meta_, xperm_, scratch_, st, nullptr, nullptr, row_align_, mbrows_);
+                                nullptr, meta_, xperm_, scratch_, st, nullptr, nullptr, align, mbrows_);
   mark(1);
   const CUtensorMap tm_x = shared_ ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
   // Routed A rows come from the materialised expert-major copy. (GEMM1 can
@@ -655,13 +661,12 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   // B200 that measured 2.5x slower: 32 scattered 128-byte row fetches per
   // k-block defeat L2 reuse across the expert's 16 n-block tiles.)
   GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_,
-              nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_, mbrows_};
+              nullptr, nullptr, nullptr, nullptr, pair ? 1 : 0, raster_, mbrows_};
   launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(2);
   GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
-              nullptr, nullptr, nullptr, nullptr, gemm_pair_ ? 1 : 0, raster_, mbrows_};
-  const CUtensorMap& tmd = gemm_pair_ ? tm_down_p_ : tm_down_;
-  launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tmd, tmd, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
+              nullptr, nullptr, nullptr, nullptr, pair ? 1 : 0, raster_, mbrows_};
+  launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tmdown, tmdown, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
   mark(3);
   launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
   launches += 3 + np + 2 + 1;  // router 3, permute, GEMM1, GEMM2, combine

@@ -340,7 +340,7 @@ def test_gemm_pair_matches_single_cta(dev, monkeypatch, name):
         c = D.DwdpContext(cfg)
         c.init_weights()
         c.set_bias(_bias(cfg))
-        x = make_x(333, cfg.hidden, 5, dev)
+        x = make_x(2000, cfg.hidden, 5, dev)  # >= 128 rows per expert: the pair path is taken
         outs.append(c.moe_forward(0, x).float().cpu().numpy())
         torch.cuda.synchronize()
         c.close()
