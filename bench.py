@@ -554,6 +554,7 @@ def main():
             "kernel_ms_per_layer": {k2.replace("_ns", ""): v for k2, v in split.items()},
             "roofline": roof, "step_roofline": step_roof, "routing": routing,
             "dep_baseline": dep, "report": acct,
+            "hbm_gb": {k2: round(v / 1e9, 2) for k2, v in ctx.memory().items()},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
         }
