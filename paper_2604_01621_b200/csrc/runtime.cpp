@@ -61,11 +61,14 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
           "ctx: unknown weight_dtype");
   fp8_ = c.weight_dtype == DWDP_WEIGHT_FP8;
   esz_ = fp8_ ? 1 : 2;
-  // bf16 expert GEMMs run on CTA pairs (cta_group::2, 256-row tiles), which
-  // needs 256-row expert segments; DWDP_GEMM_PAIR=0 selects the 1-SM kernel.
+  // The expert GEMMs run on the 1-SM kernel by default. The CTA-pair kernel
+  // (cta_group::2, 256-row segments; DWDP_GEMM_PAIR=1) is 2-10% faster per
+  // SM clock, but on the power-capped B200 it drew the clock down from ~1.3
+  // to ~0.94 GHz and the full step measured 9% slower on the same box
+  // (scripts/gpu/r1_ab_pair.sh: 144K vs 158K tokens/s).
   {
     const char* env = std::getenv("DWDP_GEMM_PAIR");
-    gemm_pair_ = !(env && env[0] == '0');
+    gemm_pair_ = env && env[0] == '1';
     row_align_ = gemm_pair_ ? 256 : 128;
     const char* r = std::getenv("DWDP_RASTER");  // experiments: m / n (default auto)
     raster_ = r ? (r[0] == 'm' ? 1 : r[0] == 'n' ? 2 : 0) : 0;
