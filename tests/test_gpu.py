@@ -329,13 +329,15 @@ def test_prefetch_handles(dev):
         c.close()
 
 
-@pytest.mark.parametrize("name", ["mid_sigmoid", "mid_fp8"])
-def test_gemm_pair_matches_single_cta(dev, monkeypatch, name):
-    """The CTA-pair GEMM path (cta_group::2, 256-row segments, the default)
-    and the 1-SM path give the same layer outputs (bf16 and e4m3 weights)."""
+@pytest.mark.parametrize("name,mode", [("mid_sigmoid", "1"), ("mid_fp8", "1"),
+                                       ("mid_sigmoid", "2"), ("mid_fp8", "2")])
+def test_gemm_pair_matches_single_cta(dev, monkeypatch, name, mode):
+    """The CTA-pair GEMM (mode 1: cta_group::2) and the B-multicast cluster GEMM
+    (mode 2), both on 256-row segments, give the same layer outputs as the
+    default 1-SM kernel (bf16 and e4m3 weights; routing included)."""
     cfg = CONFIGS.get(name) or FP8_CONFIGS[name]
     outs = []
-    for pair in ("1", "0"):
+    for pair in (mode, "0"):
         monkeypatch.setenv("DWDP_GEMM_PAIR", pair)
         c = D.DwdpContext(cfg)
         c.init_weights()
