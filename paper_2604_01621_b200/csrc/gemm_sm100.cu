@@ -692,195 +692,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   }
 }
 
-// ---------------------------------------------------------------- B multicast
-// 1-SM MMAs (M128 x N256, cta_group::1) in clusters of two CTAs that share
-// the B tile: CTA r of the cluster computes m-block 2p + r of the same expert
-// and n-block, loads its own A and B rows [128r, 128r + 128) of the n-block,
-// multicasting that half into both CTAs' shared memory. Each CTA's smem ring
-// therefore receives the full B tile while L2 serves it once: per CTA pair
-// and 64-deep k-block 96 KB of L2->SM traffic become 64 KB, without the
-// cross-SM MMA of the CTA-pair kernel. A CTA whose m-block is pure padding
-// (256-row segments) skips its A load, MMAs and stores but still releases
-// its ring slots. Stage release needs both CTAs' consumers, since the peer
-// writes into this CTA's ring: every consumer arrives on the empty barrier of
-// both CTAs (multicast commit, or plain arrives for a skipped block).
-__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                               int c0, int c1, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
-      : "memory");
-}
-__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-
-template <int MODE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
-    grouped_gemm_mc_kernel(const __grid_constant__ CUtensorMap tmA,
-                           const __grid_constant__ CUtensorMap tmA2,
-                           const __grid_constant__ CUtensorMap tmB0,
-                           const __grid_constant__ CUtensorMap tmB1, GemmArgs p) {
-  constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8;
-  constexpr bool FP8 = MODE == kSwiGLU8 || MODE == kPlain8;
-  constexpr int BKE = (MODE == kInt8 || FP8) ? 128 : 64;  // K elements per 128-byte smem row
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-  constexpr uint16_t kBoth = 3;
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < STAGES; ++st) {
-      mbar_init(&full[st], 1);   // own expect_tx arrive; A + both B halves complete the bytes
-      mbar_init(&empty[st], 2);  // both CTAs' consumers
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_holder)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB0)) : "memory");
-  }
-  tc_fence_before();
-  cluster_sync_all();  // both CTAs' barriers exist before any multicast lands
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
-
-  const int total_mb = p.meta[0];
-  const int routed_mb = p.meta[1];
-  const int nb_count = SWIGLU ? p.n_out / 128 : (p.n_out + BN - 1) / BN;
-  const int num_tiles = (total_mb >> 1) * nb_count;
-  const int kb_count = p.K / BKE;
-  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  auto live = [&](int mb) { return p.mb_rows == nullptr || p.mb_rows[mb] > 0; };
-
-  if (warp == 0) {
-    if (lane == 0) {  // ------------------ TMA producer
-      int st = 0;
-      uint32_t ph = 0;
-      for (int tile = cid; tile < num_tiles; tile += ncl) {
-        int mp, nb;
-        pair_coords(tile, nb_count, p.mb_seg, p.raster, mp, nb);
-        const int mb = 2 * mp + int(rank);
-        const int e = p.mblock_expert[mb];
-        const bool sh = p.shared_a2 && e == p.E;
-        const CUtensorMap* am = sh ? &tmA2 : &tmA;
-        const int arow = (sh ? mb - routed_mb : mb) * BM;
-        const bool load_a = live(mb);
-        // this CTA's half of the B tile: SwiGLU r = 0 gate rows, r = 1 up rows;
-        // plain rows [128r, 128r + 128) of the n-block
-        const CUtensorMap* bm = (SWIGLU && rank == 1) ? &tmB1 : &tmB0;
-        const int brow = p.slot_of[e] * p.rows_per_slot + (SWIGLU ? nb * 128 : nb * BN + int(rank) * 128);
-        for (int kb = 0; kb < kb_count; ++kb) {
-          mbar_wait(&empty[st], ph ^ 1);
-          mbar_expect_tx(&full[st], (load_a ? A_STAGE : 0) + B_STAGE);
-          if (load_a) tma_load_2d(sA + st * A_STAGE, am, &full[st], kb * BKE, arow);
-          tma_load_2d_mc(sB + st * B_STAGE + int(rank) * (B_STAGE / 2), bm, &full[st], kb * BKE, brow,
-                         kBoth);
-          if (++st == STAGES) {
-            st = 0;
-            ph ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer (each CTA, own m-block)
-      const uint32_t peer = rank ^ 1u;
-      int st = 0;
-      uint32_t ph = 0;
-      int local = 0;
-      for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
-        int mp, nb;
-        pair_coords(tile, nb_count, p.mb_seg, p.raster, mp, nb);
-        const bool work = live(2 * mp + int(rank));
-        const int a = local & 1;
-        const uint32_t aph = (local >> 1) & 1;
-        mbar_wait(&tempty[a], aph ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem_base + uint32_t(a * BN);
-        for (int kb = 0; kb < kb_count; ++kb) {
-          mbar_wait(&full[st], ph);
-          tc_fence_after();
-          if (work) {
-            const uint64_t ad = sw128_desc(smem_u32(sA + st * A_STAGE));
-            const uint64_t bd = sw128_desc(smem_u32(sB + st * B_STAGE));
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if (MODE == kInt8)
-                tc_mma_i8(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0);
-              else if (FP8)
-                tc_mma_f8(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0);
-              else
-                tc_mma(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0);
-            }
-            tc_commit_mc(&empty[st], kBoth);  // releases the slot in both CTAs
-          } else {  // padding m-block: nothing read, release the slot in both CTAs
-            mbar_arrive(&empty[st]);
-            mbar_arrive_cluster(map_to_rank(&empty[st], peer));
-          }
-          if (++st == STAGES) {
-            st = 0;
-            ph ^= 1;
-          }
-        }
-        if (work)
-          tc_commit(&tfull[a]);
-        else
-          mbar_arrive(&tfull[a]);
-      }
-    }
-  } else if (warp >= 4) {  // ------------- epilogue (own 128 rows)
-    const int q = warp & 3;
-    int local = 0;
-    for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
-      int mp, nb;
-      pair_coords(tile, nb_count, p.mb_seg, p.raster, mp, nb);
-      const int mb = 2 * mp + int(rank);
-      const int a = local & 1;
-      const uint32_t aph = (local >> 1) & 1;
-      mbar_wait(&tfull[a], aph);
-      tc_fence_after();
-      if (live(mb))
-        epilogue_tile<MODE>(p, mb, nb, tmem_base + (uint32_t(q * 32) << 16) + uint32_t(a * BN), q, lane);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[a]);
-    }
-  }
-  tc_fence_before();
-  cluster_sync_all();  // no multicast or remote arrive may target a finished CTA
-  if (warp == 2) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS));
-  }
-}
-
 // ---------------------------------------------------------------- host
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -962,16 +773,6 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
       cudaFuncSetAttribute(grouped_gemm_pair_kernel<kInt8>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
-      cudaFuncSetAttribute(grouped_gemm_mc_kernel<kSwiGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           SMEM_BYTES);
-      cudaFuncSetAttribute(grouped_gemm_mc_kernel<kPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           SMEM_BYTES);
-      cudaFuncSetAttribute(grouped_gemm_mc_kernel<kSwiGLU8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           SMEM_BYTES);
-      cudaFuncSetAttribute(grouped_gemm_mc_kernel<kPlain8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           SMEM_BYTES);
-      cudaFuncSetAttribute(grouped_gemm_mc_kernel<kInt8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           SMEM_BYTES);
       {
         cudaLaunchConfig_t lc = {};
         cudaLaunchAttribute at[1];
@@ -997,22 +798,6 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
     }
   }
   if (max_tiles <= 0) return;
-  if (args.pair == 2) {  // 1-SM MMAs, B multicast across a cluster of two
-    const int cap = 2 * pair_clusters[dev];
-    int g = max_tiles < cap ? max_tiles : cap;
-    g = g < 2 ? 2 : (g & ~1);
-    if (mode == kSwiGLU)
-      grouped_gemm_mc_kernel<kSwiGLU><<<g, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
-    else if (mode == kPlain)
-      grouped_gemm_mc_kernel<kPlain><<<g, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
-    else if (mode == kSwiGLU8)
-      grouped_gemm_mc_kernel<kSwiGLU8><<<g, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
-    else if (mode == kPlain8)
-      grouped_gemm_mc_kernel<kPlain8><<<g, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
-    else
-      grouped_gemm_mc_kernel<kInt8><<<g, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
-    return;
-  }
   if (args.pair) {
     const int cap = 2 * pair_clusters[dev];
     int g = max_tiles < cap ? max_tiles : cap;

@@ -34,11 +34,9 @@ struct GemmArgs {
   const float* a_scale;
   const float* b_scale0;
   const float* b_scale1;
-  // 0: 1-SM kernel. 1: CTA-pair kernel (cta_group::2, 256 x 256 tiles).
-  // 2: 1-SM MMAs in clusters of two CTAs sharing each B tile by TMA
-  // multicast. 1 and 2 need every expert segment (and the shared block)
-  // padded to 256 rows and, for GEMM_PLAIN / GEMM_INT8, B maps with 128-row
-  // boxes.
+  // 0: 1-SM kernel. 1: CTA-pair kernel (cta_group::2, 256 x 256 tiles): needs
+  // every expert segment (and the shared block) padded to 256 rows and, for
+  // GEMM_PLAIN / GEMM_INT8, B maps with 128-row boxes.
   int pair;
   // segment raster: 0 auto (n-block-major while the segment's A rows <= its
   // B rows), 1 always m-block-major, 2 always n-block-major (experiments)

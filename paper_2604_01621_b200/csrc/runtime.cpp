@@ -68,7 +68,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   // (scripts/gpu/r1_ab_pair.sh: 144K vs 158K tokens/s).
   {
     const char* env = std::getenv("DWDP_GEMM_PAIR");
-    gemm_pair_ = env ? (env[0] == '1' ? 1 : env[0] == '2' ? 2 : 0) : 0;
+    gemm_pair_ = env && env[0] == '1' ? 1 : 0;
     row_align_ = gemm_pair_ ? 256 : 128;
     const char* r = std::getenv("DWDP_RASTER");  // experiments: m / n (default auto)
     raster_ = r ? (r[0] == 'm' ? 1 : r[0] == 'n' ? 2 : 0) : 0;
