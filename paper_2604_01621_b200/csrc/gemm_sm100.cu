@@ -45,8 +45,6 @@ constexpr int A_STAGE = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE = BN * BK * 2;  // 32 KB
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
 constexpr uint32_t TMEM_COLS = 512;
-constexpr int PF_LEAD = 12;   // k-blocks before a tile's end at which the next tile is prefetched
-constexpr int PF_BLOCKS = 4;  // leading k-blocks of the next tile prefetched into L2
 
 // ---------------------------------------------------------------- PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -83,13 +81,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
-}
-// L2 prefetch of one TMA box (no shared memory, no barrier).
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(c0), "r"(c1)
-               : "memory");
 }
 // 4 gathered rows x 64 bf16 (4 x 128 B) into consecutive smem rows.
 __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar,
@@ -367,27 +358,7 @@ __global__ void __launch_bounds__(256, 1)
       // on the streamed operand made GEMM1 read 210 GB from HBM instead of 37;
       // evict-last on the reused one cut the isolated kernel's HBM reads to
       // 26 GB but its lines outlive the kernel and slowed the full step 11%.)
-      // The first k-blocks of the next tile come from new A rows / a new B
-      // n-block, often straight from HBM: prefetch them into L2 while this
-      // tile still has PF_LEAD k-blocks to go, so the tile switch does not
-      // drain the 4-stage ring (most visible in GEMM2's short K = f tiles).
-      const int next = tile + int(gridDim.x);
-      const int pf_at = kb_count > PF_LEAD ? kb_count - PF_LEAD : 0;
       for (int kb = 0; kb < kb_count; ++kb) {
-        if (lane == 0 && p.l2_prefetch && kb == pf_at && next < num_tiles && p.a_rows == nullptr) {
-          int mb2, nb2;
-          tile_coords(next, nb_count, p.mb_seg, mb2, nb2);
-          const int e2 = p.mblock_expert[mb2];
-          const bool sh2 = p.shared_a2 && e2 == p.E;
-          const int arow2 = (sh2 ? mb2 - routed_mb : mb2) * BM;
-          const int brow2 = p.slot_of[e2] * p.rows_per_slot + nb2 * (SWIGLU ? 128 : BN);
-          const int npf = kb_count < PF_BLOCKS ? kb_count : PF_BLOCKS;
-          for (int k2 = 0; k2 < npf; ++k2) {
-            tma_prefetch_2d(sh2 ? &tmA2 : &tmA, k2 * BKE, arow2);
-            tma_prefetch_2d(&tmB0, k2 * BKE, brow2);
-            if (SWIGLU) tma_prefetch_2d(&tmB1, k2 * BKE, brow2);
-          }
-        }
         if (lane == 0) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], A_STAGE + B_STAGE);

@@ -44,8 +44,6 @@ struct GemmArgs {
   // Optional [m-blocks] real rows of each m-block: the epilogue does not
   // store the padding rows (decode batches are mostly padding).
   const int32_t* mb_rows;
-  // 1-SM kernel: prefetch the next tile's first k-blocks into L2 (0 = off)
-  int l2_prefetch;
 };
 
 // 2-D bf16 TMA map over a row-major [rows][cols] matrix, box = 64 x box_rows,

@@ -70,8 +70,6 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     const char* env = std::getenv("DWDP_GEMM_PAIR");
     gemm_pair_ = env && env[0] == '1' ? 1 : 0;
     row_align_ = gemm_pair_ ? 256 : 128;
-    const char* pf = std::getenv("DWDP_L2_PREFETCH");  // experiments: 0 disables
-    l2pf_ = pf && pf[0] == '0' ? 0 : 1;
     const char* r = std::getenv("DWDP_RASTER");  // experiments: m / n (default auto)
     raster_ = r ? (r[0] == 'm' ? 1 : r[0] == 'n' ? 2 : 0) : 0;
   }
@@ -644,13 +642,13 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
                                   nullptr, meta_, nullptr, scratch_, st, x8, xs_, align, mbrows_);
     mark(1);
     GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 0, mbseg_,
-                nullptr, xs_, sarena_[0], sarena_[1], pair ? gemm_pair_ : 0, raster_, mbrows_, l2pf_};
+                nullptr, xs_, sarena_[0], sarena_[1], pair ? gemm_pair_ : 0, raster_, mbrows_};
     launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_x8_, tm_x8_, tm_gate_, tm_up_, g1,
                         int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
     launch_quant_rows_fp8(hbuf_, max_rows_, f_, meta_, h8_, hs_, st);
     mark(2);
     GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
-                nullptr, hs_, sarena_[2], nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_, l2pf_};
+                nullptr, hs_, sarena_[2], nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_};
     launch_grouped_gemm(GEMM_PLAIN_FP8, tm_h8_, tm_h8_, tmdown, tmdown, g2,
                         int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
     mark(3);
@@ -666,11 +664,11 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   // B200 that measured 2.5x slower: 32 scattered 128-byte row fetches per
   // k-block defeat L2 reuse across the expert's 16 n-block tiles.)
   GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_,
-              nullptr, nullptr, nullptr, nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_, l2pf_};
+              nullptr, nullptr, nullptr, nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_};
   launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(2);
   GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
-              nullptr, nullptr, nullptr, nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_, l2pf_};
+              nullptr, nullptr, nullptr, nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_};
   launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tmdown, tmdown, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
   mark(3);
   launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);

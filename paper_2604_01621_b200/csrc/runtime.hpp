@@ -164,7 +164,6 @@ class Ctx {
   int gemm_pair_ = 0;              // GemmArgs::pair: 0 1-SM, 1 CTA pair
   int row_align_ = 128;            // expert segment padding (256 with pairs)
   int raster_ = 0;                 // GemmArgs::raster (DWDP_RASTER experiments)
-  int l2pf_ = 1;                   // GemmArgs::l2_prefetch (DWDP_L2_PREFETCH=0 disables)
   // upper bound on the m-blocks of T tokens (routed segments + shared block)
   int64_t mb_bound(int64_t T) const {
     return (T * k_ + int64_t(E_) * (row_align_ - 1)) / 128 + 2 +
