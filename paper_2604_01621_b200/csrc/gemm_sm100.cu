@@ -180,12 +180,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 // (B live, A streamed once) for long segments such as the shared expert's
 // T rows, which n-major would re-read from HBM once per n-block.
 __device__ __forceinline__ void tile_coords(int tile, int nb_count, const int2* __restrict__ seg,
-                                            int& mb, int& nb) {
+                                            int raster, int& mb, int& nb) {
   mb = tile / nb_count;
   nb = tile - mb * nb_count;
-  if (seg) {
+  if (seg && raster != 1) {
     const int2 s = seg[mb];
-    if (s.y <= 2 * nb_count) {
+    if (raster == 2 || s.y <= 2 * nb_count) {
       const int local = tile - s.x * nb_count;
       nb = local / s.y;
       mb = s.x + (local - nb * s.y);
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t ph = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       int mb, nb;
-      tile_coords(tile, nb_count, p.mb_seg, mb, nb);
+      tile_coords(tile, nb_count, p.mb_seg, p.raster, mb, nb);
       const int e = p.mblock_expert[mb];
       const bool sh = p.shared_a2 && e == p.E;
       const bool gather = p.a_rows != nullptr && !sh;
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(256, 1)
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       int mb, nb;
-        tile_coords(tile, nb_count, p.mb_seg, mb, nb);
+        tile_coords(tile, nb_count, p.mb_seg, p.raster, mb, nb);
       const int a = local & 1;
       const uint32_t aph = (local >> 1) & 1;
       mbar_wait(&tfull[a], aph);
