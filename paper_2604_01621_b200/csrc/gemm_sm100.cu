@@ -82,15 +82,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
-// 4 gathered rows x 64 bf16 (4 x 128 B) into consecutive smem rows.
-__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int col, int4 rows) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(col), "r"(rows.x), "r"(rows.y),
-      "r"(rows.z), "r"(rows.w)
-      : "memory");
+// 16-byte cp.async global -> shared (L2 only), and the arrive-on-completion
+// of the calling thread's cp.asyncs on an mbarrier (counts as one arrival).
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -305,7 +303,8 @@ __global__ void __launch_bounds__(256, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      // gathering: + one cp.async-completion arrival per producer lane
+      mbar_init(&full[s], p.a_rows != nullptr ? 33 : 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -351,9 +350,13 @@ __global__ void __launch_bounds__(256, 1)
       const CUtensorMap* am = sh ? &tmA2 : &tmA;
       const int arow = (sh ? mb - routed_mb : mb) * BM;
       const int brow = p.slot_of[e] * p.rows_per_slot + nb * (SWIGLU ? 128 : BN);
-      // gather mode: lane l owns source rows 4l..4l+3 of this m-block
-      const int4 rows4 = gather ? *reinterpret_cast<const int4*>(p.a_rows + int64_t(mb) * BM + 4 * lane)
-                                : make_int4(0, 0, 0, 0);
+      // gather mode: lane l copies rows 4l..4l+3 of the m-block (8 x 16 B per
+      // row and k-block) into the SWIZZLE_128B layout TMA would have produced
+      const char* srow[4];
+      if (gather)
+        for (int i = 0; i < 4; ++i)
+          srow[i] = reinterpret_cast<const char*>(
+              p.a_src + int64_t(p.a_rows[int64_t(mb) * BM + 4 * lane + i]) * p.a_ld);
       // (L2 priority hints on these loads were measured and rejected: evict-first
       // on the streamed operand made GEMM1 read 210 GB from HBM instead of 37;
       // evict-last on the reused one cut the isolated kernel's HBM reads to
@@ -361,7 +364,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int kb = 0; kb < kb_count; ++kb) {
         if (lane == 0) {
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], A_STAGE + B_STAGE);
+          mbar_expect_tx(&full[s], (gather ? 0 : A_STAGE) + B_STAGE);
           if (!gather) tma_load_2d(sA + s * A_STAGE, am, &full[s], kb * BKE, arow);
           if (SWIGLU) {
             tma_load_2d(sB + s * B_STAGE, &tmB0, &full[s], kb * BKE, brow);
@@ -370,9 +373,20 @@ __global__ void __launch_bounds__(256, 1)
             tma_load_2d(sB + s * B_STAGE, &tmB0, &full[s], kb * BKE, brow);
           }
         }
-        if (gather) {
+        if (p.a_rows != nullptr) {
           __syncwarp();  // slot s is free (lane 0 waited on it)
-          tma_gather4(sA + s * A_STAGE + lane * 4 * 128, am, &full[s], kb * BKE, rows4);
+          if (gather) {
+            const uint32_t base = smem_u32(sA + s * A_STAGE);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int r = 4 * lane + i;
+              const char* src = srow[i] + int64_t(kb) * 128;
+#pragma unroll
+              for (int c = 0; c < 8; ++c)
+                cp_async16(base + uint32_t(r * 128 + ((c ^ (r & 7)) << 4)), src + c * 16);
+            }
+          }
+          cp_async_arrive_noinc(&full[s]);  // every lane, every stage (count 33)
         }
         if (++s == STAGES) {
           s = 0;
@@ -394,6 +408,8 @@ __global__ void __launch_bounds__(256, 1)
         for (int kb = 0; kb < kb_count; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
+          if (p.a_rows != nullptr)  // cp.async (generic proxy) writes -> tcgen05 (async proxy) reads
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           const uint64_t ad = sw128_desc(smem_u32(sA + s * A_STAGE));
           const uint64_t bd = sw128_desc(smem_u32(sB + s * B_STAGE));
 #pragma unroll

@@ -25,9 +25,10 @@ struct GemmArgs {
   // segment so the concurrently running CTAs share B tiles (the expert's
   // weights) and only the segment's A rows stay live in L2.
   const int2* mb_seg;
-  // Optional [routed rows] source row of every padded expert-major row: A is
-  // then gathered straight from the token matrix (`a` must be a gather map,
-  // box 64 x 1) with TMA tile::gather4, so no permuted copy is materialised.
+  // Optional [routed rows] source row of every padded expert-major row: the
+  // routed A rows are then gathered straight from the token matrix a_src
+  // (row stride a_ld elements) by the producer warp with cp.async into the
+  // swizzled smem tile, so no permuted copy is materialised (bf16 GEMM1).
   const int32_t* a_rows;
   // fp8 modes: D = (A_q . B_q^T) * a_scale[row] * b_scale[B row]; SwiGLU uses
   // b_scale0 for the gate rows and b_scale1 for the up rows.
@@ -44,6 +45,8 @@ struct GemmArgs {
   // Optional [m-blocks] real rows of each m-block: the epilogue does not
   // store the padding rows (decode batches are mostly padding).
   const int32_t* mb_rows;
+  const uint16_t* a_src;  // gather source (a_rows != nullptr)
+  int64_t a_ld;
 };
 
 // 2-D bf16 TMA map over a row-major [rows][cols] matrix, box = 64 x box_rows,

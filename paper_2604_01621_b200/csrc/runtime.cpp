@@ -72,6 +72,8 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     row_align_ = gemm_pair_ ? 256 : 128;
     const char* r = std::getenv("DWDP_RASTER");  // experiments: m / n (default auto)
     raster_ = r ? (r[0] == 'm' ? 1 : r[0] == 'n' ? 2 : 0) : 0;
+    const char* g = std::getenv("DWDP_GATHER");  // GEMM1 gathers routed rows from x
+    gather_ = g && g[0] == '1';
   }
   ntens_ = fp8_ ? 6 : 3;
   require(L_ >= 1, "ctx: num_layers must be >= 1");
@@ -655,8 +657,12 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
     launches += 3 + np + 3 + 1;  // router 3, permute, GEMM1 + quant + GEMM2, combine
   } else {
+  // gather_: GEMM1's producer gathers the routed rows from x (cp.async), the
+  // permute only ranks rows and writes src_row (1-SM kernel only)
+  const bool gather = gather_ && !pair;
   const int np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_,
-                                nullptr, meta_, xperm_, scratch_, st, nullptr, nullptr, align, mbrows_);
+                                gather ? srcrow_ : nullptr, meta_, gather ? nullptr : xperm_, scratch_, st,
+                                nullptr, nullptr, align, mbrows_);
   mark(1);
   const CUtensorMap tm_x = shared_ ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
   // Routed A rows come from the materialised expert-major copy. (GEMM1 can
@@ -664,7 +670,8 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   // B200 that measured 2.5x slower: 32 scattered 128-byte row fetches per
   // k-block defeat L2 reuse across the expert's 16 n-block tiles.)
   GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_,
-              nullptr, nullptr, nullptr, nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_};
+              gather ? srcrow_ : nullptr, nullptr, nullptr, nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_,
+              x, h_};
   launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(2);
   GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,

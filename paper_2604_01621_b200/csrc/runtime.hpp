@@ -164,6 +164,7 @@ class Ctx {
   int gemm_pair_ = 0;              // GemmArgs::pair: 0 1-SM, 1 CTA pair
   int row_align_ = 128;            // expert segment padding (256 with pairs)
   int raster_ = 0;                 // GemmArgs::raster (DWDP_RASTER experiments)
+  bool gather_ = false;            // GEMM1 gathers routed rows from x (DWDP_GATHER=1)
   // upper bound on the m-blocks of T tokens (routed segments + shared block)
   int64_t mb_bound(int64_t T) const {
     return (T * k_ + int64_t(E_) * (row_align_ - 1)) / 128 + 2 +

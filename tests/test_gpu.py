@@ -401,3 +401,20 @@ def test_dwdp_large_batch_bitwise(dev, engine):
             assert torch.equal(y, yf), (engine, g, r)
     for c in ranks + [full]:
         c.close()
+
+
+def test_gemm1_gather_matches_permuted_copy(dev, monkeypatch):
+    """GEMM1 gathering the routed rows from x (cp.async into the swizzled
+    tile, no X_perm copy; DWDP_GATHER=1) gives bit-identical layer outputs."""
+    cfg = CONFIGS["mid_sigmoid"]
+    outs = []
+    for g in ("1", "0"):
+        monkeypatch.setenv("DWDP_GATHER", g)
+        c = D.DwdpContext(cfg)
+        c.init_weights()
+        c.set_bias(_bias(cfg))
+        x = make_x(1500, cfg.hidden, 21, dev)
+        outs.append(c.moe_forward(0, x))
+        torch.cuda.synchronize()
+        c.close()
+    assert torch.equal(outs[0], outs[1])
