@@ -665,10 +665,12 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
                                 nullptr, nullptr, align, mbrows_);
   mark(1);
   const CUtensorMap tm_x = shared_ ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
-  // Routed A rows come from the materialised expert-major copy. (GEMM1 can
-  // also gather them from x with TMA tile::gather4 via GemmArgs::a_rows; on
-  // B200 that measured 2.5x slower: 32 scattered 128-byte row fetches per
-  // k-block defeat L2 reuse across the expert's 16 n-block tiles.)
+  // Routed A rows come from the materialised expert-major copy. GEMM1 can
+  // also gather them from x (GemmArgs::a_rows, DWDP_GATHER=1), saving the
+  // permute's 7 GB copy, but both gathers measured ~2x slower on B200: with
+  // TMA tile::gather4 42.7 GB and with cp.async 91.8 GB of HBM reads per
+  // GEMM1 instead of 26 GB -- the gathered rows are not reused from L2
+  // across the expert's 16 n-block tiles the way the contiguous copy is.
   GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_,
               gather ? srcrow_ : nullptr, nullptr, nullptr, nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_,
               x, h_};
