@@ -418,3 +418,35 @@ def test_gemm1_gather_matches_permuted_copy(dev, monkeypatch):
         torch.cuda.synchronize()
         c.close()
     assert torch.equal(outs[0], outs[1])
+
+
+# ---------------------------------------------------------------- error contract
+
+@pytest.mark.parametrize("bad", [dict(hidden=300), dict(ffn=100), dict(top_k=0), dict(top_k=17),
+                                 dict(num_experts=600), dict(rank=2, group_size=2),
+                                 dict(n_group=5), dict(topk_group=9), dict(scoring=3),
+                                 dict(engine=7), dict(slice_size=1000), dict(shared_ffn=512),
+                                 dict(weight_dtype=5), dict(max_tokens=0)])
+def test_config_errors_are_config_errors(dev, bad):
+    """Invalid configurations fail with ConfigError (status 2, reference
+    errors.hpp:11-15) before touching the GPU, never with a CUDA error."""
+    kw = dict(num_layers=1, num_experts=64, hidden=1024, ffn=256, shared_ffn=256, top_k=6,
+              n_group=8, topk_group=4, max_tokens=64)
+    kw.update(bad)
+    with pytest.raises(D.ConfigError):
+        D.DwdpContext(D.DwdpConfig(**kw))
+
+
+def test_call_errors(dev, ctxs):
+    ctx = ctxs["tiny"]
+    x = make_x(2000, 512, 1, dev)
+    with pytest.raises(D.ConfigError):
+        ctx.moe_forward(0, x)  # T > max_tokens
+    with pytest.raises(D.ConfigError):
+        ctx.moe_forward(5, x[:10])  # layer out of range
+    with pytest.raises(D.ConfigError):
+        ctx.read_expert(0, 99, 0)
+    lonely = D.DwdpContext(D.DwdpConfig(**MID, rank=0, group_size=2))
+    with pytest.raises(D.ConfigError):
+        lonely.prefetch_issue(1)  # peers not wired
+    lonely.close()
