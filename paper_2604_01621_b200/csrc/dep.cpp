@@ -295,25 +295,25 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   if (nblocks > 0 && fp8_) {
     const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_i8(x8 + send_total * h_, T, h_, 128) : tm_dep_x8_;
     GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1, dep_seg_,
-                nullptr, dep_xs_, sarena_[0], sarena_[1], gemm_pair_ == 1 ? 1 : 0, raster_, dep_mbrows_};
+                nullptr, dep_xs_, sarena_[0], sarena_[1], gemm_pair_, raster_, dep_mbrows_};
     launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_dep_x8_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
     launch_quant_rows_fp8(dep_h_, dep_cap_rows_, f_, dmeta, dep_h8_, dep_hs_, st);
   } else if (nblocks > 0) {
     const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_dep_recv_;
     GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1, dep_seg_,
-                nullptr, nullptr, nullptr, nullptr, gemm_pair_ == 1 ? 1 : 0, raster_, dep_mbrows_};
+                nullptr, nullptr, nullptr, nullptr, gemm_pair_, raster_, dep_mbrows_};
     launch_grouped_gemm(GEMM_SWIGLU, tm_dep_recv_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
   }
   mark(&rec.k[2]);
   if (nblocks > 0 && fp8_) {
     GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
-                nullptr, dep_hs_, sarena_[2], nullptr, gemm_pair_ == 1 ? 1 : 0, raster_, dep_mbrows_};
-    const CUtensorMap& tmd8 = gemm_pair_ == 1 ? tm_down_p_ : tm_down_;
+                nullptr, dep_hs_, sarena_[2], nullptr, gemm_pair_, raster_, dep_mbrows_};
+    const CUtensorMap& tmd8 = gemm_pair_ ? tm_down_p_ : tm_down_;
     launch_grouped_gemm(GEMM_PLAIN_FP8, tm_dep_h8_, tm_dep_h8_, tmd8, tmd8, g2, int(nblocks * (h_ / 256)), st);
   } else if (nblocks > 0) {
     GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
-                nullptr, nullptr, nullptr, nullptr, gemm_pair_ == 1 ? 1 : 0, raster_, dep_mbrows_};
-    const CUtensorMap& tmd = gemm_pair_ == 1 ? tm_down_p_ : tm_down_;
+                nullptr, nullptr, nullptr, nullptr, gemm_pair_, raster_, dep_mbrows_};
+    const CUtensorMap& tmd = gemm_pair_ ? tm_down_p_ : tm_down_;
     launch_grouped_gemm(GEMM_PLAIN, tm_dep_h_, tm_dep_h_, tmd, tmd, g2, int(nblocks * (h_ / 256)), st);
   }
   mark(&rec.k[3]);

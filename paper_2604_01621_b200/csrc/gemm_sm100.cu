@@ -455,184 +455,6 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-// ---------------------------------------------------------------- wide tiles
-// 1-SM kernel with 256 x 256 tiles: a tile is a "unit" of up to two
-// consecutive m-blocks of one expert segment (the last unit of an odd-length
-// segment holds one) times one n-block. Every k-block stages both A tiles and
-// the B tile once (64 KB) and issues the MMAs of both m-blocks against the
-// same B, so B's L2->SM bytes per flop halve, as in the CTA-pair kernel but
-// without cross-SM coupling and with 128-row expert segments. The two fp32
-// accumulators (one per m-block, 256 columns each) fill all of TMEM: the
-// epilogue drains the first while the next tile's MMAs into it may already
-// start once it is released, then the second.
-// Unit table (written by the permute): units[u] = {first m-block, m-blocks
-// (1 or 2), first unit of its segment, units in its segment}.
-constexpr int W_STAGE = 2 * A_STAGE + B_STAGE;  // 64 KB
-constexpr int W_STAGES = 3;
-constexpr int W_SMEM_BYTES = W_STAGES * W_STAGE + 1024 + 256;
-
-__device__ __forceinline__ void unit_coords(int tile, int nb_count, const int4* __restrict__ units,
-                                            int raster, int& u, int& nb) {
-  u = tile / nb_count;
-  nb = tile - u * nb_count;
-  const int4 U = units[u];
-  if (raster != 1 && (raster == 2 || U.w <= nb_count)) {  // segment's A rows <= B rows: n-major
-    const int local = tile - U.z * nb_count;
-    nb = local / U.w;
-    u = U.z + (local - nb * U.w);
-  }
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(384, 1)
-    grouped_gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA,
-                             const __grid_constant__ CUtensorMap tmA2,
-                             const __grid_constant__ CUtensorMap tmB0,
-                             const __grid_constant__ CUtensorMap tmB1, GemmArgs p) {
-  constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8;
-  constexpr bool FP8 = MODE == kSwiGLU8 || MODE == kPlain8;
-  constexpr int BKE = (MODE == kInt8 || FP8) ? 128 : 64;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + W_STAGES * W_STAGE);
-  uint64_t* empty = full + W_STAGES;
-  uint64_t* tfull = empty + W_STAGES;  // one per tile (both accumulators)
-  uint64_t* tempty = tfull + 1;        // [2]: accumulator i drained
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-  auto sA = [&](int st, int i) { return smem + st * W_STAGE + i * A_STAGE; };
-  auto sB = [&](int st) { return smem + st * W_STAGE + 2 * A_STAGE; };
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < W_STAGES; ++st) {
-      mbar_init(&full[st], 1);
-      mbar_init(&empty[st], 1);
-    }
-    mbar_init(&tfull[0], 1);
-    mbar_init(&tempty[0], 4);
-    mbar_init(&tempty[1], 4);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_holder)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB0)) : "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
-
-  const int routed_mb = p.meta[1];
-  const int nb_count = SWIGLU ? p.n_out / 128 : (p.n_out + BN - 1) / BN;
-  const int num_tiles = *p.unit_count * nb_count;
-  const int kb_count = p.K / BKE;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ------------------ TMA producer
-      int st = 0;
-      uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        int u, nb;
-        unit_coords(tile, nb_count, p.units, p.raster, u, nb);
-        const int4 U = p.units[u];
-        const int mb0 = U.x, cnt = U.y;
-        const int e = p.mblock_expert[mb0];
-        const bool sh = p.shared_a2 && e == p.E;
-        const CUtensorMap* am = sh ? &tmA2 : &tmA;
-        const int arow = (sh ? mb0 - routed_mb : mb0) * BM;
-        const int brow = p.slot_of[e] * p.rows_per_slot + nb * (SWIGLU ? 128 : BN);
-        for (int kb = 0; kb < kb_count; ++kb) {
-          mbar_wait(&empty[st], ph ^ 1);
-          mbar_expect_tx(&full[st], cnt * A_STAGE + B_STAGE);
-          tma_load_2d(sA(st, 0), am, &full[st], kb * BKE, arow);
-          if (cnt == 2) tma_load_2d(sA(st, 1), am, &full[st], kb * BKE, arow + BM);
-          if (SWIGLU) {
-            tma_load_2d(sB(st), &tmB0, &full[st], kb * BKE, brow);
-            tma_load_2d(sB(st) + B_STAGE / 2, &tmB1, &full[st], kb * BKE, brow);
-          } else {
-            tma_load_2d(sB(st), &tmB0, &full[st], kb * BKE, brow);
-          }
-          if (++st == W_STAGES) {
-            st = 0;
-            ph ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      int st = 0;
-      uint32_t ph = 0;
-      int local = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-        int u, nb;
-        unit_coords(tile, nb_count, p.units, p.raster, u, nb);
-        const int cnt = p.units[u].y;
-        const uint32_t tph = uint32_t(local & 1) ^ 1u;  // previous tile's drain
-        for (int kb = 0; kb < kb_count; ++kb) {
-          mbar_wait(&full[st], ph);
-          tc_fence_after();
-          const uint64_t bd = sw128_desc(smem_u32(sB(st)));
-          for (int i = 0; i < cnt; ++i) {
-            if (kb == 0) {  // accumulator i free (drained by the epilogue)?
-              mbar_wait(&tempty[i], tph);
-              tc_fence_after();
-            }
-            const uint32_t d = tmem_base + uint32_t(i * BN);
-            const uint64_t ad = sw128_desc(smem_u32(sA(st, i)));
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if (MODE == kInt8)
-                tc_mma_i8(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0);
-              else if (FP8)
-                tc_mma_f8(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0);
-              else
-                tc_mma(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0);
-            }
-          }
-          tc_commit(&empty[st]);
-          if (++st == W_STAGES) {
-            st = 0;
-            ph ^= 1;
-          }
-        }
-        tc_commit(&tfull[0]);
-      }
-    }
-  } else if (warp >= 4) {  // ------------- epilogue: warps 4-7 accumulator 0, 8-11 accumulator 1
-    const int q = warp & 3, i = (warp - 4) >> 2;
-    int local = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-      int u, nb;
-      unit_coords(tile, nb_count, p.units, p.raster, u, nb);
-      const int4 U = p.units[u];
-      mbar_wait(&tfull[0], uint32_t(local & 1));
-      tc_fence_after();
-      if (i < U.y)
-        epilogue_tile<MODE>(p, U.x + i, nb, tmem_base + (uint32_t(q * 32) << 16) + uint32_t(i * BN), q,
-                            lane);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[i]);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS));
-  }
-}
-
 // ---------------------------------------------------------------- CTA pair
 // 2-SM variant (cta_group::2) for the bf16 expert GEMMs. A cluster of two
 // CTAs on one TPC computes a 256 x 256 tile: CTA r loads A rows of m-block
@@ -967,16 +789,6 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
       cudaFuncSetAttribute(grouped_gemm_pair_kernel<kInt8>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
-      cudaFuncSetAttribute(grouped_gemm_wide_kernel<kSwiGLU>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, W_SMEM_BYTES);
-      cudaFuncSetAttribute(grouped_gemm_wide_kernel<kPlain>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, W_SMEM_BYTES);
-      cudaFuncSetAttribute(grouped_gemm_wide_kernel<kSwiGLU8>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, W_SMEM_BYTES);
-      cudaFuncSetAttribute(grouped_gemm_wide_kernel<kPlain8>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, W_SMEM_BYTES);
-      cudaFuncSetAttribute(grouped_gemm_wide_kernel<kInt8>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, W_SMEM_BYTES);
       {
         cudaLaunchConfig_t lc = {};
         cudaLaunchAttribute at[1];
@@ -1002,20 +814,6 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
     }
   }
   if (max_tiles <= 0) return;
-  if (args.pair == 2) {  // wide 256 x 256 tiles on the 1-SM kernel
-    const int grid = max_tiles < sms[dev] ? max_tiles : sms[dev];
-    if (mode == kSwiGLU)
-      grouped_gemm_wide_kernel<kSwiGLU><<<grid, 384, W_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
-    else if (mode == kPlain)
-      grouped_gemm_wide_kernel<kPlain><<<grid, 384, W_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
-    else if (mode == kSwiGLU8)
-      grouped_gemm_wide_kernel<kSwiGLU8><<<grid, 384, W_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
-    else if (mode == kPlain8)
-      grouped_gemm_wide_kernel<kPlain8><<<grid, 384, W_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
-    else
-      grouped_gemm_wide_kernel<kInt8><<<grid, 384, W_SMEM_BYTES, st>>>(a, a2, b0, b1, args);
-    return;
-  }
   if (args.pair) {
     const int cap = 2 * pair_clusters[dev];
     int g = max_tiles < cap ? max_tiles : cap;

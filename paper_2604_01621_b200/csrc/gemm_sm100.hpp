@@ -37,8 +37,7 @@ struct GemmArgs {
   const float* b_scale1;
   // 0: 1-SM kernel. 1: CTA-pair kernel (cta_group::2, 256 x 256 tiles): needs
   // every expert segment (and the shared block) padded to 256 rows and, for
-  // GEMM_PLAIN / GEMM_INT8, B maps with 128-row boxes. 2: 1-SM kernel with
-  // 256 x 256 "unit" tiles (two m-blocks share each B k-block; needs units).
+  // GEMM_PLAIN / GEMM_INT8, B maps with 128-row boxes.
   int pair;
   // segment raster: 0 auto (n-block-major while the segment's A rows <= its
   // B rows), 1 always m-block-major, 2 always n-block-major (experiments)
@@ -48,9 +47,6 @@ struct GemmArgs {
   const int32_t* mb_rows;
   const uint16_t* a_src;  // gather source (a_rows != nullptr)
   int64_t a_ld;
-  // pair == 2 (wide 256 x 256 tiles): unit table and its device-side count
-  const int4* units;
-  const int32_t* unit_count;
 };
 
 // 2-D bf16 TMA map over a row-major [rows][cols] matrix, box = 64 x box_rows,

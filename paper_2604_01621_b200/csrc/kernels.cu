@@ -750,12 +750,10 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
                                                             int2* __restrict__ mb_seg,
                                                             int32_t* __restrict__ src_row,
                                                             int32_t* __restrict__ meta,
-                                                            int32_t* __restrict__ mb_rows,
-                                                            int4* __restrict__ units) {
-  extern __shared__ int32_t sh[];  // [E] padded sizes, [E] offsets, [E] unit offsets
+                                                            int32_t* __restrict__ mb_rows) {
+  extern __shared__ int32_t sh[];  // [E] padded sizes, then [E] offsets
   int32_t* pad = sh;
   int32_t* off = sh + E;
-  int32_t* uoff = sh + 2 * E;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int32_t run = 0;
     int c = 0;
@@ -779,12 +777,10 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int32_t acc = 0, uacc = 0;
+    int32_t acc = 0;
     for (int e = 0; e < E; ++e) {
       off[e] = acc;
-      uoff[e] = uacc;
       acc += pad[e];
-      uacc += (pad[e] / MB_ROWS + 1) / 2;  // units of <= 2 m-blocks (wide GEMM tiles)
     }
     const int32_t routed_mb = acc / MB_ROWS;
     const int32_t shared_mb = shared ? int32_t((T + align - 1) / align * (align / MB_ROWS)) : 0;
@@ -792,8 +788,6 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
     meta[1] = routed_mb;
     meta[2] = acc;
     meta[3] = int32_t(T);
-    meta[4] = uacc + (shared_mb + 1) / 2;  // units (routed, then the shared segment)
-    meta[5] = uacc;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
@@ -806,11 +800,6 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
         const int32_t v = counts[e] - (b - seg.x) * MB_ROWS;
         mb_rows[b] = v < 0 ? 0 : (v > MB_ROWS ? MB_ROWS : v);
       }
-    }
-    if (units) {
-      const int32_t nu = (seg.y + 1) / 2;
-      for (int32_t j = 0; j < nu; ++j)
-        units[uoff[e] + j] = make_int4(seg.x + 2 * j, seg.y - 2 * j >= 2 ? 2 : 1, uoff[e], nu);
     }
     if (src_row)  // padding rows gather token 0 (computed, never read)
       for (int32_t r = off[e] + counts[e]; r < off[e] + pad[e]; ++r) src_row[r] = 0;
@@ -825,11 +814,6 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
         const int64_t v = T - int64_t(b) * MB_ROWS;
         mb_rows[rmb + b] = v < 0 ? 0 : (v > MB_ROWS ? MB_ROWS : int32_t(v));
       }
-    }
-    if (units) {
-      const int32_t u0 = meta[5], nu = (seg.y + 1) / 2;
-      for (int32_t j = threadIdx.x; j < nu; j += blockDim.x)
-        units[u0 + j] = make_int4(rmb + 2 * j, seg.y - 2 * j >= 2 ? 2 : 1, u0, nu);
     }
   }
 }
@@ -1226,16 +1210,16 @@ int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int 
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
                     int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
                     int32_t* scratch, cudaStream_t st, uint8_t* xperm8, float* xscale,
-                    int row_align, int32_t* mb_rows, int4* units) {
+                    int row_align, int32_t* mb_rows) {
   const int pch = permute_chunk(T);
   const int nch = int((T + pch - 1) / pch);
   int32_t* chunk_counts = scratch;
   int32_t* expert_off = scratch + int64_t(nch) * E;
   if (nch > 0)
     permute_count_kernel<<<nch, 256, E * sizeof(int32_t), st>>>(idx, T, E, k, pch, chunk_counts);
-  permute_scan_kernel<<<1, 1024, 3 * E * sizeof(int32_t), st>>>(
+  permute_scan_kernel<<<1, 1024, 2 * E * sizeof(int32_t), st>>>(
       chunk_counts, nch, E, T, shared, row_align, counts, expert_off, mblock_expert, mb_seg, src_row,
-      meta, mb_rows, units);
+      meta, mb_rows);
   // bf16 rows: rank in the scatter kernel, replicate with the bulk-copy kernel
   const bool bulk = xperm != nullptr && xperm8 == nullptr && h % 8 == 0 &&
                     size_t(PB_BUFS) * size_t(h) * 2 <= 48 * 1024;

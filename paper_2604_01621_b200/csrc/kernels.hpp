@@ -55,11 +55,7 @@ int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int 
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
                     int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
                     int32_t* scratch, cudaStream_t st, uint8_t* xperm8 = nullptr,
-                    float* xscale = nullptr, int row_align = 128, int32_t* mb_rows = nullptr,
-                    int4* units = nullptr);
-// units [m-blocks] (nullable): wide-GEMM tiles of <= 2 m-blocks per expert
-// segment, {first m-block, m-blocks, first unit of the segment, units in it};
-// meta[4] = unit count.
+                    float* xscale = nullptr, int row_align = 128, int32_t* mb_rows = nullptr);
 // mb_rows [m-blocks] (nullable): real rows of each m-block (the GEMM epilogues
 // skip the padding rows' stores).
 // row_align (128 or 256): every expert segment, and the shared-expert block,

@@ -68,8 +68,8 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   // (scripts/gpu/r1_ab_pair.sh: 144K vs 158K tokens/s).
   {
     const char* env = std::getenv("DWDP_GEMM_PAIR");
-    gemm_pair_ = env ? (env[0] == '1' ? 1 : env[0] == '2' ? 2 : 0) : 0;
-    row_align_ = gemm_pair_ == 1 ? 256 : 128;
+    gemm_pair_ = env && env[0] == '1' ? 1 : 0;
+    row_align_ = gemm_pair_ ? 256 : 128;
     const char* r = std::getenv("DWDP_RASTER");  // experiments: m / n (default auto)
     raster_ = r ? (r[0] == 'm' ? 1 : r[0] == 'n' ? 2 : 0) : 0;
     const char* g = std::getenv("DWDP_GATHER");  // GEMM1 gathers routed rows from x
@@ -140,7 +140,6 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   mblock_ = static_cast<int32_t*>(dalloc(size_t(max_mb_) * 4, &workspace_bytes));
   mbseg_ = static_cast<int2*>(dalloc(size_t(max_mb_) * sizeof(int2), &workspace_bytes));
   mbrows_ = static_cast<int32_t*>(dalloc(size_t(max_mb_) * 4, &workspace_bytes));
-  units_ = static_cast<int4*>(dalloc(size_t(max_mb_) * sizeof(int4), &workspace_bytes));
   srcrow_ = static_cast<int32_t*>(dalloc(size_t(max_rows_) * 4, &workspace_bytes));
   meta_ = static_cast<int32_t*>(dalloc(16 * 4, &workspace_bytes));
   scratch_ = static_cast<int32_t*>(
@@ -165,7 +164,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   tm_gate_ = tmap(arena_[0], int64_t(nslots_) * f_, h_, 128);
   tm_up_ = tmap(arena_[1], int64_t(nslots_) * f_, h_, 128);
   tm_down_ = tmap(arena_[2], int64_t(nslots_) * h_, f_, 256);
-  if (gemm_pair_ == 1) tm_down_p_ = tmap(arena_[2], int64_t(nslots_) * h_, f_, 128);  // half n-block per CTA
+  if (gemm_pair_) tm_down_p_ = tmap(arena_[2], int64_t(nslots_) * h_, f_, 128);  // half n-block per CTA
   tm_xperm_ = make_tmap_bf16(xperm_, max_rows_, h_, 128);
   tm_h_ = make_tmap_bf16(hbuf_, max_rows_, f_, 128);
   if (fp8_) {
@@ -221,7 +220,7 @@ Ctx::~Ctx() {
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   void* bufs[] = {arena_[0], arena_[1], arena_[2], router_w_, bias_, slot_tab_, logits_, idx_,
                   wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_, pull_items_odd_,
-                  router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_, mbseg_, mbrows_, units_, dep_seg_, srcrow_,
+                  router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_, mbseg_, mbrows_, dep_seg_, srcrow_,
                   sarena_[0], sarena_[1], sarena_[2], h8_, xs_, hs_};
   if (dep_seg_host_) cudaFreeHost(dep_seg_host_);
   for (void* b : bufs)
@@ -604,9 +603,9 @@ void Ctx::route_logits(int wl, const uint16_t* x, int64_t T, cudaStream_t st) {
   const CUtensorMap tx = make_tmap_i8(xq_, 3 * T, h_, 128);
   GemmArgs ga{int(h_), 3 * E_, 0, -1, zeros_, zeros_, rmeta_,
               reinterpret_cast<uint16_t*>(rC_), 3 * int64_t(E_), 3 * T, 0, nullptr,
-              nullptr, nullptr, nullptr, nullptr, gemm_pair_ == 1 ? 1 : 0, 0};
+              nullptr, nullptr, nullptr, nullptr, gemm_pair_, 0};
   const int64_t tiles = (3 * T + 127) / 128 * ((3 * E_ + 255) / 256);
-  const CUtensorMap& tb = gemm_pair_ == 1 ? tm_rw_p_[size_t(wl)] : tm_rw_[size_t(wl)];
+  const CUtensorMap& tb = gemm_pair_ ? tm_rw_p_[size_t(wl)] : tm_rw_[size_t(wl)];
   launch_grouped_gemm(GEMM_INT8, tx, tx, tb, tb, ga, int(std::min<int64_t>(tiles, 1 << 30)), st);
   RouterCfg rc{E_, k_, cfg.scoring, cfg.n_group, cfg.topk_group, cfg.norm_topk, cfg.routed_scale};
   launch_topk(rC_, xe_, router_we_ + size_t(wl) * E_, bias_ + size_t(wl) * E_, logits_, idx_, wts_,
@@ -633,29 +632,25 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   // expert on average (decode batches) the padding would double the MMA and
   // A-tile work of every expert, so such calls use 128-row segments and the
   // 1-SM kernel. (Rank-local choice: the DEP layout keeps row_align_.)
-  // Wide tiles (mode 2) need the permute's unit table and 128-row segments.
-  const bool pair = gemm_pair_ != 0 && T * k_ >= int64_t(E_) * 128;
+  const bool pair = gemm_pair_ && T * k_ >= int64_t(E_) * 128;
   const int align = pair ? row_align_ : 128;
-  const CUtensorMap& tmdown = pair && gemm_pair_ == 1 ? tm_down_p_ : tm_down_;
-  int4* units = pair && gemm_pair_ == 2 ? units_ : nullptr;
+  const CUtensorMap& tmdown = pair ? tm_down_p_ : tm_down_;
   if (fp8_) {
     // W8A8: the permute writes e4m3 copies of every routed row and of the
     // shared-expert rows (after meta[2]) with per-row scales; GEMM1 emits
     // bf16 H, which is re-quantised per row for GEMM2.
     uint8_t* x8 = reinterpret_cast<uint8_t*>(xperm_);
     const int np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_,
-                                  nullptr, meta_, nullptr, scratch_, st, x8, xs_, align, mbrows_, units);
+                                  nullptr, meta_, nullptr, scratch_, st, x8, xs_, align, mbrows_);
     mark(1);
     GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 0, mbseg_,
-                nullptr, xs_, sarena_[0], sarena_[1], pair ? gemm_pair_ : 0, raster_, mbrows_, nullptr, 0,
-                units, meta_ + 4};
+                nullptr, xs_, sarena_[0], sarena_[1], pair ? gemm_pair_ : 0, raster_, mbrows_};
     launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_x8_, tm_x8_, tm_gate_, tm_up_, g1,
                         int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
     launch_quant_rows_fp8(hbuf_, max_rows_, f_, meta_, h8_, hs_, st);
     mark(2);
     GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
-                nullptr, hs_, sarena_[2], nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_, nullptr, 0,
-                units, meta_ + 4};
+                nullptr, hs_, sarena_[2], nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_};
     launch_grouped_gemm(GEMM_PLAIN_FP8, tm_h8_, tm_h8_, tmdown, tmdown, g2,
                         int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
     mark(3);
@@ -664,10 +659,10 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   } else {
   // gather_: GEMM1's producer gathers the routed rows from x (cp.async), the
   // permute only ranks rows and writes src_row (1-SM kernel only)
-  const bool gather = gather_ && !pair;  // 1-SM kernel only
+  const bool gather = gather_ && !pair;
   const int np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_,
                                 gather ? srcrow_ : nullptr, meta_, gather ? nullptr : xperm_, scratch_, st,
-                                nullptr, nullptr, align, mbrows_, units);
+                                nullptr, nullptr, align, mbrows_);
   mark(1);
   const CUtensorMap tm_x = shared_ ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
   // Routed A rows come from the materialised expert-major copy. GEMM1 can
@@ -678,12 +673,11 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   // across the expert's 16 n-block tiles the way the contiguous copy is.
   GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_,
               gather ? srcrow_ : nullptr, nullptr, nullptr, nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_,
-              x, h_, units, meta_ + 4};
+              x, h_};
   launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(2);
   GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
-              nullptr, nullptr, nullptr, nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_, nullptr, 0,
-              units, meta_ + 4};
+              nullptr, nullptr, nullptr, nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_};
   launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tmdown, tmdown, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
   mark(3);
   launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);

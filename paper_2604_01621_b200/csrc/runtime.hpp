@@ -157,12 +157,11 @@ class Ctx {
   float* wts_ = nullptr;
   int2* mbseg_ = nullptr;               // [max_mb] expert segment of each m-block
   int32_t* mbrows_ = nullptr;           // [max_mb] real rows of each m-block
-  int4* units_ = nullptr;               // [max_mb] wide-GEMM units (mode 2)
   int32_t* srcrow_ = nullptr;           // [max_rows] source token of each routed row
   uint16_t *xperm_ = nullptr, *hbuf_ = nullptr;
   CUtensorMap tm_gate_, tm_up_, tm_down_, tm_xperm_, tm_h_;
   CUtensorMap tm_down_p_;          // down arena with 128-row boxes (CTA-pair GEMM2)
-  int gemm_pair_ = 0;              // GemmArgs::pair: 0 1-SM, 1 CTA pair, 2 wide 256x256 tiles
+  int gemm_pair_ = 0;              // GemmArgs::pair: 0 1-SM, 1 CTA pair
   int row_align_ = 128;            // expert segment padding (256 with pairs)
   int raster_ = 0;                 // GemmArgs::raster (DWDP_RASTER experiments)
   bool gather_ = false;            // GEMM1 gathers routed rows from x (DWDP_GATHER=1)
