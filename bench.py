@@ -175,7 +175,7 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=16)
     ap.add_argument("--ref-tokens", type=int, default=16)
     ap.add_argument("--profile", action="store_true", help="1 layer, for ncu captures")
-    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp8"],
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp8", "nvfp4"],
                     help="expert weights: bf16, or e4m3 W8A8 with per-row scales (config 5)")
     ap.add_argument("--decode", type=int, default=0,
                     help="decode phase (config 5): B tokens/rank every step instead of prefill batches")
@@ -235,6 +235,14 @@ def main():
         batches = D.sample_batches(spec, model, world, iters, with_routing=False)
         toks = [[b.tokens[r] for r in range(world)] for b in batches]
     fp8 = args.dtype == "fp8"
+    fp4 = args.dtype == "nvfp4"
+    # bytes per weight element (nvfp4: e2m1 + one e4m3 scale per 16) and the
+    # dense tensor rate relative to bf16 (no measured fp8 / fp4 figure: the
+    # nominal 2x / 4x of the measured sustained bf16 peak)
+    wb = 2.0 if args.dtype == "bf16" else 1.0 if fp8 else 0.5 + 1.0 / 16
+    rate = {"bf16": 1, "fp8": 2, "nvfp4": 4}[args.dtype]
+    if fp4:
+        args.no_dep = True  # the DEP baseline supports bf16 / fp8 experts
 
     cfg = D.DwdpConfig(num_layers=layers, rank=rank, group_size=world, device=local,
                        engine={"pull": D.ENGINE_PULL, "hybrid": D.ENGINE_HYBRID}.get(args.engine,
@@ -244,7 +252,7 @@ def main():
                        ce_inflight=args.ce_inflight,
                        weight_layers=layers if world > 1 else 1, kernel_timing=1,
                        max_tokens=args.decode or args.tokens,
-                       weight_dtype=D.WEIGHT_FP8 if fp8 else D.WEIGHT_BF16)
+                       weight_dtype=D.WEIGHT_NVFP4 if fp4 else D.WEIGHT_FP8 if fp8 else D.WEIGHT_BF16)
     ctx = D.DwdpContext(cfg)
     ctx.init_weights()
     if args.zipf > 0:
@@ -346,7 +354,7 @@ def main():
     if os.path.exists(prof):
         with open(prof) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch")
-    esz = 1 if fp8 else 2
+    esz = wb
     if args.decode:
         # decode: GEMM1 streams the gate/up rows of every touched expert once
         # (+ the shared expert); token rows are noise next to 2*f*h*esz bytes
@@ -357,14 +365,15 @@ def main():
                 "peak_source": pk["source"] + ", HBM copy",
                 "bytes_per_launch": g1_bytes, "tflops": achieved, "traffic": None}
     else:
-        tpk = pk["bf16_tflops_sustained"] * (2 if fp8 else 1)
+        tpk = pk["bf16_tflops_sustained"] * rate
         roof = {"bound": "tensor", "kernel": "grouped GEMM1 (gate/up + SwiGLU, tcgen05)",
                 "achieved": achieved, "peak": tpk, "unit": "TFLOP/s", "frac": achieved / tpk,
-                "peak_source": pk["source"] + (", sustained bf16 x 2 (fp8 dense rate; no measured fp8 figure)"
-                                               if fp8 else ", sustained bf16"),
+                "peak_source": pk["source"] + (f", sustained bf16 x {rate} ({args.dtype} dense rate; no "
+                                               f"measured {args.dtype} figure)" if rate > 1
+                                               else ", sustained bf16"),
                 "flops_per_launch": g1_flops / max(len(recs), 1),
                 "gemm2_tflops": g2_flops / (g2_ns * 1e-9) / 1e12 if g2_ns else None,
-                "traffic": traffic if not fp8 else None}
+                "traffic": traffic if args.dtype == "bf16" else None}
     split = {key: sum(r[key] for r in recs) / 1e6 / max(len(recs), 1)
              for key in ("router_ns", "permute_ns", "gemm1_ns", "gemm2_ns", "combine_ns",
                          "moe_ns", "gate_wait_ns", "prefetch_ns", "merge_ns")}
@@ -465,9 +474,9 @@ def main():
     # bytes over NVLink (900 GB/s per direction), summed over the timed steps
     # with each step's heaviest rank
     f_tok = 2.0 * h * (3 * k * f + 3 * R1["fs"] + R1["E"])
-    p_peak = pk["bf16_tflops_sustained"] * 1e12 * (2 if fp8 else 1)
+    p_peak = pk["bf16_tflops_sustained"] * 1e12 * rate
     c_loc = -(-R1["E"] // world)
-    b_rem = (R1["E"] - c_loc) * 3.0 * h * f * (1 if fp8 else 2) if world > 1 else 0.0
+    b_rem = (R1["E"] - c_loc) * 3.0 * h * f * wb if world > 1 else 0.0
     t_tensor = sum(layers * max(toks[it]) * f_tok / p_peak for it in range(args.warmup, iters))
     t_link = args.steps * layers * b_rem / 900e9
     t_roof = sum(layers * max(max(toks[it]) * f_tok / p_peak, b_rem / 900e9)
@@ -498,8 +507,8 @@ def main():
         if world > 1:
             mean_t = total_tokens / (args.steps * world)
             acct["analytic_compare"] = D.analytic_compare(
-                D.r1_model(layers, 1.0 if fp8 else 2.0),
-                D.GpuSpec(pk["bf16_tflops_sustained"] * 1e12 * (2 if fp8 else 1), pk["hbm_gbs"] * 1e9,
+                D.r1_model(layers, wb),
+                D.GpuSpec(pk["bf16_tflops_sustained"] * 1e12 * rate, pk["hbm_gbs"] * 1e9,
                           900e9),
                 D.build_placement(R1["E"], world), int(mean_t))
             acct["analytic_compare"]["tokens_per_rank"] = mean_t
@@ -508,7 +517,7 @@ def main():
             # the measured DWDP/DEP ratio
             gemm_tf = (g1_flops + g2_flops) / ((g1_ns + g2_ns) * 1e-9) if (g1_ns + g2_ns) else p_peak
             link = pf_bytes / pf_ns * 1e9 if pf_ns else 900e9
-            cal = D.analytic_compare(D.r1_model(layers, 1.0 if fp8 else 2.0),
+            cal = D.analytic_compare(D.r1_model(layers, wb),
                                      D.GpuSpec(gemm_tf, pk["hbm_gbs"] * 1e9, link),
                                      D.build_placement(R1["E"], world), int(mean_t))
             cal.update(gemm_tflops_measured=gemm_tf / 1e12, prefetch_gbs_measured=link / 1e9,
@@ -527,10 +536,11 @@ def main():
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "e4m3 (W8A8, fp32 accumulate)" if fp8 else "bf16",
+            "dtype": ("e4m3 (W8A8, fp32 accumulate)" if fp8 else
+                      "nvfp4 (W4A4 e2m1, e4m3 per-16 scales, fp32 accumulate)" if fp4 else "bf16"),
             "data": "synthetic (counter-hash random-init weights and activations)",
             "config": {"workload": (f"R1 MoE stack, config 5 (decode B={args.decode}, "
-                                    f"{'fp8' if fp8 else 'bf16'}, zipf {args.zipf}, "
+                                    f"{args.dtype}, zipf {args.zipf}, "
                                     f"{'merged' if args.merged else 'split'} fetch)" if args.decode
                                     else "R1 MoE stack, config 2 (all experts local)" if world == 1
                                     else "R1 MoE stack, config 3 (DWDP)"),
@@ -543,7 +553,7 @@ def main():
                        "prefetch_engine": (engines if world > 1 else None),
                        "slice_size": args.slice_size if world > 1 else None,
                        "l2": "inputs larger than L2: {} GB of expert weights per layer".format(
-                           "11.3 (e4m3)" if fp8 else "22.5 (bf16)"),
+                           "11.3 (e4m3)" if fp8 else "6.3 (nvfp4)" if fp4 else "22.5 (bf16)"),
                        "parallelism": f"dwdp{world}"},
             "tokens_per_s_per_gpu": value / world,
             "exposed_prefetch_ms_per_layer": exposed_ms,

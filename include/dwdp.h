@@ -210,6 +210,8 @@ int dwdp_analytic_compare(const dwdp_model_spec* m, const dwdp_gpu_spec* g,
 #define DWDP_SCORING_SIGMOID 1
 #define DWDP_WEIGHT_BF16 0
 #define DWDP_WEIGHT_FP8 1
+#define DWDP_WEIGHT_NVFP4 2 /* W4A4 NVFP4: e2m1 codes, e4m3 scales per 16
+                               elements, fp32 row scales (kind::mxf4nvf4) */
 #define DWDP_ENGINE_COPY 0 /* copy-engine peer copies on a side stream  */
 #define DWDP_ENGINE_PULL 1 /* one-launch SM pull kernel over NVLink      */
 #define DWDP_ENGINE_HYBRID 2 /* odd TDM slices on the pull kernel, even ones
@@ -243,7 +245,8 @@ typedef struct {
                              (GpuSpec::ce_inflight, hwmodel.hpp:33)       */
   int32_t weight_dtype;   /* DWDP_WEIGHT_BF16 / DWDP_WEIGHT_FP8 (e4m3 with
                              per-output-channel fp32 scales; activations
-                             quantised per row, W8A8 on tcgen05 f8f6f4)   */
+                             quantised per row, W8A8 on tcgen05 f8f6f4)
+                             or DWDP_WEIGHT_NVFP4 (W4A4, block scales)    */
   /* synthetic weights */
   uint64_t weight_seed;
   int32_t weight_layers;  /* distinct weight sets; layer l uses l % this   */
@@ -262,7 +265,7 @@ int dwdp_ctx_memory(const dwdp_ctx* ctx, uint64_t* weight_bytes,
 
 /* Multi-process peer wiring (one process per GPU): export this rank's
  * weight-arena IPC handles, then hand every rank's blob to every rank. */
-#define DWDP_IPC_BLOB_BYTES 512
+#define DWDP_IPC_BLOB_BYTES 1024
 int dwdp_ctx_export_ipc(dwdp_ctx* ctx, void* blob /*DWDP_IPC_BLOB_BYTES*/);
 int dwdp_ctx_open_peers(dwdp_ctx* ctx, const void* blobs /*N x BLOB*/);
 /* Single-process alternative: share arenas of contexts on other devices. */
@@ -278,7 +281,9 @@ int dwdp_ctx_set_bias(dwdp_ctx* ctx, const float* bias);
 /* Copy expert `e` tensor t (0 gate, 1 up, 2 down; e == E: shared) of
  * layer `layer` as currently resident for that layer into host memory
  * (raw storage: bf16, or e4m3 bytes for fp8). For fp8, t = 3, 4, 5 read the
- * fp32 per-row scales of gate, up, down. */
+ * fp32 per-row scales of gate, up, down. For nvfp4, t = 0-2 read packed
+ * e2m1 codes (rows x K/2 bytes), t = 3-5 the row scales and t = 6-8 the
+ * e4m3 block scales in the GEMM's 512-byte atom layout. */
 int dwdp_ctx_read_expert(dwdp_ctx* ctx, int layer, int expert, int t,
                          void* host_bf16);
 
@@ -436,6 +441,18 @@ int dwdp_dep_stack_forward(dwdp_ctx* ctx, const void* x, int64_t T, void* y,
  * tcgen05 grouped-GEMM kernel with one group. */
 int dwdp_gemm_bf16(const void* A, const void* B, void* D, int64_t M, int64_t N,
                    int64_t K, void* stream);
+/* NVFP4 quantisation of `rows` bf16 rows of length K (K % 256 == 0):
+ * codes [rows][K/2] (element 2i in the low nibble), e4m3 block scales in
+ * the 512-byte atom layout (ceil(rows/128)*128*K/16 bytes) and fp32 row
+ * scales -- the activation recipe of the nvfp4 MoE path. */
+int dwdp_quant_nvfp4(const void* src, int64_t rows, int64_t K, void* codes,
+                     void* sf, float* row_scale, void* stream);
+/* D[M][N] = (A . B^T) * sa[m] * sb[n] over NVFP4 operands as produced by
+ * dwdp_quant_nvfp4 (N % 256 == 0), bf16 out, on the kind::mxf4nvf4 grouped
+ * GEMM with one group. */
+int dwdp_gemm_nvfp4(const void* A, const void* A_sf, const float* A_scale,
+                    const void* B, const void* B_sf, const float* B_scale,
+                    void* D, int64_t M, int64_t N, int64_t K, void* stream);
 /* Fill a device bf16 buffer with the counter hash (oracle_fill_bf16). */
 int dwdp_fill_bf16(void* dst, int64_t n, uint64_t seed, float scale,
                    void* stream);

@@ -710,19 +710,73 @@ void oracle_quant_row_e4m3(const float* v, int64_t K, uint8_t* q, float* s) {
   *s = sc;
 }
 
-/* Quantise n rows of length K into dequantised-grid floats (q values, not
- * multiplied by the scale) + scales. */
-static void quant_rows_grid(const float* src, int64_t n, int64_t K, float* grid, float* scales,
-                            uint8_t* tmp) {
+/* ---- NVFP4 (W4A4) ------------------------------------------------------
+ * Follows kernels.cu nvfp4_block / nvfp4_fill_rows_kernel / the permute's
+ * NVFP4 branch and the kind::mxf4nvf4 GEMM (gemm_sm100.cu): products of
+ * e2m1 codes times their e4m3 block scales are exact in fp32, sums fp32,
+ * epilogue acc * (s_a * s_b). */
+uint8_t oracle_f32_to_e2m1(float x) {
+  const float a = fabsf(x);
+  const uint8_t c = a <= 0.25f ? 0 : a < 0.75f ? 1 : a <= 1.25f ? 2 : a < 1.75f ? 3
+                  : a <= 2.5f ? 4 : a < 3.5f ? 5 : a <= 5.0f ? 6 : 7;
+  return (uint8_t)((c != 0 && x < 0.0f) ? (c | 8) : c);
+}
+
+float oracle_e2m1_to_f32(uint8_t code) {
+  static const float mag[8] = {0.0f, 0.5f, 1.0f, 1.5f, 2.0f, 3.0f, 4.0f, 6.0f};
+  const float v = mag[code & 7];
+  return (code & 8) ? -v : v;
+}
+
+void oracle_nvfp4_quant_row(const float* v, int64_t K, uint8_t* codes, uint8_t* sf, float* s) {
+  float amax = 0.0f;
+  for (int64_t i = 0; i < K; ++i) amax = fmaxf(amax, fabsf(v[i]));
+  const float rs = amax > 0.0f ? amax / 2688.0f : 1.0f;
+  for (int64_t b = 0; b < K / 16; ++b) {
+    float bmax = 0.0f;
+    for (int i = 0; i < 16; ++i) bmax = fmaxf(bmax, fabsf(v[b * 16 + i]));
+    const uint8_t code = oracle_f32_to_e4m3(bmax / (6.0f * rs));
+    const float ds = oracle_e4m3_to_f32(code) * rs;
+    sf[b] = code;
+    for (int i = 0; i < 8; ++i) {
+      uint8_t lo = 0, hi = 0;
+      if (ds > 0.0f) {
+        lo = oracle_f32_to_e2m1(v[b * 16 + 2 * i] / ds);
+        hi = oracle_f32_to_e2m1(v[b * 16 + 2 * i + 1] / ds);
+      }
+      codes[b * 8 + i] = (uint8_t)(lo | (hi << 4));
+    }
+  }
+  *s = rs;
+}
+
+int64_t oracle_nvfp4_sf_offset(int64_t row, int64_t block, int64_t K) {
+  return ((row >> 7) * (K >> 6) + (block >> 2)) * 512 + (row & 31) * 16 + ((row >> 5) & 3) * 4 +
+         (block & 3);
+}
+
+/* Quantise n rows of length K into dequantised-grid floats (q values times
+ * their block scales for nvfp4; not multiplied by the row scale) + scales. */
+static void quant_rows_grid_mode(int mode, const float* src, int64_t n, int64_t K, float* grid,
+                                 float* scales, uint8_t* tmp) {
   for (int64_t r = 0; r < n; ++r) {
-    oracle_quant_row_e4m3(src + r * K, K, tmp, scales + r);
-    for (int64_t i = 0; i < K; ++i) grid[r * K + i] = oracle_e4m3_to_f32(tmp[i]);
+    if (mode == 2) {
+      uint8_t* sf = tmp + K / 2;
+      oracle_nvfp4_quant_row(src + r * K, K, tmp, sf, scales + r);
+      for (int64_t i = 0; i < K; ++i)
+        grid[r * K + i] = oracle_e2m1_to_f32((uint8_t)((tmp[i / 2] >> (4 * (i & 1))) & 15)) *
+                          oracle_e4m3_to_f32(sf[i / 16]);
+    } else {
+      oracle_quant_row_e4m3(src + r * K, K, tmp, scales + r);
+      for (int64_t i = 0; i < K; ++i) grid[r * K + i] = oracle_e4m3_to_f32(tmp[i]);
+    }
   }
 }
 
-static void ffn_rows_w8a8(const float* gate, const float* up, const float* down, int64_t h,
+static void ffn_rows_w8a8(int mode, const float* gate, const float* up, const float* down, int64_t h,
                           int64_t f, const float* const* xr, const float* scale,
                           float* const* yr, int n) {
+#define quant_rows_grid(...) quant_rows_grid_mode(mode, __VA_ARGS__)
   const int64_t mx = h > f ? h : f;
   uint8_t* tmp = malloc((size_t)mx);
   float* gq = malloc(sizeof(float) * (size_t)(f * h));
@@ -751,6 +805,7 @@ static void ffn_rows_w8a8(const float* gate, const float* up, const float* down,
   }
   free(tmp); free(gq); free(uq); free(dq); free(gs); free(us); free(ds);
   free(xq); free(hb); free(hq);
+#undef quant_rows_grid
 }
 
 static void ffn_rows_bf16(const uint16_t* gate, const uint16_t* up, const uint16_t* down,
@@ -859,7 +914,7 @@ static void expert_job(void* p, int64_t e64) {
         d[i] = bf16_to_f32(a->bd[e][i]);
       }
     }
-    ffn_rows_w8a8(g, u, d, h, f, xr, sc, yr, (int)n);
+    ffn_rows_w8a8(a->cfg->w8a8, g, u, d, h, f, xr, sc, yr, (int)n);
   } else if (resident)
     ffn_rows_bf16(a->bg[e], a->bu[e], a->bd[e], h, f, xr, sc, yr, (int)n, hb);
   else

@@ -145,6 +145,11 @@ class _Oracle(_Api):
         L.oracle_moe_forward_seeded.argtypes = [P, u64, i32, P, i64, P, P, P, P, i32]
         L.oracle_e4m3_encode.argtypes = [P, i64, P]
         L.oracle_quant_row_e4m3.argtypes = [P, i64, P, P]
+        L.oracle_nvfp4_quant_row.argtypes = [P, i64, P, P, P]
+        L.oracle_nvfp4_sf_offset.argtypes = [i64, i64, i64]
+        L.oracle_nvfp4_sf_offset.restype = i64
+        L.oracle_e2m1_to_f32.argtypes = [C.c_uint8]
+        L.oracle_e2m1_to_f32.restype = f32
         L.oracle_moe_forward_explicit.argtypes = [P, P, i64, P, P, P, P, P, P, P, P, P, P, P]
         L.oracle_moe_forward_bf16w.argtypes = [P, P, i64, P, P, P, P, P, P, P, P, i32]
 
@@ -212,6 +217,45 @@ class _Oracle(_Api):
         s = C.c_float()
         self.lib.oracle_quant_row_e4m3(_ptr(v), v.size, _ptr(q), C.byref(s))
         return q, s.value
+
+    def nvfp4_quant_rows(self, v):
+        """NVFP4 rows: codes [R][K/2], linear block scales [R][K/16] (e4m3 codes),
+        row scales [R] -- the device recipe (kernels.cu nvfp4_block)."""
+        v = np.ascontiguousarray(v, np.float32)
+        R, K = v.shape
+        codes = np.zeros((R, K // 2), np.uint8)
+        sf = np.zeros((R, K // 16), np.uint8)
+        s = np.zeros(R, np.float32)
+        for r in range(R):
+            self.lib.oracle_nvfp4_quant_row(_ptr(v[r]), K, _ptr(codes[r]), _ptr(sf[r]),
+                                            s[r:].ctypes.data)
+        return codes, sf, s
+
+    @staticmethod
+    def nvfp4_sf_atoms(sf: np.ndarray) -> np.ndarray:
+        """Linear block scales [R][K/16] -> the device's 512-byte atom layout
+        (ceil(R/128)*128*K/16 bytes; kernels.hpp nvfp4_sf_offset)."""
+        R, nb = sf.shape
+        K = nb * 16
+        rows = np.arange(R, dtype=np.int64)[:, None]
+        b = np.arange(nb, dtype=np.int64)[None, :]
+        off = ((rows >> 7) * (K >> 6) + (b >> 2)) * 512 + (rows & 31) * 16 + ((rows >> 5) & 3) * 4 + (b & 3)
+        out = np.zeros(((R + 127) // 128) * 128 * nb, np.uint8)
+        out[off.reshape(-1)] = sf.reshape(-1)
+        return out
+
+    @staticmethod
+    def nvfp4_dequant(codes: np.ndarray, sf: np.ndarray, s: np.ndarray | None = None) -> np.ndarray:
+        """codes [R][K/2] + linear block scales [R][K/16] (+ row scales) -> fp32."""
+        mag = np.array([0, .5, 1, 1.5, 2, 3, 4, 6], np.float32)
+        lut = np.concatenate([mag, -mag])
+        q = np.stack([codes & 15, codes >> 4], axis=-1).reshape(codes.shape[0], -1)
+        v = lut[q]
+        e = (sf >> 3) & 15
+        m = (sf & 7).astype(np.float32)
+        d = np.where(e > 0, (1 + m / 8) * np.exp2(e.astype(np.float32) - 7), m * 2.0 ** -9).astype(np.float32)
+        v = v * np.repeat(d, 16, axis=1)
+        return v if s is None else v * s[:, None]
 
     def moe_forward_seeded(self, cfg: MoeConfig, base: int, layer: int, x_bf16: np.ndarray,
                            T: int, bias: np.ndarray | None, nthreads: int = 0):

@@ -12,9 +12,9 @@ i32, i64, u64, f32, f64, sz = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_d
 P = C.c_void_p
 
 DWDP_OK, DWDP_ERR_CONFIG, DWDP_ERR_INVARIANT, DWDP_ERR_CUDA = 0, 2, 3, 4
-IPC_BLOB_BYTES = 512
+IPC_BLOB_BYTES = 1024
 ENGINE_COPY, ENGINE_PULL, ENGINE_HYBRID = 0, 1, 2
-WEIGHT_BF16, WEIGHT_FP8 = 0, 1
+WEIGHT_BF16, WEIGHT_FP8, WEIGHT_NVFP4 = 0, 1, 2
 
 
 class ConfigError(ValueError):
@@ -158,6 +158,8 @@ SIGNATURES = {
     "dwdp_dep_layer_forward": (i32, [P, i32, P, i64, P, i32, P]),
     "dwdp_dep_stack_forward": (i32, [P, P, i64, P, P]),
     "dwdp_gemm_bf16": (i32, [P, P, P, i64, i64, i64, P]),
+    "dwdp_quant_nvfp4": (i32, [P, i64, i64, P, P, P, P]),
+    "dwdp_gemm_nvfp4": (i32, [P, P, P, P, P, P, P, i64, i64, i64, P]),
     "dwdp_fill_bf16": (i32, [P, i64, u64, f32, P]),
 
     "dwdp_report_breakdown": (i32, [P, sz, i32, i32, i32, P, P,

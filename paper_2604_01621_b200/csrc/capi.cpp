@@ -569,36 +569,72 @@ int dwdp_dep_stack_forward(dwdp_ctx* c, const void* x, int64_t T, void* y, void*
   });
 }
 
+namespace {
+// A throwaway context for the kernel-level entry points: the GEMM only needs
+// TMA maps and tables (one per device).
+dwdp::Ctx* tiny_ctx() {
+  static dwdp::Ctx* tiny[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!tiny[dev]) {
+    dwdp_ctx_config cfg{};
+    cfg.num_layers = 1;
+    cfg.num_experts = 1;
+    cfg.hidden = 256;
+    cfg.ffn = 128;
+    cfg.top_k = 1;
+    cfg.scoring = 0;
+    cfg.n_group = 1;
+    cfg.topk_group = 1;
+    cfg.routed_scale = 1.0f;
+    cfg.group_size = 1;
+    cfg.merge_elim = 1;
+    cfg.max_tokens = 1;
+    cfg.weight_layers = 1;
+    cfg.device = dev;
+    tiny[dev] = new dwdp::Ctx(cfg);
+  }
+  return tiny[dev];
+}
+}  // namespace
+
 int dwdp_gemm_bf16(const void* A, const void* B, void* D, int64_t M, int64_t N, int64_t K,
                    void* stream) {
   return guard([&] {
     need(A, "A");
     need(B, "B");
     need(D, "D");
-    // A throwaway context-free path: the kernel only needs TMA maps and tables.
-    static dwdp::Ctx* tiny = nullptr;
-    if (!tiny) {
-      dwdp_ctx_config cfg{};
-      cfg.num_layers = 1;
-      cfg.num_experts = 1;
-      cfg.hidden = 256;
-      cfg.ffn = 128;
-      cfg.top_k = 1;
-      cfg.scoring = 0;
-      cfg.n_group = 1;
-      cfg.topk_group = 1;
-      cfg.routed_scale = 1.0f;
-      cfg.group_size = 1;
-      cfg.merge_elim = 1;
-      cfg.max_tokens = 1;
-      cfg.weight_layers = 1;
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cfg.device = dev;
-      tiny = new dwdp::Ctx(cfg);
-    }
-    tiny->gemm_bf16(static_cast<const uint16_t*>(A), static_cast<const uint16_t*>(B),
-                    static_cast<uint16_t*>(D), M, N, K, static_cast<cudaStream_t>(stream));
+    tiny_ctx()->gemm_bf16(static_cast<const uint16_t*>(A), static_cast<const uint16_t*>(B),
+                          static_cast<uint16_t*>(D), M, N, K, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int dwdp_quant_nvfp4(const void* src, int64_t rows, int64_t K, void* codes, void* sf,
+                     float* row_scale, void* stream) {
+  return guard([&] {
+    need(src, "src");
+    need(codes, "codes");
+    need(sf, "sf");
+    need(row_scale, "row_scale");
+    dwdp::require(rows >= 1 && K > 0 && K % 256 == 0, "quant_nvfp4: need rows >= 1, K % 256 == 0");
+    dwdp::launch_quant_rows_nvfp4(static_cast<const uint16_t*>(src), rows, K, nullptr,
+                                  static_cast<uint8_t*>(codes), static_cast<uint8_t*>(sf), row_scale,
+                                  static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw dwdp::CudaError(cudaGetErrorString(e));
+  });
+}
+
+int dwdp_gemm_nvfp4(const void* A, const void* A_sf, const float* A_scale, const void* B,
+                    const void* B_sf, const float* B_scale, void* D, int64_t M, int64_t N, int64_t K,
+                    void* stream) {
+  return guard([&] {
+    for (const void* p : {A, A_sf, static_cast<const void*>(A_scale), B, B_sf,
+                          static_cast<const void*>(B_scale), static_cast<const void*>(D)})
+      need(p, "operand");
+    tiny_ctx()->gemm_nvfp4(static_cast<const uint8_t*>(A), static_cast<const uint8_t*>(A_sf), A_scale,
+                           static_cast<const uint8_t*>(B), static_cast<const uint8_t*>(B_sf), B_scale,
+                           static_cast<uint16_t*>(D), M, N, K, static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -97,6 +97,7 @@ void Ctx::dep_init(const void* unique_id) {
     ~DG() { cudaSetDevice(prev); }
   } dg(cfg.device);
   require(N_ >= 2, "dep: group_size must be >= 2");
+  require(!fp4_, "dep: the DEP baseline supports bf16 and fp8 experts (not nvfp4)");
   require(E_ % N_ == 0, "dep: group_size must divide num_experts");
   require(nccl_ == nullptr, "dep: already initialised");
   NcclId id;

@@ -45,6 +45,18 @@ constexpr int A_STAGE = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE = BN * BK * 2;  // 32 KB
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
 constexpr uint32_t TMEM_COLS = 512;
+// NVFP4 modes (kind::mxf4nvf4 block16): a 128-byte smem row holds 256 e2m1
+// elements, so one stage carries 4x the K of a bf16 stage; 3 stages plus the
+// e4m3 block scales (A: 128 rows x 16 = 2 KB, B: 256 rows x 16 = 4 KB).
+// TMEM: two overlapping accumulators (columns [0,256) and [192,448)) and the
+// block scales of one k-block at [448,512); the epilogue drains the 64
+// shared columns first and releases them early (tpart), so the next tile's
+// MMAs start while the rest of the tile is still being stored.
+constexpr int FP4_STAGES = 3;
+constexpr int SFA_STAGE = 2048, SFB_STAGE = 4096;
+constexpr int SMEM_BYTES4 =
+    FP4_STAGES * (A_STAGE + B_STAGE + SFA_STAGE + SFB_STAGE) + 1024 + 256;
+constexpr uint32_t FP4_ACC1 = 192, TM_SFA = 448, TM_SFB = 464;
 
 // ---------------------------------------------------------------- PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -135,13 +147,23 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 // Kernel modes: SwiGLU-fused bf16 (GEMM1), plain bf16 (GEMM2), the exact
 // int8 x int8 -> int32 mode of the router (kind::i8, order-free accumulation),
 // and the W8A8 e4m3 modes (kind::f8f6f4, scales applied in the epilogue).
-constexpr int kSwiGLU = 0, kPlain = 1, kInt8 = 2, kSwiGLU8 = 3, kPlain8 = 4;
+constexpr int kSwiGLU = 0, kPlain = 1, kInt8 = 2, kSwiGLU8 = 3, kPlain8 = 4, kSwiGLU4 = 5,
+              kPlain4 = 6;
+template <int MODE>
+__host__ __device__ constexpr bool is_fp4() {
+  return MODE == kSwiGLU4 || MODE == kPlain4;
+}
 // Instruction descriptor, both operands K-major, M=128, N=256:
 //   f16 kind:    bf16 x bf16 -> fp32 (c_format 1, a/b_format 1 = BF16)
 //   i8 kind:     s8 x s8 -> s32      (c_format 2, a/b_format 1 = signed)
 //   f8f6f4 kind: e4m3 x e4m3 -> fp32 (c_format 1, a/b_format 0 = E4M3)
+//   mxf4nvf4:    e2m1 x e2m1 -> fp32 with e4m3 block scales (block-scaled
+//                descriptor: a/b_format 1 = E2M1, scale_format 0 = UE4M3,
+//                no c_format field, scale-factor ids 0)
 template <int MODE>
 __host__ __device__ constexpr uint32_t idesc() {
+  if (is_fp4<MODE>())
+    return (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
   return (MODE == kInt8 ? (2u << 4) : (1u << 4)) |
          (MODE == kSwiGLU8 || MODE == kPlain8 ? 0u : (1u << 7) | (1u << 10)) |
          (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -161,6 +183,33 @@ __device__ __forceinline__ void tc_mma_f8(uint32_t d_tmem, uint64_t adesc, uint6
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc_v), "r"(accum));
+}
+
+__device__ __forceinline__ void tc_mma_fp4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc_v, uint32_t accum, uint32_t sfa,
+                                           uint32_t sfb) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, %3, [%5], [%6], p;\n}" ::"r"(
+          d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc_v), "r"(accum), "r"(sfa), "r"(sfb));
+}
+// smem -> TMEM copy of one 512-byte block-scale atom: 32 rows x 128 bit,
+// replicated into the four lane quarters (each lane of quarter q then holds
+// rows lane + 32 j in column j, the layout the block-scaled MMA reads).
+__device__ __forceinline__ void tc_cp_sf(uint32_t taddr, uint32_t saddr) {
+  // no-swizzle K-major descriptor: 8-row core matrices 128 B apart (SBO)
+  const uint64_t d = uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(128 >> 4) << 32) | (uint64_t(1) << 46);
+  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(d) : "memory");
+}
+// 1-D bulk copy global -> shared, completion on an mbarrier.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -194,11 +243,21 @@ __device__ __forceinline__ void tile_coords(int tile, int nb_count, const int2* 
 // Epilogue of one 128 x BN accumulator tile: warp q of the epilogue group
 // owns TMEM lanes (rows) 32q..32q+31; tbase addresses this warp's lanes and
 // the tile's accumulator columns.
+// NVFP4 tiles start at column `start` (mod the tile width) and arrive on
+// `part` after the first two 32-column chunks: those cover the columns the
+// other accumulator overlaps.
 template <int MODE>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb, uint32_t tbase, int q,
-                                              int lane) {
-  constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8;
-  constexpr bool FP8 = MODE == kSwiGLU8 || MODE == kPlain8;
+                                              int lane, int start = 0, uint64_t* part = nullptr) {
+  constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8 || MODE == kSwiGLU4;
+  constexpr bool FP8 = MODE == kSwiGLU8 || MODE == kPlain8 || is_fp4<MODE>();  // scaled epilogue
+  auto release = [&](int i) {
+    if (part != nullptr && i == 1) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(part);
+    }
+  };
   const int64_t row = int64_t(mb) * BM + q * 32 + lane;
   const bool store = row < p.m_limit && (p.mb_rows == nullptr || q * 32 + lane < p.mb_rows[mb]);
   // fp8: per-row activation scale x per-output-channel weight scale
@@ -234,51 +293,55 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
   } else if (SWIGLU) {
     uint16_t* out = p.D + row * p.ldd + nb * 128;
 #pragma unroll 1
-    for (int c = 0; c < 128; c += 32) {
+    for (int i = 0; i < 4; ++i) {
+      const int c = (start + 32 * i) & 127;
       float g[32], u[32];
       tmem_ld32(tbase + c, g);
       tmem_ld32(tbase + 128 + c, u);
       if (FP8) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          g[i] *= sa * __ldg(sb0 + c + i);
-          u[i] *= sa * __ldg(sb1 + c + i);
+        for (int j = 0; j < 32; ++j) {
+          g[j] *= sa * __ldg(sb0 + c + j);
+          u[j] *= sa * __ldg(sb1 + c + j);
         }
       }
       uint32_t pk[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float g0 = g[2 * i], g1 = g[2 * i + 1];
-        const float h0 = __fdividef(g0, 1.0f + __expf(-g0)) * u[2 * i];
-        const float h1 = __fdividef(g1, 1.0f + __expf(-g1)) * u[2 * i + 1];
-        pk[i] = pack_bf16(h0, h1);
+      for (int j = 0; j < 16; ++j) {
+        const float g0 = g[2 * j], g1 = g[2 * j + 1];
+        const float h0 = __fdividef(g0, 1.0f + __expf(-g0)) * u[2 * j];
+        const float h1 = __fdividef(g1, 1.0f + __expf(-g1)) * u[2 * j + 1];
+        pk[j] = pack_bf16(h0, h1);
       }
       if (store) {
         uint4* o4 = reinterpret_cast<uint4*>(out + c);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          o4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        for (int w = 0; w < 4; ++w)
+          o4[w] = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
       }
+      release(i);
     }
   } else {
     uint16_t* out = p.D + row * p.ldd + nb * BN;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int i = 0; i < BN / 32; ++i) {
+      const int c = (start + 32 * i) & (BN - 1);
       float v[32];
       tmem_ld32(tbase + c, v);
       if (FP8) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] *= sa * __ldg(sb0 + c + i);
+        for (int j = 0; j < 32; ++j) v[j] *= sa * __ldg(sb0 + c + j);
       }
       uint32_t pk[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+      for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
       if (store) {
         uint4* o4 = reinterpret_cast<uint4*>(out + c);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          o4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        for (int w = 0; w < 4; ++w)
+          o4[w] = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
       }
+      release(i);
     }
   }
 }
@@ -289,20 +352,25 @@ __global__ void __launch_bounds__(256, 1)
                         const __grid_constant__ CUtensorMap tmA2,
                         const __grid_constant__ CUtensorMap tmB0,
                         const __grid_constant__ CUtensorMap tmB1, GemmArgs p) {
+  constexpr bool FP4 = is_fp4<MODE>();
+  constexpr int NST = FP4 ? FP4_STAGES : STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* sB = smem + NST * A_STAGE;
+  uint8_t* sSFA = sB + NST * B_STAGE;                     // NVFP4 only
+  uint8_t* sSFB = sSFA + (FP4 ? NST * SFA_STAGE : 0);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sSFB + (FP4 ? NST * SFB_STAGE : 0));
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tpart = tempty + 2;  // NVFP4: overlapped accumulator columns drained
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tpart + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       // gathering: + one cp.async-completion arrival per producer lane
       mbar_init(&full[s], p.a_rows != nullptr ? 33 : 1);
       mbar_init(&empty[s], 1);
@@ -310,6 +378,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
+      mbar_init(&tpart[a], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -331,12 +400,15 @@ __global__ void __launch_bounds__(256, 1)
 
   const int total_mb = p.meta[0];
   const int routed_mb = p.meta[1];
-  constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8;
+  constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8 || MODE == kSwiGLU4;
   constexpr bool FP8 = MODE == kSwiGLU8 || MODE == kPlain8;
-  constexpr int BKE = (MODE == kInt8 || FP8) ? 128 : 64;  // K elements per 128-byte smem row
+  // K elements per 128-byte smem row, and the TMA column step (map elements)
+  constexpr int BKE = FP4 ? 256 : (MODE == kInt8 || FP8) ? 128 : 64;
+  constexpr int BKC = FP4 ? 128 : BKE;
   const int nb_count = SWIGLU ? p.n_out / 128 : (p.n_out + BN - 1) / BN;
   const int num_tiles = total_mb * nb_count;
   const int kb_count = p.K / BKE;
+  const int64_t sf_chunks = p.K / 64;  // NVFP4: 512-byte scale atoms per 128 rows
 
   if (warp == 0) {  // ------------------ TMA producer (lane 0; all lanes when gathering)
     int s = 0;
@@ -364,13 +436,29 @@ __global__ void __launch_bounds__(256, 1)
       for (int kb = 0; kb < kb_count; ++kb) {
         if (lane == 0) {
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], (gather ? 0 : A_STAGE) + B_STAGE);
-          if (!gather) tma_load_2d(sA + s * A_STAGE, am, &full[s], kb * BKE, arow);
+          mbar_expect_tx(&full[s], (gather ? 0 : A_STAGE) + B_STAGE +
+                                       (FP4 ? SFA_STAGE + SFB_STAGE : 0));
+          if (!gather) tma_load_2d(sA + s * A_STAGE, am, &full[s], kb * BKC, arow);
           if (SWIGLU) {
-            tma_load_2d(sB + s * B_STAGE, &tmB0, &full[s], kb * BKE, brow);
-            tma_load_2d(sB + s * B_STAGE + B_STAGE / 2, &tmB1, &full[s], kb * BKE, brow);
+            tma_load_2d(sB + s * B_STAGE, &tmB0, &full[s], kb * BKC, brow);
+            tma_load_2d(sB + s * B_STAGE + B_STAGE / 2, &tmB1, &full[s], kb * BKC, brow);
           } else {
-            tma_load_2d(sB + s * B_STAGE, &tmB0, &full[s], kb * BKE, brow);
+            tma_load_2d(sB + s * B_STAGE, &tmB0, &full[s], kb * BKC, brow);
+          }
+          if (FP4) {  // block scales: 4 atoms (one per 64-deep MMA) per 128 rows
+            const int64_t ko = int64_t(4 * kb) * 512;
+            bulk_load(sSFA + s * SFA_STAGE, p.a_sf + (int64_t(arow >> 7) * sf_chunks) * 512 + ko,
+                      SFA_STAGE, &full[s]);
+            const int64_t rb = brow >> 7;  // B row block (gate / down rows)
+            if (SWIGLU) {
+              bulk_load(sSFB + s * SFB_STAGE, p.b_sf0 + rb * sf_chunks * 512 + ko, 2048, &full[s]);
+              bulk_load(sSFB + s * SFB_STAGE + 2048, p.b_sf1 + rb * sf_chunks * 512 + ko, 2048,
+                        &full[s]);
+            } else {
+              bulk_load(sSFB + s * SFB_STAGE, p.b_sf0 + rb * sf_chunks * 512 + ko, 2048, &full[s]);
+              bulk_load(sSFB + s * SFB_STAGE + 2048, p.b_sf0 + (rb + 1) * sf_chunks * 512 + ko, 2048,
+                        &full[s]);
+            }
           }
         }
         if (p.a_rows != nullptr) {
@@ -388,7 +476,7 @@ __global__ void __launch_bounds__(256, 1)
           }
           cp_async_arrive_noinc(&full[s]);  // every lane, every stage (count 33)
         }
-        if (++s == STAGES) {
+        if (++s == NST) {
           s = 0;
           ph ^= 1;
         }
@@ -403,8 +491,11 @@ __global__ void __launch_bounds__(256, 1)
         const int a = local & 1;
         const uint32_t aph = (local >> 1) & 1;
         mbar_wait(&tempty[a], aph ^ 1);
+        // NVFP4: the accumulators overlap; the previous tile's epilogue must
+        // have drained the shared columns
+        if (FP4 && local > 0) mbar_wait(&tpart[a ^ 1], ((local - 1) >> 1) & 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + uint32_t(a * BN);
+        const uint32_t d = tmem_base + (FP4 ? uint32_t(a) * FP4_ACC1 : uint32_t(a * BN));
         for (int kb = 0; kb < kb_count; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
@@ -412,6 +503,28 @@ __global__ void __launch_bounds__(256, 1)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           const uint64_t ad = sw128_desc(smem_u32(sA + s * A_STAGE));
           const uint64_t bd = sw128_desc(smem_u32(sB + s * B_STAGE));
+          if (FP4) {
+            // scales of this k-block -> TMEM (tcgen05.cp and tcgen05.mma
+            // execute in issue order, so one TMEM copy of the scales suffices)
+            const uint32_t sa_s = smem_u32(sSFA + s * SFA_STAGE);
+            const uint32_t sb_s = smem_u32(sSFB + s * SFB_STAGE);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              tc_cp_sf(tmem_base + TM_SFA + 4 * k, sa_s + 512 * k);
+              tc_cp_sf(tmem_base + TM_SFB + 8 * k, sb_s + 512 * k);
+              tc_cp_sf(tmem_base + TM_SFB + 8 * k + 4, sb_s + 2048 + 512 * k);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)  // 64 e2m1 (32 B) along K per MMA
+              tc_mma_fp4(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0,
+                         tmem_base + TM_SFA + 4 * k, tmem_base + TM_SFB + 8 * k);
+            tc_commit(&empty[s]);
+            if (++s == NST) {
+              s = 0;
+              ph ^= 1;
+            }
+            continue;
+          }
 #pragma unroll
           for (int k = 0; k < 4; ++k) {  // +32 B along K per MMA (16 bf16 or 32 int8)
             if (MODE == kInt8)
@@ -422,7 +535,7 @@ __global__ void __launch_bounds__(256, 1)
               tc_mma(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0);
           }
           tc_commit(&empty[s]);
-          if (++s == STAGES) {
+          if (++s == NST) {
             s = 0;
             ph ^= 1;
           }
@@ -435,12 +548,17 @@ __global__ void __launch_bounds__(256, 1)
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       int mb, nb;
-        tile_coords(tile, nb_count, p.mb_seg, p.raster, mb, nb);
+      tile_coords(tile, nb_count, p.mb_seg, p.raster, mb, nb);
       const int a = local & 1;
       const uint32_t aph = (local >> 1) & 1;
       mbar_wait(&tfull[a], aph);
       tc_fence_after();
-      epilogue_tile<MODE>(p, mb, nb, tmem_base + (uint32_t(q * 32) << 16) + uint32_t(a * BN), q, lane);
+      const uint32_t lanes = uint32_t(q * 32) << 16;
+      if (FP4)  // accumulator 0 overlaps accumulator 1 in its last 64 columns
+        epilogue_tile<MODE>(p, mb, nb, tmem_base + lanes + uint32_t(a) * FP4_ACC1, q, lane,
+                            a == 0 ? (SWIGLU ? 64 : 192) : 0, &tpart[a]);
+      else
+        epilogue_tile<MODE>(p, mb, nb, tmem_base + lanes + uint32_t(a * BN), q, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[a]);
@@ -779,6 +897,10 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
       cudaFuncSetAttribute(grouped_gemm_kernel<kPlain8>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+      cudaFuncSetAttribute(grouped_gemm_kernel<kSwiGLU4>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES4);
+      cudaFuncSetAttribute(grouped_gemm_kernel<kPlain4>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES4);
       cudaFuncSetAttribute(grouped_gemm_pair_kernel<kSwiGLU>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
       cudaFuncSetAttribute(grouped_gemm_pair_kernel<kPlain>,
@@ -814,6 +936,14 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
     }
   }
   if (max_tiles <= 0) return;
+  if (mode == kSwiGLU4 || mode == kPlain4) {  // NVFP4: 1-SM kernel only
+    const int grid = max_tiles < sms[dev] ? max_tiles : sms[dev];
+    if (mode == kSwiGLU4)
+      grouped_gemm_kernel<kSwiGLU4><<<grid, 256, SMEM_BYTES4, st>>>(a, a2, b0, b1, args);
+    else
+      grouped_gemm_kernel<kPlain4><<<grid, 256, SMEM_BYTES4, st>>>(a, a2, b0, b1, args);
+    return;
+  }
   if (args.pair) {
     const int cap = 2 * pair_clusters[dev];
     int g = max_tiles < cap ? max_tiles : cap;

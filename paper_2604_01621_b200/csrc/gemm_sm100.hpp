@@ -47,6 +47,12 @@ struct GemmArgs {
   const int32_t* mb_rows;
   const uint16_t* a_src;  // gather source (a_rows != nullptr)
   int64_t a_ld;
+  // NVFP4 modes: e4m3 block scales of A ([m-blocks][K/64][512 B] atoms) and
+  // of the B arenas ([slot][rows/128][K/64][512 B]; b_sf1: up rows of
+  // GEMM1); a_scale / b_scale* hold the fp32 row scales.
+  const uint8_t* a_sf;
+  const uint8_t* b_sf0;
+  const uint8_t* b_sf1;
 };
 
 // 2-D bf16 TMA map over a row-major [rows][cols] matrix, box = 64 x box_rows,
@@ -56,7 +62,7 @@ CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int box
 CUtensorMap make_tmap_i8(const void* base, int64_t rows, int64_t cols, int box_rows);
 
 constexpr int GEMM_SWIGLU = 0, GEMM_PLAIN = 1, GEMM_INT8 = 2, GEMM_SWIGLU_FP8 = 3,
-              GEMM_PLAIN_FP8 = 4;
+              GEMM_PLAIN_FP8 = 4, GEMM_SWIGLU_FP4 = 5, GEMM_PLAIN_FP4 = 6;
 
 // a: routed A rows (permuted tokens or H); a2: shared-expert A rows (x);
 // b0: gate (SwiGLU) or down arena; b1: up arena (SwiGLU only).

@@ -151,6 +151,105 @@ __device__ __forceinline__ uint2 quant8(uint4 v, float s) {
   return make_uint2(o[0], o[1]);
 }
 
+// ---------------------------------------------------------------- NVFP4
+// Two-level NVFP4 (W4A4, tcgen05 kind::mxf4nvf4 block16): per row an fp32
+// scale s = absmax / (448 * 6); per 16-element block an e4m3 scale code
+// sf = e4m3(block_absmax / (6 s)); elements q = e2m1(v / (e4m3(sf) * s)),
+// round to nearest even on the e2m1 grid {0, .5, 1, 1.5, 2, 3, 4, 6},
+// saturating. Same float sequence as oracle_nvfp4_quant_row.
+__device__ __forceinline__ float e4m3_to_f32(uint32_t b) {
+  const uint32_t e = (b >> 3) & 0xfu, m = b & 7u;
+  const float v = e ? __uint_as_float(((e + 120u) << 23) | (m << 20)) : float(m) * 0.001953125f;
+  return (b & 0x80u) ? -v : v;
+}
+__device__ __forceinline__ uint32_t f32_to_e2m1(float x) {
+  const float a = fabsf(x);
+  const uint32_t c = a <= 0.25f ? 0u : a < 0.75f ? 1u : a <= 1.25f ? 2u : a < 1.75f ? 3u
+                   : a <= 2.5f ? 4u : a < 3.5f ? 5u : a <= 5.0f ? 6u : 7u;
+  return (c != 0u && x < 0.0f) ? (c | 8u) : c;
+}
+// One 16-element block: packed codes (element 2i in the low nibble of byte
+// i) and the e4m3 block-scale code.
+__device__ __forceinline__ uint2 nvfp4_block(const float* v, float s, uint32_t& sf) {
+  float bmax = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) bmax = fmaxf(bmax, fabsf(v[i]));
+  sf = f32_to_e4m3(__fdiv_rn(bmax, __fmul_rn(6.0f, s)));
+  const float ds = __fmul_rn(e4m3_to_f32(sf), s);
+  uint32_t w[2] = {0u, 0u};
+  if (ds > 0.0f) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i >> 3] |= f32_to_e2m1(__fdiv_rn(v[i], ds)) << (4 * (i & 7));
+  }
+  return make_uint2(w[0], w[1]);
+}
+__device__ __forceinline__ float nvfp4_row_scale(float amax) {
+  return amax > 0.0f ? __fdiv_rn(amax, 2688.0f) : 1.0f;
+}
+__device__ __forceinline__ void unpack_bf16x16(uint4 a, uint4 b, float* v) {
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    v[2 * i] = __uint_as_float(w[i] << 16);
+    v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+
+// Synthetic NVFP4 expert weights: one warp per (slot, row) over the same
+// bf16 counter-hash values as the bf16 init.
+__global__ void __launch_bounds__(256) nvfp4_fill_rows_kernel(uint8_t* __restrict__ dst,
+                                                              uint8_t* __restrict__ sfa,
+                                                              float* __restrict__ scales,
+                                                              const uint64_t* __restrict__ seeds,
+                                                              int nslots, int rows, int64_t K,
+                                                              float scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wid >= int64_t(nslots) * rows) return;
+  const int64_t slot = wid / rows, r = wid - slot * rows;
+  const uint64_t seed = seeds[slot];
+  auto val = [&](int64_t k) { return bf16_f(bf16_bits(hash_val(seed, r * K + k, scale))); };
+  float amax = 0.0f;
+  for (int64_t k = lane; k < K; k += 32) amax = fmaxf(amax, fabsf(val(k)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const float s = nvfp4_row_scale(amax);
+  uint8_t* out = dst + (slot * rows + r) * (K / 2);
+  uint8_t* sf_slot = sfa + slot * int64_t(rows) * (K / 16);
+  for (int64_t b = lane; b < K / 16; b += 32) {
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = val(b * 16 + i);
+    uint32_t sf;
+    *reinterpret_cast<uint2*>(out + b * 8) = nvfp4_block(v, s, sf);
+    sf_slot[nvfp4_sf_offset(r, b, K)] = uint8_t(sf);
+  }
+  if (lane == 0) scales[slot * rows + r] = s;
+}
+
+// bf16 rows (rows < meta[0]*128) -> NVFP4 codes + block scales + row scale.
+__global__ void __launch_bounds__(256) quant_rows_nvfp4_kernel(const uint16_t* __restrict__ src,
+                                                               int64_t max_rows, int64_t K,
+                                                               const int32_t* __restrict__ meta,
+                                                               uint8_t* __restrict__ dst,
+                                                               uint8_t* __restrict__ sfa,
+                                                               float* __restrict__ scales) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t rows = meta ? int64_t(meta[0]) * 128 : max_rows;
+  if (r >= rows) return;
+  const uint4* row = reinterpret_cast<const uint4*>(src + r * K);
+  const float s = nvfp4_row_scale(row_absmax_bf16(row, K / 8, lane));
+  for (int64_t b = lane; b < K / 16; b += 32) {
+    float v[16];
+    unpack_bf16x16(__ldg(row + 2 * b), __ldg(row + 2 * b + 1), v);
+    uint32_t sf;
+    *reinterpret_cast<uint2*>(dst + r * (K / 2) + b * 8) = nvfp4_block(v, s, sf);
+    sfa[nvfp4_sf_offset(r, b, K)] = uint8_t(sf);
+  }
+  if (lane == 0) scales[r] = s;
+}
+
 // H (bf16, rows < meta[0]*128) -> e4m3 + per-row scale (GEMM2's A operand).
 __global__ void __launch_bounds__(256) quant_rows_fp8_kernel(const uint16_t* __restrict__ src,
                                                              int64_t max_rows, int64_t K,
@@ -823,7 +922,7 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
     int64_t h, const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ expert_off,
     int32_t* __restrict__ row_of, int32_t* __restrict__ src_row, uint16_t* __restrict__ xperm,
     uint8_t* __restrict__ xperm8, float* __restrict__ xscale, const int32_t* __restrict__ meta,
-    int shared, int pch) {
+    int shared, int pch, uint8_t* __restrict__ xsf) {
   extern __shared__ int32_t sm[];  // cursor[E], rows[pch * k]
   int32_t* cursor = sm;
   int32_t* rows = sm + E;
@@ -855,6 +954,32 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (xperm8 && xsf) {  // NVFP4: quantise each token row once, write k + shared copies
+    const int32_t shared_row0 = shared ? meta[2] : 0;
+    for (int tl = warp; tl < ntok; tl += blockDim.x >> 5) {
+      const uint4* src = reinterpret_cast<const uint4*>(x + (t0 + tl) * h);
+      const float s = nvfp4_row_scale(row_absmax_bf16(src, h / 8, lane));
+      const int64_t srow = shared_row0 + t0 + tl;
+      for (int64_t b = lane; b < h / 16; b += 32) {
+        float v[16];
+        unpack_bf16x16(__ldg(src + 2 * b), __ldg(src + 2 * b + 1), v);
+        uint32_t sf;
+        const uint2 q = nvfp4_block(v, s, sf);
+        for (int j = 0; j < k; ++j) {
+          const int64_t r = rows[tl * k + j];
+          *reinterpret_cast<uint2*>(xperm8 + r * (h / 2) + b * 8) = q;
+          xsf[nvfp4_sf_offset(r, b, h)] = uint8_t(sf);
+        }
+        if (shared) {
+          *reinterpret_cast<uint2*>(xperm8 + srow * (h / 2) + b * 8) = q;
+          xsf[nvfp4_sf_offset(srow, b, h)] = uint8_t(sf);
+        }
+      }
+      if (lane < k) xscale[rows[tl * k + lane]] = s;
+      if (shared && lane == 0) xscale[srow] = s;
+    }
+    return;
+  }
   if (xperm8) {  // W8A8: quantise each token row once (per-row scale), write k + shared copies
     const int64_t nch = h / 8;
     const int32_t shared_row0 = shared ? meta[2] : 0;
@@ -1210,7 +1335,7 @@ int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int 
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
                     int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
                     int32_t* scratch, cudaStream_t st, uint8_t* xperm8, float* xscale,
-                    int row_align, int32_t* mb_rows) {
+                    int row_align, int32_t* mb_rows, uint8_t* xsf) {
   const int pch = permute_chunk(T);
   const int nch = int((T + pch - 1) / pch);
   int32_t* chunk_counts = scratch;
@@ -1226,7 +1351,7 @@ int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int 
   if (nch > 0)
     permute_scatter_kernel<<<nch, 256, (E + pch * k) * sizeof(int32_t), st>>>(
         idx, x, T, E, k, h, chunk_counts, expert_off, row_of, src_row, bulk ? nullptr : xperm,
-        xperm8, xscale, meta, shared, pch);
+        xperm8, xscale, meta, shared, pch, xsf);
   if (bulk && T > 0) {
     const int per_sm = 5;  // 43 KB of row buffers per CTA
     const int tpc = int(std::max<int64_t>(1, (T + 148 * per_sm - 1) / (148 * per_sm)));
@@ -1242,6 +1367,21 @@ void launch_fp8_fill_rows(uint8_t* dst, float* scales, const uint64_t* seeds, in
   if (warps > 0)
     fp8_fill_rows_kernel<<<unsigned((warps + 7) / 8), 256, 0, st>>>(dst, scales, seeds, nslots, rows,
                                                                    K, scale);
+}
+
+void launch_nvfp4_fill_rows(uint8_t* dst, uint8_t* sf, float* scales, const uint64_t* seeds,
+                            int nslots, int rows, int64_t K, float scale, cudaStream_t st) {
+  const int64_t warps = int64_t(nslots) * rows;
+  if (warps > 0)
+    nvfp4_fill_rows_kernel<<<unsigned((warps + 7) / 8), 256, 0, st>>>(dst, sf, scales, seeds, nslots,
+                                                                     rows, K, scale);
+}
+
+void launch_quant_rows_nvfp4(const uint16_t* src, int64_t max_rows, int64_t K, const int32_t* meta,
+                             uint8_t* dst, uint8_t* sf, float* scales, cudaStream_t st) {
+  if (max_rows > 0)
+    quant_rows_nvfp4_kernel<<<unsigned((max_rows + 7) / 8), 256, 0, st>>>(src, max_rows, K, meta, dst,
+                                                                          sf, scales);
 }
 
 void launch_quant_rows_fp8(const uint16_t* src, int64_t max_rows, int64_t K, const int32_t* meta,

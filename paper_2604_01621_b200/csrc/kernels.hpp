@@ -55,7 +55,8 @@ int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int 
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
                     int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
                     int32_t* scratch, cudaStream_t st, uint8_t* xperm8 = nullptr,
-                    float* xscale = nullptr, int row_align = 128, int32_t* mb_rows = nullptr);
+                    float* xscale = nullptr, int row_align = 128, int32_t* mb_rows = nullptr,
+                    uint8_t* xsf = nullptr);
 // mb_rows [m-blocks] (nullable): real rows of each m-block (the GEMM epilogues
 // skip the padding rows' stores).
 // row_align (128 or 256): every expert segment, and the shared-expert block,
@@ -67,6 +68,30 @@ int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int 
 // over the bf16 counter-hash values (bit-identical to the oracle).
 void launch_fp8_fill_rows(uint8_t* dst, float* scales, const uint64_t* seeds, int nslots, int rows,
                           int64_t K, float scale, cudaStream_t st);
+// NVFP4 (weight_dtype nvfp4): with xsf != nullptr the permute writes packed
+// e2m1 rows (h/2 bytes) to xperm8, their e4m3 block scales to xsf (layout
+// nvfp4_sf_offset) and fp32 row scales to xscale.
+//
+// Block-scale layout of an NVFP4 matrix with K columns: for every 128-row
+// block and every 64-column chunk, one 512-byte atom holding the 4 block
+// scales of each row at (row % 32) * 16 + (row % 128 / 32) * 4 + block % 4 --
+// the layout tcgen05.cp 32x128b.warpx4 expects in shared memory, so the
+// GEMM moves it with plain bulk copies.
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline int64_t nvfp4_sf_offset(int64_t row, int64_t block, int64_t K) {
+  return ((row >> 7) * (K >> 6) + (block >> 2)) * 512 + (row & 31) * 16 + ((row >> 5) & 3) * 4 +
+         (block & 3);
+}
+// NVFP4 expert weights over the bf16 counter-hash values (bit-identical to
+// oracle_nvfp4_quant_row): codes [slot][rows][K/2], block scales
+// [slot][rows*K/16] (atom layout per slot), row scales [slot][rows].
+void launch_nvfp4_fill_rows(uint8_t* dst, uint8_t* sf, float* scales, const uint64_t* seeds,
+                            int nslots, int rows, int64_t K, float scale, cudaStream_t st);
+// bf16 rows (rows < meta[0]*128) -> NVFP4 codes + block scales + row scales.
+void launch_quant_rows_nvfp4(const uint16_t* src, int64_t max_rows, int64_t K, const int32_t* meta,
+                             uint8_t* dst, uint8_t* sf, float* scales, cudaStream_t st);
 // bf16 rows (rows < meta[0]*128) -> e4m3 + per-row scale.
 void launch_quant_rows_fp8(const uint16_t* src, int64_t max_rows, int64_t K, const int32_t* meta,
                            uint8_t* dst, float* scales, cudaStream_t st);

@@ -22,7 +22,7 @@ struct IpcBlob {
   int32_t rank, nslots, c;
   int64_t slot_elems;
   int32_t ntens, reserved;
-  cudaIpcMemHandle_t h[6];
+  cudaIpcMemHandle_t h[9];
 };
 static_assert(sizeof(IpcBlob) <= DWDP_IPC_BLOB_BYTES, "ipc blob too large");
 
@@ -57,10 +57,12 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   h_ = c.hidden;
   f_ = c.ffn;
   shared_ = c.shared_ffn > 0;
-  require(c.weight_dtype == DWDP_WEIGHT_BF16 || c.weight_dtype == DWDP_WEIGHT_FP8,
+  require(c.weight_dtype == DWDP_WEIGHT_BF16 || c.weight_dtype == DWDP_WEIGHT_FP8 ||
+              c.weight_dtype == DWDP_WEIGHT_NVFP4,
           "ctx: unknown weight_dtype");
   fp8_ = c.weight_dtype == DWDP_WEIGHT_FP8;
-  esz_ = fp8_ ? 1 : 2;
+  fp4_ = c.weight_dtype == DWDP_WEIGHT_NVFP4;
+  esz_ = fp8_ || fp4_ ? 1 : 2;
   // The expert GEMMs run on the 1-SM kernel by default. The CTA-pair kernel
   // (cta_group::2, 256-row segments; DWDP_GEMM_PAIR=1) is 2-10% faster per
   // SM clock, but on the power-capped B200 it drew the clock down from ~1.3
@@ -75,11 +77,12 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     const char* g = std::getenv("DWDP_GATHER");  // GEMM1 gathers routed rows from x
     gather_ = g && g[0] == '1';
   }
-  ntens_ = fp8_ ? 6 : 3;
+  ntens_ = fp4_ ? 9 : fp8_ ? 6 : 3;
   require(L_ >= 1, "ctx: num_layers must be >= 1");
   require(E_ >= 1 && E_ <= 512, "ctx: num_experts must be in [1, 512]");
   require(k_ >= 1 && k_ <= 16 && k_ <= E_, "ctx: top_k must be in [1, min(16, E)]");
   require(h_ > 0 && h_ % 256 == 0, "ctx: hidden must be a positive multiple of 256");
+  require(!fp4_ || f_ % 256 == 0, "ctx: nvfp4 needs ffn to be a multiple of 256");
   require(f_ > 0 && f_ % 128 == 0, "ctx: ffn must be a positive multiple of 128");
   require(c.shared_ffn == 0 || c.shared_ffn == c.ffn, "ctx: shared_ffn must be 0 or == ffn");
   require(c.scoring == 0 || c.scoring == 1, "ctx: unknown scoring");
@@ -109,9 +112,12 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   slot_elems_ = f_ * h_;
   for (int t = 0; t < 3; ++t)
     arena_[t] = static_cast<uint16_t*>(dalloc(tsb(t) * uint64_t(nslots_), nullptr));
-  if (fp8_)
+  if (fp8_ || fp4_)
     for (int t = 0; t < 3; ++t)
       sarena_[t] = static_cast<float*>(dalloc(tsb(3 + t) * uint64_t(nslots_), nullptr));
+  if (fp4_)
+    for (int t = 0; t < 3; ++t)
+      sfarena_[t] = static_cast<uint8_t*>(dalloc(tsb(6 + t) * uint64_t(nslots_), nullptr));
   for (int t = 0; t < ntens_; ++t) {
     weight_bytes += tsb(t) * uint64_t(recv_base_);
     recv_bytes += tsb(t) * uint64_t(nslots_ - recv_base_);
@@ -160,10 +166,11 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   zeros_ = static_cast<int32_t*>(dalloc(nz * 4, &workspace_bytes));
   DWDP_CUDA(cudaMemset(zeros_, 0, nz * 4));
 
-  auto tmap = fp8_ ? make_tmap_i8 : make_tmap_bf16;  // e4m3 tiles use the byte map
-  tm_gate_ = tmap(arena_[0], int64_t(nslots_) * f_, h_, 128);
-  tm_up_ = tmap(arena_[1], int64_t(nslots_) * f_, h_, 128);
-  tm_down_ = tmap(arena_[2], int64_t(nslots_) * h_, f_, 256);
+  auto tmap = fp8_ || fp4_ ? make_tmap_i8 : make_tmap_bf16;  // e4m3 / e2m1 tiles use the byte map
+  const int64_t kdiv = fp4_ ? 2 : 1;  // nvfp4: two elements per byte
+  tm_gate_ = tmap(arena_[0], int64_t(nslots_) * f_, h_ / kdiv, 128);
+  tm_up_ = tmap(arena_[1], int64_t(nslots_) * f_, h_ / kdiv, 128);
+  tm_down_ = tmap(arena_[2], int64_t(nslots_) * h_, f_ / kdiv, 256);
   if (gemm_pair_) tm_down_p_ = tmap(arena_[2], int64_t(nslots_) * h_, f_, 128);  // half n-block per CTA
   tm_xperm_ = make_tmap_bf16(xperm_, max_rows_, h_, 128);
   tm_h_ = make_tmap_bf16(hbuf_, max_rows_, f_, 128);
@@ -173,6 +180,15 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     hs_ = static_cast<float*>(dalloc(size_t(max_rows_) * 4, &workspace_bytes));
     tm_x8_ = make_tmap_i8(xperm_, max_rows_, h_, 128);  // X_perm8 reuses the xperm_ bytes
     tm_h8_ = make_tmap_i8(h8_, max_rows_, f_, 128);
+  }
+  if (fp4_) {
+    h8_ = static_cast<uint8_t*>(dalloc(size_t(max_rows_) * f_ / 2, &workspace_bytes));
+    hsf_ = static_cast<uint8_t*>(dalloc(size_t(max_rows_) * f_ / 16, &workspace_bytes));
+    xsf_ = static_cast<uint8_t*>(dalloc(size_t(max_rows_) * h_ / 16, &workspace_bytes));
+    xs_ = static_cast<float*>(dalloc(size_t(max_rows_) * 4, &workspace_bytes));
+    hs_ = static_cast<float*>(dalloc(size_t(max_rows_) * 4, &workspace_bytes));
+    tm_x8_ = make_tmap_i8(xperm_, max_rows_, h_ / 2, 128);  // X_perm4 reuses the xperm_ bytes
+    tm_h8_ = make_tmap_i8(h8_, max_rows_, f_ / 2, 128);
   }
 
   DWDP_CUDA(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
@@ -189,7 +205,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   DWDP_CUDA(cudaEventCreate(&epoch_));
   DWDP_CUDA(cudaEventRecord(epoch_, copy_st_));
   for (auto& ev : moe_done_) DWDP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  for (int t = 0; t < 6; ++t) peer_arena_[t].assign(size_t(N_), nullptr);
+  for (int t = 0; t < 9; ++t) peer_arena_[t].assign(size_t(N_), nullptr);
   resident_parity_.assign(size_t(L_), 0);
   build_copy_plan();
   DWDP_CUDA(cudaDeviceSynchronize());
@@ -221,7 +237,8 @@ Ctx::~Ctx() {
   void* bufs[] = {arena_[0], arena_[1], arena_[2], router_w_, bias_, slot_tab_, logits_, idx_,
                   wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_, pull_items_odd_,
                   router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_, mbseg_, mbrows_, dep_seg_, srcrow_,
-                  sarena_[0], sarena_[1], sarena_[2], h8_, xs_, hs_};
+                  sarena_[0], sarena_[1], sarena_[2], h8_, xs_, hs_, sfarena_[0], sfarena_[1],
+                  sfarena_[2], xsf_, hsf_};
   if (dep_seg_host_) cudaFreeHost(dep_seg_host_);
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -428,7 +445,10 @@ void Ctx::init_weights(float bias_scale) {
       if (shared_) seeds[size_t(shared_base_ + wl)] = tensor_seed(base, wl, E_, t);
     }
     DWDP_CUDA(cudaMemcpy(dseeds, seeds.data(), size_t(owned) * 8, cudaMemcpyHostToDevice));
-    if (fp8_)  // e4m3 rows + per-row scales over the same bf16 values
+    if (fp4_)  // e2m1 codes + block scales + row scales over the same bf16 values
+      launch_nvfp4_fill_rows(tbase(t), sfarena_[t], sarena_[t], dseeds, owned, int(trows(t)),
+                             t == 2 ? f_ : h_, t == 2 ? sf : sh, nullptr);
+    else if (fp8_)  // e4m3 rows + per-row scales over the same bf16 values
       launch_fp8_fill_rows(tbase(t), sarena_[t], dseeds, owned, int(trows(t)), t == 2 ? f_ : h_,
                            t == 2 ? sf : sh, nullptr);
     else
@@ -635,7 +655,30 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   const bool pair = gemm_pair_ && T * k_ >= int64_t(E_) * 128;
   const int align = pair ? row_align_ : 128;
   const CUtensorMap& tmdown = pair ? tm_down_p_ : tm_down_;
-  if (fp8_) {
+  if (fp4_) {
+    // W4A4 NVFP4: the permute writes e2m1 copies of every routed row and of
+    // the shared-expert rows (after meta[2]) with block + row scales; GEMM1
+    // emits bf16 H, which is re-quantised for GEMM2. 1-SM kernel only.
+    uint8_t* x4 = reinterpret_cast<uint8_t*>(xperm_);
+    const int np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_,
+                                  nullptr, meta_, nullptr, scratch_, st, x4, xs_, 128, mbrows_, xsf_);
+    mark(1);
+    GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 0, mbseg_,
+                nullptr, xs_, sarena_[0], sarena_[1], 0, raster_, mbrows_, nullptr, 0,
+                xsf_, sfarena_[0], sfarena_[1]};
+    launch_grouped_gemm(GEMM_SWIGLU_FP4, tm_x8_, tm_x8_, tm_gate_, tm_up_, g1,
+                        int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
+    launch_quant_rows_nvfp4(hbuf_, max_rows_, f_, meta_, h8_, hsf_, hs_, st);
+    mark(2);
+    GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
+                nullptr, hs_, sarena_[2], nullptr, 0, raster_, mbrows_, nullptr, 0,
+                hsf_, sfarena_[2], nullptr};
+    launch_grouped_gemm(GEMM_PLAIN_FP4, tm_h8_, tm_h8_, tm_down_, tm_down_, g2,
+                        int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
+    mark(3);
+    launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
+    launches += 3 + np + 3 + 1;  // router 3, permute, GEMM1 + quant + GEMM2, combine
+  } else if (fp8_) {
     // W8A8: the permute writes e4m3 copies of every routed row and of the
     // shared-expert rows (after meta[2]) with per-row scales; GEMM1 emits
     // bf16 H, which is re-quantised per row for GEMM2.
@@ -823,6 +866,27 @@ void Ctx::gemm_bf16(const uint16_t* A, const uint16_t* B, uint16_t* D, int64_t M
   const CUtensorMap tb = make_tmap_bf16(B, N, K, 256);
   GemmArgs a{int(K), int(N), int(N), 1, tabs, tabs + mb, tabs + mb + 4, D, N, M, 0, nullptr};
   launch_grouped_gemm(GEMM_PLAIN, ta, ta, tb, tb, a, int(mb * (N / 256)), st);
+  ++launches;
+  DWDP_CUDA(cudaGetLastError());
+  DWDP_CUDA(cudaStreamSynchronize(st));
+  cudaFree(tabs);
+}
+
+void Ctx::gemm_nvfp4(const uint8_t* A, const uint8_t* Asf, const float* As, const uint8_t* B,
+                     const uint8_t* Bsf, const float* Bs, uint16_t* D, int64_t M, int64_t N,
+                     int64_t K, cudaStream_t st) {
+  DeviceGuard dg(cfg.device);
+  require(M >= 1 && N > 0 && N % 256 == 0 && K > 0 && K % 256 == 0, "gemm: need N%256==0, K%256==0");
+  const int64_t mb = (M + 127) / 128;
+  int32_t* tabs = static_cast<int32_t*>(dalloc(size_t(mb + 8) * 4, nullptr));
+  DWDP_CUDA(cudaMemsetAsync(tabs, 0, size_t(mb + 8) * 4, st));
+  const int32_t meta[4] = {int32_t(mb), int32_t(mb), int32_t(mb * 128), 0};
+  DWDP_CUDA(cudaMemcpyAsync(tabs + mb + 4, meta, 16, cudaMemcpyHostToDevice, st));
+  const CUtensorMap ta = make_tmap_i8(A, M, K / 2, 128);
+  const CUtensorMap tb = make_tmap_i8(B, N, K / 2, 256);
+  GemmArgs a{int(K), int(N), int(N), 1, tabs, tabs + mb, tabs + mb + 4, D, N, M, 0, nullptr,
+             nullptr, As, Bs, nullptr, 0, 0, nullptr, nullptr, 0, Asf, Bsf, nullptr};
+  launch_grouped_gemm(GEMM_PLAIN_FP4, ta, ta, tb, tb, a, int(mb * (N / 256)), st);
   ++launches;
   DWDP_CUDA(cudaGetLastError());
   DWDP_CUDA(cudaStreamSynchronize(st));

@@ -85,6 +85,9 @@ class Ctx {
   std::vector<Slice> copy_plan() const { return plan_slices_; }
   int resident_parity(int l) const { return resident_parity_.at(size_t(l)); }
 
+  void gemm_nvfp4(const uint8_t* A, const uint8_t* Asf, const float* As, const uint8_t* B,
+                  const uint8_t* Bsf, const float* Bs, uint16_t* D, int64_t M, int64_t N, int64_t K,
+                  cudaStream_t st);
   void gemm_bf16(const uint16_t* A, const uint16_t* B, uint16_t* D, int64_t M, int64_t N,
                  int64_t K, cudaStream_t st);
 
@@ -119,20 +122,28 @@ class Ctx {
   // arena is one IPC object and one prefetched "param" of the copy plan.
   uint16_t* arena_[3] = {nullptr, nullptr, nullptr};
   float* sarena_[3] = {nullptr, nullptr, nullptr};
-  bool fp8_ = false;
+  // nvfp4 (fp4_): arenas 0-2 hold packed e2m1 codes, 3-5 fp32 row scales and
+  // 6-8 the e4m3 block scales (512-byte atoms, kernels.hpp nvfp4_sf_offset)
+  uint8_t* sfarena_[3] = {nullptr, nullptr, nullptr};
+  bool fp8_ = false, fp4_ = false;
   int esz_ = 2, ntens_ = 3;
   int64_t slot_elems_ = 0;
   int nslots_ = 0, shared_base_ = 0, recv_base_ = 0, merge_base_ = 0;
-  std::vector<void*> peer_arena_[6];   // per tensor arena, per peer rank (nullptr for self)
+  std::vector<void*> peer_arena_[9];   // per tensor arena, per peer rank (nullptr for self)
   uint8_t* tbase(int t) const {
-    return t < 3 ? reinterpret_cast<uint8_t*>(arena_[t]) : reinterpret_cast<uint8_t*>(sarena_[t - 3]);
+    return t < 3   ? reinterpret_cast<uint8_t*>(arena_[t])
+           : t < 6 ? reinterpret_cast<uint8_t*>(sarena_[t - 3])
+                   : sfarena_[t - 6];
   }
   int64_t trows(int t) const { return (t % 3) == 2 ? h_ : f_; }  // rows per slot
   uint64_t tsb(int t) const {  // bytes per slot of tensor arena t
-    return t < 3 ? uint64_t(slot_elems_) * uint64_t(esz_) : uint64_t(trows(t)) * 4;
+    if (t < 3) return fp4_ ? uint64_t(slot_elems_) / 2 : uint64_t(slot_elems_) * uint64_t(esz_);
+    if (t < 6) return uint64_t(trows(t)) * 4;
+    return uint64_t(slot_elems_) / 16;  // one e4m3 scale per 16 elements
   }
   // W8A8 activations
-  uint8_t* h8_ = nullptr;               // e4m3 H [max_rows][f]
+  uint8_t* h8_ = nullptr;               // e4m3 H [max_rows][f] (nvfp4: [max_rows][f/2])
+  uint8_t *xsf_ = nullptr, *hsf_ = nullptr;  // nvfp4 block scales of X_perm4 / H4
   float *xs_ = nullptr, *hs_ = nullptr;  // per-row scales of X_perm8 / H8
   CUtensorMap tm_x8_, tm_h8_;
   std::vector<void*> ipc_opened_;

@@ -10,7 +10,7 @@ from dataclasses import asdict, dataclass
 
 import numpy as np
 
-from ._lib import (ENGINE_COPY, IPC_BLOB_BYTES, WEIGHT_FP8, CtxConfigC, LayerRecordC, SliceC, check, lib)
+from ._lib import (ENGINE_COPY, IPC_BLOB_BYTES, WEIGHT_FP8, WEIGHT_NVFP4, CtxConfigC, LayerRecordC, SliceC, check, lib)
 from .planning import Slice
 
 
@@ -119,11 +119,18 @@ class DwdpContext:
         check(lib().dwdp_ctx_set_bias(self.h, b.ctypes.data))
 
     def read_expert(self, layer: int, expert: int, t: int) -> np.ndarray:
-        """Resident copy of tensor t (0 gate, 1 up, 2 down: bf16 bits, or e4m3
-        bytes for fp8 weights; fp8 only: 3/4/5 = their per-row fp32 scales)."""
+        """Resident copy of tensor t (0 gate, 1 up, 2 down: bf16 bits, e4m3
+        bytes for fp8, packed e2m1 codes [rows][K/2] for nvfp4; fp8/nvfp4:
+        3/4/5 = per-row fp32 scales; nvfp4: 6/7/8 = e4m3 block scales in the
+        512-byte atom layout, flat [rows*K/16])."""
         rows, cols = (self.cfg.ffn, self.cfg.hidden) if t % 3 < 2 else (self.cfg.hidden, self.cfg.ffn)
-        if t >= 3:
+        if t >= 6:
+            out = np.zeros(rows * cols // 16, np.uint8)
+        elif t >= 3:
             out = np.zeros(rows, np.float32)
+        elif self.cfg.weight_dtype == WEIGHT_NVFP4:
+            out = np.zeros(rows * cols // 2, np.uint8)
+            cols //= 2
         else:
             out = np.zeros(rows * cols, np.uint8 if self.cfg.weight_dtype == WEIGHT_FP8 else np.uint16)
         check(lib().dwdp_ctx_read_expert(self.h, layer, expert, t, out.ctypes.data))
@@ -240,6 +247,30 @@ def gemm_bf16(A, B, D=None, stream=None):
     N = B.shape[0]
     D = torch.empty((M, N), dtype=torch.bfloat16, device=A.device) if D is None else D
     check(lib().dwdp_gemm_bf16(_ptr(A), _ptr(B), _ptr(D), M, N, K, _stream(stream)))
+    return D
+
+
+def quant_nvfp4(x, stream=None):
+    """NVFP4 rows of a bf16 [R][K] matrix (the activation recipe): codes
+    [R][K/2] uint8, block scales in the 512-byte atom layout, fp32 row scales."""
+    import torch
+    R, K = x.shape
+    codes = torch.empty((R, K // 2), dtype=torch.uint8, device=x.device)
+    sf = torch.zeros(((R + 127) // 128 * 128) * (K // 16), dtype=torch.uint8, device=x.device)
+    s = torch.empty(R, dtype=torch.float32, device=x.device)
+    check(lib().dwdp_quant_nvfp4(_ptr(x), R, K, _ptr(codes), _ptr(sf), _ptr(s), _stream(stream)))
+    return codes, sf, s
+
+
+def gemm_nvfp4(A, B, D=None, stream=None):
+    """D = (A . B^T) * sa * sb over quant_nvfp4 outputs A = (codes, sf, s),
+    B likewise, on the kind::mxf4nvf4 grouped-GEMM kernel (one group)."""
+    import torch
+    (a, asf, as_), (b, bsf, bs) = A, B
+    M, N, K = a.shape[0], b.shape[0], 2 * a.shape[1]
+    D = torch.empty((M, N), dtype=torch.bfloat16, device=a.device) if D is None else D
+    check(lib().dwdp_gemm_nvfp4(_ptr(a), _ptr(asf), _ptr(as_), _ptr(b), _ptr(bsf), _ptr(bs), _ptr(D),
+                                M, N, K, _stream(stream)))
     return D
 
 
