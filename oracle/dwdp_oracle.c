@@ -719,7 +719,7 @@ uint8_t oracle_f32_to_e2m1(float x) {
   const float a = fabsf(x);
   const uint8_t c = a <= 0.25f ? 0 : a < 0.75f ? 1 : a <= 1.25f ? 2 : a < 1.75f ? 3
                   : a <= 2.5f ? 4 : a < 3.5f ? 5 : a <= 5.0f ? 6 : 7;
-  return (uint8_t)((c != 0 && x < 0.0f) ? (c | 8) : c);
+  return (uint8_t)(signbit(x) ? (c | 8) : c); /* sign kept, as cvt.rn.satfinite.e2m1x2 */
 }
 
 float oracle_e2m1_to_f32(uint8_t code) {
@@ -737,12 +737,13 @@ void oracle_nvfp4_quant_row(const float* v, int64_t K, uint8_t* codes, uint8_t* 
     for (int i = 0; i < 16; ++i) bmax = fmaxf(bmax, fabsf(v[b * 16 + i]));
     const uint8_t code = oracle_f32_to_e4m3(bmax / (6.0f * rs));
     const float ds = oracle_e4m3_to_f32(code) * rs;
+    const float inv = ds > 0.0f ? 1.0f / ds : 0.0f;
     sf[b] = code;
     for (int i = 0; i < 8; ++i) {
       uint8_t lo = 0, hi = 0;
       if (ds > 0.0f) {
-        lo = oracle_f32_to_e2m1(v[b * 16 + 2 * i] / ds);
-        hi = oracle_f32_to_e2m1(v[b * 16 + 2 * i + 1] / ds);
+        lo = oracle_f32_to_e2m1(v[b * 16 + 2 * i] * inv);
+        hi = oracle_f32_to_e2m1(v[b * 16 + 2 * i + 1] * inv);
       }
       codes[b * 8 + i] = (uint8_t)(lo | (hi << 4));
     }

@@ -617,10 +617,15 @@ int dwdp_quant_nvfp4(const void* src, int64_t rows, int64_t K, void* codes, void
     need(sf, "sf");
     need(row_scale, "row_scale");
     dwdp::require(rows >= 1 && K > 0 && K % 256 == 0, "quant_nvfp4: need rows >= 1, K % 256 == 0");
+    void* lin = nullptr;
+    if (cudaMalloc(&lin, size_t(rows) * size_t(K / 16)) != cudaSuccess)
+      throw dwdp::CudaError("quant_nvfp4: scratch allocation failed");
     dwdp::launch_quant_rows_nvfp4(static_cast<const uint16_t*>(src), rows, K, nullptr,
-                                  static_cast<uint8_t*>(codes), static_cast<uint8_t*>(sf), row_scale,
-                                  static_cast<cudaStream_t>(stream));
+                                  static_cast<uint8_t*>(codes), static_cast<uint8_t*>(lin),
+                                  static_cast<uint8_t*>(sf), row_scale, static_cast<cudaStream_t>(stream));
     const cudaError_t e = cudaGetLastError();
+    cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    cudaFree(lin);
     if (e != cudaSuccess) throw dwdp::CudaError(cudaGetErrorString(e));
   });
 }

@@ -44,6 +44,8 @@ constexpr int STAGES = 4;
 constexpr int A_STAGE = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE = BN * BK * 2;  // 32 KB
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
+// scaled (fp8 / nvfp4) modes add the tile's weight-row scales (256 fp32)
+constexpr int SMEM_BYTES8 = SMEM_BYTES + 1024;
 constexpr uint32_t TMEM_COLS = 512;
 // NVFP4 modes (kind::mxf4nvf4 block16): a 128-byte smem row holds 256 e2m1
 // elements, so one stage carries 4x the K of a bf16 stage; 3 stages plus the
@@ -55,7 +57,7 @@ constexpr uint32_t TMEM_COLS = 512;
 constexpr int FP4_STAGES = 3;
 constexpr int SFA_STAGE = 2048, SFB_STAGE = 4096;
 constexpr int SMEM_BYTES4 =
-    FP4_STAGES * (A_STAGE + B_STAGE + SFA_STAGE + SFB_STAGE) + 1024 + 256;
+    FP4_STAGES * (A_STAGE + B_STAGE + SFA_STAGE + SFB_STAGE) + 1024 + 256 + 1024;
 constexpr uint32_t FP4_ACC1 = 192, TM_SFA = 448, TM_SFB = 464;
 
 // ---------------------------------------------------------------- PTX
@@ -198,10 +200,22 @@ __device__ __forceinline__ void tc_mma_fp4(uint32_t d_tmem, uint64_t adesc, uint
 // smem -> TMEM copy of one 512-byte block-scale atom: 32 rows x 128 bit,
 // replicated into the four lane quarters (each lane of quarter q then holds
 // rows lane + 32 j in column j, the layout the block-scaled MMA reads).
-__device__ __forceinline__ void tc_cp_sf(uint32_t taddr, uint32_t saddr) {
-  // no-swizzle K-major descriptor: 8-row core matrices 128 B apart (SBO)
-  const uint64_t d = uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(128 >> 4) << 32) | (uint64_t(1) << 46);
+// Its smem descriptor: no-swizzle K-major, 8-row core matrices 128 B apart
+// (SBO), version 1.
+__device__ __forceinline__ uint64_t sf_desc(uint32_t saddr) {
+  return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(128 >> 4) << 32) | (uint64_t(1) << 46);
+}
+__device__ __forceinline__ void tc_cp_sf_d(uint32_t taddr, uint64_t d) {
   asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(d) : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile(
+      "{\n.reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, e;\n}"
+      : "=r"(p));
+  return p != 0;
 }
 // 1-D bulk copy global -> shared, completion on an mbarrier.
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -246,9 +260,13 @@ __device__ __forceinline__ void tile_coords(int tile, int nb_count, const int2* 
 // NVFP4 tiles start at column `start` (mod the tile width) and arrive on
 // `part` after the first two 32-column chunks: those cover the columns the
 // other accumulator overlaps.
+// Scaled modes: `ssc` (optional) holds the tile's weight-row scales in
+// shared memory (SwiGLU: 128 gate then 128 up; plain: 256) and sa_in the
+// row's activation scale, both fetched before the accumulator wait.
 template <int MODE>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb, uint32_t tbase, int q,
-                                              int lane, int start = 0, uint64_t* part = nullptr) {
+                                              int lane, int start = 0, uint64_t* part = nullptr,
+                                              const float* ssc = nullptr, float sa_in = 1.0f) {
   constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8 || MODE == kSwiGLU4;
   constexpr bool FP8 = MODE == kSwiGLU8 || MODE == kPlain8 || is_fp4<MODE>();  // scaled epilogue
   auto release = [&](int i) {
@@ -264,13 +282,22 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
   float sa = 1.0f;
   const float* sb0 = nullptr;
   const float* sb1 = nullptr;
-  if (FP8) {
+  if (FP8 && ssc != nullptr) {
+    sa = sa_in;
+    sb0 = ssc;
+    sb1 = ssc + 128;
+  } else if (FP8) {
     sa = p.a_scale[row];
     const int64_t b0 = int64_t(p.slot_of[p.mblock_expert[mb]]) * p.rows_per_slot +
                        int64_t(nb) * (SWIGLU ? 128 : BN);
     sb0 = p.b_scale0 + b0;
     sb1 = SWIGLU ? p.b_scale1 + b0 : nullptr;
   }
+  // 16-byte scale loads: shared (broadcast) or read-only global
+  auto ld4 = [&](const float* ptr) {
+    return ssc != nullptr ? *reinterpret_cast<const float4*>(ptr)
+                          : __ldg(reinterpret_cast<const float4*>(ptr));
+  };
   if (MODE == kInt8) {
     int32_t* out = reinterpret_cast<int32_t*>(p.D) + row * p.ldd + nb * BN;
     const int cols = p.n_out - nb * BN < BN ? p.n_out - nb * BN : BN;
@@ -298,11 +325,19 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
       float g[32], u[32];
       tmem_ld32(tbase + c, g);
       tmem_ld32(tbase + 128 + c, u);
-      if (FP8) {
+      if (FP8) {  // weight-row scales: 16-byte broadcast loads
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          g[j] *= sa * __ldg(sb0 + c + j);
-          u[j] *= sa * __ldg(sb1 + c + j);
+        for (int j = 0; j < 32; j += 4) {
+          const float4 s0 = ld4(sb0 + c + j);
+          const float4 s1 = ld4(sb1 + c + j);
+          g[j] *= sa * s0.x;
+          g[j + 1] *= sa * s0.y;
+          g[j + 2] *= sa * s0.z;
+          g[j + 3] *= sa * s0.w;
+          u[j] *= sa * s1.x;
+          u[j + 1] *= sa * s1.y;
+          u[j + 2] *= sa * s1.z;
+          u[j + 3] *= sa * s1.w;
         }
       }
       uint32_t pk[16];
@@ -330,7 +365,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
       tmem_ld32(tbase + c, v);
       if (FP8) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] *= sa * __ldg(sb0 + c + j);
+        for (int j = 0; j < 32; j += 4) {
+          const float4 s0 = ld4(sb0 + c + j);
+          v[j] *= sa * s0.x;
+          v[j + 1] *= sa * s0.y;
+          v[j + 2] *= sa * s0.z;
+          v[j + 3] *= sa * s0.w;
+        }
       }
       uint32_t pk[16];
 #pragma unroll
@@ -367,6 +408,7 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* tpart = tempty + 2;  // NVFP4: overlapped accumulator columns drained
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tpart + 2);
+  float* sscale = reinterpret_cast<float*>(tmem_holder + 4);  // [256] scaled modes (16-B aligned)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -482,6 +524,56 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
+  } else if (warp == 1 && FP4) {  // ---------- NVFP4 MMA issuer (whole warp, one elected lane)
+    // Per k-block: 12 smem->TMEM scale copies and 4 block-scaled MMAs. The
+    // warp stays converged and elects once per k-block, and descriptors are
+    // a per-stage base plus immediates, so the issue loop stays shorter than
+    // the 4 MMAs it feeds.
+    int s = 0;
+    uint32_t ph = 0;
+    int local = 0;
+    const uint64_t sfa0 = sf_desc(smem_u32(sSFA)), sfb0 = sf_desc(smem_u32(sSFB));
+    const uint64_t ad0 = sw128_desc(smem_u32(sA)), bd0 = sw128_desc(smem_u32(sB));
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int a = local & 1;
+      mbar_wait(&tempty[a], ((local >> 1) & 1) ^ 1);
+      // the accumulators overlap: the previous tile's epilogue must have
+      // drained the shared columns
+      if (local > 0) mbar_wait(&tpart[a ^ 1], ((local - 1) >> 1) & 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + uint32_t(a) * FP4_ACC1;
+      for (int kb = 0; kb < kb_count; ++kb) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          // descriptor start addresses are in 16-byte units
+          const uint64_t sfa = sfa0 + uint64_t(s * (SFA_STAGE >> 4));
+          const uint64_t sfb = sfb0 + uint64_t(s * (SFB_STAGE >> 4));
+          const uint64_t ad = ad0 + uint64_t(s * (A_STAGE >> 4));
+          const uint64_t bd = bd0 + uint64_t(s * (B_STAGE >> 4));
+          // tcgen05.cp and tcgen05.mma execute in issue order, so one TMEM
+          // copy of the scales suffices
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            tc_cp_sf_d(tmem_base + TM_SFA + 4 * k, sfa + 32 * k);
+            tc_cp_sf_d(tmem_base + TM_SFB + 8 * k, sfb + 32 * k);
+            tc_cp_sf_d(tmem_base + TM_SFB + 8 * k + 4, sfb + 128 + 32 * k);
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k)  // 64 e2m1 (32 B) along K per MMA
+            tc_mma_fp4(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0,
+                       tmem_base + TM_SFA + 4 * k, tmem_base + TM_SFB + 8 * k);
+          tc_commit(&empty[s]);
+        }
+        __syncwarp();
+        if (++s == NST) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      if (elect_one()) tc_commit(&tfull[a]);
+      __syncwarp();
+    }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
       int s = 0;
@@ -491,11 +583,8 @@ __global__ void __launch_bounds__(256, 1)
         const int a = local & 1;
         const uint32_t aph = (local >> 1) & 1;
         mbar_wait(&tempty[a], aph ^ 1);
-        // NVFP4: the accumulators overlap; the previous tile's epilogue must
-        // have drained the shared columns
-        if (FP4 && local > 0) mbar_wait(&tpart[a ^ 1], ((local - 1) >> 1) & 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + (FP4 ? uint32_t(a) * FP4_ACC1 : uint32_t(a * BN));
+        const uint32_t d = tmem_base + uint32_t(a * BN);
         for (int kb = 0; kb < kb_count; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
@@ -503,28 +592,6 @@ __global__ void __launch_bounds__(256, 1)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           const uint64_t ad = sw128_desc(smem_u32(sA + s * A_STAGE));
           const uint64_t bd = sw128_desc(smem_u32(sB + s * B_STAGE));
-          if (FP4) {
-            // scales of this k-block -> TMEM (tcgen05.cp and tcgen05.mma
-            // execute in issue order, so one TMEM copy of the scales suffices)
-            const uint32_t sa_s = smem_u32(sSFA + s * SFA_STAGE);
-            const uint32_t sb_s = smem_u32(sSFB + s * SFB_STAGE);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              tc_cp_sf(tmem_base + TM_SFA + 4 * k, sa_s + 512 * k);
-              tc_cp_sf(tmem_base + TM_SFB + 8 * k, sb_s + 512 * k);
-              tc_cp_sf(tmem_base + TM_SFB + 8 * k + 4, sb_s + 2048 + 512 * k);
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k)  // 64 e2m1 (32 B) along K per MMA
-              tc_mma_fp4(d, ad + 2 * k, bd + 2 * k, idesc<MODE>(), (kb | k) != 0,
-                         tmem_base + TM_SFA + 4 * k, tmem_base + TM_SFB + 8 * k);
-            tc_commit(&empty[s]);
-            if (++s == NST) {
-              s = 0;
-              ph ^= 1;
-            }
-            continue;
-          }
 #pragma unroll
           for (int k = 0; k < 4; ++k) {  // +32 B along K per MMA (16 bf16 or 32 int8)
             if (MODE == kInt8)
@@ -546,17 +613,38 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {  // ------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int local = 0;
+    constexpr bool SCALED = FP8 || FP4;
+    const int et = q * 32 + lane;  // 0..127: this thread's row of the tile
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       int mb, nb;
       tile_coords(tile, nb_count, p.mb_seg, p.raster, mb, nb);
       const int a = local & 1;
       const uint32_t aph = (local >> 1) & 1;
+      // scaled modes: fetch the tile's scales while the MMAs run, so no
+      // global-load latency sits inside the drain of the accumulator
+      float pre0 = 0.0f, pre1 = 0.0f, sa = 1.0f;
+      if (SCALED) {
+        const int64_t b0 = int64_t(p.slot_of[p.mblock_expert[mb]]) * p.rows_per_slot +
+                           int64_t(nb) * (SWIGLU ? 128 : BN);
+        pre0 = __ldg(p.b_scale0 + b0 + et);
+        pre1 = SWIGLU ? __ldg(p.b_scale1 + b0 + et) : __ldg(p.b_scale0 + b0 + 128 + et);
+        sa = __ldg(p.a_scale + int64_t(mb) * BM + et);
+      }
       mbar_wait(&tfull[a], aph);
       tc_fence_after();
+      if (SCALED) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's readers are done
+        sscale[et] = pre0;
+        sscale[128 + et] = pre1;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
       const uint32_t lanes = uint32_t(q * 32) << 16;
       if (FP4)  // accumulator 0 overlaps accumulator 1 in its last 64 columns
         epilogue_tile<MODE>(p, mb, nb, tmem_base + lanes + uint32_t(a) * FP4_ACC1, q, lane,
-                            a == 0 ? (SWIGLU ? 64 : 192) : 0, &tpart[a]);
+                            a == 0 ? (SWIGLU ? 64 : 192) : 0, &tpart[a], sscale, sa);
+      else if (SCALED)
+        epilogue_tile<MODE>(p, mb, nb, tmem_base + lanes + uint32_t(a * BN), q, lane, 0, nullptr,
+                            sscale, sa);
       else
         epilogue_tile<MODE>(p, mb, nb, tmem_base + lanes + uint32_t(a * BN), q, lane);
       tc_fence_before();
@@ -894,9 +982,9 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
       cudaFuncSetAttribute(grouped_gemm_kernel<kInt8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            SMEM_BYTES);
       cudaFuncSetAttribute(grouped_gemm_kernel<kSwiGLU8>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES8);
       cudaFuncSetAttribute(grouped_gemm_kernel<kPlain8>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES8);
       cudaFuncSetAttribute(grouped_gemm_kernel<kSwiGLU4>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES4);
       cudaFuncSetAttribute(grouped_gemm_kernel<kPlain4>,
@@ -968,9 +1056,9 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
   else if (mode == kInt8)
     grouped_gemm_kernel<kInt8><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
   else if (mode == kSwiGLU8)
-    grouped_gemm_kernel<kSwiGLU8><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+    grouped_gemm_kernel<kSwiGLU8><<<grid, 256, SMEM_BYTES8, st>>>(a, a2, b0, b1, args);
   else
-    grouped_gemm_kernel<kPlain8><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+    grouped_gemm_kernel<kPlain8><<<grid, 256, SMEM_BYTES8, st>>>(a, a2, b0, b1, args);
 }
 
 }  // namespace dwdp

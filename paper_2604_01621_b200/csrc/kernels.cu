@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(256) fp8_fill_rows_kernel(uint8_t* __restrict_
 // One warp per bf16 row: per-row e4m3 quantisation (scale = absmax / 448).
 __device__ __forceinline__ float row_absmax_bf16(const uint4* row, int64_t nch, int lane) {
   float amax = 0.0f;
+#pragma unroll 4
   for (int64_t c = lane; c < nch; c += 32) {
     const uint4 v = __ldg(row + c);
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -154,44 +155,94 @@ __device__ __forceinline__ uint2 quant8(uint4 v, float s) {
 // ---------------------------------------------------------------- NVFP4
 // Two-level NVFP4 (W4A4, tcgen05 kind::mxf4nvf4 block16): per row an fp32
 // scale s = absmax / (448 * 6); per 16-element block an e4m3 scale code
-// sf = e4m3(block_absmax / (6 s)); elements q = e2m1(v / (e4m3(sf) * s)),
-// round to nearest even on the e2m1 grid {0, .5, 1, 1.5, 2, 3, 4, 6},
-// saturating. Same float sequence as oracle_nvfp4_quant_row.
+// sf = e4m3(block_absmax / (6 s)); elements q = e2m1(v * rcp(e4m3(sf) * s))
+// with the hardware conversion (cvt.rn.satfinite.e2m1x2.f32: round to
+// nearest even on {0, .5, 1, 1.5, 2, 3, 4, 6}, saturating, sign kept) and a
+// correctly rounded reciprocal. Same float sequence as oracle_nvfp4_quant_row.
+// Work unit: one lane quantises a 64-element group (4 blocks) -> 32 bytes of
+// codes (element 2i in the low nibble of byte i) + one 32-bit word of the 4
+// block scales, which nvfp4_sf_offset keeps contiguous.
 __device__ __forceinline__ float e4m3_to_f32(uint32_t b) {
   const uint32_t e = (b >> 3) & 0xfu, m = b & 7u;
   const float v = e ? __uint_as_float(((e + 120u) << 23) | (m << 20)) : float(m) * 0.001953125f;
   return (b & 0x80u) ? -v : v;
 }
-__device__ __forceinline__ uint32_t f32_to_e2m1(float x) {
-  const float a = fabsf(x);
-  const uint32_t c = a <= 0.25f ? 0u : a < 0.75f ? 1u : a <= 1.25f ? 2u : a < 1.75f ? 3u
-                   : a <= 2.5f ? 4u : a < 3.5f ? 5u : a <= 5.0f ? 6u : 7u;
-  return (c != 0u && x < 0.0f) ? (c | 8u) : c;
+// 8 values -> 8 e2m1 codes, element i in nibble i
+__device__ __forceinline__ uint32_t e2m1x8(const float* v, float inv) {
+  uint32_t out;
+  asm("{\n.reg .b8 b0, b1, b2, b3;\n"
+      "cvt.rn.satfinite.e2m1x2.f32 b0, %2, %1;\n"
+      "cvt.rn.satfinite.e2m1x2.f32 b1, %4, %3;\n"
+      "cvt.rn.satfinite.e2m1x2.f32 b2, %6, %5;\n"
+      "cvt.rn.satfinite.e2m1x2.f32 b3, %8, %7;\n"
+      "mov.b32 %0, {b0, b1, b2, b3};\n}"
+      : "=r"(out)
+      : "f"(__fmul_rn(v[0], inv)), "f"(__fmul_rn(v[1], inv)), "f"(__fmul_rn(v[2], inv)),
+        "f"(__fmul_rn(v[3], inv)), "f"(__fmul_rn(v[4], inv)), "f"(__fmul_rn(v[5], inv)),
+        "f"(__fmul_rn(v[6], inv)), "f"(__fmul_rn(v[7], inv)));
+  return out;
 }
-// One 16-element block: packed codes (element 2i in the low nibble of byte
-// i) and the e4m3 block-scale code.
-__device__ __forceinline__ uint2 nvfp4_block(const float* v, float s, uint32_t& sf) {
-  float bmax = 0.0f;
+// 64 values (4 blocks) -> codes c[0..7] (32 bytes) and the 4 block-scale codes.
+__device__ __forceinline__ uint32_t nvfp4_group(const float* v, float s, uint32_t* c) {
+  const float s6 = __fmul_rn(6.0f, s);
+  uint32_t sfw = 0;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) bmax = fmaxf(bmax, fabsf(v[i]));
-  sf = f32_to_e4m3(__fdiv_rn(bmax, __fmul_rn(6.0f, s)));
-  const float ds = __fmul_rn(e4m3_to_f32(sf), s);
-  uint32_t w[2] = {0u, 0u};
-  if (ds > 0.0f) {
+  for (int b = 0; b < 4; ++b) {
+    float bmax = 0.0f;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) w[i >> 3] |= f32_to_e2m1(__fdiv_rn(v[i], ds)) << (4 * (i & 7));
+    for (int i = 0; i < 16; ++i) bmax = fmaxf(bmax, fabsf(v[16 * b + i]));
+    const uint32_t sf = f32_to_e4m3(__fdiv_rn(bmax, s6));
+    const float ds = __fmul_rn(e4m3_to_f32(sf), s);
+    const float inv = ds > 0.0f ? __frcp_rn(ds) : 0.0f;
+    c[2 * b] = e2m1x8(v + 16 * b, inv);
+    c[2 * b + 1] = e2m1x8(v + 16 * b + 8, inv);
+    sfw |= sf << (8 * b);
   }
-  return make_uint2(w[0], w[1]);
+  return sfw;
 }
 __device__ __forceinline__ float nvfp4_row_scale(float amax) {
   return amax > 0.0f ? __fdiv_rn(amax, 2688.0f) : 1.0f;
 }
-__device__ __forceinline__ void unpack_bf16x16(uint4 a, uint4 b, float* v) {
-  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+// 8 uint4 of bf16 (64 elements) -> floats
+__device__ __forceinline__ void unpack_bf16x64(const uint4* q, float* v) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    v[2 * i] = __uint_as_float(w[i] << 16);
-    v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t w[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[8 * j + 2 * i] = __uint_as_float(w[i] << 16);
+      v[8 * j + 2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+}
+// Block scales go to the atom layout directly (init-time weights) or, on
+// the per-step paths, to a linear [row][K/16] buffer: 4-byte atom stores
+// from scattered rows are partial-sector writes that HBM turns into
+// read-modify-writes; nvfp4_sf_relayout_kernel then builds whole atoms.
+__device__ __forceinline__ void store_group(uint8_t* codes_row, uint8_t* sf, int64_t r, int64_t g, int64_t K,
+                                            const uint32_t* c, uint32_t sfw, bool linear) {
+  uint4* o = reinterpret_cast<uint4*>(codes_row + g * 32);
+  o[0] = make_uint4(c[0], c[1], c[2], c[3]);
+  o[1] = make_uint4(c[4], c[5], c[6], c[7]);
+  *reinterpret_cast<uint32_t*>(sf + (linear ? r * (K / 16) + 4 * g : nvfp4_sf_offset(r, 4 * g, K))) = sfw;
+}
+
+// Linear block scales [rows][K/16] -> 512-byte atoms (rows < meta[0]*128, or
+// all max_rows rows padded to 128 when meta is null); one thread per
+// destination word (the 4 scales of one row and 64-column chunk).
+__global__ void __launch_bounds__(256) nvfp4_sf_relayout_kernel(const uint32_t* __restrict__ lin,
+                                                                uint32_t* __restrict__ atoms,
+                                                                int64_t max_rows, int64_t K,
+                                                                const int32_t* __restrict__ meta) {
+  const int64_t nc = K / 64;
+  const int64_t rows = meta ? int64_t(meta[0]) * 128 : (max_rows + 127) / 128 * 128;
+  const int64_t words = rows * nc;
+  for (int64_t d = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; d < words;
+       d += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t mb = d / (nc * 128), rem = d - mb * nc * 128;
+    const int64_t c = rem >> 7, w = rem & 127;
+    const int64_t r = mb * 128 + (w >> 2) + 32 * (w & 3);
+    atoms[d] = r < max_rows ? __ldg(lin + r * nc + c) : 0u;
   }
 }
 
@@ -214,15 +265,14 @@ __global__ void __launch_bounds__(256) nvfp4_fill_rows_kernel(uint8_t* __restric
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
   const float s = nvfp4_row_scale(amax);
-  uint8_t* out = dst + (slot * rows + r) * (K / 2);
   uint8_t* sf_slot = sfa + slot * int64_t(rows) * (K / 16);
-  for (int64_t b = lane; b < K / 16; b += 32) {
-    float v[16];
+  for (int64_t g = lane; g < K / 64; g += 32) {
+    float v[64];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = val(b * 16 + i);
-    uint32_t sf;
-    *reinterpret_cast<uint2*>(out + b * 8) = nvfp4_block(v, s, sf);
-    sf_slot[nvfp4_sf_offset(r, b, K)] = uint8_t(sf);
+    for (int i = 0; i < 64; ++i) v[i] = val(g * 64 + i);
+    uint32_t c[8];
+    const uint32_t sfw = nvfp4_group(v, s, c);
+    store_group(dst + (slot * rows + r) * (K / 2), sf_slot, r, g, K, c, sfw, false);
   }
   if (lane == 0) scales[slot * rows + r] = s;
 }
@@ -232,20 +282,51 @@ __global__ void __launch_bounds__(256) quant_rows_nvfp4_kernel(const uint16_t* _
                                                                int64_t max_rows, int64_t K,
                                                                const int32_t* __restrict__ meta,
                                                                uint8_t* __restrict__ dst,
-                                                               uint8_t* __restrict__ sfa,
+                                                               uint8_t* __restrict__ sfl,
                                                                float* __restrict__ scales) {
   const int lane = threadIdx.x & 31;
   const int64_t r = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t rows = meta ? int64_t(meta[0]) * 128 : max_rows;
   if (r >= rows) return;
   const uint4* row = reinterpret_cast<const uint4*>(src + r * K);
+  const int64_t ng = K / 64;
+  if (ng <= 32) {  // one group per lane: the row is read once, into registers
+    uint4 q[8];
+    float amax = 0.0f;
+    if (lane < ng) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        q[j] = __ldg(row + 8 * lane + j);
+        const uint32_t w[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          amax = fmaxf(amax, fmaxf(fabsf(__uint_as_float(w[i] << 16)),
+                                   fabsf(__uint_as_float(w[i] & 0xffff0000u))));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const float s = nvfp4_row_scale(amax);
+    if (lane < ng) {
+      float v[64];
+      unpack_bf16x64(q, v);
+      uint32_t c[8];
+      const uint32_t sfw = nvfp4_group(v, s, c);
+      store_group(dst + r * (K / 2), sfl, r, lane, K, c, sfw, true);
+    }
+    if (lane == 0) scales[r] = s;
+    return;
+  }
   const float s = nvfp4_row_scale(row_absmax_bf16(row, K / 8, lane));
-  for (int64_t b = lane; b < K / 16; b += 32) {
-    float v[16];
-    unpack_bf16x16(__ldg(row + 2 * b), __ldg(row + 2 * b + 1), v);
-    uint32_t sf;
-    *reinterpret_cast<uint2*>(dst + r * (K / 2) + b * 8) = nvfp4_block(v, s, sf);
-    sfa[nvfp4_sf_offset(r, b, K)] = uint8_t(sf);
+  for (int64_t g = lane; g < ng; g += 32) {
+    uint4 q[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) q[j] = __ldg(row + 8 * g + j);
+    float v[64];
+    unpack_bf16x64(q, v);
+    uint32_t c[8];
+    const uint32_t sfw = nvfp4_group(v, s, c);
+    store_group(dst + r * (K / 2), sfl, r, g, K, c, sfw, true);
   }
   if (lane == 0) scales[r] = s;
 }
@@ -955,28 +1036,38 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (xperm8 && xsf) {  // NVFP4: quantise each token row once, write k + shared copies
+    // row scales first (warp per token), then one thread per (token,
+    // 64-element group): 8 independent 16-byte loads per thread and
+    // coalesced 32-byte code stores across the CTA
+    float* rs = reinterpret_cast<float*>(rows + pch * k);
     const int32_t shared_row0 = shared ? meta[2] : 0;
     for (int tl = warp; tl < ntok; tl += blockDim.x >> 5) {
-      const uint4* src = reinterpret_cast<const uint4*>(x + (t0 + tl) * h);
-      const float s = nvfp4_row_scale(row_absmax_bf16(src, h / 8, lane));
-      const int64_t srow = shared_row0 + t0 + tl;
-      for (int64_t b = lane; b < h / 16; b += 32) {
-        float v[16];
-        unpack_bf16x16(__ldg(src + 2 * b), __ldg(src + 2 * b + 1), v);
-        uint32_t sf;
-        const uint2 q = nvfp4_block(v, s, sf);
-        for (int j = 0; j < k; ++j) {
-          const int64_t r = rows[tl * k + j];
-          *reinterpret_cast<uint2*>(xperm8 + r * (h / 2) + b * 8) = q;
-          xsf[nvfp4_sf_offset(r, b, h)] = uint8_t(sf);
-        }
-        if (shared) {
-          *reinterpret_cast<uint2*>(xperm8 + srow * (h / 2) + b * 8) = q;
-          xsf[nvfp4_sf_offset(srow, b, h)] = uint8_t(sf);
-        }
+      const float sc = nvfp4_row_scale(row_absmax_bf16(reinterpret_cast<const uint4*>(x + (t0 + tl) * h),
+                                                       h / 8, lane));
+      if (lane == 0) rs[tl] = sc;
+      if (lane < k) xscale[rows[tl * k + lane]] = sc;
+      if (shared && lane == 0) xscale[shared_row0 + t0 + tl] = sc;
+    }
+    __syncthreads();
+    const int ng = int(h / 64);
+    for (int it = threadIdx.x; it < ntok * ng; it += blockDim.x) {
+      const int tl = it / ng, g = it - tl * ng;
+      const uint4* src = reinterpret_cast<const uint4*>(x + (t0 + tl) * h) + 8 * g;
+      uint4 q[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) q[j] = __ldg(src + j);
+      float v[64];
+      unpack_bf16x64(q, v);
+      uint32_t c[8];
+      const uint32_t sfw = nvfp4_group(v, rs[tl], c);
+      for (int j = 0; j < k; ++j) {
+        const int64_t r = rows[tl * k + j];
+        store_group(xperm8 + r * (h / 2), xsf, r, g, h, c, sfw, true);
       }
-      if (lane < k) xscale[rows[tl * k + lane]] = s;
-      if (shared && lane == 0) xscale[srow] = s;
+      if (shared) {
+        const int64_t r = shared_row0 + t0 + tl;
+        store_group(xperm8 + r * (h / 2), xsf, r, g, h, c, sfw, true);
+      }
     }
     return;
   }
@@ -1349,7 +1440,7 @@ int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int 
   const bool bulk = xperm != nullptr && xperm8 == nullptr && h % 8 == 0 &&
                     size_t(PB_BUFS) * size_t(h) * 2 <= 48 * 1024;
   if (nch > 0)
-    permute_scatter_kernel<<<nch, 256, (E + pch * k) * sizeof(int32_t), st>>>(
+    permute_scatter_kernel<<<nch, 256, (E + pch * k + (xsf ? pch : 0)) * sizeof(int32_t), st>>>(
         idx, x, T, E, k, h, chunk_counts, expert_off, row_of, src_row, bulk ? nullptr : xperm,
         xperm8, xscale, meta, shared, pch, xsf);
   if (bulk && T > 0) {
@@ -1377,11 +1468,22 @@ void launch_nvfp4_fill_rows(uint8_t* dst, uint8_t* sf, float* scales, const uint
                                                                      rows, K, scale);
 }
 
+void launch_nvfp4_sf_relayout(const uint8_t* lin, uint8_t* atoms, int64_t max_rows, int64_t K,
+                              const int32_t* meta, cudaStream_t st) {
+  const int64_t words = (max_rows + 127) / 128 * 128 * (K / 64);
+  const int64_t blocks = std::min<int64_t>((words + 255) / 256, 148 * 16);
+  if (blocks > 0)
+    nvfp4_sf_relayout_kernel<<<unsigned(blocks), 256, 0, st>>>(reinterpret_cast<const uint32_t*>(lin),
+                                                               reinterpret_cast<uint32_t*>(atoms),
+                                                               max_rows, K, meta);
+}
+
 void launch_quant_rows_nvfp4(const uint16_t* src, int64_t max_rows, int64_t K, const int32_t* meta,
-                             uint8_t* dst, uint8_t* sf, float* scales, cudaStream_t st) {
-  if (max_rows > 0)
-    quant_rows_nvfp4_kernel<<<unsigned((max_rows + 7) / 8), 256, 0, st>>>(src, max_rows, K, meta, dst,
-                                                                          sf, scales);
+                             uint8_t* dst, uint8_t* sf_lin, uint8_t* sf, float* scales, cudaStream_t st) {
+  if (max_rows <= 0) return;
+  quant_rows_nvfp4_kernel<<<unsigned((max_rows + 7) / 8), 256, 0, st>>>(src, max_rows, K, meta, dst,
+                                                                        sf_lin, scales);
+  launch_nvfp4_sf_relayout(sf_lin, sf, max_rows, K, meta, st);
 }
 
 void launch_quant_rows_fp8(const uint16_t* src, int64_t max_rows, int64_t K, const int32_t* meta,

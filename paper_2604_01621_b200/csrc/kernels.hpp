@@ -69,8 +69,9 @@ int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int 
 void launch_fp8_fill_rows(uint8_t* dst, float* scales, const uint64_t* seeds, int nslots, int rows,
                           int64_t K, float scale, cudaStream_t st);
 // NVFP4 (weight_dtype nvfp4): with xsf != nullptr the permute writes packed
-// e2m1 rows (h/2 bytes) to xperm8, their e4m3 block scales to xsf (layout
-// nvfp4_sf_offset) and fp32 row scales to xscale.
+// e2m1 rows (h/2 bytes) to xperm8, their e4m3 block scales LINEARLY to xsf
+// ([rows][h/16]; launch_nvfp4_sf_relayout builds the GEMM's atoms) and fp32
+// row scales to xscale.
 //
 // Block-scale layout of an NVFP4 matrix with K columns: for every 128-row
 // block and every 64-column chunk, one 512-byte atom holding the 4 block
@@ -89,9 +90,14 @@ inline int64_t nvfp4_sf_offset(int64_t row, int64_t block, int64_t K) {
 // [slot][rows*K/16] (atom layout per slot), row scales [slot][rows].
 void launch_nvfp4_fill_rows(uint8_t* dst, uint8_t* sf, float* scales, const uint64_t* seeds,
                             int nslots, int rows, int64_t K, float scale, cudaStream_t st);
-// bf16 rows (rows < meta[0]*128) -> NVFP4 codes + block scales + row scales.
+// Linear block scales [rows][K/16] -> the atom layout (rows < meta[0]*128;
+// meta == nullptr: all max_rows rows, padded to 128 with zeros).
+void launch_nvfp4_sf_relayout(const uint8_t* lin, uint8_t* atoms, int64_t max_rows, int64_t K,
+                              const int32_t* meta, cudaStream_t st);
+// bf16 rows (rows < meta[0]*128) -> NVFP4 codes + block scales (through the
+// linear scratch sf_lin, [rows][K/16]) + row scales.
 void launch_quant_rows_nvfp4(const uint16_t* src, int64_t max_rows, int64_t K, const int32_t* meta,
-                             uint8_t* dst, uint8_t* sf, float* scales, cudaStream_t st);
+                             uint8_t* dst, uint8_t* sf_lin, uint8_t* sf, float* scales, cudaStream_t st);
 // bf16 rows (rows < meta[0]*128) -> e4m3 + per-row scale.
 void launch_quant_rows_fp8(const uint16_t* src, int64_t max_rows, int64_t K, const int32_t* meta,
                            uint8_t* dst, float* scales, cudaStream_t st);

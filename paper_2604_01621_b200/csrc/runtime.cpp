@@ -185,6 +185,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     h8_ = static_cast<uint8_t*>(dalloc(size_t(max_rows_) * f_ / 2, &workspace_bytes));
     hsf_ = static_cast<uint8_t*>(dalloc(size_t(max_rows_) * f_ / 16, &workspace_bytes));
     xsf_ = static_cast<uint8_t*>(dalloc(size_t(max_rows_) * h_ / 16, &workspace_bytes));
+    sfl_ = static_cast<uint8_t*>(dalloc(size_t(max_rows_) * std::max(h_, f_) / 16, &workspace_bytes));
     xs_ = static_cast<float*>(dalloc(size_t(max_rows_) * 4, &workspace_bytes));
     hs_ = static_cast<float*>(dalloc(size_t(max_rows_) * 4, &workspace_bytes));
     tm_x8_ = make_tmap_i8(xperm_, max_rows_, h_ / 2, 128);  // X_perm4 reuses the xperm_ bytes
@@ -238,7 +239,7 @@ Ctx::~Ctx() {
                   wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_, pull_items_odd_,
                   router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_, mbseg_, mbrows_, dep_seg_, srcrow_,
                   sarena_[0], sarena_[1], sarena_[2], h8_, xs_, hs_, sfarena_[0], sfarena_[1],
-                  sfarena_[2], xsf_, hsf_};
+                  sfarena_[2], xsf_, hsf_, sfl_};
   if (dep_seg_host_) cudaFreeHost(dep_seg_host_);
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -661,14 +662,15 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     // emits bf16 H, which is re-quantised for GEMM2. 1-SM kernel only.
     uint8_t* x4 = reinterpret_cast<uint8_t*>(xperm_);
     const int np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_,
-                                  nullptr, meta_, nullptr, scratch_, st, x4, xs_, 128, mbrows_, xsf_);
+                                  nullptr, meta_, nullptr, scratch_, st, x4, xs_, 128, mbrows_, sfl_);
+    launch_nvfp4_sf_relayout(sfl_, xsf_, max_rows_, h_, meta_, st);
     mark(1);
     GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 0, mbseg_,
                 nullptr, xs_, sarena_[0], sarena_[1], 0, raster_, mbrows_, nullptr, 0,
                 xsf_, sfarena_[0], sfarena_[1]};
     launch_grouped_gemm(GEMM_SWIGLU_FP4, tm_x8_, tm_x8_, tm_gate_, tm_up_, g1,
                         int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
-    launch_quant_rows_nvfp4(hbuf_, max_rows_, f_, meta_, h8_, hsf_, hs_, st);
+    launch_quant_rows_nvfp4(hbuf_, max_rows_, f_, meta_, h8_, sfl_, hsf_, hs_, st);
     mark(2);
     GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
                 nullptr, hs_, sarena_[2], nullptr, 0, raster_, mbrows_, nullptr, 0,
@@ -677,7 +679,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
                         int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
     mark(3);
     launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
-    launches += 3 + np + 3 + 1;  // router 3, permute, GEMM1 + quant + GEMM2, combine
+    launches += 3 + np + 1 + 4 + 1;  // router 3, permute + relayout, GEMM1 + quant 2 + GEMM2, combine
   } else if (fp8_) {
     // W8A8: the permute writes e4m3 copies of every routed row and of the
     // shared-expert rows (after meta[2]) with per-row scales; GEMM1 emits

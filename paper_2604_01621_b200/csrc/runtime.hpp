@@ -143,7 +143,8 @@ class Ctx {
   }
   // W8A8 activations
   uint8_t* h8_ = nullptr;               // e4m3 H [max_rows][f] (nvfp4: [max_rows][f/2])
-  uint8_t *xsf_ = nullptr, *hsf_ = nullptr;  // nvfp4 block scales of X_perm4 / H4
+  uint8_t *xsf_ = nullptr, *hsf_ = nullptr;  // nvfp4 block scales of X_perm4 / H4 (atoms)
+  uint8_t* sfl_ = nullptr;                   // nvfp4 linear block-scale scratch [rows][h/16]
   float *xs_ = nullptr, *hs_ = nullptr;  // per-row scales of X_perm8 / H8
   CUtensorMap tm_x8_, tm_h8_;
   std::vector<void*> ipc_opened_;
