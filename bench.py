@@ -241,8 +241,6 @@ def main():
     # nominal 2x / 4x of the measured sustained bf16 peak)
     wb = 2.0 if args.dtype == "bf16" else 1.0 if fp8 else 0.5 + 1.0 / 16
     rate = {"bf16": 1, "fp8": 2, "nvfp4": 4}[args.dtype]
-    if fp4:
-        args.no_dep = True  # the DEP baseline supports bf16 / fp8 experts
 
     cfg = D.DwdpConfig(num_layers=layers, rank=rank, group_size=world, device=local,
                        engine={"pull": D.ENGINE_PULL, "hybrid": D.ENGINE_HYBRID}.get(args.engine,

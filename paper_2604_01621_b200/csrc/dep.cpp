@@ -97,7 +97,6 @@ void Ctx::dep_init(const void* unique_id) {
     ~DG() { cudaSetDevice(prev); }
   } dg(cfg.device);
   require(N_ >= 2, "dep: group_size must be >= 2");
-  require(!fp4_, "dep: the DEP baseline supports bf16 and fp8 experts (not nvfp4)");
   require(E_ % N_ == 0, "dep: group_size must divide num_experts");
   require(nccl_ == nullptr, "dep: already initialised");
   NcclId id;
@@ -126,14 +125,21 @@ void Ctx::dep_reserve(int64_t rows) {
   dep_cap_rows_ = rows;
   tm_dep_recv_ = make_tmap_bf16(dep_recv_, rows, h_, 128);
   tm_dep_h_ = make_tmap_bf16(dep_h_, rows, f_, 128);
-  if (fp8_) {
-    for (void* b : {static_cast<void*>(dep_h8_), static_cast<void*>(dep_xs_), static_cast<void*>(dep_hs_)})
+  if (fp8_ || fp4_) {
+    for (void* b : {static_cast<void*>(dep_h8_), static_cast<void*>(dep_xs_), static_cast<void*>(dep_hs_),
+                    static_cast<void*>(dep_sfl_), static_cast<void*>(dep_xsf_), static_cast<void*>(dep_hsf_)})
       if (b) cudaFree(b);
-    dep_h8_ = static_cast<uint8_t*>(dalloc(size_t(rows) * f_, nullptr));
+    const int64_t kd = fp4_ ? 2 : 1;  // elements per byte
+    dep_h8_ = static_cast<uint8_t*>(dalloc(size_t(rows) * f_ / kd, nullptr));
     dep_xs_ = static_cast<float*>(dalloc(size_t(rows) * 4, nullptr));
     dep_hs_ = static_cast<float*>(dalloc(size_t(rows) * 4, nullptr));
-    tm_dep_x8_ = make_tmap_i8(dep_recv_, rows, h_, 128);
-    tm_dep_h8_ = make_tmap_i8(dep_h8_, rows, f_, 128);
+    tm_dep_x8_ = make_tmap_i8(dep_recv_, rows, h_ / kd, 128);
+    tm_dep_h8_ = make_tmap_i8(dep_h8_, rows, f_ / kd, 128);
+    if (fp4_) {
+      dep_sfl_ = static_cast<uint8_t*>(dalloc(size_t(rows) * std::max(h_, f_) / 16, nullptr));
+      dep_xsf_ = static_cast<uint8_t*>(dalloc(size_t(rows) * h_ / 16, nullptr));
+      dep_hsf_ = static_cast<uint8_t*>(dalloc(size_t(rows) * f_ / 16, nullptr));
+    }
   }
   const int64_t need_tab = rows / 128 + 16;
   if (need_tab > dep_tab_cap_) {
@@ -182,7 +188,10 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   // fp8: e4m3 send rows + scales, the shared-expert rows after the routed ones
   uint8_t* x8 = reinterpret_cast<uint8_t*>(xperm_);
   int np = 0;
-  if (T > 0 && fp8_)
+  if (T > 0 && fp4_)  // codes + linear block scales + row scales, shared rows after the routed ones
+    np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_,
+                        nullptr, scratch_, st, x8, xs_, row_align_, nullptr, sfl_);
+  else if (T > 0 && fp8_)
     np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_, nullptr, meta_,
                    nullptr, scratch_, st, x8, xs_, row_align_);  // send side: padding unused
   else if (T > 0)
@@ -251,15 +260,28 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
                             cudaMemcpyHostToDevice, st));
   DWDP_CUDA(cudaMemcpyAsync(dep_mbrows_, dep_mbrows_host_, size_t(nblocks + 1) * 4,
                             cudaMemcpyHostToDevice, st));
-  // 3. dispatch all-to-all (bf16 rows, or e4m3 rows + their fp32 scales)
+  // 3. dispatch all-to-all (bf16 rows, e4m3 rows + their fp32 scales, or
+  // e2m1 codes + linear block scales + fp32 row scales)
   const size_t rowel = size_t(h_);
   uint8_t* r8 = reinterpret_cast<uint8_t*>(dep_recv_);
+  const size_t cb = size_t(h_ / 2), sb = size_t(h_ / 16);  // nvfp4 bytes per row: codes, scales
   nccl_check(n.GroupStart(), "ncclGroupStart");
   for (int p = 0; p < N_; ++p) {
     if (p == rank_) continue;
     const size_t so = size_t(send_off[size_t(p)]), sr = size_t(send_rows[size_t(p)]);
     const size_t ro = size_t(recv_off[size_t(p)]), rr = size_t(recv_rows[size_t(p)]);
-    if (fp8_) {
+    if (fp4_) {
+      if (sr) {
+        nccl_check(n.Send(x8 + so * cb, sr * cb, kUint8, p, nccl_, st), "ncclSend");
+        nccl_check(n.Send(sfl_ + so * sb, sr * sb, kUint8, p, nccl_, st), "ncclSend");
+        nccl_check(n.Send(xs_ + so, sr, kFloat32, p, nccl_, st), "ncclSend");
+      }
+      if (rr) {
+        nccl_check(n.Recv(r8 + ro * cb, rr * cb, kUint8, p, nccl_, st), "ncclRecv");
+        nccl_check(n.Recv(dep_sfl_ + ro * sb, rr * sb, kUint8, p, nccl_, st), "ncclRecv");
+        nccl_check(n.Recv(dep_xs_ + ro, rr, kFloat32, p, nccl_, st), "ncclRecv");
+      }
+    } else if (fp8_) {
       if (sr) {
         nccl_check(n.Send(x8 + so * rowel, sr * rowel, kUint8, p, nccl_, st), "ncclSend");
         nccl_check(n.Send(xs_ + so, sr, kFloat32, p, nccl_, st), "ncclSend");
@@ -277,7 +299,11 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   if (send_rows[size_t(rank_)]) {
     const size_t so = size_t(send_off[size_t(rank_)]), ro = size_t(recv_off[size_t(rank_)]);
     const size_t sr = size_t(send_rows[size_t(rank_)]);
-    if (fp8_) {
+    if (fp4_) {
+      DWDP_CUDA(cudaMemcpyAsync(r8 + ro * cb, x8 + so * cb, sr * cb, cudaMemcpyDeviceToDevice, st));
+      DWDP_CUDA(cudaMemcpyAsync(dep_sfl_ + ro * sb, sfl_ + so * sb, sr * sb, cudaMemcpyDeviceToDevice, st));
+      DWDP_CUDA(cudaMemcpyAsync(dep_xs_ + ro, xs_ + so, sr * 4, cudaMemcpyDeviceToDevice, st));
+    } else if (fp8_) {
       DWDP_CUDA(cudaMemcpyAsync(r8 + ro * rowel, x8 + so * rowel, sr * rowel, cudaMemcpyDeviceToDevice, st));
       DWDP_CUDA(cudaMemcpyAsync(dep_xs_ + ro, xs_ + so, sr * 4, cudaMemcpyDeviceToDevice, st));
     } else {
@@ -285,15 +311,28 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
                                 cudaMemcpyDeviceToDevice, st));
     }
   }
-  if (fp8_ && shared_ && T > 0)  // shared-row scales follow the received rows
+  if ((fp8_ || fp4_) && shared_ && T > 0)  // shared-row scales follow the received rows
     DWDP_CUDA(cudaMemcpyAsync(dep_xs_ + routed_rows, xs_ + send_total, size_t(T) * 4,
                               cudaMemcpyDeviceToDevice, st));
+  if (fp4_ && shared_ && T > 0) {  // nvfp4: the shared rows' codes and scales too (one A operand)
+    DWDP_CUDA(cudaMemcpyAsync(r8 + size_t(routed_rows) * cb, x8 + size_t(send_total) * cb, size_t(T) * cb,
+                              cudaMemcpyDeviceToDevice, st));
+    DWDP_CUDA(cudaMemcpyAsync(dep_sfl_ + size_t(routed_rows) * sb, sfl_ + size_t(send_total) * sb,
+                              size_t(T) * sb, cudaMemcpyDeviceToDevice, st));
+  }
+  if (fp4_ && nblocks > 0) launch_nvfp4_sf_relayout(dep_sfl_, dep_xsf_, dep_cap_rows_, h_, dep_tab_, st);
   mark(&rec.comm[1]);
   // 4. expert-parallel grouped GEMMs (+ shared expert on own tokens)
   const int32_t* stab = slot_tab_ + size_t(layer) * 2 * (E_ + 1);
   const int32_t* dmeta = dep_tab_;
   const int32_t* dmb = dep_tab_ + 4;
-  if (nblocks > 0 && fp8_) {
+  if (nblocks > 0 && fp4_) {
+    GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 0, dep_seg_,
+                nullptr, dep_xs_, sarena_[0], sarena_[1], 0, raster_, dep_mbrows_, nullptr, 0,
+                dep_xsf_, sfarena_[0], sfarena_[1]};
+    launch_grouped_gemm(GEMM_SWIGLU_FP4, tm_dep_x8_, tm_dep_x8_, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
+    launch_quant_rows_nvfp4(dep_h_, dep_cap_rows_, f_, dmeta, dep_h8_, dep_sfl_, dep_hsf_, dep_hs_, st);
+  } else if (nblocks > 0 && fp8_) {
     const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_i8(x8 + send_total * h_, T, h_, 128) : tm_dep_x8_;
     GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1, dep_seg_,
                 nullptr, dep_xs_, sarena_[0], sarena_[1], gemm_pair_, raster_, dep_mbrows_};
@@ -306,7 +345,12 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
     launch_grouped_gemm(GEMM_SWIGLU, tm_dep_recv_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
   }
   mark(&rec.k[2]);
-  if (nblocks > 0 && fp8_) {
+  if (nblocks > 0 && fp4_) {
+    GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
+                nullptr, dep_hs_, sarena_[2], nullptr, 0, raster_, dep_mbrows_, nullptr, 0,
+                dep_hsf_, sfarena_[2], nullptr};
+    launch_grouped_gemm(GEMM_PLAIN_FP4, tm_dep_h8_, tm_dep_h8_, tm_down_, tm_down_, g2, int(nblocks * (h_ / 256)), st);
+  } else if (nblocks > 0 && fp8_) {
     GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
                 nullptr, dep_hs_, sarena_[2], nullptr, gemm_pair_, raster_, dep_mbrows_};
     const CUtensorMap& tmd8 = gemm_pair_ ? tm_down_p_ : tm_down_;
@@ -338,7 +382,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   // 6. weighted combine (shared rows follow the routed rows of the receive buffer)
   launch_combine(xperm_, row_of_, wts_, shared_ ? dep_recv_ + routed_rows * h_ : nullptr, nullptr,
                  residual ? x : nullptr, y, T, k_, h_, st);
-  launches += (T > 0 ? 3 : 0) + np + (nblocks > 0 ? (fp8_ ? 3 : 2) : 0) + 1;
+  launches += (T > 0 ? 3 : 0) + np + (nblocks > 0 ? (fp4_ ? 5 : fp8_ ? 3 : 2) : 0) + 1;
   DWDP_CUDA(cudaGetLastError());
   DWDP_CUDA(cudaEventRecord(rec.moe_end, st));
   rec.rows = routed_rows;

@@ -223,7 +223,8 @@ Ctx::~Ctx() {
   for (void* b : {static_cast<void*>(dep_recv_), static_cast<void*>(dep_h_),
                   static_cast<void*>(dep_counts_all_), static_cast<void*>(dep_tab_),
                   static_cast<void*>(dep_mbrows_), static_cast<void*>(dep_h8_),
-                  static_cast<void*>(dep_xs_), static_cast<void*>(dep_hs_)})
+                  static_cast<void*>(dep_xs_), static_cast<void*>(dep_hs_), static_cast<void*>(dep_sfl_),
+                  static_cast<void*>(dep_xsf_), static_cast<void*>(dep_hsf_)})
     if (b) cudaFree(b);
   if (dep_counts_host_) cudaFreeHost(dep_counts_host_);
   if (dep_mbrows_host_) cudaFreeHost(dep_mbrows_host_);

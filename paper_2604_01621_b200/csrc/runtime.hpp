@@ -225,6 +225,9 @@ class Ctx {
   // dep_xs_; H is re-quantised into dep_h8_ / dep_hs_
   uint8_t* dep_h8_ = nullptr;
   float *dep_xs_ = nullptr, *dep_hs_ = nullptr;
+  // nvfp4 DEP: received codes in dep_recv_ (bytes), linear block scales in
+  // dep_sfl_ (also the H quantiser's scratch), atoms in dep_xsf_ / dep_hsf_
+  uint8_t *dep_sfl_ = nullptr, *dep_xsf_ = nullptr, *dep_hsf_ = nullptr;
   CUtensorMap tm_dep_x8_, tm_dep_h8_;
   void dep_reserve(int64_t rows);
   int num_sms_ = 148;

@@ -144,10 +144,3 @@ def test_dwdp_nvfp4_group_of_two_matches_all_local(dev):
         for c in ranks:
             c.close()
     full.close()
-
-
-def test_dep_rejects_nvfp4(dev):
-    c = D.DwdpContext(D.DwdpConfig(**dict(MID, weight_dtype=D.WEIGHT_NVFP4), rank=0, group_size=2))
-    with pytest.raises(D.ConfigError):
-        c.dep_init(D.nccl_unique_id())
-    c.close()

@@ -12,7 +12,7 @@ from conftest import ROOT
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
-@pytest.mark.parametrize("engine,weight", [(0, 0), (1, 0), (2, 0), (1, 1), (0, 1)])
+@pytest.mark.parametrize("engine,weight", [(0, 0), (1, 0), (2, 0), (1, 1), (0, 1), (1, 2), (0, 2)])
 def test_dwdp_and_dep_match_all_local(engine, weight):
     n = torch.cuda.device_count()
     if n < 2:
@@ -21,7 +21,7 @@ def test_dwdp_and_dep_match_all_local(engine, weight):
     env = dict(os.environ, DWDP_ENGINE=str(engine), DWDP_WEIGHT=str(weight))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         f"--nproc-per-node={n}", "--master-addr=127.0.0.1",
-                        f"--master-port={29600 + 2 * engine + weight}", os.path.join(ROOT, "tests", "mp_check.py")],
+                        f"--master-port={29600 + 3 * engine + weight}", os.path.join(ROOT, "tests", "mp_check.py")],
                        env=env, capture_output=True, text=True, timeout=600)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
