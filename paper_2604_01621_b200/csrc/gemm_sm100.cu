@@ -44,8 +44,8 @@ constexpr int STAGES = 4;
 constexpr int A_STAGE = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE = BN * BK * 2;  // 32 KB
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
-// scaled (fp8 / nvfp4) modes add the tile's weight-row scales (256 fp32)
-constexpr int SMEM_BYTES8 = SMEM_BYTES + 1024;
+// scaled (fp8 / nvfp4) modes add the tiles' weight-row scales (2 x 256 fp32)
+constexpr int SMEM_BYTES8 = SMEM_BYTES + 2048;
 constexpr uint32_t TMEM_COLS = 512;
 // NVFP4 modes (kind::mxf4nvf4 block16): a 128-byte smem row holds 256 e2m1
 // elements, so one stage carries 4x the K of a bf16 stage; 3 stages plus the
@@ -57,7 +57,7 @@ constexpr uint32_t TMEM_COLS = 512;
 constexpr int FP4_STAGES = 3;
 constexpr int SFA_STAGE = 2048, SFB_STAGE = 4096;
 constexpr int SMEM_BYTES4 =
-    FP4_STAGES * (A_STAGE + B_STAGE + SFA_STAGE + SFB_STAGE) + 1024 + 256 + 1024;
+    FP4_STAGES * (A_STAGE + B_STAGE + SFA_STAGE + SFB_STAGE) + 1024 + 256 + 2048;
 constexpr uint32_t FP4_ACC1 = 192, TM_SFA = 448, TM_SFB = 464;
 
 // ---------------------------------------------------------------- PTX
@@ -138,6 +138,24 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Split form for software pipelining: the registers of an issued load must
+// not be read before tcgen05.wait::ld.
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms 1024 B
@@ -357,12 +375,19 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
       release(i);
     }
   } else {
+    // plain: the TMEM load of chunk i+1 is in flight while chunk i is scaled,
+    // packed and stored (GEMM2's short K leaves the drain on the critical path)
     uint16_t* out = p.D + row * p.ldd + nb * BN;
-#pragma unroll 1
+    uint32_t buf[2][32];
+    tmem_ld32_issue(tbase + (start & (BN - 1)), buf[0]);
+    tmem_ld_wait();
+#pragma unroll
     for (int i = 0; i < BN / 32; ++i) {
       const int c = (start + 32 * i) & (BN - 1);
+      if (i + 1 < BN / 32) tmem_ld32_issue(tbase + ((start + 32 * (i + 1)) & (BN - 1)), buf[(i + 1) & 1]);
       float v[32];
-      tmem_ld32(tbase + c, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(buf[i & 1][j]);
       if (FP8) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
@@ -382,6 +407,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
         for (int w = 0; w < 4; ++w)
           o4[w] = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
       }
+      tmem_ld_wait();  // chunk i+1 landed (and every read of chunks <= i is done)
       release(i);
     }
   }
@@ -408,7 +434,7 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* tpart = tempty + 2;  // NVFP4: overlapped accumulator columns drained
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tpart + 2);
-  float* sscale = reinterpret_cast<float*>(tmem_holder + 4);  // [256] scaled modes (16-B aligned)
+  float* sscale = reinterpret_cast<float*>(tmem_holder + 4);  // [2][256] scaled modes (16-B aligned)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -615,36 +641,44 @@ __global__ void __launch_bounds__(256, 1)
     int local = 0;
     constexpr bool SCALED = FP8 || FP4;
     const int et = q * 32 + lane;  // 0..127: this thread's row of the tile
+    // scaled modes: the scales of tile i+1 are loaded into registers while
+    // tile i drains, so no global-load latency sits inside a drain; they are
+    // staged in a double-buffered smem copy (one named barrier per tile)
+    float n0 = 0.0f, n1 = 0.0f, nsa = 1.0f;
+    auto fetch_scales = [&](int t) {
+      int m, n;
+      tile_coords(t, nb_count, p.mb_seg, p.raster, m, n);
+      const int64_t b0 = int64_t(p.slot_of[p.mblock_expert[m]]) * p.rows_per_slot +
+                         int64_t(n) * (SWIGLU ? 128 : BN);
+      n0 = __ldg(p.b_scale0 + b0 + et);
+      n1 = SWIGLU ? __ldg(p.b_scale1 + b0 + et) : __ldg(p.b_scale0 + b0 + 128 + et);
+      nsa = __ldg(p.a_scale + int64_t(m) * BM + et);
+    };
+    if (SCALED && blockIdx.x < num_tiles) fetch_scales(blockIdx.x);
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       int mb, nb;
       tile_coords(tile, nb_count, p.mb_seg, p.raster, mb, nb);
       const int a = local & 1;
       const uint32_t aph = (local >> 1) & 1;
-      // scaled modes: fetch the tile's scales while the MMAs run, so no
-      // global-load latency sits inside the drain of the accumulator
-      float pre0 = 0.0f, pre1 = 0.0f, sa = 1.0f;
-      if (SCALED) {
-        const int64_t b0 = int64_t(p.slot_of[p.mblock_expert[mb]]) * p.rows_per_slot +
-                           int64_t(nb) * (SWIGLU ? 128 : BN);
-        pre0 = __ldg(p.b_scale0 + b0 + et);
-        pre1 = SWIGLU ? __ldg(p.b_scale1 + b0 + et) : __ldg(p.b_scale0 + b0 + 128 + et);
-        sa = __ldg(p.a_scale + int64_t(mb) * BM + et);
-      }
+      const float pre0 = n0, pre1 = n1, sa = nsa;
+      if (SCALED && tile + int(gridDim.x) < num_tiles) fetch_scales(tile + gridDim.x);
       mbar_wait(&tfull[a], aph);
       tc_fence_after();
+      float* ssc = sscale + (local & 1) * 256;
       if (SCALED) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's readers are done
-        sscale[et] = pre0;
-        sscale[128 + et] = pre1;
+        // buffer local&1 was last read in tile local-2, before every thread
+        // passed the barrier of tile local-1
+        ssc[et] = pre0;
+        ssc[128 + et] = pre1;
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
       const uint32_t lanes = uint32_t(q * 32) << 16;
       if (FP4)  // accumulator 0 overlaps accumulator 1 in its last 64 columns
         epilogue_tile<MODE>(p, mb, nb, tmem_base + lanes + uint32_t(a) * FP4_ACC1, q, lane,
-                            a == 0 ? (SWIGLU ? 64 : 192) : 0, &tpart[a], sscale, sa);
+                            a == 0 ? (SWIGLU ? 64 : 192) : 0, &tpart[a], ssc, sa);
       else if (SCALED)
         epilogue_tile<MODE>(p, mb, nb, tmem_base + lanes + uint32_t(a * BN), q, lane, 0, nullptr,
-                            sscale, sa);
+                            ssc, sa);
       else
         epilogue_tile<MODE>(p, mb, nb, tmem_base + lanes + uint32_t(a * BN), q, lane);
       tc_fence_before();
