@@ -284,14 +284,21 @@ __device__ __forceinline__ void tile_coords(int tile, int nb_count, const int2* 
 template <int MODE>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb, uint32_t tbase, int q,
                                               int lane, int start = 0, uint64_t* part = nullptr,
-                                              const float* ssc = nullptr, float sa_in = 1.0f) {
+                                              const float* ssc = nullptr, float sa_in = 1.0f,
+                                              uint32_t part_cl = 0) {
   constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8 || MODE == kSwiGLU4;
   constexpr bool FP8 = MODE == kSwiGLU8 || MODE == kPlain8 || is_fp4<MODE>();  // scaled epilogue
-  auto release = [&](int i) {
-    if (part != nullptr && i == 1) {
+  auto release = [&](int i) {  // local barrier, or the CTA-pair leader's (cluster address)
+    if ((part != nullptr || part_cl != 0) && i == 1) {
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(part);
+      if (lane == 0) {
+        if (part_cl != 0)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(part_cl)
+                       : "memory");
+        else
+          mbar_arrive(part);
+      }
     }
   };
   const int64_t row = int64_t(mb) * BM + q * 32 + lane;
@@ -652,7 +659,7 @@ __global__ void __launch_bounds__(256, 1)
                          int64_t(n) * (SWIGLU ? 128 : BN);
       n0 = __ldg(p.b_scale0 + b0 + et);
       n1 = SWIGLU ? __ldg(p.b_scale1 + b0 + et) : __ldg(p.b_scale0 + b0 + 128 + et);
-      nsa = __ldg(p.a_scale + int64_t(m) * BM + et);
+      nsa = int64_t(m) * BM + et < p.m_limit ? __ldg(p.a_scale + int64_t(m) * BM + et) : 1.0f;
     };
     if (SCALED && blockIdx.x < num_tiles) fetch_scales(blockIdx.x);
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
@@ -948,6 +955,213 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   }
 }
 
+// ---------------------------------------------------------------- NVFP4 CTA pair
+// kind::mxf4nvf4 on CTA pairs (cta_group::2, M256 x N256 x K64 per MMA). Per
+// CTA and k-block it moves A (its 128 rows, 16 KB), half of B (16 KB), the
+// scales of its A rows (2 KB) and the scales of ALL 256 B rows (4 KB): 38 KB
+// instead of the 1-SM kernel's 54 KB, whose L2->SM traffic (~24 TB/s needed at
+// the fp4 MMA rate) is what bounds it. The leader's tcgen05.cp.cta_group::2
+// copies each CTA's scale atoms into that CTA's TMEM (same offsets); the
+// accumulators overlap as in the 1-SM kernel. Scale atoms arrive by 2-D TMA
+// (128-byte rows, 16 rows = 2 KB) so that every load of both CTAs completes
+// on the leader's barrier.
+constexpr int P4_STAGES = 5;
+constexpr int P4_A = BM * 128, P4_B = 128 * 128, P4_SFA = 2048, P4_SFB = 4096;
+constexpr int P4_STAGE = P4_A + P4_B + P4_SFA + P4_SFB;
+constexpr int P4_SMEM_BYTES = P4_STAGES * P4_STAGE + 1024 + 256 + 2048;
+
+__device__ __forceinline__ void tc_mma_pair_fp4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                                uint32_t idesc_v, uint32_t accum, uint32_t sfa,
+                                                uint32_t sfb) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, %3, [%5], [%6], p;\n}" ::"r"(
+          d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc_v), "r"(accum), "r"(sfa), "r"(sfb));
+}
+__device__ __forceinline__ void tc_cp_sf_pair(uint32_t taddr, uint64_t d) {
+  asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(d) : "memory");
+}
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    grouped_gemm_pair_fp4_kernel(const __grid_constant__ CUtensorMap tmA,
+                                 const __grid_constant__ CUtensorMap tmB0,
+                                 const __grid_constant__ CUtensorMap tmB1,
+                                 const __grid_constant__ CUtensorMap tmSA,
+                                 const __grid_constant__ CUtensorMap tmSB0,
+                                 const __grid_constant__ CUtensorMap tmSB1, GemmArgs p) {
+  constexpr bool SWIGLU = MODE == kSwiGLU4;
+  constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(256 >> 4) << 24);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  auto sA = [&](int st) { return smem + st * P4_STAGE; };
+  auto sB = [&](int st) { return smem + st * P4_STAGE + P4_A; };
+  auto sSA = [&](int st) { return smem + st * P4_STAGE + P4_A + P4_B; };
+  auto sSB = [&](int st) { return smem + st * P4_STAGE + P4_A + P4_B + P4_SFA; };
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P4_STAGES * P4_STAGE);
+  uint64_t* empty = full + P4_STAGES;
+  uint64_t* tfull = empty + P4_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* tpart = tempty + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tpart + 2);
+  float* sscale = reinterpret_cast<float*>(tmem_holder + 4);  // [2][256]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < P4_STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // leader: 4 local + 4 peer epilogue warps
+      mbar_init(&tpart[a], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int total_mb = p.meta[0];
+  const int nb_count = SWIGLU ? p.n_out / 128 : p.n_out / BN;
+  const int num_tiles = (total_mb >> 1) * nb_count;
+  const int kb_count = p.K / 256;
+  const int64_t sf_rows_per_rb = int64_t(p.K / 64) * 4;  // 128-byte rows of scales per 128 data rows
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------ TMA producer (both CTAs)
+      const uint32_t full_cl0 = map_to_rank(&full[0], 0);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        int mp, nb;
+        pair_coords(tile, nb_count, p.mb_seg, p.raster, mp, nb);
+        const int mb = 2 * mp + int(rank);
+        const int slot = p.slot_of[p.mblock_expert[mb]];
+        const int arow = mb * BM;
+        // B rows of this CTA's half, and the 128-row blocks of the whole N tile
+        const CUtensorMap* bm = (SWIGLU && rank == 1) ? &tmB1 : &tmB0;
+        const int brow = slot * p.rows_per_slot + (SWIGLU ? nb * 128 : nb * BN + int(rank) * 128);
+        const int64_t rb0 = (int64_t(slot) * p.rows_per_slot + int64_t(nb) * (SWIGLU ? 128 : BN)) >> 7;
+        const CUtensorMap* sb1 = SWIGLU ? &tmSB1 : &tmSB0;
+        const int64_t rb1 = SWIGLU ? rb0 : rb0 + 1;
+        for (int kb = 0; kb < kb_count; ++kb) {
+          mbar_wait(&empty[st], ph ^ 1);
+          const uint32_t bar = full_cl0 + uint32_t(st) * 8u;
+          if (rank == 0) mbar_expect_tx(&full[st], 2 * P4_STAGE);
+          tma_load_2d_pair(sA(st), &tmA, bar, kb * 128, arow);
+          tma_load_2d_pair(sB(st), bm, bar, kb * 128, brow);
+          tma_load_2d_pair(sSA(st), &tmSA, bar, 0, int((arow >> 7) * sf_rows_per_rb + 16 * kb));
+          tma_load_2d_pair(sSB(st), &tmSB0, bar, 0, int(rb0 * sf_rows_per_rb + 16 * kb));
+          tma_load_2d_pair(sSB(st) + 2048, sb1, bar, 0, int(rb1 * sf_rows_per_rb + 16 * kb));
+          if (++st == P4_STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {  // ---------------- MMA issuer (leader warp, one elected lane)
+      int st = 0;
+      uint32_t ph = 0;
+      int local = 0;
+      const uint64_t a0 = sw128_desc(smem_u32(sA(0))), b0 = sw128_desc(smem_u32(sB(0)));
+      const uint64_t sa0 = sf_desc(smem_u32(sSA(0))), sb0 = sf_desc(smem_u32(sSB(0)));
+      for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
+        const int a = local & 1;
+        mbar_wait(&tempty[a], ((local >> 1) & 1) ^ 1);
+        if (local > 0) mbar_wait(&tpart[a ^ 1], ((local - 1) >> 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + uint32_t(a) * FP4_ACC1;
+        for (int kb = 0; kb < kb_count; ++kb) {
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t off = uint64_t(st * (P4_STAGE >> 4));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              tc_cp_sf_pair(tmem_base + TM_SFA + 4 * k, sa0 + off + 32 * k);
+              tc_cp_sf_pair(tmem_base + TM_SFB + 8 * k, sb0 + off + 32 * k);
+              tc_cp_sf_pair(tmem_base + TM_SFB + 8 * k + 4, sb0 + off + 128 + 32 * k);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc_mma_pair_fp4(d, a0 + off + 2 * k, b0 + off + 2 * k, IDESC, (kb | k) != 0,
+                              tmem_base + TM_SFA + 4 * k, tmem_base + TM_SFB + 8 * k);
+            tc_commit_pair(&empty[st]);
+          }
+          __syncwarp();
+          if (++st == P4_STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+        if (elect_one()) tc_commit_pair(&tfull[a]);
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {  // ------------- epilogue (both CTAs, own 128 rows)
+    const int q = warp & 3;
+    const int et = q * 32 + lane;
+    const uint32_t tempty_cl0 = map_to_rank(&tempty[0], 0);
+    const uint32_t tpart_cl0 = map_to_rank(&tpart[0], 0);
+    float n0 = 0.0f, n1 = 0.0f, nsa = 1.0f;
+    auto fetch_scales = [&](int t) {
+      int mp, n;
+      pair_coords(t, nb_count, p.mb_seg, p.raster, mp, n);
+      const int m = 2 * mp + int(rank);
+      const int64_t b0 = int64_t(p.slot_of[p.mblock_expert[m]]) * p.rows_per_slot +
+                         int64_t(n) * (SWIGLU ? 128 : BN);
+      n0 = __ldg(p.b_scale0 + b0 + et);
+      n1 = SWIGLU ? __ldg(p.b_scale1 + b0 + et) : __ldg(p.b_scale0 + b0 + 128 + et);
+      nsa = int64_t(m) * BM + et < p.m_limit ? __ldg(p.a_scale + int64_t(m) * BM + et) : 1.0f;
+    };
+    if (cid < num_tiles) fetch_scales(cid);
+    int local = 0;
+    for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
+      int mp, nb;
+      pair_coords(tile, nb_count, p.mb_seg, p.raster, mp, nb);
+      const int a = local & 1;
+      const float pre0 = n0, pre1 = n1, sa = nsa;
+      if (tile + ncl < num_tiles) fetch_scales(tile + ncl);
+      mbar_wait(&tfull[a], (local >> 1) & 1);
+      tc_fence_after();
+      float* ssc = sscale + (local & 1) * 256;
+      ssc[et] = pre0;
+      ssc[128 + et] = pre1;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      epilogue_tile<MODE>(p, 2 * mp + int(rank), nb,
+                          tmem_base + (uint32_t(q * 32) << 16) + uint32_t(a) * FP4_ACC1, q, lane,
+                          a == 0 ? (SWIGLU ? 64 : 192) : 0, nullptr, ssc, sa, tpart_cl0 + uint32_t(a) * 8u);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_cl0 + uint32_t(a) * 8u);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
 // ---------------------------------------------------------------- host
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -988,6 +1202,20 @@ CUtensorMap make_tmap_2d(const void* base, int64_t rows, int64_t cols, int box_r
   return m;
 }
 
+CUtensorMap make_tmap_sf(const void* base, int64_t bytes) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {128, cuuint64_t(bytes / 128)};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {128, 16};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
+                               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled (scales) failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+
 CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int box_rows) {
   return make_tmap_2d(base, rows, cols, box_rows, false);
 }
@@ -998,7 +1226,7 @@ CUtensorMap make_tmap_i8(const void* base, int64_t rows, int64_t cols, int box_r
 
 void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
                          const CUtensorMap& b0, const CUtensorMap& b1, const GemmArgs& args,
-                         int max_tiles, cudaStream_t st) {
+                         int max_tiles, cudaStream_t st, const CUtensorMap* sf) {
   static std::mutex mu;
   static uint64_t configured = 0;  // bit per device: smem attribute set
   static int sms[64] = {0};
@@ -1023,6 +1251,10 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES4);
       cudaFuncSetAttribute(grouped_gemm_kernel<kPlain4>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES4);
+      cudaFuncSetAttribute(grouped_gemm_pair_fp4_kernel<kSwiGLU4>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, P4_SMEM_BYTES);
+      cudaFuncSetAttribute(grouped_gemm_pair_fp4_kernel<kPlain4>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, P4_SMEM_BYTES);
       cudaFuncSetAttribute(grouped_gemm_pair_kernel<kSwiGLU>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
       cudaFuncSetAttribute(grouped_gemm_pair_kernel<kPlain>,
@@ -1058,7 +1290,17 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
     }
   }
   if (max_tiles <= 0) return;
-  if (mode == kSwiGLU4 || mode == kPlain4) {  // NVFP4: 1-SM kernel only
+  if ((mode == kSwiGLU4 || mode == kPlain4) && args.pair && sf != nullptr) {  // NVFP4 CTA pairs
+    const int cap = 2 * pair_clusters[dev];
+    int g = max_tiles < cap ? max_tiles : cap;
+    g = g < 2 ? 2 : (g & ~1);
+    if (mode == kSwiGLU4)
+      grouped_gemm_pair_fp4_kernel<kSwiGLU4><<<g, 256, P4_SMEM_BYTES, st>>>(a, b0, b1, sf[0], sf[1], sf[2], args);
+    else
+      grouped_gemm_pair_fp4_kernel<kPlain4><<<g, 256, P4_SMEM_BYTES, st>>>(a, b0, b1, sf[0], sf[1], sf[2], args);
+    return;
+  }
+  if (mode == kSwiGLU4 || mode == kPlain4) {  // NVFP4 1-SM kernel
     const int grid = max_tiles < sms[dev] ? max_tiles : sms[dev];
     if (mode == kSwiGLU4)
       grouped_gemm_kernel<kSwiGLU4><<<grid, 256, SMEM_BYTES4, st>>>(a, a2, b0, b1, args);

@@ -76,6 +76,13 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     raster_ = r ? (r[0] == 'm' ? 1 : r[0] == 'n' ? 2 : 0) : 0;
     const char* g = std::getenv("DWDP_GATHER");  // GEMM1 gathers routed rows from x
     gather_ = g && g[0] == '1';
+    // NVFP4 GEMM1 on CTA pairs: 38 instead of 54 KB of L2->SM traffic per
+    // k-block (the 1-SM fp4 kernel is L2-bandwidth bound): 9.45 -> 7.93 ms
+    // per layer. GEMM2 (K = 2048, drain-bound) stays on the 1-SM kernel,
+    // where the pair measured 6.04 -> 7.95 ms. DWDP_FP4_PAIR=0 disables.
+    const char* f4 = std::getenv("DWDP_FP4_PAIR");
+    fp4_pair_ = fp4_ && (f4 ? f4[0] == '1' : true) ? 1 : 0;
+    if (fp4_pair_) row_align_ = 256;
   }
   ntens_ = fp4_ ? 9 : fp8_ ? 6 : 3;
   require(L_ >= 1, "ctx: num_layers must be >= 1");
@@ -171,7 +178,8 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   tm_gate_ = tmap(arena_[0], int64_t(nslots_) * f_, h_ / kdiv, 128);
   tm_up_ = tmap(arena_[1], int64_t(nslots_) * f_, h_ / kdiv, 128);
   tm_down_ = tmap(arena_[2], int64_t(nslots_) * h_, f_ / kdiv, 256);
-  if (gemm_pair_) tm_down_p_ = tmap(arena_[2], int64_t(nslots_) * h_, f_, 128);  // half n-block per CTA
+  if (gemm_pair_ || fp4_pair_)  // half n-block per CTA
+    tm_down_p_ = tmap(arena_[2], int64_t(nslots_) * h_, f_ / kdiv, 128);
   tm_xperm_ = make_tmap_bf16(xperm_, max_rows_, h_, 128);
   tm_h_ = make_tmap_bf16(hbuf_, max_rows_, f_, 128);
   if (fp8_) {
@@ -190,6 +198,9 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     hs_ = static_cast<float*>(dalloc(size_t(max_rows_) * 4, &workspace_bytes));
     tm_x8_ = make_tmap_i8(xperm_, max_rows_, h_ / 2, 128);  // X_perm4 reuses the xperm_ bytes
     tm_h8_ = make_tmap_i8(h8_, max_rows_, f_ / 2, 128);
+    tm_sf_x_ = make_tmap_sf(xsf_, int64_t(max_rows_) * h_ / 16);
+    tm_sf_h_ = make_tmap_sf(hsf_, int64_t(max_rows_) * f_ / 16);
+    for (int t = 0; t < 3; ++t) tm_sf_w_[t] = make_tmap_sf(sfarena_[t], int64_t(tsb(6 + t)) * nslots_);
   }
 
   DWDP_CUDA(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
@@ -662,15 +673,18 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     // the shared-expert rows (after meta[2]) with block + row scales; GEMM1
     // emits bf16 H, which is re-quantised for GEMM2. 1-SM kernel only.
     uint8_t* x4 = reinterpret_cast<uint8_t*>(xperm_);
+    const bool pair4 = fp4_pair_ && T * k_ >= int64_t(E_) * 128;  // decode batches: 1-SM kernel
     const int np = launch_permute(idx_, x, T, E_, k_, h_, shared_ ? 1 : 0, counts_, row_of_, mblock_, mbseg_,
-                                  nullptr, meta_, nullptr, scratch_, st, x4, xs_, 128, mbrows_, sfl_);
+                                  nullptr, meta_, nullptr, scratch_, st, x4, xs_, pair4 ? 256 : 128, mbrows_,
+                                  sfl_);
     launch_nvfp4_sf_relayout(sfl_, xsf_, max_rows_, h_, meta_, st);
     mark(1);
     GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 0, mbseg_,
-                nullptr, xs_, sarena_[0], sarena_[1], 0, raster_, mbrows_, nullptr, 0,
+                nullptr, xs_, sarena_[0], sarena_[1], pair4 ? 1 : 0, raster_, mbrows_, nullptr, 0,
                 xsf_, sfarena_[0], sfarena_[1]};
+    const CUtensorMap sf1[3] = {tm_sf_x_, tm_sf_w_[0], tm_sf_w_[1]};
     launch_grouped_gemm(GEMM_SWIGLU_FP4, tm_x8_, tm_x8_, tm_gate_, tm_up_, g1,
-                        int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
+                        int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st, sf1);
     launch_quant_rows_nvfp4(hbuf_, max_rows_, f_, meta_, h8_, sfl_, hsf_, hs_, st);
     mark(2);
     GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
@@ -880,16 +894,24 @@ void Ctx::gemm_nvfp4(const uint8_t* A, const uint8_t* Asf, const float* As, cons
                      int64_t K, cudaStream_t st) {
   DeviceGuard dg(cfg.device);
   require(M >= 1 && N > 0 && N % 256 == 0 && K > 0 && K % 256 == 0, "gemm: need N%256==0, K%256==0");
-  const int64_t mb = (M + 127) / 128;
+  // CTA pairs take m-blocks in pairs: the odd tail block reads zero-filled A
+  // rows and stores nothing (m_limit). (Test entry: DWDP_FP4_PAIR=1 selects.)
+  const char* f4 = std::getenv("DWDP_FP4_PAIR");
+  const int pair = f4 && f4[0] == '1' ? 1 : 0;
+  const int64_t mb = pair ? (M + 255) / 256 * 2 : (M + 127) / 128;
   int32_t* tabs = static_cast<int32_t*>(dalloc(size_t(mb + 8) * 4, nullptr));
   DWDP_CUDA(cudaMemsetAsync(tabs, 0, size_t(mb + 8) * 4, st));
   const int32_t meta[4] = {int32_t(mb), int32_t(mb), int32_t(mb * 128), 0};
   DWDP_CUDA(cudaMemcpyAsync(tabs + mb + 4, meta, 16, cudaMemcpyHostToDevice, st));
   const CUtensorMap ta = make_tmap_i8(A, M, K / 2, 128);
-  const CUtensorMap tb = make_tmap_i8(B, N, K / 2, 256);
+  const CUtensorMap tb = make_tmap_i8(B, N, K / 2, pair ? 128 : 256);
+  // scale maps cover whole 128-row blocks; the caller's buffers are padded to 128 rows
+  const CUtensorMap sf[3] = {make_tmap_sf(Asf, (M + 127) / 128 * 128 * K / 16),
+                             make_tmap_sf(Bsf, (N + 127) / 128 * 128 * K / 16),
+                             make_tmap_sf(Bsf, (N + 127) / 128 * 128 * K / 16)};
   GemmArgs a{int(K), int(N), int(N), 1, tabs, tabs + mb, tabs + mb + 4, D, N, M, 0, nullptr,
-             nullptr, As, Bs, nullptr, 0, 0, nullptr, nullptr, 0, Asf, Bsf, nullptr};
-  launch_grouped_gemm(GEMM_PLAIN_FP4, ta, ta, tb, tb, a, int(mb * (N / 256)), st);
+             nullptr, As, Bs, nullptr, pair, 0, nullptr, nullptr, 0, Asf, Bsf, nullptr};
+  launch_grouped_gemm(GEMM_PLAIN_FP4, ta, ta, tb, tb, a, int(mb * (N / 256)), st, sf);
   ++launches;
   DWDP_CUDA(cudaGetLastError());
   DWDP_CUDA(cudaStreamSynchronize(st));

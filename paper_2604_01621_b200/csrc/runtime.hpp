@@ -145,6 +145,9 @@ class Ctx {
   uint8_t* h8_ = nullptr;               // e4m3 H [max_rows][f] (nvfp4: [max_rows][f/2])
   uint8_t *xsf_ = nullptr, *hsf_ = nullptr;  // nvfp4 block scales of X_perm4 / H4 (atoms)
   uint8_t* sfl_ = nullptr;                   // nvfp4 linear block-scale scratch [rows][h/16]
+  int fp4_pair_ = 0;                         // nvfp4 GEMMs on CTA pairs (DWDP_FP4_PAIR)
+  CUtensorMap tm_sf_x_, tm_sf_h_, tm_sf_w_[3];  // nvfp4 scale atoms for the CTA-pair kernel
+  CUtensorMap tm_dep_sfx_, tm_dep_sfh_;
   float *xs_ = nullptr, *hs_ = nullptr;  // per-row scales of X_perm8 / H8
   CUtensorMap tm_x8_, tm_h8_;
   std::vector<void*> ipc_opened_;

@@ -29,6 +29,9 @@ FP4_CONFIGS = {
                             weight_dtype=D.WEIGHT_NVFP4),
     "r1_fp4": D.DwdpConfig(num_layers=1, max_tokens=512, weight_dtype=D.WEIGHT_NVFP4),
 }
+# GEMM1 runs on CTA pairs by default (DWDP_FP4_PAIR); batches with fewer than
+# 128 routed rows per expert, and contexts created with DWDP_FP4_PAIR=0, use
+# the 1-SM kernel -- test_moe_forward_nvfp4_single_cta covers that path.
 
 
 @pytest.fixture(scope="module")
@@ -64,9 +67,11 @@ def test_nvfp4_quant_bit_exact(dev, orc, R, K):
     assert (s.cpu().numpy() == os_).all()
 
 
+@pytest.mark.parametrize("pair", ["0", "1"])  # 1-SM kernel / CTA-pair kernel (cta_group::2)
 @pytest.mark.parametrize("M,N,K", [(128, 256, 256), (300, 512, 1024), (1, 256, 7168),
                                    (1000, 2048, 2048)])
-def test_gemm_nvfp4_vs_dequantised_fp32(dev, orc, M, N, K):
+def test_gemm_nvfp4_vs_dequantised_fp32(dev, orc, monkeypatch, M, N, K, pair):
+    monkeypatch.setenv("DWDP_FP4_PAIR", pair)
     a = _rand_bf16(M, K, M + 3 * K, dev)
     b = _rand_bf16(N, K, N + 5 * K, dev, scale=0.05)
     qa, qb = D.quant_nvfp4(a), D.quant_nvfp4(b)
@@ -116,6 +121,28 @@ def test_moe_forward_nvfp4_vs_oracle(dev, ctxs4, orc, name, T):
     yd = y.float().cpu().numpy()
     assert _rel(yd, yo4) < TOL_FP4, _rel(yd, yo4)
     assert _rel(yd, yo) < TOL_FP4_Q, _rel(yd, yo)
+
+
+def test_moe_forward_nvfp4_single_cta(dev, orc, monkeypatch):
+    """GEMM1 on the 1-SM kernel (DWDP_FP4_PAIR=0) vs the oracle and bitwise vs
+    the CTA-pair build of the same layer (rows are independent)."""
+    cfg = FP4_CONFIGS["mid_fp4"]
+    x = make_x(2000, cfg.hidden, 2011, dev)
+    pair = D.DwdpContext(cfg)
+    monkeypatch.setenv("DWDP_FP4_PAIR", "0")
+    single = D.DwdpContext(cfg)
+    for c in (pair, single):
+        c.init_weights()
+        c.set_bias(_bias(cfg))
+    y1, y0 = pair.moe_forward(0, x), single.moe_forward(0, x)
+    torch.cuda.synchronize()
+    oc = oracle_cfg(cfg)
+    oc.w8a8 = 2
+    yo4, _, _ = orc.moe_forward_seeded(oc, cfg.weight_seed, 0, _bf16_np(x).reshape(-1), 2000, _bias(cfg))
+    assert _rel(y0.float().cpu().numpy(), yo4) < TOL_FP4
+    assert _rel(y1.float().cpu().numpy(), yo4) < TOL_FP4
+    pair.close()
+    single.close()
 
 
 def test_dwdp_nvfp4_group_of_two_matches_all_local(dev):
