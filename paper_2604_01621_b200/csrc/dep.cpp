@@ -355,13 +355,13 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
     launch_grouped_gemm(GEMM_PLAIN_FP4, tm_dep_h8_, tm_dep_h8_, tm_down_, tm_down_, g2, int(nblocks * (h_ / 256)), st);
   } else if (nblocks > 0 && fp8_) {
     GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
-                nullptr, dep_hs_, sarena_[2], nullptr, gemm_pair_, raster_, dep_mbrows_};
-    const CUtensorMap& tmd8 = gemm_pair_ ? tm_down_p_ : tm_down_;
+                nullptr, dep_hs_, sarena_[2], nullptr, gemm2_pair_, raster_, dep_mbrows_};
+    const CUtensorMap& tmd8 = gemm2_pair_ ? tm_down_p_ : tm_down_;
     launch_grouped_gemm(GEMM_PLAIN_FP8, tm_dep_h8_, tm_dep_h8_, tmd8, tmd8, g2, int(nblocks * (h_ / 256)), st);
   } else if (nblocks > 0) {
     GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
-                nullptr, nullptr, nullptr, nullptr, gemm_pair_, raster_, dep_mbrows_};
-    const CUtensorMap& tmd = gemm_pair_ ? tm_down_p_ : tm_down_;
+                nullptr, nullptr, nullptr, nullptr, gemm2_pair_, raster_, dep_mbrows_};
+    const CUtensorMap& tmd = gemm2_pair_ ? tm_down_p_ : tm_down_;
     launch_grouped_gemm(GEMM_PLAIN, tm_dep_h_, tm_dep_h_, tmd, tmd, g2, int(nblocks * (h_ / 256)), st);
   }
   mark(&rec.k[3]);

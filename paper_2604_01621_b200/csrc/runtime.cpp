@@ -70,7 +70,9 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   // (scripts/gpu/r1_ab_pair.sh: 144K vs 158K tokens/s).
   {
     const char* env = std::getenv("DWDP_GEMM_PAIR");
-    gemm_pair_ = env && env[0] == '1' ? 1 : 0;
+    // DWDP_GEMM_PAIR=1: every GEMM on CTA pairs; =2: GEMM1 only
+    gemm_pair_ = env && (env[0] == '1' || env[0] == '2') ? 1 : 0;
+    gemm2_pair_ = env && env[0] == '1' ? 1 : 0;
     row_align_ = gemm_pair_ ? 256 : 128;
     const char* r = std::getenv("DWDP_RASTER");  // experiments: m / n (default auto)
     raster_ = r ? (r[0] == 'm' ? 1 : r[0] == 'n' ? 2 : 0) : 0;
@@ -636,9 +638,9 @@ void Ctx::route_logits(int wl, const uint16_t* x, int64_t T, cudaStream_t st) {
   const CUtensorMap tx = make_tmap_i8(xq_, 3 * T, h_, 128);
   GemmArgs ga{int(h_), 3 * E_, 0, -1, zeros_, zeros_, rmeta_,
               reinterpret_cast<uint16_t*>(rC_), 3 * int64_t(E_), 3 * T, 0, nullptr,
-              nullptr, nullptr, nullptr, nullptr, gemm_pair_, 0};
+              nullptr, nullptr, nullptr, nullptr, gemm2_pair_, 0};
   const int64_t tiles = (3 * T + 127) / 128 * ((3 * E_ + 255) / 256);
-  const CUtensorMap& tb = gemm_pair_ ? tm_rw_p_[size_t(wl)] : tm_rw_[size_t(wl)];
+  const CUtensorMap& tb = gemm2_pair_ ? tm_rw_p_[size_t(wl)] : tm_rw_[size_t(wl)];
   launch_grouped_gemm(GEMM_INT8, tx, tx, tb, tb, ga, int(std::min<int64_t>(tiles, 1 << 30)), st);
   RouterCfg rc{E_, k_, cfg.scoring, cfg.n_group, cfg.topk_group, cfg.norm_topk, cfg.routed_scale};
   launch_topk(rC_, xe_, router_we_ + size_t(wl) * E_, bias_ + size_t(wl) * E_, logits_, idx_, wts_,
@@ -667,7 +669,8 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   // 1-SM kernel. (Rank-local choice: the DEP layout keeps row_align_.)
   const bool pair = gemm_pair_ && T * k_ >= int64_t(E_) * 128;
   const int align = pair ? row_align_ : 128;
-  const CUtensorMap& tmdown = pair ? tm_down_p_ : tm_down_;
+  const bool pair2 = pair && gemm2_pair_;
+  const CUtensorMap& tmdown = pair2 ? tm_down_p_ : tm_down_;
   if (fp4_) {
     // W4A4 NVFP4: the permute writes e2m1 copies of every routed row and of
     // the shared-expert rows (after meta[2]) with block + row scales; GEMM1
@@ -710,7 +713,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     launch_quant_rows_fp8(hbuf_, max_rows_, f_, meta_, h8_, hs_, st);
     mark(2);
     GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
-                nullptr, hs_, sarena_[2], nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_};
+                nullptr, hs_, sarena_[2], nullptr, pair2 ? 1 : 0, raster_, mbrows_};
     launch_grouped_gemm(GEMM_PLAIN_FP8, tm_h8_, tm_h8_, tmdown, tmdown, g2,
                         int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
     mark(3);
@@ -737,7 +740,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(2);
   GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
-              nullptr, nullptr, nullptr, nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_};
+              nullptr, nullptr, nullptr, nullptr, pair2 ? 1 : 0, raster_, mbrows_};
   launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tmdown, tmdown, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
   mark(3);
   launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
