@@ -183,6 +183,9 @@ def main():
     ap.add_argument("--oversubscribe", action="store_true",
                     help="code-path test: WORLD_SIZE > GPUs (ranks share GPUs, gloo, no DEP); "
                          "numbers from such a run are not bench values")
+    ap.add_argument("--attention", action="store_true",
+                    help="run a DeepSeek-V3 MLA prefill block (library ops) before every MoE layer, "
+                         "in DWDP and DEP alike: the paper's prefetch window MoE(l) + Attention(l+1)")
     ap.add_argument("--zipf", type=float, default=0.0,
                     help="expert-routing skew s: router bias -ZIPF_BETA*s*ln(e+1)")
     args = ap.parse_args()
@@ -234,6 +237,10 @@ def main():
                               max(1, args.tokens // 8192), 0.0, 7)
         batches = D.sample_batches(spec, model, world, iters, with_routing=False)
         toks = [[b.tokens[r] for r in range(world)] for b in batches]
+        reqs = [[b.requests[r] for r in range(world)] for b in batches]
+    if args.attention:
+        assert not args.decode, "--attention models the prefill window"
+        args.no_e2e = True  # the e2e leg drives dwdp_stack_forward (MoE layers only)
     fp8 = args.dtype == "fp8"
     fp4 = args.dtype == "nvfp4"
     # bytes per weight element (nvfp4: e2m1 + one e4m3 scale per 16) and the
@@ -272,6 +279,38 @@ def main():
     D.fill_bf16(x, 0xC0FFEE + rank, 1.0)
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream()
+    attn = None
+    if args.attention:
+        from paper_2604_01621_b200.attention import MlaAttention, split_sequences
+        attn = MlaAttention(dev, seed=7 + rank)
+    gl = [0]  # next global layer of the DWDP stack (attention mode drives the layers itself)
+    attn_ms = [0.0, 0]  # attention time inside timed DWDP steps, layers
+    attn_flops = [0.0]
+
+    def step(T: int, it: int, dep: bool = False, timed: bool = False):
+        """One step of the L-layer stack on rank tokens x[:T] -> y[:T]."""
+        if attn is None:
+            (ctx.dep_stack_forward if dep else ctx.stack_forward)(x[:T], y[:T])
+            return
+        seqs = split_sequences(T, reqs[it][rank])
+        hcur = x[:T]
+        for l in range(layers):
+            if timed:
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+            hin = hcur + attn.forward(hcur, seqs)
+            if timed:
+                a1.record(stream)
+                attn_ev.append((a0, a1))
+                attn_flops[0] += attn.flops(seqs)
+            if dep:
+                ctx.dep_layer_forward(l, hin, y[:T], residual=True)
+            else:
+                ctx.layer_forward(gl[0] + l, hin, y[:T], residual=True)
+            hcur = y[:T]
+        if not dep:
+            gl[0] += layers
+    attn_ev = []
     # routed-count statistics of rank 0's first batch (skew and touched experts)
     _, _, cnt, _, _ = ctx.route(0, x[:toks[0][rank]])
     cnt = cnt.double().cpu()
@@ -280,8 +319,7 @@ def main():
                "bias": f"-{ZIPF_BETA}*s*ln(e+1)" if args.zipf > 0 else "0"}
 
     for it in range(args.warmup):
-        T = toks[it][rank]
-        ctx.stack_forward(x[:T], y[:T])
+        step(toks[it][rank], it)
     torch.cuda.synchronize()
     wrecs = ctx.records()
     engine = {D.ENGINE_COPY: "copy", D.ENGINE_PULL: "pull", D.ENGINE_HYBRID: "hybrid"}[cfg.engine]
@@ -298,8 +336,7 @@ def main():
             best = (0.0, "pull", D.ENGINE_PULL)
             for name, eid in (("pull", D.ENGINE_PULL), ("hybrid", D.ENGINE_HYBRID)):
                 ctx.set_engine(eid)
-                T = toks[0][rank]
-                ctx.stack_forward(x[:T], y[:T])
+                step(toks[0][rank], 0)
                 torch.cuda.synchronize()
                 rr = [r for r in ctx.records() if r["prefetch_bytes"] > 0]
                 gbs = sum(r["prefetch_bytes"] for r in rr) / max(sum(r["prefetch_ns"] for r in rr), 1.0)
@@ -317,13 +354,20 @@ def main():
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for it in range(args.warmup, iters):
-            T = toks[it][rank]
-            ctx.stack_forward(x[:T], y[:T])
+            step(toks[it][rank], it, timed=True)
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
     launches = ctx.launch_count() - n0
     ms_local = ev0.elapsed_time(ev1)
+    attention = None
+    if attn is not None:
+        a_ms = sum(a0.elapsed_time(a1) for a0, a1 in attn_ev)
+        attention = {"block": "DeepSeek-V3 MLA prefill (q_lora 1536, kv_lora 512, 128 heads, qk 128+64, v 128), "
+                              "library ops: cuBLAS GEMMs + FlashAttention-2, causal, rank tokens split into "
+                              "RankBatch::requests sequences",
+                     "ms_per_layer": a_ms / max(len(attn_ev), 1),
+                     "tflops": attn_flops[0] / (a_ms * 1e-3) / 1e12 if a_ms else None}
     ms = allmax(ms_local)
     recs = ctx.records()
     total_tokens = sum(sum(toks[it]) for it in range(args.warmup, iters))
@@ -440,8 +484,7 @@ def main():
     dep = None
     if world > 1 and not args.no_dep:
         for it in range(args.warmup):
-            T = toks[it][rank]
-            ctx.dep_stack_forward(x[:T], y[:T])
+            step(toks[it][rank], it, dep=True)
         torch.cuda.synchronize()
         ctx.records()
         barrier()
@@ -449,8 +492,7 @@ def main():
         d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         d0.record(stream)
         for it in range(args.warmup, iters):
-            T = toks[it][rank]
-            ctx.dep_stack_forward(x[:T], y[:T])
+            step(toks[it][rank], it, dep=True)
         d1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -552,6 +594,7 @@ def main():
                        "slice_size": args.slice_size if world > 1 else None,
                        "l2": "inputs larger than L2: {} GB of expert weights per layer".format(
                            "11.3 (e4m3)" if fp8 else "6.3 (nvfp4)" if fp4 else "22.5 (bf16)"),
+                       "attention_block": bool(args.attention),
                        "parallelism": f"dwdp{world}"},
             "tokens_per_s_per_gpu": value / world,
             "exposed_prefetch_ms_per_layer": exposed_ms,
@@ -563,6 +606,7 @@ def main():
             "roofline": roof, "step_roofline": step_roof, "routing": routing,
             "dep_baseline": dep, "report": acct,
             "hbm_gb": {k2: round(v / 1e9, 2) for k2, v in ctx.memory().items()},
+            "attention": attention,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
         }
