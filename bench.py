@@ -162,8 +162,8 @@ def main():
     ap.add_argument("--cv", type=float, default=0.2, help="sequence-length CV")
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--engine", default="auto", choices=["auto", "copy", "pull", "hybrid"],
-                    help="auto: copy engine unless its measured GB/s leaves prefetch exposed, "
-                         "then the SM engine (pull or hybrid) with the higher measured GB/s")
+                    help="auto: copy engine unless it leaves prefetch exposed, then the engine "
+                         "(copy, pull or hybrid) with the fastest measured step")
     ap.add_argument("--slice-size", type=int, default=64 << 20)
     ap.add_argument("--no-tdm", action="store_true")
     ap.add_argument("--merged", action="store_true", help="merge_elim off (D2D merge baseline)")
@@ -324,23 +324,31 @@ def main():
     wrecs = ctx.records()
     engine = {D.ENGINE_COPY: "copy", D.ENGINE_PULL: "pull", D.ENGINE_HYBRID: "hybrid"}[cfg.engine]
     if world > 1 and args.engine == "auto":
-        # choose by measured GB/s: keep the copy engine (no SM cost) while its
-        # bandwidth hides the pull under the compute window, else the TMA kernel
+        # keep the copy engine (no SM cost) while it hides the pull under the
+        # compute window, else probe the engines (below)
         steady = [r for r in wrecs if r["prefetch_bytes"] > 0][len(wrecs) // 2:]
         wait = sum(r["gate_wait_ns"] for r in steady)
         moe = sum(r["moe_ns"] for r in steady)
-        if steady and wait > 0.02 * moe:
-            # the copy engine leaves prefetch exposed: run one step on each SM
-            # engine (TMA pull kernel; hybrid = pull kernel + copy engines on
-            # alternating slices) and keep the one with the higher in-step GB/s
-            best = (0.0, "pull", D.ENGINE_PULL)
-            for name, eid in (("pull", D.ENGINE_PULL), ("hybrid", D.ENGINE_HYBRID)):
+        # one decision for all ranks (the probe below times steps across ranks)
+        if allmax(wait / moe if steady and moe > 0 else 0.0) > 0.02:
+            # the copy engine leaves prefetch exposed: time one step on each
+            # engine (copy; TMA pull kernel; hybrid = pull kernel + copy
+            # engines on alternating slices) and keep the fastest step (max
+            # over ranks). The SM engines move bytes faster but take SM time
+            # from the GEMMs, so in-step GB/s alone is not the criterion.
+            best = None
+            for name, eid in (("copy", D.ENGINE_COPY), ("pull", D.ENGINE_PULL), ("hybrid", D.ENGINE_HYBRID)):
                 ctx.set_engine(eid)
+                barrier()
+                p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                p0.record(stream)
                 step(toks[0][rank], 0)
+                p1.record(stream)
                 torch.cuda.synchronize()
-                rr = [r for r in ctx.records() if r["prefetch_bytes"] > 0]
-                gbs = sum(r["prefetch_bytes"] for r in rr) / max(sum(r["prefetch_ns"] for r in rr), 1.0)
-                best = max(best, (gbs, name, eid))
+                t_eng = allmax(p0.elapsed_time(p1))
+                ctx.records()
+                if best is None or t_eng < best[0]:
+                    best = (t_eng, name, eid)
             ctx.set_engine(best[2])
             engine = best[1]
     engines = [None] * world
