@@ -171,3 +171,32 @@ def test_dwdp_nvfp4_group_of_two_matches_all_local(dev):
         for c in ranks:
             c.close()
     full.close()
+
+
+@pytest.mark.parametrize("group,extra,engine,T0", [(3, 1, D.ENGINE_PULL, 64), (2, 0, D.ENGINE_COPY, 1900)])
+def test_dwdp_nvfp4_placements_and_large_batches(dev, group, extra, engine, T0):
+    """NVFP4 arenas under a non-divisible redundant placement (multi-run
+    shards over all nine tensors) and at batches whose GEMM1 runs on CTA pairs
+    (>= 128 routed rows per expert): bit-identical to the all-local model."""
+    kw = dict(MID, weight_dtype=D.WEIGHT_NVFP4, max_tokens=4096)
+    full = D.DwdpContext(D.DwdpConfig(**kw))
+    full.init_weights()
+    ranks = [D.DwdpContext(D.DwdpConfig(**kw, rank=r, group_size=group, extra_redundancy=extra,
+                                        engine=engine, slice_size=1 << 19)) for r in range(group)]
+    for c in ranks:
+        c.init_weights()
+    D.DwdpContext.link_local(ranks)
+    plan = D.build_placement(MID["num_experts"], group, extra)
+    xs = [make_x(T0 + 29 * r, MID["hidden"], 90 + r, dev) for r in range(group)]
+    for g in range(4):
+        for r in range(group):
+            y = ranks[r].layer_forward(g, xs[r], residual=False)
+            yf = full.moe_forward(g % 3, xs[r])
+            torch.cuda.synchronize()
+            assert torch.equal(y, yf), (group, extra, g, r)
+    h, f = MID["hidden"], MID["ffn"]
+    for r in range(group):
+        fetched = len(plan.fetch_lists[r])
+        assert ranks[r].records()[1]["prefetch_bytes"] == fetched * (3 * h * f // 2 + 4 * (2 * f + h) + 3 * h * f // 16)
+    for c in ranks + [full]:
+        c.close()
