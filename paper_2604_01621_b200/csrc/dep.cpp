@@ -140,6 +140,7 @@ void Ctx::dep_reserve(int64_t rows) {
       dep_xsf_ = static_cast<uint8_t*>(dalloc(size_t(rows) * h_ / 16, nullptr));
       dep_hsf_ = static_cast<uint8_t*>(dalloc(size_t(rows) * f_ / 16, nullptr));
       tm_dep_sfx_ = make_tmap_sf(dep_xsf_, rows * h_ / 16);
+      tm_dep_o_ = make_tmap_out(dep_recv_, rows, h_);
     }
   }
   const int64_t need_tab = rows / 128 + 16;
@@ -352,7 +353,9 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
     GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
                 nullptr, dep_hs_, sarena_[2], nullptr, 0, raster_, dep_mbrows_, nullptr, 0,
                 dep_hsf_, sfarena_[2], nullptr};
-    launch_grouped_gemm(GEMM_PLAIN_FP4, tm_dep_h8_, tm_dep_h8_, tm_down_, tm_down_, g2, int(nblocks * (h_ / 256)), st);
+    const CUtensorMap sf2[4] = {tm_dep_sfh_, tm_sf_w_[2], tm_sf_w_[2], tm_dep_o_};
+    launch_grouped_gemm(GEMM_PLAIN_FP4, tm_dep_h8_, tm_dep_h8_, tm_down_, tm_down_, g2, int(nblocks * (h_ / 256)),
+                        st, sf2);
   } else if (nblocks > 0 && fp8_) {
     GemmArgs g2{int(f_), int(h_), int(h_), E_, dmb, stab, dmeta, dep_recv_, h_, INT64_MAX, 0, dep_seg_,
                 nullptr, dep_hs_, sarena_[2], nullptr, gemm2_pair_, raster_, dep_mbrows_};

@@ -57,7 +57,7 @@ constexpr uint32_t TMEM_COLS = 512;
 constexpr int FP4_STAGES = 3;
 constexpr int SFA_STAGE = 2048, SFB_STAGE = 4096;
 constexpr int SMEM_BYTES4 =
-    FP4_STAGES * (A_STAGE + B_STAGE + SFA_STAGE + SFB_STAGE) + 1024 + 256 + 2048;
+    FP4_STAGES * (A_STAGE + B_STAGE + SFA_STAGE + SFB_STAGE) + 1024 + 256 + 2048 + 4 * 4096;
 constexpr uint32_t FP4_ACC1 = 192, TM_SFA = 448, TM_SFB = 464;
 
 // ---------------------------------------------------------------- PTX
@@ -285,7 +285,8 @@ template <int MODE>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb, uint32_t tbase, int q,
                                               int lane, int start = 0, uint64_t* part = nullptr,
                                               const float* ssc = nullptr, float sa_in = 1.0f,
-                                              uint32_t part_cl = 0) {
+                                              uint32_t part_cl = 0, uint8_t* stage = nullptr,
+                                              int* nstore = nullptr, const CUtensorMap* tmD = nullptr) {
   constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8 || MODE == kSwiGLU4;
   constexpr bool FP8 = MODE == kSwiGLU8 || MODE == kPlain8 || is_fp4<MODE>();  // scaled epilogue
   auto release = [&](int i) {  // local barrier, or the CTA-pair leader's (cluster address)
@@ -408,7 +409,30 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
       uint32_t pk[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
-      if (store) {
+      if (stage != nullptr) {
+        // TMA store: the warp's 32 rows x 32 columns (2 KB) go through a
+        // double-buffered SWIZZLE_64B smem box; 16-byte stores of 32
+        // different rows straight from registers cost one L1 wavefront each
+        // and were GEMM2's bottleneck (6.8 -> 4.5 ms without them)
+        uint8_t* sb = stage + (*nstore & 1) * 2048;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          *reinterpret_cast<uint4*>(sb + lane * 64 + ((w ^ ((lane >> 1) & 3)) << 4)) =
+              make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const bool any = __any_sync(0xffffffffu, store);
+        if (lane == 0 && any) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                  reinterpret_cast<uint64_t>(tmD)),
+              "r"(nb * BN + c), "r"(int(int64_t(mb) * BM + q * 32)), "r"(smem_u32(sb))
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        ++*nstore;
+      } else if (store) {
         uint4* o4 = reinterpret_cast<uint4*>(out + c);
 #pragma unroll
         for (int w = 0; w < 4; ++w)
@@ -425,7 +449,8 @@ __global__ void __launch_bounds__(256, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmA2,
                         const __grid_constant__ CUtensorMap tmB0,
-                        const __grid_constant__ CUtensorMap tmB1, GemmArgs p) {
+                        const __grid_constant__ CUtensorMap tmB1,
+                        const __grid_constant__ CUtensorMap tmD, GemmArgs p) {
   constexpr bool FP4 = is_fp4<MODE>();
   constexpr int NST = FP4 ? FP4_STAGES : STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -435,7 +460,9 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sB = smem + NST * A_STAGE;
   uint8_t* sSFA = sB + NST * B_STAGE;                     // NVFP4 only
   uint8_t* sSFB = sSFA + (FP4 ? NST * SFA_STAGE : 0);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sSFB + (FP4 ? NST * SFB_STAGE : 0));
+  constexpr bool TMA_ST = MODE == kPlain4;  // NVFP4 GEMM2: TMA-store epilogue
+  uint8_t* sStage = sSFB + (FP4 ? NST * SFB_STAGE : 0);  // [4 warps][2][2 KB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + (TMA_ST ? 4 * 4096 : 0));
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
@@ -662,6 +689,7 @@ __global__ void __launch_bounds__(256, 1)
       nsa = int64_t(m) * BM + et < p.m_limit ? __ldg(p.a_scale + int64_t(m) * BM + et) : 1.0f;
     };
     if (SCALED && blockIdx.x < num_tiles) fetch_scales(blockIdx.x);
+    int nstore = 0;  // TMA-store boxes issued by this warp (buffer parity)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       int mb, nb;
       tile_coords(tile, nb_count, p.mb_seg, p.raster, mb, nb);
@@ -682,7 +710,8 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t lanes = uint32_t(q * 32) << 16;
       if (FP4)  // accumulator 0 overlaps accumulator 1 in its last 64 columns
         epilogue_tile<MODE>(p, mb, nb, tmem_base + lanes + uint32_t(a) * FP4_ACC1, q, lane,
-                            a == 0 ? (SWIGLU ? 64 : 192) : 0, &tpart[a], ssc, sa);
+                            a == 0 ? (SWIGLU ? 64 : 192) : 0, &tpart[a], ssc, sa, 0,
+                            TMA_ST ? sStage + q * 4096 : nullptr, &nstore, &tmD);
       else if (SCALED)
         epilogue_tile<MODE>(p, mb, nb, tmem_base + lanes + uint32_t(a * BN), q, lane, 0, nullptr,
                             ssc, sa);
@@ -692,6 +721,8 @@ __global__ void __launch_bounds__(256, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[a]);
     }
+    // the staged boxes must be read out before the CTA's smem goes away
+    if (TMA_ST && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -1202,6 +1233,20 @@ CUtensorMap make_tmap_2d(const void* base, int64_t rows, int64_t cols, int box_r
   return m;
 }
 
+CUtensorMap make_tmap_out(const void* base, int64_t rows, int64_t cols) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(cols) * 2};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                               strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled (output) failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+
 CUtensorMap make_tmap_sf(const void* base, int64_t bytes) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {128, cuuint64_t(bytes / 128)};
@@ -1303,9 +1348,11 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
   if (mode == kSwiGLU4 || mode == kPlain4) {  // NVFP4 1-SM kernel
     const int grid = max_tiles < sms[dev] ? max_tiles : sms[dev];
     if (mode == kSwiGLU4)
-      grouped_gemm_kernel<kSwiGLU4><<<grid, 256, SMEM_BYTES4, st>>>(a, a2, b0, b1, args);
+      grouped_gemm_kernel<kSwiGLU4><<<grid, 256, SMEM_BYTES4, st>>>(a, a2, b0, b1, a, args);
+    else if (sf != nullptr)  // sf[3]: the bf16 output map (32 x 32 boxes, SWIZZLE_64B)
+      grouped_gemm_kernel<kPlain4><<<grid, 256, SMEM_BYTES4, st>>>(a, a2, b0, b1, sf[3], args);
     else
-      grouped_gemm_kernel<kPlain4><<<grid, 256, SMEM_BYTES4, st>>>(a, a2, b0, b1, args);
+      throw std::runtime_error("launch_grouped_gemm: the NVFP4 plain GEMM needs its output map");
     return;
   }
   if (args.pair) {
@@ -1326,15 +1373,15 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
   }
   const int grid = max_tiles < sms[dev] ? max_tiles : sms[dev];
   if (mode == kSwiGLU)
-    grouped_gemm_kernel<kSwiGLU><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+    grouped_gemm_kernel<kSwiGLU><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, a, args);
   else if (mode == kPlain)
-    grouped_gemm_kernel<kPlain><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+    grouped_gemm_kernel<kPlain><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, a, args);
   else if (mode == kInt8)
-    grouped_gemm_kernel<kInt8><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, args);
+    grouped_gemm_kernel<kInt8><<<grid, 256, SMEM_BYTES, st>>>(a, a2, b0, b1, a, args);
   else if (mode == kSwiGLU8)
-    grouped_gemm_kernel<kSwiGLU8><<<grid, 256, SMEM_BYTES8, st>>>(a, a2, b0, b1, args);
+    grouped_gemm_kernel<kSwiGLU8><<<grid, 256, SMEM_BYTES8, st>>>(a, a2, b0, b1, a, args);
   else
-    grouped_gemm_kernel<kPlain8><<<grid, 256, SMEM_BYTES8, st>>>(a, a2, b0, b1, args);
+    grouped_gemm_kernel<kPlain8><<<grid, 256, SMEM_BYTES8, st>>>(a, a2, b0, b1, a, args);
 }
 
 }  // namespace dwdp

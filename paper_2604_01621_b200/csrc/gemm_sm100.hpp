@@ -65,13 +65,17 @@ CUtensorMap make_tmap_i8(const void* base, int64_t rows, int64_t cols, int box_r
 // (2 KB = the 4 atoms of one 256-deep k-block and 128 data rows), no swizzle:
 // the CTA-pair NVFP4 GEMM loads scales with TMA.
 CUtensorMap make_tmap_sf(const void* base, int64_t bytes);
+// bf16 [rows][cols] output map, 32 x 32 boxes, SWIZZLE_64B: the TMA-store
+// epilogue of the NVFP4 GEMM2.
+CUtensorMap make_tmap_out(const void* base, int64_t rows, int64_t cols);
 
 constexpr int GEMM_SWIGLU = 0, GEMM_PLAIN = 1, GEMM_INT8 = 2, GEMM_SWIGLU_FP8 = 3,
               GEMM_PLAIN_FP8 = 4, GEMM_SWIGLU_FP4 = 5, GEMM_PLAIN_FP4 = 6;
 
 // a: routed A rows (permuted tokens or H); a2: shared-expert A rows (x);
 // b0: gate (SwiGLU) or down arena; b1: up arena (SwiGLU only).
-// sf (NVFP4 CTA-pair only, args.pair = 1): scale maps {A, B0, B1}.
+// sf: NVFP4 maps {A scales, B0 scales, B1 scales, D output}; the CTA-pair
+// kernel reads the first three, the plain (GEMM2) kernel the output map.
 void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
                          const CUtensorMap& b0, const CUtensorMap& b1, const GemmArgs& args,
                          int max_tiles, cudaStream_t st, const CUtensorMap* sf = nullptr);

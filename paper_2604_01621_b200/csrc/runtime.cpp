@@ -203,6 +203,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     tm_sf_x_ = make_tmap_sf(xsf_, int64_t(max_rows_) * h_ / 16);
     tm_sf_h_ = make_tmap_sf(hsf_, int64_t(max_rows_) * f_ / 16);
     for (int t = 0; t < 3; ++t) tm_sf_w_[t] = make_tmap_sf(sfarena_[t], int64_t(tsb(6 + t)) * nslots_);
+    tm_o_ = make_tmap_out(xperm_, max_rows_, h_);  // O (bf16) overwrites X_perm4
   }
 
   DWDP_CUDA(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
@@ -693,8 +694,9 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
                 nullptr, hs_, sarena_[2], nullptr, 0, raster_, mbrows_, nullptr, 0,
                 hsf_, sfarena_[2], nullptr};
+    const CUtensorMap sf2[4] = {tm_sf_h_, tm_sf_w_[2], tm_sf_w_[2], tm_o_};
     launch_grouped_gemm(GEMM_PLAIN_FP4, tm_h8_, tm_h8_, tm_down_, tm_down_, g2,
-                        int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
+                        int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st, sf2);
     mark(3);
     launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
     launches += 3 + np + 1 + 4 + 1;  // router 3, permute + relayout, GEMM1 + quant 2 + GEMM2, combine
@@ -909,9 +911,9 @@ void Ctx::gemm_nvfp4(const uint8_t* A, const uint8_t* Asf, const float* As, cons
   const CUtensorMap ta = make_tmap_i8(A, M, K / 2, 128);
   const CUtensorMap tb = make_tmap_i8(B, N, K / 2, pair ? 128 : 256);
   // scale maps cover whole 128-row blocks; the caller's buffers are padded to 128 rows
-  const CUtensorMap sf[3] = {make_tmap_sf(Asf, (M + 127) / 128 * 128 * K / 16),
+  const CUtensorMap sf[4] = {make_tmap_sf(Asf, (M + 127) / 128 * 128 * K / 16),
                              make_tmap_sf(Bsf, (N + 127) / 128 * 128 * K / 16),
-                             make_tmap_sf(Bsf, (N + 127) / 128 * 128 * K / 16)};
+                             make_tmap_sf(Bsf, (N + 127) / 128 * 128 * K / 16), make_tmap_out(D, M, N)};
   GemmArgs a{int(K), int(N), int(N), 1, tabs, tabs + mb, tabs + mb + 4, D, N, M, 0, nullptr,
              nullptr, As, Bs, nullptr, pair, 0, nullptr, nullptr, 0, Asf, Bsf, nullptr};
   launch_grouped_gemm(GEMM_PLAIN_FP4, ta, ta, tb, tb, a, int(mb * (N / 256)), st, sf);

@@ -148,6 +148,7 @@ class Ctx {
   int fp4_pair_ = 0;                         // nvfp4 GEMMs on CTA pairs (DWDP_FP4_PAIR)
   CUtensorMap tm_sf_x_, tm_sf_h_, tm_sf_w_[3];  // nvfp4 scale atoms for the CTA-pair kernel
   CUtensorMap tm_dep_sfx_, tm_dep_sfh_;
+  CUtensorMap tm_o_, tm_dep_o_;                 // nvfp4 GEMM2 output maps (TMA store)
   float *xs_ = nullptr, *hs_ = nullptr;  // per-row scales of X_perm8 / H8
   CUtensorMap tm_x8_, tm_h8_;
   std::vector<void*> ipc_opened_;
