@@ -141,6 +141,7 @@ void Ctx::dep_reserve(int64_t rows) {
       dep_hsf_ = static_cast<uint8_t*>(dalloc(size_t(rows) * f_ / 16, nullptr));
       tm_dep_sfx_ = make_tmap_sf(dep_xsf_, rows * h_ / 16);
       tm_dep_o_ = make_tmap_out(dep_recv_, rows, h_);
+      tm_dep_h_o_ = make_tmap_out(dep_h_, rows, f_);
     }
   }
   const int64_t need_tab = rows / 128 + 16;
@@ -332,7 +333,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
     GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 0, dep_seg_,
                 nullptr, dep_xs_, sarena_[0], sarena_[1], fp4_pair_, raster_, dep_mbrows_, nullptr, 0,
                 dep_xsf_, sfarena_[0], sfarena_[1]};
-    const CUtensorMap sf1[3] = {tm_dep_sfx_, tm_sf_w_[0], tm_sf_w_[1]};  // segments padded to row_align_
+    const CUtensorMap sf1[4] = {tm_dep_sfx_, tm_sf_w_[0], tm_sf_w_[1], tm_dep_h_o_};  // segments padded to row_align_
     launch_grouped_gemm(GEMM_SWIGLU_FP4, tm_dep_x8_, tm_dep_x8_, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)),
                         st, sf1);
     launch_quant_rows_nvfp4(dep_h_, dep_cap_rows_, f_, dmeta, dep_h8_, dep_sfl_, dep_hsf_, dep_hs_, st);

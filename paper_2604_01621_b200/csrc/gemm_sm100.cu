@@ -275,6 +275,31 @@ __device__ __forceinline__ void tile_coords(int tile, int nb_count, const int2* 
 // Epilogue of one 128 x BN accumulator tile: warp q of the epilogue group
 // owns TMEM lanes (rows) 32q..32q+31; tbase addresses this warp's lanes and
 // the tile's accumulator columns.
+// TMA store of one epilogue chunk: the warp's 32 rows x 32 bf16 columns
+// (2 KB) go through a double-buffered SWIZZLE_64B smem box; 16-byte stores of
+// 32 different rows straight from registers cost one L1 wavefront each and
+// were the NVFP4 GEMM2's bottleneck (6.8 -> 4.5 ms without them).
+__device__ __forceinline__ void tma_store_box(uint8_t* stage, int* nstore, const CUtensorMap* tmD,
+                                              const uint32_t* pk, int lane, bool store, int col, int row) {
+  uint8_t* sb = stage + (*nstore & 1) * 2048;
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+  __syncwarp();
+#pragma unroll
+  for (int w = 0; w < 4; ++w)
+    *reinterpret_cast<uint4*>(sb + lane * 64 + ((w ^ ((lane >> 1) & 3)) << 4)) =
+        make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const bool any = __any_sync(0xffffffffu, store);
+  if (lane == 0 && any) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmD)),
+                 "r"(col), "r"(row), "r"(smem_u32(sb))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  ++*nstore;
+}
+
 // NVFP4 tiles start at column `start` (mod the tile width) and arrive on
 // `part` after the first two 32-column chunks: those cover the columns the
 // other accumulator overlaps.
@@ -374,7 +399,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
         const float h1 = __fdividef(g1, 1.0f + __expf(-g1)) * u[2 * j + 1];
         pk[j] = pack_bf16(h0, h1);
       }
-      if (store) {
+      if (stage != nullptr)
+        tma_store_box(stage, nstore, tmD, pk, lane, store, nb * 128 + c, int(int64_t(mb) * BM + q * 32));
+      else if (store) {
         uint4* o4 = reinterpret_cast<uint4*>(out + c);
 #pragma unroll
         for (int w = 0; w < 4; ++w)
@@ -410,28 +437,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
 #pragma unroll
       for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
       if (stage != nullptr) {
-        // TMA store: the warp's 32 rows x 32 columns (2 KB) go through a
-        // double-buffered SWIZZLE_64B smem box; 16-byte stores of 32
-        // different rows straight from registers cost one L1 wavefront each
-        // and were GEMM2's bottleneck (6.8 -> 4.5 ms without them)
-        uint8_t* sb = stage + (*nstore & 1) * 2048;
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        __syncwarp();
-#pragma unroll
-        for (int w = 0; w < 4; ++w)
-          *reinterpret_cast<uint4*>(sb + lane * 64 + ((w ^ ((lane >> 1) & 3)) << 4)) =
-              make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const bool any = __any_sync(0xffffffffu, store);
-        if (lane == 0 && any) {
-          asm volatile(
-              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                  reinterpret_cast<uint64_t>(tmD)),
-              "r"(nb * BN + c), "r"(int(int64_t(mb) * BM + q * 32)), "r"(smem_u32(sb))
-              : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        ++*nstore;
+        tma_store_box(stage, nstore, tmD, pk, lane, store, nb * BN + c, int(int64_t(mb) * BM + q * 32));
       } else if (store) {
         uint4* o4 = reinterpret_cast<uint4*>(out + c);
 #pragma unroll
@@ -996,10 +1002,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 // accumulators overlap as in the 1-SM kernel. Scale atoms arrive by 2-D TMA
 // (128-byte rows, 16 rows = 2 KB) so that every load of both CTAs completes
 // on the leader's barrier.
-constexpr int P4_STAGES = 5;
+constexpr int P4_STAGES = 4;  // + 16 KB of TMA-store boxes
 constexpr int P4_A = BM * 128, P4_B = 128 * 128, P4_SFA = 2048, P4_SFB = 4096;
 constexpr int P4_STAGE = P4_A + P4_B + P4_SFA + P4_SFB;
-constexpr int P4_SMEM_BYTES = P4_STAGES * P4_STAGE + 1024 + 256 + 2048;
+constexpr int P4_SMEM_BYTES = P4_STAGES * P4_STAGE + 4 * 4096 + 1024 + 256 + 2048;
 
 __device__ __forceinline__ void tc_mma_pair_fp4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                                 uint32_t idesc_v, uint32_t accum, uint32_t sfa,
@@ -1022,7 +1028,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                                  const __grid_constant__ CUtensorMap tmB1,
                                  const __grid_constant__ CUtensorMap tmSA,
                                  const __grid_constant__ CUtensorMap tmSB0,
-                                 const __grid_constant__ CUtensorMap tmSB1, GemmArgs p) {
+                                 const __grid_constant__ CUtensorMap tmSB1,
+                                 const __grid_constant__ CUtensorMap tmD, GemmArgs p) {
   constexpr bool SWIGLU = MODE == kSwiGLU4;
   constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(256 >> 4) << 24);
   extern __shared__ uint8_t smem_raw[];
@@ -1032,7 +1039,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   auto sB = [&](int st) { return smem + st * P4_STAGE + P4_A; };
   auto sSA = [&](int st) { return smem + st * P4_STAGE + P4_A + P4_B; };
   auto sSB = [&](int st) { return smem + st * P4_STAGE + P4_A + P4_B + P4_SFA; };
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P4_STAGES * P4_STAGE);
+  uint8_t* sStage = smem + P4_STAGES * P4_STAGE;  // [4 warps][2][2 KB] TMA-store boxes
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + 4 * 4096);
   uint64_t* empty = full + P4_STAGES;
   uint64_t* tfull = empty + P4_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -1163,6 +1171,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       nsa = int64_t(m) * BM + et < p.m_limit ? __ldg(p.a_scale + int64_t(m) * BM + et) : 1.0f;
     };
     if (cid < num_tiles) fetch_scales(cid);
+    int nstore = 0;  // TMA-store boxes issued by this warp (buffer parity)
     int local = 0;
     for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
       int mp, nb;
@@ -1178,11 +1187,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       asm volatile("bar.sync 1, 128;" ::: "memory");
       epilogue_tile<MODE>(p, 2 * mp + int(rank), nb,
                           tmem_base + (uint32_t(q * 32) << 16) + uint32_t(a) * FP4_ACC1, q, lane,
-                          a == 0 ? (SWIGLU ? 64 : 192) : 0, nullptr, ssc, sa, tpart_cl0 + uint32_t(a) * 8u);
+                          a == 0 ? (SWIGLU ? 64 : 192) : 0, nullptr, ssc, sa, tpart_cl0 + uint32_t(a) * 8u,
+                          sStage + q * 4096, &nstore, &tmD);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_cl0 + uint32_t(a) * 8u);
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
   tc_fence_before();
   cluster_sync_all();
@@ -1340,9 +1351,11 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
     int g = max_tiles < cap ? max_tiles : cap;
     g = g < 2 ? 2 : (g & ~1);
     if (mode == kSwiGLU4)
-      grouped_gemm_pair_fp4_kernel<kSwiGLU4><<<g, 256, P4_SMEM_BYTES, st>>>(a, b0, b1, sf[0], sf[1], sf[2], args);
+      grouped_gemm_pair_fp4_kernel<kSwiGLU4><<<g, 256, P4_SMEM_BYTES, st>>>(a, b0, b1, sf[0], sf[1], sf[2], sf[3],
+                                                                            args);
     else
-      grouped_gemm_pair_fp4_kernel<kPlain4><<<g, 256, P4_SMEM_BYTES, st>>>(a, b0, b1, sf[0], sf[1], sf[2], args);
+      grouped_gemm_pair_fp4_kernel<kPlain4><<<g, 256, P4_SMEM_BYTES, st>>>(a, b0, b1, sf[0], sf[1], sf[2], sf[3],
+                                                                           args);
     return;
   }
   if (mode == kSwiGLU4 || mode == kPlain4) {  // NVFP4 1-SM kernel

@@ -84,6 +84,8 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     // where the pair measured 6.04 -> 7.95 ms. DWDP_FP4_PAIR=0 disables.
     const char* f4 = std::getenv("DWDP_FP4_PAIR");
     fp4_pair_ = fp4_ && (f4 ? f4[0] == '1' : true) ? 1 : 0;
+    const char* f42 = std::getenv("DWDP_FP4_PAIR2");
+    fp4_pair2_ = fp4_pair_ && f42 && f42[0] == '1' ? 1 : 0;
     if (fp4_pair_) row_align_ = 256;
   }
   ntens_ = fp4_ ? 9 : fp8_ ? 6 : 3;
@@ -204,6 +206,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     tm_sf_h_ = make_tmap_sf(hsf_, int64_t(max_rows_) * f_ / 16);
     for (int t = 0; t < 3; ++t) tm_sf_w_[t] = make_tmap_sf(sfarena_[t], int64_t(tsb(6 + t)) * nslots_);
     tm_o_ = make_tmap_out(xperm_, max_rows_, h_);  // O (bf16) overwrites X_perm4
+    tm_h_o_ = make_tmap_out(hbuf_, max_rows_, f_);
   }
 
   DWDP_CUDA(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
@@ -686,16 +689,17 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 0, mbseg_,
                 nullptr, xs_, sarena_[0], sarena_[1], pair4 ? 1 : 0, raster_, mbrows_, nullptr, 0,
                 xsf_, sfarena_[0], sfarena_[1]};
-    const CUtensorMap sf1[3] = {tm_sf_x_, tm_sf_w_[0], tm_sf_w_[1]};
+    const CUtensorMap sf1[4] = {tm_sf_x_, tm_sf_w_[0], tm_sf_w_[1], tm_h_o_};
     launch_grouped_gemm(GEMM_SWIGLU_FP4, tm_x8_, tm_x8_, tm_gate_, tm_up_, g1,
                         int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st, sf1);
     launch_quant_rows_nvfp4(hbuf_, max_rows_, f_, meta_, h8_, sfl_, hsf_, hs_, st);
     mark(2);
     GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
-                nullptr, hs_, sarena_[2], nullptr, 0, raster_, mbrows_, nullptr, 0,
+                nullptr, hs_, sarena_[2], nullptr, pair4 && fp4_pair2_ ? 1 : 0, raster_, mbrows_, nullptr, 0,
                 hsf_, sfarena_[2], nullptr};
     const CUtensorMap sf2[4] = {tm_sf_h_, tm_sf_w_[2], tm_sf_w_[2], tm_o_};
-    launch_grouped_gemm(GEMM_PLAIN_FP4, tm_h8_, tm_h8_, tm_down_, tm_down_, g2,
+    const CUtensorMap& tmd4 = pair4 && fp4_pair2_ ? tm_down_p_ : tm_down_;
+    launch_grouped_gemm(GEMM_PLAIN_FP4, tm_h8_, tm_h8_, tmd4, tmd4, g2,
                         int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st, sf2);
     mark(3);
     launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);

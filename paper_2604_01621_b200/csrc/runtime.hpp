@@ -149,6 +149,8 @@ class Ctx {
   CUtensorMap tm_sf_x_, tm_sf_h_, tm_sf_w_[3];  // nvfp4 scale atoms for the CTA-pair kernel
   CUtensorMap tm_dep_sfx_, tm_dep_sfh_;
   CUtensorMap tm_o_, tm_dep_o_;                 // nvfp4 GEMM2 output maps (TMA store)
+  CUtensorMap tm_h_o_, tm_dep_h_o_;             // nvfp4 GEMM1 (CTA pair) output maps
+  int fp4_pair2_ = 0;                           // GEMM2 on CTA pairs too (DWDP_FP4_PAIR2)
   float *xs_ = nullptr, *hs_ = nullptr;  // per-row scales of X_perm8 / H8
   CUtensorMap tm_x8_, tm_h8_;
   std::vector<void*> ipc_opened_;
