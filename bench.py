@@ -248,6 +248,12 @@ def main():
     # nominal 2x / 4x of the measured sustained bf16 peak)
     wb = 2.0 if args.dtype == "bf16" else 1.0 if fp8 else 0.5 + 1.0 / 16
     rate = {"bf16": 1, "fp8": 2, "nvfp4": 4}[args.dtype]
+    rate_src = "nominal"
+    lt = os.path.join(ROOT, "profiles", "r1_lt_peaks.json")  # cuBLASLt fp8 / nvfp4 vs bf16 on B200
+    if args.dtype != "bf16" and os.path.exists(lt):
+        with open(lt) as fh:
+            rate = json.load(fh)[{"fp8": "fp8_over_bf16", "nvfp4": "nvfp4_over_bf16"}[args.dtype]]
+        rate_src = "measured cuBLASLt"
 
     cfg = D.DwdpConfig(num_layers=layers, rank=rank, group_size=world, device=local,
                        engine={"pull": D.ENGINE_PULL, "hybrid": D.ENGINE_HYBRID}.get(args.engine,
@@ -418,8 +424,8 @@ def main():
         tpk = pk["bf16_tflops_sustained"] * rate
         roof = {"bound": "tensor", "kernel": "grouped GEMM1 (gate/up + SwiGLU, tcgen05)",
                 "achieved": achieved, "peak": tpk, "unit": "TFLOP/s", "frac": achieved / tpk,
-                "peak_source": pk["source"] + (f", sustained bf16 x {rate} ({args.dtype} dense rate; no "
-                                               f"measured {args.dtype} figure)" if rate > 1
+                "peak_source": pk["source"] + (f", sustained bf16 x {rate} ({rate_src} {args.dtype}/bf16 "
+                                               f"dense-GEMM ratio, profiles/r1_lt_peaks.json)" if rate != 1
                                                else ", sustained bf16"),
                 "flops_per_launch": g1_flops / max(len(recs), 1),
                 "gemm2_tflops": g2_flops / (g2_ns * 1e-9) / 1e12 if g2_ns else None,
