@@ -54,6 +54,9 @@ def main():
                            "engine": d["config"].get("prefetch_engine"),
                            "prefetch_gbs": (d.get("prefetch") or {}).get("gbs"),
                            "step_roofline_frac": (d.get("step_roofline") or {}).get("frac"),
+                           "attention_ms_per_layer": (d.get("attention") or {}).get("ms_per_layer"),
+                           "moe_ms_per_layer": (d.get("kernel_ms_per_layer") or {}).get("moe"),
+                           "extra": a.extra,
                            "clocks": d.get("clocks")}
                 out.write(json.dumps(rec) + "\n")
                 out.flush()
