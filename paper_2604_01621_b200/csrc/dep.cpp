@@ -140,6 +140,7 @@ void Ctx::dep_reserve(int64_t rows) {
       dep_xsf_ = static_cast<uint8_t*>(dalloc(size_t(rows) * h_ / 16, nullptr));
       dep_hsf_ = static_cast<uint8_t*>(dalloc(size_t(rows) * f_ / 16, nullptr));
       tm_dep_sfx_ = make_tmap_sf(dep_xsf_, rows * h_ / 16);
+      tm_dep_sfh_ = make_tmap_sf(dep_hsf_, rows * f_ / 16);
       tm_dep_o_ = make_tmap_out(dep_recv_, rows, h_);
       tm_dep_h_o_ = make_tmap_out(dep_h_, rows, f_);
     }
