@@ -331,6 +331,68 @@ __global__ void __launch_bounds__(256) quant_rows_nvfp4_kernel(const uint16_t* _
   if (lane == 0) scales[r] = s;
 }
 
+// Short rows (K <= 2048, K % 256 == 0; GEMM2's H): lane-interleaved, so every
+// load and code store of the warp is one contiguous 512 / 128-byte run (the
+// group-per-lane layout above reads 16 B from each of 32 lines per
+// instruction). A 16-element block spans a lane pair (block max by one
+// shuffle); lanes 8c..8c+7 hold the four blocks of one 64-column chunk, whose
+// scale word lane 8c writes. Same float sequence per element as nvfp4_group.
+template <int NJ>
+__global__ void __launch_bounds__(256) quant_rows_nvfp4_il_kernel(const uint16_t* __restrict__ src,
+                                                                  int64_t max_rows,
+                                                                  const int32_t* __restrict__ meta,
+                                                                  uint8_t* __restrict__ dst,
+                                                                  uint8_t* __restrict__ sfl,
+                                                                  float* __restrict__ scales) {
+  constexpr int64_t K = int64_t(NJ) * 256;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t rows = meta ? int64_t(meta[0]) * 128 : max_rows;
+  if (r >= rows) return;
+  const uint4* row = reinterpret_cast<const uint4*>(src + r * K);
+  uint4 q[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) q[j] = __ldg(row + j * 32 + lane);
+  float amax = 0.0f;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const uint32_t w[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      amax = fmaxf(amax, fmaxf(fabsf(__uint_as_float(w[i] << 16)), fabsf(__uint_as_float(w[i] & 0xffff0000u))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const float s = nvfp4_row_scale(amax);
+  const float s6 = __fmul_rn(6.0f, s);
+  uint32_t* codes = reinterpret_cast<uint32_t*>(dst + r * (K / 2));
+  uint32_t* sfw = reinterpret_cast<uint32_t*>(sfl + r * (K / 16));
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    float v[8];
+    const uint32_t w[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+    float bmax = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) bmax = fmaxf(bmax, fabsf(v[i]));
+    bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, 1));
+    const uint32_t sf = f32_to_e4m3(__fdiv_rn(bmax, s6));
+    const float ds = __fmul_rn(e4m3_to_f32(sf), s);
+    const float inv = ds > 0.0f ? __frcp_rn(ds) : 0.0f;
+    codes[j * 32 + lane] = e2m1x8(v, inv);
+    // scale bytes of blocks 2m (lane 2m) -> word of chunk lane/8
+    uint32_t word = sf << (8 * ((lane >> 1) & 3));
+    word |= __shfl_xor_sync(0xffffffffu, word, 2);
+    word |= __shfl_xor_sync(0xffffffffu, word, 4);
+    if ((lane & 7) == 0) sfw[j * 4 + (lane >> 3)] = word;
+  }
+  if (lane == 0) scales[r] = s;
+}
+
 // H (bf16, rows < meta[0]*128) -> e4m3 + per-row scale (GEMM2's A operand).
 __global__ void __launch_bounds__(256) quant_rows_fp8_kernel(const uint16_t* __restrict__ src,
                                                              int64_t max_rows, int64_t K,
@@ -1481,8 +1543,15 @@ void launch_nvfp4_sf_relayout(const uint8_t* lin, uint8_t* atoms, int64_t max_ro
 void launch_quant_rows_nvfp4(const uint16_t* src, int64_t max_rows, int64_t K, const int32_t* meta,
                              uint8_t* dst, uint8_t* sf_lin, uint8_t* sf, float* scales, cudaStream_t st) {
   if (max_rows <= 0) return;
-  quant_rows_nvfp4_kernel<<<unsigned((max_rows + 7) / 8), 256, 0, st>>>(src, max_rows, K, meta, dst,
-                                                                        sf_lin, scales);
+  const unsigned grid = unsigned((max_rows + 7) / 8);
+  if (K == 2048)
+    quant_rows_nvfp4_il_kernel<8><<<grid, 256, 0, st>>>(src, max_rows, meta, dst, sf_lin, scales);
+  else if (K == 1024)
+    quant_rows_nvfp4_il_kernel<4><<<grid, 256, 0, st>>>(src, max_rows, meta, dst, sf_lin, scales);
+  else if (K == 256)
+    quant_rows_nvfp4_il_kernel<1><<<grid, 256, 0, st>>>(src, max_rows, meta, dst, sf_lin, scales);
+  else
+    quant_rows_nvfp4_kernel<<<grid, 256, 0, st>>>(src, max_rows, K, meta, dst, sf_lin, scales);
   launch_nvfp4_sf_relayout(sf_lin, sf, max_rows, K, meta, st);
 }
 

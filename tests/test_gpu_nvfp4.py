@@ -55,7 +55,7 @@ def _rand_bf16(R, K, seed, dev, scale=1.0):
     return x.to(torch.bfloat16)
 
 
-@pytest.mark.parametrize("R,K", [(1, 256), (300, 512), (129, 7168)])
+@pytest.mark.parametrize("R,K", [(1, 256), (300, 512), (129, 7168), (77, 2048), (130, 1024)])
 def test_nvfp4_quant_bit_exact(dev, orc, R, K):
     x = _rand_bf16(R, K, R + K, dev)
     codes, sf, s = D.quant_nvfp4(x)
