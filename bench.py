@@ -183,6 +183,9 @@ def main():
     ap.add_argument("--oversubscribe", action="store_true",
                     help="code-path test: WORLD_SIZE > GPUs (ranks share GPUs, gloo, no DEP); "
                          "numbers from such a run are not bench values")
+    ap.add_argument("--extra-redundancy", type=int, default=0,
+                    help="experts each rank owns beyond E/N (build_placement extra; fewer bytes to pull, "
+                         "more HBM per rank; SURVEY.md section 8(f) row 3)")
     ap.add_argument("--attention", action="store_true",
                     help="run a DeepSeek-V3 MLA prefill block (library ops) before every MoE layer, "
                          "in DWDP and DEP alike: the paper's prefetch window MoE(l) + Attention(l+1)")
@@ -256,6 +259,7 @@ def main():
         rate_src = "measured cuBLASLt"
 
     cfg = D.DwdpConfig(num_layers=layers, rank=rank, group_size=world, device=local,
+                       extra_redundancy=args.extra_redundancy if world > 1 else 0,
                        engine={"pull": D.ENGINE_PULL, "hybrid": D.ENGINE_HYBRID}.get(args.engine,
                                                                                       D.ENGINE_COPY),
                        tdm=0 if args.no_tdm else 1, slice_size=args.slice_size,
@@ -345,13 +349,15 @@ def main():
             best = None
             for name, eid in (("copy", D.ENGINE_COPY), ("pull", D.ENGINE_PULL), ("hybrid", D.ENGINE_HYBRID)):
                 ctx.set_engine(eid)
-                barrier()
-                p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                p0.record(stream)
-                step(toks[0][rank], 0)
-                p1.record(stream)
-                torch.cuda.synchronize()
-                t_eng = allmax(p0.elapsed_time(p1))
+                t_eng = float("inf")
+                for it in range(2):  # best of two steps: one step alone is noisy under the power cap
+                    barrier()
+                    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    p0.record(stream)
+                    step(toks[it][rank], it)
+                    p1.record(stream)
+                    torch.cuda.synchronize()
+                    t_eng = min(t_eng, allmax(p0.elapsed_time(p1)) / max(1, max(toks[it])))
                 ctx.records()
                 if best is None or t_eng < best[0]:
                     best = (t_eng, name, eid)
@@ -529,7 +535,7 @@ def main():
     # with each step's heaviest rank
     f_tok = 2.0 * h * (3 * k * f + 3 * R1["fs"] + R1["E"])
     p_peak = pk["bf16_tflops_sustained"] * 1e12 * rate
-    c_loc = -(-R1["E"] // world)
+    c_loc = min(R1["E"], -(-R1["E"] // world) + args.extra_redundancy) if world > 1 else R1["E"]
     b_rem = (R1["E"] - c_loc) * 3.0 * h * f * wb if world > 1 else 0.0
     t_tensor = sum(layers * max(toks[it]) * f_tok / p_peak for it in range(args.warmup, iters))
     t_link = args.steps * layers * b_rem / 900e9
@@ -564,7 +570,7 @@ def main():
                 D.r1_model(layers, wb),
                 D.GpuSpec(pk["bf16_tflops_sustained"] * 1e12 * rate, pk["hbm_gbs"] * 1e9,
                           900e9),
-                D.build_placement(R1["E"], world), int(mean_t))
+                D.build_placement(R1["E"], world, args.extra_redundancy), int(mean_t))
             acct["analytic_compare"]["tokens_per_rank"] = mean_t
             # the same model calibrated with this run's
             # measured rates (grouped-GEMM TFLOP/s, in-step prefetch GB/s) beside
@@ -573,7 +579,7 @@ def main():
             link = pf_bytes / pf_ns * 1e9 if pf_ns else 900e9
             cal = D.analytic_compare(D.r1_model(layers, wb),
                                      D.GpuSpec(gemm_tf, pk["hbm_gbs"] * 1e9, link),
-                                     D.build_placement(R1["E"], world), int(mean_t))
+                                     D.build_placement(R1["E"], world, args.extra_redundancy), int(mean_t))
             cal.update(gemm_tflops_measured=gemm_tf / 1e12, prefetch_gbs_measured=link / 1e9,
                        measured_dwdp_over_dep=(dep or {}).get("dwdp_over_dep"))
             acct["analytic_compare_calibrated"] = cal
@@ -603,12 +609,13 @@ def main():
                        "isl": 8192, "seq_len_cv": args.cv,
                        "tokens_per_step_rank0": [toks[it][0] for it in range(args.warmup, iters)],
                        "weights": ("one 22.5 GB set aliased by all layers (N=1)" if world == 1
-                                   else f"{256 // world} owned experts/layer/GPU, {layers} layers"),
+                                   else f"{min(256, -(-256 // world) + args.extra_redundancy)} owned experts/layer/GPU, {layers} layers"),
                        "prefetch_engine": (engines if world > 1 else None),
                        "slice_size": args.slice_size if world > 1 else None,
                        "l2": "inputs larger than L2: {} GB of expert weights per layer".format(
                            "11.3 (e4m3)" if fp8 else "6.3 (nvfp4)" if fp4 else "22.5 (bf16)"),
                        "attention_block": bool(args.attention),
+                       "extra_redundancy": args.extra_redundancy,
                        "parallelism": f"dwdp{world}"},
             "tokens_per_s_per_gpu": value / world,
             "exposed_prefetch_ms_per_layer": exposed_ms,
