@@ -6,15 +6,9 @@ import math
 import pytest
 import torch
 
-from paper_2604_01621_b200.attention import MlaAttention, split_sequences
+from paper_2604_01621_b200.attention import MlaAttention
 
 pytestmark = pytest.mark.gpu
-
-
-def test_split_sequences():
-    assert split_sequences(10, 3) == [4, 3, 3]
-    assert split_sequences(5, 0) == [5]
-    assert split_sequences(0, 4) == []
 
 
 def test_mla_matches_fp32_block_causal():
