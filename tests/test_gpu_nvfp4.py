@@ -147,12 +147,13 @@ def test_moe_forward_nvfp4_single_cta(dev, orc, monkeypatch):
 
 def test_dwdp_nvfp4_group_of_two_matches_all_local(dev):
     """NVFP4 arenas (codes + row scales + block scales) prefetched over both
-    engines give bit-identical outputs to the all-local NVFP4 model."""
+    engines, and with the merged-weight fetch (D2D merge of all nine
+    tensors), give bit-identical outputs to the all-local NVFP4 model."""
     kw = dict(MID, weight_dtype=D.WEIGHT_NVFP4)
     full = D.DwdpContext(D.DwdpConfig(**kw))
     full.init_weights()
-    for engine in (D.ENGINE_COPY, D.ENGINE_PULL):
-        ranks = [D.DwdpContext(D.DwdpConfig(**kw, rank=r, group_size=2, engine=engine,
+    for engine, merge in ((D.ENGINE_COPY, 1), (D.ENGINE_PULL, 1), (D.ENGINE_COPY, 0)):
+        ranks = [D.DwdpContext(D.DwdpConfig(**kw, rank=r, group_size=2, engine=engine, merge_elim=merge,
                                             slice_size=1 << 18)) for r in range(2)]
         for c in ranks:
             c.init_weights()
