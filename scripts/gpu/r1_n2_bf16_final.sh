@@ -1,0 +1,9 @@
+# Config-4 sweep at N=2, bf16, final build (step-timed engine choice).
+mkdir -p gpurun_out
+timeout 3300 python scripts/sweep.py --gpus 2 --cv 0,0.1,0.2,0.3 --tokens 32768,65536 --steps 4 --warmup 3 --out gpurun_out/sweep_n2_bf16_final.jsonl > gpurun_out/sweep_n2_bf16_final.log 2>&1; echo "sweep rc=$?"
+cat gpurun_out/sweep_n2_bf16_final.jsonl | python -c "
+import json,sys
+for l in sys.stdin:
+    d=json.loads(l)
+    if 'error' in d: print('ERR', d); continue
+    print(d['mnt'], d['cv'], round(d['dwdp_tokens_per_s_per_gpu']), round(d['dep_tokens_per_s_per_gpu']), round(d['dwdp_over_dep'],3), round(d['exposed_prefetch_ms_per_layer'],3), d['engine'][0], round(d['prefetch_gbs'] or 0), round(d['step_roofline_frac'],3), d['clocks']['sm_mhz'])"
