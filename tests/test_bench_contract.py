@@ -54,3 +54,13 @@ def test_reference_arm_line():
         assert k in d, k
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["cores"] >= 1
+
+
+def test_bench_line_nvfp4_and_attention():
+    """The NVFP4 arm (measured-ratio peak, nvfp4 dtype label) and the attention
+    window keep the same contract."""
+    d = _run("--steps", "2", "--warmup", "3", "--layers", "2", "--tokens", "8192", "--dtype", "nvfp4",
+             "--attention", "--no-cpu-baseline")
+    assert d["dtype"].startswith("nvfp4") and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["roofline"]["unit"] == "TFLOP/s" and 0 < d["roofline"]["frac"] < 1.5
+    assert d["attention"]["ms_per_layer"] > 0 and d["config"]["attention_block"] is True
