@@ -410,19 +410,24 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
       release(i);
     }
   } else {
-    // plain: the TMEM load of chunk i+1 is in flight while chunk i is scaled,
-    // packed and stored (GEMM2's short K leaves the drain on the critical path)
+    // plain: chunks 0 and 1 (the columns the other accumulator overlaps, for
+    // NVFP4) are read first and released before any processing; afterwards
+    // the TMEM load of chunk i+2 is in flight while chunk i is scaled, packed
+    // and stored (GEMM2's short K leaves the drain on the critical path)
     uint16_t* out = p.D + row * p.ldd + nb * BN;
-    uint32_t buf[2][32];
+    constexpr int NCH = BN / 32;
+    uint32_t buf[3][32];
     tmem_ld32_issue(tbase + (start & (BN - 1)), buf[0]);
+    tmem_ld32_issue(tbase + ((start + 32) & (BN - 1)), buf[1]);
     tmem_ld_wait();
+    release(1);
 #pragma unroll
-    for (int i = 0; i < BN / 32; ++i) {
+    for (int i = 0; i < NCH; ++i) {
       const int c = (start + 32 * i) & (BN - 1);
-      if (i + 1 < BN / 32) tmem_ld32_issue(tbase + ((start + 32 * (i + 1)) & (BN - 1)), buf[(i + 1) & 1]);
+      if (i + 2 < NCH) tmem_ld32_issue(tbase + ((start + 32 * (i + 2)) & (BN - 1)), buf[(i + 2) % 3]);
       float v[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(buf[i & 1][j]);
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(buf[i % 3][j]);
       if (FP8) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
@@ -444,8 +449,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
         for (int w = 0; w < 4; ++w)
           o4[w] = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
       }
-      tmem_ld_wait();  // chunk i+1 landed (and every read of chunks <= i is done)
-      release(i);
+      if (i + 2 < NCH) tmem_ld_wait();  // chunk i+2 landed
     }
   }
 }
