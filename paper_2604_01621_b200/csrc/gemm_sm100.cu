@@ -369,13 +369,30 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
       }
     }
   } else if (SWIGLU) {
+    // the gate/up columns of chunks 0 and 1 (NVFP4: the overlapped ones) are
+    // read and released before processing; afterwards chunk i+1 loads while
+    // chunk i is processed
     uint16_t* out = p.D + row * p.ldd + nb * 128;
-#pragma unroll 1
+    uint32_t gb[2][32], ub[2][32];
+    tmem_ld32_issue(tbase + (start & 127), gb[0]);
+    tmem_ld32_issue(tbase + 128 + (start & 127), ub[0]);
+    tmem_ld32_issue(tbase + ((start + 32) & 127), gb[1]);
+    tmem_ld32_issue(tbase + 128 + ((start + 32) & 127), ub[1]);
+    tmem_ld_wait();
+    release(1);
+#pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int c = (start + 32 * i) & 127;
+      if (i >= 1 && i + 1 < 4) {
+        tmem_ld32_issue(tbase + ((start + 32 * (i + 1)) & 127), gb[(i + 1) & 1]);
+        tmem_ld32_issue(tbase + 128 + ((start + 32 * (i + 1)) & 127), ub[(i + 1) & 1]);
+      }
       float g[32], u[32];
-      tmem_ld32(tbase + c, g);
-      tmem_ld32(tbase + 128 + c, u);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        g[j] = __uint_as_float(gb[i & 1][j]);
+        u[j] = __uint_as_float(ub[i & 1][j]);
+      }
       if (FP8) {  // weight-row scales: 16-byte broadcast loads
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
@@ -407,7 +424,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
         for (int w = 0; w < 4; ++w)
           o4[w] = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
       }
-      release(i);
+      if (i >= 1 && i + 1 < 4) tmem_ld_wait();  // chunk i+1 landed
     }
   } else {
     // plain: chunks 0 and 1 (the columns the other accumulator overlaps, for
