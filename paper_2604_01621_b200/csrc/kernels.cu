@@ -1263,22 +1263,37 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
   __syncthreads();
   const bool shared = S != nullptr;
   const int64_t segs = h / 8;
+  // Every row's 16-byte load of a batch (up to 8 routed rows, the shared row
+  // and the residual) is issued before the first FMA: one load in flight per
+  // thread left the kernel latency-bound below the HBM rate. The FMA order
+  // (routed rows in j order, then shared, then residual) is unchanged.
+  constexpr int CB = 8;
   for (int64_t s = threadIdx.x; s < segs; s += blockDim.x) {
     float acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
-    for (int j = 0; j < k; ++j) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(O + int64_t(srow[j]) * h) + s);
-      const uint32_t u[4] = {v.x, v.y, v.z, v.w};
-      const float wj = sw[j];
+    uint4 vs = make_uint4(0, 0, 0, 0), vr = make_uint4(0, 0, 0, 0);
+    if (shared) vs = __ldg(reinterpret_cast<const uint4*>(S + int64_t(srow[TOPK_MAXK]) * h) + s);
+    if (resid) vr = __ldg(reinterpret_cast<const uint4*>(resid + t * h) + s);
+    for (int j0 = 0; j0 < k; j0 += CB) {
+      uint4 v[CB];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        acc[2 * q] = __fmaf_rn(wj, __uint_as_float(u[q] << 16), acc[2 * q]);
-        acc[2 * q + 1] = __fmaf_rn(wj, __uint_as_float(u[q] & 0xffff0000u), acc[2 * q + 1]);
+      for (int jj = 0; jj < CB; ++jj)
+        if (j0 + jj < k) v[jj] = __ldg(reinterpret_cast<const uint4*>(O + int64_t(srow[j0 + jj]) * h) + s);
+#pragma unroll
+      for (int jj = 0; jj < CB; ++jj) {
+        if (j0 + jj >= k) break;
+        const uint32_t u[4] = {v[jj].x, v[jj].y, v[jj].z, v[jj].w};
+        const float wj = sw[j0 + jj];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc[2 * q] = __fmaf_rn(wj, __uint_as_float(u[q] << 16), acc[2 * q]);
+          acc[2 * q + 1] = __fmaf_rn(wj, __uint_as_float(u[q] & 0xffff0000u), acc[2 * q + 1]);
+        }
       }
     }
     if (shared) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(S + int64_t(srow[TOPK_MAXK]) * h) + s);
+      const uint4 v = vs;
       const uint32_t u[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -1287,7 +1302,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
       }
     }
     if (resid) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(resid + t * h) + s);
+      const uint4 v = vr;
       const uint32_t u[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
