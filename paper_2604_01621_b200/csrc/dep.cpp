@@ -341,13 +341,13 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   } else if (nblocks > 0 && fp8_) {
     const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_i8(x8 + send_total * h_, T, h_, 128) : tm_dep_x8_;
     GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1, dep_seg_,
-                nullptr, dep_xs_, sarena_[0], sarena_[1], gemm_pair_, raster_, dep_mbrows_};
+                nullptr, dep_xs_, sarena_[0], sarena_[1], gemm1_pair_, raster_, dep_mbrows_};
     launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_dep_x8_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
     launch_quant_rows_fp8(dep_h_, dep_cap_rows_, f_, dmeta, dep_h8_, dep_hs_, st);
   } else if (nblocks > 0) {
     const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_dep_recv_;
     GemmArgs g1{int(h_), int(f_), int(f_), E_, dmb, stab, dmeta, dep_h_, f_, INT64_MAX, 1, dep_seg_,
-                nullptr, nullptr, nullptr, nullptr, gemm_pair_, raster_, dep_mbrows_};
+                nullptr, nullptr, nullptr, nullptr, gemm1_pair_, raster_, dep_mbrows_};
     launch_grouped_gemm(GEMM_SWIGLU, tm_dep_recv_, tm_x, tm_gate_, tm_up_, g1, int(nblocks * (f_ / 128)), st);
   }
   mark(&rec.k[2]);

@@ -63,16 +63,24 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   fp8_ = c.weight_dtype == DWDP_WEIGHT_FP8;
   fp4_ = c.weight_dtype == DWDP_WEIGHT_NVFP4;
   esz_ = fp8_ || fp4_ ? 1 : 2;
-  // The expert GEMMs run on the 1-SM kernel by default. The CTA-pair kernel
-  // (cta_group::2, 256-row segments; DWDP_GEMM_PAIR=1) is 2-10% faster per
-  // SM clock, but on the power-capped B200 it drew the clock down from ~1.3
-  // to ~0.94 GHz and the full step measured 9% slower on the same box
-  // (scripts/gpu/r1_ab_pair.sh: 144K vs 158K tokens/s).
+  // GEMM1 runs on the 1-SM kernel by default. With GEMM1 on the CTA-pair
+  // kernel too (cta_group::2, 256-row segments; DWDP_GEMM_PAIR=1) each GEMM
+  // is 2-10% faster per SM clock, but on the power-capped B200 it drew the
+  // clock down from ~1.3 to ~0.94 GHz and the full step measured 9% slower
+  // on the same box (scripts/gpu/r1_ab_pair.sh: 144K vs 158K tokens/s).
   {
     const char* env = std::getenv("DWDP_GEMM_PAIR");
-    // DWDP_GEMM_PAIR=1: every GEMM on CTA pairs; =2: GEMM1 only
-    gemm_pair_ = env && (env[0] == '1' || env[0] == '2') ? 1 : 0;
-    gemm2_pair_ = env && env[0] == '1' ? 1 : 0;
+    // DWDP_GEMM_PAIR=1: every GEMM on CTA pairs; =2: GEMM1 only; =3: GEMM2
+    // and the router GEMM only (GEMM1 on the 1-SM kernel, 256-row segments);
+    // unset or 0: every GEMM on the 1-SM kernel. =3 cut GEMM2 from 17.0 to
+    // 13.3 ms per layer (half the B bytes per CTA; the 1-SM GEMM2 is L2-feed
+    // bound at 73% tensor-pipe active) but the step moved +1.3/+3.9% on one
+    // box and -3.3/-2.2% on another, where the SM clock fell from 1.24 to
+    // 1.0 GHz under sw_power_cap (scripts/gpu/r1_ab_pair3.sh,
+    // r1_pair3_confirm.sh), so it stays opt-in.
+    gemm1_pair_ = env && (env[0] == '1' || env[0] == '2') ? 1 : 0;
+    gemm2_pair_ = env && (env[0] == '1' || env[0] == '3') ? 1 : 0;
+    gemm_pair_ = gemm1_pair_ || gemm2_pair_;
     row_align_ = gemm_pair_ ? 256 : 128;
     const char* r = std::getenv("DWDP_RASTER");  // experiments: m / n (default auto)
     raster_ = r ? (r[0] == 'm' ? 1 : r[0] == 'n' ? 2 : 0) : 0;
@@ -713,7 +721,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
                                   nullptr, meta_, nullptr, scratch_, st, x8, xs_, align, mbrows_);
     mark(1);
     GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 0, mbseg_,
-                nullptr, xs_, sarena_[0], sarena_[1], pair ? gemm_pair_ : 0, raster_, mbrows_};
+                nullptr, xs_, sarena_[0], sarena_[1], pair ? gemm1_pair_ : 0, raster_, mbrows_};
     launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_x8_, tm_x8_, tm_gate_, tm_up_, g1,
                         int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
     launch_quant_rows_fp8(hbuf_, max_rows_, f_, meta_, h8_, hs_, st);
@@ -741,7 +749,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   // GEMM1 instead of 26 GB -- the gathered rows are not reused from L2
   // across the expert's 16 n-block tiles the way the contiguous copy is.
   GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_,
-              gather ? srcrow_ : nullptr, nullptr, nullptr, nullptr, pair ? gemm_pair_ : 0, raster_, mbrows_,
+              gather ? srcrow_ : nullptr, nullptr, nullptr, nullptr, pair ? gemm1_pair_ : 0, raster_, mbrows_,
               x, h_};
   launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(2);

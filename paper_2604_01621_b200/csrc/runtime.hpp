@@ -179,7 +179,8 @@ class Ctx {
   uint16_t *xperm_ = nullptr, *hbuf_ = nullptr;
   CUtensorMap tm_gate_, tm_up_, tm_down_, tm_xperm_, tm_h_;
   CUtensorMap tm_down_p_;          // down arena with 128-row boxes (CTA-pair GEMM2)
-  int gemm_pair_ = 0;              // GemmArgs::pair: 0 1-SM, 1 CTA pair (GEMM1)
+  int gemm_pair_ = 0;              // any GEMM on CTA pairs (256-row segments, half-n-block maps)
+  int gemm1_pair_ = 0;             // GemmArgs::pair for GEMM1: 0 1-SM, 1 CTA pair
   int gemm2_pair_ = 0;             // GEMM2 and the router GEMM on CTA pairs too
   int row_align_ = 128;            // expert segment padding (256 with pairs)
   int raster_ = 0;                 // GemmArgs::raster (DWDP_RASTER experiments)

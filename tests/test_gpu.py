@@ -329,11 +329,13 @@ def test_prefetch_handles(dev):
         c.close()
 
 
-@pytest.mark.parametrize("name,mode", [("mid_sigmoid", "1"), ("mid_fp8", "1")])
+@pytest.mark.parametrize("name,mode", [("mid_sigmoid", "1"), ("mid_fp8", "1"), ("mid_sigmoid", "3"),
+                                       ("mid_fp8", "3")])
 def test_gemm_pair_matches_single_cta(dev, monkeypatch, name, mode):
-    """The CTA-pair GEMM (DWDP_GEMM_PAIR=1: cta_group::2, 256-row segments)
-    gives the same layer outputs as the default 1-SM kernel (bf16 and e4m3
-    weights; routing included)."""
+    """The CTA-pair GEMM (cta_group::2, 256-row segments; DWDP_GEMM_PAIR=1 for
+    every GEMM, =3 for GEMM2 and the router only) gives the
+    same layer outputs as the all-1-SM kernels (DWDP_GEMM_PAIR=0; bf16 and
+    e4m3 weights; routing included)."""
     cfg = CONFIGS.get(name) or FP8_CONFIGS[name]
     outs = []
     for pair in (mode, "0"):
