@@ -1140,7 +1140,22 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
       const uint4* src = reinterpret_cast<const uint4*>(x + (t0 + tl) * h);
       const float amax = row_absmax_bf16(src, nch, lane);
       const float s = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
-      for (int64_t c = lane; c < nch; c += 32) {
+      // four 16-byte loads in flight per lane before the quantise + k stores
+      int64_t c0 = lane;
+      for (; c0 + 96 < nch; c0 += 128) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(src + c0 + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t c = c0 + 32 * u;
+          const uint2 q = quant8(v[u], s);
+          for (int j = 0; j < k; ++j)
+            reinterpret_cast<uint2*>(xperm8 + int64_t(rows[tl * k + j]) * h)[c] = q;
+          if (shared) reinterpret_cast<uint2*>(xperm8 + int64_t(shared_row0 + t0 + tl) * h)[c] = q;
+        }
+      }
+      for (int64_t c = c0; c < nch; c += 32) {
         const uint2 q = quant8(__ldg(src + c), s);
         for (int j = 0; j < k; ++j)
           reinterpret_cast<uint2*>(xperm8 + int64_t(rows[tl * k + j]) * h)[c] = q;
