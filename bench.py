@@ -189,6 +189,10 @@ def main():
     ap.add_argument("--attention", action="store_true",
                     help="run a DeepSeek-V3 MLA prefill block (library ops) before every MoE layer, "
                          "in DWDP and DEP alike: the paper's prefetch window MoE(l) + Attention(l+1)")
+    ap.add_argument("--check", action="store_true",
+                    help="after timing (N=1): check layer 0 on the first timed batch against the CPU "
+                         "oracle -- routing of all T tokens bit-exact, 512 sampled rows within 1e-2 "
+                         "(oracle/check.py; the checker, outside every timed region)")
     ap.add_argument("--zipf", type=float, default=0.0,
                     help="expert-routing skew s: router bias -ZIPF_BETA*s*ln(e+1)")
     args = ap.parse_args()
@@ -584,6 +588,16 @@ def main():
                        measured_dwdp_over_dep=(dep or {}).get("dwdp_over_dep"))
             acct["analytic_compare_calibrated"] = cal
 
+    check = None
+    if args.check and world == 1 and not args.decode and not args.profile and args.dtype == "bf16":
+        from oracle import check as CK
+        T0 = toks[args.warmup][rank]
+        bias = None
+        if args.zipf > 0:
+            import numpy as np
+            bias = (-ZIPF_BETA * args.zipf * np.log(np.arange(R1["E"]) + 1.0)).astype(np.float32)
+        check = CK.check_layer(ctx, x[:T0], layer=0, sample_rows=512, seed=T0, bias=bias)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -628,7 +642,7 @@ def main():
             "dep_baseline": dep, "report": acct,
             "hbm_gb": {k2: round(v / 1e9, 2) for k2, v in ctx.memory().items()},
             "attention": attention,
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "check": check,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -572,24 +572,40 @@ typedef struct {
   float* logits;
   int32_t* idx;
   float* wts;
+  int64_t T;
 } route_arg;
 
-static void route_one(void* p, int64_t t) {
+/* Tokens are routed in blocks of RB so each quantised router row is reused
+ * from cache across the block; every logit is still one exact int64 sum. */
+#define RB 8
+static void route_one(void* p, int64_t blk) {
   route_arg* a = (route_arg*)p;
   const int64_t h = a->cfg->hidden;
   const int E = a->cfg->num_experts;
-  float* lg = a->logits + t * E;
-  int32_t* xq = malloc(sizeof(int32_t) * (size_t)h);
-  int ex;
-  quant_row(a->x16 ? a->x16 + t * h : NULL, a->x32 ? a->x32 + t * h : NULL, h, xq, &ex);
+  const int64_t t0 = blk * RB;
+  const int n = (int)(a->T - t0 < RB ? a->T - t0 : RB);
+  int32_t* xq = malloc(sizeof(int32_t) * (size_t)(h * RB));
+  int ex[RB];
+  for (int r = 0; r < n; ++r) {
+    const int64_t t = t0 + r;
+    quant_row(a->x16 ? a->x16 + t * h : NULL, a->x32 ? a->x32 + t * h : NULL, h, xq + r * h,
+              &ex[r]);
+  }
   for (int e = 0; e < E; ++e) {
     const int32_t* wr = a->wq + (int64_t)e * h;
-    int64_t z = 0;
-    for (int64_t i = 0; i < h; ++i) z += (int64_t)xq[i] * (int64_t)wr[i];
-    lg[e] = ldexpf((float)z, ex + a->we[e] - 296);
+    for (int r = 0; r < n; ++r) {
+      const int32_t* xr = xq + r * h;
+      int64_t z = 0;
+      for (int64_t i = 0; i < h; ++i) z += (int64_t)xr[i] * (int64_t)wr[i];
+      a->logits[(t0 + r) * E + e] = ldexpf((float)z, ex[r] + a->we[e] - 296);
+    }
   }
   free(xq);
-  select_token(a->cfg, lg, a->bias, a->idx + t * a->cfg->top_k, a->wts + t * a->cfg->top_k);
+  for (int r = 0; r < n; ++r) {
+    const int64_t t = t0 + r;
+    select_token(a->cfg, a->logits + t * E, a->bias, a->idx + t * a->cfg->top_k,
+                 a->wts + t * a->cfg->top_k);
+  }
 }
 
 /* Quantise the router rows once, route every token, release. */
@@ -603,8 +619,8 @@ static void route_all(const oracle_moe_config* cfg, const uint16_t* x16, const f
   for (int e = 0; e < E; ++e)
     quant_row(w16 ? w16 + (int64_t)e * h : NULL, w32 ? w32 + (int64_t)e * h : NULL, h,
               wq + (int64_t)e * h, &we[e]);
-  route_arg a = {cfg, x16, x32, wq, we, bias, logits, idx, wts};
-  parallel_for(T, nthreads, route_one, &a);
+  route_arg a = {cfg, x16, x32, wq, we, bias, logits, idx, wts, T};
+  parallel_for((T + RB - 1) / RB, nthreads, route_one, &a);
   free(wq);
   free(we);
 }
@@ -822,18 +838,21 @@ static void ffn_rows_bf16(const uint16_t* gate, const uint16_t* up, const uint16
       yr[r][i] += scale[r] * dot_bf16(hbuf + (int64_t)r * f, down + i * f, f);
 }
 
-/* y_rows[r] += scale[r] * FFN(x_rows[r]) for n rows of one expert. */
+/* y_rows[r] += scale[r] * FFN(x_rows[r]) for n rows of one expert. Weight
+ * rows outer, token rows inner (each weight row streamed once); every output
+ * is the same dotf as a row-at-a-time loop. hbuf: [n][f]. */
 static void ffn_rows(const float* gate, const float* up, const float* down,
                      int64_t h, int64_t f, const float* const* xr,
                      const float* scale, float* const* yr, int n, float* hbuf) {
-  for (int r = 0; r < n; ++r) {
-    for (int64_t j = 0; j < f; ++j) {
+  for (int64_t j = 0; j < f; ++j)
+    for (int r = 0; r < n; ++r) {
       const float g = dotf(xr[r], gate + j * h, h);
       const float u = dotf(xr[r], up + j * h, h);
-      hbuf[j] = siluf(g) * u;
+      hbuf[(int64_t)r * f + j] = siluf(g) * u;
     }
-    for (int64_t i = 0; i < h; ++i) yr[r][i] += scale[r] * dotf(hbuf, down + i * f, f);
-  }
+  for (int64_t i = 0; i < h; ++i)
+    for (int r = 0; r < n; ++r)
+      yr[r][i] += scale[r] * dotf(hbuf + (int64_t)r * f, down + i * f, f);
 }
 
 typedef struct {
