@@ -56,6 +56,17 @@ int dwdp_placement_holds(const dwdp_placement* p, int rank, int expert,
                          int* holds);
 /* PlacementPlan::validate (src/placement.cpp:15-45): 0 or 3. */
 int dwdp_placement_validate(const dwdp_placement* p);
+/* A placement handle from a plan held as plain tables (the value type of
+ * the C++/Python mirrors, possibly edited by the caller), checked with
+ * PlacementPlan::validate: status 3 on a broken invariant. local_sets[r] =
+ * local_flat[local_offsets[r] .. local_offsets[r+1]); fetch_lists[r] =
+ * (fetch_experts, fetch_sources)[fetch_offsets[r] .. fetch_offsets[r+1]). */
+int dwdp_placement_from_tables(int group_size, int num_experts, int local_count,
+                               int redundancy, const int* local_offsets,
+                               const int* local_flat, const int* fetch_offsets,
+                               const int* fetch_experts,
+                               const int* fetch_sources,
+                               dwdp_placement** out);
 /* prefetch_bytes = (E - c) * expert_shard_bytes (src/placement.cpp:113-116). */
 int dwdp_prefetch_bytes(const dwdp_placement* p, double expert_shard_bytes,
                         double* bytes);
@@ -133,6 +144,22 @@ int dwdp_route_tokens(int64_t tokens, int num_experts, int top_k,
 int dwdp_sample_batches(const dwdp_workload_spec* spec, int num_experts,
                         int top_k, int num_ranks, int iterations,
                         int64_t* tokens, int64_t* requests, int64_t* routed);
+/* WorkloadSpec::validate + IslDist::validate (src/workload.cpp:10-22, 66-77). */
+int dwdp_workload_validate(const dwdp_workload_spec* spec);
+/* batches_to_csv (src/workload.cpp:191-208): the reference's replay format.
+ * routed (nullable) [iterations][num_ranks][num_experts]; *len_inout =
+ * capacity in, bytes needed (incl. NUL) out. */
+int dwdp_batches_to_csv(const int64_t* tokens, const int64_t* requests,
+                        const int64_t* routed, int iterations, int num_ranks,
+                        int num_experts, char* buf, size_t* len_inout);
+/* batches_from_csv (src/workload.cpp:210-247). First call with NULL arrays
+ * returns the shape: *iterations, *num_ranks, *num_experts (the longest
+ * expert-count row; 0 if the file carries no routing). Second call fills
+ * tokens/requests [it][rank] and routed [it][rank][num_experts] (rows shorter
+ * than num_experts zero-padded; routed_len[it][rank] = their length). */
+int dwdp_batches_from_csv(const char* csv, int* iterations, int* num_ranks,
+                          int* num_experts, int64_t* tokens, int64_t* requests,
+                          int64_t* routed, int32_t* routed_len);
 /* imbalance_cv (src/workload.cpp:175-189). */
 int dwdp_imbalance_cv(const int64_t* tokens, int n, double* cv);
 /* IslDist::cv (src/workload.cpp:24-36). */
@@ -141,7 +168,7 @@ int dwdp_isl_cv(const dwdp_workload_spec* spec, double* cv);
 /* ======================================================================
  * Cost model — include/dwdpsim/modelspec.hpp:22-75, hwmodel.hpp:29-52.
  * ==================================================================== */
-typedef struct { /* MoeModelSpec, MoE-only subset */
+typedef struct { /* MoeModelSpec + CostCalibration (modelspec.hpp:13-40) */
   int32_t num_layers;
   int32_t num_experts;
   int64_t hidden_dim;
@@ -151,6 +178,12 @@ typedef struct { /* MoeModelSpec, MoE-only subset */
   int64_t shared_ffn_dim;
   double weight_bytes_per_param;
   double act_bytes_per_element;
+  double attn_proj_params;             /* attention block (layer_costs)   */
+  double kv_bytes_per_token_per_layer;
+  double others_bytes_factor;          /* Others = factor x one act pass  */
+  double calib_attention;              /* CostCalibration: 1.0 = neutral  */
+  double calib_grouped_gemm;
+  double calib_dense_gemm;
 } dwdp_model_spec;
 
 typedef struct { /* GpuSpec (hwmodel.hpp:29-38) */
@@ -175,12 +208,26 @@ typedef struct { /* OpCost (modelspec.hpp:37-41) + measured time */
   double ns;
 } dwdp_op_cost;
 
+/* Category::name (src/hwmodel.cpp:9-29); NULL for an unknown id. */
+const char* dwdp_category_name(int category);
+/* MoeModelSpec::validate (src/modelspec.cpp:6-23). */
+int dwdp_model_validate(const dwdp_model_spec* m);
 /* expert_shard_bytes (src/modelspec.cpp:32-36). */
 int dwdp_expert_shard_bytes(const dwdp_model_spec* m, double* bytes);
-/* moe_entries (src/modelspec.cpp:57-86): GroupedGemm (+ DenseGemm). */
+/* attention_entries (src/modelspec.cpp:38-55): Attention (+ Others);
+ * out capacity 2. */
+int dwdp_attention_entries(const dwdp_model_spec* m, double tokens,
+                           double mean_seq_len, dwdp_op_cost* out, int* n_out);
+/* moe_entries (src/modelspec.cpp:57-86): GroupedGemm (+ DenseGemm)
+ * (+ Others); out capacity 3. */
 int dwdp_moe_entries(const dwdp_model_spec* m, double tokens,
                      double routed_pairs, int experts_touched,
                      dwdp_op_cost* out, int* n_out);
+/* layer_costs (src/modelspec.cpp:88-98): validates the model; attn capacity
+ * 2, moe capacity 3. */
+int dwdp_layer_costs(const dwdp_model_spec* m, int64_t tokens,
+                     int64_t mean_seq_len, dwdp_op_cost* attn, int* n_attn,
+                     dwdp_op_cost* moe, int* n_moe);
 /* roofline_time (src/hwmodel.cpp:68-73). */
 int dwdp_roofline_time(double flops, double bytes, const dwdp_gpu_spec* g,
                        double* seconds);
@@ -195,10 +242,13 @@ typedef struct { /* AnalyticResult (simcore.hpp:218-225) */
   int32_t reserved;
 } dwdp_analytic_result;
 
-/* analytic_compare for the MoE-only layer (src/simcore.cpp:882-905). */
+/* analytic_compare (src/simcore.cpp:882-905) over layer_costs. With
+ * mean_seq_len == 0 the layer is the MoE block alone (the measured stack
+ * without the attention block) and the model is checked on its MoE fields
+ * only. */
 int dwdp_analytic_compare(const dwdp_model_spec* m, const dwdp_gpu_spec* g,
                           const dwdp_placement* p, int64_t tokens,
-                          dwdp_analytic_result* out);
+                          int64_t mean_seq_len, dwdp_analytic_result* out);
 
 /* ======================================================================
  * Per-GPU runtime: split-weight manager, prefetch engine, MoE forward.

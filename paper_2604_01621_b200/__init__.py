@@ -5,7 +5,8 @@ This package mirrors the reference operator API (dwdpsim names) on top of it.
 """
 from ._lib import (ENGINE_COPY, ENGINE_HYBRID, ENGINE_PULL, WEIGHT_BF16, WEIGHT_FP8, WEIGHT_NVFP4, ConfigError, CudaError, InvariantViolation,  # noqa: F401
                    lib)
-from .planning import (CopyPlan, GpuSpec, IslDist, MoeModelSpec, OpCost, PlacementPlan,  # noqa: F401
+from .planning import (CopyPlan, CostCalibration, GpuSpec, LayerWork, attention_entries, batches_from_csv,
+                       batches_to_csv, layer_costs, IslDist, MoeModelSpec, OpCost, PlacementPlan,  # noqa: F401
                        RankBatch, ShardRef, Slice, WorkloadSpec, analytic_compare,
                        assign_fetch_sources, build_copy_plan, build_placement,
                        describe_placement, expert_shard_bytes, imbalance_cv, moe_entries,

@@ -47,7 +47,10 @@ class WorkloadSpecC(C.Structure):
 class ModelSpecC(C.Structure):
     _fields_ = [("num_layers", i32), ("num_experts", i32), ("hidden_dim", i64), ("top_k", i32),
                 ("reserved", i32), ("expert_ffn_dim", i64), ("shared_ffn_dim", i64),
-                ("weight_bytes_per_param", f64), ("act_bytes_per_element", f64)]
+                ("weight_bytes_per_param", f64), ("act_bytes_per_element", f64),
+                ("attn_proj_params", f64), ("kv_bytes_per_token_per_layer", f64),
+                ("others_bytes_factor", f64), ("calib_attention", f64),
+                ("calib_grouped_gemm", f64), ("calib_dense_gemm", f64)]
 
 
 class GpuSpecC(C.Structure):
@@ -127,10 +130,20 @@ SIGNATURES = {
     "dwdp_sample_batches": (i32, [C.POINTER(WorkloadSpecC), i32, i32, i32, i32, P, P, P]),
     "dwdp_imbalance_cv": (i32, [P, i32, C.POINTER(f64)]),
     "dwdp_isl_cv": (i32, [C.POINTER(WorkloadSpecC), C.POINTER(f64)]),
+    "dwdp_workload_validate": (i32, [C.POINTER(WorkloadSpecC)]),
+    "dwdp_batches_to_csv": (i32, [P, P, P, i32, i32, i32, C.c_char_p, C.POINTER(sz)]),
+    "dwdp_batches_from_csv": (i32, [C.c_char_p, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32),
+                                    P, P, P, P]),
+    "dwdp_placement_from_tables": (i32, [i32, i32, i32, i32, P, P, P, P, P, C.POINTER(P)]),
+    "dwdp_category_name": (C.c_char_p, [i32]),
+    "dwdp_model_validate": (i32, [C.POINTER(ModelSpecC)]),
     "dwdp_expert_shard_bytes": (i32, [C.POINTER(ModelSpecC), C.POINTER(f64)]),
+    "dwdp_attention_entries": (i32, [C.POINTER(ModelSpecC), f64, f64, P, C.POINTER(i32)]),
     "dwdp_moe_entries": (i32, [C.POINTER(ModelSpecC), f64, f64, i32, P, C.POINTER(i32)]),
+    "dwdp_layer_costs": (i32, [C.POINTER(ModelSpecC), i64, i64, P, C.POINTER(i32), P,
+                               C.POINTER(i32)]),
     "dwdp_roofline_time": (i32, [f64, f64, C.POINTER(GpuSpecC), C.POINTER(f64)]),
-    "dwdp_analytic_compare": (i32, [C.POINTER(ModelSpecC), C.POINTER(GpuSpecC), P, i64,
+    "dwdp_analytic_compare": (i32, [C.POINTER(ModelSpecC), C.POINTER(GpuSpecC), P, i64, i64,
                                     C.POINTER(AnalyticC)]),
     "dwdp_ctx_create": (i32, [C.POINTER(CtxConfigC), C.POINTER(P)]),
     "dwdp_ctx_destroy": (i32, [P]),

@@ -47,6 +47,7 @@ void need(const void* p, const char* what) {
   if (!p) throw dwdp::ConfigError(std::string(what) + " is NULL");
 }
 
+// The MoeModelSpec fields every cost entry reads (no attention terms).
 dwdp::ModelSpec to_model(const dwdp_model_spec* m) {
   need(m, "model");
   dwdp::require(m->hidden_dim > 0, "model.hidden_dim must be > 0");
@@ -66,7 +67,45 @@ dwdp::ModelSpec to_model(const dwdp_model_spec* m) {
   s.shared_ffn = m->shared_ffn_dim;
   s.wbytes = m->weight_bytes_per_param;
   s.abytes = m->act_bytes_per_element;
+  s.attn_proj_params = m->attn_proj_params;
+  s.kv_bytes = m->kv_bytes_per_token_per_layer;
+  s.others_factor = m->others_bytes_factor;
+  s.calib_attention = m->calib_attention;
+  s.calib_grouped = m->calib_grouped_gemm;
+  s.calib_dense = m->calib_dense_gemm;
+  dwdp::require(s.others_factor >= 0, "model.others_bytes_factor must be >= 0");
+  dwdp::require(s.calib_attention > 0 && s.calib_grouped > 0 && s.calib_dense > 0,
+                "model.calib scalars must be > 0");
   return s;
+}
+
+// Full MoeModelSpec (modelspec.cpp:6-23), no subset pre-checks.
+dwdp::ModelSpec to_model_full(const dwdp_model_spec* m) {
+  need(m, "model");
+  dwdp::ModelSpec s;
+  s.num_layers = m->num_layers;
+  s.num_experts = m->num_experts;
+  s.top_k = m->top_k;
+  s.hidden = m->hidden_dim;
+  s.ffn = m->expert_ffn_dim;
+  s.shared_ffn = m->shared_ffn_dim;
+  s.wbytes = m->weight_bytes_per_param;
+  s.abytes = m->act_bytes_per_element;
+  s.attn_proj_params = m->attn_proj_params;
+  s.kv_bytes = m->kv_bytes_per_token_per_layer;
+  s.others_factor = m->others_bytes_factor;
+  s.calib_attention = m->calib_attention;
+  s.calib_grouped = m->calib_grouped_gemm;
+  s.calib_dense = m->calib_dense_gemm;
+  s.validate();
+  return s;
+}
+
+void put_costs(const std::vector<dwdp::OpCost>& e, dwdp_op_cost* out, int* n_out) {
+  need(out, "out");
+  need(n_out, "n_out");
+  for (size_t i = 0; i < e.size(); ++i) out[i] = {e[i].category, 0, e[i].flops, e[i].bytes, 0.0};
+  *n_out = int(e.size());
 }
 
 dwdp::WorkloadSpec to_spec(const dwdp_workload_spec* w) {
@@ -153,6 +192,33 @@ int dwdp_placement_validate(const dwdp_placement* p) {
   return guard([&] {
     need(p, "placement");
     p->p.validate();
+  });
+}
+
+int dwdp_placement_from_tables(int N, int E, int c, int red, const int* loffs,
+                               const int* lflat, const int* foffs, const int* fe, const int* fs,
+                               dwdp_placement** out) {
+  return guard([&] {
+    need(out, "out");
+    dwdp::invariant(N >= 0 && E >= 0, "placement: table shape mismatch");
+    if (N > 0) {
+      need(loffs, "local_offsets");
+      need(foffs, "fetch_offsets");
+    }
+    dwdp::Placement p;
+    p.group_size = N;
+    p.num_experts = E;
+    p.local_count = c;
+    p.redundancy = red;
+    p.local_sets.resize(size_t(N));
+    p.fetch_lists.resize(size_t(N));
+    for (int r = 0; r < N; ++r) {
+      for (int i = loffs[r]; i < loffs[r + 1]; ++i) p.local_sets[size_t(r)].push_back(lflat[i]);
+      for (int i = foffs[r]; i < foffs[r + 1]; ++i)
+        p.fetch_lists[size_t(r)].emplace_back(fe[i], fs[i]);
+    }
+    p.validate();
+    *out = new dwdp_placement{std::move(p)};
   });
 }
 
@@ -285,6 +351,69 @@ int dwdp_imbalance_cv(const int64_t* tokens, int n, double* cv) {
   });
 }
 
+int dwdp_workload_validate(const dwdp_workload_spec* w) {
+  return guard([&] { to_spec(w).validate(); });
+}
+
+int dwdp_batches_to_csv(const int64_t* tokens, const int64_t* requests, const int64_t* routed,
+                        int iters, int N, int E, char* buf, size_t* len) {
+  return guard([&] {
+    need(len, "len_inout");
+    dwdp::require(iters >= 0 && N >= 0 && E >= 0, "batches csv: negative shape");
+    if (iters * N > 0) {
+      need(tokens, "tokens");
+      need(requests, "requests");
+    }
+    dwdp::Batches b;
+    b.tokens.assign(size_t(iters), std::vector<int64_t>(size_t(N)));
+    b.requests = b.tokens;
+    b.routed.assign(size_t(iters), std::vector<std::vector<int64_t>>(size_t(N)));
+    for (int it = 0; it < iters; ++it)
+      for (int r = 0; r < N; ++r) {
+        const size_t i = size_t(it) * size_t(N) + size_t(r);
+        b.tokens[size_t(it)][size_t(r)] = tokens[i];
+        b.requests[size_t(it)][size_t(r)] = requests[i];
+        if (routed) b.routed[size_t(it)][size_t(r)].assign(routed + i * size_t(E),
+                                                             routed + (i + 1) * size_t(E));
+      }
+    const std::string s = dwdp::batches_to_csv(b);
+    const size_t cap = *len;
+    *len = s.size() + 1;
+    if (buf && cap >= s.size() + 1) std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+int dwdp_batches_from_csv(const char* csv, int* iters, int* N, int* E, int64_t* tokens,
+                          int64_t* requests, int64_t* routed, int32_t* routed_len) {
+  return guard([&] {
+    need(csv, "csv");
+    need(iters, "iterations");
+    need(N, "num_ranks");
+    need(E, "num_experts");
+    const auto b = dwdp::batches_from_csv(csv);
+    size_t nr = 0, ne = 0;
+    for (size_t it = 0; it < b.tokens.size(); ++it) {
+      nr = std::max(nr, b.tokens[it].size());
+      for (const auto& c : b.routed[it]) ne = std::max(ne, c.size());
+    }
+    *iters = int(b.tokens.size());
+    *N = int(nr);
+    *E = int(ne);
+    for (size_t it = 0; it < b.tokens.size(); ++it)
+      for (size_t r = 0; r < nr; ++r) {
+        const size_t i = it * nr + r;
+        const bool have = r < b.tokens[it].size();
+        if (tokens) tokens[i] = have ? b.tokens[it][r] : 0;
+        if (requests) requests[i] = have ? b.requests[it][r] : 0;
+        const std::vector<int64_t> none;
+        const auto& c = have ? b.routed[it][r] : none;
+        if (routed_len) routed_len[i] = int32_t(c.size());
+        if (routed)
+          for (size_t e = 0; e < ne; ++e) routed[i * ne + e] = e < c.size() ? c[e] : 0;
+      }
+  });
+}
+
 int dwdp_isl_cv(const dwdp_workload_spec* w, double* cv) {
   return guard([&] {
     need(cv, "cv");
@@ -300,14 +429,34 @@ int dwdp_expert_shard_bytes(const dwdp_model_spec* m, double* bytes) {
   });
 }
 
+const char* dwdp_category_name(int c) {
+  static const char* const names[DWDP_NUM_CATEGORIES] = {
+      "Attention", "GroupedGEMM", "DenseGEMM", "Others",
+      "Communication", "D2DCopy", "P2PCopy", "SyncWait"};
+  return c >= 0 && c < DWDP_NUM_CATEGORIES ? names[c] : nullptr;
+}
+
+int dwdp_model_validate(const dwdp_model_spec* m) {
+  return guard([&] { to_model_full(m); });
+}
+
+int dwdp_attention_entries(const dwdp_model_spec* m, double tokens, double msl,
+                           dwdp_op_cost* out, int* n_out) {
+  return guard([&] { put_costs(dwdp::attention_entries(to_model(m), tokens, msl), out, n_out); });
+}
+
 int dwdp_moe_entries(const dwdp_model_spec* m, double tokens, double pairs, int touched,
                      dwdp_op_cost* out, int* n_out) {
+  return guard([&] { put_costs(dwdp::moe_entries(to_model(m), tokens, pairs, touched), out, n_out); });
+}
+
+int dwdp_layer_costs(const dwdp_model_spec* m, int64_t tokens, int64_t msl, dwdp_op_cost* attn,
+                     int* n_attn, dwdp_op_cost* moe, int* n_moe) {
   return guard([&] {
-    need(out, "out");
-    need(n_out, "n_out");
-    const auto e = dwdp::moe_entries(to_model(m), tokens, pairs, touched);
-    for (size_t i = 0; i < e.size(); ++i) out[i] = {e[i].category, 0, e[i].flops, e[i].bytes, 0.0};
-    *n_out = int(e.size());
+    std::vector<dwdp::OpCost> a, b;
+    dwdp::layer_costs(to_model_full(m), tokens, msl, a, b);
+    put_costs(a, attn, n_attn);
+    put_costs(b, moe, n_moe);
   });
 }
 
@@ -323,19 +472,28 @@ int dwdp_roofline_time(double flops, double bytes, const dwdp_gpu_spec* g, doubl
 }
 
 int dwdp_analytic_compare(const dwdp_model_spec* m, const dwdp_gpu_spec* g,
-                          const dwdp_placement* p, int64_t tokens, dwdp_analytic_result* out) {
+                          const dwdp_placement* p, int64_t tokens, int64_t msl,
+                          dwdp_analytic_result* out) {
   return guard([&] {
     need(g, "gpu");
     need(p, "placement");
     need(out, "out");
-    const auto spec = to_model(m);
+    const auto spec = msl > 0 ? to_model_full(m) : to_model(m);
+    dwdp::require(g->peak_flops > 0, "gpu.peak_flops must be > 0");
+    dwdp::require(g->mem_bw > 0, "gpu.mem_bw must be > 0");
+    dwdp::require(g->link_bw > 0, "gpu.link_bw must be > 0");
     dwdp::require(p->p.num_experts == spec.num_experts,
                   "analytic_compare: placement does not match the model");
     dwdp::require(tokens >= 1, "layer_costs: tokens must be >= 1");
     const double t = double(tokens);
+    std::vector<dwdp::OpCost> ops, moe;
+    if (msl > 0)
+      dwdp::layer_costs(spec, tokens, msl, ops, moe);
+    else
+      moe = dwdp::moe_entries(spec, t, t * spec.top_k, spec.num_experts);
+    ops.insert(ops.end(), moe.begin(), moe.end());
     double tc = 0;
-    for (const auto& op : dwdp::moe_entries(spec, t, t * spec.top_k, spec.num_experts))
-      tc += std::max(op.flops / g->peak_flops, op.bytes / g->mem_bw);
+    for (const auto& op : ops) tc += std::max(op.flops / g->peak_flops, op.bytes / g->mem_bw);
     const double pf = double(p->p.num_experts - p->p.local_count) * dwdp::expert_shard_bytes(spec);
     *out = {};
     out->t_compute_s = tc;

@@ -39,8 +39,10 @@ void Placement::validate() const {
       covered[static_cast<size_t>(e)] = 1;
     }
     for (const auto& [e, src] : fetch_lists[static_cast<size_t>(r)]) {
+      invariant(e >= 0 && e < num_experts, "placement: expert out of range");
       invariant(!covered[static_cast<size_t>(e)], "placement: fetched expert is local");
       invariant(src != r, "placement: self-fetch");
+      invariant(src >= 0 && src < group_size, "placement: source does not hold expert");
       invariant(holds(src, e), "placement: source does not hold expert");
       covered[static_cast<size_t>(e)] = 1;
     }
@@ -355,22 +357,141 @@ double imbalance_cv(const std::vector<int64_t>& tokens) {
 }
 
 // ===================================================================== //
-// Cost formulas — src/modelspec.cpp:32-86 (MoE block only).
+// Batch CSV — src/workload.cpp:191-247 (same text format, so replay files
+// interoperate with the reference's own batches_to_csv/batches_from_csv).
+
+std::string batches_to_csv(const Batches& b) {
+  std::ostringstream os;
+  os << "iteration,rank,tokens,requests,expert_counts\n";
+  for (size_t it = 0; it < b.tokens.size(); ++it)
+    for (size_t r = 0; r < b.tokens[it].size(); ++r) {
+      os << it << ',' << r << ',' << b.tokens[it][r] << ',' << b.requests[it][r] << ',';
+      if (it < b.routed.size() && r < b.routed[it].size()) {
+        const auto& c = b.routed[it][r];
+        for (size_t e = 0; e < c.size(); ++e) os << (e ? ";" : "") << c[e];
+      }
+      os << '\n';
+    }
+  return os.str();
+}
+
+namespace {
+int64_t parse_i64(const std::string& s, const char* what) {
+  size_t used = 0;
+  int64_t v = 0;
+  try {
+    v = std::stoll(s, &used);
+  } catch (const std::exception&) {
+    used = 0;
+  }
+  require(used > 0 && used == s.size(), (std::string("batches csv: bad ") + what).c_str());
+  return v;
+}
+}  // namespace
+
+Batches batches_from_csv(const std::string& csv) {
+  std::istringstream in(csv);
+  std::string line;
+  require(static_cast<bool>(std::getline(in, line)), "batches csv: empty file");
+  require(line == "iteration,rank,tokens,requests,expert_counts", "batches csv: unexpected header");
+  Batches b;
+  while (std::getline(in, line)) {
+    if (line.empty()) continue;
+    std::vector<std::string> f;
+    size_t pos = 0;
+    for (int i = 0; i < 4; ++i) {
+      const size_t c = line.find(',', pos);
+      require(c != std::string::npos, "batches csv: missing field");
+      f.push_back(line.substr(pos, c - pos));
+      pos = c + 1;
+    }
+    const int64_t it = parse_i64(f[0], "iteration"), r = parse_i64(f[1], "rank");
+    require(it >= 0 && r >= 0, "batches csv: negative index");
+    std::vector<int64_t> counts;
+    const std::string rest = line.substr(pos);
+    for (size_t a = 0; a < rest.size();) {
+      size_t e = rest.find(';', a);
+      if (e == std::string::npos) e = rest.size();
+      counts.push_back(parse_i64(rest.substr(a, e - a), "expert count"));
+      a = e + 1;
+    }
+    const size_t I = size_t(it), R = size_t(r);
+    if (b.tokens.size() <= I) {
+      b.tokens.resize(I + 1);
+      b.requests.resize(I + 1);
+      b.routed.resize(I + 1);
+    }
+    if (b.tokens[I].size() <= R) {
+      b.tokens[I].resize(R + 1, 0);
+      b.requests[I].resize(R + 1, 0);
+      b.routed[I].resize(R + 1);
+    }
+    b.tokens[I][R] = parse_i64(f[2], "tokens");
+    b.requests[I][R] = parse_i64(f[3], "requests");
+    b.routed[I][R] = std::move(counts);
+  }
+  require(!b.tokens.empty(), "batches csv: no rows");
+  return b;
+}
+
+// ===================================================================== //
+// Cost formulas — src/modelspec.cpp:6-98.
+
+void ModelSpec::validate() const {
+  require(num_layers >= 1, "model.num_layers must be >= 1");
+  require(hidden > 0, "model.hidden_dim must be > 0");
+  require(num_experts >= 1, "model.num_experts must be >= 1");
+  require(top_k >= 1 && top_k <= num_experts, "model.top_k must be in [1, num_experts]");
+  require(ffn > 0, "model.expert_ffn_dim must be > 0");
+  require(shared_ffn >= 0, "model.shared_ffn_dim must be >= 0");
+  require(attn_proj_params > 0, "model.attn_proj_params must be > 0");
+  require(wbytes > 0, "model.weight_bytes_per_param must be > 0");
+  require(kv_bytes >= 0, "model.kv_bytes_per_token_per_layer must be >= 0");
+  require(abytes > 0, "model.act_bytes_per_element must be > 0");
+  require(others_factor >= 0, "model.others_bytes_factor must be >= 0");
+  require(calib_attention > 0 && calib_grouped > 0 && calib_dense > 0,
+          "model.calib scalars must be > 0");
+}
 
 double expert_shard_bytes(const ModelSpec& m) {
   return 3.0 * static_cast<double>(m.hidden) * static_cast<double>(m.ffn) * m.wbytes;
 }
 
+// Category ids (hwmodel.hpp:14-23): 0 Attention, 1 GroupedGemm, 2 DenseGemm, 3 Others.
+std::vector<OpCost> attention_entries(const ModelSpec& m, double tokens, double msl) {
+  const double h = static_cast<double>(m.hidden), act = tokens * h * m.abytes;
+  const double k = m.calib_attention;
+  std::vector<OpCost> out;
+  out.push_back({0, k * (2.0 * tokens * m.attn_proj_params + 2.0 * tokens * msl * h),
+                 k * (m.attn_proj_params * m.wbytes + act + tokens * m.kv_bytes)});
+  if (m.others_factor > 0) out.push_back({3, 0.0, 0.5 * m.others_factor * act});
+  return out;
+}
+
 std::vector<OpCost> moe_entries(const ModelSpec& m, double tokens, double pairs, int touched) {
   const double h = static_cast<double>(m.hidden), f = static_cast<double>(m.ffn);
   std::vector<OpCost> out;
-  out.push_back({1, 2.0 * pairs * 3.0 * h * f,
-                 static_cast<double>(touched) * expert_shard_bytes(m) + 2.0 * pairs * h * m.abytes});
+  const double g = m.calib_grouped;
+  out.push_back({1, g * 2.0 * pairs * 3.0 * h * f,
+                 g * (static_cast<double>(touched) * expert_shard_bytes(m) +
+                      2.0 * pairs * h * m.abytes)});
   if (m.shared_ffn > 0) {
-    const double fs = static_cast<double>(m.shared_ffn);
-    out.push_back({2, 2.0 * tokens * 3.0 * h * fs, 3.0 * h * fs * m.wbytes + tokens * h * m.abytes});
+    const double fs = static_cast<double>(m.shared_ffn), d = m.calib_dense;
+    out.push_back({2, d * 2.0 * tokens * 3.0 * h * fs,
+                   d * (3.0 * h * fs * m.wbytes + tokens * h * m.abytes)});
   }
+  if (m.others_factor > 0) out.push_back({3, 0.0, 0.5 * m.others_factor * tokens * h * m.abytes});
   return out;
+}
+
+void layer_costs(const ModelSpec& m, int64_t tokens, int64_t msl, std::vector<OpCost>& attn,
+                 std::vector<OpCost>& moe) {
+  m.validate();
+  require(tokens >= 1, "layer_costs: tokens must be >= 1");
+  require(msl >= 1, "layer_costs: mean_seq_len must be >= 1");
+  const double t = static_cast<double>(tokens);
+  attn = attention_entries(m, t, static_cast<double>(msl));
+  moe = moe_entries(m, t, t * m.top_k, m.num_experts);
 }
 
 }  // namespace dwdp

@@ -93,19 +93,33 @@ struct Batches {  // [iteration][rank] (+ [expert])
 Batches sample_batches(const WorkloadSpec& spec, int num_experts, int top_k,
                        int num_ranks, int iterations, bool with_routing);
 double imbalance_cv(const std::vector<int64_t>& tokens);
+// Exact workload replay (workload.hpp:77-79): one row per (iteration, rank),
+// expert counts ';'-separated. routed may be empty (no routing drawn).
+std::string batches_to_csv(const Batches& b);
+Batches batches_from_csv(const std::string& csv);
 
 // ---------------------------------------------------------------- costs
+// MoeModelSpec (modelspec.hpp:13-40) incl. the attention block terms and
+// the per-category calibration scalars.
 struct ModelSpec {
   int num_layers = 1, num_experts = 1, top_k = 1;
   int64_t hidden = 0, ffn = 0, shared_ffn = 0;
   double wbytes = 2.0, abytes = 2.0;
+  double attn_proj_params = 0, kv_bytes = 0, others_factor = 0;
+  double calib_attention = 1.0, calib_grouped = 1.0, calib_dense = 1.0;
+  void validate() const;  // modelspec.cpp:6-23
 };
 double expert_shard_bytes(const ModelSpec& m);
 struct OpCost {
-  int category;
+  int category;  // Category order of hwmodel.hpp:14-23
   double flops, bytes;
 };
+std::vector<OpCost> attention_entries(const ModelSpec& m, double tokens, double msl);
 std::vector<OpCost> moe_entries(const ModelSpec& m, double tokens,
                                 double pairs, int touched);
+// layer_costs (modelspec.cpp:88-98): validates, then attn + moe entries
+// with routed_pairs = T*k over all E experts.
+void layer_costs(const ModelSpec& m, int64_t tokens, int64_t msl, std::vector<OpCost>& attn,
+                 std::vector<OpCost>& moe);
 
 }  // namespace dwdp

@@ -11,7 +11,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import (AnalyticC, ConfigError, GpuSpecC, ModelSpecC, OpCostC, ShardRefC, SliceC,
+from ._lib import (AnalyticC, ConfigError, GpuSpecC, InvariantViolation, ModelSpecC, OpCostC, ShardRefC, SliceC,
                    WorkloadSpecC, check, lib)
 
 # --------------------------------------------------------------------------- placement
@@ -31,9 +31,10 @@ class PlacementPlan:
         return expert in self.local_sets[rank]
 
     def validate(self) -> None:
-        """Re-checks the invariants through the library (placement.cpp:15-45)."""
-        with _Placement.from_plan(self) as p:
-            check(lib().dwdp_placement_validate(p.h))
+        """Checks this plan's tables through the library (placement.cpp:15-45);
+        InvariantViolation on any broken invariant."""
+        with _Placement.from_plan(self):
+            pass
 
 
 class _Placement:
@@ -48,8 +49,20 @@ class _Placement:
 
     @classmethod
     def from_plan(cls, plan: PlacementPlan) -> "_Placement":
-        return cls.build(plan.num_experts, plan.group_size,
-                         plan.local_count - (plan.num_experts + plan.group_size - 1) // plan.group_size)
+        """Handle over this plan's own tables (validated)."""
+        if len(plan.local_sets) != plan.group_size or len(plan.fetch_lists) != plan.group_size:
+            raise InvariantViolation("placement: local_sets size mismatch")
+        loffs = np.cumsum([0] + [len(s) for s in plan.local_sets]).astype(np.int32)
+        foffs = np.cumsum([0] + [len(f) for f in plan.fetch_lists]).astype(np.int32)
+        lflat = np.array([e for s in plan.local_sets for e in s] + [0], np.int32)
+        fe = np.array([e for f in plan.fetch_lists for e, _ in f] + [0], np.int32)
+        fs = np.array([s for f in plan.fetch_lists for _, s in f] + [0], np.int32)
+        h = C.c_void_p()
+        check(lib().dwdp_placement_from_tables(
+            plan.group_size, plan.num_experts, plan.local_count, plan.redundancy,
+            loffs.ctypes.data, lflat.ctypes.data, foffs.ctypes.data, fe.ctypes.data,
+            fs.ctypes.data, C.byref(h)))
+        return cls(h)
 
     def __enter__(self):
         return self
@@ -237,6 +250,10 @@ class WorkloadSpec:
     routing_skew: float = 0.0
     seed: int = 1
 
+    def validate(self) -> None:
+        """src/workload.cpp:66-77 (+ IslDist::validate)."""
+        check(lib().dwdp_workload_validate(C.byref(_spec_c(self))))
+
 
 def _spec_c(w: WorkloadSpec) -> WorkloadSpecC:
     d = w.isl_dist
@@ -245,8 +262,16 @@ def _spec_c(w: WorkloadSpec) -> WorkloadSpecC:
 
 
 @dataclass
+class CostCalibration:
+    """modelspec.hpp:13-19: one scalar per category (1.0 = neutral)."""
+    attention: float = 1.0
+    grouped_gemm: float = 1.0
+    dense_gemm: float = 1.0
+
+
+@dataclass
 class MoeModelSpec:
-    """modelspec.hpp:22-47 (the MoE-only subset the hot path uses)."""
+    """modelspec.hpp:22-40."""
     num_layers: int = 1
     hidden_dim: int = 0
     num_experts: int = 1
@@ -255,16 +280,29 @@ class MoeModelSpec:
     shared_ffn_dim: int = 0
     weight_bytes_per_param: float = 2.0
     act_bytes_per_element: float = 2.0
+    attn_proj_params: float = 0.0
+    kv_bytes_per_token_per_layer: float = 0.0
+    others_bytes_factor: float = 0.0
+    calib: CostCalibration = field(default_factory=CostCalibration)
 
     def c(self) -> ModelSpecC:
         return ModelSpecC(self.num_layers, self.num_experts, self.hidden_dim, self.top_k, 0,
                           self.expert_ffn_dim, self.shared_ffn_dim, self.weight_bytes_per_param,
-                          self.act_bytes_per_element)
+                          self.act_bytes_per_element, self.attn_proj_params,
+                          self.kv_bytes_per_token_per_layer, self.others_bytes_factor,
+                          self.calib.attention, self.calib.grouped_gemm, self.calib.dense_gemm)
+
+    def validate(self) -> None:
+        """src/modelspec.cpp:6-23."""
+        check(lib().dwdp_model_validate(C.byref(self.c())))
 
 
 def r1_model(layers: int = 8, weight_bytes: float = 2.0) -> MoeModelSpec:
-    """DeepSeek-R1 MoE shapes (reference src/config.cpp:24-42)."""
-    return MoeModelSpec(layers, 7168, 256, 8, 2048, 2048, weight_bytes, 2.0)
+    """DeepSeek-R1 MoE shapes (reference src/config.cpp:24-42: attention
+    projection params 187e6, KV 576 B/token/layer); neutral calibration and
+    no Others traffic, i.e. the uncalibrated roofline of the measured path."""
+    return MoeModelSpec(layers, 7168, 256, 8, 2048, 2048, weight_bytes, 2.0,
+                        attn_proj_params=187e6, kv_bytes_per_token_per_layer=576.0)
 
 
 @dataclass
@@ -307,6 +345,45 @@ def sample_batches(spec: WorkloadSpec, model: MoeModelSpec, num_ranks: int, iter
     return out
 
 
+def batches_to_csv(batches: list[RankBatch]) -> str:
+    """workload.hpp:77-78 / src/workload.cpp:191-208 (the reference's replay format)."""
+    iters = len(batches)
+    N = len(batches[0].tokens) if iters else 0
+    E = len(batches[0].routed[0]) if iters and batches[0].routed and batches[0].routed[0] else 0
+    t = np.array([b.tokens for b in batches] or [[0]], np.int64)
+    q = np.array([b.requests for b in batches] or [[0]], np.int64)
+    r = np.array([b.routed for b in batches], np.int64) if E else None
+    n = C.c_size_t(0)
+    L = lib()
+    args = (t.ctypes.data, q.ctypes.data, None if r is None else r.ctypes.data, iters, N, E)
+    check(L.dwdp_batches_to_csv(*args, None, C.byref(n)))
+    buf = C.create_string_buffer(n.value)
+    check(L.dwdp_batches_to_csv(*args, buf, C.byref(n)))
+    return buf.value.decode()
+
+
+def batches_from_csv(csv: str) -> list[RankBatch]:
+    """workload.hpp:79 / src/workload.cpp:210-247."""
+    L = lib()
+    raw = csv.encode()
+    it, N, E = C.c_int32(), C.c_int32(), C.c_int32()
+    check(L.dwdp_batches_from_csv(raw, C.byref(it), C.byref(N), C.byref(E), None, None, None, None))
+    n = it.value * N.value
+    t = np.zeros(max(n, 1), np.int64)
+    q = np.zeros(max(n, 1), np.int64)
+    r = np.zeros(max(n * E.value, 1), np.int64)
+    ln = np.zeros(max(n, 1), np.int32)
+    check(L.dwdp_batches_from_csv(raw, C.byref(it), C.byref(N), C.byref(E), t.ctypes.data,
+                                  q.ctypes.data, r.ctypes.data, ln.ctypes.data))
+    out = []
+    for i in range(it.value):
+        rows = slice(i * N.value, (i + 1) * N.value)
+        routed = [r[(i * N.value + k) * E.value:(i * N.value + k) * E.value + ln[i * N.value + k]].tolist()
+                  for k in range(N.value)]
+        out.append(RankBatch(t[rows].tolist(), q[rows].tolist(), routed))
+    return out
+
+
 def imbalance_cv(batch: RankBatch) -> float:
     """src/workload.cpp:175-189."""
     a = np.asarray(batch.tokens, np.int64)
@@ -332,7 +409,20 @@ class OpCost:
     bytes: float
 
 
-_CAT = {1: "GroupedGEMM", 2: "DenseGEMM", 3: "Others"}
+def _cat(i: int) -> str:
+    return lib().dwdp_category_name(i).decode()
+
+
+def _costs(arr, n) -> list[OpCost]:
+    return [OpCost(_cat(arr[i].category), arr[i].flops, arr[i].bytes) for i in range(n.value)]
+
+
+def attention_entries(model: MoeModelSpec, tokens: float, mean_seq_len: float) -> list[OpCost]:
+    """src/modelspec.cpp:38-55."""
+    out = (OpCostC * 4)()
+    n = C.c_int32()
+    check(lib().dwdp_attention_entries(C.byref(model.c()), tokens, mean_seq_len, out, C.byref(n)))
+    return _costs(out, n)
 
 
 def moe_entries(model: MoeModelSpec, tokens: float, routed_pairs: float,
@@ -342,7 +432,26 @@ def moe_entries(model: MoeModelSpec, tokens: float, routed_pairs: float,
     n = C.c_int32()
     check(lib().dwdp_moe_entries(C.byref(model.c()), tokens, routed_pairs, experts_touched, out,
                                  C.byref(n)))
-    return [OpCost(_CAT[out[i].category], out[i].flops, out[i].bytes) for i in range(n.value)]
+    return _costs(out, n)
+
+
+@dataclass
+class LayerWork:
+    """modelspec.hpp:43-50."""
+    attn: list[OpCost]
+    moe: list[OpCost]
+
+    def total_time(self, gpu: "GpuSpec") -> float:
+        return sum(roofline_time(op.flops, op.bytes, gpu) for op in self.attn + self.moe)
+
+
+def layer_costs(model: MoeModelSpec, tokens: int, mean_seq_len: int) -> LayerWork:
+    """src/modelspec.cpp:88-98."""
+    a, m = (OpCostC * 4)(), (OpCostC * 4)()
+    na, nm = C.c_int32(), C.c_int32()
+    check(lib().dwdp_layer_costs(C.byref(model.c()), tokens, mean_seq_len, a, C.byref(na), m,
+                                 C.byref(nm)))
+    return LayerWork(_costs(a, na), _costs(m, nm))
 
 
 @dataclass
@@ -362,11 +471,12 @@ def roofline_time(flops: float, bytes_: float, gpu: GpuSpec) -> float:
 
 
 def analytic_compare(model: MoeModelSpec, gpu: GpuSpec, placement: PlacementPlan,
-                     tokens: int) -> dict:
-    """src/simcore.cpp:882-905 for the MoE-only layer."""
+                     tokens: int, mean_seq_len: int = 0) -> dict:
+    """src/simcore.cpp:882-905; mean_seq_len = 0: the MoE block alone (the
+    measured stack without attention)."""
     out = AnalyticC()
     with _Placement.from_plan(placement) as p:
         check(lib().dwdp_analytic_compare(C.byref(model.c()),
                                           C.byref(GpuSpecC(gpu.peak_flops, gpu.mem_bw, gpu.link_bw)),
-                                          p.h, tokens, C.byref(out)))
+                                          p.h, tokens, mean_seq_len, C.byref(out)))
     return {k: getattr(out, k) for k, _ in AnalyticC._fields_ if k != "reserved"}

@@ -62,22 +62,22 @@ int main() {
   int bad = 0;
   try {
     for (int engine : {DWDP_ENGINE_COPY, DWDP_ENGINE_PULL}) {
-      dwdpsim_b200::Engine r0(tiny(0, 2, engine)), r1(tiny(1, 2, engine)), full(tiny(0, 1, engine));
+      dwdpsim::Engine r0(tiny(0, 2, engine)), r1(tiny(1, 2, engine)), full(tiny(0, 1, engine));
       r0.init_weights();
       r1.init_weights();
       full.init_weights();
       dwdp_ctx* pair[2] = {r0.get(), r1.get()};
-      dwdpsim_b200::check(dwdp_ctx_link_local(pair, 2));
+      dwdpsim::detail::check(dwdp_ctx_link_local(pair, 2));
       const int64_t T = 300, h = 512;
       CUdeviceptr x, y, yf;
       CU(cuMemAlloc(&x, size_t(T * h * 2)));
       CU(cuMemAlloc(&y, size_t(T * h * 2)));
       CU(cuMemAlloc(&yf, size_t(T * h * 2)));
-      dwdpsim_b200::check(dwdp_fill_bf16(reinterpret_cast<void*>(x), T * h, 77, 1.0f, nullptr));
+      dwdpsim::detail::check(dwdp_fill_bf16(reinterpret_cast<void*>(x), T * h, 77, 1.0f, nullptr));
       std::vector<uint16_t> a(size_t(T * h)), b(size_t(T * h));
       for (int64_t g = 0; g < 4; ++g) {  // crosses the stack boundary (L = 3)
         r0.layer_forward(g, reinterpret_cast<void*>(x), T, reinterpret_cast<void*>(y), false, nullptr);
-        dwdpsim_b200::check(dwdp_moe_forward(full.get(), int(g % 3), reinterpret_cast<void*>(x), T,
+        dwdpsim::detail::check(dwdp_moe_forward(full.get(), int(g % 3), reinterpret_cast<void*>(x), T,
                                              reinterpret_cast<void*>(yf), nullptr));
         CU(cuCtxSynchronize());
         CU(cuMemcpyDtoH(a.data(), y, a.size() * 2));
@@ -89,7 +89,7 @@ int main() {
       }
       dwdp_layer_record rec[8];
       size_t n = 8;
-      dwdpsim_b200::check(dwdp_ctx_records(r0.get(), rec, &n));
+      dwdpsim::detail::check(dwdp_ctx_records(r0.get(), rec, &n));
       std::printf("R engine=%d records=%zu prefetch_bytes=%.0f\n", engine, n,
                   n > 1 ? rec[1].prefetch_bytes : -1.0);
       cuMemFree(x);

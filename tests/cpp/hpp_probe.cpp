@@ -5,7 +5,7 @@
 
 #include "dwdp.hpp"
 
-using namespace dwdpsim_b200;
+using namespace dwdpsim;
 
 int main() {
   const int cases[][3] = {{256, 8, 0}, {256, 3, 0}, {16, 4, 1}, {97, 5, 2}};
@@ -28,7 +28,13 @@ int main() {
   } catch (const ConfigError&) {
     std::printf("E ConfigError\n");
   }
-  const auto r = route_tokens(100, 16, 2, 1.2, 1);
+  MoeModelSpec m;
+  m.hidden_dim = 512;
+  m.num_experts = 16;
+  m.top_k = 2;
+  m.expert_ffn_dim = 1024;
+  m.attn_proj_params = 1;
+  const auto r = route_tokens(100, m, 1.2, 1);
   std::printf("R");
   for (auto v : r) std::printf(" %lld", static_cast<long long>(v));
   std::printf("\n");

@@ -185,3 +185,42 @@ def test_costs_match_reference_golden():
     assert D.roofline_time(1e12, 0, D.GpuSpec(1e12, 1e12, 1e9)) == 1.0
     with pytest.raises(D.ConfigError):
         D.roofline_time(0, 0, D.GpuSpec())
+
+
+def test_batches_csv_round_trip_and_errors():
+    """workload.hpp:77-79: exact workload replay through the reference's CSV
+    format (src/workload.cpp:191-247)."""
+    spec = D.WorkloadSpec(D.IslDist.uniform_ratio(1000, 0.5), 4000, 3, 1.0, 7)
+    model = D.MoeModelSpec(1, 64, 256, 8, 16, 0, 1.0, 2.0, attn_proj_params=100)
+    b = D.sample_batches(spec, model, 3, 5)
+    csv = D.batches_to_csv(b)
+    assert csv.startswith("iteration,rank,tokens,requests,expert_counts\n")
+    back = D.batches_from_csv(csv)
+    assert [x.tokens for x in back] == [x.tokens for x in b]
+    assert [x.requests for x in back] == [x.requests for x in b]
+    assert [x.routed for x in back] == [x.routed for x in b]
+    assert D.batches_to_csv(back) == csv
+    nr = D.sample_batches(spec, model, 2, 2, with_routing=False)
+    assert D.batches_from_csv(D.batches_to_csv(nr))[1].tokens == nr[1].tokens
+    for bad in ("bogus", "", "iteration,rank,tokens,requests,expert_counts\n0,0,x,1,\n"):
+        with pytest.raises(D.ConfigError):
+            D.batches_from_csv(bad)
+    with pytest.raises(D.ConfigError):
+        D.WorkloadSpec(D.IslDist.fixed(2000), 1000).validate()
+
+
+def test_layer_costs_and_model_validate():
+    """modelspec.cpp:6-98: attention + MoE entries, calibration scalars."""
+    m = D.r1_model(1)
+    m.validate()
+    w = D.layer_costs(m, 4096, 2048)
+    assert [op.category for op in w.attn] == ["Attention"]
+    assert [op.category for op in w.moe] == ["GroupedGEMM", "DenseGEMM"]
+    assert w.moe[0].flops == pytest.approx(2.0 * 4096 * 8 * 3 * 7168 * 2048)
+    m2 = D.r1_model(1)
+    m2.calib = D.CostCalibration(grouped_gemm=0.5)
+    assert D.layer_costs(m2, 4096, 2048).moe[0].flops == pytest.approx(0.5 * w.moe[0].flops)
+    with pytest.raises(D.ConfigError):
+        D.MoeModelSpec(1, 8, 4, 2, 4).validate()  # attn_proj_params must be > 0
+    with pytest.raises(D.ConfigError):
+        D.layer_costs(m, 0, 1)
