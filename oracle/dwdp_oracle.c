@@ -828,14 +828,26 @@ static void ffn_rows_w8a8(int mode, const float* gate, const float* up, const fl
 static void ffn_rows_bf16(const uint16_t* gate, const uint16_t* up, const uint16_t* down,
                           int64_t h, int64_t f, const float* const* xr, const float* scale,
                           float* const* yr, int n, float* hbuf) {
-  /* weight rows outer, token rows inner: each weight row is streamed once */
-  for (int64_t j = 0; j < f; ++j)
+  /* weight rows outer, token rows inner: each weight row is streamed once
+   * and widened to fp32 once (dotf over the widened row is the same sum as
+   * dot_bf16 over the bf16 row) */
+  const int64_t mx = h > f ? h : f;
+  float* wg = malloc(sizeof(float) * (size_t)mx);
+  float* wu = malloc(sizeof(float) * (size_t)mx);
+  for (int64_t j = 0; j < f; ++j) {
+    for (int64_t i = 0; i < h; ++i) {
+      wg[i] = bf16_to_f32(gate[j * h + i]);
+      wu[i] = bf16_to_f32(up[j * h + i]);
+    }
     for (int r = 0; r < n; ++r)
-      hbuf[(int64_t)r * f + j] =
-          siluf(dot_bf16(xr[r], gate + j * h, h)) * dot_bf16(xr[r], up + j * h, h);
-  for (int64_t i = 0; i < h; ++i)
-    for (int r = 0; r < n; ++r)
-      yr[r][i] += scale[r] * dot_bf16(hbuf + (int64_t)r * f, down + i * f, f);
+      hbuf[(int64_t)r * f + j] = siluf(dotf(xr[r], wg, h)) * dotf(xr[r], wu, h);
+  }
+  for (int64_t i = 0; i < h; ++i) {
+    for (int64_t j = 0; j < f; ++j) wg[j] = bf16_to_f32(down[i * f + j]);
+    for (int r = 0; r < n; ++r) yr[r][i] += scale[r] * dotf(hbuf + (int64_t)r * f, wg, f);
+  }
+  free(wg);
+  free(wu);
 }
 
 /* y_rows[r] += scale[r] * FFN(x_rows[r]) for n rows of one expert. Weight

@@ -5,6 +5,7 @@
 
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -635,10 +636,8 @@ int dwdp_moe_forward(dwdp_ctx* c, int layer, const void* x, int64_t T, void* y, 
       need(x, "x");
       need(y, "y");
     }
-    auto& ctx = C(c);
-    dwdp::require(layer >= 0 && layer < ctx.cfg.num_layers, "moe_forward: layer out of range");
-    ctx.moe_forward(layer, ctx.resident_parity(layer), static_cast<const uint16_t*>(x), T, static_cast<uint16_t*>(y),
-                    nullptr, static_cast<cudaStream_t>(stream));
+    C(c).moe_forward_resident(layer, static_cast<const uint16_t*>(x), T, static_cast<uint16_t*>(y),
+                              static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -732,8 +731,10 @@ namespace {
 // TMA maps and tables (one per device).
 dwdp::Ctx* tiny_ctx() {
   static dwdp::Ctx* tiny[64] = {nullptr};
+  static std::mutex mu;  // several host threads (one per GPU) may call in
   int dev = 0;
   cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
   if (!tiny[dev]) {
     dwdp_ctx_config cfg{};
     cfg.num_layers = 1;

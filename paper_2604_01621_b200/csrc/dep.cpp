@@ -394,7 +394,7 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   DWDP_CUDA(cudaGetLastError());
   DWDP_CUDA(cudaEventRecord(rec.moe_end, st));
   rec.rows = routed_rows;
-  recs_.push_back(rec);
+  push_record(rec);
 }
 
 void Ctx::dep_stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t st) {

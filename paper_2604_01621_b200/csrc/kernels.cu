@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdlib>
 #include <cstdint>
 
@@ -1263,9 +1264,11 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
                                                       const float* __restrict__ wts,
                                                       const uint16_t* __restrict__ S,
                                                       const int32_t* __restrict__ s_meta,
-                                                      const uint16_t* __restrict__ resid,
-                                                      uint16_t* __restrict__ y, int64_t T, int k,
-                                                      int64_t h) {
+                                                      const uint16_t* resid, uint16_t* y,
+                                                      int64_t T, int k, int64_t h) {
+  // resid and y alias when a stack runs in place (y = x + MoE(x) for layers
+  // l >= 1): no __restrict__ / non-coherent loads on them. Each thread reads
+  // its own 16-byte segment of resid before writing that segment of y.
   const int64_t t = blockIdx.x;
   if (t >= T) return;
   __shared__ int32_t srow[TOPK_MAXK + 1];
@@ -1289,7 +1292,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
     for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
     uint4 vs = make_uint4(0, 0, 0, 0), vr = make_uint4(0, 0, 0, 0);
     if (shared) vs = __ldg(reinterpret_cast<const uint4*>(S + int64_t(srow[TOPK_MAXK]) * h) + s);
-    if (resid) vr = __ldg(reinterpret_cast<const uint4*>(resid + t * h) + s);
+    if (resid) vr = reinterpret_cast<const uint4*>(resid + t * h)[s];
     for (int j0 = 0; j0 < k; j0 += CB) {
       uint4 v[CB];
 #pragma unroll
@@ -1602,25 +1605,29 @@ void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
 void launch_pull(const PullItem* items, int n, uint64_t max_len, int ctas, cudaStream_t st) {
   // chunk size and ring depth: 8 KB x 3 by default; DWDP_PULL_CHUNK /
   // DWDP_PULL_BUFS override them for experiments (the ring must stay small
-  // enough to co-reside with a grouped-GEMM CTA)
-  static int chunk = 0, bufs = 0;
-  static bool attr_set[64] = {false};
-  if (chunk == 0) {
+  // enough to co-reside with a grouped-GEMM CTA). One host thread per GPU may
+  // call concurrently: the settings are a thread-safe static, the smem
+  // attribute is set once per device.
+  struct PullCfg {
+    int chunk, bufs;
+  };
+  static const PullCfg pc = [] {
     const char* c = std::getenv("DWDP_PULL_CHUNK");
     const char* b = std::getenv("DWDP_PULL_BUFS");
-    chunk = c ? std::max(1024, std::min(65536, std::atoi(c))) / 16 * 16 : PULL_CHUNK_DEFAULT;
-    bufs = b ? std::max(1, std::min(PULL_BUFS_MAX, std::atoi(b))) : PULL_BUFS_DEFAULT;
-  }
+    return PullCfg{c ? std::max(1024, std::min(65536, std::atoi(c))) / 16 * 16 : PULL_CHUNK_DEFAULT,
+                   b ? std::max(1, std::min(PULL_BUFS_MAX, std::atoi(b))) : PULL_BUFS_DEFAULT};
+  }();
+  static std::once_flag attr_once[64];
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!attr_set[dev]) {
+  std::call_once(attr_once[dev & 63], [] {
     cudaFuncSetAttribute(tma_pull_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          PULL_BUFS_MAX * 65536 > 200 * 1024 ? 200 * 1024 : PULL_BUFS_MAX * 65536);
-    attr_set[dev] = true;
-  }
-  const uint64_t total = (max_len + chunk - 1) / chunk * uint64_t(n);
+  });
+  const uint64_t total = (max_len + pc.chunk - 1) / pc.chunk * uint64_t(n);
   if (n > 0)
-    tma_pull_kernel<<<ctas, 32, size_t(bufs) * chunk, st>>>(items, n, total, uint32_t(chunk), bufs);
+    tma_pull_kernel<<<ctas, 32, size_t(pc.bufs) * pc.chunk, st>>>(items, n, total, uint32_t(pc.chunk),
+                                                                  pc.bufs);
 }
 
 }  // namespace dwdp

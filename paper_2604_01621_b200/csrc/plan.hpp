@@ -26,6 +26,9 @@ struct InvariantViolation : std::logic_error {
 inline void require(bool ok, const char* msg) {
   if (!ok) throw ConfigError(msg);
 }
+inline void require(bool ok, const std::string& msg) {
+  if (!ok) throw ConfigError(msg);
+}
 inline void invariant(bool ok, const char* msg) {
   if (!ok) throw InvariantViolation(msg);
 }

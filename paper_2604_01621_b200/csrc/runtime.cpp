@@ -21,7 +21,8 @@ struct IpcBlob {
   uint32_t magic;
   int32_t rank, nslots, c;
   int64_t slot_elems;
-  int32_t ntens, reserved;
+  int32_t ntens, weight_layers;
+  int32_t weight_dtype, group_size;
   cudaIpcMemHandle_t h[9];
 };
 static_assert(sizeof(IpcBlob) <= DWDP_IPC_BLOB_BYTES, "ipc blob too large");
@@ -232,7 +233,6 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   DWDP_CUDA(cudaEventRecord(epoch_, copy_st_));
   for (auto& ev : moe_done_) DWDP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   for (int t = 0; t < 9; ++t) peer_arena_[t].assign(size_t(N_), nullptr);
-  resident_parity_.assign(size_t(L_), 0);
   build_copy_plan();
   DWDP_CUDA(cudaDeviceSynchronize());
 }
@@ -385,6 +385,9 @@ void Ctx::export_ipc(void* out) {
   b.c = c_;
   b.slot_elems = slot_elems_;
   b.ntens = ntens_;
+  b.weight_layers = WL_;
+  b.weight_dtype = cfg.weight_dtype;
+  b.group_size = N_;
   for (int t = 0; t < ntens_; ++t) DWDP_CUDA(cudaIpcGetMemHandle(&b.h[t], tbase(t)));
   std::memset(out, 0, DWDP_IPC_BLOB_BYTES);
   std::memcpy(out, &b, sizeof b);
@@ -397,7 +400,9 @@ void Ctx::open_peers(const void* blobs) {
     IpcBlob b;
     std::memcpy(&b, static_cast<const uint8_t*>(blobs) + size_t(p) * DWDP_IPC_BLOB_BYTES, sizeof b);
     require(b.magic == kIpcMagic && b.rank == p, "open_peers: malformed blob");
-    require(b.c == c_ && b.slot_elems == slot_elems_ && b.ntens == ntens_,
+    // peer_src() indexes the peer's owned region with this rank's geometry
+    require(b.c == c_ && b.slot_elems == slot_elems_ && b.ntens == ntens_ && b.nslots == nslots_ &&
+                b.weight_layers == WL_ && b.weight_dtype == cfg.weight_dtype && b.group_size == N_,
             "open_peers: peer arena geometry differs");
     for (int t = 0; t < ntens_; ++t) {
       void* ptr = nullptr;
@@ -508,7 +513,14 @@ void Ctx::read_expert(int layer, int expert, int t, void* host) {
   require(layer >= 0 && layer < L_ && expert >= 0 && expert <= E_ && t >= 0 && t < ntens_,
           "read_expert: index out of range");
   require(expert < E_ || shared_, "read_expert: no shared expert");
-  const int slot = slot_of(layer, resident_parity_[size_t(layer)], expert);
+  int par = 0;
+  if (expert < E_ && recv_index_[size_t(expert)] >= 0) {  // remote: a receive buffer
+    par = resident_buffer(layer);
+    require(par >= 0, "read_expert: the layer's remote experts are not resident");
+    // the copy stream fills the buffer asynchronously: wait for its plan
+    DWDP_CUDA(cudaEventSynchronize(plan_at(plan_of_g_.at(buf_owner_[par]))->done));
+  }
+  const int slot = slot_of(layer, par, expert);
   DWDP_CUDA(cudaMemcpy(host, tbase(t) + uint64_t(slot) * tsb(t), tsb(t), cudaMemcpyDeviceToHost));
 }
 
@@ -530,12 +542,17 @@ int64_t Ctx::prefetch_issue(int64_t g) {
   DeviceGuard dg(cfg.device);
   if (nrecv_ == 0) return -1;  // full replication: nothing to fetch (simcore.cpp:625-628)
   require(g >= 0, "prefetch_issue: negative layer");
-  if (plan_of_g_.size() <= size_t(g)) plan_of_g_.resize(size_t(g) + 1, -2);
-  invariant(plan_of_g_[size_t(g)] == -2, "dwdp: plan double issue");
+  invariant(plan_of_g_.count(g) == 0, "dwdp: plan double issue");
+  require(g > last_issued_g_, "prefetch_issue: global layers are prefetched in increasing order");
   for (int p = 0; p < N_; ++p)
     require(p == rank_ || peer_arena_[0][size_t(p)] != nullptr, "prefetch_issue: peers not wired");
   const int par = int(g & 1), l = int(g % L_), wl = l % WL_;
-  // WAR: buffer g%2 was last read by the MoE of layer g-2.
+  // The buffer's current owner (layer g-2 in the double-buffer protocol)
+  // must have been read before it is overwritten; the copy stream then waits
+  // for that read (WAR, simcore.cpp:694-696).
+  require(buf_owner_[par] < 0 || buf_read_[par],
+          "prefetch_issue: receive buffer " + std::to_string(par) + " still holds global layer " +
+              std::to_string(buf_owner_[par]) + ", whose MoE has not been enqueued");
   if (moe_done_recorded_[par]) DWDP_CUDA(cudaStreamWaitEvent(copy_st_, moe_done_[par], 0));
   Plan pl;
   pl.g = g;
@@ -604,16 +621,53 @@ int64_t Ctx::prefetch_issue(int64_t g) {
     }
   }
   DWDP_CUDA(cudaEventRecord(pl.done, copy_st_));
+  const int64_t h = plan_base_ + int64_t(plans_.size());
   plans_.push_back(pl);
-  plan_of_g_[size_t(g)] = int64_t(plans_.size()) - 1;
-  resident_parity_[size_t(l)] = par;
-  return int64_t(plans_.size()) - 1;
+  plan_of_g_[g] = h;
+  buf_owner_[par] = g;
+  buf_read_[par] = false;
+  last_issued_g_ = g;
+  retire_plans();
+  return h;
+}
+
+Plan* Ctx::plan_at(int64_t h) {
+  require(h >= 0 && h < plan_base_ + int64_t(plans_.size()), "prefetch: unknown handle");
+  if (h < plan_base_) return nullptr;  // retired: completed, events recycled
+  return &plans_[size_t(h - plan_base_)];
+}
+
+// Drop completed plans from the front that nothing can reference any more:
+// no undrained record reads their times and neither receive buffer is (or
+// will be) waited on through them (the two newest plans stay).
+void Ctx::retire_plans() {
+  while (plans_.size() > 2) {
+    Plan& p = plans_.front();
+    if (p.refs > 0 || p.g == buf_owner_[0] || p.g == buf_owner_[1]) break;
+    const cudaError_t q = cudaEventQuery(p.done);
+    if (q == cudaErrorNotReady) break;
+    DWDP_CUDA(q);
+    free_events_.push_back(p.start);
+    free_events_.push_back(p.done);
+    plan_of_g_.erase(p.g);
+    plans_.pop_front();
+    ++plan_base_;
+  }
+}
+
+int Ctx::resident_buffer(int layer) const {
+  int best = -1;
+  for (int p = 0; p < 2; ++p)
+    if (buf_owner_[p] >= 0 && buf_owner_[p] % L_ == layer && (best < 0 || buf_owner_[p] > buf_owner_[best]))
+      best = p;
+  return best;
 }
 
 bool Ctx::prefetch_done(int64_t h) {
   if (h < 0) return true;
-  require(size_t(h) < plans_.size(), "prefetch: unknown handle");
-  const cudaError_t e = cudaEventQuery(plans_[size_t(h)].done);
+  const Plan* p = plan_at(h);
+  if (!p) return true;
+  const cudaError_t e = cudaEventQuery(p->done);
   if (e == cudaErrorNotReady) return false;
   DWDP_CUDA(e);
   return true;
@@ -621,16 +675,18 @@ bool Ctx::prefetch_done(int64_t h) {
 
 void Ctx::prefetch_wait(int64_t h, cudaStream_t st) {
   if (h < 0) return;
-  require(size_t(h) < plans_.size(), "prefetch: unknown handle");
-  DWDP_CUDA(cudaStreamWaitEvent(st, plans_[size_t(h)].done, 0));
+  const Plan* p = plan_at(h);
+  if (p) DWDP_CUDA(cudaStreamWaitEvent(st, p->done, 0));
 }
 
 void Ctx::prefetch_times(int64_t h, int64_t* s, int64_t* e, double* bytes) {
   *s = *e = -1;
   *bytes = 0;
   if (h < 0) return;
-  require(size_t(h) < plans_.size(), "prefetch: unknown handle");
-  const Plan& p = plans_[size_t(h)];
+  const Plan* pp = plan_at(h);
+  require(pp != nullptr, "prefetch_times: plan retired (times are kept for the two newest plans "
+                         "and for plans of undrained layer records)");
+  const Plan& p = *pp;
   *bytes = p.bytes;
   if (!prefetch_done(h)) return;
   float ms0 = 0, ms1 = 0;
@@ -773,20 +829,33 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
 void Ctx::layer_forward(int64_t g, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
                         cudaStream_t st) {
   DeviceGuard dg(cfg.device);
+  require(g >= 0, "layer_forward: negative global layer");
   const int l = int(g % L_), par = int(g & 1);
+  if (nrecv_ > 0) {
+    // A layer runs on the experts its own plan brought in: replaying a
+    // global layer whose buffer was refilled since (or one that was never
+    // prefetched but lies behind the prefetch cursor) would silently compute
+    // with another layer's weights.
+    if (plan_of_g_.count(g) == 0)
+      require(g > last_issued_g_, "layer_forward: global layer " + std::to_string(g) +
+                                      " is behind the prefetch cursor (" +
+                                      std::to_string(last_issued_g_) + "); global layers only advance");
+    else
+      require(buf_owner_[par] == g, "layer_forward: receive buffer " + std::to_string(par) +
+                                        " no longer holds global layer " + std::to_string(g));
+  }
   cursor_ = std::max(cursor_, g + 1);
   LayerRec rec{g, T, take_event(), take_event(), take_event(), nullptr, -1};
   DWDP_CUDA(cudaEventRecord(rec.gate0, st));
   if (nrecv_ > 0) {
-    if (plan_of_g_.size() <= size_t(g) || plan_of_g_[size_t(g)] == -2) prefetch_issue(g);
-    rec.plan = plan_of_g_[size_t(g)];
+    if (plan_of_g_.count(g) == 0) prefetch_issue(g);
+    rec.plan = plan_of_g_.at(g);
     prefetch_wait(rec.plan, st);  // weight_wait (simcore.cpp:684-690)
   }
   DWDP_CUDA(cudaEventRecord(rec.gate1, st));
   // Double buffering: the next layer's buffer is free once this layer's
-  // weights are in use (simcore.cpp:694-696).
-  if (nrecv_ > 0 && (plan_of_g_.size() <= size_t(g + 1) || plan_of_g_[size_t(g + 1)] == -2))
-    prefetch_issue(g + 1);
+  // weights are in use (simcore.cpp:694-696): its owner g-1 was read.
+  if (nrecv_ > 0 && plan_of_g_.count(g + 1) == 0 && g + 1 > last_issued_g_) prefetch_issue(g + 1);
   if (nrecv_ > 0 && !cfg.merge_elim) {  // D2D merge baseline (simcore.cpp:700-703)
     for (int t = 0; t < ntens_; ++t)
       DWDP_CUDA(cudaMemcpyAsync(tbase(t) + uint64_t(merge_base_) * tsb(t),
@@ -798,8 +867,55 @@ void Ctx::layer_forward(int64_t g, const uint16_t* x, int64_t T, uint16_t* y, bo
   moe_forward(l, par, x, T, y, residual ? x : nullptr, st, &rec);
   DWDP_CUDA(cudaEventRecord(moe_done_[par], st));
   moe_done_recorded_[par] = true;
+  if (buf_owner_[par] == g) buf_read_[par] = true;
   DWDP_CUDA(cudaEventRecord(rec.moe_end, st));
+  push_record(rec);
+}
+
+void Ctx::moe_forward_resident(int layer, const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t st) {
+  DeviceGuard dg(cfg.device);
+  require(layer >= 0 && layer < L_, "moe_forward: layer out of range");
+  if (nrecv_ == 0) {  // every expert local
+    moe_forward(layer, 0, x, T, y, nullptr, st);
+    return;
+  }
+  const int par = resident_buffer(layer);
+  require(par >= 0, "moe_forward: the remote experts of layer " + std::to_string(layer) +
+                        " are not resident; prefetch a global layer of it first "
+                        "(dwdp_prefetch_issue or dwdp_layer_forward)");
+  prefetch_wait(plan_of_g_.at(buf_owner_[par]), st);
+  moe_forward(layer, par, x, T, y, nullptr, st);
+  DWDP_CUDA(cudaEventRecord(moe_done_[par], st));
+  moe_done_recorded_[par] = true;
+  buf_read_[par] = true;
+}
+
+void Ctx::push_record(const LayerRec& rec) {
+  if (rec.plan >= 0) {
+    Plan* p = plan_at(rec.plan);
+    if (p) ++p->refs;
+  }
   recs_.push_back(rec);
+  // Nobody draining (kernel_timing off, no accounting): keep the newest
+  // kMaxRecords and recycle the rest, so state stays bounded and the pinned
+  // routed-rows ring (kMetaRing slots) is never reused under a live record.
+  while (recs_.size() > kMaxRecords) {
+    LayerRec old = recs_.front();
+    recs_.pop_front();
+    DWDP_CUDA(cudaEventSynchronize(old.moe_end));
+    release_record(old);
+  }
+}
+
+void Ctx::release_record(const LayerRec& r) {
+  for (cudaEvent_t e : {r.gate0, r.gate1, r.moe_end, r.merge_end, r.k[0], r.k[1], r.k[2], r.k[3],
+                        r.comm[0], r.comm[1], r.comm[2], r.comm[3]})
+    if (e) free_events_.push_back(e);
+  if (r.plan >= 0) {
+    Plan* p = plan_at(r.plan);
+    if (p) --p->refs;
+  }
+  retire_plans();
 }
 
 // One iteration of the stack starts at the next global layer that is layer 0
@@ -841,11 +957,11 @@ size_t Ctx::drain_records(dwdp_layer_record* out, size_t cap) {
     DWDP_CUDA(cudaEventElapsedTime(&moe, r.merge_end ? r.merge_end : r.gate1, r.moe_end));
     if (r.merge_end) DWDP_CUDA(cudaEventElapsedTime(&merge, r.gate1, r.merge_end));
     double pbytes = 0;
-    if (r.plan >= 0) {
-      const Plan& p = plans_[size_t(r.plan)];
-      DWDP_CUDA(cudaEventSynchronize(p.done));
-      DWDP_CUDA(cudaEventElapsedTime(&pf, p.start, p.done));
-      pbytes = p.bytes;
+    const Plan* plan = r.plan >= 0 ? plan_at(r.plan) : nullptr;  // refs > 0: never retired
+    if (plan) {
+      DWDP_CUDA(cudaEventSynchronize(plan->done));
+      DWDP_CUDA(cudaEventElapsedTime(&pf, plan->start, plan->done));
+      pbytes = plan->bytes;
     }
     auto el = [](cudaEvent_t a, cudaEvent_t b) {
       float ms = 0;
@@ -868,18 +984,16 @@ size_t Ctx::drain_records(dwdp_layer_record* out, size_t cap) {
     const int64_t rows = r.rows >= 0 ? r.rows : r.meta_slot >= 0 ? meta_ring_[r.meta_slot * 4 + 2] : -1;
     const double dispatch = (r.k[1] && r.comm[1]) ? el(r.k[1], r.comm[1]) : 0.0;
     double pf0 = -1, pf1 = -1;
-    if (r.plan >= 0) {
-      pf0 = el(epoch_, plans_[size_t(r.plan)].start);
-      pf1 = el(epoch_, plans_[size_t(r.plan)].done);
+    if (plan) {
+      pf0 = el(epoch_, plan->start);
+      pf1 = el(epoch_, plan->done);
     }
     if (out)
       out[n] = {r.g,    r.tokens, double(wait) * 1e6, double(moe) * 1e6, double(pf) * 1e6, pbytes,
                 double(merge) * 1e6, kns[0], kns[1], kns[2], kns[3], kns[4], rows, comm, dispatch,
                 el(epoch_, r.gate0), el(epoch_, r.moe_end), pf0, pf1};
     ++n;
-    for (cudaEvent_t e : {r.gate0, r.gate1, r.moe_end, r.merge_end, r.k[0], r.k[1], r.k[2], r.k[3],
-                          r.comm[0], r.comm[1], r.comm[2], r.comm[3]})
-      if (e) free_events_.push_back(e);
+    release_record(r);
   }
   return n;
 }

@@ -4,8 +4,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <deque>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -44,6 +46,7 @@ struct Plan {  // one issued prefetch (CopyEngineSim::Plan)
   int64_t g = -1;
   cudaEvent_t start = nullptr, done = nullptr;
   double bytes = 0;
+  int refs = 0;  // undrained layer records that read this plan's times
 };
 
 struct LayerRec {
@@ -76,6 +79,11 @@ class Ctx {
 
   void moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint16_t* y,
                    const uint16_t* resid, cudaStream_t st, LayerRec* rec = nullptr);
+  // Public MoE forward of `layer` (dwdp_moe_forward): the remote experts must
+  // be resident -- a receive buffer holds a prefetched global layer g with
+  // g % L == layer; the stream waits for that plan and the read is recorded
+  // so a later prefetch into the buffer waits for it (WAR).
+  void moe_forward_resident(int layer, const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t st);
   void layer_forward(int64_t g, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
                      cudaStream_t st);
   void stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t st);
@@ -83,7 +91,6 @@ class Ctx {
              int32_t* counts, int32_t* row_of, int64_t* rows, cudaStream_t st);
   size_t drain_records(dwdp_layer_record* out, size_t cap);
   std::vector<Slice> copy_plan() const { return plan_slices_; }
-  int resident_parity(int l) const { return resident_parity_.at(size_t(l)); }
 
   void gemm_nvfp4(const uint8_t* A, const uint8_t* Asf, const float* As, const uint8_t* B,
                   const uint8_t* Bsf, const float* Bs, uint16_t* D, int64_t M, int64_t N, int64_t K,
@@ -100,7 +107,7 @@ class Ctx {
 
   dwdp_ctx_config cfg;
   uint64_t weight_bytes = 0, recv_bytes = 0, workspace_bytes = 0;
-  int64_t launches = 0;
+  std::atomic<int64_t> launches{0};
 
  private:
   void* dalloc(size_t bytes, uint64_t* account);
@@ -200,14 +207,30 @@ class Ctx {
   cudaEvent_t epoch_ = nullptr;
   cudaEvent_t moe_done_[2] = {nullptr, nullptr};
   bool moe_done_recorded_[2] = {false, false};
-  std::vector<Plan> plans_;
-  std::vector<int64_t> plan_of_g_;  // global layer -> plan index (-1 preloaded)
+  // Receive-buffer ownership: buffer p holds the experts of global layer
+  // buf_owner_[p] (-1: never filled); buf_read_[p] once an MoE reading them
+  // is enqueued (moe_done_[p] recorded after it). A plan may only overwrite
+  // a buffer whose owner has been read.
+  int64_t buf_owner_[2] = {-1, -1};
+  bool buf_read_[2] = {false, false};
+  int64_t last_issued_g_ = -1;
+  // Live plans: handle h lives at plans_[h - plan_base_]; done plans that no
+  // undrained record references and that no buffer can still be waiting on
+  // are retired (their events recycled), so serving loops hold O(1) state.
+  std::deque<Plan> plans_;
+  int64_t plan_base_ = 0;
+  std::map<int64_t, int64_t> plan_of_g_;  // live global layer -> plan handle
+  Plan* plan_at(int64_t h);
+  void retire_plans();
+  int resident_buffer(int layer) const;  // parity holding `layer`, -1 if none
+  void push_record(const LayerRec& rec);
+  void release_record(const LayerRec& r);
+  static constexpr size_t kMaxRecords = 2048;  // undrained records kept (oldest dropped)
   PullItem* pull_items_ = nullptr;  // device [WL][2][n_slices]
   PullItem* pull_items_odd_ = nullptr;  // hybrid: device [WL][2][n_slices / 2] (odd slices)
   size_t n_odd_ = 0;
   uint64_t pull_max_len_ = 0;          // longest slice (pull-kernel chunk grid)
   int64_t cursor_ = 0;              // next global layer of stack_forward
-  std::vector<int> resident_parity_;
   std::deque<LayerRec> recs_;
   std::vector<cudaEvent_t> free_events_;
   cudaEvent_t take_event();
