@@ -94,37 +94,60 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def cpu_baseline(tokens: int, layers: int):
-    """Oracle port on this host's cores (bounded sample), rank 0 / N = 1 only."""
+REF_BUDGET_S = 150.0  # wall budget of the --impl reference arm's W + K steps
+
+
+def pick_cpu_tokens(stack, steps: int, budget_s: float = REF_BUDGET_S,
+                    candidates=(1024, 512, 256, 128, 64, 32, 16)) -> int:
+    """Largest C2 sample (tokens per step through the whole stack) whose
+    `steps` steps fit the budget, from one timed 16-token probe step (per-token
+    cost only falls with T: weight streaming amortises)."""
+    import time as _t
+    x = stack.input(16)
+    t0 = _t.perf_counter()
+    stack.forward(x, 16)
+    per_tok = (_t.perf_counter() - t0) / 16
+    for T in candidates:
+        if per_tok * T * steps <= budget_s:
+            return T
+    return candidates[-1]
+
+
+def cpu_baseline(layers: int, tokens: int = 0):
+    """Oracle port on this host's cores (bounded samples), rank 0 / N = 1 only:
+    SURVEY.md §8(d) C1 layer at T in {1, 7, 64, 1000}, one C2 layer at T in
+    {64, 256, 1024}, and `value` = the L-layer C2 stack at the reference arm's
+    sample size."""
     from oracle import cpu_moe
-    tps, cores, secs = cpu_moe.time_layer(tokens, layers, steps=1, warmup=1)
-    return {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port",
-            "sample": f"{tokens} tokens through the {layers}-layer R1 MoE stack "
-                      f"(fp32 math, bf16 resident weights, {secs:.1f} s/step)"}
+    sw = cpu_moe.sweep(c2_tokens=())
+    stack = cpu_moe.CpuStack(cpu_moe.r1_config(), layers)
+    for T in (64, 256, 1024):
+        sw["c2_layer_tokens_per_s"][str(T)] = stack.tokens_per_s(T, layers=1, min_s=0.0)
+    T = tokens or pick_cpu_tokens(stack, 25)
+    tps = stack.tokens_per_s(T, min_s=0.0)
+    return {"value": tps, "unit": "tokens/s", "cores": sw["cores"], "kind": "port",
+            "sample": f"{T} tokens/step through the {layers}-layer R1 MoE stack (fp32 math, bf16 "
+                      f"resident weights); C1/C2 per-layer sweeps beside it",
+            "tokens_per_step": T, "c1_layer_tokens_per_s": sw["c1_layer_tokens_per_s"],
+            "c2_layer_tokens_per_s": sw["c2_layer_tokens_per_s"]}
 
 
 def reference_arm(args):
     """--impl reference: the CPU path of the hot path (oracle/ C restatement of the
-    MoE layer; the reference itself has no numerical MoE) on all host cores."""
+    MoE layer; the reference itself has no numerical MoE) on all host cores, on
+    the largest C2 sample whose W + K steps fit REF_BUDGET_S."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import cpu_moe, oracle as O
-    tokens = args.ref_tokens
-    layer = cpu_moe.CpuMoeLayer(cpu_moe.r1_config(), 2604_01621)
-    x = O.oracle().fill_bf16(0xC0FFEE, tokens * R1["h"], 1.0)
-    for _ in range(max(args.warmup, 1)):  # materialise every expert the stack touches
-        h = x
-        for _ in range(args.layers):
-            layer.prepare(h, tokens)
-            y, _, _ = layer.forward(h, tokens)
-            h = O.bf16_round(O.bf16_to_f32(h).reshape(tokens, -1) + y).reshape(-1)
+    stack = cpu_moe.CpuStack(cpu_moe.r1_config(), args.layers)
+    tokens = args.ref_tokens or pick_cpu_tokens(stack, args.warmup + args.steps)
+    x = stack.input(tokens)
+    for _ in range(max(args.warmup, 1)):
+        stack.forward(x, tokens)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        h = x
-        for _ in range(args.layers):
-            y, _, _ = layer.forward(h, tokens)
-            h = O.bf16_round(O.bf16_to_f32(h).reshape(tokens, -1) + y).reshape(-1)
+        stack.forward(x, tokens)
     dt = (time.perf_counter() - t0) / args.steps
     value = tokens / dt
     sim = None
@@ -140,8 +163,10 @@ def reference_arm(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "R1 MoE stack (CPU oracle port, bounded sample)",
-                       "layers": args.layers, "tokens_per_step": tokens},
+            "config": {"workload": "R1 MoE stack, config 2 shapes (CPU oracle port, bounded sample)",
+                       "layers": args.layers, "tokens_per_step": tokens,
+                       "sample_rule": f"largest T in 1024..16 whose {args.warmup}+{args.steps} steps "
+                                      f"fit {REF_BUDGET_S:.0f} s on this host"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
                              "sample": f"{tokens} tokens/step x {args.layers} layers"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
@@ -172,8 +197,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dep", action="store_true", help="skip the same-box DEP baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-tokens", type=int, default=16)
-    ap.add_argument("--ref-tokens", type=int, default=16)
+    ap.add_argument("--cpu-tokens", type=int, default=0,
+                    help="cpu_baseline stack sample (0: the reference arm's budget rule)")
+    ap.add_argument("--ref-tokens", type=int, default=0,
+                    help="--impl reference tokens per step (0: largest that fits the budget)")
     ap.add_argument("--profile", action="store_true", help="1 layer, for ncu captures")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp8", "nvfp4"],
                     help="expert weights: bf16, or e4m3 W8A8 with per-row scales (config 5)")
@@ -601,7 +628,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(args.cpu_tokens, layers)
+            cpu = cpu_baseline(layers, args.cpu_tokens)
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "error": str(e)[:200]}
 

@@ -63,26 +63,52 @@ def r1_config() -> O.MoeConfig:
     return O.MoeConfig(7168, 256, 8, 2048, 2048, 1, 8, 4, 1, 2.5)
 
 
-def time_layer(tokens: int, layers: int, steps: int, warmup: int, seed: int = 2604_01621):
-    """Tokens/s of the CPU MoE stack (L layers aliasing one weight set, as the
-    GPU N=1 arm) over a bounded token sample; returns (tokens_per_s, cores, secs/step)."""
-    cfg = r1_config()
-    layer = CpuMoeLayer(cfg, seed)
-    o = layer.o
-    x = o.fill_bf16(0xC0FFEE, tokens * cfg.hidden, 1.0)
-    layer.prepare(x, tokens)
-    cores = os.cpu_count() or 1
-    for _ in range(max(warmup, 1)):  # materialises every expert the stack touches
+def tiny_config() -> O.MoeConfig:
+    """BASELINE config 1: h 512, E 16 top-2 softmax, f 1024."""
+    return O.MoeConfig(512, 16, 2, 1024, 0, 0, 1, 1, 1, 1.0)
+
+
+class CpuStack:
+    """L layers aliasing one weight set (as the GPU N=1 arm), every expert
+    materialised up front (outside timed regions)."""
+
+    def __init__(self, cfg: O.MoeConfig, layers: int, seed: int = 2604_01621):
+        self.layer = CpuMoeLayer(cfg, seed)
+        self.layer._materialise(range(cfg.num_experts + (1 if cfg.shared_ffn else 0)))
+        self.cfg, self.layers, self.o = cfg, layers, self.layer.o
+
+    def input(self, T: int) -> np.ndarray:
+        return self.o.fill_bf16(0xC0FFEE, T * self.cfg.hidden, 1.0)
+
+    def forward(self, x: np.ndarray, T: int, layers: int | None = None) -> np.ndarray:
         h = x
-        for _ in range(layers):
-            layer.prepare(h, tokens)
-            y, _, _ = layer.forward(h, tokens)
-            h = O.bf16_round(O.bf16_to_f32(h).reshape(tokens, -1) + y).reshape(-1)
+        for _ in range(self.layers if layers is None else layers):
+            y, _, _ = self.layer.forward(h, T)
+            h = O.bf16_round(O.bf16_to_f32(h).reshape(T, -1) + y).reshape(-1)
+        return h
+
+    def tokens_per_s(self, T: int, layers: int | None = None, min_s: float = 0.5) -> float:
+        """Stack tokens/s over repeated steps of T tokens (at least min_s of work)."""
+        x = self.input(T)
+        n, t0 = 0, time.perf_counter()
+        while True:
+            self.forward(x, T, layers)
+            n += 1
+            dt = time.perf_counter() - t0
+            if dt >= min_s:
+                return T * n / dt
+
+
+def sweep(c1_tokens=(1, 7, 64, 1000), c2_tokens=(64, 256, 1024)) -> dict:
+    """SURVEY.md §8(d) CPU timing: the oracle port on C1 (one layer) and on one
+    C2 (R1-shaped) layer, tokens/s, all host cores."""
+    out = {"cores": os.cpu_count() or 1, "c1_layer_tokens_per_s": {}, "c2_layer_tokens_per_s": {}}
     t0 = time.perf_counter()
-    for _ in range(steps):
-        h = x
-        for _ in range(layers):
-            y, _, _ = layer.forward(h, tokens)
-            h = O.bf16_round(O.bf16_to_f32(h).reshape(tokens, -1) + y).reshape(-1)
-    dt = (time.perf_counter() - t0) / steps
-    return tokens / dt, cores, dt
+    c1 = CpuStack(tiny_config(), 1)
+    for T in c1_tokens:
+        out["c1_layer_tokens_per_s"][str(T)] = c1.tokens_per_s(T, min_s=0.3)
+    c2 = CpuStack(r1_config(), 1)
+    for T in c2_tokens:
+        out["c2_layer_tokens_per_s"][str(T)] = c2.tokens_per_s(T, min_s=0.0)
+    out["wall_s"] = time.perf_counter() - t0
+    return out
