@@ -15,6 +15,9 @@ import paper_2604_01621_b200 as D  # noqa: E402
 
 MID = dict(num_layers=3, num_experts=64, hidden=1024, ffn=256, shared_ffn=256, top_k=6,
            n_group=8, topk_group=4, max_tokens=1024, weight_layers=3)
+# DWDP_SHAPE=r1: the DeepSeek-R1 layer (BASELINE config 3 shapes: h 7168, E 256
+# top-8, f 2048, shared expert) with real IPC pulls of 88 MB experts
+R1 = dict(num_layers=3, max_tokens=4096, weight_layers=3)
 
 
 def main():
@@ -22,11 +25,14 @@ def main():
     local = int(os.environ["LOCAL_RANK"])
     engine = int(os.environ.get("DWDP_ENGINE", "0"))
     wdt = int(os.environ.get("DWDP_WEIGHT", "0"))
+    r1 = os.environ.get("DWDP_SHAPE", "mid") == "r1"
+    shape = R1 if r1 else MID
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    ctx = D.DwdpContext(D.DwdpConfig(**MID, rank=rank, group_size=world, device=local,
-                                     engine=engine, slice_size=1 << 19, weight_dtype=wdt))
+    ctx = D.DwdpContext(D.DwdpConfig(**shape, rank=rank, group_size=world, device=local,
+                                     engine=engine, slice_size=(64 << 20) if r1 else (1 << 19),
+                                     weight_dtype=wdt))
     ctx.init_weights()
     blobs = [None] * world
     dist.all_gather_object(blobs, ctx.export_ipc())
@@ -34,15 +40,15 @@ def main():
     ids = [D.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(ids, src=0)
     ctx.dep_init(ids[0])
-    full = D.DwdpContext(D.DwdpConfig(**MID, device=local, weight_dtype=wdt))
+    full = D.DwdpContext(D.DwdpConfig(**shape, device=local, weight_dtype=wdt))
     full.init_weights()
     torch.cuda.synchronize()
     dist.barrier()
 
     # the last rank of an N>2 group holds no tokens this step (empty DWDP
     # layer; DEP rank that only serves the others' rows)
-    T = 0 if (world > 2 and rank == world - 1) else 100 + 61 * rank
-    x = torch.empty((T, MID["hidden"]), dtype=torch.bfloat16, device=dev)
+    T = 0 if (world > 2 and rank == world - 1) else (4096 - 997 * rank if r1 else 100 + 61 * rank)
+    x = torch.empty((T, full.cfg.hidden), dtype=torch.bfloat16, device=dev)
     if T:
         D.fill_bf16(x, 1000 + rank, 1.0)
     bad = 0
@@ -71,7 +77,8 @@ def main():
     t = torch.tensor([bad], device=dev)
     dist.all_reduce(t)
     if rank == 0:
-        print(f"MPCHECK world={world} engine={engine} weight_dtype={wdt} failures={int(t.item())} "
+        print(f"MPCHECK world={world} shape={'r1' if r1 else 'mid'} engine={engine} weight_dtype={wdt} "
+              f"failures={int(t.item())} "
               f"records={len(recs)} max_wait_ms={max(waits) / 1e6 if waits else 0:.3f}", flush=True)
     ctx.close()
     full.close()
