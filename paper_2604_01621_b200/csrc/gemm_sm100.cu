@@ -327,8 +327,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
       }
     }
   };
-  const int64_t row = int64_t(mb) * BM + q * 32 + lane;
-  const bool store = row < p.m_limit && (p.mb_rows == nullptr || q * 32 + lane < p.mb_rows[mb]);
+  const int64_t arow = int64_t(mb) * BM + q * 32 + lane;  // A row (activation scale)
+  const int64_t drow0 = p.d_row0 != nullptr ? int64_t(p.d_row0[mb]) : int64_t(mb) * BM;
+  const int64_t row = drow0 + q * 32 + lane;                // output row
+  const bool store = arow < p.m_limit && (p.mb_rows == nullptr || q * 32 + lane < p.mb_rows[mb]);
   // fp8: per-row activation scale x per-output-channel weight scale
   float sa = 1.0f;
   const float* sb0 = nullptr;
@@ -338,7 +340,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
     sb0 = ssc;
     sb1 = ssc + 128;
   } else if (FP8) {
-    sa = p.a_scale[row];
+    sa = p.a_scale[arow];
     const int64_t b0 = int64_t(p.slot_of[p.mblock_expert[mb]]) * p.rows_per_slot +
                        int64_t(nb) * (SWIGLU ? 128 : BN);
     sb0 = p.b_scale0 + b0;
@@ -417,7 +419,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
         pk[j] = pack_bf16(h0, h1);
       }
       if (stage != nullptr)
-        tma_store_box(stage, nstore, tmD, pk, lane, store, nb * 128 + c, int(int64_t(mb) * BM + q * 32));
+        tma_store_box(stage, nstore, tmD, pk, lane, store, nb * 128 + c, int(drow0 + q * 32));
       else if (store) {
         uint4* o4 = reinterpret_cast<uint4*>(out + c);
 #pragma unroll
@@ -459,7 +461,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
 #pragma unroll
       for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
       if (stage != nullptr) {
-        tma_store_box(stage, nstore, tmD, pk, lane, store, nb * BN + c, int(int64_t(mb) * BM + q * 32));
+        tma_store_box(stage, nstore, tmD, pk, lane, store, nb * BN + c, int(drow0 + q * 32));
       } else if (store) {
         uint4* o4 = reinterpret_cast<uint4*>(out + c);
 #pragma unroll

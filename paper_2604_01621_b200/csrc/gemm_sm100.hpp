@@ -53,6 +53,10 @@ struct GemmArgs {
   const uint8_t* a_sf;
   const uint8_t* b_sf0;
   const uint8_t* b_sf1;
+  // Optional [m-blocks] first output row of each m-block (default mb * 128):
+  // the split layout writes GEMM1's H into 256-row expert segments and GEMM2's
+  // O back into 128-row segments (launch_split_layout). A rows stay mb * 128.
+  const int32_t* d_row0;
 };
 
 // 2-D bf16 TMA map over a row-major [rows][cols] matrix, box = 64 x box_rows,

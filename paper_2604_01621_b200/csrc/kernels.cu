@@ -1517,6 +1517,75 @@ int64_t permute_scratch_ints(int64_t T, int E) {
   return nch * E + E;
 }
 
+// Two layouts of the same expert-major rows (see launch_split_layout): per
+// expert e with c rows, segment 128-layout [o1, o1 + ceil(c/128)*128) and
+// 256-layout [o2, o2 + ceil(c/256)*256); m-block j of e holds rows
+// [j*128, j*128+128) of e's rows in both. The shared-expert block (T rows)
+// follows the routed segments in each layout.
+__global__ void __launch_bounds__(1024) split_layout_kernel(const int32_t* __restrict__ counts,
+                                                            int E, int64_t T, int shared,
+                                                            int32_t* __restrict__ mblock2,
+                                                            int2* __restrict__ mb_seg2,
+                                                            int32_t* __restrict__ mb_rows2,
+                                                            int32_t* __restrict__ meta2,
+                                                            int32_t* __restrict__ d1,
+                                                            int32_t* __restrict__ d2) {
+  extern __shared__ int32_t sm[];  // [E] 128-layout offsets, [E] 256-layout offsets, [2] totals
+  int32_t* o1 = sm;
+  int32_t* o2 = sm + E;
+  if (threadIdx.x == 0) {
+    int32_t a1 = 0, a2 = 0;
+    for (int e = 0; e < E; ++e) {
+      const int32_t c = counts[e];
+      o1[e] = a1;
+      o2[e] = a2;
+      a1 += (c + 127) / 128 * 128;
+      a2 += (c + 255) / 256 * 256;
+    }
+    sm[2 * E] = a1;
+    sm[2 * E + 1] = a2;
+    const int32_t smb2 = shared ? int32_t((T + 255) / 256 * 2) : 0;
+    meta2[0] = a2 / MB_ROWS + smb2;
+    meta2[1] = a2 / MB_ROWS;
+    meta2[2] = a2;
+    meta2[3] = int32_t(T);
+  }
+  __syncthreads();
+  const int32_t R1 = sm[2 * E], R2 = sm[2 * E + 1];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int32_t c = counts[e];
+    const int32_t n1 = (c + 127) / 128, n2 = (c + 255) / 256 * 2;
+    const int32_t b1 = o1[e] / MB_ROWS, b2 = o2[e] / MB_ROWS;
+    for (int32_t j = 0; j < n1; ++j) d1[b1 + j] = o2[e] + j * MB_ROWS;
+    for (int32_t j = 0; j < n2; ++j) {
+      mblock2[b2 + j] = e;
+      mb_seg2[b2 + j] = make_int2(b2, n2);
+      const int32_t v = c - j * MB_ROWS;
+      mb_rows2[b2 + j] = v < 0 ? 0 : (v > MB_ROWS ? MB_ROWS : v);
+      d2[b2 + j] = j < n1 ? o1[e] + j * MB_ROWS : 0;
+    }
+  }
+  if (shared) {
+    const int32_t n1 = int32_t((T + 127) / 128), n2 = int32_t((T + 255) / 256 * 2);
+    const int32_t b1 = R1 / MB_ROWS, b2 = R2 / MB_ROWS;
+    for (int32_t j = threadIdx.x; j < n2; j += blockDim.x) {
+      if (j < n1) d1[b1 + j] = R2 + j * MB_ROWS;
+      mblock2[b2 + j] = E;
+      mb_seg2[b2 + j] = make_int2(b2, n2);
+      const int64_t v = T - int64_t(j) * MB_ROWS;
+      mb_rows2[b2 + j] = v < 0 ? 0 : (v > MB_ROWS ? MB_ROWS : int32_t(v));
+      d2[b2 + j] = j < n1 ? R1 + j * MB_ROWS : 0;
+    }
+  }
+}
+
+void launch_split_layout(const int32_t* counts, int E, int64_t T, int shared, int32_t* mblock2,
+                         int2* mb_seg2, int32_t* mb_rows2, int32_t* meta2, int32_t* d1, int32_t* d2,
+                         cudaStream_t st) {
+  split_layout_kernel<<<1, 1024, (2 * E + 2) * sizeof(int32_t), st>>>(counts, E, T, shared, mblock2,
+                                                                      mb_seg2, mb_rows2, meta2, d1, d2);
+}
+
 int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int k, int64_t h,
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
                     int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,

@@ -57,6 +57,16 @@ int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int 
                     int32_t* scratch, cudaStream_t st, uint8_t* xperm8 = nullptr,
                     float* xscale = nullptr, int row_align = 128, int32_t* mb_rows = nullptr,
                     uint8_t* xsf = nullptr);
+// Split layout: the permuted rows stay in 128-row expert segments (X_perm, O,
+// GEMM1's m-blocks), while H is laid out in 256-row segments so GEMM2 runs on
+// CTA pairs. From the permute's counts this writes the 256-row layout's
+// m-block tables (mblock2, mb_seg2, mb_rows2, meta2) and the per-m-block
+// output row bases that move rows between the two layouts: d1 [128-layout
+// m-blocks] = H row of GEMM1's output block, d2 [256-layout m-blocks] = O row
+// (128 layout) of GEMM2's output block. One launch, one CTA.
+void launch_split_layout(const int32_t* counts, int E, int64_t T, int shared, int32_t* mblock2,
+                         int2* mb_seg2, int32_t* mb_rows2, int32_t* meta2, int32_t* d1, int32_t* d2,
+                         cudaStream_t st);
 // mb_rows [m-blocks] (nullable): real rows of each m-block (the GEMM epilogues
 // skip the padding rows' stores).
 // row_align (128 or 256): every expert segment, and the shared-expert block,

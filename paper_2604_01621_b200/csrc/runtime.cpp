@@ -83,6 +83,10 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     gemm2_pair_ = env && (env[0] == '1' || env[0] == '3') ? 1 : 0;
     gemm_pair_ = gemm1_pair_ || gemm2_pair_;
     row_align_ = gemm_pair_ ? 256 : 128;
+    // =4: split layout -- GEMM1 keeps the 1-SM kernel and 128-row segments,
+    // its epilogue writes H into 256-row segments and GEMM2 alone runs on CTA
+    // pairs (bf16 experts)
+    split2_ = env && env[0] == '4' && !fp8_ && !fp4_;
     const char* r = std::getenv("DWDP_RASTER");  // experiments: m / n (default auto)
     raster_ = r ? (r[0] == 'm' ? 1 : r[0] == 'n' ? 2 : 0) : 0;
     const char* g = std::getenv("DWDP_GATHER");  // GEMM1 gathers routed rows from x
@@ -171,7 +175,18 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   scratch_ = static_cast<int32_t*>(
       dalloc(size_t(permute_scratch_ints(max_tokens_, E_)) * 4, &workspace_bytes));
   xperm_ = static_cast<uint16_t*>(dalloc(size_t(max_rows_) * h_ * 2, &workspace_bytes));
-  hbuf_ = static_cast<uint16_t*>(dalloc(size_t(max_rows_) * f_ * 2, &workspace_bytes));
+  int64_t h_rows = max_rows_;
+  if (split2_) {
+    max_mb2_ = mb_bound256(max_tokens_);
+    h_rows = std::max(h_rows, max_mb2_ * 128);
+    mblock2_ = static_cast<int32_t*>(dalloc(size_t(max_mb2_) * 4, &workspace_bytes));
+    mbseg2_ = static_cast<int2*>(dalloc(size_t(max_mb2_) * sizeof(int2), &workspace_bytes));
+    mbrows2_ = static_cast<int32_t*>(dalloc(size_t(max_mb2_) * 4, &workspace_bytes));
+    d2_ = static_cast<int32_t*>(dalloc(size_t(max_mb2_) * 4, &workspace_bytes));
+    d1_ = static_cast<int32_t*>(dalloc(size_t(max_mb_) * 4, &workspace_bytes));
+    meta2_ = static_cast<int32_t*>(dalloc(16 * 4, &workspace_bytes));
+  }
+  hbuf_ = static_cast<uint16_t*>(dalloc(size_t(h_rows) * f_ * 2, &workspace_bytes));
   router_wq_ = static_cast<int8_t*>(dalloc(size_t(WL_) * 3 * E_ * h_, &weight_bytes));
   router_we_ = static_cast<int32_t*>(dalloc(size_t(WL_) * E_ * 4, &weight_bytes));
   for (int wl = 0; wl < WL_; ++wl) {
@@ -191,10 +206,10 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   tm_gate_ = tmap(arena_[0], int64_t(nslots_) * f_, h_ / kdiv, 128);
   tm_up_ = tmap(arena_[1], int64_t(nslots_) * f_, h_ / kdiv, 128);
   tm_down_ = tmap(arena_[2], int64_t(nslots_) * h_, f_ / kdiv, 256);
-  if (gemm_pair_ || fp4_pair_)  // half n-block per CTA
+  if (gemm_pair_ || fp4_pair_ || split2_)  // half n-block per CTA
     tm_down_p_ = tmap(arena_[2], int64_t(nslots_) * h_, f_ / kdiv, 128);
   tm_xperm_ = make_tmap_bf16(xperm_, max_rows_, h_, 128);
-  tm_h_ = make_tmap_bf16(hbuf_, max_rows_, f_, 128);
+  tm_h_ = make_tmap_bf16(hbuf_, h_rows, f_, 128);
   if (fp8_) {
     h8_ = static_cast<uint8_t*>(dalloc(size_t(max_rows_) * f_, &workspace_bytes));
     xs_ = static_cast<float*>(dalloc(size_t(max_rows_) * 4, &workspace_bytes));
@@ -261,6 +276,9 @@ Ctx::~Ctx() {
   for (cudaEvent_t e : free_events_) cudaEventDestroy(e);
   if (meta_ring_) cudaFreeHost(meta_ring_);
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
+  for (void* b : {static_cast<void*>(mblock2_), static_cast<void*>(mbseg2_), static_cast<void*>(mbrows2_),
+                  static_cast<void*>(meta2_), static_cast<void*>(d1_), static_cast<void*>(d2_)})
+    if (b) cudaFree(b);
   void* bufs[] = {arena_[0], arena_[1], arena_[2], router_w_, bias_, slot_tab_, logits_, idx_,
                   wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_, pull_items_odd_,
                   router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_, mbseg_, mbrows_, dep_seg_, srcrow_,
@@ -804,14 +822,33 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   // TMA tile::gather4 42.7 GB and with cp.async 91.8 GB of HBM reads per
   // GEMM1 instead of 26 GB -- the gathered rows are not reused from L2
   // across the expert's 16 n-block tiles the way the contiguous copy is.
+  // split layout: GEMM2 on CTA pairs over H in 256-row segments (only when
+  // experts average >= one m-block, as for `pair`)
+  const bool split = split2_ && T * k_ >= int64_t(E_) * 128;
+  if (split) {
+    launch_split_layout(counts_, E_, T, shared_ ? 1 : 0, mblock2_, mbseg2_, mbrows2_, meta2_, d1_, d2_, st);
+    ++launches;
+  }
   GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_,
               gather ? srcrow_ : nullptr, nullptr, nullptr, nullptr, pair ? gemm1_pair_ : 0, raster_, mbrows_,
               x, h_};
+  if (split) g1.d_row0 = d1_;
   launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1, int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(2);
   GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
               nullptr, nullptr, nullptr, nullptr, pair2 ? 1 : 0, raster_, mbrows_};
-  launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tmdown, tmdown, g2, int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
+  int64_t mb2_ub = mb_ub;
+  if (split) {
+    g2.mblock_expert = mblock2_;
+    g2.meta = meta2_;
+    g2.mb_seg = mbseg2_;
+    g2.mb_rows = mbrows2_;
+    g2.d_row0 = d2_;
+    g2.pair = 1;
+    mb2_ub = mb_bound256(T);
+  }
+  launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, split ? tm_down_p_ : tmdown, split ? tm_down_p_ : tmdown, g2,
+                      int(std::min<int64_t>(mb2_ub * (h_ / 256), 1 << 30)), st);
   mark(3);
   launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
   launches += 3 + np + 2 + 1;  // router 3, permute, GEMM1, GEMM2, combine
@@ -844,6 +881,13 @@ void Ctx::layer_forward(int64_t g, const uint16_t* x, int64_t T, uint16_t* y, bo
       require(buf_owner_[par] == g, "layer_forward: receive buffer " + std::to_string(par) +
                                         " no longer holds global layer " + std::to_string(g));
   }
+  // Layers the caller skipped (g jumps past a prefetched layer, e.g. a stack
+  // iteration starting at the next layer 0) are abandoned: nothing reads
+  // their buffer any more, so the next plan may overwrite it. (Their data
+  // stays valid until then: a later moe_forward of that layer still checks
+  // the buffer's owner.)
+  for (int p = 0; p < 2; ++p)
+    if (buf_owner_[p] >= 0 && buf_owner_[p] < g && !buf_read_[p]) buf_read_[p] = true;
   cursor_ = std::max(cursor_, g + 1);
   LayerRec rec{g, T, take_event(), take_event(), take_event(), nullptr, -1};
   DWDP_CUDA(cudaEventRecord(rec.gate0, st));

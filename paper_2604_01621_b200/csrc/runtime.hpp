@@ -190,6 +190,16 @@ class Ctx {
   int gemm1_pair_ = 0;             // GemmArgs::pair for GEMM1: 0 1-SM, 1 CTA pair
   int gemm2_pair_ = 0;             // GEMM2 and the router GEMM on CTA pairs too
   int row_align_ = 128;            // expert segment padding (256 with pairs)
+  // split layout (DWDP_GEMM_PAIR=4): GEMM1 1-SM on 128-row segments, H in
+  // 256-row segments, GEMM2 on CTA pairs (launch_split_layout)
+  bool split2_ = false;
+  int32_t *mblock2_ = nullptr, *mbrows2_ = nullptr, *meta2_ = nullptr, *d1_ = nullptr,
+          *d2_ = nullptr;
+  int2* mbseg2_ = nullptr;
+  int64_t max_mb2_ = 0;
+  int64_t mb_bound256(int64_t T) const {
+    return (T * k_ + int64_t(E_) * 255) / 128 + 2 + (shared_ ? (T + 255) / 256 * 2 : 0);
+  }
   int raster_ = 0;                 // GemmArgs::raster (DWDP_RASTER experiments)
   bool gather_ = false;            // GEMM1 gathers routed rows from x (DWDP_GATHER=1)
   // upper bound on the m-blocks of T tokens (routed segments + shared block)

@@ -330,10 +330,12 @@ def test_prefetch_handles(dev):
 
 
 @pytest.mark.parametrize("name,mode", [("mid_sigmoid", "1"), ("mid_fp8", "1"), ("mid_sigmoid", "3"),
-                                       ("mid_fp8", "3")])
+                                       ("mid_fp8", "3"), ("mid_sigmoid", "4")])
 def test_gemm_pair_matches_single_cta(dev, monkeypatch, name, mode):
     """The CTA-pair GEMM (cta_group::2, 256-row segments; DWDP_GEMM_PAIR=1 for
-    every GEMM, =3 for GEMM2 and the router only) gives the
+    every GEMM, =3 for GEMM2 and the router only, =4 the split layout: GEMM1
+    1-SM on 128-row segments writing H into 256-row segments, GEMM2 on pairs)
+    gives the
     same layer outputs as the all-1-SM kernels (DWDP_GEMM_PAIR=0; bf16 and
     e4m3 weights; routing included)."""
     cfg = CONFIGS.get(name) or FP8_CONFIGS[name]

@@ -81,6 +81,31 @@ def test_layer_forward_rewind_is_refused():
             c.close()
 
 
+def test_stack_iteration_may_skip_a_prefetched_layer():
+    """layer_forward(0..4) prefetches layer 5; stack_forward then starts the
+    next iteration at global layer 6, abandoning 5: its buffer is reusable and
+    every layer stays exact."""
+    full = D.DwdpContext(D.DwdpConfig(**MID))
+    full.init_weights()
+    ranks = _group()
+    try:
+        x = _x(64, MID["hidden"], 21)
+        for g in range(5):
+            ranks[0].layer_forward(g, x, residual=False)
+        y = ranks[0].stack_forward(x)
+        yf = full.stack_forward(x)  # all-local stack: layers 0, 1, 2 with residual
+        torch.cuda.synchronize()
+        assert torch.equal(y, yf)
+        recs = ranks[0].records()
+        assert [r["global_layer"] for r in recs][-3:] == [6, 7, 8]
+        assert torch.isfinite(y.float()).all()
+        with pytest.raises(D.ConfigError):
+            ranks[0].layer_forward(5, x, residual=False)  # abandoned and refilled by layer 7
+    finally:
+        for c in ranks + [full]:
+            c.close()
+
+
 def test_moe_forward_needs_resident_experts_and_records_its_read():
     full = D.DwdpContext(D.DwdpConfig(**MID))
     full.init_weights()
