@@ -295,6 +295,8 @@ class _Ref(_Api):
         L.ref_simulate_store.argtypes = [i32, i32, i32, i64, i32, i32, i64, i64, f64, f64, f64, f64,
                                          i32, i32, i32, i32, f64, f64, f64, i64, i32, u64, i32, u64,
                                          i32, P]
+        L.ref_simulate_store_cal.argtypes = [i32, i32, i32, i64, i32, i32, i64, i64, f64, P, i32, i32,
+                                             i32, i32, f64, f64, f64, i64, i32, u64, i32, u64, i32, P]
         L.ref_report_events.argtypes = [i32, P, P, P, P, P, P, P]
         L.ref_report_breakdown.argtypes = [i32, P, C.c_char_p, i32]
         L.ref_compare.argtypes = [P, P, P, C.c_char_p, i32]
@@ -327,6 +329,42 @@ class _Ref(_Api):
                                          C.byref(n))
         assert st == 0, self.lib.ref_last_error()
         ne = n.value
+        i32a = np.zeros((max(ne, 1), 6), np.int32)
+        i64a = np.zeros((max(ne, 1), 2), np.int64)
+        by = np.zeros(max(ne, 1), np.float64)
+        isa = np.zeros(N * iters, np.int64)
+        iea = np.zeros(N * iters, np.int64)
+        tka = np.zeros(N * iters, np.int64)
+        dims = np.zeros(3, np.int32)
+        st = self.lib.ref_report_events(slot, _ptr(i32a), _ptr(i64a), _ptr(by), _ptr(isa),
+                                        _ptr(iea), _ptr(tka), _ptr(dims))
+        assert st == 0, self.lib.ref_last_error()
+        bd = np.zeros(35, np.float64)
+        csv = C.create_string_buffer(8192)
+        st = self.lib.ref_report_breakdown(slot, _ptr(bd), csv, 8192)
+        assert st == 0, self.lib.ref_last_error()
+        return {"events": (i32a[:ne], i64a[:ne], by[:ne]), "iter_start": isa, "iter_end": iea,
+                "iter_tokens": tka, "dims": dims.tolist(), "breakdown": bd,
+                "csv": csv.value.decode()}
+
+    def simulate_report_cal(self, slot: int, dwdp: bool, layers, h, E, k, f, fs, wb, cal: dict, N,
+                            iters, warmup, kind, length, ratio, sd, mnt, bpr, seed, tdm=True,
+                            slice_size=1 << 20, merge_elim=True):
+        """simulate_dwdp / simulate_dep with calibrated GpuSpec + CostCalibration
+        (cal: peak_flops, mem_bw, link_bw, ce_inflight, grouped_gemm, dense_gemm,
+        others_bytes_factor, mem_interference) into report slot `slot`; returns
+        the same dict as simulate_report."""
+        keys = ("peak_flops", "mem_bw", "link_bw", "ce_inflight", "grouped_gemm", "dense_gemm",
+                "others_bytes_factor", "mem_interference")
+        c = np.array([float(cal[k]) for k in keys], np.float64)
+        n = C.c_int()
+        st = self.lib.ref_simulate_store_cal(slot, int(dwdp), layers, h, E, k, f, fs, wb, _ptr(c), N,
+                                             iters, warmup, kind, length, ratio, sd, mnt, bpr, seed,
+                                             int(tdm), slice_size, int(merge_elim), C.byref(n))
+        assert st == 0, self.lib.ref_last_error()
+        return self._report(slot, n.value, N, iters)
+
+    def _report(self, slot: int, ne: int, N: int, iters: int):
         i32a = np.zeros((max(ne, 1), 6), np.int32)
         i64a = np.zeros((max(ne, 1), 2), np.int64)
         by = np.zeros(max(ne, 1), np.float64)

@@ -192,19 +192,49 @@ int ref_moe_entries(int64_t hidden, int E, int top_k, int64_t ffn,
 namespace {
 RunReport g_reports[4];  // slots for the report-accounting pins
 
+// Calibration inputs of the measured-trace loop (scripts/calibrate.py):
+// GpuSpec peak/mem/link/ce_inflight and CostCalibration + Others factor
+// (include/dwdpsim/modelspec.hpp:15-19, hwmodel.hpp:29-38).
+struct SimCal {
+  double peak_flops, mem_bw, link_bw;
+  int ce_inflight;
+  double grouped_gemm, dense_gemm, others_bytes_factor;
+  int mem_interference;
+};
+
+RunReport run_sim_cal(int dwdp, int layers, int64_t hidden, int E, int top_k, int64_t ffn,
+                      int64_t shared_ffn, double wbytes, const SimCal& c, int N, int iters,
+                      int warmup, int isl_kind, double length, double ratio, double sd,
+                      int64_t mnt, int batch_per_rank, uint64_t seed, int tdm, uint64_t slice,
+                      int merge_elim);
+
 RunReport run_sim(int dwdp, int layers, int64_t hidden, int E, int top_k, int64_t ffn,
                   int64_t shared_ffn, double wbytes, double peak_flops, double mem_bw,
                   double link_bw, int N, int iters, int warmup, int isl_kind, double length,
                   double ratio, double sd, int64_t mnt, int batch_per_rank, uint64_t seed,
                   int tdm, uint64_t slice, int merge_elim) {
+  const SimCal c{peak_flops, mem_bw, link_bw, 2, 1.0, 1.0, 0.0, 0};
+  return run_sim_cal(dwdp, layers, hidden, E, top_k, ffn, shared_ffn, wbytes, c, N, iters, warmup,
+                     isl_kind, length, ratio, sd, mnt, batch_per_rank, seed, tdm, slice, merge_elim);
+}
+
+RunReport run_sim_cal(int dwdp, int layers, int64_t hidden, int E, int top_k, int64_t ffn,
+                      int64_t shared_ffn, double wbytes, const SimCal& c, int N, int iters,
+                      int warmup, int isl_kind, double length, double ratio, double sd,
+                      int64_t mnt, int batch_per_rank, uint64_t seed, int tdm, uint64_t slice,
+                      int merge_elim) {
     MoeModelSpec m =
         make_model(layers, hidden, E, top_k, ffn, shared_ffn, wbytes, 2.0);
+    m.calib.grouped_gemm = c.grouped_gemm;
+    m.calib.dense_gemm = c.dense_gemm;
+    m.others_bytes_factor = c.others_bytes_factor;
     GpuSpec g;
-    g.peak_flops = peak_flops;
-    g.mem_bw = mem_bw;
-    g.link_bw = link_bw;
+    g.peak_flops = c.peak_flops;
+    g.mem_bw = c.mem_bw;
+    g.link_bw = c.link_bw;
+    g.ce_inflight = c.ce_inflight;
     InterferenceParams ip;
-    ip.mem_interference_on = false;
+    ip.mem_interference_on = c.mem_interference != 0;
     ip.power_interference_on = false;
     WorkloadSpec w;
     w.isl_dist.kind = static_cast<IslDist::Kind>(isl_kind);
@@ -283,6 +313,26 @@ int ref_simulate_store(int slot, int dwdp, int layers, int64_t hidden, int E, in
     g_reports[slot] = run_sim(dwdp, layers, hidden, E, top_k, ffn, shared_ffn, wbytes,
                               peak_flops, mem_bw, link_bw, N, iters, warmup, isl_kind, length,
                               ratio, sd, mnt, batch_per_rank, seed, tdm, slice, merge_elim);
+    *n_events = static_cast<int>(g_reports[slot].events.size());
+  });
+}
+
+// Same with the calibration loop's inputs: cal = {peak_flops, mem_bw,
+// link_bw, ce_inflight, calib.grouped_gemm, calib.dense_gemm,
+// others_bytes_factor, mem_interference_on}.
+int ref_simulate_store_cal(int slot, int dwdp, int layers, int64_t hidden, int E, int top_k,
+                           int64_t ffn, int64_t shared_ffn, double wbytes, const double* cal,
+                           int N, int iters, int warmup, int isl_kind, double length,
+                           double ratio, double sd, int64_t mnt, int batch_per_rank,
+                           uint64_t seed, int tdm, uint64_t slice, int merge_elim,
+                           int* n_events) {
+  return guarded([&] {
+    require(slot >= 0 && slot < 4, "slot out of range");
+    const SimCal c{cal[0], cal[1], cal[2], static_cast<int>(cal[3]), cal[4], cal[5], cal[6],
+                   static_cast<int>(cal[7])};
+    g_reports[slot] = run_sim_cal(dwdp, layers, hidden, E, top_k, ffn, shared_ffn, wbytes, c, N,
+                                  iters, warmup, isl_kind, length, ratio, sd, mnt, batch_per_rank,
+                                  seed, tdm, slice, merge_elim);
     *n_events = static_cast<int>(g_reports[slot].events.size());
   });
 }
