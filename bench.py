@@ -466,7 +466,10 @@ def main():
                                                else ", sustained bf16"),
                 "flops_per_launch": g1_flops / max(len(recs), 1),
                 "gemm2_tflops": g2_flops / (g2_ns * 1e-9) / 1e12 if g2_ns else None,
-                "traffic": traffic if args.dtype == "bf16" else None}
+                "traffic": traffic if args.dtype == "bf16" else None,
+                "traffic_source": ("dram__bytes_read.sum + dram__bytes_write.sum of GEMM1 from one committed "
+                                   "ncu --set full capture (profiles/gemm1_dram.json), not measured in this run"
+                                   if args.dtype == "bf16" and traffic else None)}
     split = {key: sum(r[key] for r in recs) / 1e6 / max(len(recs), 1)
              for key in ("router_ns", "permute_ns", "gemm1_ns", "gemm2_ns", "combine_ns",
                          "moe_ns", "gate_wait_ns", "prefetch_ns", "merge_ns")}
@@ -551,6 +554,38 @@ def main():
         drecs = ctx.records()
         all_drecs = gather(drecs)
         dval = total_tokens / (dms / 1e3)
+        dep2 = None
+        if args.dtype == "bf16":
+            # the stronger DEP: token-deduplicated dispatch + partial combine
+            # (dwdp_dep_set_mode(1)), same kernels, same box
+            ctx.dep_set_mode(1)
+            for it in range(args.warmup):
+                step(toks[it][rank], it, dep=True)
+            torch.cuda.synchronize()
+            ctx.records()
+            barrier()
+            torch.cuda.synchronize()
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            q0.record(stream)
+            for it in range(args.warmup, iters):
+                step(toks[it][rank], it, dep=True)
+            q1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            qms = allmax(q0.elapsed_time(q1))
+            qrecs = ctx.records()
+            ctx.dep_set_mode(0)
+            qval = total_tokens / (qms / 1e3)
+            dep2 = {"value": qval, "tokens_per_s_per_gpu": qval / world, "ms_per_step": qms / args.steps,
+                    "comm_ms_per_layer": sum(r["comm_ns"] for r in qrecs) / 1e6 / max(len(qrecs), 1),
+                    "kernel_ms_per_layer": {key.replace("_ns", ""): sum(r[key] for r in qrecs) / 1e6
+                                            / max(len(qrecs), 1)
+                                            for key in ("router_ns", "permute_ns", "gemm1_ns",
+                                                        "gemm2_ns", "combine_ns")},
+                    "dwdp_over_dep": value / qval,
+                    "what": "token-deduplicated dispatch (each token row once per peer rank) + "
+                            "receive-side permute merging sources + per-rank partial combine; "
+                            "token counts exchanged once per step"}
         dep = {"value": dval, "unit": "tokens/s", "tokens_per_s_per_gpu": dval / world,
                "ms_per_step": dms / args.steps,
                "comm_ms_per_layer": sum(r["comm_ns"] for r in drecs) / 1e6 / max(len(drecs), 1),
@@ -558,7 +593,10 @@ def main():
                                        / max(len(drecs), 1)
                                        for key in ("router_ns", "permute_ns", "gemm1_ns",
                                                    "gemm2_ns", "combine_ns")},
-               "dwdp_over_dep": value / dval}
+               "dwdp_over_dep": value / dval,
+               "what": "reference DEP semantics: every (token, expert) row to the expert's rank "
+                       "(simcore.cpp:321-324), per-expert counts exchanged each layer",
+               "dedupe": dep2}
 
     # ---- whole-step roofline (north star / SURVEY.md §8(d)): per layer the
     # slower of the layer's flops at the tensor peak and the remote-expert
