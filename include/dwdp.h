@@ -481,6 +481,15 @@ int dwdp_ctx_launch_count(const dwdp_ctx* ctx, int64_t* n);
 #define DWDP_NCCL_ID_BYTES 128
 int dwdp_nccl_unique_id(void* id /*DWDP_NCCL_ID_BYTES*/);
 int dwdp_dep_init(dwdp_ctx* ctx, const void* nccl_id);
+/* DEP variant: 0 (default) = the reference's semantics, every (token,
+ * expert) pair's row sent to the expert's rank (simcore.cpp:321-324) with
+ * per-expert counts exchanged per layer; 1 = token-deduplicated dispatch
+ * (each token row once per peer rank, with its routing), receive-side
+ * permute merging each expert's rows across sources, per-rank partial
+ * combine so one row per (token, rank) returns, token counts exchanged once
+ * per stack (bf16 experts). Outputs within bf16 rounding of mode 0 (the
+ * per-rank partial sums are rounded to bf16 before the final sum). */
+int dwdp_dep_set_mode(dwdp_ctx* ctx, int mode);
 int dwdp_dep_layer_forward(dwdp_ctx* ctx, int layer, const void* x, int64_t T,
                            void* y, int residual, void* stream);
 int dwdp_dep_stack_forward(dwdp_ctx* ctx, const void* x, int64_t T, void* y,

@@ -168,6 +168,7 @@ SIGNATURES = {
     "dwdp_ctx_launch_count": (i32, [P, C.POINTER(i64)]),
     "dwdp_nccl_unique_id": (i32, [P]),
     "dwdp_dep_init": (i32, [P, P]),
+    "dwdp_dep_set_mode": (i32, [P, i32]),
     "dwdp_dep_layer_forward": (i32, [P, i32, P, i64, P, i32, P]),
     "dwdp_dep_stack_forward": (i32, [P, P, i64, P, P]),
     "dwdp_gemm_bf16": (i32, [P, P, P, i64, i64, i64, P]),

@@ -30,7 +30,7 @@ namespace {
 struct NcclId {
   char internal[DWDP_NCCL_ID_BYTES];
 };
-constexpr int kUint8 = 1, kInt32 = 2, kFloat32 = 7, kBf16 = 9;
+constexpr int kUint8 = 1, kInt32 = 2, kInt64 = 4, kFloat32 = 7, kBf16 = 9;
 
 struct Nccl {
   int (*GetUniqueId)(NcclId*) = nullptr;
@@ -176,6 +176,11 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
   require(nccl_ != nullptr, "dep: call dep_init first");
   require(layer >= 0 && layer < L_, "dep: layer out of range");
   require(T >= 0 && T <= max_tokens_, "dep: T exceeds max_tokens");
+  if (dep_mode == 1) {  // standalone layer: its own token-count exchange
+    const auto Ts = dep2_exchange_tokens(T, st);
+    dep2_layer_forward(layer, x, T, y, residual, st, Ts);
+    return;
+  }
   const Nccl& n = nccl();
   const int wl = layer % WL_;
   const int per = E_ / N_;
@@ -398,7 +403,175 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
 }
 
 void Ctx::dep_stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t st) {
+  if (dep_mode == 1) {
+    const auto Ts = dep2_exchange_tokens(T, st);  // once per stack: every layer has the same T
+    for (int l = 0; l < L_; ++l) dep2_layer_forward(l, l == 0 ? x : y, T, y, true, st, Ts);
+    return;
+  }
   for (int l = 0; l < L_; ++l) dep_layer_forward(l, l == 0 ? x : y, T, y, true, st);
+}
+
+// ===================================================================== //
+// DEP mode 1: token-deduplicated dispatch + partial combine.
+
+void Ctx::dep2_alloc() {
+  if (dep2_x_) return;
+  require(!fp8_ && !fp4_, "dep mode 1: bf16 experts only");
+  const int64_t rows = int64_t(N_) * max_tokens_;
+  dep2_x_ = static_cast<uint16_t*>(dalloc(size_t(rows) * h_ * 2, &workspace_bytes));
+  dep2_idx_ = static_cast<int32_t*>(dalloc(size_t(rows) * k_ * 4, &workspace_bytes));
+  dep2_loc_ = static_cast<int32_t*>(dalloc(size_t(rows) * k_ * 4, &workspace_bytes));
+  dep2_rowof_ = static_cast<int32_t*>(dalloc(size_t(rows) * k_ * 4, &workspace_bytes));
+  dep2_wts_ = static_cast<float*>(dalloc(size_t(rows) * k_ * 4, &workspace_bytes));
+  dep2_scratch_ = static_cast<int32_t*>(
+      dalloc(size_t(permute_scratch_ints(rows, E_)) * 4, &workspace_bytes));
+  dep2_rowf_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * N_ * 4, &workspace_bytes));
+  dep2_wf_ = static_cast<float*>(dalloc(size_t(max_tokens_) * N_ * 4, &workspace_bytes));
+  dep2_tok_ = static_cast<int32_t*>(dalloc(size_t(N_) * 8 * 2, &workspace_bytes));
+  DWDP_CUDA(cudaHostAlloc(&dep2_tok_host_, size_t(N_) * 8, 0));
+  DWDP_CUDA(cudaHostAlloc(&dep2_flag_host_, 16, 0));
+  dep2_flag_host_[0] = 0;
+  // the final parts [N][T] live in dep_recv_ (>= N * max_tokens rows)
+  dep_reserve(std::max<int64_t>(max_rows_, rows));
+}
+
+std::vector<int64_t> Ctx::dep2_exchange_tokens(int64_t T, cudaStream_t st) {
+  require(nccl_ != nullptr, "dep: call dep_init first");
+  dep2_alloc();
+  // a previous layer's receive side overflowed its row capacity: loud
+  invariant(dep2_flag_host_[0] == 0, "dep mode 1: receive-side rows exceeded the workspace");
+  const Nccl& n = nccl();
+  int64_t* dt = reinterpret_cast<int64_t*>(dep2_tok_);
+  DWDP_CUDA(cudaMemcpyAsync(dt + N_, &T, 8, cudaMemcpyHostToDevice, st));
+  nccl_check(n.AllGather(dt + N_, dt, 1, kInt64, nccl_, st), "ncclAllGather");
+  DWDP_CUDA(cudaMemcpyAsync(dep2_tok_host_, dt, size_t(N_) * 8, cudaMemcpyDeviceToHost, st));
+  DWDP_CUDA(cudaStreamSynchronize(st));
+  return std::vector<int64_t>(dep2_tok_host_, dep2_tok_host_ + N_);
+}
+
+void Ctx::dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
+                             cudaStream_t st, const std::vector<int64_t>& Ts) {
+  struct DG {
+    int prev = -1;
+    explicit DG(int d) {
+      cudaGetDevice(&prev);
+      cudaSetDevice(d);
+    }
+    ~DG() { cudaSetDevice(prev); }
+  } dg(cfg.device);
+  require(layer >= 0 && layer < L_, "dep: layer out of range");
+  require(T >= 0 && T <= max_tokens_, "dep: T exceeds max_tokens");
+  require(int64_t(Ts.size()) == N_ && Ts[size_t(rank_)] == T, "dep mode 1: token counts out of date");
+  const Nccl& n = nccl();
+  const int wl = layer % WL_, per = E_ / N_, lo = rank_ * per;
+  std::vector<int64_t> off(size_t(N_) + 1, 0);
+  for (int r = 0; r < N_; ++r) off[size_t(r) + 1] = off[size_t(r)] + Ts[size_t(r)];
+  const int64_t Tall = off[size_t(N_)];
+  LayerRec rec{int64_t(layer), T, take_event(), take_event(), take_event(), nullptr, -1};
+  DWDP_CUDA(cudaEventRecord(rec.gate0, st));
+  DWDP_CUDA(cudaEventRecord(rec.gate1, st));
+  auto mark = [&](cudaEvent_t* slot) {
+    *slot = take_event();
+    DWDP_CUDA(cudaEventRecord(*slot, st));
+  };
+  // 1. router + top-k of the rank's own tokens
+  if (T > 0) route_logits(wl, x, T, st);
+  mark(&rec.k[0]);
+  mark(&rec.comm[0]);  // dispatch start (same point as the router end)
+  // 2. dispatch: every token row once to every peer, with its k expert ids
+  // and weights (the receiver keeps the pairs of its own expert block)
+  const size_t hk = size_t(k_);
+  nccl_check(n.GroupStart(), "ncclGroupStart");
+  for (int p = 0; p < N_; ++p) {
+    if (p == rank_) continue;
+    if (T > 0) {
+      nccl_check(n.Send(x, size_t(T) * size_t(h_), kBf16, p, nccl_, st), "ncclSend");
+      nccl_check(n.Send(idx_, size_t(T) * hk, kInt32, p, nccl_, st), "ncclSend");
+      nccl_check(n.Send(wts_, size_t(T) * hk, kFloat32, p, nccl_, st), "ncclSend");
+    }
+    const int64_t o = off[size_t(p)], tp = Ts[size_t(p)];
+    if (tp > 0) {
+      nccl_check(n.Recv(dep2_x_ + o * h_, size_t(tp) * size_t(h_), kBf16, p, nccl_, st), "ncclRecv");
+      nccl_check(n.Recv(dep2_idx_ + o * k_, size_t(tp) * hk, kInt32, p, nccl_, st), "ncclRecv");
+      nccl_check(n.Recv(dep2_wts_ + o * k_, size_t(tp) * hk, kFloat32, p, nccl_, st), "ncclRecv");
+    }
+  }
+  nccl_check(n.GroupEnd(), "ncclGroupEnd");
+  const int64_t mine = off[size_t(rank_)];
+  if (T > 0) {
+    DWDP_CUDA(cudaMemcpyAsync(dep2_x_ + mine * h_, x, size_t(T) * h_ * 2, cudaMemcpyDeviceToDevice, st));
+    DWDP_CUDA(cudaMemcpyAsync(dep2_idx_ + mine * k_, idx_, size_t(T) * hk * 4, cudaMemcpyDeviceToDevice, st));
+    DWDP_CUDA(cudaMemcpyAsync(dep2_wts_ + mine * k_, wts_, size_t(T) * hk * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  mark(&rec.comm[1]);
+  // 3. receive-side permute over every rank's tokens, local experts only:
+  // each expert's rows of all sources form one segment; shared expert on
+  // the rank's own T tokens (its A rows read from x)
+  launch_localize_idx(dep2_idx_, Tall * k_, lo, lo + per, dep2_loc_, st);
+  int np = 1;
+  if (Tall > 0)
+    np += launch_permute(dep2_loc_, dep2_x_, Tall, E_, k_, h_, shared_ ? 1 : 0, counts_, dep2_rowof_, mblock_,
+                         mbseg_, nullptr, meta_, xperm_, dep2_scratch_, st, nullptr, nullptr, 128, mbrows_,
+                         nullptr, T, max_rows_);
+  mark(&rec.k[1]);
+  // 4. grouped GEMMs (the rank's expert block + its shared expert)
+  const int32_t* stab = slot_tab_ + size_t(layer) * 2 * (E_ + 1);
+  const int64_t mb_ub = max_mb_;
+  const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
+  GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_,
+              nullptr, nullptr, nullptr, nullptr, 0, raster_, mbrows_};
+  if (Tall > 0)
+    launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1,
+                        int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
+  mark(&rec.k[2]);
+  GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
+              nullptr, nullptr, nullptr, nullptr, 0, raster_, mbrows_};
+  if (Tall > 0)
+    launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tm_down_, tm_down_, g2,
+                        int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
+  mark(&rec.k[3]);
+  // 5. partial combine per received token: sum over this rank's experts of
+  // the token's k (row < 0: computed elsewhere); own tokens straight into
+  // their slot of the final parts, the rest into the dispatch buffer
+  uint16_t* parts = dep_recv_;  // [N][T] partial rows of this rank's tokens
+  for (int r = 0; r < N_; ++r) {
+    const int64_t o = off[size_t(r)], tr = Ts[size_t(r)];
+    if (tr == 0) continue;
+    uint16_t* dst = r == rank_ ? parts + int64_t(rank_) * T * h_ : dep2_x_ + o * h_;
+    launch_combine(xperm_, dep2_rowof_ + o * k_, dep2_wts_ + o * k_, nullptr, nullptr, nullptr, dst, tr, k_,
+                   h_, st);
+    ++np;
+  }
+  mark(&rec.comm[2]);
+  // 6. return all-to-all: one partial row per (token, rank)
+  nccl_check(n.GroupStart(), "ncclGroupStart");
+  for (int p = 0; p < N_; ++p) {
+    if (p == rank_) continue;
+    const int64_t tp = Ts[size_t(p)];
+    if (tp > 0)
+      nccl_check(n.Send(dep2_x_ + off[size_t(p)] * h_, size_t(tp) * size_t(h_), kBf16, p, nccl_, st),
+                 "ncclSend");
+    if (T > 0)
+      nccl_check(n.Recv(parts + int64_t(p) * T * h_, size_t(T) * size_t(h_), kBf16, p, nccl_, st), "ncclRecv");
+  }
+  nccl_check(n.GroupEnd(), "ncclGroupEnd");
+  mark(&rec.comm[3]);
+  // 7. final combine: y = sum over ranks (rank order) + shared + residual
+  if (T > 0) {
+    if (dep2_rowf_T_ != T) {
+      launch_rank_rows(dep2_rowf_, dep2_wf_, T, N_, st);
+      dep2_rowf_T_ = T;
+      ++np;
+    }
+    launch_combine(parts, dep2_rowf_, dep2_wf_, shared_ ? xperm_ : nullptr, meta_, residual ? x : nullptr, y, T,
+                   N_, h_, st);
+  }
+  // receive-side overflow flag (meta[4]) -> host, checked at the next stack
+  DWDP_CUDA(cudaMemcpyAsync(dep2_flag_host_, meta_ + 4, 4, cudaMemcpyDeviceToHost, st));
+  launches += (T > 0 ? 3 : 0) + np + (Tall > 0 ? 2 : 0) + 1;
+  DWDP_CUDA(cudaGetLastError());
+  DWDP_CUDA(cudaEventRecord(rec.moe_end, st));
+  push_record(rec);
 }
 
 }  // namespace dwdp

@@ -976,7 +976,10 @@ __global__ void __launch_bounds__(256) permute_count_kernel(const int32_t* __res
   __syncthreads();
   const int64_t p0 = int64_t(blockIdx.x) * pch * k;
   const int64_t p1 = (p0 + int64_t(pch) * k < T * k) ? p0 + int64_t(pch) * k : T * k;
-  for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) atomicAdd(&hist[idx[p]], 1);
+  for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+    const int e = idx[p];
+    if (e >= 0) atomicAdd(&hist[e], 1);  // e < 0: pair not computed here (DEP: remote expert)
+  }
   __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x)
     chunk_counts[int64_t(blockIdx.x) * E + e] = hist[e];
@@ -993,7 +996,8 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
                                                             int2* __restrict__ mb_seg,
                                                             int32_t* __restrict__ src_row,
                                                             int32_t* __restrict__ meta,
-                                                            int32_t* __restrict__ mb_rows) {
+                                                            int32_t* __restrict__ mb_rows,
+                                                            int64_t shared_T, int64_t cap_rows) {
   extern __shared__ int32_t sh[];  // [E] padded sizes, then [E] offsets
   int32_t* pad = sh;
   int32_t* off = sh + E;
@@ -1026,13 +1030,19 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
       acc += pad[e];
     }
     const int32_t routed_mb = acc / MB_ROWS;
-    const int32_t shared_mb = shared ? int32_t((T + align - 1) / align * (align / MB_ROWS)) : 0;
-    meta[0] = routed_mb + shared_mb;
-    meta[1] = routed_mb;
-    meta[2] = acc;
-    meta[3] = int32_t(T);
+    const int32_t shared_mb =
+        shared ? int32_t((shared_T + align - 1) / align * (align / MB_ROWS)) : 0;
+    // capacity guard (callers whose row count is data-dependent, e.g. the DEP
+    // receive side): an overflowing layer computes nothing and raises meta[4]
+    const bool over = cap_rows > 0 && int64_t(acc) + int64_t(shared_mb) * MB_ROWS > cap_rows;
+    meta[0] = over ? 0 : routed_mb + shared_mb;
+    meta[1] = over ? 0 : routed_mb;
+    meta[2] = over ? 0 : acc;
+    meta[3] = int32_t(shared_T);
+    meta[4] = over ? 1 : 0;
   }
   __syncthreads();
+  if (meta[4]) return;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     expert_off[e] = off[e];
     const int2 seg = make_int2(off[e] / MB_ROWS, pad[e] / MB_ROWS);
@@ -1054,7 +1064,7 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int32_t* __restrict_
       mblock_expert[rmb + b] = E;
       mb_seg[rmb + b] = seg;
       if (mb_rows) {
-        const int64_t v = T - int64_t(b) * MB_ROWS;
+        const int64_t v = shared_T - int64_t(b) * MB_ROWS;
         mb_rows[rmb + b] = v < 0 ? 0 : (v > MB_ROWS ? MB_ROWS : int32_t(v));
       }
     }
@@ -1080,18 +1090,24 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
     for (int s = 0; s < npairs; s += 32) {
       const int pl = s + lane;
       const bool act = pl < npairs;
-      const unsigned am = __ballot_sync(0xffffffffu, act);
-      if (act) {
-        const int e = idx[t0 * k + pl];
-        const unsigned peers = __match_any_sync(am, e);
+      const int e = act ? idx[t0 * k + pl] : -1;
+      // pairs with e < 0 are not computed on this rank (DEP receive side),
+      // and none are after a capacity overflow (meta[4])
+      const bool live = act && e >= 0 && !(meta && meta[4]);
+      const unsigned lm = __ballot_sync(0xffffffffu, live);
+      if (live) {
+        const unsigned peers = __match_any_sync(lm, e);
         const int rank = __popc(peers & ((1u << lane) - 1u));
         const int before = cursor[e];
         const int pos = expert_off[e] + chunk_base[int64_t(blockIdx.x) * E + e] + before + rank;
         rows[pl] = pos;
         row_of[t0 * k + pl] = pos;
         if (src_row) src_row[pos] = int32_t(t0 + pl / k);
-        __syncwarp(am);
+        __syncwarp(lm);
         if (lane == 31 - __clz(peers)) cursor[e] = before + __popc(peers);
+      } else if (act) {
+        rows[pl] = -1;
+        row_of[t0 * k + pl] = -1;
       }
       __syncwarp();
     }
@@ -1108,7 +1124,7 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
       const float sc = nvfp4_row_scale(row_absmax_bf16(reinterpret_cast<const uint4*>(x + (t0 + tl) * h),
                                                        h / 8, lane));
       if (lane == 0) rs[tl] = sc;
-      if (lane < k) xscale[rows[tl * k + lane]] = sc;
+      if (lane < k && rows[tl * k + lane] >= 0) xscale[rows[tl * k + lane]] = sc;
       if (shared && lane == 0) xscale[shared_row0 + t0 + tl] = sc;
     }
     __syncthreads();
@@ -1125,7 +1141,7 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
       const uint32_t sfw = nvfp4_group(v, rs[tl], c);
       for (int j = 0; j < k; ++j) {
         const int64_t r = rows[tl * k + j];
-        store_group(xperm8 + r * (h / 2), xsf, r, g, h, c, sfw, true);
+        if (r >= 0) store_group(xperm8 + r * (h / 2), xsf, r, g, h, c, sfw, true);
       }
       if (shared) {
         const int64_t r = shared_row0 + t0 + tl;
@@ -1152,17 +1168,17 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
           const int64_t c = c0 + 32 * u;
           const uint2 q = quant8(v[u], s);
           for (int j = 0; j < k; ++j)
-            reinterpret_cast<uint2*>(xperm8 + int64_t(rows[tl * k + j]) * h)[c] = q;
+            if (rows[tl * k + j] >= 0) reinterpret_cast<uint2*>(xperm8 + int64_t(rows[tl * k + j]) * h)[c] = q;
           if (shared) reinterpret_cast<uint2*>(xperm8 + int64_t(shared_row0 + t0 + tl) * h)[c] = q;
         }
       }
       for (int64_t c = c0; c < nch; c += 32) {
         const uint2 q = quant8(__ldg(src + c), s);
         for (int j = 0; j < k; ++j)
-          reinterpret_cast<uint2*>(xperm8 + int64_t(rows[tl * k + j]) * h)[c] = q;
+          if (rows[tl * k + j] >= 0) reinterpret_cast<uint2*>(xperm8 + int64_t(rows[tl * k + j]) * h)[c] = q;
         if (shared) reinterpret_cast<uint2*>(xperm8 + int64_t(shared_row0 + t0 + tl) * h)[c] = q;
       }
-      if (lane < k) xscale[rows[tl * k + lane]] = s;
+      if (lane < k && rows[tl * k + lane] >= 0) xscale[rows[tl * k + lane]] = s;
       if (shared && lane == 0) xscale[shared_row0 + t0 + tl] = s;
     }
     return;
@@ -1180,6 +1196,7 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
 #pragma unroll
       for (int u = 0; u < 4; ++u) v[u] = __ldg(src + s + 32 * u);
       for (int j = 0; j < k; ++j) {
+        if (dst[j] < 0) continue;
         uint4* d = reinterpret_cast<uint4*>(xperm + int64_t(dst[j]) * h) + s;
 #pragma unroll
         for (int u = 0; u < 4; ++u) d[32 * u] = v[u];
@@ -1187,7 +1204,8 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
     }
     for (; s < segs; s += 32) {
       const uint4 v = __ldg(src + s);
-      for (int j = 0; j < k; ++j) reinterpret_cast<uint4*>(xperm + int64_t(dst[j]) * h)[s] = v;
+      for (int j = 0; j < k; ++j)
+        if (dst[j] >= 0) reinterpret_cast<uint4*>(xperm + int64_t(dst[j]) * h)[s] = v;
     }
   }
 }
@@ -1245,10 +1263,11 @@ __global__ void __launch_bounds__(32) permute_copy_bulk_kernel(const uint16_t* _
     } while (!ok);
     const int32_t* dst = row_of + (t0 + i) * k;
     for (int j = 0; j < k; ++j)
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-                       xperm + int64_t(dst[j]) * h),
-                   "r"(pb_smem(pbuf + size_t(b) * bytes)), "r"(bytes)
-                   : "memory");
+      if (dst[j] >= 0)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                         xperm + int64_t(dst[j]) * h),
+                     "r"(pb_smem(pbuf + size_t(b) * bytes)), "r"(bytes)
+                     : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     if (i + PB_BUFS < n) {  // buffer b is refilled once its stores have read it
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -1297,7 +1316,10 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
       uint4 v[CB];
 #pragma unroll
       for (int jj = 0; jj < CB; ++jj)
-        if (j0 + jj < k) v[jj] = __ldg(reinterpret_cast<const uint4*>(O + int64_t(srow[j0 + jj]) * h) + s);
+        if (j0 + jj < k)  // row < 0: the pair is computed on another rank (DEP partial combine)
+          v[jj] = srow[j0 + jj] >= 0
+                      ? __ldg(reinterpret_cast<const uint4*>(O + int64_t(srow[j0 + jj]) * h) + s)
+                      : make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (int jj = 0; jj < CB; ++jj) {
         if (j0 + jj >= k) break;
@@ -1586,11 +1608,45 @@ void launch_split_layout(const int32_t* counts, int E, int64_t T, int shared, in
                                                                       mb_seg2, mb_rows2, meta2, d1, d2);
 }
 
+// DEP receive side: pairs whose expert lies outside this rank's block
+// [lo, hi) are marked -1 (not computed here); local ones keep their global id.
+__global__ void localize_idx_kernel(const int32_t* __restrict__ in, int64_t n, int lo, int hi,
+                                    int32_t* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int e = in[i];
+    out[i] = (e >= lo && e < hi) ? e : -1;
+  }
+}
+
+void launch_localize_idx(const int32_t* in, int64_t n, int lo, int hi, int32_t* out, cudaStream_t st) {
+  if (n > 0)
+    localize_idx_kernel<<<unsigned(std::min<int64_t>((n + 255) / 256, 148 * 8)), 256, 0, st>>>(in, n, lo,
+                                                                                               hi, out);
+}
+
+// row_of[t][r] = r * T + t, w = 1: the DEP final combine sums the N ranks'
+// partial rows of token t with combine_kernel (fma(1, v, acc) = v + acc).
+__global__ void rank_rows_kernel(int32_t* __restrict__ row_of, float* __restrict__ w, int64_t T,
+                                 int N) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < T * N; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / N, r = i - t * N;
+    row_of[i] = int32_t(r * T + t);
+    w[i] = 1.0f;
+  }
+}
+
+void launch_rank_rows(int32_t* row_of, float* w, int64_t T, int N, cudaStream_t st) {
+  if (T > 0)
+    rank_rows_kernel<<<unsigned(std::min<int64_t>((T * N + 255) / 256, 148 * 8)), 256, 0, st>>>(row_of, w, T,
+                                                                                              N);
+}
+
 int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int k, int64_t h,
                     int shared, int32_t* counts, int32_t* row_of, int32_t* mblock_expert,
                     int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
                     int32_t* scratch, cudaStream_t st, uint8_t* xperm8, float* xscale,
-                    int row_align, int32_t* mb_rows, uint8_t* xsf) {
+                    int row_align, int32_t* mb_rows, uint8_t* xsf, int64_t shared_T,
+                    int64_t cap_rows) {
   const int pch = permute_chunk(T);
   const int nch = int((T + pch - 1) / pch);
   int32_t* chunk_counts = scratch;
@@ -1599,7 +1655,7 @@ int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int 
     permute_count_kernel<<<nch, 256, E * sizeof(int32_t), st>>>(idx, T, E, k, pch, chunk_counts);
   permute_scan_kernel<<<1, 1024, 2 * E * sizeof(int32_t), st>>>(
       chunk_counts, nch, E, T, shared, row_align, counts, expert_off, mblock_expert, mb_seg, src_row,
-      meta, mb_rows);
+      meta, mb_rows, shared_T < 0 ? T : shared_T, cap_rows);
   // bf16 rows: rank in the scatter kernel, replicate with the bulk-copy kernel
   const bool bulk = xperm != nullptr && xperm8 == nullptr && h % 8 == 0 &&
                     size_t(PB_BUFS) * size_t(h) * 2 <= 48 * 1024;

@@ -56,7 +56,16 @@ int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int 
                     int2* mb_seg, int32_t* src_row, int32_t* meta, uint16_t* xperm,
                     int32_t* scratch, cudaStream_t st, uint8_t* xperm8 = nullptr,
                     float* xscale = nullptr, int row_align = 128, int32_t* mb_rows = nullptr,
-                    uint8_t* xsf = nullptr);
+                    uint8_t* xsf = nullptr, int64_t shared_T = -1, int64_t cap_rows = 0);
+// idx entries < 0 are pairs not computed on this rank (row_of = -1, no copy;
+// combine_kernel skips them). shared_T (default T): rows of the shared-expert
+// block (the DEP receive side permutes all ranks' tokens but runs the shared
+// expert on its own). cap_rows > 0: if the padded rows would exceed it, the
+// layer computes nothing and meta[4] = 1 (the caller raises).
+// DEP receive side: idx -> idx with every expert outside [lo, hi) set to -1.
+void launch_localize_idx(const int32_t* in, int64_t n, int lo, int hi, int32_t* out, cudaStream_t st);
+// row_of[t][r] = r*T + t and weights 1 for the DEP final combine over N ranks.
+void launch_rank_rows(int32_t* row_of, float* w, int64_t T, int N, cudaStream_t st);
 // Split layout: the permuted rows stay in 128-row expert segments (X_perm, O,
 // GEMM1's m-blocks), while H is laid out in 256-row segments so GEMM2 runs on
 // CTA pairs. From the permute's counts this writes the 256-row layout's

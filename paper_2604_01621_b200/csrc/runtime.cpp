@@ -68,7 +68,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   // kernel too (cta_group::2, 256-row segments; DWDP_GEMM_PAIR=1) each GEMM
   // is 2-10% faster per SM clock, but on the power-capped B200 it drew the
   // clock down from ~1.3 to ~0.94 GHz and the full step measured 9% slower
-  // on the same box (scripts/gpu/r1_ab_pair.sh: 144K vs 158K tokens/s).
+  // on the same box (scripts/gpu/r1/r1_ab_pair.sh: 144K vs 158K tokens/s).
   {
     const char* env = std::getenv("DWDP_GEMM_PAIR");
     // DWDP_GEMM_PAIR=1: every GEMM on CTA pairs; =2: GEMM1 only; =3: GEMM2
@@ -77,7 +77,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     // 13.3 ms per layer (half the B bytes per CTA; the 1-SM GEMM2 is L2-feed
     // bound at 73% tensor-pipe active) but the step moved +1.3/+3.9% on one
     // box and -3.3/-2.2% on another, where the SM clock fell from 1.24 to
-    // 1.0 GHz under sw_power_cap (scripts/gpu/r1_ab_pair3.sh,
+    // 1.0 GHz under sw_power_cap (scripts/gpu/r1/r1_ab_pair3.sh,
     // r1_pair3_confirm.sh), so it stays opt-in.
     gemm1_pair_ = env && (env[0] == '1' || env[0] == '2') ? 1 : 0;
     gemm2_pair_ = env && (env[0] == '1' || env[0] == '3') ? 1 : 0;
@@ -267,6 +267,12 @@ Ctx::~Ctx() {
                   static_cast<void*>(dep_xsf_), static_cast<void*>(dep_hsf_)})
     if (b) cudaFree(b);
   if (dep_counts_host_) cudaFreeHost(dep_counts_host_);
+  for (void* b : {static_cast<void*>(dep2_x_), static_cast<void*>(dep2_idx_), static_cast<void*>(dep2_loc_),
+                  static_cast<void*>(dep2_rowof_), static_cast<void*>(dep2_wts_), static_cast<void*>(dep2_scratch_),
+                  static_cast<void*>(dep2_rowf_), static_cast<void*>(dep2_wf_), static_cast<void*>(dep2_tok_)})
+    if (b) cudaFree(b);
+  if (dep2_tok_host_) cudaFreeHost(dep2_tok_host_);
+  if (dep2_flag_host_) cudaFreeHost(dep2_flag_host_);
   if (dep_mbrows_host_) cudaFreeHost(dep_mbrows_host_);
   if (dep_tab_host_) cudaFreeHost(dep_tab_host_);
   for (auto& p : plans_) {
@@ -1014,7 +1020,15 @@ size_t Ctx::drain_records(dwdp_layer_record* out, size_t cap) {
     };
     double kns[5] = {0, 0, 0, 0, 0}, comm = 0;
     const cudaEvent_t begin = r.merge_end ? r.merge_end : r.gate1;
-    if (r.k[0] && r.k[3] && r.comm[1] && r.comm[3]) {  // DEP layer
+    if (r.k[0] && r.k[3] && r.comm[0] && r.comm[1] && r.comm[2] && r.comm[3]) {  // DEP mode 1 layer
+      // router | dispatch | permute | GEMM1 | GEMM2 | partial combine | return | final combine
+      kns[0] = el(begin, r.k[0]);
+      kns[1] = el(r.comm[1], r.k[1]);
+      kns[2] = el(r.k[1], r.k[2]);
+      kns[3] = el(r.k[2], r.k[3]);
+      kns[4] = el(r.k[3], r.comm[2]) + el(r.comm[3], r.moe_end);
+      comm = el(r.k[0], r.comm[1]) + el(r.comm[2], r.comm[3]);
+    } else if (r.k[0] && r.k[3] && r.comm[1] && r.comm[3]) {  // DEP layer
       kns[0] = el(begin, r.k[0]);
       kns[1] = el(r.k[0], r.k[1]);
       kns[2] = el(r.comm[1], r.k[2]);
@@ -1026,7 +1040,8 @@ size_t Ctx::drain_records(dwdp_layer_record* out, size_t cap) {
       for (int i = 0; i < 5; ++i) kns[i] = el(seq[i], seq[i + 1]);
     }
     const int64_t rows = r.rows >= 0 ? r.rows : r.meta_slot >= 0 ? meta_ring_[r.meta_slot * 4 + 2] : -1;
-    const double dispatch = (r.k[1] && r.comm[1]) ? el(r.k[1], r.comm[1]) : 0.0;
+    const double dispatch = (r.comm[0] && r.comm[1]) ? el(r.k[0], r.comm[1])
+                            : (r.k[1] && r.comm[1]) ? el(r.k[1], r.comm[1]) : 0.0;
     double pf0 = -1, pf1 = -1;
     if (plan) {
       pf0 = el(epoch_, plan->start);

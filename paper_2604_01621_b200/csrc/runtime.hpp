@@ -104,6 +104,17 @@ class Ctx {
   void dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
                          cudaStream_t st);
   void dep_stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t st);
+  // DEP variant (dwdp_dep_set_mode(1)): token-deduplicated dispatch (each
+  // token row goes once to every peer rank, with its routing), receive-side
+  // permute that merges each local expert's rows across sources (no
+  // per-(source, expert) padding), per-rank partial combine, one row per
+  // (token, rank) back, final sum at the source; message sizes are the ranks'
+  // token counts, exchanged once per stack instead of per-expert counts per
+  // layer (bf16 experts).
+  int dep_mode = 0;
+  void dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
+                          cudaStream_t st, const std::vector<int64_t>& Ts);
+  std::vector<int64_t> dep2_exchange_tokens(int64_t T, cudaStream_t st);
 
   dwdp_ctx_config cfg;
   uint64_t weight_bytes = 0, recv_bytes = 0, workspace_bytes = 0;
@@ -271,6 +282,15 @@ class Ctx {
   uint8_t *dep_sfl_ = nullptr, *dep_xsf_ = nullptr, *dep_hsf_ = nullptr;
   CUtensorMap tm_dep_x8_, tm_dep_h8_;
   void dep_reserve(int64_t rows);
+  // DEP mode 1 buffers: all ranks' token rows (then the partial rows sent
+  // back), their routing, local row_of, permute scratch, final-combine tables
+  uint16_t* dep2_x_ = nullptr;
+  int32_t *dep2_idx_ = nullptr, *dep2_loc_ = nullptr, *dep2_rowof_ = nullptr, *dep2_scratch_ = nullptr,
+          *dep2_rowf_ = nullptr, *dep2_tok_ = nullptr, *dep2_flag_host_ = nullptr;
+  float *dep2_wts_ = nullptr, *dep2_wf_ = nullptr;
+  int64_t* dep2_tok_host_ = nullptr;
+  int64_t dep2_rowf_T_ = -1;
+  void dep2_alloc();
   int num_sms_ = 148;
 };
 

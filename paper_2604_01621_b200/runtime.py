@@ -206,6 +206,11 @@ class DwdpContext:
         assert len(nccl_id) == 128
         check(lib().dwdp_dep_init(self.h, C.create_string_buffer(nccl_id, 128)))
 
+    def dep_set_mode(self, mode: int) -> None:
+        """0: per-pair dispatch (reference semantics); 1: token-deduplicated
+        dispatch + partial combine (dwdp_dep_set_mode)."""
+        check(lib().dwdp_dep_set_mode(self.h, mode))
+
     def dep_layer_forward(self, layer: int, x, y=None, residual: bool = True, stream=None):
         y = self._out(x, y)
         check(lib().dwdp_dep_layer_forward(self.h, layer, _ptr(x), x.shape[0], _ptr(y),

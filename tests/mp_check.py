@@ -72,6 +72,27 @@ def main():
     if not torch.equal(y1, y2):
         print(f"rank {rank}: stack DWDP != stack DEP", flush=True)
         bad += 1
+    # DEP mode 1 (token-deduplicated dispatch, partial combine): within bf16
+    # rounding of the all-local layer (per-rank partial sums are rounded)
+    if wdt == 0:
+        ctx.dep_set_mode(1)
+        for l in range(3):
+            y_d2 = ctx.dep_layer_forward(l, x, residual=False)
+            y_ref = full.moe_forward(l, x)
+            torch.cuda.synchronize()
+            if T:
+                err = ((y_d2.float() - y_ref.float()).norm() / y_ref.float().norm()).item()
+                if not err < 1e-2:
+                    print(f"rank {rank} layer {l}: DEP mode 1 rel err {err}", flush=True)
+                    bad += 1
+        y3 = ctx.dep_stack_forward(x)
+        torch.cuda.synchronize()
+        if T:
+            err = ((y3.float() - y1.float()).norm() / y1.float().norm()).item()
+            if not err < 1e-2:
+                print(f"rank {rank}: DEP mode 1 stack rel err {err}", flush=True)
+                bad += 1
+        ctx.dep_set_mode(0)
     recs = ctx.records()
     waits = [r["gate_wait_ns"] for r in recs if r["prefetch_bytes"] > 0]
     t = torch.tensor([bad], device=dev)
