@@ -378,6 +378,7 @@ def main():
             # over ranks). The SM engines move bytes faster but take SM time
             # from the GEMMs, so in-step GB/s alone is not the criterion.
             best = None
+            probe = {}
             for name, eid in (("copy", D.ENGINE_COPY), ("pull", D.ENGINE_PULL), ("hybrid", D.ENGINE_HYBRID)):
                 ctx.set_engine(eid)
                 t_eng = float("inf")
@@ -390,6 +391,7 @@ def main():
                     torch.cuda.synchronize()
                     t_eng = min(t_eng, allmax(p0.elapsed_time(p1)) / max(1, max(toks[it])))
                 ctx.records()
+                probe[name] = t_eng * 1e3  # us per token of the step's largest rank
                 if best is None or t_eng < best[0]:
                     best = (t_eng, name, eid)
             ctx.set_engine(best[2])
@@ -397,6 +399,7 @@ def main():
     engines = [None] * world
     if world > 1:
         dist.all_gather_object(engines, engine)
+    engine_probe = locals().get("probe")
     n0 = ctx.launch_count()
 
     barrier()
@@ -690,6 +693,7 @@ def main():
                        "weights": ("one 22.5 GB set aliased by all layers (N=1)" if world == 1
                                    else f"{min(256, -(-256 // world) + args.extra_redundancy)} owned experts/layer/GPU, {layers} layers"),
                        "prefetch_engine": (engines if world > 1 else None),
+                       "engine_probe_us_per_token": engine_probe,
                        "slice_size": args.slice_size if world > 1 else None,
                        "l2": "inputs larger than L2: {} GB of expert weights per layer".format(
                            "11.3 (e4m3)" if fp8 else "6.3 (nvfp4)" if fp4 else "22.5 (bf16)"),

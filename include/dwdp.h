@@ -495,6 +495,31 @@ int dwdp_dep_layer_forward(dwdp_ctx* ctx, int layer, const void* x, int64_t T,
 int dwdp_dep_stack_forward(dwdp_ctx* ctx, const void* x, int64_t T, void* y,
                            void* stream);
 
+/* ---- MLA attention block of the prefetch window -----------------------
+ * The paper's window is MoE(l) + Attention(l+1); the
+ * reference costs the attention block as attention_entries
+ * (src/modelspec.cpp:38-55). DeepSeek-V3 MLA prefill on sm_100a kernels:
+ * the five projections on the tcgen05 GEMM, RMSNorm / RoPE / K-V assembly,
+ * and a tcgen05 causal flash-attention core (qk 128 nope + 64 rope, v 128).
+ * Weights are caller-owned device bf16 [out][in]; wkv_a has its
+ * kv_lora + rope rows zero-padded to a multiple of 256. x, y: [T][hidden];
+ * seq_lens: host array of n_seqs back-to-back sequence lengths summing to T
+ * (RoPE positions and the causal mask restart per sequence). */
+typedef struct {
+  int32_t hidden, heads, q_lora, kv_lora, nope, rope, v_dim, device;
+  int64_t max_tokens;
+  float rope_theta, softmax_scale;
+} dwdp_mla_config;
+typedef struct {
+  const void *wq_a, *wq_b, *wkv_a, *wkv_b, *wo;
+} dwdp_mla_weights;
+typedef struct dwdp_mla dwdp_mla;
+int dwdp_mla_create(const dwdp_mla_config* cfg, dwdp_mla** out);
+int dwdp_mla_destroy(dwdp_mla* m);
+int dwdp_mla_forward(dwdp_mla* m, const dwdp_mla_weights* w, const void* x, int64_t T,
+                     const int64_t* seq_lens, int n_seqs, void* y, void* stream);
+int dwdp_mla_launch_count(const dwdp_mla* m, int64_t* n);
+
 /* ---- kernel-level entry points (tests / microbenchmarks) --------------- */
 /* D[M][N] = A[M][K] . B[N][K]^T, bf16 in, fp32 accumulate, bf16 out, on the
  * tcgen05 grouped-GEMM kernel with one group. */

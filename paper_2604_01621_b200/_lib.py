@@ -87,6 +87,16 @@ class LayerRecordC(C.Structure):
                 ("prefetch_start_ns", f64), ("prefetch_end_ns", f64)]
 
 
+class MlaConfigC(C.Structure):
+    _fields_ = [("hidden", i32), ("heads", i32), ("q_lora", i32), ("kv_lora", i32), ("nope", i32),
+                ("rope", i32), ("v_dim", i32), ("device", i32), ("max_tokens", i64),
+                ("rope_theta", f32), ("softmax_scale", f32)]
+
+
+class MlaWeightsC(C.Structure):
+    _fields_ = [("wq_a", P), ("wq_b", P), ("wkv_a", P), ("wkv_b", P), ("wo", P)]
+
+
 NC = 8  # DWDP_NUM_CATEGORIES
 
 
@@ -171,6 +181,10 @@ SIGNATURES = {
     "dwdp_dep_set_mode": (i32, [P, i32]),
     "dwdp_dep_layer_forward": (i32, [P, i32, P, i64, P, i32, P]),
     "dwdp_dep_stack_forward": (i32, [P, P, i64, P, P]),
+    "dwdp_mla_create": (i32, [C.POINTER(MlaConfigC), C.POINTER(P)]),
+    "dwdp_mla_destroy": (i32, [P]),
+    "dwdp_mla_forward": (i32, [P, C.POINTER(MlaWeightsC), P, i64, P, i32, P, P]),
+    "dwdp_mla_launch_count": (i32, [P, C.POINTER(i64)]),
     "dwdp_gemm_bf16": (i32, [P, P, P, i64, i64, i64, P]),
     "dwdp_quant_nvfp4": (i32, [P, i64, i64, P, P, P, P]),
     "dwdp_gemm_nvfp4": (i32, [P, P, P, P, P, P, P, i64, i64, i64, P]),

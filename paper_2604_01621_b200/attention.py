@@ -3,13 +3,16 @@ window.
 
 The paper hides the pull of layer l+1's experts behind MoE(l) + Attention(l+1)
 (PAPER.md:168-171); the reference models attention only as cost entries
-(`attention_entries`, src/modelspec.cpp:38-55). This is the caller's attention
-for the bench: it runs on the compute stream between the MoE layers, so the
-one-sided prefetch the runtime issued at MoE(l)'s gate overlaps it exactly as
-in the paper's schedule. It is built from library operations (cuBLAS GEMMs
-through torch.matmul, FlashAttention-2 -- or torch's flash SDPA backend --
-elementwise RMSNorm and RoPE) -- not a hand-written kernel and not part of
-the C-ABI product path.
+(`attention_entries`, src/modelspec.cpp:38-55). It runs on the compute stream
+between the MoE layers, so the one-sided prefetch the runtime issued at
+MoE(l)'s gate overlaps it exactly as in the paper's schedule.
+
+backend="native" (default): the block through libdwdp.so's C-ABI
+(dwdp_mla_forward) on sm_100a kernels only -- the five projections on the
+tcgen05 grouped-GEMM kernel, RMSNorm / RoPE / K-V assembly kernels and the
+tcgen05 causal flash-attention core (csrc/attn_sm100.cu); qk 128 + 64, v 128.
+backend="library": the same block from library ops (cuBLAS through
+torch.matmul, FlashAttention-2), kept as the comparison arm.
 
 Shapes (DeepSeek-V3 config): hidden 7168, 128 heads, q_lora_rank 1536,
 kv_lora_rank 512, qk_nope 128, qk_rope 64, v_head 128. Weights are random
@@ -30,9 +33,12 @@ except Exception:  # noqa: BLE001
 class MlaAttention:
     def __init__(self, device, seed: int = 0, hidden: int = 7168, heads: int = 128,
                  q_lora: int = 1536, kv_lora: int = 512, nope: int = 128, rope: int = 64,
-                 v_dim: int = 128, theta: float = 10000.0):
+                 v_dim: int = 128, theta: float = 10000.0, backend: str = "native"):
         import torch
 
+        assert backend in ("native", "library"), backend
+        self.backend, self.device, self.theta = backend, device, theta
+        self._handle, self._cap = None, 0
         self.h, self.H, self.nope, self.rope, self.v = hidden, heads, nope, rope, v_dim
         self.kv_lora = kv_lora
         g = torch.Generator(device=device).manual_seed(seed)
@@ -46,6 +52,48 @@ class MlaAttention:
         self.wkv_b = w(heads * (nope + v_dim), kv_lora)
         self.wo = w(hidden, heads * v_dim)
         self.inv_freq = 1.0 / (theta ** (torch.arange(0, rope, 2, device=device, dtype=torch.float32) / rope))
+        # native backend: kv_a rows zero-padded to a multiple of 256 (GEMM n-blocks)
+        rows = (kv_lora + rope + 255) // 256 * 256
+        self.wkv_a_pad = torch.zeros((rows, hidden), dtype=torch.bfloat16, device=device)
+        self.wkv_a_pad[:kv_lora + rope] = self.wkv_a
+
+    def close(self) -> None:
+        if self._handle is not None:
+            from ._lib import check, lib
+            check(lib().dwdp_mla_destroy(self._handle))
+            self._handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def _native(self, x, seqs):
+        import ctypes as C
+
+        import numpy as np
+        import torch
+
+        from ._lib import MlaConfigC, MlaWeightsC, check, lib
+        T = x.shape[0]
+        if self._handle is None or T > self._cap:
+            self.close()
+            cap = max(T, 128)
+            cfg = MlaConfigC(self.h, self.H, self.wq_a.shape[0], self.kv_lora, self.nope, self.rope, self.v,
+                             x.device.index or 0, cap, self.theta,
+                             1.0 / math.sqrt(self.nope + self.rope))
+            h = C.c_void_p()
+            check(lib().dwdp_mla_create(C.byref(cfg), C.byref(h)))
+            self._handle, self._cap = h, cap
+        w = MlaWeightsC(self.wq_a.data_ptr(), self.wq_b.data_ptr(), self.wkv_a_pad.data_ptr(),
+                        self.wkv_b.data_ptr(), self.wo.data_ptr())
+        y = torch.empty((T, self.h), dtype=torch.bfloat16, device=x.device)
+        sl = np.ascontiguousarray(seqs, dtype=np.int64)
+        x = x.contiguous()
+        check(lib().dwdp_mla_forward(self._handle, C.byref(w), x.data_ptr(), T, sl.ctypes.data, len(sl),
+                                     y.data_ptr(), torch.cuda.current_stream().cuda_stream))
+        return y
 
     def flops(self, seqs: list[int]) -> float:
         """Algorithmic FLOP of forward() over sequences of these lengths."""
@@ -77,6 +125,8 @@ class MlaAttention:
         import torch
         import torch.nn.functional as F
 
+        if self.backend == "native":
+            return self._native(x, seqs)
         T, H = x.shape[0], self.H
         q = (self._rms(x @ self.wq_a.T) @ self.wq_b.T).view(T, H, self.nope + self.rope)
         kva = x @ self.wkv_a.T

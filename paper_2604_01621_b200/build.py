@@ -19,9 +19,9 @@ LIB = os.path.join(PKG, "libdwdp.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
-CU = ["kernels.cu", "gemm_sm100.cu"]
-CPP = ["plan.cpp", "report.cpp", "runtime.cpp", "dep.cpp", "capi.cpp"]
-HEADERS = ["kernels.hpp", "gemm_sm100.hpp", "plan.hpp", "runtime.hpp", "report.hpp"]
+CU = ["kernels.cu", "gemm_sm100.cu", "attn_sm100.cu"]
+CPP = ["plan.cpp", "report.cpp", "runtime.cpp", "dep.cpp", "capi.cpp", "mla.cpp"]
+HEADERS = ["kernels.hpp", "gemm_sm100.hpp", "plan.hpp", "runtime.hpp", "report.hpp", "attn_sm100.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -1,0 +1,441 @@
+// MLA prefill attention block on Blackwell (sm_100a): the attention step of
+// the DWDP prefetch window, MoE(l) + Attention(l+1), whose
+// cost the reference models as attention_entries (src/modelspec.cpp:38-55,
+// phase AttnOps at src/simcore.cpp:666-674).
+//
+// DeepSeek-V3 MLA (no weight absorption, the prefill form):
+//   q   = rms(x Wq_a^T) Wq_b^T                 [T][H][128 nope | 64 rope]
+//   kva = x Wkv_a^T                            [T][512 ckv | 64 k_rope]
+//   kv  = rms(ckv) Wkv_b^T                     [T][H][128 k_nope | 128 v]
+//   q_rope, k_rope <- RoPE(position in sequence)
+//   o   = softmax(q k^T / sqrt(192), causal per sequence) v   [T][H][128]
+//   y   = o Wo^T
+// The five projections run on the tcgen05 grouped-GEMM kernel (one dense
+// group); RMSNorm, RoPE and the K / V^T assembly are small glue kernels; the
+// attention core is mla_attn_kernel below.
+//
+// mla_attn_kernel: one CTA per (128-query tile of a sequence, head),
+// 256 threads, warp-specialised:
+//   warp 0      TMA producer: Q tile once (3 boxes of 128 x 64), then per
+//               64-key tile K (3 boxes) and V^T (one [128 dv][64 keys] box)
+//               into a 3-stage ring
+//   warp 1      MMA issuer: S_j = Q K_j^T (tcgen05 kind::f16, M128 N64 K192
+//               into TMEM, double-buffered), then O_j = P_{j-1} V_{j-1}
+//               (M128 N128 K64, double-buffered), one elected thread
+//   warp 2      TMEM allocator (512 columns: S0 S1 | O0 | O1)
+//   warps 4-7   softmax + epilogue, one query row per thread (TMEM lane):
+//               tcgen05.ld S, scale + causal mask, online softmax in exp2
+//               form, P (bf16) into the SWIZZLE_128B smem tile the next MMA
+//               reads as its A operand, and O_acc = O_acc * alpha + O_j in
+//               registers; finally O_acc / l stored as bf16.
+// K_j's stage is released by the commit after the PV MMA of tile j, so the
+// softmax of tile j overlaps S_{j+1} and PV_{j-1} on the tensor core.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+
+#include "attn_sm100.hpp"
+
+namespace dwdp {
+namespace {
+
+constexpr int AQ = 128, AK = 64, DQK = 192, DV = 128, KVS = 3;
+constexpr int Q_BOX = AQ * 64 * 2;   // 16 KB: 128 rows x 64 columns
+constexpr int K_BOX = AK * 64 * 2;   // 8 KB
+constexpr int Q_BYTES = 3 * Q_BOX;   // 48 KB
+constexpr int K_BYTES = 3 * K_BOX;   // 24 KB
+constexpr int V_BYTES = DV * AK * 2; // 16 KB
+constexpr int P_BYTES = AQ * AK * 2; // 16 KB
+constexpr int ATT_SMEM = 1024 + Q_BYTES + KVS * (K_BYTES + V_BYTES) + 2 * P_BYTES + 256;
+// kind::f16 instruction descriptors, K-major A and B, bf16 in, fp32 out
+constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(AK >> 3) << 17) |
+                             (uint32_t(AQ >> 4) << 24);
+constexpr uint32_t IDESC_O = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(DV >> 3) << 17) |
+                             (uint32_t(AQ >> 4) << 24);
+constexpr uint32_t TM_S = 0, TM_O = 128;  // S buffers at 0 / 64, O buffers at 128 / 256
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// K-major SWIZZLE_128B operand descriptor (8-row atoms 1024 B apart, sm_100 version 1)
+__device__ __forceinline__ uint64_t desc(uint32_t saddr) {
+  return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+__device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  return uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(a))) |
+         (uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(b))) << 16);
+}
+
+__global__ void __launch_bounds__(256, 1)
+    mla_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const AttnTile* __restrict__ tiles,
+                    uint16_t* __restrict__ out, int H, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sQ = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = sQ + Q_BYTES;
+  uint8_t* sV = sK + KVS * K_BYTES;
+  uint8_t* sP = sV + KVS * V_BYTES;
+  uint64_t* q_full = reinterpret_cast<uint64_t*>(sP + 2 * P_BYTES);
+  uint64_t* kv_full = q_full + 1;
+  uint64_t* kv_empty = kv_full + KVS;
+  uint64_t* s_full = kv_empty + KVS;
+  uint64_t* s_empty = s_full + 2;
+  uint64_t* p_full = s_empty + 2;
+  uint64_t* p_empty = p_full + 2;
+  uint64_t* o_full = p_empty + 2;
+  uint64_t* o_empty = o_full + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_empty + 2);
+
+  const AttnTile tile = tiles[blockIdx.x];
+  const int head = blockIdx.y;
+  const int q_hi = min(tile.q0 + AQ, tile.len);  // queries [q0, q_hi) attend keys [0, q_hi)
+  const int nt = (q_hi + AK - 1) / AK;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    bar_init(q_full, 1);
+    for (int s = 0; s < KVS; ++s) {
+      bar_init(&kv_full[s], 1);
+      bar_init(&kv_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      bar_init(&s_full[b], 1);
+      bar_init(&s_empty[b], 4);
+      bar_init(&p_full[b], 4);
+      bar_init(&p_empty[b], 1);
+      bar_init(&o_full[b], 1);
+      bar_init(&o_empty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_holder)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer
+      bar_expect(q_full, Q_BYTES);
+      for (int a = 0; a < 3; ++a) tma3(sQ + a * Q_BOX, &tmQ, q_full, a * 64, head, tile.start + tile.q0);
+      for (int j = 0; j < nt; ++j) {
+        const int s = j % KVS;
+        bar_wait(&kv_empty[s], ((j / KVS) & 1) ^ 1);
+        bar_expect(&kv_full[s], K_BYTES + V_BYTES);
+        for (int a = 0; a < 3; ++a)
+          tma3(sK + s * K_BYTES + a * K_BOX, &tmK, &kv_full[s], a * 64, head, tile.start + j * AK);
+        tma3(sV + s * V_BYTES, &tmV, &kv_full[s], tile.vstart + j * AK, 0, head);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      bar_wait(q_full, 0);
+      fence_after();
+      const uint64_t qd = desc(su32(sQ));
+      auto pv = [&](int i) {  // O_i = P_i V_i into O buffer i % 2
+        const int b = i & 1;
+        bar_wait(&p_full[b], (i >> 1) & 1);
+        bar_wait(&o_empty[b], ((i >> 1) & 1) ^ 1);
+        fence_after();
+        const uint64_t pd = desc(su32(sP + b * P_BYTES));
+        const uint64_t vd = desc(su32(sV + (i % KVS) * V_BYTES));
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // 16 keys (32 bytes) per MMA
+          mma(tmem + TM_O + uint32_t(b) * DV, pd + 2 * k, vd + 2 * k, IDESC_O, k != 0);
+        commit(&o_full[b]);
+        commit(&kv_empty[i % KVS]);
+        commit(&p_empty[b]);
+      };
+      for (int j = 0; j < nt; ++j) {
+        const int b = j & 1, s = j % KVS;
+        bar_wait(&s_empty[b], ((j >> 1) & 1) ^ 1);
+        bar_wait(&kv_full[s], (j / KVS) & 1);
+        fence_after();
+        const uint64_t kd = desc(su32(sK + s * K_BYTES));
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma(tmem + TM_S + uint32_t(b) * AK, qd + uint64_t(a * (Q_BOX >> 4)) + 2 * k,
+                kd + uint64_t(a * (K_BOX >> 4)) + 2 * k, IDESC_S, (a | k) != 0);
+        commit(&s_full[b]);
+        if (j >= 1) pv(j - 1);
+      }
+      pv(nt - 1);
+    }
+  } else if (warp >= 4) {  // -------------------------------------------- softmax + epilogue
+    const int q = warp & 3, row = q * 32 + lane;
+    const int qi = tile.q0 + row;  // query position in its sequence
+    const uint32_t lb = uint32_t(q * 32) << 16;
+    float m = -INFINITY, l = 0.0f, alpha_prev = 0.0f;
+    float o[DV];
+#pragma unroll
+    for (int d = 0; d < DV; ++d) o[d] = 0.0f;
+    for (int j = 0; j <= nt; ++j) {
+      float alpha = 0.0f;
+      if (j < nt) {
+        const int b = j & 1;
+        bar_wait(&s_full[b], (j >> 1) & 1);
+        fence_after();
+        uint32_t r0[32], r1[32];
+        ld32(tmem + lb + TM_S + uint32_t(b) * AK, r0);
+        ld32(tmem + lb + TM_S + uint32_t(b) * AK + 32, r1);
+        ld_wait();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(&s_empty[b]);
+        float sv[AK];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < AK; ++c) {
+          const float v = __uint_as_float(c < 32 ? r0[c] : r1[c - 32]) * scale_log2;
+          sv[c] = (j * AK + c <= qi) ? v : -INFINITY;  // causal (keys past the sequence are > qi)
+          mx = fmaxf(mx, sv[c]);
+        }
+        const float m_new = fmaxf(m, mx);
+        alpha = exp2f(m - m_new);
+        float sum = 0.0f;
+#pragma unroll
+        for (int c = 0; c < AK; ++c) {
+          sv[c] = exp2f(sv[c] - m_new);
+          sum += sv[c];
+        }
+        l = l * alpha + sum;
+        m = m_new;
+        // P row (bf16, 128 B) into the SWIZZLE_128B tile: chunk c of row r at c ^ (r % 8)
+        bar_wait(&p_empty[b], ((j >> 1) & 1) ^ 1);
+        uint8_t* prow = sP + b * P_BYTES + (row >> 3) * 1024 + (row & 7) * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) << 4)) =
+              make_uint4(pack2(sv[8 * c], sv[8 * c + 1]), pack2(sv[8 * c + 2], sv[8 * c + 3]),
+                         pack2(sv[8 * c + 4], sv[8 * c + 5]), pack2(sv[8 * c + 6], sv[8 * c + 7]));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) bar_arrive(&p_full[b]);
+      }
+      if (j >= 1) {  // O_acc = O_acc * alpha_{j-1} + O_{j-1}
+        const int i = j - 1, b = i & 1;
+        bar_wait(&o_full[b], (i >> 1) & 1);
+        fence_after();
+#pragma unroll
+        for (int ch = 0; ch < DV / 32; ++ch) {
+          uint32_t r[32];
+          ld32(tmem + lb + TM_O + uint32_t(b) * DV + uint32_t(ch * 32), r);
+          ld_wait();
+#pragma unroll
+          for (int x = 0; x < 32; ++x) o[ch * 32 + x] = o[ch * 32 + x] * alpha_prev + __uint_as_float(r[x]);
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(&o_empty[b]);
+      }
+      alpha_prev = alpha;
+    }
+    if (qi < tile.len) {
+      const float inv = 1.0f / l;
+      uint4* dst = reinterpret_cast<uint4*>(out + (int64_t(tile.start + qi) * H + head) * DV);
+#pragma unroll
+      for (int c = 0; c < DV / 8; ++c)
+        dst[c] = make_uint4(pack2(o[8 * c] * inv, o[8 * c + 1] * inv), pack2(o[8 * c + 2] * inv, o[8 * c + 3] * inv),
+                            pack2(o[8 * c + 4] * inv, o[8 * c + 5] * inv), pack2(o[8 * c + 6] * inv, o[8 * c + 7] * inv));
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// ---------------------------------------------------------------- glue
+// RMSNorm without weight (x * rsqrt(mean(x^2) + eps)), one warp per row, fp32 math.
+__global__ void rmsnorm_kernel(const uint16_t* __restrict__ in, int64_t ld_in, uint16_t* __restrict__ out,
+                               int64_t ld_out, int64_t rows, int D, float eps) {
+  const int64_t r = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const uint16_t* x = in + r * ld_in;
+  float ss = 0.0f;
+  for (int i = lane; i < D; i += 32) {
+    const float v = __uint_as_float(uint32_t(x[i]) << 16);
+    ss += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float inv = rsqrtf(ss / float(D) + eps);
+  uint16_t* y = out + r * ld_out;
+  for (int i = lane; i < D; i += 32)
+    y[i] = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(uint32_t(x[i]) << 16) * inv));
+}
+
+// RoPE on the 64 rope dims of every q head, in place (interleaved pairs
+// (2i, 2i+1), angle pos * theta^(-2i/64)); one thread per (token, head, pair).
+__global__ void q_rope_kernel(uint16_t* __restrict__ q, const int32_t* __restrict__ pos, int64_t T, int H,
+                              float log2_theta) {
+  const int64_t n = T * H * 32;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / (H * 32);
+    const int p = int(i % 32);
+    uint16_t* v = q + (i / 32) * DQK + 128 + 2 * p;
+    const float ang = float(pos[t]) * exp2f(-log2_theta * float(2 * p) / 64.0f);
+    float sn, cs;
+    sincosf(ang, &sn, &cs);
+    const float x1 = __uint_as_float(uint32_t(v[0]) << 16), x2 = __uint_as_float(uint32_t(v[1]) << 16);
+    v[0] = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * cs - x2 * sn));
+    v[1] = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * sn + x2 * cs));
+  }
+}
+
+// K [T][H][192] = (k_nope of kv | RoPE(k_rope) shared by the heads) and
+// V^T [H][128][ldv] (token t at column vcol[t]) from kv [T][H][256]
+// (k_nope | v). One CTA per (64-token block, head); V goes through shared
+// memory so the reads of kv and the writes of V^T are row-contiguous runs.
+__global__ void __launch_bounds__(256) kv_assemble_kernel(const uint16_t* __restrict__ kv,
+                                                          const uint16_t* __restrict__ kva, int64_t ld_kva,
+                                                          int kv_lora, const int32_t* __restrict__ pos,
+                                                          const int32_t* __restrict__ vcol, int64_t T, int H,
+                                                          float log2_theta, uint16_t* __restrict__ K,
+                                                          uint16_t* __restrict__ Vt, int64_t ldv) {
+  __shared__ uint16_t tv[64][DV + 2];
+  __shared__ int32_t col[64];
+  const int64_t t0 = int64_t(blockIdx.x) * 64;
+  const int h = blockIdx.y;
+  if (threadIdx.x < 64) col[threadIdx.x] = t0 + threadIdx.x < T ? vcol[t0 + threadIdx.x] : -1;
+  for (int i = threadIdx.x; i < 64 * (DQK / 2); i += blockDim.x) {  // K: pairs of elements
+    const int tl = i / (DQK / 2), c = 2 * (i % (DQK / 2));
+    const int64_t t = t0 + tl;
+    if (t >= T) continue;
+    uint16_t* dk = K + (t * H + h) * DQK + c;
+    if (c < 128) {
+      const uint16_t* s = kv + (t * H + h) * 256 + c;
+      dk[0] = s[0];
+      dk[1] = s[1];
+    } else {
+      const int p = (c - 128) / 2;
+      const uint16_t* s = kva + t * ld_kva + kv_lora + 2 * p;
+      const float ang = float(pos[t]) * exp2f(-log2_theta * float(2 * p) / 64.0f);
+      float sn, cs;
+      sincosf(ang, &sn, &cs);
+      const float x1 = __uint_as_float(uint32_t(s[0]) << 16), x2 = __uint_as_float(uint32_t(s[1]) << 16);
+      dk[0] = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * cs - x2 * sn));
+      dk[1] = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * sn + x2 * cs));
+    }
+  }
+  for (int i = threadIdx.x; i < 64 * DV; i += blockDim.x) {
+    const int tl = i / DV, d = i % DV;
+    const int64_t t = t0 + tl;
+    tv[tl][d] = t < T ? kv[(t * H + h) * 256 + 128 + d] : uint16_t(0);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < DV * 64; i += blockDim.x) {
+    const int d = i / 64, tl = i % 64;
+    if (col[tl] >= 0) Vt[(int64_t(h) * DV + d) * ldv + col[tl]] = tv[tl][d];
+  }
+}
+
+}  // namespace
+
+void launch_mla_attention(const uint16_t* q, const uint16_t* k, const uint16_t* vt, int64_t T, int64_t ldv,
+                          int H, const AttnTile* tiles, int ntiles, float softmax_scale, uint16_t* out,
+                          cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(mla_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ATT_SMEM);
+  });
+  if (ntiles <= 0 || T <= 0) return;
+  const int64_t dq[3] = {DQK, H, T}, sq[2] = {DQK * 2, int64_t(H) * DQK * 2};
+  const int bq[3] = {64, 1, AQ}, bk[3] = {64, 1, AK};
+  const CUtensorMap tq = make_tmap_3d_bf16(q, dq, sq, bq);
+  const CUtensorMap tk = make_tmap_3d_bf16(k, dq, sq, bk);
+  const int64_t dv[3] = {ldv, DV, H}, sv[2] = {ldv * 2, int64_t(DV) * ldv * 2};
+  const int bv[3] = {AK, DV, 1};
+  const CUtensorMap tv = make_tmap_3d_bf16(vt, dv, sv, bv);
+  mla_attn_kernel<<<dim3(unsigned(ntiles), unsigned(H)), 256, ATT_SMEM, st>>>(
+      tq, tk, tv, tiles, out, H, softmax_scale * 1.4426950408889634f);
+}
+
+void launch_rmsnorm(const uint16_t* in, int64_t ld_in, uint16_t* out, int64_t ld_out, int64_t rows, int D,
+                    float eps, cudaStream_t st) {
+  if (rows > 0) rmsnorm_kernel<<<unsigned((rows + 7) / 8), 256, 0, st>>>(in, ld_in, out, ld_out, rows, D, eps);
+}
+
+void launch_q_rope(uint16_t* q, const int32_t* pos, int64_t T, int H, float theta, cudaStream_t st) {
+  const int64_t n = T * H * 32;
+  if (n > 0)
+    q_rope_kernel<<<unsigned(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0, st>>>(q, pos, T, H,
+                                                                                         std::log2(theta));
+}
+
+void launch_kv_assemble(const uint16_t* kv, const uint16_t* kva, int64_t ld_kva, int kv_lora, const int32_t* pos,
+                        const int32_t* vcol, int64_t T, int H, float theta, uint16_t* K, uint16_t* Vt,
+                        int64_t ldv, cudaStream_t st) {
+  if (T > 0)
+    kv_assemble_kernel<<<dim3(unsigned((T + 63) / 64), unsigned(H)), 256, 0, st>>>(
+        kv, kva, ld_kva, kv_lora, pos, vcol, T, H, std::log2(theta), K, Vt, ldv);
+}
+
+}  // namespace dwdp

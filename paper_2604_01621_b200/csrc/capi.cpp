@@ -123,6 +123,12 @@ dwdp::WorkloadSpec to_spec(const dwdp_workload_spec* w) {
   return s;
 }
 
+}  // namespace
+
+int dwdp::capi_guard(const std::function<void()>& f) { return guard(f); }
+
+namespace {
+
 dwdp::Ctx& C(dwdp_ctx* c) {
   need(c, "ctx");
   return *c->impl;

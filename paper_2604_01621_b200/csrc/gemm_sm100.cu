@@ -249,6 +249,19 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
          (uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(b))) << 16);
 }
 
+// Group tables, or a single dense group (GemmArgs::dense_m > 0: expert 0 in
+// slot 0, no device tables or meta; rows >= dense_m are not stored).
+__device__ __forceinline__ int g_expert(const GemmArgs& p, int mb) {
+  return p.mblock_expert ? p.mblock_expert[mb] : 0;
+}
+__device__ __forceinline__ int g_slot(const GemmArgs& p, int e) { return p.slot_of ? p.slot_of[e] : 0; }
+__device__ __forceinline__ int g_total_mb(const GemmArgs& p) {
+  return p.dense_m > 0 ? int((p.dense_m + 127) / 128) : p.meta[0];
+}
+__device__ __forceinline__ int g_routed_mb(const GemmArgs& p) {
+  return p.dense_m > 0 ? int((p.dense_m + 127) / 128) : p.meta[1];
+}
+
 // Linear tile id -> (m-block, n-block). Tiles of a segment (consecutive
 // m-blocks of one expert) occupy the id range [start*NB, (start+len)*NB), so
 // the segment is found from the m-block tile/NB falls in. Inside a segment the
@@ -341,7 +354,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
     sb1 = ssc + 128;
   } else if (FP8) {
     sa = p.a_scale[arow];
-    const int64_t b0 = int64_t(p.slot_of[p.mblock_expert[mb]]) * p.rows_per_slot +
+    const int64_t b0 = int64_t(g_slot(p, g_expert(p, mb))) * p.rows_per_slot +
                        int64_t(nb) * (SWIGLU ? 128 : BN);
     sb0 = p.b_scale0 + b0;
     sb1 = SWIGLU ? p.b_scale1 + b0 : nullptr;
@@ -529,8 +542,8 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  const int total_mb = p.meta[0];
-  const int routed_mb = p.meta[1];
+  const int total_mb = g_total_mb(p);
+  const int routed_mb = g_routed_mb(p);
   constexpr bool SWIGLU = MODE == kSwiGLU || MODE == kSwiGLU8 || MODE == kSwiGLU4;
   constexpr bool FP8 = MODE == kSwiGLU8 || MODE == kPlain8;
   // K elements per 128-byte smem row, and the TMA column step (map elements)
@@ -547,12 +560,12 @@ __global__ void __launch_bounds__(256, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       int mb, nb;
       tile_coords(tile, nb_count, p.mb_seg, p.raster, mb, nb);
-      const int e = p.mblock_expert[mb];
+      const int e = g_expert(p, mb);
       const bool sh = p.shared_a2 && e == p.E;
       const bool gather = p.a_rows != nullptr && !sh;
       const CUtensorMap* am = sh ? &tmA2 : &tmA;
       const int arow = (sh ? mb - routed_mb : mb) * BM;
-      const int brow = p.slot_of[e] * p.rows_per_slot + nb * (SWIGLU ? 128 : BN);
+      const int brow = g_slot(p, e) * p.rows_per_slot + nb * (SWIGLU ? 128 : BN);
       // gather mode: lane l copies rows 4l..4l+3 of the m-block (8 x 16 B per
       // row and k-block) into the SWIZZLE_128B layout TMA would have produced
       const char* srow[4];
@@ -711,7 +724,7 @@ __global__ void __launch_bounds__(256, 1)
     auto fetch_scales = [&](int t) {
       int m, n;
       tile_coords(t, nb_count, p.mb_seg, p.raster, m, n);
-      const int64_t b0 = int64_t(p.slot_of[p.mblock_expert[m]]) * p.rows_per_slot +
+      const int64_t b0 = int64_t(g_slot(p, g_expert(p, m))) * p.rows_per_slot +
                          int64_t(n) * (SWIGLU ? 128 : BN);
       n0 = __ldg(p.b_scale0 + b0 + et);
       n1 = SWIGLU ? __ldg(p.b_scale1 + b0 + et) : __ldg(p.b_scale0 + b0 + 128 + et);
@@ -914,8 +927,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  const int total_mb = p.meta[0];
-  const int routed_mb = p.meta[1];
+  const int total_mb = g_total_mb(p);
+  const int routed_mb = g_routed_mb(p);
   const int nb_count = SWIGLU ? p.n_out / 128 : (p.n_out + BN - 1) / BN;
   const int num_tiles = (total_mb >> 1) * nb_count;
   const int kb_count = p.K / BKE;
@@ -930,12 +943,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         int mp, nb;
         pair_coords(tile, nb_count, p.mb_seg, p.raster, mp, nb);
         const int mb = 2 * mp + int(rank);
-        const int e = p.mblock_expert[mb];
+        const int e = g_expert(p, mb);
         const bool sh = p.shared_a2 && e == p.E;
         const CUtensorMap* am = sh ? &tmA2 : &tmA;
         const int arow = (sh ? mb - routed_mb : mb) * BM;
         const CUtensorMap* bm = (SWIGLU && rank == 1) ? &tmB1 : &tmB0;
-        const int brow = p.slot_of[e] * p.rows_per_slot +
+        const int brow = g_slot(p, e) * p.rows_per_slot +
                          (SWIGLU ? nb * 128 : nb * BN + int(rank) * 128);
         for (int kb = 0; kb < kb_count; ++kb) {
           mbar_wait(&empty[st], ph ^ 1);
@@ -1097,7 +1110,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  const int total_mb = p.meta[0];
+  const int total_mb = g_total_mb(p);
   const int nb_count = SWIGLU ? p.n_out / 128 : p.n_out / BN;
   const int num_tiles = (total_mb >> 1) * nb_count;
   const int kb_count = p.K / 256;
@@ -1113,7 +1126,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         int mp, nb;
         pair_coords(tile, nb_count, p.mb_seg, p.raster, mp, nb);
         const int mb = 2 * mp + int(rank);
-        const int slot = p.slot_of[p.mblock_expert[mb]];
+        const int slot = g_slot(p, g_expert(p, mb));
         const int arow = mb * BM;
         // B rows of this CTA's half, and the 128-row blocks of the whole N tile
         const CUtensorMap* bm = (SWIGLU && rank == 1) ? &tmB1 : &tmB0;
@@ -1187,7 +1200,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       int mp, n;
       pair_coords(t, nb_count, p.mb_seg, p.raster, mp, n);
       const int m = 2 * mp + int(rank);
-      const int64_t b0 = int64_t(p.slot_of[p.mblock_expert[m]]) * p.rows_per_slot +
+      const int64_t b0 = int64_t(g_slot(p, g_expert(p, m))) * p.rows_per_slot +
                          int64_t(n) * (SWIGLU ? 128 : BN);
       n0 = __ldg(p.b_scale0 + b0 + et);
       n1 = SWIGLU ? __ldg(p.b_scale1 + b0 + et) : __ldg(p.b_scale0 + b0 + 128 + et);
@@ -1264,6 +1277,21 @@ CUtensorMap make_tmap_2d(const void* base, int64_t rows, int64_t cols, int box_r
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+
+CUtensorMap make_tmap_3d_bf16(const void* base, const int64_t dims[3], const int64_t strides[2],
+                              const int box[3]) {
+  CUtensorMap m;
+  const cuuint64_t d[3] = {cuuint64_t(dims[0]), cuuint64_t(dims[1]), cuuint64_t(dims[2])};
+  const cuuint64_t st[2] = {cuuint64_t(strides[0]), cuuint64_t(strides[1])};
+  const cuuint32_t b[3] = {cuuint32_t(box[0]), cuuint32_t(box[1]), cuuint32_t(box[2])};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), d, st, b, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled (3-D) failed (" + std::to_string(int(r)) + ")");
   return m;
 }
 

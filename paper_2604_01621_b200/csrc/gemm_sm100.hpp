@@ -57,6 +57,9 @@ struct GemmArgs {
   // the split layout writes GEMM1's H into 256-row expert segments and GEMM2's
   // O back into 128-row segments (launch_split_layout). A rows stay mb * 128.
   const int32_t* d_row0;
+  // > 0: one dense group of dense_m A rows (no tables, meta or slot map;
+  // mblock_expert / slot_of / meta may be null; set m_limit = dense_m)
+  int64_t dense_m;
 };
 
 // 2-D bf16 TMA map over a row-major [rows][cols] matrix, box = 64 x box_rows,
@@ -69,6 +72,10 @@ CUtensorMap make_tmap_i8(const void* base, int64_t rows, int64_t cols, int box_r
 // (2 KB = the 4 atoms of one 256-deep k-block and 128 data rows), no swizzle:
 // the CTA-pair NVFP4 GEMM loads scales with TMA.
 CUtensorMap make_tmap_sf(const void* base, int64_t bytes);
+// 3-D bf16 map (dims innermost first, strides in bytes of dims 1 and 2),
+// SWIZZLE_128B (box[0] * 2 must be 128 bytes): the attention's per-head tiles.
+CUtensorMap make_tmap_3d_bf16(const void* base, const int64_t dims[3], const int64_t strides[2],
+                              const int box[3]);
 // bf16 [rows][cols] output map, 32 x 32 boxes, SWIZZLE_64B: the TMA-store
 // epilogue of the NVFP4 GEMM2.
 CUtensorMap make_tmap_out(const void* base, int64_t rows, int64_t cols);

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdint>
 #include <deque>
+#include <functional>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -23,6 +24,9 @@ struct CudaError : std::runtime_error {
 };
 
 void nccl_unique_id(void* out);  // dep.cpp
+// The C-ABI's exception -> status mapping (capi.cpp), for entry points
+// defined in other translation units (mla.cpp).
+int capi_guard(const std::function<void()>& f);
 void nccl_destroy(void* comm);
 
 #define DWDP_CUDA(x)                                                                         \
