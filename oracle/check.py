@@ -8,6 +8,8 @@ batch (R1 shapes, T ~ 61K tokens) with the CPU oracle:
   counts and the stable expert-major permutation rows, against oracle_route /
   oracle_permute (the DeepSeek-V3 routing restated in oracle/dwdp_oracle.c;
   rows sum to T*k as include/dwdpsim/workload.hpp:50-52 requires);
+* the exact (22-bit fixed point, int64-sum) router's top-k against float64
+  logits for all T tokens (fp64_agreement);
 * layer outputs on a seeded sample of rows (every MoE row depends only on its
   own token, so a row subset through the oracle is exact) within the stated
   normwise relative error of the oracle's fp32 math.
@@ -71,6 +73,9 @@ def check_layer(ctx, x, layer: int = 0, sample_rows: int = 512, seed: int = 0,
         "padded_rows": int(total),
         "touched_experts": int((ocounts > 0).sum()),
         "oracle_route_s": round(t_route, 2),
+        # the exact router's selection vs float64 logits (weak point of a
+        # quantised-exact router: near-ties between experts)
+        "fp64_routing": fp64_agreement(oc, xb, T, wr, oidx, bias),
     }
     # sampled rows: first, last and a seeded draw
     rng = np.random.default_rng(seed)
@@ -95,3 +100,40 @@ def check_layer(ctx, x, layer: int = 0, sample_rows: int = 512, seed: int = 0,
                      and res["sample_routing_equal"] and res["rel_err_normwise"] < 1e-2
                      and res["max_row_rel_err"] < 1e-2)
     return res
+
+
+def fp64_route(cfg, x_bf16: np.ndarray, T: int, w_router_bf16: np.ndarray, bias=None):
+    """DeepSeek-V3 / Qwen routing with float64 logits (x . Wr^T of bf16
+    values: every product exact, the 7168-term sums to ~1e-16): the
+    unquantised selection the exact 22-bit router is compared against.
+    Returns idx [T][k] ordered like oracle_route (descending choice score,
+    ties to the lower expert)."""
+    E, k, h = cfg.num_experts, cfg.top_k, cfg.hidden
+    x = O.bf16_to_f32(x_bf16).reshape(T, h).astype(np.float64)
+    w = O.bf16_to_f32(w_router_bf16).reshape(E, h).astype(np.float64)
+    lg = x @ w.T
+    if cfg.scoring == 1:
+        sc = 1.0 / (1.0 + np.exp(-lg))
+        ch = sc + (0.0 if bias is None else np.asarray(bias, np.float64)[None, :])
+    else:
+        ch = lg.copy()
+    G = max(cfg.n_group, 1)
+    if G > 1 and cfg.topk_group < G:
+        gs = E // G
+        g2 = np.sort(ch.reshape(T, G, gs), axis=-1)[..., -2:].sum(-1) if gs >= 2 else ch.reshape(T, G, gs)[..., 0]
+        order = np.argsort(-g2, axis=1, kind="stable")[:, :cfg.topk_group]
+        keep = np.zeros((T, G), bool)
+        np.put_along_axis(keep, order, True, axis=1)
+        ch = np.where(np.repeat(keep, gs, axis=1), ch, 0.0)
+    return np.argsort(-ch, axis=1, kind="stable")[:, :k].astype(np.int32)
+
+
+def fp64_agreement(cfg, x_bf16: np.ndarray, T: int, w_router_bf16: np.ndarray, idx_exact: np.ndarray,
+                   bias=None) -> dict:
+    """How often the exact 22-bit router's top-k differs from float64 routing."""
+    ref = fp64_route(cfg, x_bf16, T, w_router_bf16, bias)
+    same_set = (np.sort(ref, 1) == np.sort(idx_exact, 1)).all(1)
+    same_order = (ref == idx_exact).all(1)
+    return {"tokens": int(T), "topk_set_mismatch_tokens": int((~same_set).sum()),
+            "topk_order_mismatch_tokens": int((~same_order).sum()),
+            "topk_set_agreement": float(same_set.mean())}
