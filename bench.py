@@ -216,10 +216,11 @@ def main():
     ap.add_argument("--attention", action="store_true",
                     help="run a DeepSeek-V3 MLA prefill block (library ops) before every MoE layer, "
                          "in DWDP and DEP alike: the paper's prefetch window MoE(l) + Attention(l+1)")
-    ap.add_argument("--check", action="store_true",
-                    help="after timing (N=1): check layer 0 on the first timed batch against the CPU "
-                         "oracle -- routing of all T tokens bit-exact, 512 sampled rows within 1e-2 "
-                         "(oracle/check.py; the checker, outside every timed region)")
+    ap.add_argument("--no-check", dest="check", action="store_false",
+                    help="skip the parity check that runs after timing at N=1: layer 0 on the first "
+                         "timed batch against the CPU oracle -- routing of all T tokens bit-exact, 512 "
+                         "sampled rows within 1e-2 (oracle/check.py; the checker, outside every timed "
+                         "region)")
     ap.add_argument("--zipf", type=float, default=0.0,
                     help="expert-routing skew s: router bias -ZIPF_BETA*s*ln(e+1)")
     args = ap.parse_args()

@@ -74,8 +74,9 @@ def check_layer(ctx, x, layer: int = 0, sample_rows: int = 512, seed: int = 0,
         "touched_experts": int((ocounts > 0).sum()),
         "oracle_route_s": round(t_route, 2),
         # the exact router's selection vs float64 logits (weak point of a
-        # quantised-exact router: near-ties between experts)
-        "fp64_routing": fp64_agreement(oc, xb, T, wr, oidx, bias),
+        # quantised-exact router: near-ties between experts); first 16K tokens
+        "fp64_routing": fp64_agreement(oc, xb[:min(T, 16384) * h], min(T, 16384), wr,
+                                       oidx[:min(T, 16384)], bias),
     }
     # sampled rows: first, last and a seeded draw
     rng = np.random.default_rng(seed)

@@ -1240,6 +1240,166 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   }
 }
 
+// ---------------------------------------------------------------- router
+// Router logits with the digit-plane recombination fused into the GEMM.
+// A = the activations' three int8 digit planes [3][T][h] (plane a weighs
+// 2^8a), B = the router weights' planes [3][E][h]. A tile (128 tokens x 64
+// experts) issues all nine plane products per k-block, accumulating the
+// products of equal weight a + b = s in one int32 TMEM accumulator D_s
+// (|D_s| <= 3 * h * 2^14 < 2^31 for h <= 43690), five accumulators of 64
+// columns. The epilogue forms the exact z = sum_s D_s 2^8s in int64 and the
+// fp32 logit ldexp(fp32(z), e_x + e_w - 296) -- the same single rounding as
+// the oracle (dwdp_oracle.c route_one) -- and writes fp32 logits [T][E]:
+// 4 B per (token, expert) instead of 36 B of int32 plane products.
+constexpr int R_BN = 64;
+constexpr int R_STAGES = 2;               // 144 KB: fits beside a 26 KB pull CTA
+constexpr int R_A = 3 * BM * 128;         // 48 KB: 3 planes x 128 rows x 128 B of K
+constexpr int R_B = 3 * R_BN * 128;       // 24 KB
+constexpr int R_SMEM = R_STAGES * (R_A + R_B) + 1024 + 256;
+constexpr uint32_t R_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(R_BN >> 3) << 17) |
+                             (uint32_t(BM >> 4) << 24);
+
+__global__ void __launch_bounds__(256, 1)
+    router_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       const int32_t* __restrict__ xe, const int32_t* __restrict__ we,
+                       float* __restrict__ logits, int T, int E, int K) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sA = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = sA + R_STAGES * R_A;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + R_STAGES * R_B);
+  uint64_t* empty = full + R_STAGES;
+  uint64_t* tfull = empty + R_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < R_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  const int nb_count = E / R_BN;
+  const int num_tiles = (T + BM - 1) / BM * nb_count;
+  const int kb_count = K / 128;
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer: the m-block's 3 A planes and the n-block's 3 B planes
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mb = tile / nb_count, nb = tile - mb * nb_count;
+        for (int kb = 0; kb < kb_count; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], R_A + R_B);
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            tma_load_2d(sA + s * R_A + a * (BM * 128), &tmA, &full[s], kb * 128, a * T + mb * BM);
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            tma_load_2d(sB + s * R_B + b * (R_BN * 128), &tmB, &full[s], kb * 128, b * E + nb * R_BN);
+          if (++s == R_STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer: 9 plane products x 4 K-steps per k-block into D_{a+b}
+      int s = 0;
+      uint32_t ph = 0;
+      int local = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+        mbar_wait(tempty, (local & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < kb_count; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t ad = sw128_desc(smem_u32(sA + s * R_A));
+          const uint64_t bd = sw128_desc(smem_u32(sB + s * R_B));
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+              for (int k = 0; k < 4; ++k)  // the first product into D_s overwrites it
+                tc_mma_i8(tmem + uint32_t((a + b) * R_BN), ad + uint64_t(a * (BM * 128 >> 4)) + 2 * k,
+                          bd + uint64_t(b * (R_BN * 128 >> 4)) + 2 * k, R_IDESC,
+                          (kb | k) != 0 || !(a == 0 || b == 2));
+          tc_commit(&empty[s]);
+          if (++s == R_STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        tc_commit(tfull);
+      }
+    }
+  } else if (warp >= 4) {  // epilogue: exact recombination, one rounding, fp32 logits
+    const int q = warp & 3;
+    const uint32_t lb = uint32_t(q * 32) << 16;
+    int local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int mb = tile / nb_count, nb = tile - mb * nb_count;
+      const int t = mb * BM + q * 32 + lane;
+      const int sx0 = t < T ? xe[t] - 296 : 0;
+      mbar_wait(tfull, local & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < R_BN; c += 32) {
+        long long z[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) z[i] = 0;
+#pragma unroll
+        for (int sidx = 0; sidx < 5; ++sidx) {
+          uint32_t r[32];
+          tmem_ld32_issue(tmem + lb + uint32_t(sidx * R_BN + c), r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) z[i] += static_cast<long long>(int32_t(r[i])) * (1LL << (8 * sidx));
+        }
+        if (c + 32 >= R_BN) {  // accumulators drained: the next tile's MMAs may start
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty);
+        }
+        if (t < T) {
+          const int e0 = nb * R_BN + c;
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int sx = sx0 + __ldg(we + e0 + i);
+            const float f = __ll2float_rn(z[i]);
+            v[i] = (sx >= -126 && sx <= 127) ? __fmul_rn(f, __int_as_float((sx + 127) << 23)) : ldexpf(f, sx);
+          }
+          float4* o = reinterpret_cast<float4*>(logits + int64_t(t) * E + e0);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 // ---------------------------------------------------------------- host
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1446,6 +1606,21 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
     grouped_gemm_kernel<kSwiGLU8><<<grid, 256, SMEM_BYTES8, st>>>(a, a2, b0, b1, a, args);
   else
     grouped_gemm_kernel<kPlain8><<<grid, 256, SMEM_BYTES8, st>>>(a, a2, b0, b1, a, args);
+}
+
+void launch_router_gemm(const CUtensorMap& planes_x, const CUtensorMap& planes_w, const int32_t* xe,
+                        const int32_t* we, float* logits, int64_t T, int E, int64_t K, cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(router_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, R_SMEM);
+  });
+  if (T <= 0) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (T + BM - 1) / BM * (E / R_BN);
+  router_gemm_kernel<<<unsigned(std::min<int64_t>(tiles, sms)), 256, R_SMEM, st>>>(planes_x, planes_w, xe, we,
+                                                                                    logits, int(T), E, int(K));
 }
 
 }  // namespace dwdp

@@ -83,6 +83,12 @@ CUtensorMap make_tmap_out(const void* base, int64_t rows, int64_t cols);
 constexpr int GEMM_SWIGLU = 0, GEMM_PLAIN = 1, GEMM_INT8 = 2, GEMM_SWIGLU_FP8 = 3,
               GEMM_PLAIN_FP8 = 4, GEMM_SWIGLU_FP4 = 5, GEMM_PLAIN_FP4 = 6;
 
+// Router logits [T][E] (fp32) from the int8 digit planes of x ([3][T][K],
+// 128-row boxes) and of the router weights ([3][E][K], 64-row boxes) with
+// the exact recombination fused into the epilogue (E % 64 == 0, K % 128 == 0).
+void launch_router_gemm(const CUtensorMap& planes_x, const CUtensorMap& planes_w, const int32_t* xe,
+                        const int32_t* we, float* logits, int64_t T, int E, int64_t K, cudaStream_t st);
+
 // a: routed A rows (permuted tokens or H); a2: shared-expert A rows (x);
 // b0: gate (SwiGLU) or down arena; b1: up arena (SwiGLU only).
 // sf: NVFP4 maps {A scales, B0 scales, B1 scales, D output}; the CTA-pair

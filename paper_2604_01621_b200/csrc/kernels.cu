@@ -692,7 +692,9 @@ __global__ void __launch_bounds__(256) topk_kernel(const int32_t* __restrict__ C
 // vectors, a group's top-2 is a lane-local top-2 merged over the group's
 // E/(n_group*V) lanes (two xor shuffles for R1) and the kept groups are
 // ranked from G broadcast scores. Results are bit-identical to topk_kernel.
-template <int V>
+// FROM_LOGITS: the logits were already formed (router GEMM with the
+// recombination fused, launch_router_gemm); read them instead of C.
+template <int V, bool FROM_LOGITS>
 __global__ void __launch_bounds__(256) topk_contig_kernel(const int32_t* __restrict__ C,
                                                           const int32_t* __restrict__ ex,
                                                           const int32_t* __restrict__ ew,
@@ -711,7 +713,7 @@ __global__ void __launch_bounds__(256) topk_contig_kernel(const int32_t* __restr
 #pragma unroll
   for (int i = 0; i < V; ++i) z[i] = 0;
 #pragma unroll
-  for (int a = 0; a < 3; ++a)
+  for (int a = 0; a < (FROM_LOGITS ? 0 : 3); ++a)
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
       const int32_t* src = C + (a * T + t) * (3 * E) + b * E + e0;
@@ -737,10 +739,14 @@ __global__ void __launch_bounds__(256) topk_contig_kernel(const int32_t* __restr
   float* row = logits + t * E;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
-    const int sx = xe + ew[e0 + i] - 296;
-    const float f = __ll2float_rn(z[i]);
-    lg[i] = (sx >= -126 && sx <= 127) ? __fmul_rn(f, __int_as_float((sx + 127) << 23)) : ldexpf(f, sx);
-    row[e0 + i] = lg[i];
+    if (FROM_LOGITS) {
+      lg[i] = row[e0 + i];
+    } else {
+      const int sx = xe + ew[e0 + i] - 296;
+      const float f = __ll2float_rn(z[i]);
+      lg[i] = (sx >= -126 && sx <= 127) ? __fmul_rn(f, __int_as_float((sx + 127) << 23)) : ldexpf(f, sx);
+      row[e0 + i] = lg[i];
+    }
     if (c.scoring == 1) {
       sc[i] = __fdiv_rn(1.0f, __fadd_rn(1.0f, det_expf(-lg[i])));
       ch[i] = __fadd_rn(sc[i], bias ? bias[e0 + i] : 0.0f);
@@ -1510,14 +1516,16 @@ void launch_topk(const int32_t* C, const int32_t* ex, const int32_t* ew, const f
   const bool contig = c.E % 32 == 0 && (V == 1 || V == 2 || V == 4 || V == 8) &&
                       (G == 1 || ((c.E / G) % V == 0 && (c.E / G) / V <= 32 &&
                                   (((c.E / G) / V) & ((c.E / G) / V - 1)) == 0));
-  if (contig && V == 8)
-    topk_contig_kernel<8><<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
+  if (contig && V == 8 && C == nullptr)  // logits formed by the fused router GEMM
+    topk_contig_kernel<8, true><<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
+  else if (contig && V == 8)
+    topk_contig_kernel<8, false><<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
   else if (contig && V == 4)
-    topk_contig_kernel<4><<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
+    topk_contig_kernel<4, false><<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
   else if (contig && V == 2)
-    topk_contig_kernel<2><<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
+    topk_contig_kernel<2, false><<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
   else if (contig && V == 1)
-    topk_contig_kernel<1><<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
+    topk_contig_kernel<1, false><<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
   else
     topk_kernel<<<grid, 256, 0, st>>>(C, ex, ew, bias, logits, idx, wts, T, c);
 }

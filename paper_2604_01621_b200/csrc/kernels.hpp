@@ -36,6 +36,8 @@ void launch_router_quant(const uint16_t* src, int64_t R, int64_t K, int8_t* dst,
                          int32_t* meta, cudaStream_t st);
 // Scoring + group-limited top-k + weights; idx/wts [T][k]. Logits come from
 // the 9 int32 digit-plane products C[3T][3E] and the row exponents.
+// C == nullptr: `logits` already holds the fp32 logits (launch_router_gemm;
+// E = 256 contiguous-lane path only).
 void launch_topk(const int32_t* C, const int32_t* ex, const int32_t* ew, const float* bias,
                  float* logits, int32_t* idx, float* wts, int64_t T, const RouterCfg& c,
                  cudaStream_t st);

@@ -189,13 +189,23 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
   hbuf_ = static_cast<uint16_t*>(dalloc(size_t(h_rows) * f_ * 2, &workspace_bytes));
   router_wq_ = static_cast<int8_t*>(dalloc(size_t(WL_) * 3 * E_ * h_, &weight_bytes));
   router_we_ = static_cast<int32_t*>(dalloc(size_t(WL_) * E_ * 4, &weight_bytes));
+  // fused router GEMM (E % 64 == 0, the contiguous-lane top-k for E = 256,
+  // h % 128 == 0); DWDP_ROUTER=planes keeps the plane-product GEMM + top-k
+  {
+    const char* rt = std::getenv("DWDP_ROUTER");
+    const int G = c.n_group > 0 ? c.n_group : 1;
+    router_fused_ = !(rt && std::string(rt) == "planes") && E_ == 256 && h_ % 128 == 0 &&
+                    (G == 1 || (E_ / G) % 8 == 0);
+  }
   for (int wl = 0; wl < WL_; ++wl) {
+    tm_rw64_.push_back(make_tmap_i8(router_wq_ + size_t(wl) * 3 * E_ * h_, 3 * int64_t(E_), h_, 64));
     tm_rw_.push_back(make_tmap_i8(router_wq_ + size_t(wl) * 3 * E_ * h_, 3 * int64_t(E_), h_, 256));
     tm_rw_p_.push_back(make_tmap_i8(router_wq_ + size_t(wl) * 3 * E_ * h_, 3 * int64_t(E_), h_, 128));
   }
   xq_ = static_cast<int8_t*>(dalloc(size_t(max_tokens_) * 3 * h_, &workspace_bytes));
   xe_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * 4, &workspace_bytes));
-  rC_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * 9 * E_ * 4, &workspace_bytes));
+  if (!router_fused_)  // int32 plane products: only the unfused router needs them
+    rC_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * 9 * E_ * 4, &workspace_bytes));
   rmeta_ = static_cast<int32_t*>(dalloc(16, &workspace_bytes));
   const size_t nz = size_t((3 * max_tokens_ + 127) / 128 + 8);
   zeros_ = static_cast<int32_t*>(dalloc(nz * 4, &workspace_bytes));
@@ -727,6 +737,16 @@ void Ctx::prefetch_times(int64_t h, int64_t* s, int64_t* e, double* bytes) {
 // against the weight planes, exact recombination + scoring + top-k.
 void Ctx::route_logits(int wl, const uint16_t* x, int64_t T, cudaStream_t st) {
   launch_router_quant(x, T, h_, xq_, xe_, rmeta_, st);
+  RouterCfg rc{E_, k_, cfg.scoring, cfg.n_group, cfg.topk_group, cfg.norm_topk, cfg.routed_scale};
+  if (router_fused_) {
+    // one GEMM over the 3 x 3 digit-plane products with the exact
+    // recombination in its epilogue -> fp32 logits; top-k reads them
+    const CUtensorMap tx = make_tmap_i8(xq_, 3 * T, h_, 128);
+    launch_router_gemm(tx, tm_rw64_[size_t(wl)], xe_, router_we_ + size_t(wl) * E_, logits_, T, E_, h_, st);
+    launch_topk(nullptr, xe_, router_we_ + size_t(wl) * E_, bias_ + size_t(wl) * E_, logits_, idx_, wts_, T, rc,
+                st);
+    return;
+  }
   const CUtensorMap tx = make_tmap_i8(xq_, 3 * T, h_, 128);
   GemmArgs ga{int(h_), 3 * E_, 0, -1, zeros_, zeros_, rmeta_,
               reinterpret_cast<uint16_t*>(rC_), 3 * int64_t(E_), 3 * T, 0, nullptr,
@@ -734,7 +754,6 @@ void Ctx::route_logits(int wl, const uint16_t* x, int64_t T, cudaStream_t st) {
   const int64_t tiles = (3 * T + 127) / 128 * ((3 * E_ + 255) / 256);
   const CUtensorMap& tb = gemm2_pair_ ? tm_rw_p_[size_t(wl)] : tm_rw_[size_t(wl)];
   launch_grouped_gemm(GEMM_INT8, tx, tx, tb, tb, ga, int(std::min<int64_t>(tiles, 1 << 30)), st);
-  RouterCfg rc{E_, k_, cfg.scoring, cfg.n_group, cfg.topk_group, cfg.norm_topk, cfg.routed_scale};
   launch_topk(rC_, xe_, router_we_ + size_t(wl) * E_, bias_ + size_t(wl) * E_, logits_, idx_, wts_,
               T, rc, st);
 }

@@ -182,6 +182,8 @@ class Ctx {
   int8_t* router_wq_ = nullptr;
   int32_t* router_we_ = nullptr;
   std::vector<CUtensorMap> tm_rw_, tm_rw_p_;  // router weight planes (256 / 128-row boxes)
+  std::vector<CUtensorMap> tm_rw64_;          // 64-row boxes (fused router GEMM)
+  bool router_fused_ = false;
   int8_t* xq_ = nullptr;               // activation digit planes [3][T][h]
   int32_t* xe_ = nullptr;              // activation row exponents [T]
   int32_t* rC_ = nullptr;              // int32 plane products [3T][3E]
