@@ -405,6 +405,8 @@ void launch_mla_attention(const uint16_t* q, const uint16_t* k, const uint16_t* 
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncSetAttribute(mla_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ATT_SMEM);
+    cudaFuncSetAttribute(mla_attn_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
   });
   if (ntiles <= 0 || T <= 0) return;
   const int64_t dq[3] = {DQK, H, T}, sq[2] = {DQK * 2, int64_t(H) * DQK * 2};

@@ -393,8 +393,8 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
                               size_t(send_rows[size_t(rank_)]) * rowel * 2, cudaMemcpyDeviceToDevice, st));
   mark(&rec.comm[3]);
   // 6. weighted combine (shared rows follow the routed rows of the receive buffer)
-  launch_combine(xperm_, row_of_, wts_, shared_ ? dep_recv_ + routed_rows * h_ : nullptr, nullptr,
-                 residual ? x : nullptr, y, T, k_, h_, st);
+  combine_into(xperm_, row_of_, wts_, shared_ ? dep_recv_ + routed_rows * h_ : nullptr, nullptr,
+               residual ? x : nullptr, y, T, k_, st);
   launches += (T > 0 ? 3 : 0) + np + (nblocks > 0 ? (fp4_ ? 5 : fp8_ ? 3 : 2) : 0) + 1;
   DWDP_CUDA(cudaGetLastError());
   DWDP_CUDA(cudaEventRecord(rec.moe_end, st));
@@ -403,12 +403,20 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
 }
 
 void Ctx::dep_stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t st) {
-  if (dep_mode == 1) {
-    const auto Ts = dep2_exchange_tokens(T, st);  // once per stack: every layer has the same T
-    for (int l = 0; l < L_; ++l) dep2_layer_forward(l, l == 0 ? x : y, T, y, true, st, Ts);
-    return;
+  std::vector<int64_t> Ts;
+  if (dep_mode == 1) Ts = dep2_exchange_tokens(T, st);  // once per stack: every layer has the same T
+  uint16_t* p = ping();  // ping-pong as in stack_forward
+  const uint16_t* in = x;
+  for (int l = 0; l < L_; ++l) {
+    uint16_t* out = ((L_ - 1 - l) % 2 == 0) ? y : p;
+    if (in == out) out = (out == y) ? p : y;
+    if (dep_mode == 1)
+      dep2_layer_forward(l, in, T, out, true, st, Ts);
+    else
+      dep_layer_forward(l, in, T, out, true, st);
+    in = out;
   }
-  for (int l = 0; l < L_; ++l) dep_layer_forward(l, l == 0 ? x : y, T, y, true, st);
+  if (in != y) DWDP_CUDA(cudaMemcpyAsync(y, in, size_t(T) * h_ * 2, cudaMemcpyDeviceToDevice, st));
 }
 
 // ===================================================================== //
@@ -427,7 +435,23 @@ void Ctx::dep2_alloc() {
       dalloc(size_t(permute_scratch_ints(rows, E_)) * 4, &workspace_bytes));
   dep2_rowf_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * N_ * 4, &workspace_bytes));
   dep2_wf_ = static_cast<float*>(dalloc(size_t(max_tokens_) * N_ * 4, &workspace_bytes));
-  dep2_tok_ = static_cast<int32_t*>(dalloc(size_t(N_) * 8 * 2, &workspace_bytes));
+  dep2_tok_ = static_cast<int32_t*>(dalloc(size_t(N_) * 8 * 4, &workspace_bytes));
+  {
+    const int per = E_ / N_;
+    const int64_t balanced = max_tokens_ * k_;  // a rank's expected routed rows
+    const int64_t routed = std::min<int64_t>(rows * std::min(k_, per), balanced * 13 / 10);
+    dep2_cap_rows_ = (routed + int64_t(per) * 128 + max_tokens_ + 127) / 128 * 128 + 256;
+    dep2_max_mb_ = dep2_cap_rows_ / 128 + 4;
+    dep2_xperm_ = static_cast<uint16_t*>(dalloc(size_t(dep2_cap_rows_) * h_ * 2, &workspace_bytes));
+    dep2_h_ = static_cast<uint16_t*>(dalloc(size_t(dep2_cap_rows_) * f_ * 2, &workspace_bytes));
+    dep2_mblock_ = static_cast<int32_t*>(dalloc(size_t(dep2_max_mb_) * 4, &workspace_bytes));
+    dep2_mbrows_ = static_cast<int32_t*>(dalloc(size_t(dep2_max_mb_) * 4, &workspace_bytes));
+    dep2_mbseg_ = static_cast<int2*>(dalloc(size_t(dep2_max_mb_) * sizeof(int2), &workspace_bytes));
+    dep2_meta_ = static_cast<int32_t*>(dalloc(16 * 4, &workspace_bytes));
+    DWDP_CUDA(cudaMemset(dep2_meta_, 0, 16 * 4));
+    tm_dep2_xperm_ = make_tmap_bf16(dep2_xperm_, dep2_cap_rows_, h_, 128);
+    tm_dep2_h_ = make_tmap_bf16(dep2_h_, dep2_cap_rows_, f_, 128);
+  }
   DWDP_CUDA(cudaHostAlloc(&dep2_tok_host_, size_t(N_) * 8, 0));
   DWDP_CUDA(cudaHostAlloc(&dep2_flag_host_, 16, 0));
   dep2_flag_host_[0] = 0;
@@ -438,15 +462,25 @@ void Ctx::dep2_alloc() {
 std::vector<int64_t> Ctx::dep2_exchange_tokens(int64_t T, cudaStream_t st) {
   require(nccl_ != nullptr, "dep: call dep_init first");
   dep2_alloc();
-  // a previous layer's receive side overflowed its row capacity: loud
-  invariant(dep2_flag_host_[0] == 0, "dep mode 1: receive-side rows exceeded the workspace");
   const Nccl& n = nccl();
+  // (T, overflow flag of this rank's previous layers) from every rank: a
+  // receive-side overflow anywhere raises on all ranks at the same point
+  // (a single rank raising would leave the others waiting in NCCL)
   int64_t* dt = reinterpret_cast<int64_t*>(dep2_tok_);
-  DWDP_CUDA(cudaMemcpyAsync(dt + N_, &T, 8, cudaMemcpyHostToDevice, st));
-  nccl_check(n.AllGather(dt + N_, dt, 1, kInt64, nccl_, st), "ncclAllGather");
-  DWDP_CUDA(cudaMemcpyAsync(dep2_tok_host_, dt, size_t(N_) * 8, cudaMemcpyDeviceToHost, st));
+  const int64_t mine[2] = {T, int64_t(dep2_flag_host_[0])};
+  DWDP_CUDA(cudaMemcpyAsync(dt + 2 * N_, mine, 16, cudaMemcpyHostToDevice, st));
+  nccl_check(n.AllGather(dt + 2 * N_, dt, 2, kInt64, nccl_, st), "ncclAllGather");
+  std::vector<int64_t> all(size_t(2 * N_));
+  DWDP_CUDA(cudaMemcpyAsync(all.data(), dt, size_t(2 * N_) * 8, cudaMemcpyDeviceToHost, st));
   DWDP_CUDA(cudaStreamSynchronize(st));
-  return std::vector<int64_t>(dep2_tok_host_, dep2_tok_host_ + N_);
+  std::vector<int64_t> Ts(static_cast<size_t>(N_));
+  bool over = false;
+  for (int r = 0; r < N_; ++r) {
+    Ts[size_t(r)] = all[size_t(2 * r)];
+    over = over || all[size_t(2 * r + 1)] != 0;
+  }
+  invariant(!over, "dep mode 1: receive-side rows exceeded the workspace on some rank");
+  return Ts;
 }
 
 void Ctx::dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
@@ -510,24 +544,24 @@ void Ctx::dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* 
   launch_localize_idx(dep2_idx_, Tall * k_, lo, lo + per, dep2_loc_, st);
   int np = 1;
   if (Tall > 0)
-    np += launch_permute(dep2_loc_, dep2_x_, Tall, E_, k_, h_, shared_ ? 1 : 0, counts_, dep2_rowof_, mblock_,
-                         mbseg_, nullptr, meta_, xperm_, dep2_scratch_, st, nullptr, nullptr, 128, mbrows_,
-                         nullptr, T, max_rows_);
+    np += launch_permute(dep2_loc_, dep2_x_, Tall, E_, k_, h_, shared_ ? 1 : 0, counts_, dep2_rowof_,
+                         dep2_mblock_, dep2_mbseg_, nullptr, dep2_meta_, dep2_xperm_, dep2_scratch_, st, nullptr,
+                         nullptr, 128, dep2_mbrows_, nullptr, T, dep2_cap_rows_);
   mark(&rec.k[1]);
   // 4. grouped GEMMs (the rank's expert block + its shared expert)
   const int32_t* stab = slot_tab_ + size_t(layer) * 2 * (E_ + 1);
-  const int64_t mb_ub = max_mb_;
-  const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_xperm_;
-  GemmArgs g1{int(h_), int(f_), int(f_), E_, mblock_, stab, meta_, hbuf_, f_, INT64_MAX, 1, mbseg_,
-              nullptr, nullptr, nullptr, nullptr, 0, raster_, mbrows_};
+  const int64_t mb_ub = dep2_max_mb_;
+  const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_dep2_xperm_;
+  GemmArgs g1{int(h_), int(f_), int(f_), E_, dep2_mblock_, stab, dep2_meta_, dep2_h_, f_, INT64_MAX, 1,
+              dep2_mbseg_, nullptr, nullptr, nullptr, nullptr, 0, raster_, dep2_mbrows_};
   if (Tall > 0)
-    launch_grouped_gemm(GEMM_SWIGLU, tm_xperm_, tm_x, tm_gate_, tm_up_, g1,
+    launch_grouped_gemm(GEMM_SWIGLU, tm_dep2_xperm_, tm_x, tm_gate_, tm_up_, g1,
                         int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
   mark(&rec.k[2]);
-  GemmArgs g2{int(f_), int(h_), int(h_), E_, mblock_, stab, meta_, xperm_, h_, INT64_MAX, 0, mbseg_,
-              nullptr, nullptr, nullptr, nullptr, 0, raster_, mbrows_};
+  GemmArgs g2{int(f_), int(h_), int(h_), E_, dep2_mblock_, stab, dep2_meta_, dep2_xperm_, h_, INT64_MAX, 0,
+              dep2_mbseg_, nullptr, nullptr, nullptr, nullptr, 0, raster_, dep2_mbrows_};
   if (Tall > 0)
-    launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, tm_down_, tm_down_, g2,
+    launch_grouped_gemm(GEMM_PLAIN, tm_dep2_h_, tm_dep2_h_, tm_down_, tm_down_, g2,
                         int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
   mark(&rec.k[3]);
   // 5. partial combine per received token: sum over this rank's experts of
@@ -538,8 +572,7 @@ void Ctx::dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* 
     const int64_t o = off[size_t(r)], tr = Ts[size_t(r)];
     if (tr == 0) continue;
     uint16_t* dst = r == rank_ ? parts + int64_t(rank_) * T * h_ : dep2_x_ + o * h_;
-    launch_combine(xperm_, dep2_rowof_ + o * k_, dep2_wts_ + o * k_, nullptr, nullptr, nullptr, dst, tr, k_,
-                   h_, st);
+    launch_combine_partial(dep2_xperm_, dep2_rowof_ + o * k_, dep2_wts_ + o * k_, dst, tr, k_, h_, st);
     ++np;
   }
   mark(&rec.comm[2]);
@@ -563,11 +596,18 @@ void Ctx::dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* 
       dep2_rowf_T_ = T;
       ++np;
     }
-    launch_combine(parts, dep2_rowf_, dep2_wf_, shared_ ? xperm_ : nullptr, meta_, residual ? x : nullptr, y, T,
-                   N_, h_, st);
+    combine_into(parts, dep2_rowf_, dep2_wf_, shared_ ? dep2_xperm_ : nullptr, dep2_meta_,
+                 residual ? x : nullptr, y, T, N_, st);
   }
   // receive-side overflow flag (meta[4]) -> host, checked at the next stack
-  DWDP_CUDA(cudaMemcpyAsync(dep2_flag_host_, meta_ + 4, 4, cudaMemcpyDeviceToHost, st));
+  // sticky per rank until raised: max over the stack's layers
+  DWDP_CUDA(cudaMemcpyAsync(dep2_flag_host_ + 1, dep2_meta_ + 4, 4, cudaMemcpyDeviceToHost, st));
+  DWDP_CUDA(cudaLaunchHostFunc(
+      st, [](void* p) {
+        int32_t* f = static_cast<int32_t*>(p);
+        f[0] |= f[1];
+      },
+      dep2_flag_host_));
   launches += (T > 0 ? 3 : 0) + np + (Tall > 0 ? 2 : 0) + 1;
   DWDP_CUDA(cudaGetLastError());
   DWDP_CUDA(cudaEventRecord(rec.moe_end, st));

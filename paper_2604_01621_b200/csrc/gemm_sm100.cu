@@ -1506,6 +1506,26 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
       cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
       cudaFuncSetAttribute(grouped_gemm_kernel<kSwiGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            SMEM_BYTES);
+      {  // maximal shared-memory carveout for every GEMM (see configure_max_shared_carveout_kernels)
+        const int c = cudaSharedmemCarveoutMaxShared;
+        const void* fs[] = {
+            reinterpret_cast<const void*>(grouped_gemm_kernel<kSwiGLU>),
+            reinterpret_cast<const void*>(grouped_gemm_kernel<kPlain>),
+            reinterpret_cast<const void*>(grouped_gemm_kernel<kInt8>),
+            reinterpret_cast<const void*>(grouped_gemm_kernel<kSwiGLU8>),
+            reinterpret_cast<const void*>(grouped_gemm_kernel<kPlain8>),
+            reinterpret_cast<const void*>(grouped_gemm_kernel<kSwiGLU4>),
+            reinterpret_cast<const void*>(grouped_gemm_kernel<kPlain4>),
+            reinterpret_cast<const void*>(grouped_gemm_pair_kernel<kSwiGLU>),
+            reinterpret_cast<const void*>(grouped_gemm_pair_kernel<kPlain>),
+            reinterpret_cast<const void*>(grouped_gemm_pair_kernel<kSwiGLU8>),
+            reinterpret_cast<const void*>(grouped_gemm_pair_kernel<kPlain8>),
+            reinterpret_cast<const void*>(grouped_gemm_pair_kernel<kInt8>),
+            reinterpret_cast<const void*>(grouped_gemm_pair_fp4_kernel<kSwiGLU4>),
+            reinterpret_cast<const void*>(grouped_gemm_pair_fp4_kernel<kPlain4>),
+            reinterpret_cast<const void*>(router_gemm_kernel)};
+        for (const void* f : fs) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+      }
       cudaFuncSetAttribute(grouped_gemm_kernel<kPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            SMEM_BYTES);
       cudaFuncSetAttribute(grouped_gemm_kernel<kInt8>, cudaFuncAttributeMaxDynamicSharedMemorySize,

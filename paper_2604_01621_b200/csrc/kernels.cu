@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <stdexcept>
 #include <cstdlib>
 #include <cstdint>
 
@@ -1284,16 +1285,17 @@ __global__ void __launch_bounds__(32) permute_copy_bulk_kernel(const uint16_t* _
 }
 
 // ---------------------------------------------------------------- combine
+// resid never aliases y: the stacks ping-pong between two buffers
+// (Ctx::stack_forward), so every input is read through the non-coherent path.
+// SKIP_NEG: rows < 0 are pairs computed on another rank (DEP partial combine).
+template <bool SKIP_NEG>
 __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict__ O,
                                                       const int32_t* __restrict__ row_of,
                                                       const float* __restrict__ wts,
                                                       const uint16_t* __restrict__ S,
                                                       const int32_t* __restrict__ s_meta,
-                                                      const uint16_t* resid, uint16_t* y,
-                                                      int64_t T, int k, int64_t h) {
-  // resid and y alias when a stack runs in place (y = x + MoE(x) for layers
-  // l >= 1): no __restrict__ / non-coherent loads on them. Each thread reads
-  // its own 16-byte segment of resid before writing that segment of y.
+                                                      const uint16_t* __restrict__ resid,
+                                                      uint16_t* __restrict__ y, int64_t T, int k, int64_t h) {
   const int64_t t = blockIdx.x;
   if (t >= T) return;
   __shared__ int32_t srow[TOPK_MAXK + 1];
@@ -1317,15 +1319,17 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
     for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
     uint4 vs = make_uint4(0, 0, 0, 0), vr = make_uint4(0, 0, 0, 0);
     if (shared) vs = __ldg(reinterpret_cast<const uint4*>(S + int64_t(srow[TOPK_MAXK]) * h) + s);
-    if (resid) vr = reinterpret_cast<const uint4*>(resid + t * h)[s];
+    if (resid) vr = __ldg(reinterpret_cast<const uint4*>(resid + t * h) + s);
     for (int j0 = 0; j0 < k; j0 += CB) {
       uint4 v[CB];
 #pragma unroll
       for (int jj = 0; jj < CB; ++jj)
-        if (j0 + jj < k)  // row < 0: the pair is computed on another rank (DEP partial combine)
-          v[jj] = srow[j0 + jj] >= 0
-                      ? __ldg(reinterpret_cast<const uint4*>(O + int64_t(srow[j0 + jj]) * h) + s)
-                      : make_uint4(0, 0, 0, 0);
+        if (j0 + jj < k) {
+          if (SKIP_NEG && srow[j0 + jj] < 0)
+            v[jj] = make_uint4(0, 0, 0, 0);
+          else
+            v[jj] = __ldg(reinterpret_cast<const uint4*>(O + int64_t(srow[j0 + jj]) * h) + s);
+        }
 #pragma unroll
       for (int jj = 0; jj < CB; ++jj) {
         if (j0 + jj >= k) break;
@@ -1731,8 +1735,15 @@ void launch_quant_rows_fp8(const uint16_t* src, int64_t max_rows, int64_t K, con
 void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
                     const uint16_t* S, const int32_t* s_meta, const uint16_t* resid, uint16_t* y,
                     int64_t T, int k, int64_t h, cudaStream_t st) {
+  if (T <= 0) return;
+  if (resid == y) throw std::runtime_error("combine: resid must not alias y");
+  combine_kernel<false><<<unsigned(T), 128, 0, st>>>(O, row_of, wts, S, s_meta, resid, y, T, k, h);
+}
+
+void launch_combine_partial(const uint16_t* O, const int32_t* row_of, const float* wts, uint16_t* y, int64_t T,
+                            int k, int64_t h, cudaStream_t st) {
   if (T > 0)
-    combine_kernel<<<unsigned(T), 128, 0, st>>>(O, row_of, wts, S, s_meta, resid, y, T, k, h);
+    combine_kernel<true><<<unsigned(T), 128, 0, st>>>(O, row_of, wts, nullptr, nullptr, nullptr, y, T, k, h);
 }
 
 void launch_pull(const PullItem* items, int n, uint64_t max_len, int ctas, cudaStream_t st) {
@@ -1761,6 +1772,39 @@ void launch_pull(const PullItem* items, int n, uint64_t max_len, int ctas, cudaS
   if (n > 0)
     tma_pull_kernel<<<ctas, 32, size_t(pc.bufs) * pc.chunk, st>>>(items, n, total, uint32_t(pc.chunk),
                                                                   pc.bufs);
+}
+
+// Every kernel of the layer path asks for the maximal shared-memory carveout.
+// An SM's L1 / shared split is set by the first CTA that lands on it while it
+// is idle; CTAs of kernels with another split cannot join until it drains. The
+// one-warp pull kernel (24 KB) left to the driver's default got SMs configured
+// for small shared memory, and the 194 KB grouped-GEMM CTAs then waited for
+// the whole pull (GEMM1 11 -> 35 ms per layer at N = 4 with the pull engine).
+void configure_max_shared_carveout_kernels() {
+  const int c = cudaSharedmemCarveoutMaxShared;
+  auto set = [&](const void* f) { cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, c); };
+  set(reinterpret_cast<const void*>(tma_pull_kernel));
+  set(reinterpret_cast<const void*>(router_quant_kernel));
+  set(reinterpret_cast<const void*>(topk_kernel));
+  set(reinterpret_cast<const void*>(topk_contig_kernel<8, true>));
+  set(reinterpret_cast<const void*>(topk_contig_kernel<8, false>));
+  set(reinterpret_cast<const void*>(topk_contig_kernel<4, false>));
+  set(reinterpret_cast<const void*>(topk_contig_kernel<2, false>));
+  set(reinterpret_cast<const void*>(topk_contig_kernel<1, false>));
+  set(reinterpret_cast<const void*>(permute_count_kernel));
+  set(reinterpret_cast<const void*>(permute_scan_kernel));
+  set(reinterpret_cast<const void*>(permute_scatter_kernel));
+  set(reinterpret_cast<const void*>(permute_copy_bulk_kernel));
+  set(reinterpret_cast<const void*>(combine_kernel<false>));
+  set(reinterpret_cast<const void*>(combine_kernel<true>));
+  set(reinterpret_cast<const void*>(quant_rows_fp8_kernel));
+  set(reinterpret_cast<const void*>(quant_rows_nvfp4_kernel));
+  set(reinterpret_cast<const void*>(quant_rows_nvfp4_il_kernel<8>));
+  set(reinterpret_cast<const void*>(nvfp4_sf_relayout_kernel));
+  set(reinterpret_cast<const void*>(split_layout_kernel));
+  set(reinterpret_cast<const void*>(localize_idx_kernel));
+  set(reinterpret_cast<const void*>(rank_rows_kernel));
+  cudaGetLastError();
 }
 
 }  // namespace dwdp

@@ -129,6 +129,10 @@ void launch_quant_rows_fp8(const uint16_t* src, int64_t max_rows, int64_t K, con
 void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
                     const uint16_t* S, const int32_t* s_meta, const uint16_t* resid, uint16_t* y,
                     int64_t T, int k, int64_t h, cudaStream_t st);
+// y[t] = sum_j w[t,j] O[row_of[t,j]] over the pairs with row_of >= 0 only
+// (the DEP receive side's partial rows; no shared expert, no residual).
+void launch_combine_partial(const uint16_t* O, const int32_t* row_of, const float* wts, uint16_t* y, int64_t T,
+                            int k, int64_t h, cudaStream_t st);
 
 // One-launch P2P pull of a slice list over NVLink: work[i] = {src, dst, len}.
 struct PullItem {
@@ -141,5 +145,10 @@ void launch_pull(const PullItem* items_dev, int n_items, uint64_t max_len, int c
 
 // Grouped GEMM on tcgen05 (gemm_sm100.cu). See GemmArgs there.
 struct GroupedGemm;
+
+// Preferred shared-memory carveout = maximum for every layer-path kernel of
+// this file (so a GEMM CTA can always join an SM running a pull CTA); per
+// device, once.
+void configure_max_shared_carveout_kernels();
 
 }  // namespace dwdp

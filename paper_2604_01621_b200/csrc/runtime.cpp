@@ -3,6 +3,8 @@
 //   prefetch engine/handles — CopyEngineSim, simcore.cpp:72-283 / simcore.hpp:87-151
 //   per-rank layer loop     — simulate_dwdp MoeGate/MoeOps, simcore.cpp:640-733
 //   static transfer list    — prefetch_transfers, simcore.cpp:486-515
+#include <mutex>
+
 #include "runtime.hpp"
 
 #include <algorithm>
@@ -129,6 +131,10 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     throw CudaError("dwdp: device " + std::to_string(c.device) + " is sm_" + std::to_string(cc) +
                     "; this build targets sm_100a only");
   num_sms_ = prop.multiProcessorCount;
+  {
+    static std::once_flag carveout_once[64];
+    std::call_once(carveout_once[c.device & 63], [] { configure_max_shared_carveout_kernels(); });
+  }
   if (N_ >= 2) pl_ = build_placement(E_, N_, c.extra_redundancy);
   build_layout();
 
@@ -277,6 +283,9 @@ Ctx::~Ctx() {
                   static_cast<void*>(dep_xsf_), static_cast<void*>(dep_hsf_)})
     if (b) cudaFree(b);
   if (dep_counts_host_) cudaFreeHost(dep_counts_host_);
+  for (void* b : {static_cast<void*>(dep2_xperm_), static_cast<void*>(dep2_h_), static_cast<void*>(dep2_mblock_),
+                  static_cast<void*>(dep2_mbrows_), static_cast<void*>(dep2_mbseg_), static_cast<void*>(dep2_meta_)})
+    if (b) cudaFree(b);
   for (void* b : {static_cast<void*>(dep2_x_), static_cast<void*>(dep2_idx_), static_cast<void*>(dep2_loc_),
                   static_cast<void*>(dep2_rowof_), static_cast<void*>(dep2_wts_), static_cast<void*>(dep2_scratch_),
                   static_cast<void*>(dep2_rowf_), static_cast<void*>(dep2_wf_), static_cast<void*>(dep2_tok_)})
@@ -295,6 +304,7 @@ Ctx::~Ctx() {
   for (void* b : {static_cast<void*>(mblock2_), static_cast<void*>(mbseg2_), static_cast<void*>(mbrows2_),
                   static_cast<void*>(meta2_), static_cast<void*>(d1_), static_cast<void*>(d2_)})
     if (b) cudaFree(b);
+  if (ping_) cudaFree(ping_);
   void* bufs[] = {arena_[0], arena_[1], arena_[2], router_w_, bias_, slot_tab_, logits_, idx_,
                   wts_, row_of_, counts_, mblock_, meta_, scratch_, xperm_, hbuf_, pull_items_, pull_items_odd_,
                   router_wq_, router_we_, xq_, xe_, rC_, rmeta_, zeros_, mbseg_, mbrows_, dep_seg_, srcrow_,
@@ -809,7 +819,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     launch_grouped_gemm(GEMM_PLAIN_FP4, tm_h8_, tm_h8_, tmd4, tmd4, g2,
                         int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st, sf2);
     mark(3);
-    launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
+    combine_into(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, st);
     launches += 3 + np + 1 + 4 + 1;  // router 3, permute + relayout, GEMM1 + quant 2 + GEMM2, combine
   } else if (fp8_) {
     // W8A8: the permute writes e4m3 copies of every routed row and of the
@@ -830,7 +840,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     launch_grouped_gemm(GEMM_PLAIN_FP8, tm_h8_, tm_h8_, tmdown, tmdown, g2,
                         int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
     mark(3);
-    launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
+    combine_into(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, st);
     launches += 3 + np + 3 + 1;  // router 3, permute, GEMM1 + quant + GEMM2, combine
   } else {
   // gather_: GEMM1's producer gathers the routed rows from x (cp.async), the
@@ -875,7 +885,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, split ? tm_down_p_ : tmdown, split ? tm_down_p_ : tmdown, g2,
                       int(std::min<int64_t>(mb2_ub * (h_ / 256), 1 << 30)), st);
   mark(3);
-  launch_combine(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, h_, st);
+  combine_into(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, st);
   launches += 3 + np + 2 + 1;  // router 3, permute, GEMM1, GEMM2, combine
   }
   if (timed) {
@@ -989,9 +999,37 @@ void Ctx::release_record(const LayerRec& r) {
 
 // One iteration of the stack starts at the next global layer that is layer 0
 // (global layer g = iteration * L + l, simcore.cpp:711-728).
+uint16_t* Ctx::ping() {
+  if (!ping_) ping_ = static_cast<uint16_t*>(dalloc(size_t(max_tokens_) * h_ * 2, &workspace_bytes));
+  return ping_;
+}
+
+void Ctx::combine_into(const uint16_t* O, const int32_t* row_of, const float* wts, const uint16_t* S,
+                       const int32_t* s_meta, const uint16_t* resid, uint16_t* y, int64_t T, int k,
+                       cudaStream_t st) {
+  if (resid == nullptr || resid != y) {
+    launch_combine(O, row_of, wts, S, s_meta, resid, y, T, k, h_, st);
+    return;
+  }
+  uint16_t* tmp = ping();  // in-place call (x == y): never read and written by one kernel
+  launch_combine(O, row_of, wts, S, s_meta, resid, tmp, T, k, h_, st);
+  DWDP_CUDA(cudaMemcpyAsync(y, tmp, size_t(T) * h_ * 2, cudaMemcpyDeviceToDevice, st));
+}
+
+// Layer outputs alternate between y and the ping buffer, ending in y, so no
+// layer's residual input aliases its output (x == y is allowed: the first
+// layer then writes the ping buffer).
 void Ctx::stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t st) {
   const int64_t g0 = (cursor_ + L_ - 1) / L_ * L_;
-  for (int l = 0; l < L_; ++l) layer_forward(g0 + l, l == 0 ? x : y, T, y, true, st);
+  uint16_t* p = ping();
+  const uint16_t* in = x;
+  for (int l = 0; l < L_; ++l) {
+    uint16_t* out = ((L_ - 1 - l) % 2 == 0) ? y : p;
+    if (in == out) out = (out == y) ? p : y;  // x == y on the first layer
+    layer_forward(g0 + l, in, T, out, true, st);
+    in = out;
+  }
+  if (in != y) DWDP_CUDA(cudaMemcpyAsync(y, in, size_t(T) * h_ * 2, cudaMemcpyDeviceToDevice, st));
 }
 
 void Ctx::route(int layer, const uint16_t* x, int64_t T, int32_t* idx, float* wts,

@@ -288,12 +288,29 @@ class Ctx {
   uint8_t *dep_sfl_ = nullptr, *dep_xsf_ = nullptr, *dep_hsf_ = nullptr;
   CUtensorMap tm_dep_x8_, tm_dep_h8_;
   void dep_reserve(int64_t rows);
+  // layer-output ping-pong buffer [max_tokens][h] bf16: the stacks alternate
+  // y / ping so a layer's residual input never aliases its output
+  uint16_t* ping_ = nullptr;
+  uint16_t* ping();
+  // combine into y, or (when resid aliases y: in-place single-layer calls)
+  // into ping and copy back
+  void combine_into(const uint16_t* O, const int32_t* row_of, const float* wts, const uint16_t* S,
+                    const int32_t* s_meta, const uint16_t* resid, uint16_t* y, int64_t T, int k,
+                    cudaStream_t st);
   // DEP mode 1 buffers: all ranks' token rows (then the partial rows sent
   // back), their routing, local row_of, permute scratch, final-combine tables
   uint16_t* dep2_x_ = nullptr;
   int32_t *dep2_idx_ = nullptr, *dep2_loc_ = nullptr, *dep2_rowof_ = nullptr, *dep2_scratch_ = nullptr,
           *dep2_rowf_ = nullptr, *dep2_tok_ = nullptr, *dep2_flag_host_ = nullptr;
   float *dep2_wts_ = nullptr, *dep2_wf_ = nullptr;
+  // receive-side expert-major rows / H / m-block tables, sized for 1.3x the
+  // balanced load (routing skew across expert blocks); overflow is detected
+  // on the device and raised on every rank at the next token exchange
+  uint16_t *dep2_xperm_ = nullptr, *dep2_h_ = nullptr;
+  int32_t *dep2_mblock_ = nullptr, *dep2_mbrows_ = nullptr, *dep2_meta_ = nullptr;
+  int2* dep2_mbseg_ = nullptr;
+  int64_t dep2_cap_rows_ = 0, dep2_max_mb_ = 0;
+  CUtensorMap tm_dep2_xperm_, tm_dep2_h_;
   int64_t* dep2_tok_host_ = nullptr;
   int64_t dep2_rowf_T_ = -1;
   void dep2_alloc();
