@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../../include/dwdp.h"
+#include "kernels.hpp"
 #include "plan.hpp"
 #include "report.hpp"
 #include "runtime.hpp"
@@ -618,7 +619,10 @@ int dwdp_ctx_set_engine(dwdp_ctx* c, int engine) {
   return guard([&] {
     dwdp::require(engine == DWDP_ENGINE_COPY || engine == DWDP_ENGINE_PULL || engine == DWDP_ENGINE_HYBRID,
                   "ctx: unknown engine");
-    C(c).cfg.engine = engine;
+    auto& ctx = C(c);
+    ctx.cfg.engine = engine;
+    cudaSetDevice(ctx.cfg.device);
+    dwdp::configure_max_shared_carveout_kernels(ctx.cfg.group_size > 1 && engine != DWDP_ENGINE_COPY);
   });
 }
 

@@ -1774,16 +1774,21 @@ void launch_pull(const PullItem* items, int n, uint64_t max_len, int ctas, cudaS
                                                                   pc.bufs);
 }
 
-// Every kernel of the layer path asks for the maximal shared-memory carveout.
-// An SM's L1 / shared split is set by the first CTA that lands on it while it
-// is idle; CTAs of kernels with another split cannot join until it drains. The
-// one-warp pull kernel (24 KB) left to the driver's default got SMs configured
-// for small shared memory, and the 194 KB grouped-GEMM CTAs then waited for
-// the whole pull (GEMM1 11 -> 35 ms per layer at N = 4 with the pull engine).
-void configure_max_shared_carveout_kernels() {
-  const int c = cudaSharedmemCarveoutMaxShared;
+// Shared-memory carveout of the layer-path kernels. An SM's L1 / shared split
+// is set by the first CTA that lands on it while it is idle; CTAs needing
+// more shared memory cannot join until it drains. With an SM pull engine
+// running beside the layer (N > 1, pull / hybrid), a pull CTA resident on an
+// SM configured by a small kernel kept the 194 KB grouped-GEMM CTAs off it
+// for the whole pull (GEMM1 11 -> 35 ms per layer at N = 4): then every
+// layer-path kernel asks for the maximal carveout. Otherwise only the pull
+// kernel does, and the small kernels keep the driver's choice -- the maximal
+// carveout shrinks L1 and slowed the combine 1.47 -> 1.87 ms per layer
+// (profiles/r2_ab_carveout.jsonl).
+void configure_max_shared_carveout_kernels(bool all) {
+  const int c = all ? int(cudaSharedmemCarveoutMaxShared) : int(cudaSharedmemCarveoutDefault);
   auto set = [&](const void* f) { cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, c); };
-  set(reinterpret_cast<const void*>(tma_pull_kernel));
+  cudaFuncSetAttribute(reinterpret_cast<const void*>(tma_pull_kernel),
+                       cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared));
   set(reinterpret_cast<const void*>(router_quant_kernel));
   set(reinterpret_cast<const void*>(topk_kernel));
   set(reinterpret_cast<const void*>(topk_contig_kernel<8, true>));

@@ -146,9 +146,10 @@ void launch_pull(const PullItem* items_dev, int n_items, uint64_t max_len, int c
 // Grouped GEMM on tcgen05 (gemm_sm100.cu). See GemmArgs there.
 struct GroupedGemm;
 
-// Preferred shared-memory carveout = maximum for every layer-path kernel of
-// this file (so a GEMM CTA can always join an SM running a pull CTA); per
-// device, once.
-void configure_max_shared_carveout_kernels();
+// Preferred shared-memory carveout of this file's layer-path kernels: maximal
+// for all of them (`all`: an SM pull engine runs beside the layer, so a GEMM
+// CTA must always be able to join an SM holding a pull CTA), else maximal for
+// the pull kernel only.
+void configure_max_shared_carveout_kernels(bool all);
 
 }  // namespace dwdp

@@ -131,10 +131,7 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     throw CudaError("dwdp: device " + std::to_string(c.device) + " is sm_" + std::to_string(cc) +
                     "; this build targets sm_100a only");
   num_sms_ = prop.multiProcessorCount;
-  {
-    static std::once_flag carveout_once[64];
-    std::call_once(carveout_once[c.device & 63], [] { configure_max_shared_carveout_kernels(); });
-  }
+  configure_max_shared_carveout_kernels(N_ > 1 && c.engine != DWDP_ENGINE_COPY);
   if (N_ >= 2) pl_ = build_placement(E_, N_, c.extra_redundancy);
   build_layout();
 
