@@ -486,8 +486,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, int mb, int nb,
   }
 }
 
+// At most 232 registers per thread: two GEMM warps per SM sub-partition
+// (2 x 32 x 232 of its 16K registers) leave room for the 32-thread pull
+// kernel's warp (36 registers) beside the GEMM CTA. At 238 (the compiler's
+// free choice) the pull CTAs and the GEMM could not co-reside and GEMM1 waited
+// for the whole pull (11 -> 27-35 ms per layer with the pull engine).
 template <int MODE>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __maxnreg__(232)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmA2,
                         const __grid_constant__ CUtensorMap tmB0,

@@ -50,7 +50,9 @@ class Mla {
     T_ = c.max_tokens;
     kva_ld_ = (c.kv_lora + c.rope + 255) / 256 * 256;
     max_tiles_ = T_ / 128 + T_ + 1;  // one partial tile per sequence at most
-    ldv_ = (T_ + 64 * (max_tiles_ + 1) + 7) / 8 * 8;  // every sequence's V^T columns start 64-aligned
+    // every sequence's V^T columns start 64-aligned: room for 64 sequences'
+    // padding up front, grown on demand (forward) for more, shorter ones
+    ldv_ = (T_ + 64 * 64 + 7) / 8 * 8;
     auto alloc = [&](size_t bytes) {
       void* p = nullptr;
       DWDP_CUDA(cudaMalloc(&p, bytes));
@@ -64,7 +66,7 @@ class Mla {
     ckv_ = alloc(size_t(T_) * c.kv_lora * 2);
     kv_ = alloc(size_t(T_) * H_ * 256 * 2);
     k_ = alloc(size_t(T_) * H_ * 192 * 2);
-    vt_ = alloc(size_t(H_) * 128 * ldv_ * 2);
+    DWDP_CUDA(cudaMalloc(reinterpret_cast<void**>(&vt_), size_t(H_) * 128 * ldv_ * 2));
     o_ = alloc(size_t(T_) * H_ * 128 * 2);
     pos_ = reinterpret_cast<int32_t*>(alloc(size_t(2 * T_) * 4));  // positions, then V^T columns
     tiles_ = reinterpret_cast<AttnTile*>(alloc(size_t(max_tiles_) * sizeof(AttnTile)));
@@ -75,6 +77,7 @@ class Mla {
   ~Mla() {
     cudaDeviceSynchronize();
     for (void* p : bufs_) cudaFree(p);
+    if (vt_) cudaFree(vt_);
     if (pos_h_) cudaFreeHost(pos_h_);
     if (tiles_h_) cudaFreeHost(tiles_h_);
     if (staged_) cudaEventDestroy(staged_);
@@ -107,7 +110,11 @@ class Mla {
       s0 += L;
       v0 += (L + 63) / 64 * 64;
     }
-    require(v0 <= ldv_, "mla: V^T columns exceed the workspace");
+    if (v0 > ldv_) {  // many short sequences: grow V^T (cudaFree synchronises)
+      cudaFree(vt_);
+      ldv_ = (v0 + 4096 + 7) / 8 * 8;
+      DWDP_CUDA(cudaMalloc(reinterpret_cast<void**>(&vt_), size_t(H_) * 128 * ldv_ * 2));
+    }
     std::stable_sort(tl.begin(), tl.end(), [](const AttnTile& a, const AttnTile& b) {
       return std::min(a.q0 + 128, a.len) > std::min(b.q0 + 128, b.len);
     });
