@@ -418,9 +418,11 @@ def main():
     attention = None
     if attn is not None:
         a_ms = sum(a0.elapsed_time(a1) for a0, a1 in attn_ev)
-        attention = {"block": "DeepSeek-V3 MLA prefill (q_lora 1536, kv_lora 512, 128 heads, qk 128+64, v 128), "
-                              "library ops: cuBLAS GEMMs + FlashAttention-2, causal, rank tokens split into "
-                              "RankBatch::requests sequences",
+        attention = {"block": "DeepSeek-V3 MLA prefill (q_lora 1536, kv_lora 512, 128 heads, qk 128+64, v 128) "
+                              + ("on sm_100a kernels (dwdp_mla_forward: tcgen05 projections, tcgen05 causal "
+                                 "flash attention)" if attn.backend == "native" else
+                                 "from library ops (cuBLAS GEMMs + FlashAttention-2)")
+                              + ", causal, rank tokens split into RankBatch::requests sequences",
                      "ms_per_layer": a_ms / max(len(attn_ev), 1),
                      "tflops": attn_flops[0] / (a_ms * 1e-3) / 1e12 if a_ms else None}
     ms = allmax(ms_local)
