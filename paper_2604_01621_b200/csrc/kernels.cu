@@ -879,8 +879,10 @@ __global__ void __launch_bounds__(256) router_quant_kernel(const uint16_t* __res
   const int64_t nch = K / 8;
   extern __shared__ uint4 rq_rows[];  // [warps per block][nch] when staged
   if (staged) {  // one HBM read: pass 1 stages the row in smem, pass 2 quantises from it
+    // Pass 1: the row's largest magnitude (sign-cleared bf16 bits order like
+    // the values) gives the exponent field emax, two elements per __vmaxu2.
     uint4* srow = rq_rows + (threadIdx.x >> 5) * nch;
-    int m = 0;
+    uint32_t mx = 0;
     for (int64_t c0 = lane; c0 < nch; c0 += 32 * RQ_UNROLL) {
       uint4 v[RQ_UNROLL];
 #pragma unroll
@@ -892,36 +894,43 @@ __global__ void __launch_bounds__(256) router_quant_kernel(const uint16_t* __res
       for (int u = 0; u < RQ_UNROLL; ++u) {
         const int64_t c = c0 + 32 * u;
         if (c < nch) srow[c] = v[u];
-        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          int mant, eb;
-          bf16_fields((w[q >> 1] >> (16 * (q & 1))) & 0xFFFFu, mant, eb);
-          if (mant && eb > m) m = eb;
-        }
+        mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(v[u].x & 0x7FFF7FFFu, v[u].y & 0x7FFF7FFFu),
+                                   __vmaxu2(v[u].z & 0x7FFF7FFFu, v[u].w & 0x7FFF7FFFu)));
       }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (m == 0) m = 1;
+    for (int o = 16; o > 0; o >>= 1) mx = __vmaxu2(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const uint32_t top = max(mx & 0xFFFFu, mx >> 16);
+    const int m = top ? max(int(top >> 7), 1) : 1;  // = max over nonzero elements of max(E, 1)
+    // Pass 2: Q = trunc(x * 2^(148 - emax)) (exact: a bf16 times a power of
+    // two; |Q| < 2^22), digits of Q = d0 + 2^8 d1 + 2^16 d2 in [-128, 127]:
+    // Q1 = (Q + 128) >> 8, Q2 = (Q1 + 128) >> 8, digits = their low bytes.
+    const int kx = 148 - m;  // in [-106, 147]: beyond 127 split into 2^64 * 2^(kx-64)
+    const float s1 = __int_as_float(((kx > 127 ? 64 : kx) + 127) << 23);
+    const float s2 = kx > 127 ? __int_as_float((kx - 64 + 127) << 23) : 1.0f;
+    __syncwarp();
     for (int64_t c = lane; c < nch; c += 32) {
       const uint4 v = srow[c];
       const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-      uint32_t p0[2] = {0, 0}, p1[2] = {0, 0}, p2[2] = {0, 0};
+      uint32_t p[3][2];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int Q = fixed22((w[q >> 1] >> (16 * (q & 1))) & 0xFFFFu, m);
-        const int d0 = int(int8_t(uint8_t(Q & 0xFF)));
-        const int Q1 = (Q - d0) >> 8;
-        const int d1 = int(int8_t(uint8_t(Q1 & 0xFF)));
-        const int d2 = (Q1 - d1) >> 8;
-        p0[q >> 2] |= uint32_t(uint8_t(d0)) << (8 * (q & 3));
-        p1[q >> 2] |= uint32_t(uint8_t(d1)) << (8 * (q & 3));
-        p2[q >> 2] |= uint32_t(uint8_t(d2)) << (8 * (q & 3));
+      for (int hw = 0; hw < 2; ++hw) {  // two words = four elements per packed plane word
+        int q0[4], q1[4], q2[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t word = w[2 * hw + (e >> 1)];
+          const float f = __uint_as_float((e & 1) ? (word & 0xFFFF0000u) : (word << 16));
+          q0[e] = __float2int_rz(__fmul_rn(__fmul_rn(f, s1), s2));
+          q1[e] = (q0[e] + 128) >> 8;
+          q2[e] = (q1[e] + 128) >> 8;
+        }
+        p[0][hw] = __byte_perm(__byte_perm(q0[0], q0[1], 0x40), __byte_perm(q0[2], q0[3], 0x40), 0x5410);
+        p[1][hw] = __byte_perm(__byte_perm(q1[0], q1[1], 0x40), __byte_perm(q1[2], q1[3], 0x40), 0x5410);
+        p[2][hw] = __byte_perm(__byte_perm(q2[0], q2[1], 0x40), __byte_perm(q2[2], q2[3], 0x40), 0x5410);
       }
-      *reinterpret_cast<uint2*>(dst + (0 * R + r) * K + c * 8) = make_uint2(p0[0], p0[1]);
-      *reinterpret_cast<uint2*>(dst + (1 * R + r) * K + c * 8) = make_uint2(p1[0], p1[1]);
-      *reinterpret_cast<uint2*>(dst + (2 * R + r) * K + c * 8) = make_uint2(p2[0], p2[1]);
+      *reinterpret_cast<uint2*>(dst + (0 * R + r) * K + c * 8) = make_uint2(p[0][0], p[0][1]);
+      *reinterpret_cast<uint2*>(dst + (1 * R + r) * K + c * 8) = make_uint2(p[1][0], p[1][1]);
+      *reinterpret_cast<uint2*>(dst + (2 * R + r) * K + c * 8) = make_uint2(p[2][0], p[2][1]);
     }
     if (lane == 0) emax[r] = m;
     return;
