@@ -20,14 +20,21 @@
 //               64-key tile K (3 boxes) and V^T (one [128 dv][64 keys] box)
 //               into a 3-stage ring
 //   warp 1      MMA issuer: S_j = Q K_j^T (tcgen05 kind::f16, M128 N64 K192
-//               into TMEM, double-buffered), then O_j = P_{j-1} V_{j-1}
-//               (M128 N128 K64, double-buffered), one elected thread
-//   warp 2      TMEM allocator (512 columns: S0 S1 | O0 | O1)
-//   warps 4-7   softmax + epilogue, one query row per thread (TMEM lane):
-//               tcgen05.ld S, scale + causal mask, online softmax in exp2
-//               form, P (bf16) into the SWIZZLE_128B smem tile the next MMA
-//               reads as its A operand, and O_acc = O_acc * alpha + O_j in
-//               registers; finally O_acc / l stored as bf16.
+//               into TMEM, double-buffered), then O += P_{j-1} V_{j-1}
+//               (M128 N128 K64) into ONE TMEM accumulator, one elected thread
+//   warp 2      TMEM allocator (256 columns: S0 S1 | O)
+//   warps 4-11  softmax + epilogue, one query row per thread pair (TMEM lane),
+//               each warp of a pair on 32 of the 64 S columns:
+//               tcgen05.ld S, causal mask (diagonal tiles only), online
+//               softmax in exp2 form against a LAZY reference max m_ref,
+//               P (bf16) into the SWIZZLE_128B smem tile the next MMA reads
+//               as its A operand. O never leaves TMEM until the epilogue:
+//               P = exp2(s - m_ref) is only rescaled when a row's max
+//               grows by more than 2^8 over m_ref (then the warp waits for
+//               the previous PV, multiplies its O rows in TMEM by
+//               alpha = exp2(m_ref - m_new) with tcgen05.ld/st, and moves
+//               m_ref) -- P <= 2^8 stays exact in bf16 scaling terms and the
+//               fp32 accumulator has the range. Epilogue: O / l as bf16.
 // K_j's stage is released by the commit after the PV MMA of tile j, so the
 // softmax of tile j overlaps S_{j+1} and PV_{j-1} on the tensor core.
 #include <cuda.h>
@@ -52,13 +59,17 @@ constexpr int Q_BYTES = 3 * Q_BOX;   // 48 KB
 constexpr int K_BYTES = 3 * K_BOX;   // 24 KB
 constexpr int V_BYTES = DV * AK * 2; // 16 KB
 constexpr int P_BYTES = AQ * AK * 2; // 16 KB
-constexpr int ATT_SMEM = 1024 + Q_BYTES + KVS * (K_BYTES + V_BYTES) + 2 * P_BYTES + 256;
+constexpr int XCH_BYTES = 2 * 2 * AQ * 4;  // row-max exchange between the two column halves, per tile parity
+constexpr int ATT_THREADS = 384;
+constexpr int ATT_SMEM = 1024 + Q_BYTES + KVS * (K_BYTES + V_BYTES) + 2 * P_BYTES + XCH_BYTES + 256;
 // kind::f16 instruction descriptors, K-major A and B, bf16 in, fp32 out
 constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(AK >> 3) << 17) |
                              (uint32_t(AQ >> 4) << 24);
 constexpr uint32_t IDESC_O = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(DV >> 3) << 17) |
                              (uint32_t(AQ >> 4) << 24);
-constexpr uint32_t TM_S = 0, TM_O = 128;  // S buffers at 0 / 64, O buffers at 128 / 256
+constexpr int SB = 3;                      // S buffers: S_{j+2} is issued while softmax(j) runs
+constexpr uint32_t TM_S = 0, TM_O = 256;  // S buffers at 0 / 64 / 128, the O accumulator at 256
+constexpr float RESCALE_LOG2 = 8.0f;      // lazy rescale threshold (log2 units)
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -118,13 +129,43 @@ __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr)
       : "memory");
 }
+__device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void sts(float* p, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(su32(p)), "f"(v) : "memory");
+}
+__device__ __forceinline__ float lds(const float* p) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(su32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\nselp.u32 %0, 1, 0, e;\n}" : "=r"(p));
+  return p != 0;
+}
 __device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ uint32_t pack2(float a, float b) {
-  return uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(a))) |
-         (uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(b))) << 16);
+__device__ __forceinline__ uint32_t pack2(float a, float b) {  // one F2FP.BF16.F32.PACK_AB
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
 }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(ATT_THREADS, 1)
     mla_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const AttnTile* __restrict__ tiles,
                     uint16_t* __restrict__ out, int H, float scale_log2) {
@@ -133,16 +174,18 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sK = sQ + Q_BYTES;
   uint8_t* sV = sK + KVS * K_BYTES;
   uint8_t* sP = sV + KVS * V_BYTES;
-  uint64_t* q_full = reinterpret_cast<uint64_t*>(sP + 2 * P_BYTES);
-  uint64_t* kv_full = q_full + 1;
-  uint64_t* kv_empty = kv_full + KVS;
-  uint64_t* s_full = kv_empty + KVS;
-  uint64_t* s_empty = s_full + 2;
-  uint64_t* p_full = s_empty + 2;
+  float* xch = reinterpret_cast<float*>(sP + 2 * P_BYTES);  // [tile parity][half][row]
+  uint64_t* q_full = reinterpret_cast<uint64_t*>(sP + 2 * P_BYTES + XCH_BYTES);
+  uint64_t* k_full = q_full + 1;  // K and V rings: a K stage is free once S_j is done, a V stage after PV_j
+  uint64_t* k_empty = k_full + KVS;
+  uint64_t* v_full = k_empty + KVS;
+  uint64_t* v_empty = v_full + KVS;
+  uint64_t* s_full = v_empty + KVS;
+  uint64_t* s_empty = s_full + SB;
+  uint64_t* p_full = s_empty + SB;
   uint64_t* p_empty = p_full + 2;
   uint64_t* o_full = p_empty + 2;
-  uint64_t* o_empty = o_full + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_empty + 2);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 1);
 
   const AttnTile tile = tiles[blockIdx.x];
   const int head = blockIdx.y;
@@ -152,17 +195,20 @@ __global__ void __launch_bounds__(256, 1)
   if (threadIdx.x == 0) {
     bar_init(q_full, 1);
     for (int s = 0; s < KVS; ++s) {
-      bar_init(&kv_full[s], 1);
-      bar_init(&kv_empty[s], 1);
+      bar_init(&k_full[s], 1);
+      bar_init(&k_empty[s], 1);
+      bar_init(&v_full[s], 1);
+      bar_init(&v_empty[s], 1);
+    }
+    for (int b = 0; b < SB; ++b) {
+      bar_init(&s_full[b], 1);
+      bar_init(&s_empty[b], 8);
     }
     for (int b = 0; b < 2; ++b) {
-      bar_init(&s_full[b], 1);
-      bar_init(&s_empty[b], 4);
-      bar_init(&p_full[b], 4);
+      bar_init(&p_full[b], 8);
       bar_init(&p_empty[b], 1);
-      bar_init(&o_full[b], 1);
-      bar_init(&o_empty[b], 4);
     }
+    bar_init(o_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -182,38 +228,31 @@ __global__ void __launch_bounds__(256, 1)
       for (int a = 0; a < 3; ++a) tma3(sQ + a * Q_BOX, &tmQ, q_full, a * 64, head, tile.start + tile.q0);
       for (int j = 0; j < nt; ++j) {
         const int s = j % KVS;
-        bar_wait(&kv_empty[s], ((j / KVS) & 1) ^ 1);
-        bar_expect(&kv_full[s], K_BYTES + V_BYTES);
+        bar_wait(&k_empty[s], ((j / KVS) & 1) ^ 1);
+        bar_expect(&k_full[s], K_BYTES);
         for (int a = 0; a < 3; ++a)
-          tma3(sK + s * K_BYTES + a * K_BOX, &tmK, &kv_full[s], a * 64, head, tile.start + j * AK);
-        tma3(sV + s * V_BYTES, &tmV, &kv_full[s], tile.vstart + j * AK, 0, head);
+          tma3(sK + s * K_BYTES + a * K_BOX, &tmK, &k_full[s], a * 64, head, tile.start + j * AK);
+        bar_wait(&v_empty[s], ((j / KVS) & 1) ^ 1);
+        bar_expect(&v_full[s], V_BYTES);
+        tma3(sV + s * V_BYTES, &tmV, &v_full[s], tile.vstart + j * AK, 0, head);
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ------------------------------------------------ MMA issuer
-      bar_wait(q_full, 0);
+  } else if (warp == 1) {  // ------------------------------------------ MMA issuer
+    // The whole warp runs the schedule (waits, descriptor arithmetic) so the
+    // operands are warp-uniform and live in uniform registers; one elected
+    // lane issues. (With a lane-0-only branch ptxas wrapped every
+    // tcgen05.mma in an R2UR/ELECT loop, ~40 issue cycles per 32-cycle
+    // M128 N64 K16 MMA -- the issuing thread, not the tensor pipe, set the pace.)
+    bar_wait(q_full, 0);
+    fence_after();
+    const uint64_t qd = desc(su32(sQ));
+    auto qk = [&](int j) {  // S_j = Q K_j^T into S buffer j % SB
+      const int b = j % SB, s = j % KVS;
+      bar_wait(&s_empty[b], ((j / SB) & 1) ^ 1);
+      bar_wait(&k_full[s], (j / KVS) & 1);
       fence_after();
-      const uint64_t qd = desc(su32(sQ));
-      auto pv = [&](int i) {  // O_i = P_i V_i into O buffer i % 2
-        const int b = i & 1;
-        bar_wait(&p_full[b], (i >> 1) & 1);
-        bar_wait(&o_empty[b], ((i >> 1) & 1) ^ 1);
-        fence_after();
-        const uint64_t pd = desc(su32(sP + b * P_BYTES));
-        const uint64_t vd = desc(su32(sV + (i % KVS) * V_BYTES));
-#pragma unroll
-        for (int k = 0; k < 4; ++k)  // 16 keys (32 bytes) per MMA
-          mma(tmem + TM_O + uint32_t(b) * DV, pd + 2 * k, vd + 2 * k, IDESC_O, k != 0);
-        commit(&o_full[b]);
-        commit(&kv_empty[i % KVS]);
-        commit(&p_empty[b]);
-      };
-      for (int j = 0; j < nt; ++j) {
-        const int b = j & 1, s = j % KVS;
-        bar_wait(&s_empty[b], ((j >> 1) & 1) ^ 1);
-        bar_wait(&kv_full[s], (j / KVS) & 1);
-        fence_after();
-        const uint64_t kd = desc(su32(sK + s * K_BYTES));
+      const uint64_t kd = desc(su32(sK + s * K_BYTES));
+      if (elect_one()) {
 #pragma unroll
         for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -221,86 +260,149 @@ __global__ void __launch_bounds__(256, 1)
             mma(tmem + TM_S + uint32_t(b) * AK, qd + uint64_t(a * (Q_BOX >> 4)) + 2 * k,
                 kd + uint64_t(a * (K_BOX >> 4)) + 2 * k, IDESC_S, (a | k) != 0);
         commit(&s_full[b]);
-        if (j >= 1) pv(j - 1);
+        commit(&k_empty[s]);
       }
-      pv(nt - 1);
+      __syncwarp();
+    };
+    auto pv = [&](int i) {  // O += P_i V_i
+      const int b = i & 1, s = i % KVS;
+      bar_wait(&p_full[b], (i >> 1) & 1);
+      bar_wait(&v_full[s], (i / KVS) & 1);
+      fence_after();
+      const uint64_t pd = desc(su32(sP + b * P_BYTES));
+      const uint64_t vd = desc(su32(sV + s * V_BYTES));
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // 16 keys (32 bytes) per MMA
+          mma(tmem + TM_O, pd + 2 * k, vd + 2 * k, IDESC_O, (i | k) != 0);
+        commit(&v_empty[s]);
+        commit(&p_empty[b]);
+      }
+      __syncwarp();
+    };
+    // S runs two tiles ahead of PV: S_{j+2} is issued right after PV_{j-1},
+    // so the tensor pipe has QK^T work while softmax(j) is still running
+    qk(0);
+    if (nt > 1) qk(1);
+    for (int j = 0; j < nt; ++j) {
+      if (j + 2 < nt) qk(j + 2);
+      pv(j);
     }
+    if (elect_one()) commit(o_full);
+    __syncwarp();
   } else if (warp >= 4) {  // -------------------------------------------- softmax + epilogue
-    const int q = warp & 3, row = q * 32 + lane;
+    // warps 4-7 take S columns [0, 32) of the TMEM lanes (warp % 4) * 32 ..,
+    // warps 8-11 columns [32, 64) of the same lanes: two warps per SM
+    // sub-partition hide each other's latency. The pair agrees on the row max
+    // through xch + a named barrier per lane quarter; each owns half of O.
+    const int q = warp & 3, hf = (warp - 4) >> 2, row = q * 32 + lane;
     const int qi = tile.q0 + row;  // query position in its sequence
     const uint32_t lb = uint32_t(q * 32) << 16;
-    float m = -INFINITY, l = 0.0f, alpha_prev = 0.0f;
-    float o[DV];
+    constexpr int HC = AK / 2, HO = DV / 2;
+    float m_ref = -INFINITY, l = 0.0f;  // l = sum of exp2(s - m_ref) over this half's keys
+    for (int j = 0; j < nt; ++j) {
+      const int b = j & 1, sb = j % SB;
+      bar_wait(&s_full[sb], (j / SB) & 1);
+      fence_after();
+      uint32_t r[HC];
+      ld32(tmem + lb + TM_S + uint32_t(sb) * AK + uint32_t(hf * HC), r);
+      ld_wait();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(&s_empty[sb]);
+      float sv[HC];
+      const int k0 = j * AK + hf * HC;
+      float m0 = -INFINITY, m1 = -INFINITY;
+      if (k0 + HC - 1 <= tile.q0) {  // all keys at or below every row's diagonal: no mask
 #pragma unroll
-    for (int d = 0; d < DV; ++d) o[d] = 0.0f;
-    for (int j = 0; j <= nt; ++j) {
-      float alpha = 0.0f;
-      if (j < nt) {
-        const int b = j & 1;
-        bar_wait(&s_full[b], (j >> 1) & 1);
-        fence_after();
-        uint32_t r0[32], r1[32];
-        ld32(tmem + lb + TM_S + uint32_t(b) * AK, r0);
-        ld32(tmem + lb + TM_S + uint32_t(b) * AK + 32, r1);
-        ld_wait();
-        fence_before();
-        __syncwarp();
-        if (lane == 0) bar_arrive(&s_empty[b]);
-        float sv[AK];
-        float mx = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < AK; ++c) {
-          const float v = __uint_as_float(c < 32 ? r0[c] : r1[c - 32]) * scale_log2;
-          sv[c] = (j * AK + c <= qi) ? v : -INFINITY;  // causal (keys past the sequence are > qi)
-          mx = fmaxf(mx, sv[c]);
+        for (int c = 0; c < HC; c += 2) {
+          sv[c] = __uint_as_float(r[c]);
+          sv[c + 1] = __uint_as_float(r[c + 1]);
+          m0 = fmaxf(m0, sv[c]);
+          m1 = fmaxf(m1, sv[c + 1]);
         }
-        const float m_new = fmaxf(m, mx);
-        alpha = exp2f(m - m_new);
-        float sum = 0.0f;
+      } else {
 #pragma unroll
-        for (int c = 0; c < AK; ++c) {
-          sv[c] = exp2f(sv[c] - m_new);
-          sum += sv[c];
+        for (int c = 0; c < HC; c += 2) {  // causal (keys past the sequence are > qi)
+          sv[c] = (k0 + c <= qi) ? __uint_as_float(r[c]) : -INFINITY;
+          sv[c + 1] = (k0 + c + 1 <= qi) ? __uint_as_float(r[c + 1]) : -INFINITY;
+          m0 = fmaxf(m0, sv[c]);
+          m1 = fmaxf(m1, sv[c + 1]);
         }
-        l = l * alpha + sum;
-        m = m_new;
-        // P row (bf16, 128 B) into the SWIZZLE_128B tile: chunk c of row r at c ^ (r % 8)
-        bar_wait(&p_empty[b], ((j >> 1) & 1) ^ 1);
-        uint8_t* prow = sP + b * P_BYTES + (row >> 3) * 1024 + (row & 7) * 128;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) << 4)) =
-              make_uint4(pack2(sv[8 * c], sv[8 * c + 1]), pack2(sv[8 * c + 2], sv[8 * c + 3]),
-                         pack2(sv[8 * c + 4], sv[8 * c + 5]), pack2(sv[8 * c + 6], sv[8 * c + 7]));
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) bar_arrive(&p_full[b]);
       }
-      if (j >= 1) {  // O_acc = O_acc * alpha_{j-1} + O_{j-1}
-        const int i = j - 1, b = i & 1;
-        bar_wait(&o_full[b], (i >> 1) & 1);
+      float mx = fmaxf(m0, m1);
+      sts(xch + (b * 2 + hf) * AQ + row, mx);
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");
+      mx = fmaxf(mx, lds(xch + (b * 2 + (hf ^ 1)) * AQ + row)) * scale_log2;
+      const bool grow = mx > m_ref + RESCALE_LOG2;  // identical in both halves
+      if (j == 0) {
+        m_ref = mx;  // key 0 is visible to every row: finite
+      } else if (__any_sync(0xffffffffu, grow)) {
+        // rescale this warp's half of its O rows in TMEM once PV_{j-1} (and
+        // so every earlier PV) has completed; PV_j waits for p_full below
+        const float alpha = grow ? ex2(m_ref - mx) : 1.0f;
+        if (grow) {
+          l *= alpha;
+          m_ref = mx;
+        }
+        bar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);
         fence_after();
 #pragma unroll
-        for (int ch = 0; ch < DV / 32; ++ch) {
-          uint32_t r[32];
-          ld32(tmem + lb + TM_O + uint32_t(b) * DV + uint32_t(ch * 32), r);
+        for (int ch = 0; ch < HO / 32; ++ch) {
+          uint32_t o[32];
+          ld32(tmem + lb + TM_O + uint32_t(hf * HO + ch * 32), o);
           ld_wait();
 #pragma unroll
-          for (int x = 0; x < 32; ++x) o[ch * 32 + x] = o[ch * 32 + x] * alpha_prev + __uint_as_float(r[x]);
+          for (int x = 0; x < 32; ++x) o[x] = __float_as_uint(__uint_as_float(o[x]) * alpha);
+          st32(tmem + lb + TM_O + uint32_t(hf * HO + ch * 32), o);
         }
-        fence_before();
-        __syncwarp();
-        if (lane == 0) bar_arrive(&o_empty[b]);
+        st_wait();
       }
-      alpha_prev = alpha;
-    }
-    if (qi < tile.len) {
-      const float inv = 1.0f / l;
-      uint4* dst = reinterpret_cast<uint4*>(out + (int64_t(tile.start + qi) * H + head) * DV);
+      const float nm = -m_ref;
+      float s0 = 0.0f, s1 = 0.0f;
 #pragma unroll
-      for (int c = 0; c < DV / 8; ++c)
-        dst[c] = make_uint4(pack2(o[8 * c] * inv, o[8 * c + 1] * inv), pack2(o[8 * c + 2] * inv, o[8 * c + 3] * inv),
-                            pack2(o[8 * c + 4] * inv, o[8 * c + 5] * inv), pack2(o[8 * c + 6] * inv, o[8 * c + 7] * inv));
+      for (int c = 0; c < HC; c += 2) {
+        sv[c] = ex2(fmaf(sv[c], scale_log2, nm));
+        sv[c + 1] = ex2(fmaf(sv[c + 1], scale_log2, nm));
+        s0 += sv[c];
+        s1 += sv[c + 1];
+      }
+      l += s0 + s1;
+      // this half's 64 bytes of the P row into the SWIZZLE_128B tile: chunk c of row r at c ^ (r % 8)
+      bar_wait(&p_empty[b], ((j >> 1) & 1) ^ 1);
+      uint8_t* prow = sP + b * P_BYTES + (row >> 3) * 1024 + (row & 7) * 128;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4*>(prow + (((hf * 4 + c) ^ (row & 7)) << 4)) =
+            make_uint4(pack2(sv[8 * c], sv[8 * c + 1]), pack2(sv[8 * c + 2], sv[8 * c + 3]),
+                       pack2(sv[8 * c + 4], sv[8 * c + 5]), pack2(sv[8 * c + 6], sv[8 * c + 7]));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(&p_full[b]);
+    }
+    // row sum over both halves (the exchange slot of parity nt & 1 is free:
+    // both halves passed the barrier of tile nt - 1, which used the other)
+    sts(xch + ((nt & 1) * 2 + hf) * AQ + row, l);
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");
+    l += lds(xch + ((nt & 1) * 2 + (hf ^ 1)) * AQ + row);
+    bar_wait(o_full, 0);
+    fence_after();
+    const float inv = 1.0f / l;
+    uint4* dst = reinterpret_cast<uint4*>(out + (int64_t(tile.start + qi) * H + head) * DV + hf * HO);
+#pragma unroll
+    for (int ch = 0; ch < HO / 32; ++ch) {
+      uint32_t o[32];
+      ld32(tmem + lb + TM_O + uint32_t(hf * HO + ch * 32), o);
+      ld_wait();
+      if (qi < tile.len) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float* f = reinterpret_cast<const float*>(&o[8 * c]);
+          dst[ch * 4 + c] = make_uint4(pack2(f[0] * inv, f[1] * inv), pack2(f[2] * inv, f[3] * inv),
+                                       pack2(f[4] * inv, f[5] * inv), pack2(f[6] * inv, f[7] * inv));
+        }
+      }
     }
   }
   fence_before();
@@ -416,7 +518,7 @@ void launch_mla_attention(const uint16_t* q, const uint16_t* k, const uint16_t* 
   const int64_t dv[3] = {ldv, DV, H}, sv[2] = {ldv * 2, int64_t(DV) * ldv * 2};
   const int bv[3] = {AK, DV, 1};
   const CUtensorMap tv = make_tmap_3d_bf16(vt, dv, sv, bv);
-  mla_attn_kernel<<<dim3(unsigned(ntiles), unsigned(H)), 256, ATT_SMEM, st>>>(
+  mla_attn_kernel<<<dim3(unsigned(ntiles), unsigned(H)), ATT_THREADS, ATT_SMEM, st>>>(
       tq, tk, tv, tiles, out, H, softmax_scale * 1.4426950408889634f);
 }
 
