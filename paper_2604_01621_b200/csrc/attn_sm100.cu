@@ -52,23 +52,25 @@
 namespace dwdp {
 namespace {
 
-constexpr int AQ = 128, AK = 64, DQK = 192, DV = 128, KVS = 3;
+constexpr int AQ = 128, AK = 64, DQK = 192, DV = 128, KVS = 4;
 constexpr int Q_BOX = AQ * 64 * 2;   // 16 KB: 128 rows x 64 columns
 constexpr int K_BOX = AK * 64 * 2;   // 8 KB
 constexpr int Q_BYTES = 3 * Q_BOX;   // 48 KB
 constexpr int K_BYTES = 3 * K_BOX;   // 24 KB
 constexpr int V_BYTES = DV * AK * 2; // 16 KB
-constexpr int P_BYTES = AQ * AK * 2; // 16 KB
 constexpr int XCH_BYTES = 2 * 2 * AQ * 4;  // row-max exchange between the two column halves, per tile parity
 constexpr int ATT_THREADS = 384;
-constexpr int ATT_SMEM = 1024 + Q_BYTES + KVS * (K_BYTES + V_BYTES) + 2 * P_BYTES + XCH_BYTES + 256;
+constexpr int ATT_SMEM = 1024 + Q_BYTES + KVS * (K_BYTES + V_BYTES) + XCH_BYTES + 256;
 // kind::f16 instruction descriptors, K-major A and B, bf16 in, fp32 out
 constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(AK >> 3) << 17) |
                              (uint32_t(AQ >> 4) << 24);
 constexpr uint32_t IDESC_O = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(DV >> 3) << 17) |
                              (uint32_t(AQ >> 4) << 24);
-constexpr int SB = 3;                      // S buffers: S_{j+2} is issued while softmax(j) runs
-constexpr uint32_t TM_S = 0, TM_O = 256;  // S buffers at 0 / 64 / 128, the O accumulator at 256
+// TMEM (512 columns): Q as the A operand of QK^T (192 bf16 per lane = 96
+// columns), four S buffers that the softmax overwrites in place with P (the A
+// operand of PV, 64 bf16 = 32 columns), one O accumulator.
+constexpr int SB = 4;
+constexpr uint32_t TM_Q = 0, TM_S = 128, TM_O = 384;
 constexpr float RESCALE_LOG2 = 8.0f;      // lazy rescale threshold (log2 units)
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -112,6 +114,13 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// A operand in TMEM (lane = row, 2 bf16 per column), B from shared memory
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
 // K-major SWIZZLE_128B operand descriptor (8-row atoms 1024 B apart, sm_100 version 1)
 __device__ __forceinline__ uint64_t desc(uint32_t saddr) {
   return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
@@ -137,6 +146,13 @@ __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&r)[32]) {
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
       "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
 __device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -173,18 +189,17 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   uint8_t* sQ = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = sQ + Q_BYTES;
   uint8_t* sV = sK + KVS * K_BYTES;
-  uint8_t* sP = sV + KVS * V_BYTES;
-  float* xch = reinterpret_cast<float*>(sP + 2 * P_BYTES);  // [tile parity][half][row]
-  uint64_t* q_full = reinterpret_cast<uint64_t*>(sP + 2 * P_BYTES + XCH_BYTES);
-  uint64_t* k_full = q_full + 1;  // K and V rings: a K stage is free once S_j is done, a V stage after PV_j
+  float* xch = reinterpret_cast<float*>(sV + KVS * V_BYTES);  // [tile parity][half][row]
+  uint64_t* q_full = reinterpret_cast<uint64_t*>(sV + KVS * V_BYTES + XCH_BYTES);
+  uint64_t* q_tmem = q_full + 1;  // Q copied into TMEM
+  uint64_t* k_full = q_tmem + 1;  // K and V rings: a K stage is free once S_j is done, a V stage after PV_j
   uint64_t* k_empty = k_full + KVS;
   uint64_t* v_full = k_empty + KVS;
   uint64_t* v_empty = v_full + KVS;
-  uint64_t* s_full = v_empty + KVS;
-  uint64_t* s_empty = s_full + SB;
-  uint64_t* p_full = s_empty + SB;
-  uint64_t* p_empty = p_full + 2;
-  uint64_t* o_full = p_empty + 2;
+  uint64_t* s_full = v_empty + KVS;  // S_j in buffer j % SB
+  uint64_t* p_full = s_full + SB;    // P_j written over it
+  uint64_t* s_free = p_full + SB;    // PV_j done: buffer reusable, and every earlier PV is done
+  uint64_t* o_full = s_free + SB;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 1);
 
   const AttnTile tile = tiles[blockIdx.x];
@@ -194,6 +209,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     bar_init(q_full, 1);
+    bar_init(q_tmem, 4);
     for (int s = 0; s < KVS; ++s) {
       bar_init(&k_full[s], 1);
       bar_init(&k_empty[s], 1);
@@ -202,11 +218,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     }
     for (int b = 0; b < SB; ++b) {
       bar_init(&s_full[b], 1);
-      bar_init(&s_empty[b], 8);
-    }
-    for (int b = 0; b < 2; ++b) {
       bar_init(&p_full[b], 8);
-      bar_init(&p_empty[b], 1);
+      bar_init(&s_free[b], 1);
     }
     bar_init(o_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -240,15 +253,15 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   } else if (warp == 1) {  // ------------------------------------------ MMA issuer
     // The whole warp runs the schedule (waits, descriptor arithmetic) so the
     // operands are warp-uniform and live in uniform registers; one elected
-    // lane issues. (With a lane-0-only branch ptxas wrapped every
-    // tcgen05.mma in an R2UR/ELECT loop, ~40 issue cycles per 32-cycle
-    // M128 N64 K16 MMA -- the issuing thread, not the tensor pipe, set the pace.)
-    bar_wait(q_full, 0);
+    // lane issues. Both A operands come from TMEM (Q, and P written over S):
+    // an SS-mode M128 N64 K16 MMA is bound by its shared-memory operand reads
+    // (57 cycles measured vs 32 of math, scripts/micro/mma_rate.cu), a
+    // TS-mode one reads only the 2 KB K slice.
+    bar_wait(q_tmem, 0);
     fence_after();
-    const uint64_t qd = desc(su32(sQ));
     auto qk = [&](int j) {  // S_j = Q K_j^T into S buffer j % SB
       const int b = j % SB, s = j % KVS;
-      bar_wait(&s_empty[b], ((j / SB) & 1) ^ 1);
+      bar_wait(&s_free[b], ((j / SB) & 1) ^ 1);  // PV_{j-SB} has consumed P_{j-SB}
       bar_wait(&k_full[s], (j / KVS) & 1);
       fence_after();
       const uint64_t kd = desc(su32(sK + s * K_BYTES));
@@ -257,26 +270,26 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         for (int a = 0; a < 3; ++a)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma(tmem + TM_S + uint32_t(b) * AK, qd + uint64_t(a * (Q_BOX >> 4)) + 2 * k,
-                kd + uint64_t(a * (K_BOX >> 4)) + 2 * k, IDESC_S, (a | k) != 0);
+            mma_ts(tmem + TM_S + uint32_t(b) * AK, tmem + TM_Q + uint32_t(a * 32 + k * 8),
+                   kd + uint64_t(a * (K_BOX >> 4)) + 2 * k, IDESC_S, (a | k) != 0);
         commit(&s_full[b]);
         commit(&k_empty[s]);
       }
       __syncwarp();
     };
     auto pv = [&](int i) {  // O += P_i V_i
-      const int b = i & 1, s = i % KVS;
-      bar_wait(&p_full[b], (i >> 1) & 1);
+      const int b = i % SB, s = i % KVS;
+      bar_wait(&p_full[b], (i / SB) & 1);
       bar_wait(&v_full[s], (i / KVS) & 1);
       fence_after();
-      const uint64_t pd = desc(su32(sP + b * P_BYTES));
       const uint64_t vd = desc(su32(sV + s * V_BYTES));
       if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)  // 16 keys (32 bytes) per MMA
-          mma(tmem + TM_O, pd + 2 * k, vd + 2 * k, IDESC_O, (i | k) != 0);
+        for (int k = 0; k < 4; ++k)  // 16 keys = 8 TMEM columns of P per MMA
+          mma_ts(tmem + TM_O, tmem + TM_S + uint32_t(b) * AK + uint32_t(k * 8), vd + 2 * k, IDESC_O,
+                 (i | k) != 0);
         commit(&v_empty[s]);
-        commit(&p_empty[b]);
+        commit(&s_free[b]);
       }
       __syncwarp();
     };
@@ -299,17 +312,33 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     const int qi = tile.q0 + row;  // query position in its sequence
     const uint32_t lb = uint32_t(q * 32) << 16;
     constexpr int HC = AK / 2, HO = DV / 2;
+    if (hf == 0) {  // Q row (SWIZZLE_128B smem, 16-byte chunk c of row r at c ^ (r % 8)) into TMEM
+      bar_wait(q_full, 0);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        uint32_t v[32];
+        const uint8_t* src = sQ + a * Q_BOX + (row >> 3) * 1024 + (row & 7) * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 u = *reinterpret_cast<const uint4*>(src + ((c ^ (row & 7)) << 4));
+          v[4 * c] = u.x, v[4 * c + 1] = u.y, v[4 * c + 2] = u.z, v[4 * c + 3] = u.w;
+        }
+        st32(tmem + lb + TM_Q + uint32_t(a * 32), v);
+      }
+      st_wait();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(q_tmem);
+    }
     float m_ref = -INFINITY, l = 0.0f;  // l = sum of exp2(s - m_ref) over this half's keys
     for (int j = 0; j < nt; ++j) {
       const int b = j & 1, sb = j % SB;
+      const uint32_t sbuf = tmem + lb + TM_S + uint32_t(sb) * AK;
       bar_wait(&s_full[sb], (j / SB) & 1);
       fence_after();
       uint32_t r[HC];
-      ld32(tmem + lb + TM_S + uint32_t(sb) * AK + uint32_t(hf * HC), r);
+      ld32(sbuf + uint32_t(hf * HC), r);
       ld_wait();
-      fence_before();
-      __syncwarp();
-      if (lane == 0) bar_arrive(&s_empty[sb]);
       float sv[HC];
       const int k0 = j * AK + hf * HC;
       float m0 = -INFINITY, m1 = -INFINITY;
@@ -331,6 +360,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         }
       }
       float mx = fmaxf(m0, m1);
+      // the exchange barrier also orders both halves' S loads before either
+      // half writes P over columns [0, 32) of the buffer
       sts(xch + (b * 2 + hf) * AQ + row, mx);
       asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");
       mx = fmaxf(mx, lds(xch + (b * 2 + (hf ^ 1)) * AQ + row)) * scale_log2;
@@ -345,7 +376,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           l *= alpha;
           m_ref = mx;
         }
-        bar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        bar_wait(&s_free[(j - 1) % SB], ((j - 1) / SB) & 1);
         fence_after();
 #pragma unroll
         for (int ch = 0; ch < HO / 32; ++ch) {
@@ -356,30 +387,24 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           for (int x = 0; x < 32; ++x) o[x] = __float_as_uint(__uint_as_float(o[x]) * alpha);
           st32(tmem + lb + TM_O + uint32_t(hf * HO + ch * 32), o);
         }
-        st_wait();
       }
       const float nm = -m_ref;
       float s0 = 0.0f, s1 = 0.0f;
+      uint32_t pk[HC / 2];
 #pragma unroll
       for (int c = 0; c < HC; c += 2) {
-        sv[c] = ex2(fmaf(sv[c], scale_log2, nm));
-        sv[c + 1] = ex2(fmaf(sv[c + 1], scale_log2, nm));
-        s0 += sv[c];
-        s1 += sv[c + 1];
+        const float e0 = ex2(fmaf(sv[c], scale_log2, nm)), e1 = ex2(fmaf(sv[c + 1], scale_log2, nm));
+        s0 += e0;
+        s1 += e1;
+        pk[c / 2] = pack2(e0, e1);
       }
       l += s0 + s1;
-      // this half's 64 bytes of the P row into the SWIZZLE_128B tile: chunk c of row r at c ^ (r % 8)
-      bar_wait(&p_empty[b], ((j >> 1) & 1) ^ 1);
-      uint8_t* prow = sP + b * P_BYTES + (row >> 3) * 1024 + (row & 7) * 128;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        *reinterpret_cast<uint4*>(prow + (((hf * 4 + c) ^ (row & 7)) << 4)) =
-            make_uint4(pack2(sv[8 * c], sv[8 * c + 1]), pack2(sv[8 * c + 2], sv[8 * c + 3]),
-                       pack2(sv[8 * c + 4], sv[8 * c + 5]), pack2(sv[8 * c + 6], sv[8 * c + 7]));
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      // this half's 32 keys of P (bf16 pairs) over TMEM columns [16 hf, 16 hf + 16) of the buffer
+      st16(sbuf + uint32_t(hf * (HC / 2)), pk);
+      st_wait();
       fence_before();
       __syncwarp();
-      if (lane == 0) bar_arrive(&p_full[b]);
+      if (lane == 0) bar_arrive(&p_full[sb]);
     }
     // row sum over both halves (the exchange slot of parity nt & 1 is free:
     // both halves passed the barrier of tile nt - 1, which used the other)
