@@ -15,28 +15,31 @@
 // attention core is mla_attn_kernel below.
 //
 // mla_attn_kernel: one CTA per (128-query tile of a sequence, head),
-// 256 threads, warp-specialised:
+// 384 threads, warp-specialised:
 //   warp 0      TMA producer: Q tile once (3 boxes of 128 x 64), then per
 //               64-key tile K (3 boxes) and V^T (one [128 dv][64 keys] box)
-//               into a 3-stage ring
-//   warp 1      MMA issuer: S_j = Q K_j^T (tcgen05 kind::f16, M128 N64 K192
-//               into TMEM, double-buffered), then O += P_{j-1} V_{j-1}
-//               (M128 N128 K64) into ONE TMEM accumulator, one elected thread
-//   warp 2      TMEM allocator (256 columns: S0 S1 | O)
+//               into separate 4-stage rings
+//   warp 1      MMA issuer (whole warp runs the schedule, one elected lane
+//               issues): S_j = Q K_j^T (tcgen05 kind::f16, M128 N64 K192, A =
+//               Q in TMEM) into S buffer j % 4, and O += P_j V_j (M128 N128
+//               K64, A = P in TMEM) into ONE TMEM accumulator; S runs two
+//               tiles ahead of PV
+//   warp 2      TMEM allocator (512 columns: Q 96 | S/P x4 of 64 | O 128)
 //   warps 4-11  softmax + epilogue, one query row per thread pair (TMEM lane),
-//               each warp of a pair on 32 of the 64 S columns:
-//               tcgen05.ld S, causal mask (diagonal tiles only), online
-//               softmax in exp2 form against a LAZY reference max m_ref,
-//               P (bf16) into the SWIZZLE_128B smem tile the next MMA reads
-//               as its A operand. O never leaves TMEM until the epilogue:
-//               P = exp2(s - m_ref) is only rescaled when a row's max
-//               grows by more than 2^8 over m_ref (then the warp waits for
-//               the previous PV, multiplies its O rows in TMEM by
+//               each warp of a pair on 32 of the 64 S columns (warps 4-7
+//               first copy the Q rows from smem into TMEM): tcgen05.ld S,
+//               causal mask (diagonal tiles only), row max agreed through
+//               smem + a named barrier, online softmax in exp2 form against a
+//               LAZY reference max m_ref, P as bf16 pairs written over the S
+//               columns it came from (tcgen05.st). O never leaves TMEM until
+//               the epilogue: P = exp2(s - m_ref) is only rescaled when a
+//               row's max grows by more than 2^8 over m_ref (then the warp
+//               waits for the previous PV, multiplies its O rows in TMEM by
 //               alpha = exp2(m_ref - m_new) with tcgen05.ld/st, and moves
-//               m_ref) -- P <= 2^8 stays exact in bf16 scaling terms and the
+//               m_ref) -- P <= 2^8 keeps the bf16 relative precision and the
 //               fp32 accumulator has the range. Epilogue: O / l as bf16.
-// K_j's stage is released by the commit after the PV MMA of tile j, so the
-// softmax of tile j overlaps S_{j+1} and PV_{j-1} on the tensor core.
+// A K stage is released when its S MMA completes, a V stage and the S/P
+// buffer when the PV MMA of that tile completes.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
