@@ -61,8 +61,9 @@ constexpr int K_BOX = AK * 64 * 2;   // 8 KB
 constexpr int Q_BYTES = 3 * Q_BOX;   // 48 KB
 constexpr int K_BYTES = 3 * K_BOX;   // 24 KB
 constexpr int V_BYTES = DV * AK * 2; // 16 KB
-constexpr int XCH_BYTES = 2 * 2 * AQ * 4;  // row-max exchange between the two column halves, per tile parity
-constexpr int ATT_THREADS = 384;
+constexpr int NG = 2;  // softmax column groups: NG warps per TMEM lane quarter, AK / NG S columns each
+constexpr int XCH_BYTES = 2 * NG * AQ * 4;  // row-max exchange between the column groups, per tile parity
+constexpr int ATT_THREADS = 128 + NG * 128;
 constexpr int ATT_SMEM = 1024 + Q_BYTES + KVS * (K_BYTES + V_BYTES) + XCH_BYTES + 256;
 // kind::f16 instruction descriptors, K-major A and B, bf16 in, fp32 out
 constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(AK >> 3) << 17) |
@@ -152,6 +153,27 @@ __device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&r)[16]) {
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+template <int N>
+__device__ __forceinline__ void ldn(uint32_t taddr, uint32_t (&r)[N]) {
+  if constexpr (N == 32) ld32(taddr, r); else ld16(taddr, r);
+}
+template <int N>
+__device__ __forceinline__ void stn(uint32_t taddr, const uint32_t (&r)[N]) {
+  if constexpr (N == 16) st16(taddr, r); else st8(taddr, r);
+}
 __device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -215,7 +237,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     }
     for (int b = 0; b < SB; ++b) {
       bar_init(&s_full[b], 1);
-      bar_init(&p_full[b], 8);
+      bar_init(&p_full[b], 4 * NG);
       bar_init(&s_free[b], 1);
     }
     bar_init(o_full, 1);
@@ -301,14 +323,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     if (elect_one()) commit(o_full);
     __syncwarp();
   } else if (warp >= 4) {  // -------------------------------------------- softmax + epilogue
-    // warps 4-7 take S columns [0, 32) of the TMEM lanes (warp % 4) * 32 ..,
-    // warps 8-11 columns [32, 64) of the same lanes: two warps per SM
-    // sub-partition hide each other's latency. The pair agrees on the row max
-    // through xch + a named barrier per lane quarter; each owns half of O.
+    // warps 4 + 4g + q (g < NG) take S columns [g AK/NG, (g+1) AK/NG) of
+    // the TMEM lanes 32q ..: NG warps per SM sub-partition hide each other's
+    // latency. The group agrees on the row max through xch + a named barrier
+    // per lane quarter; each warp owns DV/NG columns of O.
     const int q = warp & 3, hf = (warp - 4) >> 2, row = q * 32 + lane;
     const int qi = tile.q0 + row;  // query position in its sequence
     const uint32_t lb = uint32_t(q * 32) << 16;
-    constexpr int HC = AK / 2, HO = DV / 2;
+    constexpr int HC = AK / NG, HO = DV / NG;
     if (hf == 0) {  // Q row (SWIZZLE_128B smem, 16-byte chunk c of row r at c ^ (r % 8)) into TMEM
       bar_wait(q_full, 0);
 #pragma unroll
@@ -334,7 +356,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       bar_wait(&s_full[sb], (j / SB) & 1);
       fence_after();
       uint32_t r[HC];
-      ld32(sbuf + uint32_t(hf * HC), r);
+      ldn<HC>(sbuf + uint32_t(hf * HC), r);
       ld_wait();
       float sv[HC];
       const int k0 = j * AK + hf * HC;
@@ -357,12 +379,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         }
       }
       float mx = fmaxf(m0, m1);
-      // the exchange barrier also orders both halves' S loads before either
-      // half writes P over columns [0, 32) of the buffer
-      sts(xch + (b * 2 + hf) * AQ + row, mx);
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");
-      mx = fmaxf(mx, lds(xch + (b * 2 + (hf ^ 1)) * AQ + row)) * scale_log2;
-      const bool grow = mx > m_ref + RESCALE_LOG2;  // identical in both halves
+      // the exchange barrier also orders every group's S loads before any
+      // group writes P over columns [0, 32) of the buffer
+      sts(xch + (b * NG + hf) * AQ + row, mx);
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * NG) : "memory");
+#pragma unroll
+      for (int g = 1; g < NG; ++g) mx = fmaxf(mx, lds(xch + (b * NG + (hf + g) % NG) * AQ + row));
+      mx *= scale_log2;
+      const bool grow = mx > m_ref + RESCALE_LOG2;  // identical in every group
       if (j == 0) {
         m_ref = mx;  // key 0 is visible to every row: finite
       } else if (__any_sync(0xffffffffu, grow)) {
@@ -396,18 +420,19 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         pk[c / 2] = pack2(e0, e1);
       }
       l += s0 + s1;
-      // this half's 32 keys of P (bf16 pairs) over TMEM columns [16 hf, 16 hf + 16) of the buffer
-      st16(sbuf + uint32_t(hf * (HC / 2)), pk);
+      // this group's keys of P (bf16 pairs) over TMEM columns [hf HC/2, (hf+1) HC/2) of the buffer
+      stn<HC / 2>(sbuf + uint32_t(hf * (HC / 2)), pk);
       st_wait();
       fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(&p_full[sb]);
     }
-    // row sum over both halves (the exchange slot of parity nt & 1 is free:
-    // both halves passed the barrier of tile nt - 1, which used the other)
-    sts(xch + ((nt & 1) * 2 + hf) * AQ + row, l);
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");
-    l += lds(xch + ((nt & 1) * 2 + (hf ^ 1)) * AQ + row);
+    // row sum over the groups (the exchange slot of parity nt & 1 is free:
+    // every group passed the barrier of tile nt - 1, which used the other)
+    sts(xch + ((nt & 1) * NG + hf) * AQ + row, l);
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * NG) : "memory");
+#pragma unroll
+    for (int g = 1; g < NG; ++g) l += lds(xch + ((nt & 1) * NG + (hf + g) % NG) * AQ + row);
     bar_wait(o_full, 0);
     fence_after();
     const float inv = 1.0f / l;
