@@ -1263,6 +1263,8 @@ constexpr int R_B = 3 * R_BN * 128;       // 24 KB
 constexpr int R_SMEM = R_STAGES * (R_A + R_B) + 1024 + 256;
 constexpr uint32_t R_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(R_BN >> 3) << 17) |
                              (uint32_t(BM >> 4) << 24);
+constexpr uint32_t R_IDESC3 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(3 * R_BN >> 3) << 17) |
+                              (uint32_t(BM >> 4) << 24);  // N = the 3 stacked weight planes
 
 __global__ void __launch_bounds__(256, 1)
     router_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -1323,35 +1325,52 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer: 9 plane products x 4 K-steps per k-block into D_{a+b}
-      int s = 0;
-      uint32_t ph = 0;
-      int local = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-        mbar_wait(tempty, (local & 1) ^ 1);
+    // MMA issuer. The B stage holds the three weight planes as 192
+    // contiguous rows, so one M128 N192 MMA with A plane a writes the
+    // products (a, 0..2) into columns [64a, 64a + 192) = D_a, D_{a+1},
+    // D_{a+2}: three MMAs per K32 step instead of nine N64 ones (an SS-mode
+    // N64 MMA is bound by its 6 KB of smem operand reads, 57 cycles for 32
+    // of math, scripts/micro/mma_rate.cu). The tile's first K32 step uses
+    // the nine N64 products so each D_s is overwritten exactly once. The
+    // whole warp runs the schedule (warp-uniform descriptors); one elected
+    // lane issues.
+    int s = 0;
+    uint32_t ph = 0;
+    int local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      mbar_wait(tempty, (local & 1) ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < kb_count; ++kb) {
+        mbar_wait(&full[s], ph);
         tc_fence_after();
-        for (int kb = 0; kb < kb_count; ++kb) {
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint64_t ad = sw128_desc(smem_u32(sA + s * R_A));
-          const uint64_t bd = sw128_desc(smem_u32(sB + s * R_B));
+        const uint64_t ad = sw128_desc(smem_u32(sA + s * R_A));
+        const uint64_t bd = sw128_desc(smem_u32(sB + s * R_B));
+        if (elect_one()) {
+          int k0 = 0;
+          if (kb == 0) {  // first K32 step: D_s = the first product of weight s, then accumulate
 #pragma unroll
-          for (int a = 0; a < 3; ++a)
+            for (int a = 0; a < 3; ++a)
 #pragma unroll
-            for (int b = 0; b < 3; ++b)
-#pragma unroll
-              for (int k = 0; k < 4; ++k)  // the first product into D_s overwrites it
-                tc_mma_i8(tmem + uint32_t((a + b) * R_BN), ad + uint64_t(a * (BM * 128 >> 4)) + 2 * k,
-                          bd + uint64_t(b * (R_BN * 128 >> 4)) + 2 * k, R_IDESC,
-                          (kb | k) != 0 || !(a == 0 || b == 2));
-          tc_commit(&empty[s]);
-          if (++s == R_STAGES) {
-            s = 0;
-            ph ^= 1;
+              for (int b = 0; b < 3; ++b)
+                tc_mma_i8(tmem + uint32_t((a + b) * R_BN), ad + uint64_t(a * (BM * 128 >> 4)),
+                          bd + uint64_t(b * (R_BN * 128 >> 4)), R_IDESC, !(a == 0 || b == 2));
+            k0 = 1;
           }
+          for (int k = k0; k < 4; ++k)
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+              tc_mma_i8(tmem + uint32_t(a * R_BN), ad + uint64_t(a * (BM * 128 >> 4)) + 2 * k, bd + 2 * k,
+                        R_IDESC3, 1);
+          tc_commit(&empty[s]);
         }
-        tc_commit(tfull);
+        __syncwarp();
+        if (++s == R_STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
       }
+      if (elect_one()) tc_commit(tfull);
+      __syncwarp();
     }
   } else if (warp >= 4) {  // epilogue: exact recombination, one rounding, fp32 logits
     const int q = warp & 3;
