@@ -561,7 +561,7 @@ def main():
         all_drecs = gather(drecs)
         dval = total_tokens / (dms / 1e3)
         dep2 = None
-        if args.dtype == "bf16":
+        if True:
             # the stronger DEP: token-deduplicated dispatch + partial combine
             # (dwdp_dep_set_mode(1)), same kernels, same box
             ctx.dep_set_mode(1)

@@ -487,7 +487,8 @@ int dwdp_dep_init(dwdp_ctx* ctx, const void* nccl_id);
  * (each token row once per peer rank, with its routing), receive-side
  * permute merging each expert's rows across sources, per-rank partial
  * combine so one row per (token, rank) returns, token counts exchanged once
- * per stack (bf16 experts). Outputs within bf16 rounding of mode 0 (the
+ * per stack (bf16, fp8 and nvfp4 experts: the receiver quantises the rows it
+ * keeps, as the DWDP path does). Outputs within bf16 rounding of mode 0 (the
  * per-rank partial sums are rounded to bf16 before the final sum). */
 int dwdp_dep_set_mode(dwdp_ctx* ctx, int mode);
 int dwdp_dep_layer_forward(dwdp_ctx* ctx, int layer, const void* x, int64_t T,

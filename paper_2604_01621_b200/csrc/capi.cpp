@@ -716,9 +716,7 @@ int dwdp_dep_init(dwdp_ctx* c, const void* id) {
 int dwdp_dep_set_mode(dwdp_ctx* c, int mode) {
   return guard([&] {
     dwdp::require(mode == 0 || mode == 1, "dep: mode must be 0 (per-pair) or 1 (token dedupe)");
-    auto& ctx = C(c);
-    dwdp::require(mode == 0 || ctx.cfg.weight_dtype == DWDP_WEIGHT_BF16, "dep mode 1: bf16 experts only");
-    ctx.dep_mode = mode;
+    C(c).dep_mode = mode;
   });
 }
 

@@ -424,7 +424,6 @@ void Ctx::dep_stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStrea
 
 void Ctx::dep2_alloc() {
   if (dep2_x_) return;
-  require(!fp8_ && !fp4_, "dep mode 1: bf16 experts only");
   const int64_t rows = int64_t(N_) * max_tokens_;
   dep2_x_ = static_cast<uint16_t*>(dalloc(size_t(rows) * h_ * 2, &workspace_bytes));
   dep2_idx_ = static_cast<int32_t*>(dalloc(size_t(rows) * k_ * 4, &workspace_bytes));
@@ -451,6 +450,23 @@ void Ctx::dep2_alloc() {
     DWDP_CUDA(cudaMemset(dep2_meta_, 0, 16 * 4));
     tm_dep2_xperm_ = make_tmap_bf16(dep2_xperm_, dep2_cap_rows_, h_, 128);
     tm_dep2_h_ = make_tmap_bf16(dep2_h_, dep2_cap_rows_, f_, 128);
+    if (fp8_ || fp4_) {  // quantised rows in the dep2_xperm_ bytes, as X_perm8 / X_perm4 in the DWDP path
+      const int64_t kd = fp4_ ? 2 : 1, R = dep2_cap_rows_;
+      dep2_h8_ = static_cast<uint8_t*>(dalloc(size_t(R * f_ / kd), &workspace_bytes));
+      dep2_xs_ = static_cast<float*>(dalloc(size_t(R) * 4, &workspace_bytes));
+      dep2_hs_ = static_cast<float*>(dalloc(size_t(R) * 4, &workspace_bytes));
+      tm_dep2_x8_ = make_tmap_i8(dep2_xperm_, R, h_ / kd, 128);
+      tm_dep2_h8_ = make_tmap_i8(dep2_h8_, R, f_ / kd, 128);
+      if (fp4_) {
+        dep2_sfl_ = static_cast<uint8_t*>(dalloc(size_t(R * std::max(h_, f_) / 16), &workspace_bytes));
+        dep2_xsf_ = static_cast<uint8_t*>(dalloc(size_t(R * h_ / 16), &workspace_bytes));
+        dep2_hsf_ = static_cast<uint8_t*>(dalloc(size_t(R * f_ / 16), &workspace_bytes));
+        tm_dep2_sfx_ = make_tmap_sf(dep2_xsf_, R * h_ / 16);
+        tm_dep2_sfh_ = make_tmap_sf(dep2_hsf_, R * f_ / 16);
+        tm_dep2_o_ = make_tmap_out(dep2_xperm_, R, h_);
+        tm_dep2_h_o_ = make_tmap_out(dep2_h_, R, f_);
+      }
+    }
   }
   DWDP_CUDA(cudaHostAlloc(&dep2_tok_host_, size_t(N_) * 8, 0));
   DWDP_CUDA(cudaHostAlloc(&dep2_flag_host_, 16, 0));
@@ -498,9 +514,15 @@ void Ctx::dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* 
   require(int64_t(Ts.size()) == N_ && Ts[size_t(rank_)] == T, "dep mode 1: token counts out of date");
   const Nccl& n = nccl();
   const int wl = layer % WL_, per = E_ / N_, lo = rank_ * per;
-  std::vector<int64_t> off(size_t(N_) + 1, 0);
-  for (int r = 0; r < N_; ++r) off[size_t(r) + 1] = off[size_t(r)] + Ts[size_t(r)];
-  const int64_t Tall = off[size_t(N_)];
+  // receive layout: this rank's tokens first (the permute's shared-expert
+  // rows are tokens [0, T) of its input), then the peers in rank order
+  std::vector<int64_t> off(size_t(N_), 0);
+  int64_t Tall = T;
+  for (int r = 0; r < N_; ++r)
+    if (r != rank_) {
+      off[size_t(r)] = Tall;
+      Tall += Ts[size_t(r)];
+    }
   LayerRec rec{int64_t(layer), T, take_event(), take_event(), take_event(), nullptr, -1};
   DWDP_CUDA(cudaEventRecord(rec.gate0, st));
   DWDP_CUDA(cudaEventRecord(rec.gate1, st));
@@ -531,7 +553,7 @@ void Ctx::dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* 
     }
   }
   nccl_check(n.GroupEnd(), "ncclGroupEnd");
-  const int64_t mine = off[size_t(rank_)];
+  const int64_t mine = 0;
   if (T > 0) {
     DWDP_CUDA(cudaMemcpyAsync(dep2_x_ + mine * h_, x, size_t(T) * h_ * 2, cudaMemcpyDeviceToDevice, st));
     DWDP_CUDA(cudaMemcpyAsync(dep2_idx_ + mine * k_, idx_, size_t(T) * hk * 4, cudaMemcpyDeviceToDevice, st));
@@ -542,28 +564,70 @@ void Ctx::dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* 
   // each expert's rows of all sources form one segment; shared expert on
   // the rank's own T tokens (its A rows read from x)
   launch_localize_idx(dep2_idx_, Tall * k_, lo, lo + per, dep2_loc_, st);
-  int np = 1;
-  if (Tall > 0)
-    np += launch_permute(dep2_loc_, dep2_x_, Tall, E_, k_, h_, shared_ ? 1 : 0, counts_, dep2_rowof_,
-                         dep2_mblock_, dep2_mbseg_, nullptr, dep2_meta_, dep2_xperm_, dep2_scratch_, st, nullptr,
-                         nullptr, 128, dep2_mbrows_, nullptr, T, dep2_cap_rows_);
-  mark(&rec.k[1]);
-  // 4. grouped GEMMs (the rank's expert block + its shared expert)
   const int32_t* stab = slot_tab_ + size_t(layer) * 2 * (E_ + 1);
   const int64_t mb_ub = dep2_max_mb_;
-  const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_dep2_xperm_;
-  GemmArgs g1{int(h_), int(f_), int(f_), E_, dep2_mblock_, stab, dep2_meta_, dep2_h_, f_, INT64_MAX, 1,
-              dep2_mbseg_, nullptr, nullptr, nullptr, nullptr, 0, raster_, dep2_mbrows_};
-  if (Tall > 0)
-    launch_grouped_gemm(GEMM_SWIGLU, tm_dep2_xperm_, tm_x, tm_gate_, tm_up_, g1,
-                        int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30)), st);
-  mark(&rec.k[2]);
-  GemmArgs g2{int(f_), int(h_), int(h_), E_, dep2_mblock_, stab, dep2_meta_, dep2_xperm_, h_, INT64_MAX, 0,
-              dep2_mbseg_, nullptr, nullptr, nullptr, nullptr, 0, raster_, dep2_mbrows_};
-  if (Tall > 0)
-    launch_grouped_gemm(GEMM_PLAIN, tm_dep2_h_, tm_dep2_h_, tm_down_, tm_down_, g2,
-                        int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
-  mark(&rec.k[3]);
+  const int g1_tiles = int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30));
+  const int g2_tiles = int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30));
+  int np = 1;
+  if (fp8_ || fp4_) {
+    // quantised experts, as the DWDP path: the permute writes e4m3 (e2m1 +
+    // block scales) copies of every local (token, expert) row and of the own
+    // tokens' shared-expert rows with row scales; GEMM1 emits bf16 H, which
+    // is re-quantised for GEMM2; O (bf16) overwrites the quantised rows
+    uint8_t* x8 = reinterpret_cast<uint8_t*>(dep2_xperm_);
+    if (Tall > 0)
+      np += launch_permute(dep2_loc_, dep2_x_, Tall, E_, k_, h_, shared_ ? 1 : 0, counts_, dep2_rowof_,
+                           dep2_mblock_, dep2_mbseg_, nullptr, dep2_meta_, nullptr, dep2_scratch_, st, x8,
+                           dep2_xs_, 128, dep2_mbrows_, fp4_ ? dep2_sfl_ : nullptr, T, dep2_cap_rows_);
+    if (fp4_ && Tall > 0) {
+      launch_nvfp4_sf_relayout(dep2_sfl_, dep2_xsf_, dep2_cap_rows_, h_, dep2_meta_, st);
+      ++np;
+    }
+    mark(&rec.k[1]);
+    if (Tall > 0 && fp4_) {
+      GemmArgs g1{int(h_), int(f_), int(f_), E_, dep2_mblock_, stab, dep2_meta_, dep2_h_, f_, INT64_MAX, 0,
+                  dep2_mbseg_, nullptr, dep2_xs_, sarena_[0], sarena_[1], 0, raster_, dep2_mbrows_, nullptr, 0,
+                  dep2_xsf_, sfarena_[0], sfarena_[1]};
+      const CUtensorMap sf1[4] = {tm_dep2_sfx_, tm_sf_w_[0], tm_sf_w_[1], tm_dep2_h_o_};
+      launch_grouped_gemm(GEMM_SWIGLU_FP4, tm_dep2_x8_, tm_dep2_x8_, tm_gate_, tm_up_, g1, g1_tiles, st, sf1);
+      launch_quant_rows_nvfp4(dep2_h_, dep2_cap_rows_, f_, dep2_meta_, dep2_h8_, dep2_sfl_, dep2_hsf_, dep2_hs_,
+                              st);
+    } else if (Tall > 0) {
+      GemmArgs g1{int(h_), int(f_), int(f_), E_, dep2_mblock_, stab, dep2_meta_, dep2_h_, f_, INT64_MAX, 0,
+                  dep2_mbseg_, nullptr, dep2_xs_, sarena_[0], sarena_[1], 0, raster_, dep2_mbrows_};
+      launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_dep2_x8_, tm_dep2_x8_, tm_gate_, tm_up_, g1, g1_tiles, st);
+      launch_quant_rows_fp8(dep2_h_, dep2_cap_rows_, f_, dep2_meta_, dep2_h8_, dep2_hs_, st);
+    }
+    mark(&rec.k[2]);
+    if (Tall > 0 && fp4_) {
+      GemmArgs g2{int(f_), int(h_), int(h_), E_, dep2_mblock_, stab, dep2_meta_, dep2_xperm_, h_, INT64_MAX, 0,
+                  dep2_mbseg_, nullptr, dep2_hs_, sarena_[2], nullptr, 0, raster_, dep2_mbrows_, nullptr, 0,
+                  dep2_hsf_, sfarena_[2], nullptr};
+      const CUtensorMap sf2[4] = {tm_dep2_sfh_, tm_sf_w_[2], tm_sf_w_[2], tm_dep2_o_};
+      launch_grouped_gemm(GEMM_PLAIN_FP4, tm_dep2_h8_, tm_dep2_h8_, tm_down_, tm_down_, g2, g2_tiles, st, sf2);
+    } else if (Tall > 0) {
+      GemmArgs g2{int(f_), int(h_), int(h_), E_, dep2_mblock_, stab, dep2_meta_, dep2_xperm_, h_, INT64_MAX, 0,
+                  dep2_mbseg_, nullptr, dep2_hs_, sarena_[2], nullptr, 0, raster_, dep2_mbrows_};
+      launch_grouped_gemm(GEMM_PLAIN_FP8, tm_dep2_h8_, tm_dep2_h8_, tm_down_, tm_down_, g2, g2_tiles, st);
+    }
+    mark(&rec.k[3]);
+  } else {
+    if (Tall > 0)
+      np += launch_permute(dep2_loc_, dep2_x_, Tall, E_, k_, h_, shared_ ? 1 : 0, counts_, dep2_rowof_,
+                           dep2_mblock_, dep2_mbseg_, nullptr, dep2_meta_, dep2_xperm_, dep2_scratch_, st, nullptr,
+                           nullptr, 128, dep2_mbrows_, nullptr, T, dep2_cap_rows_);
+    mark(&rec.k[1]);
+    // 4. grouped GEMMs (the rank's expert block + its shared expert)
+    const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_dep2_xperm_;
+    GemmArgs g1{int(h_), int(f_), int(f_), E_, dep2_mblock_, stab, dep2_meta_, dep2_h_, f_, INT64_MAX, 1,
+                dep2_mbseg_, nullptr, nullptr, nullptr, nullptr, 0, raster_, dep2_mbrows_};
+    if (Tall > 0) launch_grouped_gemm(GEMM_SWIGLU, tm_dep2_xperm_, tm_x, tm_gate_, tm_up_, g1, g1_tiles, st);
+    mark(&rec.k[2]);
+    GemmArgs g2{int(f_), int(h_), int(h_), E_, dep2_mblock_, stab, dep2_meta_, dep2_xperm_, h_, INT64_MAX, 0,
+                dep2_mbseg_, nullptr, nullptr, nullptr, nullptr, 0, raster_, dep2_mbrows_};
+    if (Tall > 0) launch_grouped_gemm(GEMM_PLAIN, tm_dep2_h_, tm_dep2_h_, tm_down_, tm_down_, g2, g2_tiles, st);
+    mark(&rec.k[3]);
+  }
   // 5. partial combine per received token: sum over this rank's experts of
   // the token's k (row < 0: computed elsewhere); own tokens straight into
   // their slot of the final parts, the rest into the dispatch buffer
@@ -608,7 +672,7 @@ void Ctx::dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* 
         f[0] |= f[1];
       },
       dep2_flag_host_));
-  launches += (T > 0 ? 3 : 0) + np + (Tall > 0 ? 2 : 0) + 1;
+  launches += (T > 0 ? 3 : 0) + np + (Tall > 0 ? (fp4_ || fp8_ ? 3 : 2) : 0) + 1;
   DWDP_CUDA(cudaGetLastError());
   DWDP_CUDA(cudaEventRecord(rec.moe_end, st));
   push_record(rec);

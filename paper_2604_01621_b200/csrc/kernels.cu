@@ -1136,12 +1136,13 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
     // coalesced 32-byte code stores across the CTA
     float* rs = reinterpret_cast<float*>(rows + pch * k);
     const int32_t shared_row0 = shared ? meta[2] : 0;
+    const int64_t shared_T = shared ? meta[3] : 0;  // tokens [0, shared_T) have a shared-expert row
     for (int tl = warp; tl < ntok; tl += blockDim.x >> 5) {
       const float sc = nvfp4_row_scale(row_absmax_bf16(reinterpret_cast<const uint4*>(x + (t0 + tl) * h),
                                                        h / 8, lane));
       if (lane == 0) rs[tl] = sc;
       if (lane < k && rows[tl * k + lane] >= 0) xscale[rows[tl * k + lane]] = sc;
-      if (shared && lane == 0) xscale[shared_row0 + t0 + tl] = sc;
+      if (t0 + tl < shared_T && lane == 0) xscale[shared_row0 + t0 + tl] = sc;
     }
     __syncthreads();
     const int ng = int(h / 64);
@@ -1159,7 +1160,7 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
         const int64_t r = rows[tl * k + j];
         if (r >= 0) store_group(xperm8 + r * (h / 2), xsf, r, g, h, c, sfw, true);
       }
-      if (shared) {
+      if (t0 + tl < shared_T) {
         const int64_t r = shared_row0 + t0 + tl;
         store_group(xperm8 + r * (h / 2), xsf, r, g, h, c, sfw, true);
       }
@@ -1169,8 +1170,10 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
   if (xperm8) {  // W8A8: quantise each token row once (per-row scale), write k + shared copies
     const int64_t nch = h / 8;
     const int32_t shared_row0 = shared ? meta[2] : 0;
+    const int64_t shared_T = shared ? meta[3] : 0;
     for (int tl = warp; tl < ntok; tl += blockDim.x >> 5) {
       const uint4* src = reinterpret_cast<const uint4*>(x + (t0 + tl) * h);
+      const bool sh = t0 + tl < shared_T;
       const float amax = row_absmax_bf16(src, nch, lane);
       const float s = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
       // four 16-byte loads in flight per lane before the quantise + k stores
@@ -1185,17 +1188,17 @@ __global__ void __launch_bounds__(256) permute_scatter_kernel(
           const uint2 q = quant8(v[u], s);
           for (int j = 0; j < k; ++j)
             if (rows[tl * k + j] >= 0) reinterpret_cast<uint2*>(xperm8 + int64_t(rows[tl * k + j]) * h)[c] = q;
-          if (shared) reinterpret_cast<uint2*>(xperm8 + int64_t(shared_row0 + t0 + tl) * h)[c] = q;
+          if (sh) reinterpret_cast<uint2*>(xperm8 + int64_t(shared_row0 + t0 + tl) * h)[c] = q;
         }
       }
       for (int64_t c = c0; c < nch; c += 32) {
         const uint2 q = quant8(__ldg(src + c), s);
         for (int j = 0; j < k; ++j)
           if (rows[tl * k + j] >= 0) reinterpret_cast<uint2*>(xperm8 + int64_t(rows[tl * k + j]) * h)[c] = q;
-        if (shared) reinterpret_cast<uint2*>(xperm8 + int64_t(shared_row0 + t0 + tl) * h)[c] = q;
+        if (sh) reinterpret_cast<uint2*>(xperm8 + int64_t(shared_row0 + t0 + tl) * h)[c] = q;
       }
       if (lane < k && rows[tl * k + lane] >= 0) xscale[rows[tl * k + lane]] = s;
-      if (shared && lane == 0) xscale[shared_row0 + t0 + tl] = s;
+      if (sh && lane == 0) xscale[shared_row0 + t0 + tl] = s;
     }
     return;
   }

@@ -311,6 +311,11 @@ class Ctx {
   int2* dep2_mbseg_ = nullptr;
   int64_t dep2_cap_rows_ = 0, dep2_max_mb_ = 0;
   CUtensorMap tm_dep2_xperm_, tm_dep2_h_;
+  // fp8 / nvfp4 experts: e4m3 / e2m1 copies of the received rows live in the
+  // dep2_xperm_ bytes (as X_perm8 in the DWDP path), H re-quantised into dep2_h8_
+  uint8_t *dep2_h8_ = nullptr, *dep2_sfl_ = nullptr, *dep2_xsf_ = nullptr, *dep2_hsf_ = nullptr;
+  float *dep2_xs_ = nullptr, *dep2_hs_ = nullptr;
+  CUtensorMap tm_dep2_x8_, tm_dep2_h8_, tm_dep2_sfx_, tm_dep2_sfh_, tm_dep2_o_, tm_dep2_h_o_;
   int64_t* dep2_tok_host_ = nullptr;
   int64_t dep2_rowf_T_ = -1;
   void dep2_alloc();

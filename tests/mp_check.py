@@ -72,9 +72,10 @@ def main():
     if not torch.equal(y1, y2):
         print(f"rank {rank}: stack DWDP != stack DEP", flush=True)
         bad += 1
-    # DEP mode 1 (token-deduplicated dispatch, partial combine): within bf16
-    # rounding of the all-local layer (per-rank partial sums are rounded)
-    if wdt == 0:
+    # DEP mode 1 (token-deduplicated dispatch, partial combine; bf16, fp8
+    # and nvfp4 experts): within bf16 rounding of the all-local layer
+    # (per-rank partial sums are rounded)
+    if True:
         ctx.dep_set_mode(1)
         for l in range(3):
             y_d2 = ctx.dep_layer_forward(l, x, residual=False)

@@ -28,7 +28,7 @@ def test_dwdp_and_dep_match_all_local(engine, weight):
     assert "failures=0" in out, out[-4000:]
 
 
-@pytest.mark.parametrize("engine,weight", [(1, 0), (0, 0), (1, 1)])
+@pytest.mark.parametrize("engine,weight", [(1, 0), (0, 0), (1, 1), (0, 2)])
 def test_dwdp_and_dep_match_all_local_r1_shapes(engine, weight):
     """BASELINE config 3 shapes (R1 layer, 88 MB bf16 experts) over real CUDA
     IPC pulls: DWDP and DEP layers bit-identical to the all-local model."""
