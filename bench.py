@@ -560,11 +560,14 @@ def main():
         drecs = ctx.records()
         all_drecs = gather(drecs)
         dval = total_tokens / (dms / 1e3)
-        dep2 = None
-        if True:
-            # the stronger DEP: token-deduplicated dispatch + partial combine
-            # (dwdp_dep_set_mode(1)), same kernels, same box
-            ctx.dep_set_mode(1)
+        what = {1: "token-deduplicated dispatch (each token row once to every peer rank) + receive-side permute "
+                   "merging sources + per-rank partial combine; token counts exchanged once per step",
+                2: "owner-only dispatch (each token row once to each rank owning one of its experts; per-layer "
+                   "row counts exchanged) + receive-side permute + per-rank partial combine"}
+
+        def dep_mode_run(mode):
+            # the stronger DEPs (dwdp_dep_set_mode), same kernels, same box
+            ctx.dep_set_mode(mode)
             for it in range(args.warmup):
                 step(toks[it][rank], it, dep=True)
             torch.cuda.synchronize()
@@ -582,16 +585,16 @@ def main():
             qrecs = ctx.records()
             ctx.dep_set_mode(0)
             qval = total_tokens / (qms / 1e3)
-            dep2 = {"value": qval, "tokens_per_s_per_gpu": qval / world, "ms_per_step": qms / args.steps,
+            return {"value": qval, "tokens_per_s_per_gpu": qval / world, "ms_per_step": qms / args.steps,
                     "comm_ms_per_layer": sum(r["comm_ns"] for r in qrecs) / 1e6 / max(len(qrecs), 1),
                     "kernel_ms_per_layer": {key.replace("_ns", ""): sum(r[key] for r in qrecs) / 1e6
                                             / max(len(qrecs), 1)
                                             for key in ("router_ns", "permute_ns", "gemm1_ns",
                                                         "gemm2_ns", "combine_ns")},
-                    "dwdp_over_dep": value / qval,
-                    "what": "token-deduplicated dispatch (each token row once per peer rank) + "
-                            "receive-side permute merging sources + per-rank partial combine; "
-                            "token counts exchanged once per step"}
+                    "dwdp_over_dep": value / qval, "what": what[mode]}
+
+        dep2 = dep_mode_run(1)
+        dep3 = dep_mode_run(2)
         dep = {"value": dval, "unit": "tokens/s", "tokens_per_s_per_gpu": dval / world,
                "ms_per_step": dms / args.steps,
                "comm_ms_per_layer": sum(r["comm_ns"] for r in drecs) / 1e6 / max(len(drecs), 1),
@@ -602,7 +605,8 @@ def main():
                "dwdp_over_dep": value / dval,
                "what": "reference DEP semantics: every (token, expert) row to the expert's rank "
                        "(simcore.cpp:321-324), per-expert counts exchanged each layer",
-               "dedupe": dep2}
+               "dedupe": dep2, "dedupe_owners": dep3,
+               "dwdp_over_best_dep": value / max(dval, dep2["value"], dep3["value"])}
 
     # ---- whole-step roofline (north star / SURVEY.md §8(d)): per layer the
     # slower of the layer's flops at the tensor peak and the remote-expert

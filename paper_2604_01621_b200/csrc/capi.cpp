@@ -715,7 +715,8 @@ int dwdp_dep_init(dwdp_ctx* c, const void* id) {
 
 int dwdp_dep_set_mode(dwdp_ctx* c, int mode) {
   return guard([&] {
-    dwdp::require(mode == 0 || mode == 1, "dep: mode must be 0 (per-pair) or 1 (token dedupe)");
+    dwdp::require(mode >= 0 && mode <= 2,
+                  "dep: mode must be 0 (per-pair), 1 (token rows to every peer) or 2 (to the owning ranks)");
     C(c).dep_mode = mode;
   });
 }

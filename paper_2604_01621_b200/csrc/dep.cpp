@@ -181,6 +181,10 @@ void Ctx::dep_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y
     dep2_layer_forward(layer, x, T, y, residual, st, Ts);
     return;
   }
+  if (dep_mode == 2) {
+    dep3_layer_forward(layer, x, T, y, residual, st);
+    return;
+  }
   const Nccl& n = nccl();
   const int wl = layer % WL_;
   const int per = E_ / N_;
@@ -412,6 +416,8 @@ void Ctx::dep_stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStrea
     if (in == out) out = (out == y) ? p : y;
     if (dep_mode == 1)
       dep2_layer_forward(l, in, T, out, true, st, Ts);
+    else if (dep_mode == 2)
+      dep3_layer_forward(l, in, T, out, true, st);
     else
       dep_layer_forward(l, in, T, out, true, st);
     in = out;
@@ -424,7 +430,8 @@ void Ctx::dep_stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStrea
 
 void Ctx::dep2_alloc() {
   if (dep2_x_) return;
-  const int64_t rows = int64_t(N_) * max_tokens_;
+  // mode 2 receives up to 127 padding rows per source segment
+  const int64_t rows = int64_t(N_) * (max_tokens_ + 128);
   dep2_x_ = static_cast<uint16_t*>(dalloc(size_t(rows) * h_ * 2, &workspace_bytes));
   dep2_idx_ = static_cast<int32_t*>(dalloc(size_t(rows) * k_ * 4, &workspace_bytes));
   dep2_loc_ = static_cast<int32_t*>(dalloc(size_t(rows) * k_ * 4, &workspace_bytes));
@@ -499,6 +506,85 @@ std::vector<int64_t> Ctx::dep2_exchange_tokens(int64_t T, cudaStream_t st) {
   return Ts;
 }
 
+// The receive side shared by DEP modes 1 and 2: the received token rows
+// dep2_x_ [Tall][h] (this rank's own T tokens first) with their routing
+// dep2_idx_ / dep2_wts_ -> expert outputs O in dep2_xperm_ (routed rows, then
+// the own tokens' shared-expert rows from dep2_meta_[2]); rec.k[1..3] marked.
+// Returns the kernel launches issued.
+int Ctx::dep2_experts(int layer, const uint16_t* x, int64_t T, int64_t Tall, cudaStream_t st, LayerRec& rec) {
+  const int per = E_ / N_, lo = rank_ * per;
+  launch_localize_idx(dep2_idx_, Tall * k_, lo, lo + per, dep2_loc_, st);
+  const int32_t* stab = slot_tab_ + size_t(layer) * 2 * (E_ + 1);
+  const int64_t mb_ub = dep2_max_mb_;
+  const int g1_tiles = int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30));
+  const int g2_tiles = int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30));
+  int np = 1;
+  auto mark = [&](cudaEvent_t* slot) {
+    *slot = take_event();
+    DWDP_CUDA(cudaEventRecord(*slot, st));
+  };
+  if (fp8_ || fp4_) {
+    // quantised experts, as the DWDP path: the permute writes e4m3 (e2m1 +
+    // block scales) copies of every local (token, expert) row and of the own
+    // tokens' shared-expert rows with row scales; GEMM1 emits bf16 H, which
+    // is re-quantised for GEMM2; O (bf16) overwrites the quantised rows
+    uint8_t* x8 = reinterpret_cast<uint8_t*>(dep2_xperm_);
+    if (Tall > 0)
+      np += launch_permute(dep2_loc_, dep2_x_, Tall, E_, k_, h_, shared_ ? 1 : 0, counts_, dep2_rowof_,
+                           dep2_mblock_, dep2_mbseg_, nullptr, dep2_meta_, nullptr, dep2_scratch_, st, x8,
+                           dep2_xs_, 128, dep2_mbrows_, fp4_ ? dep2_sfl_ : nullptr, T, dep2_cap_rows_);
+    if (fp4_ && Tall > 0) {
+      launch_nvfp4_sf_relayout(dep2_sfl_, dep2_xsf_, dep2_cap_rows_, h_, dep2_meta_, st);
+      ++np;
+    }
+    mark(&rec.k[1]);
+    if (Tall > 0 && fp4_) {
+      GemmArgs g1{int(h_), int(f_), int(f_), E_, dep2_mblock_, stab, dep2_meta_, dep2_h_, f_, INT64_MAX, 0,
+                  dep2_mbseg_, nullptr, dep2_xs_, sarena_[0], sarena_[1], 0, raster_, dep2_mbrows_, nullptr, 0,
+                  dep2_xsf_, sfarena_[0], sfarena_[1]};
+      const CUtensorMap sf1[4] = {tm_dep2_sfx_, tm_sf_w_[0], tm_sf_w_[1], tm_dep2_h_o_};
+      launch_grouped_gemm(GEMM_SWIGLU_FP4, tm_dep2_x8_, tm_dep2_x8_, tm_gate_, tm_up_, g1, g1_tiles, st, sf1);
+      launch_quant_rows_nvfp4(dep2_h_, dep2_cap_rows_, f_, dep2_meta_, dep2_h8_, dep2_sfl_, dep2_hsf_, dep2_hs_,
+                              st);
+    } else if (Tall > 0) {
+      GemmArgs g1{int(h_), int(f_), int(f_), E_, dep2_mblock_, stab, dep2_meta_, dep2_h_, f_, INT64_MAX, 0,
+                  dep2_mbseg_, nullptr, dep2_xs_, sarena_[0], sarena_[1], 0, raster_, dep2_mbrows_};
+      launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_dep2_x8_, tm_dep2_x8_, tm_gate_, tm_up_, g1, g1_tiles, st);
+      launch_quant_rows_fp8(dep2_h_, dep2_cap_rows_, f_, dep2_meta_, dep2_h8_, dep2_hs_, st);
+    }
+    mark(&rec.k[2]);
+    if (Tall > 0 && fp4_) {
+      GemmArgs g2{int(f_), int(h_), int(h_), E_, dep2_mblock_, stab, dep2_meta_, dep2_xperm_, h_, INT64_MAX, 0,
+                  dep2_mbseg_, nullptr, dep2_hs_, sarena_[2], nullptr, 0, raster_, dep2_mbrows_, nullptr, 0,
+                  dep2_hsf_, sfarena_[2], nullptr};
+      const CUtensorMap sf2[4] = {tm_dep2_sfh_, tm_sf_w_[2], tm_sf_w_[2], tm_dep2_o_};
+      launch_grouped_gemm(GEMM_PLAIN_FP4, tm_dep2_h8_, tm_dep2_h8_, tm_down_, tm_down_, g2, g2_tiles, st, sf2);
+    } else if (Tall > 0) {
+      GemmArgs g2{int(f_), int(h_), int(h_), E_, dep2_mblock_, stab, dep2_meta_, dep2_xperm_, h_, INT64_MAX, 0,
+                  dep2_mbseg_, nullptr, dep2_hs_, sarena_[2], nullptr, 0, raster_, dep2_mbrows_};
+      launch_grouped_gemm(GEMM_PLAIN_FP8, tm_dep2_h8_, tm_dep2_h8_, tm_down_, tm_down_, g2, g2_tiles, st);
+    }
+    mark(&rec.k[3]);
+  } else {
+    if (Tall > 0)
+      np += launch_permute(dep2_loc_, dep2_x_, Tall, E_, k_, h_, shared_ ? 1 : 0, counts_, dep2_rowof_,
+                           dep2_mblock_, dep2_mbseg_, nullptr, dep2_meta_, dep2_xperm_, dep2_scratch_, st, nullptr,
+                           nullptr, 128, dep2_mbrows_, nullptr, T, dep2_cap_rows_);
+    mark(&rec.k[1]);
+    // 4. grouped GEMMs (the rank's expert block + its shared expert)
+    const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_dep2_xperm_;
+    GemmArgs g1{int(h_), int(f_), int(f_), E_, dep2_mblock_, stab, dep2_meta_, dep2_h_, f_, INT64_MAX, 1,
+                dep2_mbseg_, nullptr, nullptr, nullptr, nullptr, 0, raster_, dep2_mbrows_};
+    if (Tall > 0) launch_grouped_gemm(GEMM_SWIGLU, tm_dep2_xperm_, tm_x, tm_gate_, tm_up_, g1, g1_tiles, st);
+    mark(&rec.k[2]);
+    GemmArgs g2{int(f_), int(h_), int(h_), E_, dep2_mblock_, stab, dep2_meta_, dep2_xperm_, h_, INT64_MAX, 0,
+                dep2_mbseg_, nullptr, nullptr, nullptr, nullptr, 0, raster_, dep2_mbrows_};
+    if (Tall > 0) launch_grouped_gemm(GEMM_PLAIN, tm_dep2_h_, tm_dep2_h_, tm_down_, tm_down_, g2, g2_tiles, st);
+    mark(&rec.k[3]);
+  }
+  return np;
+}
+
 void Ctx::dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
                              cudaStream_t st, const std::vector<int64_t>& Ts) {
   struct DG {
@@ -563,71 +649,7 @@ void Ctx::dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* 
   // 3. receive-side permute over every rank's tokens, local experts only:
   // each expert's rows of all sources form one segment; shared expert on
   // the rank's own T tokens (its A rows read from x)
-  launch_localize_idx(dep2_idx_, Tall * k_, lo, lo + per, dep2_loc_, st);
-  const int32_t* stab = slot_tab_ + size_t(layer) * 2 * (E_ + 1);
-  const int64_t mb_ub = dep2_max_mb_;
-  const int g1_tiles = int(std::min<int64_t>(mb_ub * (f_ / 128), 1 << 30));
-  const int g2_tiles = int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30));
-  int np = 1;
-  if (fp8_ || fp4_) {
-    // quantised experts, as the DWDP path: the permute writes e4m3 (e2m1 +
-    // block scales) copies of every local (token, expert) row and of the own
-    // tokens' shared-expert rows with row scales; GEMM1 emits bf16 H, which
-    // is re-quantised for GEMM2; O (bf16) overwrites the quantised rows
-    uint8_t* x8 = reinterpret_cast<uint8_t*>(dep2_xperm_);
-    if (Tall > 0)
-      np += launch_permute(dep2_loc_, dep2_x_, Tall, E_, k_, h_, shared_ ? 1 : 0, counts_, dep2_rowof_,
-                           dep2_mblock_, dep2_mbseg_, nullptr, dep2_meta_, nullptr, dep2_scratch_, st, x8,
-                           dep2_xs_, 128, dep2_mbrows_, fp4_ ? dep2_sfl_ : nullptr, T, dep2_cap_rows_);
-    if (fp4_ && Tall > 0) {
-      launch_nvfp4_sf_relayout(dep2_sfl_, dep2_xsf_, dep2_cap_rows_, h_, dep2_meta_, st);
-      ++np;
-    }
-    mark(&rec.k[1]);
-    if (Tall > 0 && fp4_) {
-      GemmArgs g1{int(h_), int(f_), int(f_), E_, dep2_mblock_, stab, dep2_meta_, dep2_h_, f_, INT64_MAX, 0,
-                  dep2_mbseg_, nullptr, dep2_xs_, sarena_[0], sarena_[1], 0, raster_, dep2_mbrows_, nullptr, 0,
-                  dep2_xsf_, sfarena_[0], sfarena_[1]};
-      const CUtensorMap sf1[4] = {tm_dep2_sfx_, tm_sf_w_[0], tm_sf_w_[1], tm_dep2_h_o_};
-      launch_grouped_gemm(GEMM_SWIGLU_FP4, tm_dep2_x8_, tm_dep2_x8_, tm_gate_, tm_up_, g1, g1_tiles, st, sf1);
-      launch_quant_rows_nvfp4(dep2_h_, dep2_cap_rows_, f_, dep2_meta_, dep2_h8_, dep2_sfl_, dep2_hsf_, dep2_hs_,
-                              st);
-    } else if (Tall > 0) {
-      GemmArgs g1{int(h_), int(f_), int(f_), E_, dep2_mblock_, stab, dep2_meta_, dep2_h_, f_, INT64_MAX, 0,
-                  dep2_mbseg_, nullptr, dep2_xs_, sarena_[0], sarena_[1], 0, raster_, dep2_mbrows_};
-      launch_grouped_gemm(GEMM_SWIGLU_FP8, tm_dep2_x8_, tm_dep2_x8_, tm_gate_, tm_up_, g1, g1_tiles, st);
-      launch_quant_rows_fp8(dep2_h_, dep2_cap_rows_, f_, dep2_meta_, dep2_h8_, dep2_hs_, st);
-    }
-    mark(&rec.k[2]);
-    if (Tall > 0 && fp4_) {
-      GemmArgs g2{int(f_), int(h_), int(h_), E_, dep2_mblock_, stab, dep2_meta_, dep2_xperm_, h_, INT64_MAX, 0,
-                  dep2_mbseg_, nullptr, dep2_hs_, sarena_[2], nullptr, 0, raster_, dep2_mbrows_, nullptr, 0,
-                  dep2_hsf_, sfarena_[2], nullptr};
-      const CUtensorMap sf2[4] = {tm_dep2_sfh_, tm_sf_w_[2], tm_sf_w_[2], tm_dep2_o_};
-      launch_grouped_gemm(GEMM_PLAIN_FP4, tm_dep2_h8_, tm_dep2_h8_, tm_down_, tm_down_, g2, g2_tiles, st, sf2);
-    } else if (Tall > 0) {
-      GemmArgs g2{int(f_), int(h_), int(h_), E_, dep2_mblock_, stab, dep2_meta_, dep2_xperm_, h_, INT64_MAX, 0,
-                  dep2_mbseg_, nullptr, dep2_hs_, sarena_[2], nullptr, 0, raster_, dep2_mbrows_};
-      launch_grouped_gemm(GEMM_PLAIN_FP8, tm_dep2_h8_, tm_dep2_h8_, tm_down_, tm_down_, g2, g2_tiles, st);
-    }
-    mark(&rec.k[3]);
-  } else {
-    if (Tall > 0)
-      np += launch_permute(dep2_loc_, dep2_x_, Tall, E_, k_, h_, shared_ ? 1 : 0, counts_, dep2_rowof_,
-                           dep2_mblock_, dep2_mbseg_, nullptr, dep2_meta_, dep2_xperm_, dep2_scratch_, st, nullptr,
-                           nullptr, 128, dep2_mbrows_, nullptr, T, dep2_cap_rows_);
-    mark(&rec.k[1]);
-    // 4. grouped GEMMs (the rank's expert block + its shared expert)
-    const CUtensorMap tm_x = shared_ && T > 0 ? make_tmap_bf16(x, T, h_, 128) : tm_dep2_xperm_;
-    GemmArgs g1{int(h_), int(f_), int(f_), E_, dep2_mblock_, stab, dep2_meta_, dep2_h_, f_, INT64_MAX, 1,
-                dep2_mbseg_, nullptr, nullptr, nullptr, nullptr, 0, raster_, dep2_mbrows_};
-    if (Tall > 0) launch_grouped_gemm(GEMM_SWIGLU, tm_dep2_xperm_, tm_x, tm_gate_, tm_up_, g1, g1_tiles, st);
-    mark(&rec.k[2]);
-    GemmArgs g2{int(f_), int(h_), int(h_), E_, dep2_mblock_, stab, dep2_meta_, dep2_xperm_, h_, INT64_MAX, 0,
-                dep2_mbseg_, nullptr, nullptr, nullptr, nullptr, 0, raster_, dep2_mbrows_};
-    if (Tall > 0) launch_grouped_gemm(GEMM_PLAIN, tm_dep2_h_, tm_dep2_h_, tm_down_, tm_down_, g2, g2_tiles, st);
-    mark(&rec.k[3]);
-  }
+  int np = dep2_experts(layer, x, T, Tall, st, rec);
   // 5. partial combine per received token: sum over this rank's experts of
   // the token's k (row < 0: computed elsewhere); own tokens straight into
   // their slot of the final parts, the rest into the dispatch buffer
@@ -673,6 +695,163 @@ void Ctx::dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* 
       },
       dep2_flag_host_));
   launches += (T > 0 ? 3 : 0) + np + (Tall > 0 ? (fp4_ || fp8_ ? 3 : 2) : 0) + 1;
+  DWDP_CUDA(cudaGetLastError());
+  DWDP_CUDA(cudaEventRecord(rec.moe_end, st));
+  push_record(rec);
+}
+
+// ===================================================================== //
+// DEP mode 2: every token row only to the ranks that own at least one of its
+// experts (the own rank always), one partial row back per (token, rank).
+
+void Ctx::dep3_alloc() {
+  dep2_alloc();
+  if (dep3_idx2_) return;
+  const int k2 = k_ + 1;
+  dep3_cap_rows_ = max_tokens_ * std::min(k2, N_) + int64_t(N_) * 128;
+  dep3_idx2_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * k2 * 4, &workspace_bytes));
+  dep3_rowof2_ = static_cast<int32_t*>(dalloc(size_t(max_tokens_) * k2 * 4, &workspace_bytes));
+  dep3_ones_ = static_cast<float*>(dalloc(size_t(max_tokens_) * k2 * 4, &workspace_bytes));
+  launch_fill_f32(dep3_ones_, max_tokens_ * k2, 1.0f, nullptr);
+  dep3_xsend_ = static_cast<uint16_t*>(dalloc(size_t(dep3_cap_rows_) * h_ * 2, &workspace_bytes));
+  dep3_sidx_ = static_cast<int32_t*>(dalloc(size_t(dep3_cap_rows_) * k_ * 4, &workspace_bytes));
+  dep3_swts_ = static_cast<float*>(dalloc(size_t(dep3_cap_rows_) * k_ * 4, &workspace_bytes));
+  dep3_counts_ = static_cast<int32_t*>(dalloc(size_t(N_ + 1) * (N_ + 2) * 4, &workspace_bytes));
+  dep3_meta_ = static_cast<int32_t*>(dalloc(16 * 4, &workspace_bytes));
+  dep3_scratch_ = static_cast<int32_t*>(dalloc(size_t(permute_scratch_ints(max_tokens_, N_)) * 4, &workspace_bytes));
+  dep3_mblock_ = static_cast<int32_t*>(dalloc(size_t(dep3_cap_rows_ / 128 + 8) * 4, &workspace_bytes));
+  dep3_mbseg_ = static_cast<int2*>(dalloc(size_t(dep3_cap_rows_ / 128 + 8) * sizeof(int2), &workspace_bytes));
+  DWDP_CUDA(cudaHostAlloc(&dep3_counts_host_, size_t(N_) * (N_ + 1) * 4, 0));
+  DWDP_CUDA(cudaDeviceSynchronize());
+}
+
+void Ctx::dep3_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
+                             cudaStream_t st) {
+  dep3_alloc();
+  const Nccl& n = nccl();
+  const int wl = layer % WL_, per = E_ / N_, k2 = k_ + 1;
+  LayerRec rec{int64_t(layer), T, take_event(), take_event(), take_event(), nullptr, -1};
+  DWDP_CUDA(cudaEventRecord(rec.gate0, st));
+  DWDP_CUDA(cudaEventRecord(rec.gate1, st));
+  auto mark = [&](cudaEvent_t* slot) {
+    *slot = take_event();
+    DWDP_CUDA(cudaEventRecord(*slot, st));
+  };
+  // 1. router + top-k, destination ranks, token rows permuted into one
+  // segment per destination rank (128-row padded), each row's routing
+  int np = 0;
+  if (T > 0) route_logits(wl, x, T, st);
+  mark(&rec.k[0]);
+  if (T > 0) {
+    launch_dest_ranks(idx_, T, k_, per, rank_, dep3_idx2_, st);
+    np += 1 + launch_permute(dep3_idx2_, x, T, N_, k2, h_, 0, dep3_counts_, dep3_rowof2_, dep3_mblock_, dep3_mbseg_,
+                             nullptr, dep3_meta_, dep3_xsend_, dep3_scratch_, st, nullptr, nullptr, 128);
+    DWDP_CUDA(cudaMemsetAsync(dep3_sidx_, 0xFF, size_t(dep3_cap_rows_) * k_ * 4, st));  // padding rows: idx -1
+    launch_scatter_routing(idx_, wts_, dep3_rowof2_, T, k_, k2, dep3_sidx_, dep3_swts_, st);
+    ++np;
+  } else {
+    DWDP_CUDA(cudaMemsetAsync(dep3_counts_, 0, size_t(N_) * 4, st));
+  }
+  mark(&rec.comm[0]);  // the send-side permute counts as dispatch
+  // 2. rows per (source, destination) from every rank (one host sync, as mode 0)
+  // plus this rank's sticky receive-overflow flag of earlier layers: every
+  // rank raises at the same point (one rank raising alone would leave the
+  // others waiting in NCCL)
+  const size_t nc = size_t(N_) + 1;
+  int32_t* call = dep3_counts_ + nc;
+  DWDP_CUDA(cudaMemcpyAsync(dep3_counts_ + N_, dep2_flag_host_, 4, cudaMemcpyHostToDevice, st));
+  nccl_check(n.AllGather(dep3_counts_, call, nc, kInt32, nccl_, st), "ncclAllGather");
+  DWDP_CUDA(cudaMemcpyAsync(dep3_counts_host_, call, size_t(N_) * nc * 4, cudaMemcpyDeviceToHost, st));
+  DWDP_CUDA(cudaStreamSynchronize(st));
+  for (int p = 0; p < N_; ++p)
+    invariant(dep3_counts_host_[size_t(p) * nc + size_t(N_)] == 0,
+              "dep mode 2: receive-side rows exceeded the workspace on some rank");
+  auto pad = [](int64_t v) { return (v + 127) / 128 * 128; };
+  const size_t nr = size_t(N_);
+  std::vector<int64_t> send_off(nr), send_rows(nr), recv_off(nr), recv_rows(nr);
+  int64_t acc = 0;
+  for (int p = 0; p < N_; ++p) {  // the permute's segment layout, rank order
+    send_off[size_t(p)] = acc;
+    send_rows[size_t(p)] = pad(dep3_counts_host_[size_t(rank_) * nc + size_t(p)]);
+    acc += send_rows[size_t(p)];
+  }
+  for (int p = 0; p < N_; ++p) recv_rows[size_t(p)] = pad(dep3_counts_host_[size_t(p) * nc + size_t(rank_)]);
+  int64_t Rtot = recv_rows[size_t(rank_)];  // own rows first: tokens [0, T) in order
+  recv_off[size_t(rank_)] = 0;
+  for (int p = 0; p < N_; ++p)
+    if (p != rank_) {
+      recv_off[size_t(p)] = Rtot;
+      Rtot += recv_rows[size_t(p)];
+    }
+  invariant(Rtot <= int64_t(N_) * (max_tokens_ + 128) && acc <= dep3_cap_rows_, "dep mode 2: row capacity");
+  // 3. dispatch: rows + their routing
+  const size_t hk = size_t(k_);
+  nccl_check(n.GroupStart(), "ncclGroupStart");
+  for (int p = 0; p < N_; ++p) {
+    if (p == rank_) continue;
+    const size_t so = size_t(send_off[size_t(p)]), sr = size_t(send_rows[size_t(p)]);
+    const size_t ro = size_t(recv_off[size_t(p)]), rr = size_t(recv_rows[size_t(p)]);
+    if (sr) {
+      nccl_check(n.Send(dep3_xsend_ + so * h_, sr * size_t(h_), kBf16, p, nccl_, st), "ncclSend");
+      nccl_check(n.Send(dep3_sidx_ + so * hk, sr * hk, kInt32, p, nccl_, st), "ncclSend");
+      nccl_check(n.Send(dep3_swts_ + so * hk, sr * hk, kFloat32, p, nccl_, st), "ncclSend");
+    }
+    if (rr) {
+      nccl_check(n.Recv(dep2_x_ + ro * h_, rr * size_t(h_), kBf16, p, nccl_, st), "ncclRecv");
+      nccl_check(n.Recv(dep2_idx_ + ro * hk, rr * hk, kInt32, p, nccl_, st), "ncclRecv");
+      nccl_check(n.Recv(dep2_wts_ + ro * hk, rr * hk, kFloat32, p, nccl_, st), "ncclRecv");
+    }
+  }
+  nccl_check(n.GroupEnd(), "ncclGroupEnd");
+  {
+    const size_t so = size_t(send_off[size_t(rank_)]), sr = size_t(send_rows[size_t(rank_)]);
+    if (sr) {
+      DWDP_CUDA(cudaMemcpyAsync(dep2_x_, dep3_xsend_ + so * h_, sr * h_ * 2, cudaMemcpyDeviceToDevice, st));
+      DWDP_CUDA(cudaMemcpyAsync(dep2_idx_, dep3_sidx_ + so * hk, sr * hk * 4, cudaMemcpyDeviceToDevice, st));
+      DWDP_CUDA(cudaMemcpyAsync(dep2_wts_, dep3_swts_ + so * hk, sr * hk * 4, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  mark(&rec.comm[1]);
+  // 4. the rank's experts on every received row (+ shared expert on its own T)
+  np += dep2_experts(layer, x, T, Rtot, st, rec);
+  // 5. one partial row per received row, in the receive layout
+  launch_combine_partial(dep2_xperm_, dep2_rowof_, dep2_wts_, dep2_x_, Rtot, k_, h_, st);
+  ++np;
+  mark(&rec.comm[2]);
+  // 6. return: the partial rows back into the send layout
+  nccl_check(n.GroupStart(), "ncclGroupStart");
+  for (int p = 0; p < N_; ++p) {
+    if (p == rank_) continue;
+    const size_t so = size_t(send_off[size_t(p)]), sr = size_t(send_rows[size_t(p)]);
+    const size_t ro = size_t(recv_off[size_t(p)]), rr = size_t(recv_rows[size_t(p)]);
+    if (rr) nccl_check(n.Send(dep2_x_ + ro * h_, rr * size_t(h_), kBf16, p, nccl_, st), "ncclSend");
+    if (sr) nccl_check(n.Recv(dep3_xsend_ + so * h_, sr * size_t(h_), kBf16, p, nccl_, st), "ncclRecv");
+  }
+  nccl_check(n.GroupEnd(), "ncclGroupEnd");
+  if (send_rows[size_t(rank_)])
+    DWDP_CUDA(cudaMemcpyAsync(dep3_xsend_ + send_off[size_t(rank_)] * h_, dep2_x_,
+                              size_t(send_rows[size_t(rank_)]) * h_ * 2, cudaMemcpyDeviceToDevice, st));
+  mark(&rec.comm[3]);
+  // 7. y = sum of the token's partials (own rank first, then its destination
+  // ranks in first-occurrence order) + shared + residual
+  if (T > 0) {
+    const uint16_t* resid = residual ? x : nullptr;
+    uint16_t* out = (resid != nullptr && resid == y) ? ping() : y;
+    launch_combine_sparse(dep3_xsend_, dep3_rowof2_, dep3_ones_, shared_ ? dep2_xperm_ : nullptr, dep2_meta_, resid,
+                          out, T, k2, h_, st);
+    if (out != y) DWDP_CUDA(cudaMemcpyAsync(y, out, size_t(T) * h_ * 2, cudaMemcpyDeviceToDevice, st));
+    ++np;
+  }
+  // receive-side overflow (meta[4]) -> the sticky host flag, exchanged with
+  // the next layer's counts
+  DWDP_CUDA(cudaMemcpyAsync(dep2_flag_host_ + 1, dep2_meta_ + 4, 4, cudaMemcpyDeviceToHost, st));
+  DWDP_CUDA(cudaLaunchHostFunc(
+      st, [](void* p) {
+        int32_t* f = static_cast<int32_t*>(p);
+        f[0] |= f[1];
+      },
+      dep2_flag_host_));
+  launches += np + (T > 0 ? 2 : 0) + (Rtot > 0 ? (fp4_ || fp8_ ? 3 : 2) : 0);
   DWDP_CUDA(cudaGetLastError());
   DWDP_CUDA(cudaEventRecord(rec.moe_end, st));
   push_record(rec);

@@ -1659,6 +1659,55 @@ __global__ void rank_rows_kernel(int32_t* __restrict__ row_of, float* __restrict
   }
 }
 
+namespace {
+__global__ void dest_ranks_kernel(const int32_t* __restrict__ idx, int64_t T, int k, int per, int self,
+                                  int32_t* __restrict__ idx2) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < T; t += int64_t(gridDim.x) * blockDim.x) {
+    int32_t* o = idx2 + t * (k + 1);
+    o[0] = self;
+    for (int j = 0; j < k; ++j) {
+      const int r = idx[t * k + j] / per;
+      bool first = r != self;
+      for (int i = 0; i < j && first; ++i) first = idx[t * k + i] / per != r;
+      o[1 + j] = first ? r : -1;
+    }
+  }
+}
+__global__ void scatter_routing_kernel(const int32_t* __restrict__ idx, const float* __restrict__ wts,
+                                       const int32_t* __restrict__ row_of2, int64_t T, int k, int k2,
+                                       int32_t* __restrict__ sidx, float* __restrict__ swts) {
+  const int64_t n = T * k2;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t r = row_of2[i];
+    if (r < 0) continue;
+    const int64_t t = i / k2;
+    for (int j = 0; j < k; ++j) {
+      sidx[int64_t(r) * k + j] = idx[t * k + j];
+      swts[int64_t(r) * k + j] = wts[t * k + j];
+    }
+  }
+}
+__global__ void fill_f32_kernel(float* p, int64_t n, float v) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+}  // namespace
+
+void launch_dest_ranks(const int32_t* idx, int64_t T, int k, int per, int self, int32_t* idx2, cudaStream_t st) {
+  if (T > 0)
+    dest_ranks_kernel<<<unsigned(std::min<int64_t>((T + 255) / 256, 148 * 8)), 256, 0, st>>>(idx, T, k, per, self,
+                                                                                            idx2);
+}
+void launch_scatter_routing(const int32_t* idx, const float* wts, const int32_t* row_of2, int64_t T, int k, int k2,
+                            int32_t* sidx, float* swts, cudaStream_t st) {
+  if (T > 0)
+    scatter_routing_kernel<<<unsigned(std::min<int64_t>((T * k2 + 255) / 256, 148 * 8)), 256, 0, st>>>(
+        idx, wts, row_of2, T, k, k2, sidx, swts);
+}
+void launch_fill_f32(float* p, int64_t n, float v, cudaStream_t st) {
+  if (n > 0) fill_f32_kernel<<<unsigned(std::min<int64_t>((n + 255) / 256, 148 * 8)), 256, 0, st>>>(p, n, v);
+}
+
 void launch_rank_rows(int32_t* row_of, float* w, int64_t T, int N, cudaStream_t st) {
   if (T > 0)
     rank_rows_kernel<<<unsigned(std::min<int64_t>((T * N + 255) / 256, 148 * 8)), 256, 0, st>>>(row_of, w, T,
@@ -1750,6 +1799,14 @@ void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
   if (T <= 0) return;
   if (resid == y) throw std::runtime_error("combine: resid must not alias y");
   combine_kernel<false><<<unsigned(T), 128, 0, st>>>(O, row_of, wts, S, s_meta, resid, y, T, k, h);
+}
+
+void launch_combine_sparse(const uint16_t* O, const int32_t* row_of, const float* wts, const uint16_t* S,
+                           const int32_t* s_meta, const uint16_t* resid, uint16_t* y, int64_t T, int k, int64_t h,
+                           cudaStream_t st) {
+  if (T <= 0) return;
+  if (resid == y) throw std::runtime_error("combine: resid must not alias y");
+  combine_kernel<true><<<unsigned(T), 128, 0, st>>>(O, row_of, wts, S, s_meta, resid, y, T, k, h);
 }
 
 void launch_combine_partial(const uint16_t* O, const int32_t* row_of, const float* wts, uint16_t* y, int64_t T,

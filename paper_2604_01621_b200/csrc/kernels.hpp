@@ -66,6 +66,15 @@ int launch_permute(const int32_t* idx, const uint16_t* x, int64_t T, int E, int 
 // layer computes nothing and meta[4] = 1 (the caller raises).
 // DEP receive side: idx -> idx with every expert outside [lo, hi) set to -1.
 void launch_localize_idx(const int32_t* in, int64_t n, int lo, int hi, int32_t* out, cudaStream_t st);
+// DEP mode 2 send side: idx2 [T][k + 1] = {self, then the rank of each
+// expert at its first occurrence in the token's list if it is not self, else
+// -1}: one row per (token, destination rank), the own rank always first.
+void launch_dest_ranks(const int32_t* idx, int64_t T, int k, int per, int self, int32_t* idx2, cudaStream_t st);
+// DEP mode 2: copy each token's routing (k ids, k weights) to every send row
+// of that token (row_of2 [T][k2], -1 = no row).
+void launch_scatter_routing(const int32_t* idx, const float* wts, const int32_t* row_of2, int64_t T, int k, int k2,
+                            int32_t* sidx, float* swts, cudaStream_t st);
+void launch_fill_f32(float* p, int64_t n, float v, cudaStream_t st);
 // row_of[t][r] = r*T + t and weights 1 for the DEP final combine over N ranks.
 void launch_rank_rows(int32_t* row_of, float* w, int64_t T, int N, cudaStream_t st);
 // Split layout: the permuted rows stay in 128-row expert segments (X_perm, O,
@@ -129,6 +138,10 @@ void launch_quant_rows_fp8(const uint16_t* src, int64_t max_rows, int64_t K, con
 void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
                     const uint16_t* S, const int32_t* s_meta, const uint16_t* resid, uint16_t* y,
                     int64_t T, int k, int64_t h, cudaStream_t st);
+// row_of < 0 entries skipped (DEP mode 2's final combine over destination ranks)
+void launch_combine_sparse(const uint16_t* O, const int32_t* row_of, const float* wts, const uint16_t* S,
+                           const int32_t* s_meta, const uint16_t* resid, uint16_t* y, int64_t T, int k, int64_t h,
+                           cudaStream_t st);
 // y[t] = sum_j w[t,j] O[row_of[t,j]] over the pairs with row_of >= 0 only
 // (the DEP receive side's partial rows; no shared expert, no residual).
 void launch_combine_partial(const uint16_t* O, const int32_t* row_of, const float* wts, uint16_t* y, int64_t T,

@@ -119,6 +119,10 @@ class Ctx {
   void dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
                           cudaStream_t st, const std::vector<int64_t>& Ts);
   std::vector<int64_t> dep2_exchange_tokens(int64_t T, cudaStream_t st);
+  int dep2_experts(int layer, const uint16_t* x, int64_t T, int64_t Tall, cudaStream_t st, LayerRec& rec);
+  // DEP mode 2: each token row only to the ranks that own one of its experts
+  void dep3_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* y, bool residual,
+                          cudaStream_t st);
 
   dwdp_ctx_config cfg;
   uint64_t weight_bytes = 0, recv_bytes = 0, workspace_bytes = 0;
@@ -319,6 +323,15 @@ class Ctx {
   int64_t* dep2_tok_host_ = nullptr;
   int64_t dep2_rowf_T_ = -1;
   void dep2_alloc();
+  // DEP mode 2 send side: destination ranks [T][k+1], the permute by rank
+  // (send rows in rank segments), the rows' routing, per-rank counts
+  int32_t *dep3_idx2_ = nullptr, *dep3_rowof2_ = nullptr, *dep3_sidx_ = nullptr, *dep3_counts_ = nullptr,
+          *dep3_counts_host_ = nullptr, *dep3_meta_ = nullptr, *dep3_scratch_ = nullptr, *dep3_mblock_ = nullptr;
+  int2* dep3_mbseg_ = nullptr;
+  float *dep3_swts_ = nullptr, *dep3_ones_ = nullptr;
+  uint16_t* dep3_xsend_ = nullptr;
+  int64_t dep3_cap_rows_ = 0;
+  void dep3_alloc();
   int num_sms_ = 148;
 };
 

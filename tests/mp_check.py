@@ -72,11 +72,12 @@ def main():
     if not torch.equal(y1, y2):
         print(f"rank {rank}: stack DWDP != stack DEP", flush=True)
         bad += 1
-    # DEP mode 1 (token-deduplicated dispatch, partial combine; bf16, fp8
-    # and nvfp4 experts): within bf16 rounding of the all-local layer
+    # DEP modes 1 (token rows to every peer) and 2 (token rows only to the
+    # ranks owning one of the token's experts), partial combine; bf16, fp8
+    # and nvfp4 experts: within bf16 rounding of the all-local layer
     # (per-rank partial sums are rounded)
-    if True:
-        ctx.dep_set_mode(1)
+    for mode in (1, 2):
+        ctx.dep_set_mode(mode)
         for l in range(3):
             y_d2 = ctx.dep_layer_forward(l, x, residual=False)
             y_ref = full.moe_forward(l, x)
@@ -84,7 +85,7 @@ def main():
             if T:
                 err = ((y_d2.float() - y_ref.float()).norm() / y_ref.float().norm()).item()
                 if not err < 1e-2:
-                    print(f"rank {rank} layer {l}: DEP mode 1 rel err {err}", flush=True)
+                    print(f"rank {rank} layer {l}: DEP mode {mode} rel err {err}", flush=True)
                     bad += 1
         y3 = ctx.dep_stack_forward(x)
         torch.cuda.synchronize()
@@ -95,7 +96,7 @@ def main():
         if T:
             err = ((y3.float() - y1.float()).norm() / y1.float().norm()).item()
             if not err < stol:
-                print(f"rank {rank}: DEP mode 1 stack rel err {err}", flush=True)
+                print(f"rank {rank}: DEP mode {mode} stack rel err {err}", flush=True)
                 bad += 1
         ctx.dep_set_mode(0)
     recs = ctx.records()
