@@ -473,6 +473,14 @@ void Ctx::dep2_alloc() {
         tm_dep2_o_ = make_tmap_out(dep2_xperm_, R, h_);
         tm_dep2_h_o_ = make_tmap_out(dep2_h_, R, f_);
       }
+      const int64_t M = max_tokens_;
+      dq_x_ = static_cast<uint8_t*>(dalloc(size_t(M * qrow_bytes()), &workspace_bytes));
+      dq_xs_ = static_cast<float*>(dalloc(size_t(M) * 4, &workspace_bytes));
+      dq_xsr_ = static_cast<float*>(dalloc(size_t(rows) * 4, &workspace_bytes));
+      if (fp4_) {
+        dq_sfl_ = static_cast<uint8_t*>(dalloc(size_t(M * h_ / 16), &workspace_bytes));
+        dq_sflr_ = static_cast<uint8_t*>(dalloc(size_t(rows * h_ / 16), &workspace_bytes));
+      }
     }
   }
   DWDP_CUDA(cudaHostAlloc(&dep2_tok_host_, size_t(N_) * 8, 0));
@@ -506,6 +514,17 @@ std::vector<int64_t> Ctx::dep2_exchange_tokens(int64_t T, cudaStream_t st) {
   return Ts;
 }
 
+// Quantised experts: the own token rows quantised once before the dispatch
+// (the same per-row e4m3 scale / e2m1 codes with block and row scales the
+// DWDP permute computes), so the wire carries 1 or 0.56 bytes per element.
+void Ctx::dq_quantize_own(const uint16_t* x, int64_t T, cudaStream_t st) {
+  if (T <= 0) return;
+  if (fp4_)
+    launch_quant_rows_nvfp4(x, T, h_, nullptr, dq_x_, dq_sfl_, dep2_xsf_, dq_xs_, st);
+  else
+    launch_quant_rows_fp8(x, T, h_, nullptr, dq_x_, dq_xs_, st);
+}
+
 // The receive side shared by DEP modes 1 and 2: the received token rows
 // dep2_x_ [Tall][h] (this rank's own T tokens first) with their routing
 // dep2_idx_ / dep2_wts_ -> expert outputs O in dep2_xperm_ (routed rows, then
@@ -528,11 +547,21 @@ int Ctx::dep2_experts(int layer, const uint16_t* x, int64_t T, int64_t Tall, cud
     // block scales) copies of every local (token, expert) row and of the own
     // tokens' shared-expert rows with row scales; GEMM1 emits bf16 H, which
     // is re-quantised for GEMM2; O (bf16) overwrites the quantised rows
+    // the received rows are already quantised (codes in the dep2_x_ bytes,
+    // row scales dq_xsr_, nvfp4 linear block scales dq_sflr_): the permute
+    // moves qrow-byte code rows as bf16 pairs, qrow_meta places each row's
+    // scales and the own tokens' shared-expert rows
     uint8_t* x8 = reinterpret_cast<uint8_t*>(dep2_xperm_);
-    if (Tall > 0)
-      np += launch_permute(dep2_loc_, dep2_x_, Tall, E_, k_, h_, shared_ ? 1 : 0, counts_, dep2_rowof_,
-                           dep2_mblock_, dep2_mbseg_, nullptr, dep2_meta_, nullptr, dep2_scratch_, st, x8,
-                           dep2_xs_, 128, dep2_mbrows_, fp4_ ? dep2_sfl_ : nullptr, T, dep2_cap_rows_);
+    const int64_t qrow = qrow_bytes();
+    if (Tall > 0) {
+      np += launch_permute(dep2_loc_, dep2_x_, Tall, E_, k_, qrow / 2, shared_ ? 1 : 0, counts_, dep2_rowof_,
+                           dep2_mblock_, dep2_mbseg_, nullptr, dep2_meta_, dep2_xperm_, dep2_scratch_, st, nullptr,
+                           nullptr, 128, dep2_mbrows_, nullptr, T, dep2_cap_rows_);
+      launch_qrow_meta(dep2_rowof_, Tall, k_, dq_xsr_, fp4_ ? dq_sflr_ : nullptr, int(h_ / 16), dep2_xs_,
+                       fp4_ ? dep2_sfl_ : nullptr, dep2_meta_, shared_ ? T : 0,
+                       reinterpret_cast<const uint8_t*>(dep2_x_), qrow, x8, st);
+      ++np;
+    }
     if (fp4_ && Tall > 0) {
       launch_nvfp4_sf_relayout(dep2_sfl_, dep2_xsf_, dep2_cap_rows_, h_, dep2_meta_, st);
       ++np;
@@ -621,29 +650,52 @@ void Ctx::dep2_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* 
   mark(&rec.k[0]);
   mark(&rec.comm[0]);  // dispatch start (same point as the router end)
   // 2. dispatch: every token row once to every peer, with its k expert ids
-  // and weights (the receiver keeps the pairs of its own expert block)
+  // and weights (the receiver keeps the pairs of its own expert block);
+  // quantised experts: the rows travel quantised (codes, row scale, nvfp4
+  // block scales)
   const size_t hk = size_t(k_);
+  const bool q = fp8_ || fp4_;
+  const size_t qrow = size_t(qrow_bytes()), sfb = size_t(h_ / 16);
+  uint8_t* rx = reinterpret_cast<uint8_t*>(dep2_x_);
+  if (q) dq_quantize_own(x, T, st);
   nccl_check(n.GroupStart(), "ncclGroupStart");
   for (int p = 0; p < N_; ++p) {
     if (p == rank_) continue;
     if (T > 0) {
-      nccl_check(n.Send(x, size_t(T) * size_t(h_), kBf16, p, nccl_, st), "ncclSend");
+      if (q) {
+        nccl_check(n.Send(dq_x_, size_t(T) * qrow, kUint8, p, nccl_, st), "ncclSend");
+        nccl_check(n.Send(dq_xs_, size_t(T), kFloat32, p, nccl_, st), "ncclSend");
+        if (fp4_) nccl_check(n.Send(dq_sfl_, size_t(T) * sfb, kUint8, p, nccl_, st), "ncclSend");
+      } else {
+        nccl_check(n.Send(x, size_t(T) * size_t(h_), kBf16, p, nccl_, st), "ncclSend");
+      }
       nccl_check(n.Send(idx_, size_t(T) * hk, kInt32, p, nccl_, st), "ncclSend");
       nccl_check(n.Send(wts_, size_t(T) * hk, kFloat32, p, nccl_, st), "ncclSend");
     }
     const int64_t o = off[size_t(p)], tp = Ts[size_t(p)];
     if (tp > 0) {
-      nccl_check(n.Recv(dep2_x_ + o * h_, size_t(tp) * size_t(h_), kBf16, p, nccl_, st), "ncclRecv");
+      if (q) {
+        nccl_check(n.Recv(rx + size_t(o) * qrow, size_t(tp) * qrow, kUint8, p, nccl_, st), "ncclRecv");
+        nccl_check(n.Recv(dq_xsr_ + o, size_t(tp), kFloat32, p, nccl_, st), "ncclRecv");
+        if (fp4_) nccl_check(n.Recv(dq_sflr_ + size_t(o) * sfb, size_t(tp) * sfb, kUint8, p, nccl_, st), "ncclRecv");
+      } else {
+        nccl_check(n.Recv(dep2_x_ + o * h_, size_t(tp) * size_t(h_), kBf16, p, nccl_, st), "ncclRecv");
+      }
       nccl_check(n.Recv(dep2_idx_ + o * k_, size_t(tp) * hk, kInt32, p, nccl_, st), "ncclRecv");
       nccl_check(n.Recv(dep2_wts_ + o * k_, size_t(tp) * hk, kFloat32, p, nccl_, st), "ncclRecv");
     }
   }
   nccl_check(n.GroupEnd(), "ncclGroupEnd");
-  const int64_t mine = 0;
-  if (T > 0) {
-    DWDP_CUDA(cudaMemcpyAsync(dep2_x_ + mine * h_, x, size_t(T) * h_ * 2, cudaMemcpyDeviceToDevice, st));
-    DWDP_CUDA(cudaMemcpyAsync(dep2_idx_ + mine * k_, idx_, size_t(T) * hk * 4, cudaMemcpyDeviceToDevice, st));
-    DWDP_CUDA(cudaMemcpyAsync(dep2_wts_ + mine * k_, wts_, size_t(T) * hk * 4, cudaMemcpyDeviceToDevice, st));
+  if (T > 0) {  // own rows first in the receive layout
+    if (q) {
+      DWDP_CUDA(cudaMemcpyAsync(rx, dq_x_, size_t(T) * qrow, cudaMemcpyDeviceToDevice, st));
+      DWDP_CUDA(cudaMemcpyAsync(dq_xsr_, dq_xs_, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
+      if (fp4_) DWDP_CUDA(cudaMemcpyAsync(dq_sflr_, dq_sfl_, size_t(T) * sfb, cudaMemcpyDeviceToDevice, st));
+    } else {
+      DWDP_CUDA(cudaMemcpyAsync(dep2_x_, x, size_t(T) * h_ * 2, cudaMemcpyDeviceToDevice, st));
+    }
+    DWDP_CUDA(cudaMemcpyAsync(dep2_idx_, idx_, size_t(T) * hk * 4, cudaMemcpyDeviceToDevice, st));
+    DWDP_CUDA(cudaMemcpyAsync(dep2_wts_, wts_, size_t(T) * hk * 4, cudaMemcpyDeviceToDevice, st));
   }
   mark(&rec.comm[1]);
   // 3. receive-side permute over every rank's tokens, local experts only:
@@ -721,6 +773,10 @@ void Ctx::dep3_alloc() {
   dep3_scratch_ = static_cast<int32_t*>(dalloc(size_t(permute_scratch_ints(max_tokens_, N_)) * 4, &workspace_bytes));
   dep3_mblock_ = static_cast<int32_t*>(dalloc(size_t(dep3_cap_rows_ / 128 + 8) * 4, &workspace_bytes));
   dep3_mbseg_ = static_cast<int2*>(dalloc(size_t(dep3_cap_rows_ / 128 + 8) * sizeof(int2), &workspace_bytes));
+  if (fp8_ || fp4_) {
+    dq_xs_send_ = static_cast<float*>(dalloc(size_t(dep3_cap_rows_) * 4, &workspace_bytes));
+    if (fp4_) dq_sfl_send_ = static_cast<uint8_t*>(dalloc(size_t(dep3_cap_rows_ * h_ / 16), &workspace_bytes));
+  }
   DWDP_CUDA(cudaHostAlloc(&dep3_counts_host_, size_t(N_) * (N_ + 1) * 4, 0));
   DWDP_CUDA(cudaDeviceSynchronize());
 }
@@ -730,6 +786,10 @@ void Ctx::dep3_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* 
   dep3_alloc();
   const Nccl& n = nccl();
   const int wl = layer % WL_, per = E_ / N_, k2 = k_ + 1;
+  const bool q = fp8_ || fp4_;
+  const size_t qrow = size_t(qrow_bytes()), sfb = size_t(h_ / 16);
+  uint8_t* sx = reinterpret_cast<uint8_t*>(dep3_xsend_);
+  uint8_t* rx = reinterpret_cast<uint8_t*>(dep2_x_);
   LayerRec rec{int64_t(layer), T, take_event(), take_event(), take_event(), nullptr, -1};
   DWDP_CUDA(cudaEventRecord(rec.gate0, st));
   DWDP_CUDA(cudaEventRecord(rec.gate1, st));
@@ -744,8 +804,17 @@ void Ctx::dep3_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* 
   mark(&rec.k[0]);
   if (T > 0) {
     launch_dest_ranks(idx_, T, k_, per, rank_, dep3_idx2_, st);
-    np += 1 + launch_permute(dep3_idx2_, x, T, N_, k2, h_, 0, dep3_counts_, dep3_rowof2_, dep3_mblock_, dep3_mbseg_,
-                             nullptr, dep3_meta_, dep3_xsend_, dep3_scratch_, st, nullptr, nullptr, 128);
+    if (q) {  // quantised experts: the rows travel quantised, with their scales
+      dq_quantize_own(x, T, st);
+      np += 2 + launch_permute(dep3_idx2_, reinterpret_cast<const uint16_t*>(dq_x_), T, N_, k2, qrow / 2, 0,
+                               dep3_counts_, dep3_rowof2_, dep3_mblock_, dep3_mbseg_, nullptr, dep3_meta_,
+                               dep3_xsend_, dep3_scratch_, st, nullptr, nullptr, 128);
+      launch_qrow_meta(dep3_rowof2_, T, k2, dq_xs_, fp4_ ? dq_sfl_ : nullptr, int(sfb), dq_xs_send_, dq_sfl_send_,
+                       nullptr, 0, nullptr, 0, nullptr, st);
+    } else {
+      np += 1 + launch_permute(dep3_idx2_, x, T, N_, k2, h_, 0, dep3_counts_, dep3_rowof2_, dep3_mblock_,
+                               dep3_mbseg_, nullptr, dep3_meta_, dep3_xsend_, dep3_scratch_, st, nullptr, nullptr, 128);
+    }
     DWDP_CUDA(cudaMemsetAsync(dep3_sidx_, 0xFF, size_t(dep3_cap_rows_) * k_ * 4, st));  // padding rows: idx -1
     launch_scatter_routing(idx_, wts_, dep3_rowof2_, T, k_, k2, dep3_sidx_, dep3_swts_, st);
     ++np;
@@ -792,12 +861,24 @@ void Ctx::dep3_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* 
     const size_t so = size_t(send_off[size_t(p)]), sr = size_t(send_rows[size_t(p)]);
     const size_t ro = size_t(recv_off[size_t(p)]), rr = size_t(recv_rows[size_t(p)]);
     if (sr) {
-      nccl_check(n.Send(dep3_xsend_ + so * h_, sr * size_t(h_), kBf16, p, nccl_, st), "ncclSend");
+      if (q) {
+        nccl_check(n.Send(sx + so * qrow, sr * qrow, kUint8, p, nccl_, st), "ncclSend");
+        nccl_check(n.Send(dq_xs_send_ + so, sr, kFloat32, p, nccl_, st), "ncclSend");
+        if (fp4_) nccl_check(n.Send(dq_sfl_send_ + so * sfb, sr * sfb, kUint8, p, nccl_, st), "ncclSend");
+      } else {
+        nccl_check(n.Send(dep3_xsend_ + so * h_, sr * size_t(h_), kBf16, p, nccl_, st), "ncclSend");
+      }
       nccl_check(n.Send(dep3_sidx_ + so * hk, sr * hk, kInt32, p, nccl_, st), "ncclSend");
       nccl_check(n.Send(dep3_swts_ + so * hk, sr * hk, kFloat32, p, nccl_, st), "ncclSend");
     }
     if (rr) {
-      nccl_check(n.Recv(dep2_x_ + ro * h_, rr * size_t(h_), kBf16, p, nccl_, st), "ncclRecv");
+      if (q) {
+        nccl_check(n.Recv(rx + ro * qrow, rr * qrow, kUint8, p, nccl_, st), "ncclRecv");
+        nccl_check(n.Recv(dq_xsr_ + ro, rr, kFloat32, p, nccl_, st), "ncclRecv");
+        if (fp4_) nccl_check(n.Recv(dq_sflr_ + ro * sfb, rr * sfb, kUint8, p, nccl_, st), "ncclRecv");
+      } else {
+        nccl_check(n.Recv(dep2_x_ + ro * h_, rr * size_t(h_), kBf16, p, nccl_, st), "ncclRecv");
+      }
       nccl_check(n.Recv(dep2_idx_ + ro * hk, rr * hk, kInt32, p, nccl_, st), "ncclRecv");
       nccl_check(n.Recv(dep2_wts_ + ro * hk, rr * hk, kFloat32, p, nccl_, st), "ncclRecv");
     }
@@ -805,8 +886,14 @@ void Ctx::dep3_layer_forward(int layer, const uint16_t* x, int64_t T, uint16_t* 
   nccl_check(n.GroupEnd(), "ncclGroupEnd");
   {
     const size_t so = size_t(send_off[size_t(rank_)]), sr = size_t(send_rows[size_t(rank_)]);
-    if (sr) {
+    if (sr && q) {
+      DWDP_CUDA(cudaMemcpyAsync(rx, sx + so * qrow, sr * qrow, cudaMemcpyDeviceToDevice, st));
+      DWDP_CUDA(cudaMemcpyAsync(dq_xsr_, dq_xs_send_ + so, sr * 4, cudaMemcpyDeviceToDevice, st));
+      if (fp4_) DWDP_CUDA(cudaMemcpyAsync(dq_sflr_, dq_sfl_send_ + so * sfb, sr * sfb, cudaMemcpyDeviceToDevice, st));
+    } else if (sr) {
       DWDP_CUDA(cudaMemcpyAsync(dep2_x_, dep3_xsend_ + so * h_, sr * h_ * 2, cudaMemcpyDeviceToDevice, st));
+    }
+    if (sr) {
       DWDP_CUDA(cudaMemcpyAsync(dep2_idx_, dep3_sidx_ + so * hk, sr * hk * 4, cudaMemcpyDeviceToDevice, st));
       DWDP_CUDA(cudaMemcpyAsync(dep2_wts_, dep3_swts_ + so * hk, sr * hk * 4, cudaMemcpyDeviceToDevice, st));
     }

@@ -1687,6 +1687,37 @@ __global__ void scatter_routing_kernel(const int32_t* __restrict__ idx, const fl
     }
   }
 }
+__device__ __forceinline__ void copy_row_warp(uint8_t* dst, const uint8_t* src, int64_t bytes, int lane) {
+  for (int64_t c = lane; c < bytes / 16; c += 32)
+    reinterpret_cast<uint4*>(dst)[c] = __ldg(reinterpret_cast<const uint4*>(src) + c);
+}
+__global__ void __launch_bounds__(256) qrow_meta_kernel(const int32_t* __restrict__ row_of, int64_t T, int k,
+                                                        const float* __restrict__ xs,
+                                                        const uint8_t* __restrict__ sfl, int sfb,
+                                                        float* __restrict__ xs_out, uint8_t* __restrict__ sfl_out,
+                                                        const int32_t* __restrict__ meta, int64_t shared_T,
+                                                        const uint8_t* __restrict__ codes, int64_t qrow,
+                                                        uint8_t* __restrict__ codes_out) {
+  if (meta && meta[4]) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t shared_row0 = meta ? meta[2] : 0;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); t < T;
+       t += int64_t(gridDim.x) * (blockDim.x >> 5)) {
+    const float s = xs[t];
+    for (int j = 0; j < k; ++j) {
+      const int32_t r = row_of[t * k + j];
+      if (r < 0) continue;
+      if (lane == 0) xs_out[r] = s;
+      if (sfl) copy_row_warp(sfl_out + int64_t(r) * sfb, sfl + t * sfb, sfb, lane);
+    }
+    if (meta && t < shared_T) {
+      const int64_t R = shared_row0 + t;
+      if (lane == 0) xs_out[R] = s;
+      if (sfl) copy_row_warp(sfl_out + R * sfb, sfl + t * sfb, sfb, lane);
+      copy_row_warp(codes_out + R * qrow, codes + t * qrow, qrow, lane);
+    }
+  }
+}
 __global__ void fill_f32_kernel(float* p, int64_t n, float v) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     p[i] = v;
@@ -1703,6 +1734,13 @@ void launch_scatter_routing(const int32_t* idx, const float* wts, const int32_t*
   if (T > 0)
     scatter_routing_kernel<<<unsigned(std::min<int64_t>((T * k2 + 255) / 256, 148 * 8)), 256, 0, st>>>(
         idx, wts, row_of2, T, k, k2, sidx, swts);
+}
+void launch_qrow_meta(const int32_t* row_of, int64_t T, int k, const float* xs, const uint8_t* sfl, int sfb,
+                      float* xs_out, uint8_t* sfl_out, const int32_t* meta, int64_t shared_T, const uint8_t* codes,
+                      int64_t qrow, uint8_t* codes_out, cudaStream_t st) {
+  if (T > 0)
+    qrow_meta_kernel<<<unsigned(std::min<int64_t>((T + 7) / 8, 148 * 16)), 256, 0, st>>>(
+        row_of, T, k, xs, sfl, sfb, xs_out, sfl_out, meta, shared_T, codes, qrow, codes_out);
 }
 void launch_fill_f32(float* p, int64_t n, float v, cudaStream_t st) {
   if (n > 0) fill_f32_kernel<<<unsigned(std::min<int64_t>((n + 255) / 256, 148 * 8)), 256, 0, st>>>(p, n, v);

@@ -75,6 +75,15 @@ void launch_dest_ranks(const int32_t* idx, int64_t T, int k, int per, int self, 
 void launch_scatter_routing(const int32_t* idx, const float* wts, const int32_t* row_of2, int64_t T, int k, int k2,
                             int32_t* sidx, float* swts, cudaStream_t st);
 void launch_fill_f32(float* p, int64_t n, float v, cudaStream_t st);
+// DEP modes 1/2 with quantised rows on the wire: for every row r = row_of[t][j]
+// >= 0 copy token t's row scale xs[t] (and its sfb-byte linear block-scale
+// row sfl[t], nvfp4) to xs_out[r] / sfl_out[r]. With meta (receive side):
+// tokens t < shared_T also get the shared-expert row R = meta[2] + t (scale,
+// block scales and the qrow-byte code row codes[t] -> codes_out[R]); nothing
+// is written after a receive overflow (meta[4]).
+void launch_qrow_meta(const int32_t* row_of, int64_t T, int k, const float* xs, const uint8_t* sfl, int sfb,
+                      float* xs_out, uint8_t* sfl_out, const int32_t* meta, int64_t shared_T, const uint8_t* codes,
+                      int64_t qrow, uint8_t* codes_out, cudaStream_t st);
 // row_of[t][r] = r*T + t and weights 1 for the DEP final combine over N ranks.
 void launch_rank_rows(int32_t* row_of, float* w, int64_t T, int N, cudaStream_t st);
 // Split layout: the permuted rows stay in 128-row expert segments (X_perm, O,

@@ -320,6 +320,13 @@ class Ctx {
   uint8_t *dep2_h8_ = nullptr, *dep2_sfl_ = nullptr, *dep2_xsf_ = nullptr, *dep2_hsf_ = nullptr;
   float *dep2_xs_ = nullptr, *dep2_hs_ = nullptr;
   CUtensorMap tm_dep2_x8_, tm_dep2_h8_, tm_dep2_sfx_, tm_dep2_sfh_, tm_dep2_o_, tm_dep2_h_o_;
+  // quantised rows on the wire (modes 1 and 2): the own tokens' codes, row
+  // scales and linear block scales; the received rows' scales (codes in the
+  // dep2_x_ bytes); mode 2's send rows' scales
+  uint8_t *dq_x_ = nullptr, *dq_sfl_ = nullptr, *dq_sflr_ = nullptr, *dq_sfl_send_ = nullptr;
+  float *dq_xs_ = nullptr, *dq_xsr_ = nullptr, *dq_xs_send_ = nullptr;
+  int64_t qrow_bytes() const { return fp4_ ? h_ / 2 : h_; }
+  void dq_quantize_own(const uint16_t* x, int64_t T, cudaStream_t st);
   int64_t* dep2_tok_host_ = nullptr;
   int64_t dep2_rowf_T_ = -1;
   void dep2_alloc();

@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round 2, N=4: DEP mode 1 with fp8 / nvfp4 experts -- multi-GPU parity
+# Round 2, N=4: DEP modes 1 and 2 with fp8 / nvfp4 experts (quantised rows on the wire) -- multi-GPU parity
 # (mp_check: DWDP, DEP mode 0 bit-identical, mode 1 within 1e-2 of all-local),
 # then DWDP vs both DEP baselines at MNT 32K and 64K in fp8 and nvfp4.
 mkdir -p gpurun_out
@@ -17,7 +17,9 @@ import json, sys
 dt, tk = sys.argv[1], sys.argv[2]
 d = json.loads([l for l in open(f"gpurun_out/r2_bench_n4_{dt}_{tk}.json").read().splitlines() if l.startswith("{")][-1])
 dep = d["dep_baseline"]; q = dep.get("dedupe") or {}
+q2 = dep.get("dedupe_owners") or {}
 print(dt, tk, "dwdp", round(d["value"]), "dep0", round(dep["value"]), "dep1", round(q.get("value", 0)),
+      "dep2", round(q2.get("value", 0)), "best", round(dep.get("dwdp_over_best_dep", 0), 3),
       "exposed", round(d["exposed_prefetch_ms_per_layer"], 3))
 PY
   done
