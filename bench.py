@@ -439,6 +439,18 @@ def main():
 
     from paper_2604_01621_b200 import report as RP
     all_recs = gather(recs)
+    # per-rank view of the timed DWDP steps (ranks never wait for each other,
+    # so the step time is the slowest rank's): its own timed-region length,
+    # tokens and per-layer split
+    a_local = (sum(a0.elapsed_time(a1) for a0, a1 in attn_ev) / max(len(attn_ev), 1)) if attn is not None else None
+    mine = {"rank": rank, "ms_per_step": ms_local / args.steps,
+            "tokens_per_step": sum(toks[it][rank] for it in range(args.warmup, iters)) / args.steps,
+            "attention_ms_per_layer": a_local}
+    for key in ("moe_ns", "gate_wait_ns", "prefetch_ns"):
+        mine[key.replace("_ns", "_ms_per_layer")] = sum(r[key] for r in recs) / 1e6 / max(len(recs), 1)
+    pf_b, pf_t = sum(r["prefetch_bytes"] for r in recs), sum(r["prefetch_ns"] for r in recs)
+    mine["prefetch_gbs"] = pf_b / pf_t if pf_t else None
+    per_rank = gather(mine)
 
     # ---- per-kernel split and roofline of the dominant kernel (grouped GEMM1)
     k, h, f = R1["k"], R1["h"], R1["f"]
@@ -709,6 +721,7 @@ def main():
                        "parallelism": f"dwdp{world}"},
             "tokens_per_s_per_gpu": value / world,
             "exposed_prefetch_ms_per_layer": exposed_ms,
+            "per_rank": per_rank if world > 1 else None,
             "merge_ms_per_layer": split["merge_ns"] if args.merged else None,
             "prefetch": ({"bytes_per_layer": pf_bytes / max(len(recs), 1),
                           "gbs": pf_bytes / pf_ns if pf_ns else None,
