@@ -487,9 +487,11 @@ int dwdp_dep_init(dwdp_ctx* ctx, const void* nccl_id);
  * (each token row once per peer rank, with its routing), receive-side
  * permute merging each expert's rows across sources, per-rank partial
  * combine so one row per (token, rank) returns, token counts exchanged once
- * per stack (bf16, fp8 and nvfp4 experts: the receiver quantises the rows it
- * keeps, as the DWDP path does). Outputs within bf16 rounding of mode 0 (the
- * per-rank partial sums are rounded to bf16 before the final sum). */
+ * per stack; 2 = each token row only to the ranks owning one of its experts
+ * (own rank first), row counts exchanged per layer. Quantised experts (fp8,
+ * nvfp4): modes 1 and 2 send the rows quantised once by the sender (codes +
+ * scales). Modes 1 and 2 are within bf16 rounding of mode 0 (the per-rank
+ * partial sums are rounded to bf16 before the final sum). */
 int dwdp_dep_set_mode(dwdp_ctx* ctx, int mode);
 int dwdp_dep_layer_forward(dwdp_ctx* ctx, int layer, const void* x, int64_t T,
                            void* y, int residual, void* stream);

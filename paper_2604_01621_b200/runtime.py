@@ -207,8 +207,10 @@ class DwdpContext:
         check(lib().dwdp_dep_init(self.h, C.create_string_buffer(nccl_id, 128)))
 
     def dep_set_mode(self, mode: int) -> None:
-        """0: per-pair dispatch (reference semantics); 1: token-deduplicated
-        dispatch + partial combine (dwdp_dep_set_mode)."""
+        """0: per-pair dispatch (reference semantics); 1: each token row once to
+        every peer; 2: only to the ranks owning one of its experts; 1 and 2
+        merge on the receive side and return one partial row per (token,
+        rank) (dwdp_dep_set_mode)."""
         check(lib().dwdp_dep_set_mode(self.h, mode))
 
     def dep_layer_forward(self, layer: int, x, y=None, residual: bool = True, stream=None):
