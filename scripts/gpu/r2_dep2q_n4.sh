@@ -3,14 +3,14 @@
 # (mp_check: DWDP, DEP mode 0 bit-identical, mode 1 within 1e-2 of all-local),
 # then DWDP vs both DEP baselines at MNT 32K and 64K in fp8 and nvfp4.
 mkdir -p gpurun_out
-timeout 2400 python -m pytest tests/test_multigpu.py -q -p no:cacheprovider -k "match_all_local" > gpurun_out/r2_dep2q_n4_pytest.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/r2_dep2q_n4_pytest.log
-tail -3 gpurun_out/r2_dep2q_n4_pytest.log
+timeout 2400 python -m pytest tests/test_multigpu.py -q -p no:cacheprovider -k "match_all_local" > gpurun_out/r2_qwire_n4_pytest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/r2_qwire_n4_pytest.log
+tail -3 gpurun_out/r2_qwire_n4_pytest.log
 for dt in fp8 nvfp4; do
   for tk in 32768 65536; do
     timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node=4 --master-addr=127.0.0.1 \
       --master-port=29731 bench.py --gpus 4 --steps 6 --warmup 3 --no-e2e --dtype $dt --tokens $tk \
-      > gpurun_out/r2_bench_n4_${dt}_${tk}.json 2> gpurun_out/r2_bench_n4_${dt}_${tk}.err
+      > gpurun_out/r2_bench_n4_${dt}_${tk}_qwire.json 2> gpurun_out/r2_bench_n4_${dt}_${tk}_qwire.err
     echo "bench $dt $tk rc=$?"
     python - "$dt" "$tk" <<'PY'
 import json, sys
