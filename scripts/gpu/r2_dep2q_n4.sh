@@ -15,7 +15,7 @@ for dt in fp8 nvfp4; do
     python - "$dt" "$tk" <<'PY'
 import json, sys
 dt, tk = sys.argv[1], sys.argv[2]
-d = json.loads([l for l in open(f"gpurun_out/r2_bench_n4_{dt}_{tk}.json").read().splitlines() if l.startswith("{")][-1])
+d = json.loads([l for l in open(f"gpurun_out/r2_bench_n4_{dt}_{tk}_qwire.json").read().splitlines() if l.startswith("{")][-1])
 dep = d["dep_baseline"]; q = dep.get("dedupe") or {}
 q2 = dep.get("dedupe_owners") or {}
 print(dt, tk, "dwdp", round(d["value"]), "dep0", round(dep["value"]), "dep1", round(q.get("value", 0)),
