@@ -722,6 +722,12 @@ def main():
             "tokens_per_s_per_gpu": value / world,
             "exposed_prefetch_ms_per_layer": exposed_ms,
             "per_rank": per_rank if world > 1 else None,
+            # DWDP ranks never wait for each other: in serving each rank takes
+            # its next batch when it finishes, so the sustained rate is the sum
+            # of the ranks' own rates (not the headline value, which follows the
+            # bench contract: all tokens over the slowest rank's time)
+            "value_independent_ranks": (sum(r["tokens_per_step"] / (r["ms_per_step"] / 1e3) for r in per_rank)
+                                        if world > 1 else None),
             "merge_ms_per_layer": split["merge_ns"] if args.merged else None,
             "prefetch": ({"bytes_per_layer": pf_bytes / max(len(recs), 1),
                           "gbs": pf_bytes / pf_ns if pf_ns else None,
