@@ -49,6 +49,12 @@ def main():
                            "dwdp_tokens_per_s_per_gpu": d["tokens_per_s_per_gpu"],
                            "dep_tokens_per_s_per_gpu": dep.get("tokens_per_s_per_gpu"),
                            "dwdp_over_dep": dep.get("dwdp_over_dep"),
+                           "dep_mode1_tokens_per_s_per_gpu": (dep.get("dedupe") or {}).get("tokens_per_s_per_gpu"),
+                           "dep_mode2_tokens_per_s_per_gpu": (dep.get("dedupe_owners") or {}).get(
+                               "tokens_per_s_per_gpu"),
+                           "dwdp_over_best_dep": dep.get("dwdp_over_best_dep"),
+                           "dwdp_independent_ranks_per_gpu": (d.get("value_independent_ranks") or 0) / a.gpus
+                           or None,
                            "exposed_prefetch_ms_per_layer": d["exposed_prefetch_ms_per_layer"],
                            "dep_comm_ms_per_layer": dep.get("comm_ms_per_layer"),
                            "engine": d["config"].get("prefetch_engine"),
