@@ -860,39 +860,6 @@ __device__ __forceinline__ int fixed22(uint32_t b, int emax) {
 constexpr int RQ_WARPS = 2;   // rows (warps) per CTA when the rows are staged in smem
 constexpr int RQ_UNROLL = 7;  // 16-byte loads in flight per lane (h = 7168: 4 x 7 x 32 chunks)
 
-// The exact router's row quantisation (oracle route_one): emax from the
-// largest magnitude of the row's bf16 bits; Q = trunc(x * 2^(148 - emax)),
-// exact and |Q| < 2^22, split into three int8 digits (Q = d0 + 2^8 d1 +
-// 2^16 d2). Shared by router_quant_kernel and the combine that emits the next
-// layer's planes.
-__device__ __forceinline__ int rq_emax(uint32_t mx) {  // mx: packed max of (bits & 0x7FFF) pairs
-  const uint32_t top = max(mx & 0xFFFFu, mx >> 16);
-  return top ? max(int(top >> 7), 1) : 1;  // = max over nonzero elements of max(E, 1)
-}
-__device__ __forceinline__ void rq_scales(int m, float& s1, float& s2) {
-  const int kx = 148 - m;  // in [-106, 147]: beyond 127 split into 2^64 * 2^(kx-64)
-  s1 = __int_as_float(((kx > 127 ? 64 : kx) + 127) << 23);
-  s2 = kx > 127 ? __int_as_float((kx - 64 + 127) << 23) : 1.0f;
-}
-// 8 bf16 (4 words) -> the three digit planes' 8 bytes each (p[plane][2])
-__device__ __forceinline__ void rq_digits8(const uint32_t (&w)[4], float s1, float s2, uint32_t (&p)[3][2]) {
-#pragma unroll
-  for (int hw = 0; hw < 2; ++hw) {  // two words = four elements per packed plane word
-    int q0[4], q1[4], q2[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const uint32_t word = w[2 * hw + (e >> 1)];
-      const float f = __uint_as_float((e & 1) ? (word & 0xFFFF0000u) : (word << 16));
-      q0[e] = __float2int_rz(__fmul_rn(__fmul_rn(f, s1), s2));
-      q1[e] = (q0[e] + 128) >> 8;
-      q2[e] = (q1[e] + 128) >> 8;
-    }
-    p[0][hw] = __byte_perm(__byte_perm(q0[0], q0[1], 0x40), __byte_perm(q0[2], q0[3], 0x40), 0x5410);
-    p[1][hw] = __byte_perm(__byte_perm(q1[0], q1[1], 0x40), __byte_perm(q1[2], q1[3], 0x40), 0x5410);
-    p[2][hw] = __byte_perm(__byte_perm(q2[0], q2[1], 0x40), __byte_perm(q2[2], q2[3], 0x40), 0x5410);
-  }
-}
-
 __global__ void __launch_bounds__(256) router_quant_kernel(const uint16_t* __restrict__ src,
                                                            int64_t R, int64_t K,
                                                            int8_t* __restrict__ dst,
@@ -933,18 +900,34 @@ __global__ void __launch_bounds__(256) router_quant_kernel(const uint16_t* __res
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = __vmaxu2(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const int m = rq_emax(mx);
+    const uint32_t top = max(mx & 0xFFFFu, mx >> 16);
+    const int m = top ? max(int(top >> 7), 1) : 1;  // = max over nonzero elements of max(E, 1)
     // Pass 2: Q = trunc(x * 2^(148 - emax)) (exact: a bf16 times a power of
     // two; |Q| < 2^22), digits of Q = d0 + 2^8 d1 + 2^16 d2 in [-128, 127]:
     // Q1 = (Q + 128) >> 8, Q2 = (Q1 + 128) >> 8, digits = their low bytes.
-    float s1, s2;
-    rq_scales(m, s1, s2);
+    const int kx = 148 - m;  // in [-106, 147]: beyond 127 split into 2^64 * 2^(kx-64)
+    const float s1 = __int_as_float(((kx > 127 ? 64 : kx) + 127) << 23);
+    const float s2 = kx > 127 ? __int_as_float((kx - 64 + 127) << 23) : 1.0f;
     __syncwarp();
     for (int64_t c = lane; c < nch; c += 32) {
       const uint4 v = srow[c];
       const uint32_t w[4] = {v.x, v.y, v.z, v.w};
       uint32_t p[3][2];
-      rq_digits8(w, s1, s2, p);
+#pragma unroll
+      for (int hw = 0; hw < 2; ++hw) {  // two words = four elements per packed plane word
+        int q0[4], q1[4], q2[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t word = w[2 * hw + (e >> 1)];
+          const float f = __uint_as_float((e & 1) ? (word & 0xFFFF0000u) : (word << 16));
+          q0[e] = __float2int_rz(__fmul_rn(__fmul_rn(f, s1), s2));
+          q1[e] = (q0[e] + 128) >> 8;
+          q2[e] = (q1[e] + 128) >> 8;
+        }
+        p[0][hw] = __byte_perm(__byte_perm(q0[0], q0[1], 0x40), __byte_perm(q0[2], q0[3], 0x40), 0x5410);
+        p[1][hw] = __byte_perm(__byte_perm(q1[0], q1[1], 0x40), __byte_perm(q1[2], q1[3], 0x40), 0x5410);
+        p[2][hw] = __byte_perm(__byte_perm(q2[0], q2[1], 0x40), __byte_perm(q2[2], q2[3], 0x40), 0x5410);
+      }
       *reinterpret_cast<uint2*>(dst + (0 * R + r) * K + c * 8) = make_uint2(p[0][0], p[0][1]);
       *reinterpret_cast<uint2*>(dst + (1 * R + r) * K + c * 8) = make_uint2(p[1][0], p[1][1]);
       *reinterpret_cast<uint2*>(dst + (2 * R + r) * K + c * 8) = make_uint2(p[2][0], p[2][1]);
@@ -1317,22 +1300,14 @@ __global__ void __launch_bounds__(32) permute_copy_bulk_kernel(const uint16_t* _
 // resid never aliases y: the stacks ping-pong between two buffers
 // (Ctx::stack_forward), so every input is read through the non-coherent path.
 // SKIP_NEG: rows < 0 are pairs computed on another rank (DEP partial combine).
-constexpr int CB_PLANE_SEGS = 8;  // 16-byte output segments kept per thread when emitting planes (h <= 8192)
-
-// PLANES: also emit the next layer's router digit planes [3][T][h] and row
-// exponents of the bf16 output row (the same bits router_quant would read),
-// from the output segments kept in registers; the stack's next layer then
-// skips router_quant.
-template <bool SKIP_NEG, bool PLANES = false>
+template <bool SKIP_NEG>
 __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict__ O,
                                                       const int32_t* __restrict__ row_of,
                                                       const float* __restrict__ wts,
                                                       const uint16_t* __restrict__ S,
                                                       const int32_t* __restrict__ s_meta,
                                                       const uint16_t* __restrict__ resid,
-                                                      uint16_t* __restrict__ y, int64_t T, int k, int64_t h,
-                                                      int8_t* __restrict__ planes = nullptr,
-                                                      int32_t* __restrict__ emax = nullptr) {
+                                                      uint16_t* __restrict__ y, int64_t T, int k, int64_t h) {
   const int64_t t = blockIdx.x;
   if (t >= T) return;
   __shared__ int32_t srow[TOPK_MAXK + 1];
@@ -1350,7 +1325,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
   // thread left the kernel latency-bound below the HBM rate. The FMA order
   // (routed rows in j order, then shared, then residual) is unchanged.
   constexpr int CB = 8;
-  auto seg = [&](int64_t s) -> uint4 {
+  for (int64_t s = threadIdx.x; s < segs; s += blockDim.x) {
     float acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
@@ -1401,46 +1376,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       o[q] = uint32_t(bf16_bits(acc[2 * q])) | (uint32_t(bf16_bits(acc[2 * q + 1])) << 16);
-    const uint4 out = make_uint4(o[0], o[1], o[2], o[3]);
-    reinterpret_cast<uint4*>(y + t * h)[s] = out;
-    return out;
-  };
-  if constexpr (!PLANES) {
-    for (int64_t s = threadIdx.x; s < segs; s += blockDim.x) seg(s);
-  } else {
-    // the output segments stay in registers for the digit pass (h <= 8192)
-    uint4 keep[CB_PLANE_SEGS];
-    uint32_t pmx = 0;
-#pragma unroll
-    for (int i = 0; i < CB_PLANE_SEGS; ++i) {
-      const int64_t s = threadIdx.x + int64_t(i) * 128;
-      keep[i] = make_uint4(0, 0, 0, 0);
-      if (s < segs) keep[i] = seg(s);
-      pmx = __vmaxu2(pmx, __vmaxu2(__vmaxu2(keep[i].x & 0x7FFF7FFFu, keep[i].y & 0x7FFF7FFFu),
-                                   __vmaxu2(keep[i].z & 0x7FFF7FFFu, keep[i].w & 0x7FFF7FFFu)));
-    }
-    __shared__ uint32_t red[4];
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) pmx = __vmaxu2(pmx, __shfl_xor_sync(0xffffffffu, pmx, o));
-    if (lane == 0) red[threadIdx.x >> 5] = pmx;
-    __syncthreads();
-    pmx = __vmaxu2(__vmaxu2(red[0], red[1]), __vmaxu2(red[2], red[3]));
-    const int m = rq_emax(pmx);
-    float s1, s2;
-    rq_scales(m, s1, s2);
-#pragma unroll
-    for (int i = 0; i < CB_PLANE_SEGS; ++i) {
-      const int64_t s = threadIdx.x + int64_t(i) * 128;
-      if (s >= segs) break;
-      const uint32_t w[4] = {keep[i].x, keep[i].y, keep[i].z, keep[i].w};
-      uint32_t p[3][2];
-      rq_digits8(w, s1, s2, p);
-#pragma unroll
-      for (int pl = 0; pl < 3; ++pl)
-        *reinterpret_cast<uint2*>(planes + (pl * T + t) * h + s * 8) = make_uint2(p[pl][0], p[pl][1]);
-    }
-    if (threadIdx.x == 0) emax[t] = m;
+    reinterpret_cast<uint4*>(y + t * h)[s] = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -1897,15 +1833,9 @@ void launch_quant_rows_fp8(const uint16_t* src, int64_t max_rows, int64_t K, con
 
 void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
                     const uint16_t* S, const int32_t* s_meta, const uint16_t* resid, uint16_t* y,
-                    int64_t T, int k, int64_t h, cudaStream_t st, int8_t* planes, int32_t* emax) {
+                    int64_t T, int k, int64_t h, cudaStream_t st) {
   if (T <= 0) return;
   if (resid == y) throw std::runtime_error("combine: resid must not alias y");
-  if (planes) {
-    if (h % 8 != 0 || h / 8 > 128 * CB_PLANE_SEGS) throw std::runtime_error("combine: planes need h <= 8192");
-    combine_kernel<false, true><<<unsigned(T), 128, 0, st>>>(O, row_of, wts, S, s_meta, resid, y, T, k, h, planes,
-                                                             emax);
-    return;
-  }
   combine_kernel<false><<<unsigned(T), 128, 0, st>>>(O, row_of, wts, S, s_meta, resid, y, T, k, h);
 }
 
@@ -1979,7 +1909,6 @@ void configure_max_shared_carveout_kernels(bool all) {
   set(reinterpret_cast<const void*>(permute_copy_bulk_kernel));
   set(reinterpret_cast<const void*>(combine_kernel<false>));
   set(reinterpret_cast<const void*>(combine_kernel<true>));
-  set(reinterpret_cast<const void*>(combine_kernel<false, true>));
   set(reinterpret_cast<const void*>(quant_rows_fp8_kernel));
   set(reinterpret_cast<const void*>(quant_rows_nvfp4_kernel));
   set(reinterpret_cast<const void*>(quant_rows_nvfp4_il_kernel<8>));

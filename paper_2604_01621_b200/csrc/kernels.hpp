@@ -146,8 +146,7 @@ void launch_quant_rows_fp8(const uint16_t* src, int64_t max_rows, int64_t K, con
 // (S == nullptr: no shared expert).
 void launch_combine(const uint16_t* O, const int32_t* row_of, const float* wts,
                     const uint16_t* S, const int32_t* s_meta, const uint16_t* resid, uint16_t* y,
-                    int64_t T, int k, int64_t h, cudaStream_t st, int8_t* planes = nullptr,
-                    int32_t* emax = nullptr);
+                    int64_t T, int k, int64_t h, cudaStream_t st);
 // row_of < 0 entries skipped (DEP mode 2's final combine over destination ranks)
 void launch_combine_sparse(const uint16_t* O, const int32_t* row_of, const float* wts, const uint16_t* S,
                            const int32_t* s_meta, const uint16_t* resid, uint16_t* y, int64_t T, int k, int64_t h,

@@ -743,13 +743,7 @@ void Ctx::prefetch_times(int64_t h, int64_t* s, int64_t* e, double* bytes) {
 // Exact router: digit planes of x (quant kernel), int8 tensor-core products
 // against the weight planes, exact recombination + scoring + top-k.
 void Ctx::route_logits(int wl, const uint16_t* x, int64_t T, cudaStream_t st) {
-  const bool have_planes = router_fused_ && x == planes_for_ && T == planes_T_;
-  planes_for_ = nullptr;
-  planes_T_ = -1;
-  if (!have_planes)
-    launch_router_quant(x, T, h_, xq_, xe_, rmeta_, st);
-  else
-    --launches;  // the callers count the router as three launches
+  launch_router_quant(x, T, h_, xq_, xe_, rmeta_, st);
   RouterCfg rc{E_, k_, cfg.scoring, cfg.n_group, cfg.topk_group, cfg.norm_topk, cfg.routed_scale};
   if (router_fused_) {
     // one GEMM over the 3 x 3 digit-plane products with the exact
@@ -822,7 +816,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     launch_grouped_gemm(GEMM_PLAIN_FP4, tm_h8_, tm_h8_, tmd4, tmd4, g2,
                         int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st, sf2);
     mark(3);
-    combine_into(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, st, true);
+    combine_into(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, st);
     launches += 3 + np + 1 + 4 + 1;  // router 3, permute + relayout, GEMM1 + quant 2 + GEMM2, combine
   } else if (fp8_) {
     // W8A8: the permute writes e4m3 copies of every routed row and of the
@@ -843,7 +837,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
     launch_grouped_gemm(GEMM_PLAIN_FP8, tm_h8_, tm_h8_, tmdown, tmdown, g2,
                         int(std::min<int64_t>(mb_ub * (h_ / 256), 1 << 30)), st);
     mark(3);
-    combine_into(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, st, true);
+    combine_into(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, st);
     launches += 3 + np + 3 + 1;  // router 3, permute, GEMM1 + quant + GEMM2, combine
   } else {
   // gather_: GEMM1's producer gathers the routed rows from x (cp.async), the
@@ -888,7 +882,7 @@ void Ctx::moe_forward(int layer, int parity, const uint16_t* x, int64_t T, uint1
   launch_grouped_gemm(GEMM_PLAIN, tm_h_, tm_h_, split ? tm_down_p_ : tmdown, split ? tm_down_p_ : tmdown, g2,
                       int(std::min<int64_t>(mb2_ub * (h_ / 256), 1 << 30)), st);
   mark(3);
-  combine_into(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, st, true);
+  combine_into(xperm_, row_of_, wts_, shared_ ? xperm_ : nullptr, meta_, resid, y, T, k_, st);
   launches += 3 + np + 2 + 1;  // router 3, permute, GEMM1, GEMM2, combine
   }
   if (timed) {
@@ -1009,20 +1003,14 @@ uint16_t* Ctx::ping() {
 
 void Ctx::combine_into(const uint16_t* O, const int32_t* row_of, const float* wts, const uint16_t* S,
                        const int32_t* s_meta, const uint16_t* resid, uint16_t* y, int64_t T, int k,
-                       cudaStream_t st, bool planes) {
-  // planes: also the next layer's router digit planes of y (stack_forward)
-  planes = planes && emit_planes_ && router_fused_ && h_ % 8 == 0 && h_ <= 8192;
-  int8_t* pq = planes ? xq_ : nullptr;
-  int32_t* pe = planes ? xe_ : nullptr;
+                       cudaStream_t st) {
   if (resid == nullptr || resid != y) {
-    launch_combine(O, row_of, wts, S, s_meta, resid, y, T, k, h_, st, pq, pe);
-  } else {
-    uint16_t* tmp = ping();  // in-place call (x == y): never read and written by one kernel
-    launch_combine(O, row_of, wts, S, s_meta, resid, tmp, T, k, h_, st, pq, pe);
-    DWDP_CUDA(cudaMemcpyAsync(y, tmp, size_t(T) * h_ * 2, cudaMemcpyDeviceToDevice, st));
+    launch_combine(O, row_of, wts, S, s_meta, resid, y, T, k, h_, st);
+    return;
   }
-  planes_for_ = planes ? y : nullptr;
-  planes_T_ = planes ? T : -1;
+  uint16_t* tmp = ping();  // in-place call (x == y): never read and written by one kernel
+  launch_combine(O, row_of, wts, S, s_meta, resid, tmp, T, k, h_, st);
+  DWDP_CUDA(cudaMemcpyAsync(y, tmp, size_t(T) * h_ * 2, cudaMemcpyDeviceToDevice, st));
 }
 
 // Layer outputs alternate between y and the ping buffer, ending in y, so no
@@ -1035,13 +1023,9 @@ void Ctx::stack_forward(const uint16_t* x, int64_t T, uint16_t* y, cudaStream_t 
   for (int l = 0; l < L_; ++l) {
     uint16_t* out = ((L_ - 1 - l) % 2 == 0) ? y : p;
     if (in == out) out = (out == y) ? p : y;  // x == y on the first layer
-    emit_planes_ = l + 1 < L_;
     layer_forward(g0 + l, in, T, out, true, st);
     in = out;
   }
-  emit_planes_ = false;
-  planes_for_ = nullptr;
-  planes_T_ = -1;
   if (in != y) DWDP_CUDA(cudaMemcpyAsync(y, in, size_t(T) * h_ * 2, cudaMemcpyDeviceToDevice, st));
 }
 

@@ -188,12 +188,6 @@ class Ctx {
   std::vector<CUtensorMap> tm_rw_, tm_rw_p_;  // router weight planes (256 / 128-row boxes)
   std::vector<CUtensorMap> tm_rw64_;          // 64-row boxes (fused router GEMM)
   bool router_fused_ = false;
-  // stack_forward: layer l's combine also writes layer l+1's router digit
-  // planes (xq_) and row exponents (xe_) from its bf16 output; the next
-  // route_logits on exactly that output (pointer and T) skips router_quant
-  bool emit_planes_ = false;
-  const uint16_t* planes_for_ = nullptr;
-  int64_t planes_T_ = -1;
   int8_t* xq_ = nullptr;               // activation digit planes [3][T][h]
   int32_t* xe_ = nullptr;              // activation row exponents [T]
   int32_t* rC_ = nullptr;              // int32 plane products [3T][3E]
@@ -306,7 +300,7 @@ class Ctx {
   // into ping and copy back
   void combine_into(const uint16_t* O, const int32_t* row_of, const float* wts, const uint16_t* S,
                     const int32_t* s_meta, const uint16_t* resid, uint16_t* y, int64_t T, int k,
-                    cudaStream_t st, bool planes = false);
+                    cudaStream_t st);
   // DEP mode 1 buffers: all ranks' token rows (then the partial rows sent
   // back), their routing, local row_of, permute scratch, final-combine tables
   uint16_t* dep2_x_ = nullptr;

@@ -454,24 +454,3 @@ def test_call_errors(dev, ctxs):
     with pytest.raises(D.ConfigError):
         lonely.prefetch_issue(1)  # peers not wired
     lonely.close()
-
-
-def test_stack_emits_next_router_planes_bitwise(dev):
-    """stack_forward has layer l's combine write layer l+1's router digit
-    planes and row exponents from its bf16 output (no router_quant pass);
-    layer-by-layer calls quantise their input themselves. Both must give the
-    same stack output bit for bit (routing is exact, so any digit or
-    exponent difference would change it)."""
-    cfg = D.DwdpConfig(**MID)
-    a, b = D.DwdpContext(cfg), D.DwdpContext(cfg)
-    a.init_weights()
-    b.init_weights()
-    x = make_x(300, cfg.hidden, 5, dev)
-    y_stack = a.stack_forward(x)
-    h = x
-    for g in range(cfg.num_layers):
-        h = b.layer_forward(g, h, residual=True)
-    torch.cuda.synchronize()
-    assert torch.equal(y_stack, h)
-    a.close()
-    b.close()
