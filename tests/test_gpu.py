@@ -454,3 +454,21 @@ def test_call_errors(dev, ctxs):
     with pytest.raises(D.ConfigError):
         lonely.prefetch_issue(1)  # peers not wired
     lonely.close()
+
+
+def test_stack_matches_layer_by_layer_bitwise(dev):
+    """stack_forward (ping-pong buffers, prefetch chain) against the same
+    layers called one by one with residual, bit for bit."""
+    cfg = D.DwdpConfig(**MID)
+    a, b = D.DwdpContext(cfg), D.DwdpContext(cfg)
+    a.init_weights()
+    b.init_weights()
+    x = make_x(300, cfg.hidden, 5, dev)
+    y_stack = a.stack_forward(x)
+    h = x
+    for g in range(cfg.num_layers):
+        h = b.layer_forward(g, h, residual=True)
+    torch.cuda.synchronize()
+    assert torch.equal(y_stack, h)
+    a.close()
+    b.close()
