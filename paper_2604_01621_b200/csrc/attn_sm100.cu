@@ -47,6 +47,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 
@@ -111,6 +112,12 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
 __device__ __forceinline__ void commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
                : "memory");
+}
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 // A operand in TMEM (lane = row, 2 bf16 per column), B from shared memory
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -460,6 +467,253 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------- two query tiles per CTA
+// mla_attn2_kernel: one CTA per (256-query pair of tiles X = A, B of a
+// sequence, head). The tensor pipe alternates between the tiles, so one
+// tile's softmax overlaps the other tile's MMAs; K and V tiles are loaded
+// once for both. QK^T runs in SS mode (both Q tiles stay in shared memory:
+// the TMEM holds two S/P double buffers and two O accumulators), PV in TS
+// mode with P written over S. One softmax warp per TMEM lane quarter and
+// tile (64 columns per thread row), no cross-warp exchange.
+constexpr int A2_KVS = 3;
+constexpr int A2_THREADS = 384;
+constexpr int A2_SMEM = 1024 + 2 * Q_BYTES + A2_KVS * (K_BYTES + V_BYTES) + 256;
+// TMEM: tile X's S/P buffers at 256X (+ 64 b), its O accumulator at 256X + 128
+__device__ __forceinline__ uint32_t a2_tm_s(int x) { return uint32_t(x) * 256u; }
+__device__ __forceinline__ uint32_t a2_tm_o(int x) { return uint32_t(x) * 256u + 128u; }
+
+__global__ void __launch_bounds__(A2_THREADS, 1)
+    mla_attn2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const AttnTile* __restrict__ tiles,
+                     uint16_t* __restrict__ out, int H, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sQ = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = sQ + 2 * Q_BYTES;
+  uint8_t* sV = sK + A2_KVS * K_BYTES;
+  uint64_t* q_full = reinterpret_cast<uint64_t*>(sV + A2_KVS * V_BYTES);
+  uint64_t* k_full = q_full + 1;
+  uint64_t* k_empty = k_full + A2_KVS;
+  uint64_t* v_full = k_empty + A2_KVS;
+  uint64_t* v_empty = v_full + A2_KVS;
+  uint64_t* s_full = v_empty + A2_KVS;  // [tile][2]
+  uint64_t* p_full = s_full + 4;        // [tile][2]
+  uint64_t* s_free = p_full + 4;        // [tile][2]: PV done, buffer reusable
+  uint64_t* o_full = s_free + 4;        // [tile]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 2);
+
+  const AttnTile tile = tiles[blockIdx.x];
+  const int head = blockIdx.y;
+  const int ntile = tile.q0 + AQ < tile.len ? 2 : 1;  // tile B exists
+  int nt[2];
+  for (int x = 0; x < 2; ++x) nt[x] = (min(tile.q0 + x * AQ + AQ, tile.len) + AK - 1) / AK;
+  const int ntk = nt[ntile - 1];  // KV tiles to stream (B's range covers A's)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    bar_init(q_full, 1);
+    for (int s = 0; s < A2_KVS; ++s) {
+      bar_init(&k_full[s], 1);
+      bar_init(&k_empty[s], 1);
+      bar_init(&v_full[s], 1);
+      bar_init(&v_empty[s], 1);
+    }
+    for (int b = 0; b < 4; ++b) {
+      bar_init(&s_full[b], 1);
+      bar_init(&p_full[b], 4);
+      bar_init(&s_free[b], 1);
+    }
+    bar_init(&o_full[0], 1);
+    bar_init(&o_full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_holder)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer
+      bar_expect(q_full, uint32_t(ntile * Q_BYTES));
+      for (int x = 0; x < ntile; ++x)
+        for (int a = 0; a < 3; ++a)
+          tma3(sQ + x * Q_BYTES + a * Q_BOX, &tmQ, q_full, a * 64, head, tile.start + tile.q0 + x * AQ);
+      for (int j = 0; j < ntk; ++j) {
+        const int s = j % A2_KVS;
+        bar_wait(&k_empty[s], ((j / A2_KVS) & 1) ^ 1);
+        bar_expect(&k_full[s], K_BYTES);
+        for (int a = 0; a < 3; ++a)
+          tma3(sK + s * K_BYTES + a * K_BOX, &tmK, &k_full[s], a * 64, head, tile.start + j * AK);
+        bar_wait(&v_empty[s], ((j / A2_KVS) & 1) ^ 1);
+        bar_expect(&v_full[s], V_BYTES);
+        tma3(sV + s * V_BYTES, &tmV, &v_full[s], tile.vstart + j * AK, 0, head);
+      }
+    }
+  } else if (warp == 1) {  // ------------------------------------------ MMA issuer (warp-uniform)
+    bar_wait(q_full, 0);
+    fence_after();
+    auto qk = [&](int x, int j) {  // S_X(j) = Q_X K_j^T into S_X buffer j % 2
+      const int b = j & 1;
+      bar_wait(&s_free[x * 2 + b], ((j >> 1) & 1) ^ 1);  // PV_X(j - 2) has consumed P_X(j - 2)
+      fence_after();
+      const uint64_t qd = desc(su32(sQ + x * Q_BYTES));
+      const uint64_t kd = desc(su32(sK + (j % A2_KVS) * K_BYTES));
+      if (elect_one()) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_ss(tmem + a2_tm_s(x) + uint32_t(b) * AK, qd + uint64_t(a * (Q_BOX >> 4)) + 2 * k,
+                   kd + uint64_t(a * (K_BOX >> 4)) + 2 * k, IDESC_S, (a | k) != 0);
+        commit(&s_full[x * 2 + b]);
+      }
+      __syncwarp();
+    };
+    auto pv = [&](int x, int i) {  // O_X += P_X(i) V_i
+      const int b = i & 1;
+      bar_wait(&p_full[x * 2 + b], (i >> 1) & 1);
+      fence_after();
+      const uint64_t vd = desc(su32(sV + (i % A2_KVS) * V_BYTES));
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // 16 keys = 8 TMEM columns of P per MMA
+          mma_ts(tmem + a2_tm_o(x), tmem + a2_tm_s(x) + uint32_t(b) * AK + uint32_t(k * 8), vd + 2 * k, IDESC_O,
+                 (i | k) != 0);
+        commit(&s_free[x * 2 + b]);
+      }
+      __syncwarp();
+    };
+    auto pvs = [&](int i) {  // PV of KV tile i for every tile that uses it, then free its V stage
+      const int s = i % A2_KVS;
+      bar_wait(&v_full[s], (i / A2_KVS) & 1);
+      for (int x = 0; x < ntile; ++x)
+        if (i < nt[x]) pv(x, i);
+      if (elect_one()) commit(&v_empty[s]);
+      __syncwarp();
+    };
+    for (int j = 0; j < ntk; ++j) {
+      const int s = j % A2_KVS;
+      bar_wait(&k_full[s], (j / A2_KVS) & 1);
+      for (int x = 0; x < ntile; ++x)
+        if (j < nt[x]) qk(x, j);
+      if (elect_one()) commit(&k_empty[s]);
+      __syncwarp();
+      if (j >= 1) pvs(j - 1);
+    }
+    pvs(ntk - 1);
+    if (elect_one()) {
+      commit(&o_full[0]);
+      commit(&o_full[1]);
+    }
+    __syncwarp();
+  } else if (warp >= 4) {  // ----------------------------------------- softmax + epilogue
+    const int x = (warp - 4) >> 2, q = warp & 3, row = q * 32 + lane;
+    const int q0 = tile.q0 + x * AQ;
+    if (x < ntile) {  // no early return: every warp reaches the final barrier
+      const int qi = q0 + row;  // query position in its sequence
+      const uint32_t lb = uint32_t(q * 32) << 16;
+      const uint32_t o_acc = tmem + lb + a2_tm_o(x);
+      float m_ref = -INFINITY, l = 0.0f;
+      for (int j = 0; j < nt[x]; ++j) {
+        const int b = j & 1;
+        const uint32_t sbuf = tmem + lb + a2_tm_s(x) + uint32_t(b) * AK;
+        bar_wait(&s_full[x * 2 + b], (j >> 1) & 1);
+        fence_after();
+        uint32_t r0[32], r1[32];
+        ld32(sbuf, r0);
+        ld32(sbuf + 32, r1);
+        ld_wait();
+        float sv[AK];
+        const int k0 = j * AK;
+        float m0 = -INFINITY, m1 = -INFINITY;
+        if (k0 + AK - 1 <= q0) {  // all keys at or below every row's diagonal: no mask
+#pragma unroll
+          for (int c = 0; c < AK; c += 2) {
+            sv[c] = __uint_as_float(c < 32 ? r0[c] : r1[c - 32]);
+            sv[c + 1] = __uint_as_float(c + 1 < 32 ? r0[c + 1] : r1[c - 31]);
+            m0 = fmaxf(m0, sv[c]);
+            m1 = fmaxf(m1, sv[c + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < AK; c += 2) {  // causal (keys past the sequence are > qi)
+            sv[c] = (k0 + c <= qi) ? __uint_as_float(c < 32 ? r0[c] : r1[c - 32]) : -INFINITY;
+            sv[c + 1] = (k0 + c + 1 <= qi) ? __uint_as_float(c + 1 < 32 ? r0[c + 1] : r1[c - 31]) : -INFINITY;
+            m0 = fmaxf(m0, sv[c]);
+            m1 = fmaxf(m1, sv[c + 1]);
+          }
+        }
+        const float mx = fmaxf(m0, m1) * scale_log2;
+        const bool grow = mx > m_ref + RESCALE_LOG2;
+        if (j == 0) {
+          m_ref = mx;  // key 0 is visible to every row: finite
+        } else if (__any_sync(0xffffffffu, grow)) {
+          const float alpha = grow ? ex2(m_ref - mx) : 1.0f;
+          if (grow) {
+            l *= alpha;
+            m_ref = mx;
+          }
+          bar_wait(&s_free[x * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);  // PV_X(j - 1) done
+          fence_after();
+#pragma unroll
+          for (int ch = 0; ch < DV / 32; ++ch) {
+            uint32_t o[32];
+            ld32(o_acc + uint32_t(ch * 32), o);
+            ld_wait();
+#pragma unroll
+            for (int y = 0; y < 32; ++y) o[y] = __float_as_uint(__uint_as_float(o[y]) * alpha);
+            st32(o_acc + uint32_t(ch * 32), o);
+          }
+        }
+        const float nm = -m_ref;
+        float s0 = 0.0f, s1 = 0.0f;
+        uint32_t pk[32];
+#pragma unroll
+        for (int c = 0; c < AK; c += 2) {
+          const float e0 = ex2(fmaf(sv[c], scale_log2, nm)), e1 = ex2(fmaf(sv[c + 1], scale_log2, nm));
+          s0 += e0;
+          s1 += e1;
+          pk[c / 2] = pack2(e0, e1);
+        }
+        l += s0 + s1;
+        st32(sbuf, pk);  // P (bf16 pairs) over the first 32 S columns
+        st_wait();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(&p_full[x * 2 + b]);
+      }
+      bar_wait(&o_full[x], 0);
+      fence_after();
+      const float inv = 1.0f / l;
+      uint4* dst = reinterpret_cast<uint4*>(out + (int64_t(tile.start + qi) * H + head) * DV);
+#pragma unroll
+      for (int ch = 0; ch < DV / 32; ++ch) {
+        uint32_t o[32];
+        ld32(o_acc + uint32_t(ch * 32), o);
+        ld_wait();
+        if (qi < tile.len) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float* f = reinterpret_cast<const float*>(&o[8 * c]);
+            dst[ch * 4 + c] = make_uint4(pack2(f[0] * inv, f[1] * inv), pack2(f[2] * inv, f[3] * inv),
+                                         pack2(f[4] * inv, f[5] * inv), pack2(f[6] * inv, f[7] * inv));
+          }
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 // ---------------------------------------------------------------- glue
 // RMSNorm without weight (x * rsqrt(mean(x^2) + eps)), one warp per row, fp32 math.
 __global__ void rmsnorm_kernel(const uint16_t* __restrict__ in, int64_t ld_in, uint16_t* __restrict__ out,
@@ -548,6 +802,14 @@ __global__ void __launch_bounds__(256) kv_assemble_kernel(const uint16_t* __rest
 
 }  // namespace
 
+int mla_attention_query_step() {
+  static const int step = [] {
+    const char* e = std::getenv("DWDP_ATTN_PAIR");
+    return e && std::atoi(e) != 0 ? 2 * AQ : AQ;
+  }();
+  return step;
+}
+
 void launch_mla_attention(const uint16_t* q, const uint16_t* k, const uint16_t* vt, int64_t T, int64_t ldv,
                           int H, const AttnTile* tiles, int ntiles, float softmax_scale, uint16_t* out,
                           cudaStream_t st) {
@@ -555,6 +817,9 @@ void launch_mla_attention(const uint16_t* q, const uint16_t* k, const uint16_t* 
   std::call_once(once, [] {
     cudaFuncSetAttribute(mla_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ATT_SMEM);
     cudaFuncSetAttribute(mla_attn_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(mla_attn2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A2_SMEM);
+    cudaFuncSetAttribute(mla_attn2_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
   });
   if (ntiles <= 0 || T <= 0) return;
@@ -565,8 +830,12 @@ void launch_mla_attention(const uint16_t* q, const uint16_t* k, const uint16_t* 
   const int64_t dv[3] = {ldv, DV, H}, sv[2] = {ldv * 2, int64_t(DV) * ldv * 2};
   const int bv[3] = {AK, DV, 1};
   const CUtensorMap tv = make_tmap_3d_bf16(vt, dv, sv, bv);
-  mla_attn_kernel<<<dim3(unsigned(ntiles), unsigned(H)), ATT_THREADS, ATT_SMEM, st>>>(
-      tq, tk, tv, tiles, out, H, softmax_scale * 1.4426950408889634f);
+  if (mla_attention_query_step() == 2 * AQ)
+    mla_attn2_kernel<<<dim3(unsigned(ntiles), unsigned(H)), A2_THREADS, A2_SMEM, st>>>(
+        tq, tk, tv, tiles, out, H, softmax_scale * 1.4426950408889634f);
+  else
+    mla_attn_kernel<<<dim3(unsigned(ntiles), unsigned(H)), ATT_THREADS, ATT_SMEM, st>>>(
+        tq, tk, tv, tiles, out, H, softmax_scale * 1.4426950408889634f);
 }
 
 void launch_rmsnorm(const uint16_t* in, int64_t ld_in, uint16_t* out, int64_t ld_out, int64_t rows, int D,

@@ -99,6 +99,7 @@ class Mla {
     // positions and (heaviest-first) query tiles, staged through pinned memory
     DWDP_CUDA(cudaEventSynchronize(staged_));
     std::vector<AttnTile> tl;
+    const int qstep = mla_attention_query_step();
     int64_t s0 = 0, v0 = 0;
     for (int i = 0; i < nseq; ++i) {
       const int64_t L = seqs[i];
@@ -106,7 +107,7 @@ class Mla {
         pos_h_[s0 + t] = int32_t(t);
         pos_h_[T + s0 + t] = int32_t(v0 + t);
       }
-      for (int64_t q0 = 0; q0 < L; q0 += 128) tl.push_back({int32_t(s0), int32_t(L), int32_t(q0), int32_t(v0)});
+      for (int64_t q0 = 0; q0 < L; q0 += qstep) tl.push_back({int32_t(s0), int32_t(L), int32_t(q0), int32_t(v0)});
       s0 += L;
       v0 += (L + 63) / 64 * 64;
     }
@@ -115,8 +116,8 @@ class Mla {
       ldv_ = (v0 + 4096 + 7) / 8 * 8;
       DWDP_CUDA(cudaMalloc(reinterpret_cast<void**>(&vt_), size_t(H_) * 128 * ldv_ * 2));
     }
-    std::stable_sort(tl.begin(), tl.end(), [](const AttnTile& a, const AttnTile& b) {
-      return std::min(a.q0 + 128, a.len) > std::min(b.q0 + 128, b.len);
+    std::stable_sort(tl.begin(), tl.end(), [qstep](const AttnTile& a, const AttnTile& b) {
+      return std::min(a.q0 + qstep, a.len) > std::min(b.q0 + qstep, b.len);
     });
     require(int64_t(tl.size()) <= max_tiles_, "mla: too many query tiles");
     std::copy(tl.begin(), tl.end(), tiles_h_);
