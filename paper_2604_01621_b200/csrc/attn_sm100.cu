@@ -14,6 +14,9 @@
 // group); RMSNorm, RoPE and the K / V^T assembly are small glue kernels; the
 // attention core is mla_attn_kernel below.
 //
+// Two kernels: mla_attn2_kernel (default, further below) runs two query
+// tiles per CTA on one K/V stream; mla_attn_kernel (DWDP_ATTN_PAIR=0) is the
+// one-tile form with Q in TMEM, described here:
 // mla_attn_kernel: one CTA per (128-query tile of a sequence, head),
 // 384 threads, warp-specialised:
 //   warp 0      TMA producer: Q tile once (3 boxes of 128 x 64), then per
@@ -802,12 +805,18 @@ __global__ void __launch_bounds__(256) kv_assemble_kernel(const uint16_t* __rest
 
 }  // namespace
 
-int mla_attention_query_step() {
-  static const int step = [] {
+// 1 (default): two query tiles per CTA (mla_attn2_kernel); DWDP_ATTN_PAIR=0:
+// one tile per CTA (mla_attn_kernel, TS-mode QK^T)
+static int attn_variant() {
+  static const int v = [] {
     const char* e = std::getenv("DWDP_ATTN_PAIR");
-    return e && std::atoi(e) != 0 ? 2 * AQ : AQ;
+    return e ? std::atoi(e) : 1;
   }();
-  return step;
+  return v;
+}
+
+int mla_attention_query_step() {
+  return attn_variant() ? 2 * AQ : AQ;
 }
 
 void launch_mla_attention(const uint16_t* q, const uint16_t* k, const uint16_t* vt, int64_t T, int64_t ldv,
@@ -819,6 +828,7 @@ void launch_mla_attention(const uint16_t* q, const uint16_t* k, const uint16_t* 
     cudaFuncSetAttribute(mla_attn_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(mla_attn2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A2_SMEM);
+
     cudaFuncSetAttribute(mla_attn2_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
   });
@@ -830,7 +840,7 @@ void launch_mla_attention(const uint16_t* q, const uint16_t* k, const uint16_t* 
   const int64_t dv[3] = {ldv, DV, H}, sv[2] = {ldv * 2, int64_t(DV) * ldv * 2};
   const int bv[3] = {AK, DV, 1};
   const CUtensorMap tv = make_tmap_3d_bf16(vt, dv, sv, bv);
-  if (mla_attention_query_step() == 2 * AQ)
+  if (attn_variant() == 1)
     mla_attn2_kernel<<<dim3(unsigned(ntiles), unsigned(H)), A2_THREADS, A2_SMEM, st>>>(
         tq, tk, tv, tiles, out, H, softmax_scale * 1.4426950408889634f);
   else
