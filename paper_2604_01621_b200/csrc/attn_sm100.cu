@@ -45,7 +45,6 @@
 // buffer when the PV MMA of that tile completes.
 #include <cuda.h>
 #include <cuda_bf16.h>
-#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -73,8 +72,6 @@ constexpr int ATT_SMEM = 1024 + Q_BYTES + KVS * (K_BYTES + V_BYTES) + XCH_BYTES 
 // kind::f16 instruction descriptors, K-major A and B, bf16 in, fp32 out
 constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(AK >> 3) << 17) |
                              (uint32_t(AQ >> 4) << 24);
-// QK^T with an f16 accumulator (half the TMEM bytes the softmax reads)
-constexpr uint32_t IDESC_S16 = (1u << 7) | (1u << 10) | (uint32_t(AK >> 3) << 17) | (uint32_t(AQ >> 4) << 24);
 constexpr uint32_t IDESC_O = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(DV >> 3) << 17) |
                              (uint32_t(AQ >> 4) << 24);
 // TMEM (512 columns): Q as the A operand of QK^T (192 bf16 per lane = 96
@@ -488,7 +485,6 @@ constexpr int A2_SMEM = 1024 + 2 * Q_BYTES + A2_KVS * (K_BYTES + V_BYTES) + 256;
 __device__ __forceinline__ uint32_t a2_tm_s(int x) { return uint32_t(x) * 256u; }
 __device__ __forceinline__ uint32_t a2_tm_o(int x) { return uint32_t(x) * 256u + 128u; }
 
-template <bool SF16>
 __global__ void __launch_bounds__(A2_THREADS, 1)
     mla_attn2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const AttnTile* __restrict__ tiles,
@@ -575,7 +571,7 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             mma_ss(tmem + a2_tm_s(x) + uint32_t(b) * AK, qd + uint64_t(a * (Q_BOX >> 4)) + 2 * k,
-                   kd + uint64_t(a * (K_BOX >> 4)) + 2 * k, SF16 ? IDESC_S16 : IDESC_S, (a | k) != 0);
+                   kd + uint64_t(a * (K_BOX >> 4)) + 2 * k, IDESC_S, (a | k) != 0);
         commit(&s_full[x * 2 + b]);
       }
       __syncwarp();
@@ -631,26 +627,9 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
         bar_wait(&s_full[x * 2 + b], (j >> 1) & 1);
         fence_after();
         uint32_t r0[32], r1[32];
-        if constexpr (SF16) {  // S as f16 pairs: 64 keys in 32 columns
-          uint32_t h[32];
-          ld32(sbuf, h);
-          ld_wait();
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h[c]));
-            if (c < 16) {
-              r0[2 * c] = __float_as_uint(f.x);
-              r0[2 * c + 1] = __float_as_uint(f.y);
-            } else {
-              r1[2 * c - 32] = __float_as_uint(f.x);
-              r1[2 * c - 31] = __float_as_uint(f.y);
-            }
-          }
-        } else {
-          ld32(sbuf, r0);
-          ld32(sbuf + 32, r1);
-          ld_wait();
-        }
+        ld32(sbuf, r0);
+        ld32(sbuf + 32, r1);
+        ld_wait();
         float sv[AK];
         const int k0 = j * AK;
         float m0 = -INFINITY, m1 = -INFINITY;
@@ -848,11 +827,9 @@ void launch_mla_attention(const uint16_t* q, const uint16_t* k, const uint16_t* 
     cudaFuncSetAttribute(mla_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ATT_SMEM);
     cudaFuncSetAttribute(mla_attn_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(mla_attn2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, A2_SMEM);
-    cudaFuncSetAttribute(mla_attn2_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(mla_attn2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, A2_SMEM);
-    cudaFuncSetAttribute(mla_attn2_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(mla_attn2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A2_SMEM);
+
+    cudaFuncSetAttribute(mla_attn2_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
   });
   if (ntiles <= 0 || T <= 0) return;
@@ -863,10 +840,8 @@ void launch_mla_attention(const uint16_t* q, const uint16_t* k, const uint16_t* 
   const int64_t dv[3] = {ldv, DV, H}, sv[2] = {ldv * 2, int64_t(DV) * ldv * 2};
   const int bv[3] = {AK, DV, 1};
   const CUtensorMap tv = make_tmap_3d_bf16(vt, dv, sv, bv);
-  static const bool sf16 = std::getenv("DWDP_ATTN_SF16") != nullptr;
   if (attn_variant() == 1)
-    (sf16 ? mla_attn2_kernel<true> : mla_attn2_kernel<false>)<<<dim3(unsigned(ntiles), unsigned(H)), A2_THREADS,
-                                                              A2_SMEM, st>>>(
+    mla_attn2_kernel<<<dim3(unsigned(ntiles), unsigned(H)), A2_THREADS, A2_SMEM, st>>>(
         tq, tk, tv, tiles, out, H, softmax_scale * 1.4426950408889634f);
   else
     mla_attn_kernel<<<dim3(unsigned(ntiles), unsigned(H)), ATT_THREADS, ATT_SMEM, st>>>(
