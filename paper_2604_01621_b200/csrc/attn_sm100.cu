@@ -14,9 +14,9 @@
 // group); RMSNorm, RoPE and the K / V^T assembly are small glue kernels; the
 // attention core is mla_attn_kernel below.
 //
-// Two kernels: mla_attn2_kernel (default, further below) runs two query
-// tiles per CTA on one K/V stream; mla_attn_kernel (DWDP_ATTN_PAIR=0) is the
-// one-tile form with Q in TMEM, described here:
+// Two kernels: mla_attn_kernel (default, described here) and
+// mla_attn2_kernel (DWDP_ATTN_PAIR=1, further below), two query tiles per
+// CTA on one K/V stream.
 // mla_attn_kernel: one CTA per (128-query tile of a sequence, head),
 // 384 threads, warp-specialised:
 //   warp 0      TMA producer: Q tile once (3 boxes of 128 x 64), then per
@@ -805,12 +805,12 @@ __global__ void __launch_bounds__(256) kv_assemble_kernel(const uint16_t* __rest
 
 }  // namespace
 
-// 1 (default): two query tiles per CTA (mla_attn2_kernel); DWDP_ATTN_PAIR=0:
-// one tile per CTA (mla_attn_kernel, TS-mode QK^T)
+// 0 (default): one query tile per CTA (mla_attn_kernel, TS-mode QK^T);
+// DWDP_ATTN_PAIR=1: two query tiles per CTA (mla_attn2_kernel)
 static int attn_variant() {
   static const int v = [] {
     const char* e = std::getenv("DWDP_ATTN_PAIR");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;
   }();
   return v;
 }

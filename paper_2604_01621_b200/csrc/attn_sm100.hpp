@@ -23,8 +23,8 @@ struct AttnTile {
 void launch_mla_attention(const uint16_t* q, const uint16_t* k, const uint16_t* vt, int64_t T, int64_t ldv,
                           int H, const AttnTile* tiles, int ntiles, float softmax_scale, uint16_t* out,
                           cudaStream_t st);
-// Query rows per AttnTile the attention kernel expects: 256 for the default
-// two-tile kernel, 128 with DWDP_ATTN_PAIR=0.
+// Query rows per AttnTile the attention kernel expects: 128, or 256 for the
+// two-tile kernel (DWDP_ATTN_PAIR=1).
 int mla_attention_query_step();
 // y[r] = x[r] * rsqrt(mean(x[r]^2) + eps), rows of D elements (bf16, fp32 math).
 void launch_rmsnorm(const uint16_t* in, int64_t ld_in, uint16_t* out, int64_t ld_out, int64_t rows, int D,
