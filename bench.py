@@ -739,6 +739,15 @@ def main():
             # bench contract: all tokens over the slowest rank's time)
             "value_independent_ranks": (sum(r["tokens_per_step"] / (r["ms_per_step"] / 1e3) for r in per_rank)
                                         if world > 1 else None),
+            # the reference's own definitions (src/simcore.cpp:35-47, SURVEY.md
+            # §8(d)): tokens/s/GPU = (1/N) sum over ranks of each rank's tokens
+            # over its own steady-state time; exposed = weight-wait averaged
+            # over ranks
+            "reference_definition": ({"tokens_per_s_per_gpu": sum(r["tokens_per_step"] / (r["ms_per_step"] / 1e3)
+                                                                  for r in per_rank) / world,
+                                      "exposed_prefetch_ms_per_layer": sum(r["gate_wait_ms_per_layer"]
+                                                                           for r in per_rank) / world}
+                                     if world > 1 else None),
             "merge_ms_per_layer": split["merge_ns"] if args.merged else None,
             "prefetch": ({"bytes_per_layer": pf_bytes / max(len(recs), 1),
                           "gbs": pf_bytes / pf_ns if pf_ns else None,
