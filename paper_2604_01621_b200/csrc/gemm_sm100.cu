@@ -1424,6 +1424,186 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ---------------------------------------------------------------- router, CTA pairs
+// router_gemm_pair_kernel: the same product on CTA pairs (cta_group::2, M =
+// 256 tokens). Each CTA stages its own 128 token rows of the three activation
+// planes and half of the 192 stacked weight rows (32-row boxes: rank r holds
+// stacked rows [96r, 96r + 96)), so one M256 N192 K32 MMA per activation
+// plane and K32 step reads 7 KB of shared memory per SM instead of 10 KB and
+// stays under the MMA time. The accumulators are zeroed by the epilogue
+// (after each drain, and once at start), so every product accumulates.
+constexpr int RP_STAGES = 3;
+constexpr int RP_A = 3 * BM * 128;  // 48 KB
+constexpr int RP_B = 96 * 128;      // 12 KB
+constexpr int RP_SMEM = RP_STAGES * (RP_A + RP_B) + 1024 + 256;
+constexpr uint32_t RP_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(3 * R_BN >> 3) << 17) |
+                              (uint32_t(256 >> 4) << 24);
+
+__device__ __forceinline__ void tmem_st32_zero(uint32_t taddr) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(0u)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    router_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                            const int32_t* __restrict__ xe, const int32_t* __restrict__ we,
+                            float* __restrict__ logits, int T, int E, int K) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  auto sA = [&](int st) { return smem + st * (RP_A + RP_B); };
+  auto sB = [&](int st) { return smem + st * (RP_A + RP_B) + RP_A; };
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RP_STAGES * (RP_A + RP_B));
+  uint64_t* empty = full + RP_STAGES;
+  uint64_t* tfull = empty + RP_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < RP_STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 8);  // leader: 4 local + 4 peer epilogue warps
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  const int nb_count = E / R_BN;
+  const int num_tiles = (T + 2 * BM - 1) / (2 * BM) * nb_count;
+  const int kb_count = K / 128;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer (both CTAs): own A rows, own half of the stacked weight rows
+      const uint32_t full_cl0 = map_to_rank(&full[0], 0);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        const int mp = tile / nb_count, nb = tile - mp * nb_count;
+        const int mb = 2 * mp + int(rank);
+        for (int kb = 0; kb < kb_count; ++kb) {
+          mbar_wait(&empty[st], ph ^ 1);
+          const uint32_t bar = full_cl0 + uint32_t(st) * 8u;
+          if (rank == 0) mbar_expect_tx(&full[st], 2 * (RP_A + RP_B));
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            tma_load_2d_pair(sA(st) + a * (BM * 128), &tmA, bar, kb * 128, a * T + mb * BM);
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const int srow = 96 * int(rank) + 32 * i;  // stacked row: plane srow / 64, row srow % 64
+            tma_load_2d_pair(sB(st) + i * (32 * 128), &tmB, bar, kb * 128, (srow / 64) * E + nb * R_BN + srow % 64);
+          }
+          if (++st == RP_STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {  // MMA issuer (leader; whole warp, one elected lane issues)
+      int st = 0;
+      uint32_t ph = 0;
+      int local = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
+        mbar_wait(tempty, local & 1);  // accumulators drained and zeroed
+        tc_fence_after();
+        for (int kb = 0; kb < kb_count; ++kb) {
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          const uint64_t ad = sw128_desc(smem_u32(sA(st)));
+          const uint64_t bd = sw128_desc(smem_u32(sB(st)));
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+              for (int a = 0; a < 3; ++a)
+                tc_mma_pair_i8(tmem + uint32_t(a * R_BN), ad + uint64_t(a * (BM * 128 >> 4)) + 2 * k, bd + 2 * k,
+                               RP_IDESC, 1);
+            tc_commit_pair(&empty[st]);
+          }
+          __syncwarp();
+          if (++st == RP_STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+        if (elect_one()) tc_commit_pair(tfull);
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {  // epilogue (both CTAs, own 128 rows): exact recombination, one rounding
+    const int q = warp & 3;
+    const uint32_t lb = uint32_t(q * 32) << 16;
+    const uint32_t tempty_cl0 = map_to_rank(tempty, 0);
+    auto zero_and_release = [&]() {
+#pragma unroll
+      for (int c = 0; c < 5 * R_BN; c += 32) tmem_st32_zero(tmem + lb + uint32_t(c));
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_cl0);
+    };
+    zero_and_release();
+    int local = 0;
+    for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
+      const int mp = tile / nb_count, nb = tile - mp * nb_count;
+      const int t = (2 * mp + int(rank)) * BM + q * 32 + lane;
+      const int sx0 = t < T ? xe[t] - 296 : 0;
+      mbar_wait(tfull, local & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < R_BN; c += 32) {
+        long long z[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) z[i] = 0;
+#pragma unroll
+        for (int sidx = 0; sidx < 5; ++sidx) {
+          uint32_t r[32];
+          tmem_ld32_issue(tmem + lb + uint32_t(sidx * R_BN + c), r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) z[i] += static_cast<long long>(int32_t(r[i])) * (1LL << (8 * sidx));
+        }
+        if (c + 32 >= R_BN) zero_and_release();  // every accumulator column read: the next tile may start
+        if (t < T) {
+          const int e0 = nb * R_BN + c;
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int sx = sx0 + __ldg(we + e0 + i);
+            const float f = __ll2float_rn(z[i]);
+            v[i] = (sx >= -126 && sx <= 127) ? __fmul_rn(f, __int_as_float((sx + 127) << 23)) : ldexpf(f, sx);
+          }
+          float4* o = reinterpret_cast<float4*>(logits + int64_t(t) * E + e0);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+
 // ---------------------------------------------------------------- host
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1650,6 +1830,22 @@ void launch_grouped_gemm(int mode, const CUtensorMap& a, const CUtensorMap& a2,
     grouped_gemm_kernel<kSwiGLU8><<<grid, 256, SMEM_BYTES8, st>>>(a, a2, b0, b1, a, args);
   else
     grouped_gemm_kernel<kPlain8><<<grid, 256, SMEM_BYTES8, st>>>(a, a2, b0, b1, a, args);
+}
+
+void launch_router_gemm_pair(const CUtensorMap& planes_x, const CUtensorMap& planes_w32, const int32_t* xe,
+                             const int32_t* we, float* logits, int64_t T, int E, int64_t K, cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(router_gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, RP_SMEM);
+  });
+  if (T <= 0) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (T + 2 * BM - 1) / (2 * BM) * (E / R_BN);
+  const int g = int(std::min<int64_t>(tiles, sms / 2)) * 2;  // whole clusters of two, persistent
+  router_gemm_pair_kernel<<<unsigned(g), 256, RP_SMEM, st>>>(planes_x, planes_w32, xe, we, logits, int(T), E,
+                                                             int(K));
 }
 
 void launch_router_gemm(const CUtensorMap& planes_x, const CUtensorMap& planes_w, const int32_t* xe,

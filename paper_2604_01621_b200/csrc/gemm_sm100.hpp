@@ -88,6 +88,9 @@ constexpr int GEMM_SWIGLU = 0, GEMM_PLAIN = 1, GEMM_INT8 = 2, GEMM_SWIGLU_FP8 = 
 // the exact recombination fused into the epilogue (E % 64 == 0, K % 128 == 0).
 void launch_router_gemm(const CUtensorMap& planes_x, const CUtensorMap& planes_w, const int32_t* xe,
                         const int32_t* we, float* logits, int64_t T, int E, int64_t K, cudaStream_t st);
+// The same on CTA pairs (256 tokens per tile; weight planes as 32-row boxes).
+void launch_router_gemm_pair(const CUtensorMap& planes_x, const CUtensorMap& planes_w32, const int32_t* xe,
+                             const int32_t* we, float* logits, int64_t T, int E, int64_t K, cudaStream_t st);
 
 // a: routed A rows (permuted tokens or H); a2: shared-expert A rows (x);
 // b0: gate (SwiGLU) or down arena; b1: up arena (SwiGLU only).

@@ -199,9 +199,12 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     const int G = c.n_group > 0 ? c.n_group : 1;
     router_fused_ = !(rt && std::string(rt) == "planes") && E_ == 256 && h_ % 128 == 0 &&
                     (G == 1 || (E_ / G) % 8 == 0);
+    const char* rp = std::getenv("DWDP_ROUTER_PAIR");  // the fused GEMM on CTA pairs (A/B)
+    router_pair_ = router_fused_ && rp != nullptr && std::atoi(rp) != 0;
   }
   for (int wl = 0; wl < WL_; ++wl) {
     tm_rw64_.push_back(make_tmap_i8(router_wq_ + size_t(wl) * 3 * E_ * h_, 3 * int64_t(E_), h_, 64));
+    tm_rw32_.push_back(make_tmap_i8(router_wq_ + size_t(wl) * 3 * E_ * h_, 3 * int64_t(E_), h_, 32));
     tm_rw_.push_back(make_tmap_i8(router_wq_ + size_t(wl) * 3 * E_ * h_, 3 * int64_t(E_), h_, 256));
     tm_rw_p_.push_back(make_tmap_i8(router_wq_ + size_t(wl) * 3 * E_ * h_, 3 * int64_t(E_), h_, 128));
   }
@@ -749,7 +752,10 @@ void Ctx::route_logits(int wl, const uint16_t* x, int64_t T, cudaStream_t st) {
     // one GEMM over the 3 x 3 digit-plane products with the exact
     // recombination in its epilogue -> fp32 logits; top-k reads them
     const CUtensorMap tx = make_tmap_i8(xq_, 3 * T, h_, 128);
-    launch_router_gemm(tx, tm_rw64_[size_t(wl)], xe_, router_we_ + size_t(wl) * E_, logits_, T, E_, h_, st);
+    if (router_pair_)
+      launch_router_gemm_pair(tx, tm_rw32_[size_t(wl)], xe_, router_we_ + size_t(wl) * E_, logits_, T, E_, h_, st);
+    else
+      launch_router_gemm(tx, tm_rw64_[size_t(wl)], xe_, router_we_ + size_t(wl) * E_, logits_, T, E_, h_, st);
     launch_topk(nullptr, xe_, router_we_ + size_t(wl) * E_, bias_ + size_t(wl) * E_, logits_, idx_, wts_, T, rc,
                 st);
     return;

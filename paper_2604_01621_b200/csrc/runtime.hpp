@@ -187,6 +187,8 @@ class Ctx {
   int32_t* router_we_ = nullptr;
   std::vector<CUtensorMap> tm_rw_, tm_rw_p_;  // router weight planes (256 / 128-row boxes)
   std::vector<CUtensorMap> tm_rw64_;          // 64-row boxes (fused router GEMM)
+  std::vector<CUtensorMap> tm_rw32_;          // 32-row boxes (fused router GEMM on CTA pairs)
+  bool router_pair_ = false;
   bool router_fused_ = false;
   int8_t* xq_ = nullptr;               // activation digit planes [3][T][h]
   int32_t* xe_ = nullptr;              // activation row exponents [T]
