@@ -199,8 +199,9 @@ Ctx::Ctx(const dwdp_ctx_config& c) : cfg(c) {
     const int G = c.n_group > 0 ? c.n_group : 1;
     router_fused_ = !(rt && std::string(rt) == "planes") && E_ == 256 && h_ % 128 == 0 &&
                     (G == 1 || (E_ / G) % 8 == 0);
-    const char* rp = std::getenv("DWDP_ROUTER_PAIR");  // the fused GEMM on CTA pairs (A/B)
-    router_pair_ = router_fused_ && rp != nullptr && std::atoi(rp) != 0;
+    // the fused GEMM on CTA pairs (default; DWDP_ROUTER_PAIR=0: the 1-SM kernel)
+    const char* rp = std::getenv("DWDP_ROUTER_PAIR");
+    router_pair_ = router_fused_ && !(rp != nullptr && std::atoi(rp) == 0);
   }
   for (int wl = 0; wl < WL_; ++wl) {
     tm_rw64_.push_back(make_tmap_i8(router_wq_ + size_t(wl) * 3 * E_ * h_, 3 * int64_t(E_), h_, 64));
