@@ -58,6 +58,9 @@ def main():
                                "dwdp_tokens_per_s_per_gpu": d["tokens_per_s_per_gpu"],
                                "dep_tokens_per_s_per_gpu": dep.get("tokens_per_s_per_gpu"),
                                "dwdp_over_dep": dep.get("dwdp_over_dep"),
+                               "dep_mode1_ms_per_step": (dep.get("dedupe") or {}).get("ms_per_step"),
+                               "dep_mode2_ms_per_step": (dep.get("dedupe_owners") or {}).get("ms_per_step"),
+                               "dwdp_over_best_dep": dep.get("dwdp_over_best_dep"),
                                "exposed_prefetch_ms_per_layer": d["exposed_prefetch_ms_per_layer"],
                                "merge_ms_per_layer": d.get("merge_ms_per_layer"),
                                "dep_comm_ms_per_layer": dep.get("comm_ms_per_layer"),
