@@ -444,8 +444,15 @@ void Ctx::dep2_alloc() {
   dep2_tok_ = static_cast<int32_t*>(dalloc(size_t(N_) * 8 * 4, &workspace_bytes));
   {
     const int per = E_ / N_;
+    // receive-side routed rows: the worst case (every received row carries
+    // min(k, per) of this rank's experts) when it fits an 8 GB budget (decode
+    // batches under Zipf skew), else 1.3x a balanced rank's k T rows (large
+    // prefill batches, where routing is close to balanced; an overflowing
+    // layer raises on every rank)
     const int64_t balanced = max_tokens_ * k_;  // a rank's expected routed rows
-    const int64_t routed = std::min<int64_t>(rows * std::min(k_, per), balanced * 13 / 10);
+    const int64_t worst = rows * std::min(k_, per);
+    const int64_t budget_rows = (int64_t(8) << 30) / (2 * h_ + 3 * f_);
+    const int64_t routed = std::min<int64_t>(worst, std::max<int64_t>(balanced * 13 / 10, budget_rows));
     dep2_cap_rows_ = (routed + int64_t(per) * 128 + max_tokens_ + 127) / 128 * 128 + 256;
     dep2_max_mb_ = dep2_cap_rows_ / 128 + 4;
     dep2_xperm_ = static_cast<uint16_t*>(dalloc(size_t(dep2_cap_rows_) * h_ * 2, &workspace_bytes));

@@ -61,6 +61,8 @@ def main():
                                "dep_mode1_ms_per_step": (dep.get("dedupe") or {}).get("ms_per_step"),
                                "dep_mode2_ms_per_step": (dep.get("dedupe_owners") or {}).get("ms_per_step"),
                                "dwdp_over_best_dep": dep.get("dwdp_over_best_dep"),
+                               "dep_mode_errors": [x.get("error") for x in (dep.get("dedupe") or {}, dep.get("dedupe_owners") or {})
+                                                   if x.get("error")],
                                "exposed_prefetch_ms_per_layer": d["exposed_prefetch_ms_per_layer"],
                                "merge_ms_per_layer": d.get("merge_ms_per_layer"),
                                "dep_comm_ms_per_layer": dep.get("comm_ms_per_layer"),
